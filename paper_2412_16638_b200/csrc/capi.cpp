@@ -1,0 +1,509 @@
+// extern "C" boundary (include/mprk_b200.h).  Every entry point catches the
+// internal exceptions and maps them onto the reference's error hierarchy
+// codes; the message is kept per thread for mprkb_last_error().
+#include "mprk_b200.h"
+
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <string>
+
+#include "krylov.hpp"
+#include "stepper.hpp"
+
+namespace mprkb {
+long long kernel_launches();
+}
+
+using namespace mprkb;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return MPRKB_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_err = std::string("out of memory: ") + e.what();
+    return MPRKB_ERROR;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MPRKB_ERROR;
+  }
+}
+
+cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+Numerics num_of(int v) {
+  if (v != MPRKB_FAST && v != MPRKB_PARITY) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "numerics must be FAST or PARITY");
+  return v == MPRKB_PARITY ? Numerics::Parity : Numerics::Fast;
+}
+
+Equation eq_of(int e) {
+  switch (e) {
+    case MPRKB_HEAT: return Equation::Heat;
+    case MPRKB_ADVECTION: return Equation::Advection;
+    case MPRKB_ADVECTION_DIFFUSION: return Equation::AdvectionDiffusion;
+  }
+  MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "unknown equation");
+}
+
+void check_dtype(int dt, bool allow_f16 = false) {
+  if (dt < 0 || dt > (allow_f16 ? 4 : 3)) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "unknown dtype");
+}
+
+StencilSpec spec_of(int n, int stencil, double sigma, double gamma) {
+  if (n < 2) MPRKB_THROW(MPRKB_DIMENSION_TOO_SMALL, "KronSumOperator: n must be at least 2");
+  if (stencil < 0 || stencil > 1) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "unknown stencil");
+  StencilSpec s;
+  s.n = n;
+  s.stencil = stencil;
+  s.sigma = sigma;
+  s.gamma = gamma;
+  return s;
+}
+
+StepperConfig config_of(const mprkb_config* c) {
+  if (!c) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "null config");
+  StepperConfig s;
+  s.eq = eq_of(c->equation);
+  s.n = c->n;
+  if (c->q <= 0 || c->q > MPRKB_MAX_STAGES || !c->a_high || !c->a_eps || !c->b)
+    MPRKB_THROW(MPRKB_ERROR, "tableau: stage count must be in [1, 16] with all coefficient blocks given");
+  s.tab.name = "custom";
+  s.tab.q = c->q;
+  s.tab.a_high.assign(c->a_high, c->a_high + c->q * c->q);
+  s.tab.a_eps.assign(c->a_eps, c->a_eps + c->q * c->q);
+  s.tab.b.assign(c->b, c->b + c->q);
+  s.tau = c->tau;
+  s.t_end = c->t_end;
+  s.tol = c->tol;
+  if (c->implicit_precision != MPRKB_F32 && c->implicit_precision != MPRKB_F64)
+    MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "implicit precision must be F32 or F64");
+  s.f32 = c->implicit_precision == MPRKB_F32;
+  s.max_iter = c->max_iter;
+  s.num = num_of(c->numerics);
+  s.precond = c->preconditioner == MPRKB_PRECOND_FASTDIAG ? 0 : c->preconditioner == MPRKB_PRECOND_NONE ? 1 : 2;
+  s.block = c->block_size;
+  s.block_storage = c->block_storage;
+  s.nu = c->nu;
+  s.timings = c->record_timings != 0;
+  return s;
+}
+
+void fill_report(const SolveReport& r, mprkb_solve_report* out) {
+  if (!out) return;
+  out->iterations = r.iterations;
+  out->converged = r.converged ? 1 : 0;
+  out->failure = r.failure;
+  out->true_residual = r.true_residual;
+  out->history_length = (int)r.history.size();
+  for (int i = 0; i < out->history_length && i < out->history_capacity && out->residual_history; ++i)
+    out->residual_history[i] = r.history[i];
+}
+
+}  // namespace
+
+struct mprkb_op {
+  std::unique_ptr<Op> op;
+};
+
+struct mprkb_stepper {
+  std::unique_ptr<Stepper> s;
+  StepTrace last;
+  DevBuf u;  // staging for the host-buffer entry point
+  double* pinned = nullptr;
+  ~mprkb_stepper() {
+    if (pinned) cudaFreeHost(pinned);
+  }
+};
+
+extern "C" {
+
+const char* mprkb_last_error(void) { return g_err.c_str(); }
+int mprkb_version(void) { return 1; }
+long long mprkb_kernel_launches(void) { return mprkb::kernel_launches(); }
+
+int mprkb_device_count(int* count) {
+  return guarded([&] {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    *count = n;
+  });
+}
+int mprkb_malloc(void** dptr, size_t bytes) {
+  return guarded([&] {
+    require_device();
+    CUDA_CHECK(cudaMalloc(dptr, bytes));
+  });
+}
+int mprkb_free(void* dptr) { return guarded([&] { CUDA_CHECK(cudaFree(dptr)); }); }
+int mprkb_memcpy_h2d(void* dst, const void* src, size_t bytes, void* stream) {
+  return guarded([&] { CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, S(stream))); });
+}
+int mprkb_memcpy_d2h(void* dst, const void* src, size_t bytes, void* stream) {
+  return guarded([&] {
+    CUDA_CHECK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, S(stream)));
+    CUDA_CHECK(cudaStreamSynchronize(S(stream)));
+  });
+}
+int mprkb_memset(void* dptr, int value, size_t bytes, void* stream) {
+  return guarded([&] { CUDA_CHECK(cudaMemsetAsync(dptr, value, bytes, S(stream))); });
+}
+int mprkb_stream_synchronize(void* stream) {
+  return guarded([&] { CUDA_CHECK(cudaStreamSynchronize(S(stream))); });
+}
+int mprkb_device_synchronize(void) { return guarded([&] { CUDA_CHECK(cudaDeviceSynchronize()); }); }
+
+// ---- problem setup ----------------------------------------------------------
+int mprkb_make_problem(int equation, int n, double* u0, double* forcing, double* h, double* gamma) {
+  return guarded([&] {
+    const Problem p = make_problem(eq_of(equation), n);
+    if (u0) std::memcpy(u0, p.u0.data(), p.u0.size() * sizeof(double));
+    if (forcing && !p.forcing.empty()) std::memcpy(forcing, p.forcing.data(), p.forcing.size() * sizeof(double));
+    if (h) *h = p.h;
+    if (gamma) *gamma = p.gamma_k;
+  });
+}
+
+int mprkb_heat_exact(int n, double t, double* out) {
+  return guarded([&] {
+    const auto u = heat_exact(make_problem(Equation::Heat, n), t);
+    std::memcpy(out, u.data(), u.size() * sizeof(double));
+  });
+}
+
+int mprkb_builtin_tableau(const char* name, int cap, int* q, double* a_high, double* a_eps, double* b,
+                          double* c) {
+  return guarded([&] {
+    const Tableau t = builtin_tableau(name ? name : "");
+    if (t.q * t.q > cap) MPRKB_THROW(MPRKB_LENGTH_MISMATCH, "tableau: capacity too small");
+    *q = t.q;
+    std::memcpy(a_high, t.a_high.data(), t.a_high.size() * sizeof(double));
+    std::memcpy(a_eps, t.a_eps.data(), t.a_eps.size() * sizeof(double));
+    std::memcpy(b, t.b.data(), t.b.size() * sizeof(double));
+    if (c) std::memcpy(c, t.c.data(), t.c.size() * sizeof(double));
+  });
+}
+
+// ---- kernels on device vectors ---------------------------------------------------
+int mprkb_stencil_apply(int dtype, int n, int stencil, double sigma, double gamma, const void* x, void* out,
+                        void* stream) {
+  return guarded([&] {
+    require_device();
+    check_dtype(dtype);
+    StencilOp op(dtype, spec_of(n, stencil, sigma, gamma));
+    op.apply(x, out, S(stream));
+  });
+}
+
+int mprkb_tensor_apply(int dtype, int side, int n, const void* q, const void* x, void* out, int numerics,
+                       void* stream) {
+  return guarded([&] {
+    require_device();
+    check_dtype(dtype);
+    if (side < 0 || side > 2) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "unknown tensor side");
+    if (n < 1) MPRKB_THROW(MPRKB_LENGTH_MISMATCH, "apply_tensor: x must be n^3");
+    const Numerics num = num_of(numerics);
+    switch (dtype) {
+      case 0: tensor_apply<float>(side, n, (const float*)q, (const float*)x, (float*)out, nullptr, num, S(stream)); break;
+      case 1: tensor_apply<double>(side, n, (const double*)q, (const double*)x, (double*)out, nullptr, num, S(stream)); break;
+      case 2: tensor_apply<c32>(side, n, (const c32*)q, (const c32*)x, (c32*)out, nullptr, num, S(stream)); break;
+      default: tensor_apply<c64>(side, n, (const c64*)q, (const c64*)x, (c64*)out, nullptr, num, S(stream)); break;
+    }
+  });
+}
+
+int mprkb_dot(int dtype, size_t m, const void* a, const void* b, int conjugate_dot, int numerics, double* result,
+              void* stream) {
+  return guarded([&] {
+    require_device();
+    check_dtype(dtype);
+    const Numerics num = num_of(numerics);
+    Reducer red(1);
+    const RedSlot s = red.slot(0);
+    cudaStream_t st = S(stream);
+    const bool cplx = dtype >= 2;
+    switch (dtype) {
+      case 0: dot_real<float>(m, (const float*)a, (const float*)b, s, num, st); break;
+      case 1: dot_real<double>(m, (const double*)a, (const double*)b, s, num, st); break;
+      case 2:
+        if (conjugate_dot) dot_conj<c32>(m, (const c32*)a, (const c32*)b, s, num, st);
+        else dot_real<c32>(m, (const c32*)a, (const c32*)b, s, num, st);
+        break;
+      default:
+        if (conjugate_dot) dot_conj<c64>(m, (const c64*)a, (const c64*)b, s, num, st);
+        else dot_real<c64>(m, (const c64*)a, (const c64*)b, s, num, st);
+        break;
+    }
+    stream_sync(st);
+    result[0] = red.host(0)[0];
+    if (cplx && conjugate_dot) result[1] = red.host(0)[1];
+  });
+}
+
+// ---- operators -------------------------------------------------------------------
+int mprkb_op_stencil(int dtype, int n, int stencil, double sigma, double gamma, mprkb_op** out) {
+  return guarded([&] {
+    check_dtype(dtype);
+    *out = new mprkb_op{std::make_unique<StencilOp>(dtype, spec_of(n, stencil, sigma, gamma))};
+  });
+}
+
+int mprkb_op_fastdiag(int dtype, int n, const void* qa, const void* qa_inv, const void* qb, const void* qb_inv,
+                      const void* qc, const void* qc_inv, const void* lambda_a, const void* lambda_b,
+                      const void* lambda_c, int numerics, mprkb_op** out) {
+  return guarded([&] {
+    require_device();
+    check_dtype(dtype);
+    *out = new mprkb_op{make_fastdiag(dtype, n, qa, qa_inv, qb, qb_inv, qc, qc_inv, lambda_a, lambda_b, lambda_c,
+                                      num_of(numerics))};
+  });
+}
+
+int mprkb_op_fastdiag_stage(int dtype, int equation, int n, double tau, double a, int numerics, mprkb_op** out) {
+  return guarded([&] {
+    require_device();
+    check_dtype(dtype);
+    const Problem p = make_problem(eq_of(equation), n);
+    *out = new mprkb_op{make_stage_fastdiag(dtype, p, tau, a, num_of(numerics))};
+  });
+}
+
+int mprkb_op_block_jacobi(int dtype, int equation, int n, double tau, double a, int block, int storage,
+                          mprkb_op** out) {
+  return guarded([&] {
+    require_device();
+    check_dtype(dtype);
+    check_dtype(storage, true);
+    const Problem p = make_problem(eq_of(equation), n);
+    *out = new mprkb_op{make_block_jacobi(dtype, p, tau, a, block, storage)};
+  });
+}
+
+int mprkb_op_csr(int dtype, int rows, const int* row_ptr, const int* cols, const void* values, int storage,
+                 mprkb_op** out) {
+  return guarded([&] {
+    require_device();
+    check_dtype(dtype);
+    check_dtype(storage, true);
+    *out = new mprkb_op{make_csr(dtype, rows, row_ptr, cols, values, storage)};
+  });
+}
+
+int mprkb_op_csr_stencil(int dtype, int n, int stencil, double sigma, double gamma, int storage, mprkb_op** out) {
+  return guarded([&] {
+    require_device();
+    check_dtype(dtype);
+    check_dtype(storage, true);
+    *out = new mprkb_op{make_csr_stencil(dtype, spec_of(n, stencil, sigma, gamma), storage)};
+  });
+}
+
+int mprkb_op_callback(int dtype, size_t m, mprkb_apply_fn fn, void* ctx, mprkb_op** out) {
+  return guarded([&] {
+    check_dtype(dtype);
+    if (!fn) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "null callback");
+    *out = new mprkb_op{std::make_unique<CallbackOp>(dtype, m, fn, ctx)};
+  });
+}
+
+int mprkb_op_apply(mprkb_op* op, const void* x, void* out, void* stream) {
+  return guarded([&] {
+    if (!op) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "null operator");
+    op->op->apply(x, out, S(stream));
+  });
+}
+
+void mprkb_op_destroy(mprkb_op* op) { delete op; }
+
+// ---- Krylov -------------------------------------------------------------------------
+static int krylov(bool use_cg, int dtype, size_t m, mprkb_op* op, mprkb_op* precond, const void* b, void* x,
+                  double tol, int max_iter, int numerics, mprkb_solve_report* report, void* stream) {
+  return guarded([&] {
+    require_device();
+    check_dtype(dtype);
+    if (!op) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "null operator");
+    if (op->op->size() != m || (precond && precond->op->size() != m))
+      MPRKB_THROW(MPRKB_LENGTH_MISMATCH, use_cg ? "cg: x0 length != b length" : "gmres: x0 length != b length");
+    if (op->op->dtype() != dtype || (precond && precond->op->dtype() != dtype))
+      MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "operator dtype != solve dtype");
+    const Numerics num = num_of(numerics);
+    const Crit crit{tol, max_iter};
+    Op* P = precond ? precond->op.get() : nullptr;
+    SolveReport rep;
+    cudaStream_t st = S(stream);
+    auto run = [&](auto tag) {
+      using T = decltype(tag);
+      KrylovWork<T> w(m);
+      if constexpr (!is_cplx<T>) {
+        if (use_cg) {
+          cg_solve<T>(*op->op, P, (const T*)b, (T*)x, crit, num, w, rep, st);
+          return;
+        }
+      } else {
+        if (use_cg) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "cg: complex systems use gmres");
+      }
+      gmres_solve<T>(*op->op, P, (const T*)b, (T*)x, crit, num, w, rep, st);
+    };
+    switch (dtype) {
+      case 0: run(float{}); break;
+      case 1: run(double{}); break;
+      case 2: run(c32{}); break;
+      default: run(c64{}); break;
+    }
+    stream_sync(st);
+    fill_report(rep, report);
+  });
+}
+
+int mprkb_cg(int dtype, size_t m, mprkb_op* op, mprkb_op* precond, const void* b, void* x, double tol, int max_iter,
+             int numerics, mprkb_solve_report* report, void* stream) {
+  return krylov(true, dtype, m, op, precond, b, x, tol, max_iter, numerics, report, stream);
+}
+
+int mprkb_gmres(int dtype, size_t m, mprkb_op* op, mprkb_op* precond, const void* b, void* x, double tol,
+                int max_iter, int numerics, mprkb_solve_report* report, void* stream) {
+  return krylov(false, dtype, m, op, precond, b, x, tol, max_iter, numerics, report, stream);
+}
+
+// ---- Stepper / integrate -------------------------------------------------------------
+void mprkb_config_init(mprkb_config* c) {
+  std::memset(c, 0, sizeof *c);
+  c->equation = MPRKB_HEAT;
+  c->t_end = 0.1;
+  c->tol = 1e-6;
+  c->implicit_precision = MPRKB_F64;
+  c->max_iter = 40;
+  c->numerics = MPRKB_FAST;
+  c->preconditioner = MPRKB_PRECOND_FASTDIAG;
+  c->block_size = 8;
+  c->block_storage = -1;
+  c->nu = 0.0;
+}
+
+int mprkb_stepper_create(const mprkb_config* cfg, mprkb_stepper** out) {
+  return guarded([&] {
+    const StepperConfig c = config_of(cfg);
+    auto* h = new mprkb_stepper;
+    try {
+      h->s = std::make_unique<Stepper>(c);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+static void fill_trace(const StepTrace& t, mprkb_step_trace* out) {
+  if (!out) return;
+  std::memset(out, 0, sizeof *out);
+  out->n_solves = (int)t.solves.size();
+  out->solver_failure = t.solver_failure ? 1 : 0;
+  for (int i = 0; i < out->n_solves && i < MPRKB_MAX_STAGES; ++i) {
+    out->iterations[i] = t.solves[i].iterations;
+    out->converged[i] = t.solves[i].converged ? 1 : 0;
+    out->failure[i] = t.solves[i].failure;
+    out->true_residual[i] = t.solves[i].true_residual;
+  }
+}
+
+int mprkb_stepper_step(mprkb_stepper* s, double* u_host, mprkb_step_trace* trace) {
+  return guarded([&] {
+    const size_t m = s->s->size();
+    cudaStream_t st = s->s->stream();
+    if (!s->u.get()) s->u.alloc(m * sizeof(double));
+    CUDA_CHECK(cudaMemcpyAsync(s->u.get(), u_host, m * sizeof(double), cudaMemcpyHostToDevice, st));
+    s->s->step(s->u.as<double>(), s->last);
+    CUDA_CHECK(cudaMemcpyAsync(u_host, s->u.get(), m * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_CHECK(cudaStreamSynchronize(st));
+    fill_trace(s->last, trace);
+  });
+}
+
+int mprkb_stepper_step_device(mprkb_stepper* s, double* u_dev, mprkb_step_trace* trace) {
+  return guarded([&] {
+    s->s->step(u_dev, s->last);
+    fill_trace(s->last, trace);
+  });
+}
+
+int mprkb_stepper_initial_state(mprkb_stepper* s, double* u_host) {
+  return guarded([&] {
+    const auto& u0 = s->s->problem().u0;
+    std::memcpy(u_host, u0.data(), u0.size() * sizeof(double));
+  });
+}
+
+int mprkb_stepper_history(mprkb_stepper* s, int idx, double* buf, int cap, int* len) {
+  return guarded([&] {
+    if (idx < 0 || idx >= (int)s->last.solves.size()) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "solve index out of range");
+    const auto& h = s->last.solves[idx].history;
+    *len = (int)h.size();
+    for (int i = 0; i < *len && i < cap; ++i) buf[i] = h[i];
+  });
+}
+
+void* mprkb_stepper_stream(mprkb_stepper* s) { return s ? (void*)s->s->stream() : nullptr; }
+
+int mprkb_stepper_timing(mprkb_stepper* s, int i, const char** label, long long* count, double* seconds) {
+  const auto& e = s->s->timer().entries();
+  if (i < 0 || i >= (int)e.size()) return (int)e.size();
+  if (label) *label = e[i].label.c_str();
+  if (count) *count = e[i].count;
+  if (seconds) *seconds = e[i].seconds;
+  return (int)e.size();
+}
+
+void mprkb_stepper_destroy(mprkb_stepper* s) { delete s; }
+
+static void fill_result(const IntegrationResult& r, double* state_host, mprkb_result* result) {
+  {
+    if (state_host) std::memcpy(state_host, r.state.data(), r.state.size() * sizeof(double));
+    if (result) {
+      const double nan = std::numeric_limits<double>::quiet_NaN();
+      result->error_max = r.error_max ? *r.error_max : nan;
+      result->error_l2 = r.error_l2 ? *r.error_l2 : nan;
+      result->mean_iterations = r.mean_iterations;
+      result->total_iterations = r.total_iterations;
+      result->steps = r.steps;
+      result->solver_failure = r.solver_failure ? 1 : 0;
+      result->wall_seconds = r.wall_seconds;
+      result->n_solves = (int)r.solve_iterations.size();
+      for (int i = 0; i < result->n_solves && i < result->solve_iterations_capacity && result->solve_iterations; ++i)
+        result->solve_iterations[i] = r.solve_iterations[i];
+    }
+  }
+}
+
+int mprkb_integrate(const mprkb_config* cfg, const double* reference_host, size_t reference_len,
+                    double* state_host, mprkb_result* result) {
+  return guarded([&] {
+    const StepperConfig c = config_of(cfg);
+    std::vector<double> ref;
+    if (reference_host) ref.assign(reference_host, reference_host + reference_len);
+    fill_result(integrate(c, reference_host ? &ref : nullptr), state_host, result);
+  });
+}
+
+int mprkb_stepper_integrate(mprkb_stepper* s, const double* reference_host, size_t reference_len,
+                            double* state_host, mprkb_result* result) {
+  return guarded([&] {
+    std::vector<double> ref;
+    if (reference_host) ref.assign(reference_host, reference_host + reference_len);
+    fill_result(integrate_with(*s->s, reference_host ? &ref : nullptr, std::chrono::steady_clock::now()),
+                state_host, result);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,414 @@
+#include "krylov.hpp"
+
+#include <cmath>
+#include <complex>
+#include <cstring>
+
+namespace mprkb {
+
+// ---------------------------------------------------------------------------
+// EventTimer
+// ---------------------------------------------------------------------------
+EventTimer::~EventTimer() {
+  for (auto& o : open_) {
+    cudaEventDestroy(o.a);
+    cudaEventDestroy(o.b);
+  }
+  for (auto e : pool_) cudaEventDestroy(e);
+}
+
+cudaEvent_t EventTimer::get() {
+  if (!pool_.empty()) {
+    cudaEvent_t e = pool_.back();
+    pool_.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  CUDA_CHECK(cudaEventCreate(&e));
+  return e;
+}
+
+int EventTimer::begin(const char* label, cudaStream_t st) {
+  if (!enabled_) return -1;
+  Open o{label, get(), get()};
+  CUDA_CHECK(cudaEventRecord(o.a, st));
+  open_.push_back(o);
+  return (int)open_.size() - 1;
+}
+
+void EventTimer::end(int id, cudaStream_t st) {
+  if (id < 0) return;
+  CUDA_CHECK(cudaEventRecord(open_[id].b, st));
+}
+
+void EventTimer::resolve() {
+  for (auto& o : open_) {
+    float ms = 0.f;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, o.a, o.b));
+    Entry* e = nullptr;
+    for (auto& x : entries_)
+      if (x.label == o.label) e = &x;
+    if (!e) {
+      entries_.push_back(Entry{o.label, 0, 0.0});
+      e = &entries_.back();
+    }
+    ++e->count;
+    e->seconds += ms * 1e-3;
+    pool_.push_back(o.a);
+    pool_.push_back(o.b);
+  }
+  open_.clear();
+}
+
+namespace {
+
+struct Bracket {
+  EventTimer* t;
+  int id;
+  cudaStream_t st;
+  Bracket(EventTimer* timer, const char* label, cudaStream_t s) : t(timer), id(-1), st(s) {
+    if (t) id = t->begin(label, st);
+  }
+  ~Bracket() {
+    if (t) t->end(id, st);
+  }
+};
+
+template <class T> struct HostScalar { using type = T; };
+template <> struct HostScalar<c32> { using type = std::complex<float>; };
+template <> struct HostScalar<c64> { using type = std::complex<double>; };
+
+// detail::scalar_cast<T>(double) (operators.hpp:30-33)
+template <class H>
+H scast(double x) {
+  if constexpr (std::is_floating_point_v<H>)
+    return static_cast<H>(x);
+  else
+    return static_cast<H>(static_cast<typename H::value_type>(x));
+}
+template <class H>
+H conj_val(H x) {
+  if constexpr (std::is_floating_point_v<H>)
+    return x;
+  else
+    return std::conj(x);
+}
+template <class T, class H>
+T to_dev(const H& h) {
+  T t;
+  static_assert(sizeof(T) == sizeof(H));
+  std::memcpy(&t, &h, sizeof(T));
+  return t;
+}
+
+}  // namespace
+
+template <class T>
+KrylovWork<T>::KrylovWork(size_t m) : red(2), m_(m) {
+  for (auto& v : vecs_) v.alloc(m * sizeof(T));
+}
+
+template <class T>
+T* KrylovWork<T>::basis(int j) {
+  while ((int)basis_.size() <= j) basis_.emplace_back(m_ * sizeof(T));
+  return basis_[j].template as<T>();
+}
+
+// ---------------------------------------------------------------------------
+// cg<T>  (krylov.hpp:100-168)
+// ---------------------------------------------------------------------------
+template <class T>
+void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, KrylovWork<T>& w,
+              SolveReport& rep, cudaStream_t st, EventTimer* timer) {
+  using R = real_t<T>;
+  const size_t m = w.size();
+  if (A.size() != m || (P && P->size() != m)) MPRKB_THROW(2, "cg: operator size != vector length");
+  rep = SolveReport{};
+  Bracket whole(timer, "solver", st);
+  const bool fast = num == Numerics::Fast;
+  const StencilSpec* S = fast ? A.stencil() : nullptr;
+  const RedSlot s0 = w.red.slot(0);
+  T *r = w.v(0), *z = w.v(1), *p = w.v(2), *q = w.v(3);
+
+  auto fetch = [&]() -> R {
+    stream_sync(st);
+    return (R)w.red.host(0)[0];
+  };
+  auto rdot = [&](const T* a, const T* c) -> R {
+    dot_real<T>(m, a, c, s0, num, st);
+    return fetch();
+  };
+  auto op = [&](const T* in, T* out) {
+    Bracket br(timer, "stencil", st);
+    A.apply(in, out, st);
+  };
+  auto pre = [&](const T* in, T* out) {
+    if (P) {
+      Bracket br(timer, "precond", st);
+      P->apply(in, out, st);
+    } else {
+      CUDA_CHECK(cudaMemcpyAsync(out, in, m * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    }
+  };
+  // dst = b - A x, returns dot_real(dst, dst)
+  auto residual = [&](T* dst) -> R {
+    if (S) {
+      Bracket br(timer, "stencil", st);
+      stencil_residual<T>(*S, x, b, dst, &s0, st);
+      return fetch();
+    }
+    op(x, q);
+    vsub<T>(m, b, q, dst, fast ? &s0 : nullptr, st);
+    return fast ? fetch() : rdot(dst, dst);
+  };
+
+  const double r0 = (double)std::sqrt(residual(r));
+  rep.history.push_back(r0);
+  double rnorm = r0;
+  bool x_clean = true;  // ||b - A x|| of the current x is known
+  double clean_true = r0;
+  if (crit.satisfied(rnorm, r0)) {
+    rep.converged = true;
+  } else {
+    pre(r, z);
+    std::swap(p, z);  // p = z
+    R rz = rdot(r, p);
+    for (int k = 0; k < crit.max_iter; ++k) {
+      if (!(rz > R{})) {
+        rep.failure = 2;
+        break;
+      }
+      R pq;
+      if (S) {
+        Bracket br(timer, "stencil", st);
+        stencil_apply_dot<T>(*S, p, q, s0, st);
+        pq = fetch();
+      } else {
+        op(p, q);
+        pq = rdot(p, q);
+      }
+      if (!(pq > R{})) {
+        rep.failure = 2;
+        break;
+      }
+      const R alpha = rz / pq;
+      cg_update<T>(m, alpha, x, p, r, q, fast ? &s0 : nullptr, st);
+      x_clean = false;
+      ++rep.iterations;
+      rnorm = (double)std::sqrt(fast ? fetch() : rdot(r, r));
+      rep.history.push_back(rnorm);
+      if (crit.satisfied(rnorm, r0)) {
+        const double rt = (double)std::sqrt(residual(q));
+        x_clean = true;
+        clean_true = rt;
+        if (crit.satisfied(rt, r0)) {
+          rep.converged = true;
+          break;
+        }
+        std::swap(r, q);  // r = q (verified residual), restart
+        rep.history.back() = rt;
+        pre(r, z);
+        std::swap(p, z);
+        rz = rdot(r, p);
+        continue;
+      }
+      pre(r, z);
+      const R rz_next = rdot(r, z);
+      const R beta = rz_next / rz;
+      rz = rz_next;
+      xpby<T>(m, z, beta, p, st);
+    }
+    if (!rep.converged && rep.failure == 0) rep.failure = 1;
+  }
+  // exit true residual (krylov.hpp:164-166): recomputing it for an unchanged
+  // x would reproduce the same value, so reuse it.
+  rep.true_residual = x_clean ? clean_true : (double)std::sqrt(residual(q));
+}
+
+// ---------------------------------------------------------------------------
+// gmres<T>  (krylov.hpp:181-311)
+// ---------------------------------------------------------------------------
+template <class T>
+void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, KrylovWork<T>& w,
+                 SolveReport& rep, cudaStream_t st, EventTimer* timer) {
+  using R = real_t<T>;
+  using H = typename HostScalar<T>::type;
+  const size_t m = w.size();
+  if (A.size() != m || (P && P->size() != m)) MPRKB_THROW(2, "gmres: operator size != vector length");
+  rep = SolveReport{};
+  Bracket whole(timer, "solver", st);
+  const bool fast = num == Numerics::Fast;
+  const RedSlot s0 = w.red.slot(0);
+  const int kmax = crit.max_iter;
+  T *t = w.v(0), *wv = w.v(1), *xc = w.v(2), *wt = w.v(3);
+
+  auto fetch = [&]() -> R {
+    stream_sync(st);
+    return (R)w.red.host(0)[0];
+  };
+  auto norm2 = [&](const T* v) -> R {
+    dot_real<T>(m, v, v, s0, num, st);
+    return std::sqrt(fetch());
+  };
+  auto dotc = [&](const T* a, const T* c) -> H {
+    dot_conj<T>(m, a, c, s0, num, st);
+    stream_sync(st);
+    if constexpr (is_cplx<T>)
+      return H((R)w.red.host(0)[0], (R)w.red.host(0)[1]);
+    else
+      return (R)w.red.host(0)[0];
+  };
+  auto op = [&](const T* in, T* out) {
+    Bracket br(timer, "stencil", st);
+    A.apply(in, out, st);
+  };
+  auto pre = [&](const T* in, T* out) {
+    if (P) {
+      Bracket br(timer, "precond", st);
+      P->apply(in, out, st);
+    } else {
+      CUDA_CHECK(cudaMemcpyAsync(out, in, m * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    }
+  };
+  // dst = b - A v  (fused when the operator is a stencil and numerics FAST)
+  auto residual_of = [&](const T* v, T* dst) {
+    if (fast && A.stencil()) {
+      Bracket br(timer, "stencil", st);
+      stencil_residual<T>(*A.stencil(), v, b, dst, nullptr, st);
+      return;
+    }
+    op(v, dst);
+    vsub<T>(m, b, dst, dst, nullptr, st);
+  };
+
+  residual_of(x, t);
+  pre(t, wv);  // w = P(b - A x0)
+  const double beta = (double)norm2(wv);
+  rep.history.push_back(beta);
+
+  if (crit.satisfied(beta, beta) || beta == 0.0) {
+    rep.converged = true;
+  } else {
+    std::vector<std::vector<H>> h_cols;
+    h_cols.reserve(kmax);
+    std::vector<R> cs(kmax, R{});
+    std::vector<H> sn(kmax, H{});
+    std::vector<H> s(kmax + 1, H{});
+    std::vector<T*> basis;
+    s[0] = scast<H>(beta);
+    bool x_built = false;
+
+    // xc = x + sum_j y_j v_j with y from the rotated triangular system
+    auto candidate_into = [&](int cols, T* dst) {
+      std::vector<H> y(cols, H{});
+      for (int i = cols - 1; i >= 0; --i) {
+        H acc = s[i];
+        for (int j = i + 1; j < cols; ++j) acc -= h_cols[j][i] * y[j];
+        y[i] = acc / h_cols[i][i];
+      }
+      std::vector<T> yd(cols);
+      for (int j = 0; j < cols; ++j) yd[j] = to_dev<T>(y[j]);
+      candidate<T>(m, x, basis.data(), yd.data(), cols, dst, st);
+    };
+
+    {
+      const H inv0 = scast<H>(1.0) / scast<H>(beta);
+      basis.push_back(w.basis(0));
+      vscale<T>(m, wv, to_dev<T>(inv0), basis[0], st);
+    }
+
+    int k = 0;
+    for (; k < kmax;) {
+      op(basis[k], t);
+      pre(t, wv);
+      std::vector<H> h(k + 2, H{});
+      for (int j = 0; j <= k; ++j) {  // modified Gram-Schmidt
+        const H hj = dotc(basis[j], wv);
+        h[j] = hj;
+        vaxmy<T>(m, to_dev<T>(hj), basis[j], wv, st);
+      }
+      const R wnorm = norm2(wv);
+      h[k + 1] = scast<H>(static_cast<double>(wnorm));
+      const bool happy = !(static_cast<double>(wnorm) > 0.0);
+
+      for (int j = 0; j < k; ++j) {
+        const H tmp = scast<H>(cs[j]) * h[j] + sn[j] * h[j + 1];
+        h[j + 1] = scast<H>(cs[j]) * h[j + 1] - conj_val(sn[j]) * h[j];
+        h[j] = tmp;
+      }
+      const R anorm = std::abs(h[k]);
+      const R bnorm = std::abs(h[k + 1]);
+      const R rho = std::sqrt(anorm * anorm + bnorm * bnorm);
+      if (rho == R{}) {
+        cs[k] = R{1};
+        sn[k] = H{};
+      } else if (anorm == R{}) {
+        cs[k] = R{};
+        sn[k] = scast<H>(1.0);
+      } else {
+        cs[k] = anorm / rho;
+        sn[k] = (h[k] / scast<H>(static_cast<double>(anorm))) * scast<H>(static_cast<double>(bnorm / rho));
+      }
+      h[k] = scast<H>(cs[k]) * h[k] + sn[k] * h[k + 1];
+      h[k + 1] = H{};
+      s[k + 1] = -conj_val(sn[k]) * s[k];
+      s[k] = scast<H>(cs[k]) * s[k];
+      h_cols.push_back(std::move(h));
+
+      ++rep.iterations;
+      ++k;
+      const double est = static_cast<double>(std::abs(s[k]));
+      rep.history.push_back(est);
+
+      if (happy) {
+        rep.converged = true;
+        break;
+      }
+      if (crit.satisfied(est, beta)) {
+        candidate_into(k, xc);
+        residual_of(xc, t);
+        pre(t, wt);
+        const double rt = static_cast<double>(norm2(wt));
+        if (crit.satisfied(rt, beta)) {
+          CUDA_CHECK(cudaMemcpyAsync(x, xc, m * sizeof(T), cudaMemcpyDeviceToDevice, st));
+          x_built = true;
+          rep.converged = true;
+          break;
+        }
+        rep.history.back() = rt;
+      }
+      if (k == kmax) break;
+      const H inv = scast<H>(1.0) / scast<H>(static_cast<double>(wnorm));
+      basis.push_back(w.basis(k));
+      vscale<T>(m, wv, to_dev<T>(inv), basis[k], st);
+    }
+    if (!rep.converged) rep.failure = 1;
+    if (!x_built) {
+      candidate_into(k, xc);
+      CUDA_CHECK(cudaMemcpyAsync(x, xc, m * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    }
+  }
+
+  residual_of(x, t);
+  rep.true_residual = static_cast<double>(norm2(t));
+}
+
+template class KrylovWork<float>;
+template class KrylovWork<double>;
+template class KrylovWork<c32>;
+template class KrylovWork<c64>;
+
+template void cg_solve<float>(Op&, Op*, const float*, float*, const Crit&, Numerics, KrylovWork<float>&,
+                              SolveReport&, cudaStream_t, EventTimer*);
+template void cg_solve<double>(Op&, Op*, const double*, double*, const Crit&, Numerics, KrylovWork<double>&,
+                               SolveReport&, cudaStream_t, EventTimer*);
+template void gmres_solve<float>(Op&, Op*, const float*, float*, const Crit&, Numerics, KrylovWork<float>&,
+                                 SolveReport&, cudaStream_t, EventTimer*);
+template void gmres_solve<double>(Op&, Op*, const double*, double*, const Crit&, Numerics,
+                                  KrylovWork<double>&, SolveReport&, cudaStream_t, EventTimer*);
+template void gmres_solve<c32>(Op&, Op*, const c32*, c32*, const Crit&, Numerics, KrylovWork<c32>&,
+                               SolveReport&, cudaStream_t, EventTimer*);
+template void gmres_solve<c64>(Op&, Op*, const c64*, c64*, const Crit&, Numerics, KrylovWork<c64>&,
+                               SolveReport&, cudaStream_t, EventTimer*);
+
+}  // namespace mprkb

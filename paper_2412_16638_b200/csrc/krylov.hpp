@@ -1,0 +1,87 @@
+// Preconditioned CG and left-preconditioned MGS-GMRES on device vectors
+// (krylov.hpp:100-311 of the reference).  All O(1)/O(k^2) scalar logic —
+// alpha, beta, the stopping tests, the true-residual veto, Givens rotations,
+// the Hessenberg back-substitution — runs on the host in the reference's own
+// expressions (this file is compiled by g++), so with PARITY numerics the
+// iterates, residual histories and iteration counts are bitwise the
+// reference's; with FAST numerics the vector work uses fused kernels and
+// fp64-accumulated tree reductions.
+#pragma once
+
+#include <string>
+#include <vector>
+
+#include "ops.hpp"
+
+namespace mprkb {
+
+struct Crit {
+  double tol = 1e-6;
+  int max_iter = 40;
+  // StoppingCriterion::satisfied (krylov.hpp:21-23)
+  bool satisfied(double rnorm, double r0norm) const {
+    return rnorm <= tol || (r0norm > 0 && rnorm / r0norm <= tol);
+  }
+};
+
+struct SolveReport {
+  int iterations = 0;
+  bool converged = false;
+  int failure = 0;  // 0 none, 1 max-iter, 2 breakdown
+  double true_residual = 0.0;
+  std::vector<double> history;
+};
+
+// Per-label device-time accumulator (TimingRegistry, timing.hpp:23-47) fed by
+// CUDA event brackets; resolved with resolve() after a stream synchronize.
+class EventTimer {
+ public:
+  explicit EventTimer(bool enabled) : enabled_(enabled) {}
+  ~EventTimer();
+  bool enabled() const { return enabled_; }
+  int begin(const char* label, cudaStream_t st);  // returns bracket id (-1 disabled)
+  void end(int id, cudaStream_t st);
+  void resolve();  // call after the stream is idle
+  struct Entry {
+    std::string label;
+    long long count = 0;
+    double seconds = 0.0;
+  };
+  const std::vector<Entry>& entries() const { return entries_; }
+
+ private:
+  struct Open {
+    std::string label;
+    cudaEvent_t a, b;
+  };
+  bool enabled_;
+  std::vector<Open> open_;
+  std::vector<cudaEvent_t> pool_;
+  std::vector<Entry> entries_;
+  cudaEvent_t get();
+};
+
+template <class T>
+class KrylovWork {
+ public:
+  explicit KrylovWork(size_t m);
+  T* v(int i) { return vecs_[i].template as<T>(); }
+  T* basis(int j);
+  size_t size() const { return m_; }
+  Reducer red;
+
+ private:
+  size_t m_;
+  DevBuf vecs_[4];
+  std::vector<DevBuf> basis_;
+};
+
+template <class T>
+void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, KrylovWork<T>& w,
+              SolveReport& rep, cudaStream_t st, EventTimer* timer = nullptr);
+
+template <class T>
+void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, KrylovWork<T>& w,
+                 SolveReport& rep, cudaStream_t st, EventTimer* timer = nullptr);
+
+}  // namespace mprkb

@@ -1,0 +1,99 @@
+// Host-side launchers of the sm_100a kernels (defined in kernels.cu).
+//
+// Every launcher takes device pointers and a stream, never allocates, and
+// mirrors one reference function (file:line in kernels.cu).
+#pragma once
+
+#include "types.hpp"
+
+namespace mprkb {
+
+// ---- stencil family (operators.hpp:113-161) ------------------------------------
+struct StencilSpec {
+  int n = 0;
+  int stencil = 0;      // 0 Dirichlet Laplace, 1 periodic central, 2 adv-diff (central + periodic Laplace)
+  double sigma = 0.0;   // identity shift
+  double gamma = 0.0;   // stencil scale
+  double gamma2 = 0.0;  // second (diffusion) scale for stencil 2
+};
+
+// out = sigma x + gamma K3 x
+template <class T>
+void stencil_apply(const StencilSpec& s, const T* x, T* out, cudaStream_t st);
+// r = b - (sigma x + gamma K3 x); optional fused fp64 sum of r.r into `red`
+template <class T>
+void stencil_residual(const StencilSpec& s, const T* x, const T* b, T* r, const RedSlot* red,
+                      cudaStream_t st);
+// q = A p with fused p.q (dot_real) into red
+template <class T>
+void stencil_apply_dot(const StencilSpec& s, const T* p, T* q, const RedSlot& red, cudaStream_t st);
+
+// apply_f (operators.cpp:81-96), F64 policy: out = K y + g, y read as double
+// or widened from float (`y32`), g may be null.
+void apply_f64(const StencilSpec& k, const double* y, const float* y32, const double* g, double* out,
+               cudaStream_t st);
+// apply_f F32 policy: out32 = K f32(y) + f32(g) in binary32 (stored as float;
+// widening to double is exact and deferred to the consumer).  Sets *flag when
+// |y| overflows binary32 (precision.hpp:100-104).
+void apply_f32(const StencilSpec& k, const double* y, const float* y32, const float* g32, float* out32,
+               int* flag, cudaStream_t st);
+
+// ---- tensor contractions (precond.hpp:69-122) --------------------------------------
+// side 0 L (stride n^2), 1 M (stride n), 2 R (stride 1).  pd: fused diag scale
+// of the output (precond.hpp:172) or null.
+template <class T>
+void tensor_apply(int side, int n, const T* q, const T* x, T* out, const T* pd, Numerics num,
+                  cudaStream_t st);
+// pd_inv[i+jn+kn^2] = 1/(la_i + lb_j + lc_k) in T (precond.hpp:139-150); real
+// types only (IEEE division is correctly rounded on both sides).  *zero_flag
+// (initialised to INT_MAX by the caller) receives the smallest linear index
+// whose eigenvalue sum is exactly zero.
+template <class T>
+void pd_inv_device(int n, const T* la, const T* lb, const T* lc, T* pd, int* zero_flag, cudaStream_t st);
+
+// ---- reductions (krylov.hpp:43-71) --------------------------------------------------
+// dot_real(a, b): FAST -> fp64 tree into red.out[0]; PARITY -> sequential in real_t<T>
+template <class T>
+void dot_real(size_t m, const T* a, const T* b, const RedSlot& red, Numerics num, cudaStream_t st);
+// complex dot with conjugated first argument -> red.out[0..1]
+template <class T>
+void dot_conj(size_t m, const T* a, const T* b, const RedSlot& red, Numerics num, cudaStream_t st);
+
+// ---- vector updates (krylov.hpp:111-158, 191-301) ------------------------------------
+template <class T>
+void vsub(size_t m, const T* b, const T* q, T* r, const RedSlot* red, cudaStream_t st);  // r = b - q
+template <class T>
+void cg_update(size_t m, real_t<T> alpha, T* x, const T* p, T* r, const T* q, const RedSlot* red,
+               cudaStream_t st);  // x += a p; r -= a q
+template <class T>
+void xpby(size_t m, const T* z, real_t<T> beta, T* p, cudaStream_t st);  // p = z + beta p
+template <class T>
+void vscale(size_t m, const T* w, T s, T* v, cudaStream_t st);  // v = w * s
+template <class T>
+void vaxmy(size_t m, T h, const T* v, T* w, cudaStream_t st);  // w -= h v
+// xc = x + sum_j y_j v_j (sequential in j per element)
+template <class T>
+void candidate(size_t m, const T* x, const T* const* basis, const T* y, int cols, T* xc,
+               cudaStream_t st);
+
+// ---- stage kernels (stepper.cpp:14-33, 157-205) ------------------------------------------
+constexpr int kMaxTerms = 40;
+struct CombineTerms {
+  int count = 0;
+  double coef[kMaxTerms];
+  const void* ptr[kMaxTerms];
+  int is_f32[kMaxTerms];
+};
+// rhs = u + sum_t coef_t * v_t (one axpy per term, in order), written as:
+// out_kind 0: double (+ finite flag), 1: float (downcast, overflow flag),
+// 2: c32 (float, 0), 3: c64 (double, 0).
+void combine(size_t m, const double* u, const CombineTerms& t, int out_kind, void* out, int* flag,
+             cudaStream_t st);
+// y = widen(x) / real_part(x) of the solver output, + non-finite flag.
+void extract_stage(size_t m, int src_kind, const void* x, double* y, int* flag, cudaStream_t st);
+// u += sum_t coef_t * v_t, + non-finite flag on u.
+void final_update(size_t m, double* u, const CombineTerms& t, int* flag, cudaStream_t st);
+// element casts for the op-level API: narrow (overflow flag) / widen / promote
+void narrow_f64(size_t m, const double* x, float* y, int* flag, cudaStream_t st);
+
+}  // namespace mprkb

@@ -1,0 +1,211 @@
+#include "ops.hpp"
+
+#include <climits>
+#include <complex>
+#include <cstring>
+
+namespace mprkb {
+
+namespace {
+
+template <class T>
+struct HostOf {
+  using type = T;
+};
+template <>
+struct HostOf<c32> {
+  using type = std::complex<float>;
+};
+template <>
+struct HostOf<c64> {
+  using type = std::complex<double>;
+};
+
+// downcast_scalar (precision.hpp:100-104): RNE narrowing, refusing overflow
+float narrow(double x) {
+  if (!std::isnan(x) && std::abs(x) >= 3.402823669209384634633746074317e+38)
+    MPRKB_THROW(6, "downcast: |" + std::to_string(x) + "| exceeds the binary32 range");
+  return static_cast<float>(x);
+}
+
+void upload(DevBuf& d, const void* host, size_t bytes) {
+  d.alloc(bytes);
+  CUDA_CHECK(cudaMemcpy(d.get(), host, bytes, cudaMemcpyHostToDevice));
+}
+
+}  // namespace
+
+StencilOp::StencilOp(int dtype, const StencilSpec& s) : Op(dtype, (size_t)s.n * s.n * s.n), spec_(s) {
+  if (s.n < 2) MPRKB_THROW(3, "KronSumOperator: n must be at least 2");
+}
+
+void StencilOp::apply(const void* x, void* out, cudaStream_t st) {
+  switch (dtype()) {
+    case 0: stencil_apply<float>(spec_, static_cast<const float*>(x), static_cast<float*>(out), st); break;
+    case 1: stencil_apply<double>(spec_, static_cast<const double*>(x), static_cast<double*>(out), st); break;
+    case 2: stencil_apply<c32>(spec_, static_cast<const c32*>(x), static_cast<c32*>(out), st); break;
+    case 3: stencil_apply<c64>(spec_, static_cast<const c64*>(x), static_cast<c64*>(out), st); break;
+    default: MPRKB_THROW(10, "stencil: unsupported dtype");
+  }
+}
+
+template <class T>
+FastDiagOp<T>::FastDiagOp(int n, const T* qa, const T* qa_inv, const T* qb, const T* qb_inv, const T* qc,
+                          const T* qc_inv, const T* la, const T* lb, const T* lc, Numerics num)
+    : Op(dtype_of<T>::v, (size_t)n * n * n), n_(n), num_(num) {
+  if (n < 2) MPRKB_THROW(3, "FastDiagPreconditioner: n must be at least 2");
+  const size_t nn = (size_t)n * n, m = nn * n;
+  const T* src[6] = {qa, qa_inv, qb, qb_inv, qc, qc_inv};
+  for (int i = 0; i < 6; ++i) upload(q_[i], src[i], nn * sizeof(T));
+  pd_.alloc(m * sizeof(T));
+  t1_.alloc(m * sizeof(T));
+  t2_.alloc(m * sizeof(T));
+  int zi = INT_MAX;
+  if constexpr (!is_cplx<T>) {
+    // pd_inv[i+jn+kn^2] = 1/(la_i+lb_j+lc_k) in T on the device: IEEE
+    // division and the same left-to-right sum => bitwise the reference's.
+    DevBuf dl, flag(sizeof(int));
+    std::vector<T> lam(3 * (size_t)n);
+    std::memcpy(lam.data(), la, n * sizeof(T));
+    std::memcpy(lam.data() + n, lb, n * sizeof(T));
+    std::memcpy(lam.data() + 2 * n, lc, n * sizeof(T));
+    upload(dl, lam.data(), lam.size() * sizeof(T));
+    CUDA_CHECK(cudaMemcpy(flag.get(), &zi, sizeof(int), cudaMemcpyHostToDevice));
+    pd_inv_device<T>(n, dl.as<T>(), dl.as<T>() + n, dl.as<T>() + 2 * n, pd_.as<T>(), flag.as<int>(), 0);
+    CUDA_CHECK(cudaMemcpy(&zi, flag.get(), sizeof(int), cudaMemcpyDeviceToHost));
+  } else {
+    // complex: 1/sum through libgcc's complex division on the host, exactly
+    // the reference's ctor (precond.hpp:140-150), then upload.
+    using H = typename HostOf<T>::type;
+    const H* A = reinterpret_cast<const H*>(la);
+    const H* B = reinterpret_cast<const H*>(lb);
+    const H* C = reinterpret_cast<const H*>(lc);
+    std::vector<H> pd(m);
+    const H one = static_cast<H>(static_cast<typename H::value_type>(1.0));
+    for (size_t k = 0; k < (size_t)n && zi == INT_MAX; ++k)
+      for (size_t j = 0; j < (size_t)n && zi == INT_MAX; ++j)
+        for (size_t i = 0; i < (size_t)n; ++i) {
+          const H sum = A[i] + B[j] + C[k];
+          if (sum == H{}) {
+            zi = (int)(i + j * n + k * nn);
+            break;
+          }
+          pd[i + j * n + k * nn] = one / sum;
+        }
+    if (zi == INT_MAX) CUDA_CHECK(cudaMemcpy(pd_.get(), pd.data(), m * sizeof(T), cudaMemcpyHostToDevice));
+  }
+  if (zi != INT_MAX) {
+    const int i = zi % n, j = (zi / n) % n, k = zi / (int)nn;
+    MPRKB_THROW(7, "FastDiagPreconditioner: eigenvalue triple sums to zero at (" + std::to_string(i) + "," +
+                       std::to_string(j) + "," + std::to_string(k) + ")");
+  }
+}
+
+// apply_inverse (precond.hpp:153-186): R, M, L with the inverse factors, the
+// diagonal scale fused into the L pass, then R, M, L with the forward factors.
+template <class T>
+void FastDiagOp<T>::apply(const void* xv, void* outv, cudaStream_t st) {
+  const T* x = static_cast<const T*>(xv);
+  T* out = static_cast<T*>(outv);
+  T* t1 = t1_.as<T>();
+  T* t2 = t2_.as<T>();
+  tensor_apply<T>(2, n_, q_[1].as<T>(), x, t1, nullptr, num_, st);
+  tensor_apply<T>(1, n_, q_[3].as<T>(), t1, t2, nullptr, num_, st);
+  tensor_apply<T>(0, n_, q_[5].as<T>(), t2, t1, pd_.as<T>(), num_, st);
+  tensor_apply<T>(2, n_, q_[0].as<T>(), t1, t2, nullptr, num_, st);
+  tensor_apply<T>(1, n_, q_[2].as<T>(), t2, t1, nullptr, num_, st);
+  tensor_apply<T>(0, n_, q_[4].as<T>(), t1, out, nullptr, num_, st);
+}
+
+template class FastDiagOp<float>;
+template class FastDiagOp<double>;
+template class FastDiagOp<c32>;
+template class FastDiagOp<c64>;
+
+void CallbackOp::apply(const void* x, void* out, cudaStream_t st) {
+  const int rc = fn_(ctx_, x, out, st);
+  if (rc != 0) MPRKB_THROW(rc, "ApplyFn callback returned an error");
+}
+
+StencilSpec stage_spec(const Problem& p, double tau, double a) {
+  StencilSpec s;
+  s.n = p.n;
+  s.stencil = p.eq == Equation::Heat ? 0 : (p.eq == Equation::Advection ? 1 : 2);
+  s.sigma = 1.0;
+  s.gamma = -tau * a * p.gamma_k;
+  s.gamma2 = -tau * a * p.gamma_d;
+  return s;
+}
+
+StencilSpec rhs_spec(const Problem& p) {
+  StencilSpec s;
+  s.n = p.n;
+  s.stencil = p.eq == Equation::Heat ? 0 : (p.eq == Equation::Advection ? 1 : 2);
+  s.sigma = 0.0;
+  s.gamma = p.gamma_k;
+  s.gamma2 = p.gamma_d;
+  return s;
+}
+
+std::unique_ptr<Op> make_stage_fastdiag(int dtype, const Problem& p, double tau, double a, Numerics num) {
+  const double g = -tau * a * p.gamma_k;  // stage_gamma (precond.cpp:10-12)
+  const int n = p.n;
+  if (p.eq == Equation::Heat) {
+    std::vector<double> qa, qai, la, qb, qbi, lb;
+    spectral_dirichlet(n, 1.0, g, qa, qai, la);
+    spectral_dirichlet(n, 0.0, g, qb, qbi, lb);
+    if (dtype == 1)
+      return std::make_unique<FastDiagOp<double>>(n, qa.data(), qai.data(), qb.data(), qbi.data(), qb.data(),
+                                                  qbi.data(), la.data(), lb.data(), lb.data(), num);
+    if (dtype != 0) MPRKB_THROW(10, "heat preconditioner: dtype must be F32 or F64");
+    auto nar = [](const std::vector<double>& v) {
+      std::vector<float> o(v.size());
+      for (size_t i = 0; i < v.size(); ++i) o[i] = narrow(v[i]);
+      return o;
+    };
+    const auto fa = nar(qa), fai = nar(qai), fla = nar(la), fb = nar(qb), fbi = nar(qbi), flb = nar(lb);
+    return std::make_unique<FastDiagOp<float>>(n, fa.data(), fai.data(), fb.data(), fbi.data(), fb.data(),
+                                               fbi.data(), fla.data(), flb.data(), flb.data(), num);
+  }
+  const double g2 = -tau * a * p.gamma_d;
+  std::vector<std::complex<double>> qa, qai, la, qb, qbi, lb;
+  spectral_periodic(n, 1.0, g, qa, qai, la, g2);
+  spectral_periodic(n, 0.0, g, qb, qbi, lb, g2);
+  if (dtype == 3)
+    return std::make_unique<FastDiagOp<c64>>(
+        n, reinterpret_cast<const c64*>(qa.data()), reinterpret_cast<const c64*>(qai.data()),
+        reinterpret_cast<const c64*>(qb.data()), reinterpret_cast<const c64*>(qbi.data()),
+        reinterpret_cast<const c64*>(qb.data()), reinterpret_cast<const c64*>(qbi.data()),
+        reinterpret_cast<const c64*>(la.data()), reinterpret_cast<const c64*>(lb.data()),
+        reinterpret_cast<const c64*>(lb.data()), num);
+  if (dtype != 2) MPRKB_THROW(10, "advection preconditioner: dtype must be C32 or C64");
+  auto nar = [](const std::vector<std::complex<double>>& v) {
+    std::vector<std::complex<float>> o(v.size());
+    for (size_t i = 0; i < v.size(); ++i) o[i] = {narrow(v[i].real()), narrow(v[i].imag())};
+    return o;
+  };
+  const auto fa = nar(qa), fai = nar(qai), fla = nar(la), fb = nar(qb), fbi = nar(qbi), flb = nar(lb);
+  auto C = [](const std::vector<std::complex<float>>& v) { return reinterpret_cast<const c32*>(v.data()); };
+  return std::make_unique<FastDiagOp<c32>>(n, C(fa), C(fai), C(fb), C(fbi), C(fb), C(fbi), C(fla), C(flb),
+                                           C(flb), num);
+}
+
+std::unique_ptr<Op> make_fastdiag(int dtype, int n, const void* qa, const void* qa_inv, const void* qb,
+                                  const void* qb_inv, const void* qc, const void* qc_inv, const void* la,
+                                  const void* lb, const void* lc, Numerics num) {
+  switch (dtype) {
+#define MK(T)                                                                                             \
+  return std::make_unique<FastDiagOp<T>>(                                                                 \
+      n, static_cast<const T*>(qa), static_cast<const T*>(qa_inv), static_cast<const T*>(qb),             \
+      static_cast<const T*>(qb_inv), static_cast<const T*>(qc), static_cast<const T*>(qc_inv),            \
+      static_cast<const T*>(la), static_cast<const T*>(lb), static_cast<const T*>(lc), num)
+    case 0: MK(float);
+    case 1: MK(double);
+    case 2: MK(c32);
+    case 3: MK(c64);
+#undef MK
+  }
+  MPRKB_THROW(10, "fastdiag: unsupported dtype");
+}
+
+}  // namespace mprkb

@@ -1,0 +1,91 @@
+// Linear operators on device vectors: the B200 side of the reference's
+// ApplyFn<T> plug-in slot (krylov.hpp:38-39).
+#pragma once
+
+#include <memory>
+#include <vector>
+
+#include "launch.hpp"
+#include "problem.hpp"
+#include "runtime.hpp"
+
+namespace mprkb {
+
+class Op {
+ public:
+  Op(int dtype, size_t m) : dtype_(dtype), m_(m) {}
+  virtual ~Op() = default;
+  int dtype() const { return dtype_; }
+  size_t size() const { return m_; }
+  virtual void apply(const void* x, void* out, cudaStream_t st) = 0;
+  // Non-null when the operator is a built-in KronSum stencil: lets the FAST
+  // solvers fuse residual / dot epilogues into the stencil pass.
+  virtual const StencilSpec* stencil() const { return nullptr; }
+
+ private:
+  int dtype_;
+  size_t m_;
+};
+
+// KronSumOperator (operators.hpp:35-48): sigma I + gamma (I(x)I(x)K + ...).
+class StencilOp final : public Op {
+ public:
+  StencilOp(int dtype, const StencilSpec& s);
+  void apply(const void* x, void* out, cudaStream_t st) override;
+  const StencilSpec* stencil() const override { return &spec_; }
+
+ private:
+  StencilSpec spec_;
+};
+
+// FastDiagPreconditioner<T> (precond.hpp:30-53): P^-1 = (Qc(x)Qb(x)Qa) diag(pd)
+// (Qc^-1 (x) Qb^-1 (x) Qa^-1).  Device-resident factors, pd_inv and two
+// scratch vectors (not re-entrant, like the reference's mutable t1_/t2_).
+template <class T>
+class FastDiagOp final : public Op {
+ public:
+  // Host arrays in T layout: q* (n*n row-major), lambda_* (n).
+  FastDiagOp(int n, const T* qa, const T* qa_inv, const T* qb, const T* qb_inv, const T* qc, const T* qc_inv,
+             const T* la, const T* lb, const T* lc, Numerics num);
+  void apply(const void* x, void* out, cudaStream_t st) override;
+  int n() const { return n_; }
+
+ private:
+  int n_;
+  Numerics num_;
+  DevBuf q_[6];  // qa, qa_inv, qb, qb_inv, qc, qc_inv
+  DevBuf pd_, t1_, t2_;
+};
+
+// User callback (the literal ApplyFn slot across the C-ABI).
+class CallbackOp final : public Op {
+ public:
+  using Fn = int (*)(void*, const void*, void*, void*);
+  CallbackOp(int dtype, size_t m, Fn fn, void* ctx) : Op(dtype, m), fn_(fn), ctx_(ctx) {}
+  void apply(const void* x, void* out, cudaStream_t st) override;
+
+ private:
+  Fn fn_;
+  void* ctx_;
+};
+
+// Stage operator I - tau a K of a problem (stage_operator, operators.cpp:77-79).
+StencilSpec stage_spec(const Problem& p, double tau, double a);
+// The problem's own K (sigma 0) for f evaluations.
+StencilSpec rhs_spec(const Problem& p);
+
+// build_heat_precond(_f32) / build_advection_precond(_f32) (precond.cpp:14-42),
+// dtype selects the arithmetic (F32/F64 heat, C32/C64 advection).
+std::unique_ptr<Op> make_stage_fastdiag(int dtype, const Problem& p, double tau, double a, Numerics num);
+// FastDiag from caller-provided factors (the public FastDiagPreconditioner ctor).
+std::unique_ptr<Op> make_fastdiag(int dtype, int n, const void* qa, const void* qa_inv, const void* qb,
+                                  const void* qb_inv, const void* qc, const void* qc_inv, const void* la,
+                                  const void* lb, const void* lc, Numerics num);
+
+// Block-Jacobi and CSR extensions (ops_ext.cpp).
+std::unique_ptr<Op> make_block_jacobi(int dtype, const Problem& p, double tau, double a, int block, int storage);
+std::unique_ptr<Op> make_csr(int dtype, int rows, const int* row_ptr, const int* cols, const void* values,
+                             int storage);
+std::unique_ptr<Op> make_csr_stencil(int dtype, const StencilSpec& s, int storage);
+
+}  // namespace mprkb

@@ -1,0 +1,108 @@
+// Deterministic reductions for the Krylov dots/norms (krylov.hpp:43-71).
+//
+// FAST numerics: every kernel that produces a vector can also fold a dot
+// product into its epilogue.  Each CTA reduces its fp64 partial with warp
+// shuffles, writes it to `partial[cta]`, and the last CTA to finish (atomic
+// ticket) sums all partials in a FIXED order and writes the scalar straight to
+// host-mapped pinned memory.  One launch, no second pass over HBM, bitwise
+// reproducible run to run.  fp32 products are formed exactly in fp64
+// (24+24 < 53 bits), so the result is far more accurate than the reference's
+// sequential fp32 sum (SURVEY.md §0 finding 2).
+//
+// PARITY numerics: `seq_dot` reproduces the reference's single-accumulator
+// left-to-right sum in the working precision bit for bit.
+#pragma once
+
+#include "device.cuh"
+
+namespace mprkb {
+
+template <int NV>
+__device__ __forceinline__ void warp_sum(double (&v)[NV]) {
+#pragma unroll
+  for (int c = 0; c < NV; ++c)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[c] += __shfl_xor_sync(0xffffffffu, v[c], o);
+}
+
+// Block-wide sum; result valid in thread 0.  All threads of the block must call.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV]) {
+  __shared__ double sh[32][NV];
+  const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+  const int nth = blockDim.x * blockDim.y * blockDim.z;
+  warp_sum<NV>(v);
+  const int lane = tid & 31, wid = tid >> 5;
+  __syncthreads();
+  if (lane == 0)
+#pragma unroll
+    for (int c = 0; c < NV; ++c) sh[wid][c] = v[c];
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = (nth + 31) >> 5;
+#pragma unroll
+    for (int c = 0; c < NV; ++c) v[c] = lane < nw ? sh[lane][c] : 0.0;
+    warp_sum<NV>(v);
+  }
+}
+
+// Finish a grid-wide reduction: every thread passes its private partial.
+template <int NV>
+__device__ __forceinline__ void grid_reduce(double (&v)[NV], const RedSlot& s) {
+  __shared__ bool last;
+  const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
+  const int nth = blockDim.x * blockDim.y * blockDim.z;
+  const unsigned bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
+  block_sum<NV>(v);
+  if (tid == 0) {
+#pragma unroll
+    for (int c = 0; c < NV; ++c) s.partial[(size_t)bid * NV + c] = v[c];
+    __threadfence();
+    const unsigned t = atomicAdd(s.ticket, 1u);
+    last = (t == nb - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double w[NV];
+#pragma unroll
+  for (int c = 0; c < NV; ++c) w[c] = 0.0;
+  for (unsigned b = tid; b < nb; b += nth)
+#pragma unroll
+    for (int c = 0; c < NV; ++c) w[c] += __ldcg(s.partial + (size_t)b * NV + c);
+  block_sum<NV>(w);
+  if (tid == 0) {
+#pragma unroll
+    for (int c = 0; c < NV; ++c) s.out[c] = w[c];
+    *s.ticket = 0u;
+    __threadfence_system();
+  }
+}
+
+// ---- per-element dot contributions in fp64 --------------------------------------
+__device__ __forceinline__ void dot_acc(double (&v)[1], float a, float b) {
+  v[0] = __fma_rn((double)a, (double)b, v[0]);
+}
+__device__ __forceinline__ void dot_acc(double (&v)[1], double a, double b) {
+  v[0] = __fma_rn(a, b, v[0]);
+}
+// dot_real for complex: re*re + im*im
+__device__ __forceinline__ void dot_acc(double (&v)[1], c32 a, c32 b) {
+  v[0] = __fma_rn((double)a.re, (double)b.re, v[0]);
+  v[0] = __fma_rn((double)a.im, (double)b.im, v[0]);
+}
+__device__ __forceinline__ void dot_acc(double (&v)[1], c64 a, c64 b) {
+  v[0] = __fma_rn(a.re, b.re, v[0]);
+  v[0] = __fma_rn(a.im, b.im, v[0]);
+}
+// conjugated complex dot: conj(a) * b
+template <class R>
+__device__ __forceinline__ void cdot_acc(double (&v)[2], cplx<R> a, cplx<R> b) {
+  v[0] = __fma_rn((double)a.re, (double)b.re, v[0]);
+  v[0] = __fma_rn((double)a.im, (double)b.im, v[0]);
+  v[1] = __fma_rn((double)a.re, (double)b.im, v[1]);
+  v[1] = __fma_rn(-(double)a.im, (double)b.re, v[1]);
+}
+
+}  // namespace mprkb

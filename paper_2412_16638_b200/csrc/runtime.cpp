@@ -1,0 +1,105 @@
+#include "runtime.hpp"
+
+#include <atomic>
+#include <cstring>
+#include <string>
+
+namespace mprkb {
+
+namespace {
+std::atomic<long long> g_launches{0};
+bool g_debug_sync = false;
+}  // namespace
+
+long long kernel_launches() { return g_launches.load(std::memory_order_relaxed); }
+
+void cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
+  const int code = (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) ? 21 : 20;
+  throw Error(code, std::string("CUDA error ") + cudaGetErrorString(e) + " in " + what + " (" + file + ":" +
+                        std::to_string(line) + ")");
+}
+
+void after_launch(const char* name) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  const cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Error(20, std::string("kernel launch failed (") + name + "): " + cudaGetErrorString(e));
+  }
+  if (g_debug_sync) {
+    const cudaError_t s = cudaDeviceSynchronize();
+    if (s != cudaSuccess) throw Error(20, std::string("kernel failed (") + name + "): " + cudaGetErrorString(s));
+  }
+}
+
+void set_debug_sync(bool on) { g_debug_sync = on; }
+
+int sm_count() {
+  static int cached = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess)
+      return v;
+    cudaGetLastError();
+    return 148;
+  }();
+  return cached;
+}
+
+void require_device() {
+  int n = 0;
+  const cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    throw Error(21, "no CUDA device available: the B200 path has no CPU fallback");
+  }
+}
+
+void DevBuf::alloc(size_t bytes) {
+  release();
+  if (bytes == 0) return;
+  CUDA_CHECK(cudaMalloc(&p_, bytes));
+  bytes_ = bytes;
+}
+
+void DevBuf::release() {
+  if (p_) cudaFree(p_);
+  p_ = nullptr;
+  bytes_ = 0;
+}
+
+Reducer::Reducer(int slots) : slots_(slots) {
+  partial_.alloc(sizeof(double) * 2 * kMaxPartials * slots);
+  ticket_.alloc(sizeof(unsigned) * slots);
+  CUDA_CHECK(cudaMemset(ticket_.get(), 0, sizeof(unsigned) * slots));
+  CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&host_), sizeof(double) * 2 * slots, cudaHostAllocMapped));
+  std::memset(host_, 0, sizeof(double) * 2 * slots);
+}
+
+Reducer::~Reducer() {
+  if (host_) cudaFreeHost(host_);
+}
+
+RedSlot Reducer::slot(int i) const {
+  RedSlot s;
+  s.partial = partial_.as<double>() + (size_t)2 * kMaxPartials * i;
+  s.ticket = ticket_.as<unsigned>() + i;
+  double* dptr = nullptr;
+  CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dptr), host_ + 2 * i, 0));
+  s.out = dptr;
+  return s;
+}
+
+Flags::Flags(int count) : count_(count) {
+  CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&host_), sizeof(int) * count, cudaHostAllocMapped));
+  clear();
+}
+
+Flags::~Flags() {
+  if (host_) cudaFreeHost(host_);
+}
+
+void Flags::clear() { std::memset(host_, 0, sizeof(int) * count_); }
+
+void stream_sync(cudaStream_t st) { CUDA_CHECK(cudaStreamSynchronize(st)); }
+
+}  // namespace mprkb

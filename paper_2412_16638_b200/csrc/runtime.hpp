@@ -1,0 +1,79 @@
+// Host-side RAII for device memory, the reduction workspace and error flags.
+#pragma once
+
+#include <utility>
+#include <vector>
+
+#include "types.hpp"
+
+namespace mprkb {
+
+void require_device();  // throws Error(21) when no CUDA device is present
+
+// Owning device allocation (cudaMalloc: 256-byte aligned).
+class DevBuf {
+ public:
+  DevBuf() = default;
+  explicit DevBuf(size_t bytes) { alloc(bytes); }
+  ~DevBuf() { release(); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p_(std::exchange(o.p_, nullptr)), bytes_(std::exchange(o.bytes_, 0)) {}
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p_ = std::exchange(o.p_, nullptr);
+      bytes_ = std::exchange(o.bytes_, 0);
+    }
+    return *this;
+  }
+  void alloc(size_t bytes);
+  void release();
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p_);
+  }
+  void* get() const { return p_; }
+  size_t bytes() const { return bytes_; }
+
+ private:
+  void* p_ = nullptr;
+  size_t bytes_ = 0;
+};
+
+// Grid-reduction targets: per slot a partial buffer + ticket on the device and
+// a host-mapped pinned result (read after a stream synchronize).
+class Reducer {
+ public:
+  explicit Reducer(int slots = 4);
+  ~Reducer();
+  Reducer(const Reducer&) = delete;
+  Reducer& operator=(const Reducer&) = delete;
+  RedSlot slot(int i) const;
+  const double* host(int i) const { return host_ + 2 * i; }
+
+ private:
+  int slots_;
+  DevBuf partial_, ticket_;
+  double* host_ = nullptr;
+};
+
+// Device error flags (non-finite / overflow) with host-mapped mirror.
+class Flags {
+ public:
+  explicit Flags(int count = 64);
+  ~Flags();
+  Flags(const Flags&) = delete;
+  Flags& operator=(const Flags&) = delete;
+  int* dev(int i) const { return host_ + i; }  // host-mapped, device-writable
+  int value(int i) const { return ((volatile int*)host_)[i]; }
+  void clear();
+
+ private:
+  int count_;
+  int* host_ = nullptr;
+};
+
+void stream_sync(cudaStream_t st);
+
+}  // namespace mprkb

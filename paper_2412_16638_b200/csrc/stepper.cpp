@@ -1,0 +1,295 @@
+#include "stepper.hpp"
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+
+namespace mprkb {
+
+namespace {
+
+struct Bracket {
+  EventTimer* t;
+  int id = -1;
+  cudaStream_t st;
+  Bracket(EventTimer& timer, const char* label, cudaStream_t s) : t(&timer), st(s) {
+    if (t->enabled()) id = t->begin(label, st);
+  }
+  ~Bracket() {
+    if (id >= 0) t->end(id, st);
+  }
+};
+
+void add_term(CombineTerms& t, double coef, const void* ptr, int is_f32) {
+  if (t.count >= kMaxTerms) MPRKB_THROW(1, "stepper: too many stage couplings");
+  t.coef[t.count] = coef;
+  t.ptr[t.count] = ptr;
+  t.is_f32[t.count] = is_f32;
+  ++t.count;
+}
+
+}  // namespace
+
+static const StepperConfig& device_checked(const StepperConfig& cfg) {
+  require_device();
+  return cfg;
+}
+
+Stepper::Stepper(const StepperConfig& cfg)
+    : cfg_(device_checked(cfg)), prob_(make_problem(cfg.eq, cfg.n, cfg.nu)), m_(prob_.size()), flags_(256),
+      timer_(cfg.timings) {
+  const Tableau& t = cfg_.tab;
+  const int q = t.q;
+  if (q <= 0 || q > 16) MPRKB_THROW(1, "stepper: stage count must be in [1, 16]");
+  CUDA_CHECK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  const bool heat = cfg_.eq == Equation::Heat;
+  solve_dtype_ = (heat ? 0 : 2) + (cfg_.f32 ? 0 : 1);
+  kspec_ = rhs_spec(prob_);
+
+  // need_f64 / need_feps masks (stepper.cpp:60-66)
+  need_f64_.assign(q, 0);
+  need_feps_.assign(q, 0);
+  for (int j = 0; j < q; ++j) {
+    if (t.b[j] != 0.0) need_f64_[j] = 1;
+    for (int i = j + 1; i < q; ++i) {
+      if (t.ah(i, j) != 0.0) need_f64_[j] = 1;
+      if (t.ae(i, j) != 0.0) need_feps_[j] = 1;
+    }
+  }
+  // one stage solver (operator + preconditioner) per distinct diagonal
+  // coefficient (stepper.cpp:68-94)
+  const Numerics num = cfg_.num;
+  solver_of_stage_.assign(q, -1);
+  for (int i = 0; i < q; ++i) {
+    const double a = t.ae(i, i);
+    if (a == 0.0) continue;
+    int idx = -1;
+    for (size_t s = 0; s < solvers_.size(); ++s)
+      if (solvers_[s].a == a) idx = (int)s;
+    if (idx < 0) {
+      StageSolver s;
+      s.a = a;
+      s.op = std::make_unique<StencilOp>(solve_dtype_, stage_spec(prob_, cfg_.tau, a));
+      if (cfg_.precond == 0)
+        s.pre = make_stage_fastdiag(solve_dtype_, prob_, cfg_.tau, a, num);
+      else if (cfg_.precond == 2)
+        s.pre = make_block_jacobi(solve_dtype_, prob_, cfg_.tau, a, cfg_.block,
+                                  cfg_.block_storage < 0 ? solve_dtype_ % 2 : cfg_.block_storage);
+      solvers_.push_back(std::move(s));
+      idx = (int)solvers_.size() - 1;
+    }
+    solver_of_stage_[i] = idx;
+  }
+
+  // device-resident vectors
+  const size_t m = m_;
+  if (!prob_.forcing.empty()) {
+    g64_.alloc(m * sizeof(double));
+    CUDA_CHECK(cudaMemcpy(g64_.get(), prob_.forcing.data(), m * sizeof(double), cudaMemcpyHostToDevice));
+    if (cfg_.f32) {
+      g32_.alloc(m * sizeof(float));
+      narrow_f64(m, g64_.as<double>(), g32_.as<float>(), flags_.dev(0), st_);
+    }
+  }
+  f_hi_.resize(q);
+  f_eps_.resize(q);
+  for (int i = 0; i < q; ++i) {
+    if (need_f64_[i]) f_hi_[i].alloc(m * sizeof(double));
+    if (need_feps_[i] && (cfg_.f32 || !need_f64_[i])) f_eps_[i].alloc(m * (cfg_.f32 ? sizeof(float) : sizeof(double)));
+  }
+  y_.alloc(m * sizeof(double));
+  if (!solvers_.empty()) {
+    const size_t s = dtype_size(solve_dtype_);
+    bsol_.alloc(m * s);
+    xsol_.alloc(m * s);
+    switch (solve_dtype_) {
+      case 0: w32_ = std::make_unique<KrylovWork<float>>(m); break;
+      case 1: w64_ = std::make_unique<KrylovWork<double>>(m); break;
+      case 2: wc32_ = std::make_unique<KrylovWork<c32>>(m); break;
+      default: wc64_ = std::make_unique<KrylovWork<c64>>(m); break;
+    }
+  }
+  stream_sync(st_);
+}
+
+Stepper::~Stepper() {
+  if (st_) cudaStreamDestroy(st_);
+}
+
+// Stepper::step (stepper.cpp:149-206).  Reference-order error semantics:
+// every check the reference performs (downcast overflow, non-finite stage)
+// raises a device flag in its own slot; the flags are inspected in program
+// order before u is touched, so the first failing check is the one thrown.
+void Stepper::step(double* u, StepTrace& trace) {
+  trace = StepTrace{};
+  flags_.clear();
+  struct Check {
+    int slot, code;
+    const char* msg;
+  };
+  std::vector<Check> checks;
+  int next = 1;
+  auto check_slot = [&](int code, const char* msg) {
+    if (next >= 255) MPRKB_THROW(1, "stepper: too many checks");
+    checks.push_back({next, code, msg});
+    return flags_.dev(next++);
+  };
+  int* sink = flags_.dev(0);
+  auto raise_flags = [&]() {
+    stream_sync(st_);
+    for (const Check& c : checks)
+      if (flags_.value(c.slot)) MPRKB_THROW(c.code, c.msg);
+  };
+
+  const Tableau& t = cfg_.tab;
+  const int q = t.q;
+  const double tau = cfg_.tau;
+  const size_t m = m_;
+  const Crit crit{cfg_.tol, cfg_.max_iter};
+  std::vector<const void*> fh(q, nullptr), fe(q, nullptr);
+  std::vector<int> fe32(q, 0);
+  const char* kOverflow = "downcast: value exceeds the binary32 range";
+  const char* kStage = "stage vector picked up a NaN or infinity";
+
+  for (int i = 0; i < q; ++i) {
+    CombineTerms terms;
+    for (int j = 0; j < i; ++j) {
+      if (t.ah(i, j) != 0.0) add_term(terms, tau * t.ah(i, j), fh[j], 0);
+      if (t.ae(i, j) != 0.0) add_term(terms, tau * t.ae(i, j), fe[j], fe32[j]);
+    }
+    const double a = t.ae(i, i);
+    if (a != 0.0) {
+      if (!prob_.forcing.empty()) add_term(terms, tau * a, g64_.get(), 0);
+      StageSolver& S = solvers_[solver_of_stage_[i]];
+      const int out_kind = solve_dtype_ == 0 ? 1 : solve_dtype_ == 1 ? 0 : solve_dtype_;
+      int* flag = (solve_dtype_ == 0 || solve_dtype_ == 2) ? check_slot(6, kOverflow) : sink;
+      {
+        Bracket br(timer_, "axpy", st_);
+        combine(m, u, terms, out_kind, bsol_.get(), flag, st_);
+      }
+      // x0 = narrowed rhs (stepper.cpp:111, 120, 135, 146)
+      CUDA_CHECK(cudaMemcpyAsync(xsol_.get(), bsol_.get(), m * dtype_size(solve_dtype_), cudaMemcpyDeviceToDevice, st_));
+      SolveReport rep;
+      EventTimer* tm = timer_.enabled() ? &timer_ : nullptr;
+      switch (solve_dtype_) {
+        case 0:
+          cg_solve<float>(*S.op, S.pre.get(), bsol_.as<float>(), xsol_.as<float>(), crit, cfg_.num, *w32_, rep, st_, tm);
+          break;
+        case 1:
+          cg_solve<double>(*S.op, S.pre.get(), bsol_.as<double>(), xsol_.as<double>(), crit, cfg_.num, *w64_, rep, st_, tm);
+          break;
+        case 2:
+          gmres_solve<c32>(*S.op, S.pre.get(), bsol_.as<c32>(), xsol_.as<c32>(), crit, cfg_.num, *wc32_, rep, st_, tm);
+          break;
+        default:
+          gmres_solve<c64>(*S.op, S.pre.get(), bsol_.as<c64>(), xsol_.as<c64>(), crit, cfg_.num, *wc64_, rep, st_, tm);
+          break;
+      }
+      extract_stage(m, solve_dtype_, xsol_.get(), y_.as<double>(), check_slot(9, kStage), st_);
+      if (!rep.converged) trace.solver_failure = true;
+      trace.solves.push_back(std::move(rep));
+    } else {
+      Bracket br(timer_, "axpy", st_);
+      combine(m, u, terms, 0, y_.get(), check_slot(9, kStage), st_);
+    }
+
+    const double* g = prob_.forcing.empty() ? nullptr : g64_.as<double>();
+    if (need_f64_[i]) {
+      Bracket br(timer_, "stencil", st_);
+      apply_f64(kspec_, y_.as<double>(), nullptr, g, f_hi_[i].as<double>(), st_);
+      fh[i] = f_hi_[i].get();
+    }
+    if (need_feps_[i]) {
+      if (cfg_.f32) {
+        Bracket br(timer_, "stencil", st_);
+        apply_f32(kspec_, y_.as<double>(), nullptr, g ? g32_.as<float>() : nullptr, f_eps_[i].as<float>(),
+                  check_slot(6, kOverflow), st_);
+        fe[i] = f_eps_[i].get();
+        fe32[i] = 1;
+      } else if (need_f64_[i]) {
+        fe[i] = fh[i];  // f_eps aliases f_hi (stepper.cpp:191-192)
+      } else {
+        Bracket br(timer_, "stencil", st_);
+        apply_f64(kspec_, y_.as<double>(), nullptr, g, f_eps_[i].as<double>(), st_);
+        fe[i] = f_eps_[i].get();
+      }
+    }
+  }
+  raise_flags();
+
+  CombineTerms fin;
+  for (int i = 0; i < q; ++i)
+    if (t.b[i] != 0.0) add_term(fin, tau * t.b[i], fh[i], 0);
+  {
+    Bracket br(timer_, "axpy", st_);
+    final_update(m, u, fin, check_slot(9, "updated state picked up a NaN or infinity"), st_);
+  }
+  raise_flags();
+  if (timer_.enabled()) timer_.resolve();
+}
+
+// integrate (stepper.cpp:218-269)
+IntegrationResult integrate(const StepperConfig& cfg, const std::vector<double>* reference) {
+  // make_problem runs before integrate in every reference caller
+  // (bindings.cpp:134), so a too-small grid is reported first.
+  if (cfg.n < (cfg.eq == Equation::Heat ? 2 : 3))
+    MPRKB_THROW(3, "make_problem: grid too small for the requested equation");
+  if (!(cfg.tau > 0.0)) MPRKB_THROW(1, "integrate: tau must be positive");
+  const double ratio = cfg.t_end / cfg.tau;
+  const long long steps = std::llround(ratio);
+  if (steps < 1 || std::abs(steps * cfg.tau - cfg.t_end) > 1e-9 * std::max(1.0, std::abs(cfg.t_end)))
+    MPRKB_THROW(1, "integrate: tau must divide t_end");
+
+  const auto wall_start = std::chrono::steady_clock::now();
+  Stepper stepper(cfg);
+  return integrate_with(stepper, reference, wall_start);
+}
+
+IntegrationResult integrate_with(Stepper& stepper, const std::vector<double>* reference,
+                                 std::chrono::steady_clock::time_point wall_start) {
+  const StepperConfig& cfg = stepper.config();
+  if (!(cfg.tau > 0.0)) MPRKB_THROW(1, "integrate: tau must be positive");
+  const long long steps = std::llround(cfg.t_end / cfg.tau);
+  if (steps < 1 || std::abs(steps * cfg.tau - cfg.t_end) > 1e-9 * std::max(1.0, std::abs(cfg.t_end)))
+    MPRKB_THROW(1, "integrate: tau must divide t_end");
+  IntegrationResult res;
+  res.steps = (int)steps;
+  const size_t m = stepper.size();
+  DevBuf u(m * sizeof(double));
+  CUDA_CHECK(cudaMemcpy(u.get(), stepper.problem().u0.data(), m * sizeof(double), cudaMemcpyHostToDevice));
+  for (long long s = 0; s < steps; ++s) {
+    StepTrace trace;
+    stepper.step(u.as<double>(), trace);
+    res.solver_failure = res.solver_failure || trace.solver_failure;
+    for (const SolveReport& rep : trace.solves) {
+      res.solve_iterations.push_back(rep.iterations);
+      res.total_iterations += rep.iterations;
+    }
+  }
+  res.state.resize(m);
+  CUDA_CHECK(cudaMemcpy(res.state.data(), u.get(), m * sizeof(double), cudaMemcpyDeviceToHost));
+  res.mean_iterations = res.solve_iterations.empty()
+                            ? 0.0
+                            : static_cast<double>(res.total_iterations) / static_cast<double>(res.solve_iterations.size());
+  const std::vector<double>* target = reference;
+  std::vector<double> exact;
+  if (target == nullptr && cfg.eq == Equation::Heat) {
+    exact = heat_exact(stepper.problem(), cfg.t_end);
+    target = &exact;
+  }
+  if (target != nullptr) {
+    if (target->size() != res.state.size()) MPRKB_THROW(2, "integrate: reference state has the wrong length");
+    double worst = 0.0, sq = 0.0;
+    for (size_t i = 0; i < res.state.size(); ++i) {
+      const double e = res.state[i] - (*target)[i];
+      worst = std::max(worst, std::abs(e));
+      sq += e * e;
+    }
+    res.error_max = worst;
+    res.error_l2 = std::sqrt(sq / static_cast<double>(res.state.size()));
+  }
+  res.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall_start).count();
+  return res;
+}
+
+}  // namespace mprkb

@@ -1,0 +1,89 @@
+// Split-tableau DIRK time stepper on device-resident state
+// (Stepper / integrate, stepper.hpp:53-99, stepper.cpp:53-269).
+#pragma once
+
+#include <chrono>
+#include <memory>
+#include <optional>
+#include <vector>
+
+#include "krylov.hpp"
+#include "problem.hpp"
+
+namespace mprkb {
+
+struct StepperConfig {
+  Equation eq = Equation::Heat;
+  int n = 0;
+  Tableau tab;
+  double tau = 0.0, t_end = 0.1, tol = 1e-6;
+  bool f32 = false;  // PrecisionPolicy::implicit == F32
+  int max_iter = 40;
+  Numerics num = Numerics::Fast;
+  int precond = 0;  // 0 FastDiag, 1 none, 2 block-Jacobi
+  int block = 8;
+  int block_storage = -1;
+  double nu = 0.0;
+  bool timings = false;
+};
+
+struct StepTrace {
+  std::vector<SolveReport> solves;
+  bool solver_failure = false;
+};
+
+class Stepper {
+ public:
+  explicit Stepper(const StepperConfig& cfg);
+  ~Stepper();
+  // one step on device state u (n^3 doubles), in place
+  void step(double* u_dev, StepTrace& trace);
+  const Problem& problem() const { return prob_; }
+  cudaStream_t stream() const { return st_; }
+  size_t size() const { return m_; }
+  EventTimer& timer() { return timer_; }
+  const StepperConfig& config() const { return cfg_; }
+
+ private:
+  struct StageSolver {
+    double a = 0.0;
+    std::unique_ptr<Op> op;
+    std::unique_ptr<Op> pre;
+  };
+  StepperConfig cfg_;
+  Problem prob_;
+  size_t m_;
+  cudaStream_t st_ = nullptr;
+  StencilSpec kspec_;
+  int solve_dtype_;
+  DevBuf g64_, g32_;
+  std::vector<StageSolver> solvers_;
+  std::vector<int> solver_of_stage_;
+  std::vector<char> need_f64_, need_feps_;
+  std::vector<DevBuf> f_hi_, f_eps_;
+  DevBuf y_, bsol_, xsol_;
+  std::unique_ptr<KrylovWork<float>> w32_;
+  std::unique_ptr<KrylovWork<double>> w64_;
+  std::unique_ptr<KrylovWork<c32>> wc32_;
+  std::unique_ptr<KrylovWork<c64>> wc64_;
+  Flags flags_;
+  EventTimer timer_;
+};
+
+struct IntegrationResult {
+  std::vector<double> state;
+  std::optional<double> error_max, error_l2;
+  double mean_iterations = 0.0;
+  long long total_iterations = 0;
+  std::vector<int> solve_iterations;
+  bool solver_failure = false;
+  double wall_seconds = 0.0;
+  int steps = 0;
+};
+
+IntegrationResult integrate(const StepperConfig& cfg, const std::vector<double>* reference);
+// integrate on an existing stepper (its timing registry then holds the run's labels)
+IntegrationResult integrate_with(Stepper& stepper, const std::vector<double>* reference,
+                                 std::chrono::steady_clock::time_point wall_start);
+
+}  // namespace mprkb

@@ -1,0 +1,91 @@
+// Plain C++ declarations shared by the nvcc-compiled kernels and the
+// g++-compiled host side (Krylov scalar logic, Stepper, C-ABI).  The host
+// side is deliberately built by g++ -O3 -std=gnu++20 like the reference, so
+// every host scalar expression (alpha, beta, Givens rotations, complex
+// divisions via libgcc) rounds identically to the reference's.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#if defined(__CUDACC__)
+#define MPRKB_HD __host__ __device__
+#else
+#define MPRKB_HD
+#endif
+
+namespace mprkb {
+
+// ---- errors (mirror proj/include/mprk/errors.hpp; codes = include/mprk_b200.h)
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+#define MPRKB_THROW(code, msg) throw ::mprkb::Error((code), (msg))
+
+[[noreturn]] void cuda_fail(cudaError_t e, const char* what, const char* file, int line);
+#define CUDA_CHECK(x)                                                        \
+  do {                                                                       \
+    cudaError_t e_ = (x);                                                    \
+    if (e_ != cudaSuccess) ::mprkb::cuda_fail(e_, #x, __FILE__, __LINE__);   \
+  } while (0)
+// After a launch: count it (mprkb_kernel_launches) and surface launch errors.
+void after_launch(const char* name);
+#define LAUNCHED(name) ::mprkb::after_launch(name)
+int sm_count();
+
+// ---- scalar types (precond.cpp:46-49 instantiations) --------------------------
+template <class R>
+struct alignas(2 * sizeof(R)) cplx {
+  R re, im;
+};
+using c32 = cplx<float>;
+using c64 = cplx<double>;
+
+template <class T> struct real_of { using type = T; };
+template <class R> struct real_of<cplx<R>> { using type = R; };
+template <class T> using real_t = typename real_of<T>::type;
+template <class T> constexpr bool is_cplx = false;
+template <class R> constexpr bool is_cplx<cplx<R>> = true;
+
+template <class T> struct dtype_of;
+template <> struct dtype_of<float> { static constexpr int v = 0; };
+template <> struct dtype_of<double> { static constexpr int v = 1; };
+template <> struct dtype_of<c32> { static constexpr int v = 2; };
+template <> struct dtype_of<c64> { static constexpr int v = 3; };
+
+inline size_t dtype_size(int dt) {
+  switch (dt) {
+    case 0: return 4;
+    case 1: return 8;
+    case 2: return 8;
+    case 3: return 16;
+    case 4: return 2;
+  }
+  MPRKB_THROW(10, "unknown dtype " + std::to_string(dt));
+}
+
+// Grid sizing: capped at a multiple of the SM count (148 on B200).
+inline unsigned grid_for(size_t work, unsigned block, unsigned per_sm = 8) {
+  size_t g = (work + block - 1) / block;
+  const size_t cap = (size_t)sm_count() * per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (unsigned)g;
+}
+
+enum class Numerics { Fast = 0, Parity = 1 };
+
+// One grid-wide reduction target (see reduce.cuh).
+struct RedSlot {
+  double* partial = nullptr;   // >= gridDim * NV doubles (device)
+  unsigned* ticket = nullptr;  // zero between uses (device)
+  double* out = nullptr;       // NV doubles, host-mapped pinned memory
+};
+constexpr int kMaxPartials = 1 << 16;
+
+}  // namespace mprkb

@@ -1,0 +1,167 @@
+"""GPU parity of the kernel-level boundary (the ApplyFn plug-in slot).
+
+Every kernel is compared with the UNMODIFIED reference (oracle/_ref) on the
+same seeded inputs:
+  * stencils — always bitwise (the kernel reproduces the reference's exact
+    operation sequence in every numerics mode);
+  * tensor contractions / FastDiag — bitwise with PARITY numerics, within
+    the stated fp tolerance with FAST (FMA) numerics;
+  * dots — bitwise with PARITY (sequential accumulation in the working
+    precision), fp64-accurate with FAST.
+Reference tests re-targeted: test_operators.cpp:41-131, test_precond.cpp:61-266.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+DT = {0: np.float32, 1: np.float64, 2: np.complex64, 3: np.complex128}
+# FAST-mode contraction tolerance relative to max|out| (FMA vs mul+add on
+# n-term dot products): a few ulps * sqrt(n)
+FAST_TOL = {0: 2e-5, 1: 1e-13, 2: 2e-5, 3: 1e-13}
+
+
+def rnd(rng, kind, m):
+    x = rng.uniform(-1, 1, m)
+    if kind >= 2:
+        x = x + 1j * rng.uniform(-1, 1, m)
+    return x.astype(DT[kind])
+
+
+def to_dev(torch, a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def same_bits(a, b):
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    return a.shape == b.shape and np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3])
+@pytest.mark.parametrize("stencil", [0, 1])
+@pytest.mark.parametrize("n", [2, 3, 5, 17, 40])
+def test_stencil_bitwise(gpu, mp, ref, kind, stencil, n):
+    import torch
+
+    if stencil == 1 and n < 3:
+        pytest.skip("periodic stencil needs n >= 3")
+    rng = np.random.default_rng(1000 + 7 * n + kind)
+    x = rnd(rng, kind, n ** 3)
+    for sigma, gamma in ((1.0, -0.37), (0.0, -1.0 / (1.0 / (n - 1)) ** 2), (1.0, 12.5)):
+        want = ref.stencil(kind, n, stencil, sigma, gamma, x)
+        got = mp.stencil_apply(to_dev(torch, x), n, stencil, sigma, gamma).cpu().numpy()
+        assert same_bits(got, want), (kind, stencil, n, sigma, np.abs(got - want).max())
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3])
+@pytest.mark.parametrize("side", [0, 1, 2])
+@pytest.mark.parametrize("n", [2, 3, 7, 33, 64, 130])
+def test_tensor_parity_and_fast(gpu, mp, ref, kind, side, n):
+    import torch
+
+    if n == 130 and kind == 3:
+        pytest.skip("reference cost")
+    rng = np.random.default_rng(2000 + 11 * n + 3 * side + kind)
+    q = rnd(rng, kind, n * n)
+    x = rnd(rng, kind, n ** 3)
+    want = ref.tensor(kind, side, n, q, x)
+    qd, xd = to_dev(torch, q), to_dev(torch, x)
+    got = mp.tensor_apply(side, n, qd, xd, "parity").cpu().numpy()
+    assert same_bits(got, want), (kind, side, n, np.abs(got - want).max())
+    fast = mp.tensor_apply(side, n, qd, xd, "fast").cpu().numpy()
+    scale = max(1.0, np.abs(want).max())
+    assert np.abs(fast - want).max() <= FAST_TOL[kind] * scale * np.sqrt(n)
+
+
+def test_tensor_permutation_known_answer(gpu, mp):
+    """n = 2 permutation picks out each side's stride (test_precond.cpp:99-109)."""
+    import torch
+
+    swap = torch.tensor([0.0, 1.0, 1.0, 0.0], dtype=torch.float64, device="cuda")
+    x = torch.arange(1, 9, dtype=torch.float64, device="cuda")
+    assert mp.tensor_apply(2, 2, swap, x, "parity").tolist() == [2, 1, 4, 3, 6, 5, 8, 7]
+    assert mp.tensor_apply(1, 2, swap, x, "parity").tolist() == [3, 4, 1, 2, 7, 8, 5, 6]
+    assert mp.tensor_apply(0, 2, swap, x, "parity").tolist() == [5, 6, 7, 8, 1, 2, 3, 4]
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3])
+@pytest.mark.parametrize("n", [3, 8, 32])
+def test_fastdiag_stage_bitwise(gpu, mp, ref, kind, n):
+    import torch
+
+    rng = np.random.default_rng(3000 + n + kind)
+    x = rnd(rng, kind, n ** 3)
+    eq = "heat" if kind <= 1 else "advection"
+    tau = 0.01 if kind <= 1 else 1.0 / 640.0
+    for a in (0.5, 1.957161067302390):
+        want = ref.fastdiag(kind, n, tau, a, x)
+        P = mp.Operator.fastdiag_stage(kind, eq, n, tau, a, "parity")
+        got = P.apply(to_dev(torch, x)).cpu().numpy()
+        assert same_bits(got, want), (kind, n, a, np.abs(got - want).max())
+        F = mp.Operator.fastdiag_stage(kind, eq, n, tau, a, "fast")
+        fast = F.apply(to_dev(torch, x)).cpu().numpy()
+        assert np.abs(fast - want).max() <= 50 * FAST_TOL[kind] * max(1.0, np.abs(want).max())
+
+
+def test_fastdiag_is_exact_inverse_of_stage_operator(gpu, mp):
+    """P^-1 (I - tau a K) x == x (test_precond.cpp:165-198), fp64."""
+    import torch
+
+    n, tau, a = 12, 0.025, 0.5
+    h = 1.0 / (n - 1)
+    rng = np.random.default_rng(5)
+    x = torch.from_numpy(rng.uniform(-1, 1, n ** 3)).cuda()
+    Ax = mp.stencil_apply(x, n, 0, 1.0, -tau * a * (-1.0 / h ** 2))
+    P = mp.Operator.fastdiag_stage(1, "heat", n, tau, a)
+    back = P.apply(Ax)
+    assert torch.max(torch.abs(back - x)).item() < 1e-10
+
+
+def test_fastdiag_ctor_errors(gpu, mp):
+    """ZeroEigenvalueSum / DimensionTooSmall from the public ctor (test_precond.cpp:233-245, 290-304)."""
+    idm = np.eye(2).ravel()
+    with pytest.raises(mp.ZeroEigenvalueSum):
+        mp.Operator.fastdiag(1, 2, idm, idm, idm, idm, idm, idm, [1.0, 2.0], [-3.0, 5.0], [2.0, 7.0])
+    mp.Operator.fastdiag(1, 2, idm, idm, idm, idm, idm, idm, [1.0, 2.0], [1.0, 2.0], [1.0, 2.0])
+    with pytest.raises(mp.DimensionTooSmall):
+        mp.Operator.fastdiag(1, 1, [1.0], [1.0], [1.0], [1.0], [1.0], [1.0], [1.0], [1.0], [1.0])
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3])
+@pytest.mark.parametrize("m", [1, 1000, 32768, 100003])
+def test_dot_parity_sequential(gpu, mp, kind, m):
+    import torch
+
+    rng = np.random.default_rng(4000 + m + kind)
+    a = rnd(rng, kind, m)
+    b = rnd(rng, kind, m)
+    R = np.float32 if kind in (0, 2) else np.float64
+    # the reference's detail::dot_real (krylov.hpp:43-54): one accumulator in R
+    if kind <= 1:
+        terms = (a * b).astype(R)
+    else:
+        terms = (a.real * b.real).astype(R) + (a.imag * b.imag).astype(R)
+    acc = R(0)
+    for t in terms.tolist():
+        acc = R(acc + R(t))
+    got = mp.dot(to_dev(torch, a), to_dev(torch, b), numerics="parity")
+    assert got == float(acc)
+    fast = mp.dot(to_dev(torch, a), to_dev(torch, b), numerics="fast")
+    exact = float(np.sum(terms.astype(np.float64)))
+    assert abs(fast - exact) <= 1e-12 * max(1.0, np.sum(np.abs(terms.astype(np.float64))))
+
+
+def test_dot_conjugated(gpu, mp):
+    import torch
+
+    rng = np.random.default_rng(9)
+    a = rnd(rng, 3, 5000)
+    b = rnd(rng, 3, 5000)
+    acc = 0j
+    for x, y in zip(a.tolist(), b.tolist()):
+        acc = acc + x.conjugate() * y
+    got = mp.dot(to_dev(torch, a), to_dev(torch, b), conjugate=True, numerics="parity")
+    assert got == acc
+    fast = mp.dot(to_dev(torch, a), to_dev(torch, b), conjugate=True, numerics="fast")
+    assert abs(fast - np.vdot(a, b)) < 1e-10
