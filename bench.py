@@ -1,0 +1,387 @@
+#!/usr/bin/env python3
+"""Headline benchmark: mixed-precision DIRK time steps on a 3D heat grid.
+
+Metric (BASELINE.json): RK time-steps/s & DOF-updates/s for the 3D heat
+mixed DIRK at 256^3 (configs[1]).  `value` = DOF-updates/s of the whole job
+(n^3 x steps / s, summed over ranks); `steps_per_s` rides along.
+
+Workload (one "step" = one Stepper::step, stepper.cpp:149-206):
+  heat 256^3, midpoint1 = the 2-stage mixed DIRK (fp32 implicit stage solved
+  by CG + the reference's FastDiag preconditioner, fp64 explicit corrector),
+  tau = 0.01, tol = 1e-3 (the fp32 attainable floor at 256^3 is 1.8e-4
+  relative, SURVEY.md §0 finding 4), max_iter 40, state resident in HBM.
+
+Arms
+  default           this repo's CUDA path (libmprk_b200.so, FAST numerics)
+  --impl reference  the reference's own CPU implementation (oracle/_ref, the
+                    unmodified reference sources, OpenMP on all host cores),
+                    same workload, bounded sample of steps.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+Multi-GPU: launched under torch.distributed.run, one rank per GPU; every rank
+steps its own 256^3 grid (replicas, weak scaling), timing = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "RK time-steps/s & DOF-updates/s, 3D heat 256³–512³ mixed DIRK; SpMV HBM GB/s"
+N_GRID = 256
+METHOD = "midpoint1"
+TAU = 0.01
+TOL = 1e-3
+PREC = "f32"
+MAX_ITER = 40
+
+
+def workload_config(n_gpus: int) -> dict:
+    return {
+        "workload": f"heat {N_GRID}^3, {METHOD} (2-stage mixed DIRK: fp32 implicit CG + FastDiag, "
+                    f"fp64 explicit corrector), tau={TAU}, tol={TOL}",
+        "n": N_GRID, "dof": N_GRID ** 3, "method": METHOD, "implicit_precision": PREC,
+        "preconditioner": "fastdiag", "tau": TAU, "tol": TOL, "max_iter": MAX_ITER,
+        "state": "resident in HBM (f64)",
+        "l2": "no flush: one step streams ~3.5 GB through HBM (state alone 134 MB > 126 MB L2)",
+        "parallelism": "single" if n_gpus == 1 else f"replicas x{n_gpus}",
+    }
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------------------------
+# clocks sampling during the timed region
+# ---------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (FileNotFoundError, OSError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------
+# CPU reference (oracle/_ref: the reference sources compiled unmodified)
+# ---------------------------------------------------------------------------------
+def reference_steps(n: int, steps_wanted: int, budget_s: float, threads: int):
+    """Time the reference's own Stepper::step on this host; returns
+    (seconds per step list, threads, sample description)."""
+    from oracle.oracle import Reference, ensure_built, have_reference
+
+    ensure_built(ref=True)
+    if not have_reference():
+        return None
+    R = Reference()
+    R.set_threads(threads)
+    tab = R.tableau(METHOD)
+    st = R.stepper(0, n, tab, TAU, TOL, PREC, MAX_ITER)
+    u, *_ = R.make_problem(0, n)
+    times = []
+    t_start = time.perf_counter()
+    while len(times) < steps_wanted:
+        t0 = time.perf_counter()
+        st.step(u)
+        times.append(time.perf_counter() - t0)
+        if time.perf_counter() - t_start + times[-1] > budget_s:
+            break
+    return times
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    # warm-up: at most one step (the CPU needs none for steady state; it only
+    # faults in the 2 GB working set), then a bounded sample of timed steps
+    budget = float(os.environ.get("MPRKB_REF_BUDGET_S", "150"))
+    t0 = time.perf_counter()
+    warm = reference_steps(N_GRID, min(args.warmup, 1), budget / 3, threads) if args.warmup else []
+    if warm is None:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmprk_ref.so not built"}))
+        return 0
+    times = reference_steps(N_GRID, args.steps, budget, threads)
+    per_step = sum(times) / len(times)
+    value = N_GRID ** 3 / per_step
+    sample = (f"{len(times)} of {args.steps} requested steps of the same workload "
+              f"(+{len(warm)} warm-up), wall clock, {threads} OpenMP threads")
+    line = {
+        "metric": METRIC, "value": value, "unit": "DOF-updates/s", "n_gpus": args.gpus, "steps": len(times),
+        "warmup": len(warm), "ms_per_step": per_step * 1e3, "steps_per_s": 1.0 / per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
+        "config": workload_config(1), "impl": "reference",
+        "cpu_baseline": {"value": value, "unit": "DOF-updates/s", "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "DOF-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "wall_s": time.perf_counter() - t0,
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------------------------
+# the CUDA arm
+# ---------------------------------------------------------------------------------
+def load_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    capture (profiles/ncu_summary_r01.json), if present."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("dominant_kernel_dram_bytes_per_launch")
+    except (OSError, ValueError):
+        return None
+
+
+def measure_contraction(mp, torch, stream_ptr, reps=20):
+    """Average duration of one FastDiag tensor-contraction launch (the
+    dominant kernel), timed with CUDA events on the launching stream."""
+    n = N_GRID
+    P = mp.Operator.fastdiag_stage(0, "heat", n, TAU, 0.5, "fast")
+    x = torch.randn(n ** 3, dtype=torch.float32, device="cuda")
+    s = torch.cuda.ExternalStream(stream_ptr) if stream_ptr else torch.cuda.current_stream()
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            P.apply(x)
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        for _ in range(reps):
+            P.apply(x)
+        b.record(s)
+        b.synchronize()
+    ms_apply = a.elapsed_time(b) / reps
+    return ms_apply / 6.0  # six contraction launches per apply (diag fused)
+
+
+def run_cuda_arm(args):
+    import torch
+
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    else:
+        torch.cuda.set_device(0)
+    import paper_2412_16638_b200 as mp
+
+    n = N_GRID
+    m = n ** 3
+    tab = mp.midpoint_corrected(1)
+    st = mp.Stepper("heat", n, tab, TAU, TOL, PREC, MAX_ITER)
+    stream = torch.cuda.ExternalStream(st.stream)
+    u = torch.from_numpy(st.initial_state()).cuda()
+    torch.cuda.synchronize()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+            torch.cuda.synchronize()
+
+    iters = []
+    for _ in range(args.warmup):
+        tr = st.step_device(u)
+    barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = mp.kernel_launches()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        tr = st.step_device(u)
+        iters.append(tr["iterations"])
+    ev1.record(stream)
+    ev1.synchronize()
+    barrier()
+    launches = mp.kernel_launches() - launches0
+    clk = clocks.stop()
+    ms_total = ev0.elapsed_time(ev1)
+    t_local = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(t_local, op=torch.distributed.ReduceOp.MAX)
+    ms_total = t_local.item()
+    ms_step = ms_total / args.steps
+    value = world * m * args.steps / (ms_total * 1e-3)
+
+    # ---- e2e: the public C-ABI call with a HOST (pinned) state buffer, H2D +
+    # D2H inside the timed region every step
+    u_host = torch.from_numpy(st.initial_state()).pin_memory()
+    u_np = u_host.numpy()
+    for _ in range(max(1, min(args.warmup, 2))):
+        st.step(u_np)
+    barrier()
+    t0 = time.perf_counter()
+    e2e_steps = max(1, min(args.steps, 10))
+    for _ in range(e2e_steps):
+        st.step(u_np)
+    t_e2e = time.perf_counter() - t0
+    te = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+    e2e_value = world * m * e2e_steps / te.item()
+
+    line = None
+    if rank == 0:
+        # ---- roofline of the dominant kernel: the FastDiag contraction
+        # (CUDA-core FP32 FMA bound; 2 n^4 flop per launch = n^3 outputs x n MACs)
+        ms_launch = measure_contraction(mp, torch, st.stream)
+        flops = 2.0 * n ** 4
+        achieved = flops / (ms_launch * 1e-3) / 1e12
+        peak = mp_fma_peak(mp, 0)
+        # ---- HBM-bound companion: the fp64 stencil (K1), 2*8*N bytes per launch
+        ms_sten = measure_stencil(mp, torch, st.stream)
+        gbs = 16.0 * m / (ms_sten * 1e-3) / 1e9
+        peaks = load_peaks()
+        line = {
+            "metric": METRIC, "value": value, "unit": "DOF-updates/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "steps_per_s": 1e3 / ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
+            "data": "synthetic (make_problem: u0 = 0, g = sin sin sin)", "config": workload_config(world),
+            "iterations_per_solve": sorted(set(i for it in iters for i in it)),
+            "gpu_launches": launches,
+            "e2e": {"value": e2e_value, "unit": "DOF-updates/s", "h2d_bytes_per_step": 8 * m,
+                    "d2h_bytes_per_step": 8 * m, "steps": e2e_steps,
+                    "note": "Stepper.step(host pinned f64 state) through the C-ABI, wall clock"},
+            "roofline": {"kernel": "k_tensor (FastDiag contraction, fp32 FFMA)", "bound": "compute",
+                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "peak_source": "measured FP32 FMA peak (mprkb_measure_fma_peak, this run)",
+                         "flop_per_launch": flops, "ms_per_launch": ms_launch, "traffic": load_traffic()},
+            "roofline_hbm": {"kernel": "k_stencil (fp64 7-point)", "bound": "hbm", "achieved": gbs,
+                             "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"],
+                             "peak_source": peaks["src"], "bytes_per_launch": 16.0 * m, "ms_per_launch": ms_sten},
+            "clocks": clk,
+        }
+        if not args.no_cpu_baseline and world == 1:
+            budget = float(os.environ.get("MPRKB_CPU_BASELINE_S", "30"))
+            threads = os.cpu_count() or 1
+            times = reference_steps(N_GRID, 1, budget, threads)
+            if times:
+                per = sum(times) / len(times)
+                line["cpu_baseline"] = {"value": N_GRID ** 3 / per, "unit": "DOF-updates/s", "cores": threads,
+                                        "kind": "reference",
+                                        "sample": f"{len(times)} step(s) of the same workload, {threads} threads"}
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    if line is not None:
+        print(json.dumps(line))
+    return 0
+
+
+def mp_fma_peak(mp, dtype):
+    import ctypes as C
+
+    v = C.c_double()
+    mp.check(mp._c.lib.mprkb_measure_fma_peak(dtype, C.byref(v)))
+    return v.value
+
+
+def measure_stencil(mp, torch, stream_ptr, reps=20):
+    n = N_GRID
+    x = torch.randn(n ** 3, dtype=torch.float64, device="cuda")
+    A = mp.Operator.stencil(1, n, 0, 1.0, -1.0)
+    s = torch.cuda.ExternalStream(stream_ptr)
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            A.apply(x)
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(s)
+        for _ in range(reps):
+            A.apply(x)
+        b.record(s)
+        b.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "src": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
+    except (OSError, ValueError, KeyError):
+        return {"hbm_gbs": 6650.0, "src": "B200_PROFILING.md fallback"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_cuda_arm(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

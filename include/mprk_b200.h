@@ -73,6 +73,9 @@ int mprkb_stream_synchronize(void* stream);
 int mprkb_device_synchronize(void);
 /* Number of kernels this library has launched since load (instrumentation). */
 long long mprkb_kernel_launches(void);
+/* Measured CUDA-core FMA throughput (TFLOP/s) for F32 or F64: the roofline
+ * denominator of the FastDiag contractions (instrumentation). */
+int mprkb_measure_fma_peak(int dtype, double* tflops);
 
 /* ---- problem setup (operators.cpp:29-79), host ------------------------------ */
 /* make_problem(eq, n): u0 (n^3), forcing (n^3; heat only, may be NULL),

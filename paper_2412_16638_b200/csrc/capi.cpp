@@ -507,3 +507,15 @@ int mprkb_stepper_integrate(mprkb_stepper* s, const double* reference_host, size
 }
 
 }  // extern "C"
+
+namespace mprkb {
+double fma_peak_tflops(int dtype);
+}
+
+extern "C" int mprkb_measure_fma_peak(int dtype, double* tflops) {
+  return guarded([&] {
+    require_device();
+    if (dtype != MPRKB_F32 && dtype != MPRKB_F64) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "dtype must be F32 or F64");
+    *tflops = mprkb::fma_peak_tflops(dtype);
+  });
+}

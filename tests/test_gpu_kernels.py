@@ -147,9 +147,12 @@ def test_dot_parity_sequential(gpu, mp, kind, m):
         acc = R(acc + R(t))
     got = mp.dot(to_dev(torch, a), to_dev(torch, b), numerics="parity")
     assert got == float(acc)
+    # FAST: products formed exactly in fp64 (24+24 < 53 bits), fp64 tree sum
     fast = mp.dot(to_dev(torch, a), to_dev(torch, b), numerics="fast")
-    exact = float(np.sum(terms.astype(np.float64)))
-    assert abs(fast - exact) <= 1e-12 * max(1.0, np.sum(np.abs(terms.astype(np.float64))))
+    a64, b64 = a.astype(np.complex128 if kind >= 2 else np.float64), b.astype(np.complex128 if kind >= 2 else np.float64)
+    prods = (a64 * b64).real if kind <= 1 else a64.real * b64.real + a64.imag * b64.imag
+    exact = float(np.sum(prods))
+    assert abs(fast - exact) <= 1e-12 * max(1.0, float(np.sum(np.abs(prods))))
 
 
 def test_dot_conjugated(gpu, mp):
