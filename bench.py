@@ -6,10 +6,14 @@ mixed DIRK at 256^3 (configs[1]).  `value` = DOF-updates/s of the whole job
 (n^3 x steps / s, summed over ranks); `steps_per_s` rides along.
 
 Workload (one "step" = one Stepper::step, stepper.cpp:149-206):
-  heat 256^3, midpoint1 = the 2-stage mixed DIRK (fp32 implicit stage solved
-  by CG + the reference's FastDiag preconditioner, fp64 explicit corrector),
-  tau = 0.01, tol = 1e-3 (the fp32 attainable floor at 256^3 is 1.8e-4
-  relative, SURVEY.md §0 finding 4), max_iter 40, state resident in HBM.
+  heat 256^3, 4s3pB = Grant's 4-stage 3rd-order mixed DIRK (four fp32
+  implicit stage solves by CG + the reference's FastDiag preconditioner,
+  fp64 explicit couplings, fp64 state), tau = 0.01, tol = 1e-3 (the fp32
+  attainable floor at 256^3 is 1.8e-4 relative, SURVEY.md §0 finding 4),
+  max_iter 40, state resident in HBM.  (midpoint1, the 2-stage member, is
+  not usable for long fp32 runs at this size: its explicit corrector
+  amplifies fp32 stage rounding by ~(tau |K|)^2/2 = 3e7 per step and the run
+  diverges after ~20 steps — the paper's divergence caveat.)
 
 Arms
   default           this repo's CUDA path (libmprk_b200.so, FAST numerics)
@@ -39,7 +43,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "RK time-steps/s & DOF-updates/s, 3D heat 256³–512³ mixed DIRK; SpMV HBM GB/s"
 N_GRID = 256
-METHOD = "midpoint1"
+METHOD = "4s3pB"
 TAU = 0.01
 TOL = 1e-3
 PREC = "f32"
@@ -48,8 +52,8 @@ MAX_ITER = 40
 
 def workload_config(n_gpus: int) -> dict:
     return {
-        "workload": f"heat {N_GRID}^3, {METHOD} (2-stage mixed DIRK: fp32 implicit CG + FastDiag, "
-                    f"fp64 explicit corrector), tau={TAU}, tol={TOL}",
+        "workload": f"heat {N_GRID}^3, {METHOD} (4-stage mixed DIRK: fp32 implicit CG + FastDiag, "
+                    f"fp64 explicit couplings/state), tau={TAU}, tol={TOL}",
         "n": N_GRID, "dof": N_GRID ** 3, "method": METHOD, "implicit_precision": PREC,
         "preconditioner": "fastdiag", "tau": TAU, "tol": TOL, "max_iter": MAX_ITER,
         "state": "resident in HBM (f64)",
@@ -231,7 +235,7 @@ def run_cuda_arm(args):
 
     n = N_GRID
     m = n ** 3
-    tab = mp.midpoint_corrected(1)
+    tab = mp.builtin(METHOD)
     st = mp.Stepper("heat", n, tab, TAU, TOL, PREC, MAX_ITER)
     stream = torch.cuda.ExternalStream(st.stream)
     u = torch.from_numpy(st.initial_state()).cuda()

@@ -1,0 +1,549 @@
+// HBM-bound vector kernels: Krylov reductions and updates (krylov.hpp), the
+// RK stage combination / final update (stepper.cpp), precision casts.
+//
+// Every kernel streams its operands exactly once with 16/32-byte vector
+// accesses (4 elements per thread-iteration, 2x unrolled), one full wave of
+// 148 x 8 CTAs; per-element arithmetic is the reference's (no contraction),
+// so results are bitwise the reference's except where a FAST reduction is
+// folded in (fp64-accumulated, deterministic, see reduce.cuh).
+#include "launch.hpp"
+#include "reduce.cuh"
+#include "vec.cuh"
+
+namespace mprkb {
+
+namespace {
+
+constexpr unsigned kBlock = 256;
+
+inline unsigned wave(size_t m) { return grid_for((m + 3) / 4, kBlock, 8); }
+
+// Iterate [0, m): f4(base) on aligned 4-element chunks, f1(i) on the tail.
+template <class F4, class F1>
+__device__ __forceinline__ void for_each4(size_t m, F4&& f4, F1&& f1) {
+  const size_t nv = m / 4;
+  const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t v = tid;
+  for (; v + stride < nv; v += 2 * stride) {
+    f4(4 * v);
+    f4(4 * (v + stride));
+  }
+  if (v < nv) f4(4 * v);
+  for (size_t i = 4 * nv + tid; i < m; i += stride) f1(i);
+}
+
+}  // namespace
+
+// ============================================================================
+// reductions (detail::dot_real / dot, krylov.hpp:43-71)
+// ============================================================================
+template <class T>
+__global__ void __launch_bounds__(kBlock) k_dot_fast(size_t m, const T* a, const T* b, RedSlot red) {
+  double v[1] = {0.0};
+  for_each4(
+      m,
+      [&](size_t i) {
+        const V4<T> x = ld4(a + i), y = ld4(b + i);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) dot_acc(v, x.x[e], y.x[e]);
+      },
+      [&](size_t i) { dot_acc(v, ldg(a + i), ldg(b + i)); });
+  grid_reduce<1>(v, red);
+}
+
+template <class T>
+__global__ void __launch_bounds__(kBlock) k_cdot_fast(size_t m, const T* a, const T* b, RedSlot red) {
+  double v[2] = {0.0, 0.0};
+  for_each4(
+      m,
+      [&](size_t i) {
+        const V4<T> x = ld4(a + i), y = ld4(b + i);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) cdot_acc(v, x.x[e], y.x[e]);
+      },
+      [&](size_t i) { cdot_acc(v, ldg(a + i), ldg(b + i)); });
+  grid_reduce<2>(v, red);
+}
+
+// PARITY: the reference's single left-to-right accumulator in real_t<T>.
+// 256 threads stage coalesced chunks of the exactly rounded per-element
+// terms in shared memory; thread 0 adds them in index order.
+constexpr int SEQ_CHUNK = 2048;
+
+__device__ __forceinline__ float term_real(float a, float b) { return xmul(a, b); }
+__device__ __forceinline__ double term_real(double a, double b) { return xmul(a, b); }
+template <class R>
+__device__ __forceinline__ R term_real(cplx<R> a, cplx<R> b) {
+  return xadd(xmul(a.re, b.re), xmul(a.im, b.im));
+}
+
+template <class T>
+__global__ void __launch_bounds__(256) k_dot_seq(size_t m, const T* a, const T* b, double* out) {
+  using R = real_t<T>;
+  __shared__ R buf[SEQ_CHUNK];
+  R acc = R(0);
+  for (size_t base = 0; base < m; base += SEQ_CHUNK) {
+    const int cnt = (int)min((size_t)SEQ_CHUNK, m - base);
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x) buf[t] = term_real(ldg(a + base + t), ldg(b + base + t));
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int t = 0; t < cnt; ++t) acc = xadd(acc, buf[t]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = (double)acc;
+    __threadfence_system();
+  }
+}
+
+// acc += conj(a_i) * b_i, complex accumulator
+template <class R>
+__global__ void __launch_bounds__(256) k_cdot_seq(size_t m, const cplx<R>* a, const cplx<R>* b, double* out) {
+  constexpr int CH = SEQ_CHUNK / 2;
+  __shared__ cplx<R> buf[CH];
+  cplx<R> acc{R(0), R(0)};
+  for (size_t base = 0; base < m; base += CH) {
+    const int cnt = (int)min((size_t)CH, m - base);
+    for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
+      const cplx<R> x = ldg(a + base + t), y = ldg(b + base + t);
+      buf[t] = xmul(cplx<R>{x.re, -x.im}, y);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int t = 0; t < cnt; ++t) acc = xadd(acc, buf[t]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = (double)acc.re;
+    out[1] = (double)acc.im;
+    __threadfence_system();
+  }
+}
+
+template <class T>
+void dot_real(size_t m, const T* a, const T* b, const RedSlot& red, Numerics num, cudaStream_t st) {
+  if (num == Numerics::Parity)
+    k_dot_seq<T><<<1, 256, 0, st>>>(m, a, b, red.out);
+  else
+    k_dot_fast<T><<<wave(m), kBlock, 0, st>>>(m, a, b, red);
+  LAUNCHED("dot");
+}
+
+template <class T>
+void dot_conj(size_t m, const T* a, const T* b, const RedSlot& red, Numerics num, cudaStream_t st) {
+  if constexpr (is_cplx<T>) {
+    if (num == Numerics::Parity)
+      k_cdot_seq<real_t<T>><<<1, 256, 0, st>>>(m, a, b, red.out);
+    else
+      k_cdot_fast<T><<<wave(m), kBlock, 0, st>>>(m, a, b, red);
+    LAUNCHED("dot");
+  } else {
+    dot_real<T>(m, a, b, red, num, st);
+  }
+}
+
+// ============================================================================
+// vector updates
+// ============================================================================
+// r = b - q   (krylov.hpp:111, 141, 165, 193, 285, 308)
+template <class T, bool RED>
+__global__ void __launch_bounds__(kBlock) k_vsub(size_t m, const T* b, const T* q, T* r, RedSlot red) {
+  double v[1] = {0.0};
+  for_each4(
+      m,
+      [&](size_t i) {
+        const V4<T> x = ld4rw(b + i), y = ld4rw(q + i);
+        V4<T> o;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          o.x[e] = xsub(x.x[e], y.x[e]);
+          if (RED) dot_acc(v, o.x[e], o.x[e]);
+        }
+        st4(r + i, o);
+      },
+      [&](size_t i) {
+        const T o = xsub(b[i], q[i]);
+        r[i] = o;
+        if (RED) dot_acc(v, o, o);
+      });
+  if (RED) grid_reduce<1>(v, red);
+}
+
+template <class T>
+void vsub(size_t m, const T* b, const T* q, T* r, const RedSlot* red, cudaStream_t st) {
+  if (red)
+    k_vsub<T, true><<<wave(m), kBlock, 0, st>>>(m, b, q, r, *red);
+  else
+    k_vsub<T, false><<<wave(m), kBlock, 0, st>>>(m, b, q, r, RedSlot{});
+  LAUNCHED("vsub");
+}
+
+// x += alpha p; r -= alpha q  (+ r.r)   (krylov.hpp:134-137)
+template <class T, bool RED>
+__global__ void __launch_bounds__(kBlock) k_cg_update(size_t m, real_t<T> alpha, T* x, const T* p, T* r,
+                                                      const T* q, RedSlot red) {
+  double v[1] = {0.0};
+  for_each4(
+      m,
+      [&](size_t i) {
+        V4<T> xv = ld4rw(x + i), rv = ld4rw(r + i);
+        const V4<T> pv = ld4(p + i), qv = ld4(q + i);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          xv.x[e] = xadd(xv.x[e], xscale(alpha, pv.x[e]));
+          rv.x[e] = xsub(rv.x[e], xscale(alpha, qv.x[e]));
+          if (RED) dot_acc(v, rv.x[e], rv.x[e]);
+        }
+        st4(x + i, xv);
+        st4(r + i, rv);
+      },
+      [&](size_t i) {
+        x[i] = xadd(x[i], xscale(alpha, ldg(p + i)));
+        const T rv = xsub(r[i], xscale(alpha, ldg(q + i)));
+        r[i] = rv;
+        if (RED) dot_acc(v, rv, rv);
+      });
+  if (RED) grid_reduce<1>(v, red);
+}
+
+template <class T>
+void cg_update(size_t m, real_t<T> alpha, T* x, const T* p, T* r, const T* q, const RedSlot* red,
+               cudaStream_t st) {
+  if (red)
+    k_cg_update<T, true><<<wave(m), kBlock, 0, st>>>(m, alpha, x, p, r, q, *red);
+  else
+    k_cg_update<T, false><<<wave(m), kBlock, 0, st>>>(m, alpha, x, p, r, q, RedSlot{});
+  LAUNCHED("cg_update");
+}
+
+// p = z + beta p   (krylov.hpp:158)
+template <class T>
+__global__ void __launch_bounds__(kBlock) k_xpby(size_t m, const T* z, real_t<T> beta, T* p) {
+  for_each4(
+      m,
+      [&](size_t i) {
+        const V4<T> zv = ld4(z + i);
+        V4<T> pv = ld4rw(p + i);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) pv.x[e] = xadd(zv.x[e], xscale(beta, pv.x[e]));
+        st4(p + i, pv);
+      },
+      [&](size_t i) { p[i] = xadd(ldg(z + i), xscale(beta, p[i])); });
+}
+
+template <class T>
+void xpby(size_t m, const T* z, real_t<T> beta, T* p, cudaStream_t st) {
+  k_xpby<T><<<wave(m), kBlock, 0, st>>>(m, z, beta, p);
+  LAUNCHED("xpby");
+}
+
+// v = w; v *= s   (krylov.hpp:229-231, 298-300)
+template <class T>
+__global__ void __launch_bounds__(kBlock) k_vscale(size_t m, const T* w, T s, T* v) {
+  for_each4(
+      m,
+      [&](size_t i) {
+        V4<T> a = ld4rw(w + i);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) a.x[e] = xmul(a.x[e], s);
+        st4(v + i, a);
+      },
+      [&](size_t i) { v[i] = xmul(w[i], s); });
+}
+
+template <class T>
+void vscale(size_t m, const T* w, T s, T* v, cudaStream_t st) {
+  k_vscale<T><<<wave(m), kBlock, 0, st>>>(m, w, s, v);
+  LAUNCHED("vscale");
+}
+
+// w -= h v   (krylov.hpp:241)
+template <class T>
+__global__ void __launch_bounds__(kBlock) k_vaxmy(size_t m, T h, const T* v, T* w) {
+  for_each4(
+      m,
+      [&](size_t i) {
+        V4<T> a = ld4rw(w + i);
+        const V4<T> b = ld4(v + i);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) a.x[e] = xsub(a.x[e], xmul(h, b.x[e]));
+        st4(w + i, a);
+      },
+      [&](size_t i) { w[i] = xsub(w[i], xmul(h, ldg(v + i))); });
+}
+
+template <class T>
+void vaxmy(size_t m, T h, const T* v, T* w, cudaStream_t st) {
+  k_vaxmy<T><<<wave(m), kBlock, 0, st>>>(m, h, v, w);
+  LAUNCHED("vaxmy");
+}
+
+constexpr int kMaxBasis = 128;
+template <class T>
+struct BasisArgs {
+  const T* v[kMaxBasis];
+  T y[kMaxBasis];
+};
+
+// xc = x; xc += y_j v_j for j in order   (krylov.hpp:223-226)
+template <class T>
+__global__ void __launch_bounds__(kBlock) k_candidate(size_t m, const T* x, int cols, const BasisArgs<T>* args,
+                                                      T* xc) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < m; i += (size_t)gridDim.x * blockDim.x) {
+    T acc = ldg(x + i);
+    for (int j = 0; j < cols; ++j) acc = xadd(acc, xmul(args->y[j], ldg(args->v[j] + i)));
+    xc[i] = acc;
+  }
+}
+
+template <class T>
+void candidate(size_t m, const T* x, const T* const* basis, const T* y, int cols, T* xc, cudaStream_t st) {
+  static thread_local BasisArgs<T>* d_args = nullptr;
+  static thread_local BasisArgs<T>* h_args = nullptr;
+  if (cols > kMaxBasis) MPRKB_THROW(1, "gmres: basis larger than 128 vectors is not supported");
+  if (!d_args) {
+    CUDA_CHECK(cudaMalloc(&d_args, sizeof(BasisArgs<T>)));
+    CUDA_CHECK(cudaMallocHost(&h_args, sizeof(BasisArgs<T>)));
+  }
+  CUDA_CHECK(cudaStreamSynchronize(st));  // the previous use of the staging block has finished
+  for (int j = 0; j < cols; ++j) {
+    h_args->v[j] = basis[j];
+    h_args->y[j] = y[j];
+  }
+  CUDA_CHECK(cudaMemcpyAsync(d_args, h_args, sizeof(BasisArgs<T>), cudaMemcpyHostToDevice, st));
+  k_candidate<T><<<grid_for(m, kBlock, 8), kBlock, 0, st>>>(m, x, cols, d_args, xc);
+  LAUNCHED("candidate");
+}
+
+// ============================================================================
+// stage kernels (stepper.cpp)
+// ============================================================================
+__device__ __forceinline__ bool f32_overflows(double x) {
+  return !isnan(x) && fabs(x) >= 3.402823669209384634633746074317e+38;
+}
+
+__device__ __forceinline__ V4<double> term4(const CombineTerms& t, int c, size_t i) {
+  if (t.is_f32[c]) {
+    const V4<float> f = ld4(static_cast<const float*>(t.ptr[c]) + i);
+    return {{(double)f.x[0], (double)f.x[1], (double)f.x[2], (double)f.x[3]}};
+  }
+  return ld4(static_cast<const double*>(t.ptr[c]) + i);
+}
+__device__ __forceinline__ double term1(const CombineTerms& t, int c, size_t i) {
+  return t.is_f32[c] ? (double)ldg(static_cast<const float*>(t.ptr[c]) + i) : ldg(static_cast<const double*>(t.ptr[c]) + i);
+}
+
+// rhs = u; rhs += (tau a_ij) f_j ...; rhs += (tau a_ii) g   (stepper.cpp:157-172)
+// out_kind 0 double (+finite flag), 1 float (overflow flag), 2 c32, 3 c64
+template <int KIND>
+__global__ void __launch_bounds__(kBlock) k_combine(size_t m, const double* u, CombineTerms t, void* out,
+                                                    int* flag) {
+  bool bad = false;
+  auto emit = [&](size_t i, double r) {
+    if (KIND == 0) {
+      static_cast<double*>(out)[i] = r;
+      bad |= !isfinite(r);
+    } else if (KIND == 1) {
+      bad |= f32_overflows(r);
+      static_cast<float*>(out)[i] = __double2float_rn(r);
+    } else if (KIND == 2) {
+      bad |= f32_overflows(r);
+      static_cast<c32*>(out)[i] = c32{__double2float_rn(r), 0.0f};
+    } else {
+      static_cast<c64*>(out)[i] = c64{r, 0.0};
+    }
+  };
+  for_each4(
+      m,
+      [&](size_t i) {
+        V4<double> r = ld4(u + i);
+        for (int c = 0; c < t.count; ++c) {
+          const V4<double> v = term4(t, c, i);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) r.x[e] = xadd(r.x[e], xmul(t.coef[c], v.x[e]));
+        }
+        if (KIND == 0) {
+          st4(static_cast<double*>(out) + i, r);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) bad |= !isfinite(r.x[e]);
+        } else if (KIND == 1) {
+          V4<float> f;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            bad |= f32_overflows(r.x[e]);
+            f.x[e] = __double2float_rn(r.x[e]);
+          }
+          st4(static_cast<float*>(out) + i, f);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) emit(i + e, r.x[e]);
+        }
+      },
+      [&](size_t i) {
+        double r = ldg(u + i);
+        for (int c = 0; c < t.count; ++c) r = xadd(r, xmul(t.coef[c], term1(t, c, i)));
+        emit(i, r);
+      });
+  if (bad) *flag = 1;
+}
+
+void combine(size_t m, const double* u, const CombineTerms& t, int out_kind, void* out, int* flag,
+             cudaStream_t st) {
+  switch (out_kind) {
+    case 0: k_combine<0><<<wave(m), kBlock, 0, st>>>(m, u, t, out, flag); break;
+    case 1: k_combine<1><<<wave(m), kBlock, 0, st>>>(m, u, t, out, flag); break;
+    case 2: k_combine<2><<<wave(m), kBlock, 0, st>>>(m, u, t, out, flag); break;
+    default: k_combine<3><<<wave(m), kBlock, 0, st>>>(m, u, t, out, flag); break;
+  }
+  LAUNCHED("combine");
+}
+
+// y = upcast(x32) / x64 / real_part(xc) + check_finite  (stepper.cpp:18-33, 121, 146, 181)
+template <int SRC>
+__global__ void __launch_bounds__(kBlock) k_extract(size_t m, const void* x, double* y, int* flag) {
+  bool bad = false;
+  auto get = [&](size_t i) -> double {
+    if (SRC == 0) return (double)ldg(static_cast<const float*>(x) + i);
+    if (SRC == 1) return ldg(static_cast<const double*>(x) + i);
+    if (SRC == 2) return (double)ldg(static_cast<const c32*>(x) + i).re;
+    return ldg(static_cast<const c64*>(x) + i).re;
+  };
+  for_each4(
+      m,
+      [&](size_t i) {
+        V4<double> o;
+        if (SRC == 0) {
+          const V4<float> f = ld4(static_cast<const float*>(x) + i);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) o.x[e] = (double)f.x[e];
+        } else if (SRC == 1) {
+          o = ld4(static_cast<const double*>(x) + i);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) o.x[e] = get(i + e);
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) bad |= !isfinite(o.x[e]);
+        st4(y + i, o);
+      },
+      [&](size_t i) {
+        const double v = get(i);
+        y[i] = v;
+        bad |= !isfinite(v);
+      });
+  if (bad) *flag = 1;
+}
+
+void extract_stage(size_t m, int src_kind, const void* x, double* y, int* flag, cudaStream_t st) {
+  switch (src_kind) {
+    case 0: k_extract<0><<<wave(m), kBlock, 0, st>>>(m, x, y, flag); break;
+    case 1: k_extract<1><<<wave(m), kBlock, 0, st>>>(m, x, y, flag); break;
+    case 2: k_extract<2><<<wave(m), kBlock, 0, st>>>(m, x, y, flag); break;
+    default: k_extract<3><<<wave(m), kBlock, 0, st>>>(m, x, y, flag); break;
+  }
+  LAUNCHED("extract");
+}
+
+// u += (tau b_i) f_i ...; check_finite(u)   (stepper.cpp:200-205)
+__global__ void __launch_bounds__(kBlock) k_final(size_t m, double* u, CombineTerms t, int* flag) {
+  bool bad = false;
+  for_each4(
+      m,
+      [&](size_t i) {
+        V4<double> r = ld4rw(u + i);
+        for (int c = 0; c < t.count; ++c) {
+          const V4<double> v = term4(t, c, i);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) r.x[e] = xadd(r.x[e], xmul(t.coef[c], v.x[e]));
+        }
+        st4(u + i, r);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) bad |= !isfinite(r.x[e]);
+      },
+      [&](size_t i) {
+        double r = u[i];
+        for (int c = 0; c < t.count; ++c) r = xadd(r, xmul(t.coef[c], term1(t, c, i)));
+        u[i] = r;
+        bad |= !isfinite(r);
+      });
+  if (bad) *flag = 1;
+}
+
+void final_update(size_t m, double* u, const CombineTerms& t, int* flag, cudaStream_t st) {
+  k_final<<<wave(m), kBlock, 0, st>>>(m, u, t, flag);
+  LAUNCHED("final_update");
+}
+
+__global__ void __launch_bounds__(kBlock) k_narrow(size_t m, const double* x, float* y, int* flag) {
+  bool bad = false;
+  for_each4(
+      m,
+      [&](size_t i) {
+        const V4<double> v = ld4(x + i);
+        V4<float> f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          bad |= f32_overflows(v.x[e]);
+          f.x[e] = __double2float_rn(v.x[e]);
+        }
+        st4(y + i, f);
+      },
+      [&](size_t i) {
+        const double v = ldg(x + i);
+        bad |= f32_overflows(v);
+        y[i] = __double2float_rn(v);
+      });
+  if (bad) *flag = 1;
+}
+
+void narrow_f64(size_t m, const double* x, float* y, int* flag, cudaStream_t st) {
+  k_narrow<<<wave(m), kBlock, 0, st>>>(m, x, y, flag);
+  LAUNCHED("narrow");
+}
+
+// pd_inv[i+jn+kn^2] = 1/(la_i + lb_j + lc_k) in T (precond.hpp:139-150)
+__device__ __forceinline__ float rcp_exact(float s) { return __fdiv_rn(1.0f, s); }
+__device__ __forceinline__ double rcp_exact(double s) { return __ddiv_rn(1.0, s); }
+
+template <class T>
+__global__ void k_pd_inv(int n, const T* la, const T* lb, const T* lc, T* pd, int* zero_flag) {
+  const long nn = n, m = nn * nn * nn;
+  for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < m; idx += (long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx % nn), j = (int)((idx / nn) % nn), k = (int)(idx / (nn * nn));
+    const T sum = xadd(xadd(la[i], lb[j]), lc[k]);
+    // smallest offending linear index = the reference's first throw (k, j, i loop order)
+    if (sum == T(0)) atomicMin(zero_flag, (int)(idx < 0x7ffffffeL ? idx : 0x7ffffffeL));
+    pd[idx] = rcp_exact(sum);
+  }
+}
+
+template <class T>
+void pd_inv_device(int n, const T* la, const T* lb, const T* lc, T* pd, int* zero_flag, cudaStream_t st) {
+  const size_t m = (size_t)n * n * n;
+  k_pd_inv<T><<<grid_for(m, 256), 256, 0, st>>>(n, la, lb, lc, pd, zero_flag);
+  LAUNCHED("pd_inv");
+}
+
+// ============================================================================
+#define INST_BLAS(T)                                                                                  \
+  template void dot_real<T>(size_t, const T*, const T*, const RedSlot&, Numerics, cudaStream_t);     \
+  template void dot_conj<T>(size_t, const T*, const T*, const RedSlot&, Numerics, cudaStream_t);     \
+  template void vsub<T>(size_t, const T*, const T*, T*, const RedSlot*, cudaStream_t);               \
+  template void vscale<T>(size_t, const T*, T, T*, cudaStream_t);                                    \
+  template void vaxmy<T>(size_t, T, const T*, T*, cudaStream_t);                                     \
+  template void candidate<T>(size_t, const T*, const T* const*, const T*, int, T*, cudaStream_t);
+
+INST_BLAS(float)
+INST_BLAS(double)
+INST_BLAS(c32)
+INST_BLAS(c64)
+
+template void cg_update<float>(size_t, float, float*, const float*, float*, const float*, const RedSlot*, cudaStream_t);
+template void cg_update<double>(size_t, double, double*, const double*, double*, const double*, const RedSlot*, cudaStream_t);
+template void xpby<float>(size_t, const float*, float, float*, cudaStream_t);
+template void xpby<double>(size_t, const double*, double, double*, cudaStream_t);
+template void pd_inv_device<float>(int, const float*, const float*, const float*, float*, int*, cudaStream_t);
+template void pd_inv_device<double>(int, const double*, const double*, const double*, double*, int*, cudaStream_t);
+
+}  // namespace mprkb

@@ -40,10 +40,11 @@ void apply_f32(const StencilSpec& k, const double* y, const float* y32, const fl
 
 // ---- tensor contractions (precond.hpp:69-122) --------------------------------------
 // side 0 L (stride n^2), 1 M (stride n), 2 R (stride 1).  pd: fused diag scale
-// of the output (precond.hpp:172) or null.
+// of the output (precond.hpp:172) or null.  fold: Q has the Dirichlet sine
+// symmetry Q[n-1-a][q] = (-1)^q Q[a][q] (FAST numerics may halve the flops).
 template <class T>
 void tensor_apply(int side, int n, const T* q, const T* x, T* out, const T* pd, Numerics num,
-                  cudaStream_t st);
+                  cudaStream_t st, bool fold = false);
 // pd_inv[i+jn+kn^2] = 1/(la_i + lb_j + lc_k) in T (precond.hpp:139-150); real
 // types only (IEEE division is correctly rounded on both sides).  *zero_flag
 // (initialised to INT_MAX by the caller) receives the smallest linear index

@@ -1,6 +1,8 @@
 #include "ops.hpp"
 
+#include <algorithm>
 #include <climits>
+#include <cmath>
 #include <complex>
 #include <cstring>
 
@@ -57,6 +59,23 @@ FastDiagOp<T>::FastDiagOp(int n, const T* qa, const T* qa_inv, const T* qb, cons
   const size_t nn = (size_t)n * n, m = nn * n;
   const T* src[6] = {qa, qa_inv, qb, qb_inv, qc, qc_inv};
   for (int i = 0; i < 6; ++i) upload(q_[i], src[i], nn * sizeof(T));
+  if constexpr (!is_cplx<T>) {
+    // FAST numerics may use the Dirichlet sine symmetry
+    // Q[n-1-a][q] = (-1)^q Q[a][q] (spectral.cpp:17-20) to halve the flops;
+    // enabled per factor only when the supplied matrix has it.
+    if (num == Numerics::Fast)
+      for (int f = 0; f < 6; ++f) {
+        const T* Q = src[f];
+        double scale = 0.0, worst = 0.0;
+        for (size_t i = 0; i < nn; ++i) scale = std::max(scale, std::abs((double)Q[i]));
+        for (int a = 0; a < n && worst <= 1e-6 * scale; ++a)
+          for (int q = 0; q < n; ++q) {
+            const double want = (q % 2 ? -1.0 : 1.0) * (double)Q[(size_t)a * n + q];
+            worst = std::max(worst, std::abs((double)Q[(size_t)(n - 1 - a) * n + q] - want));
+          }
+        fold_[f] = scale > 0.0 && worst <= 1e-6 * scale;
+      }
+  }
   pd_.alloc(m * sizeof(T));
   t1_.alloc(m * sizeof(T));
   t2_.alloc(m * sizeof(T));
@@ -109,12 +128,12 @@ void FastDiagOp<T>::apply(const void* xv, void* outv, cudaStream_t st) {
   T* out = static_cast<T*>(outv);
   T* t1 = t1_.as<T>();
   T* t2 = t2_.as<T>();
-  tensor_apply<T>(2, n_, q_[1].as<T>(), x, t1, nullptr, num_, st);
-  tensor_apply<T>(1, n_, q_[3].as<T>(), t1, t2, nullptr, num_, st);
-  tensor_apply<T>(0, n_, q_[5].as<T>(), t2, t1, pd_.as<T>(), num_, st);
-  tensor_apply<T>(2, n_, q_[0].as<T>(), t1, t2, nullptr, num_, st);
-  tensor_apply<T>(1, n_, q_[2].as<T>(), t2, t1, nullptr, num_, st);
-  tensor_apply<T>(0, n_, q_[4].as<T>(), t1, out, nullptr, num_, st);
+  tensor_apply<T>(2, n_, q_[1].as<T>(), x, t1, nullptr, num_, st, fold_[1]);
+  tensor_apply<T>(1, n_, q_[3].as<T>(), t1, t2, nullptr, num_, st, fold_[3]);
+  tensor_apply<T>(0, n_, q_[5].as<T>(), t2, t1, pd_.as<T>(), num_, st, fold_[5]);
+  tensor_apply<T>(2, n_, q_[0].as<T>(), t1, t2, nullptr, num_, st, fold_[0]);
+  tensor_apply<T>(1, n_, q_[2].as<T>(), t2, t1, nullptr, num_, st, fold_[2]);
+  tensor_apply<T>(0, n_, q_[4].as<T>(), t1, out, nullptr, num_, st, fold_[4]);
 }
 
 template class FastDiagOp<float>;

@@ -53,6 +53,7 @@ class FastDiagOp final : public Op {
  private:
   int n_;
   Numerics num_;
+  bool fold_[6] = {false, false, false, false, false, false};  // sine symmetry per factor
   DevBuf q_[6];  // qa, qa_inv, qb, qb_inv, qc, qc_inv
   DevBuf pd_, t1_, t2_;
 };

@@ -1,0 +1,393 @@
+// 7-point stencil family (KronSumOperator::apply<T>, operators.hpp:113-161)
+// and its fused epilogues (residual, dot, apply_f with forcing and casts).
+//
+// HBM layout: x-fastest n^3 vector.  Two kernels:
+//  * k_stencil4 (real T, n % 4 == 0): a warp covers 128 consecutive i (4 per
+//    lane, 16/32-byte vector loads); i+-1 come from warp shuffles, j+-1 from
+//    the neighbouring rows (L1/L2), k+-1 from registers while the CTA marches
+//    over SKC planes with a two-plane-deep prefetch.  Each vector is read
+//    from HBM ~once and written once.
+//  * k_stencil (any T, any n): one element per thread, same marching.
+// Ghost values outside a Dirichlet domain are +0 and are always subtracted:
+// x - (+0) == x exactly (including -0), so the branch-free form is
+// bit-identical to the reference's conditional subtractions.
+#include "launch.hpp"
+#include "reduce.cuh"
+#include "vec.cuh"
+
+namespace mprkb {
+
+namespace {
+
+__device__ __forceinline__ bool f32_overflows(double x) {
+  return !isnan(x) && fabs(x) >= 3.402823669209384634633746074317e+38;
+}
+
+// ---- loaders ------------------------------------------------------------------
+template <class T>
+struct LdPlain {
+  using type = T;
+  const T* p;
+  __device__ __forceinline__ T ld1(long i) const { return ldg(p + i); }
+  __device__ __forceinline__ V4<T> ld4(long i) const { return ::mprkb::ld4(p + i); }
+};
+// double vector read in binary32 (apply_f F32: downcast(u), operators.cpp:88);
+// flags |u| past the binary32 range (precision.hpp:100-104)
+struct LdD2F {
+  using type = float;
+  const double* p;
+  int* flag;
+  __device__ __forceinline__ float cvt(double x) const {
+    if (f32_overflows(x)) *flag = 1;
+    return __double2float_rn(x);
+  }
+  __device__ __forceinline__ float ld1(long i) const { return cvt(ldg(p + i)); }
+  __device__ __forceinline__ V4<float> ld4(long i) const {
+    const V4<double> d = ::mprkb::ld4(p + i);
+    return {{cvt(d.x[0]), cvt(d.x[1]), cvt(d.x[2]), cvt(d.x[3])}};
+  }
+};
+// float vector widened to double (exact)
+struct LdF2D {
+  using type = double;
+  const float* p;
+  __device__ __forceinline__ double ld1(long i) const { return (double)ldg(p + i); }
+  __device__ __forceinline__ V4<double> ld4(long i) const {
+    const V4<float> f = ::mprkb::ld4(p + i);
+    return {{(double)f.x[0], (double)f.x[1], (double)f.x[2], (double)f.x[3]}};
+  }
+};
+
+template <class T>
+__device__ __forceinline__ T shfl_up1(T v) {
+  return __shfl_up_sync(0xffffffffu, v, 1);
+}
+template <class T>
+__device__ __forceinline__ T shfl_down1(T v) {
+  return __shfl_down_sync(0xffffffffu, v, 1);
+}
+
+// The reference's arithmetic for one point (operators.hpp:133-140, 149-158);
+// xl/xr/ym/yp/zm/zp are the i-1, i+1, j-1, j+1, k-1, k+1 neighbours.
+template <class T>
+__device__ __forceinline__ T point(int stencil, real_t<T> s, real_t<T> g, real_t<T> g2, T x, T xl, T xr, T ym,
+                                   T yp, T zm, T zp) {
+  using R = real_t<T>;
+  if (stencil == 0) {
+    T acc = xscale((R)6.0, x);
+    acc = xsub(acc, xl);
+    acc = xsub(acc, xr);
+    acc = xsub(acc, ym);
+    acc = xsub(acc, yp);
+    acc = xsub(acc, zm);
+    acc = xsub(acc, zp);
+    return xadd(xscale(s, x), xscale(g, acc));
+  }
+  T acc = xsub(xr, xl);
+  acc = xadd(acc, xsub(yp, ym));
+  acc = xadd(acc, xsub(zp, zm));
+  T val = xadd(xscale(s, x), xscale(g, acc));
+  if (stencil == 2) {
+    // advection-diffusion extension (no reference counterpart):
+    // + gamma2 * (6x - sum of the six periodic neighbours)
+    T lap = xscale((R)6.0, x);
+    lap = xsub(lap, xl);
+    lap = xsub(lap, xr);
+    lap = xsub(lap, ym);
+    lap = xsub(lap, yp);
+    lap = xsub(lap, zm);
+    lap = xsub(lap, zp);
+    val = xadd(val, xscale(g2, lap));
+  }
+  return val;
+}
+
+// ---- epilogues (vector form: 4 consecutive points; scalar form: 1) ---------------
+template <class T>
+struct EpiStore {
+  T* out;
+  struct State {};
+  __device__ void init(State&) const {}
+  __device__ __forceinline__ void v4(State&, long i, const V4<T>& v, const V4<T>&) const { st4(out + i, v); }
+  __device__ __forceinline__ void s1(State&, long i, T v, T) const { out[i] = v; }
+  __device__ void finish(State&) const {}
+};
+
+template <class T, bool RED>
+struct EpiResidual {
+  const T* b;
+  T* r;
+  RedSlot red;
+  struct State {
+    double v[1];
+  };
+  __device__ void init(State& s) const { s.v[0] = 0.0; }
+  __device__ __forceinline__ void v4(State& s, long i, const V4<T>& v, const V4<T>&) const {
+    const V4<T> bv = ld4rw(b + i);
+    V4<T> o;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      o.x[e] = xsub(bv.x[e], v.x[e]);
+      if (RED) dot_acc(s.v, o.x[e], o.x[e]);
+    }
+    if (r) st4(r + i, o);
+  }
+  __device__ __forceinline__ void s1(State& s, long i, T v, T) const {
+    const T o = xsub(b[i], v);
+    if (r) r[i] = o;
+    if (RED) dot_acc(s.v, o, o);
+  }
+  __device__ void finish(State& s) const {
+    if (RED) grid_reduce<1>(s.v, red);
+  }
+};
+
+template <class T>
+struct EpiStoreDot {
+  T* out;
+  RedSlot red;
+  struct State {
+    double v[1];
+  };
+  __device__ void init(State& s) const { s.v[0] = 0.0; }
+  __device__ __forceinline__ void v4(State& s, long i, const V4<T>& v, const V4<T>& xc) const {
+    st4(out + i, v);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) dot_acc(s.v, xc.x[e], v.x[e]);
+  }
+  __device__ __forceinline__ void s1(State& s, long i, T v, T xc) const {
+    out[i] = v;
+    dot_acc(s.v, xc, v);
+  }
+  __device__ void finish(State& s) const { grid_reduce<1>(s.v, red); }
+};
+
+// apply_f F64: out = K y + g   (operators.cpp:83-86)
+struct EpiF64Forcing {
+  const double* g;
+  double* out;
+  struct State {};
+  __device__ void init(State&) const {}
+  __device__ __forceinline__ void v4(State&, long i, const V4<double>& v, const V4<double>&) const {
+    if (g) {
+      const V4<double> gv = ld4(g + i);
+      V4<double> o;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) o.x[e] = xadd(v.x[e], gv.x[e]);
+      st4(out + i, o);
+    } else {
+      st4(out + i, v);
+    }
+  }
+  __device__ __forceinline__ void s1(State&, long i, double v, double) const { out[i] = g ? xadd(v, ldg(g + i)) : v; }
+  __device__ void finish(State&) const {}
+};
+
+// apply_f F32: out32 = K f32(y) + f32(g)   (operators.cpp:88-95)
+struct EpiF32Forcing {
+  const float* g32;
+  float* out;
+  struct State {};
+  __device__ void init(State&) const {}
+  __device__ __forceinline__ void v4(State&, long i, const V4<float>& v, const V4<float>&) const {
+    if (g32) {
+      const V4<float> gv = ld4(g32 + i);
+      V4<float> o;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) o.x[e] = xadd(v.x[e], gv.x[e]);
+      st4(out + i, o);
+    } else {
+      st4(out + i, v);
+    }
+  }
+  __device__ __forceinline__ void s1(State&, long i, float v, float) const { out[i] = g32 ? xadd(v, ldg(g32 + i)) : v; }
+  __device__ void finish(State&) const {}
+};
+
+// ---- scalar kernel -----------------------------------------------------------------
+constexpr int SBX = 32, SBY = 8, SKC = 16;
+
+template <class Src, class Epi>
+__global__ void __launch_bounds__(SBX* SBY)
+    k_stencil(int n, int stencil, real_t<typename Src::type> s, real_t<typename Src::type> g,
+              real_t<typename Src::type> g2, Src src, Epi epi) {
+  using T = typename Src::type;
+  const int i = blockIdx.x * SBX + threadIdx.x;
+  const int j = blockIdx.y * SBY + threadIdx.y;
+  const int k0 = blockIdx.z * SKC;
+  const int k1 = min(n, k0 + SKC);
+  const long nn = n, n2 = nn * nn;
+  typename Epi::State st;
+  epi.init(st);
+  if (i < n && j < n) {
+    const bool periodic = stencil != 0;
+    const long col = i + (long)j * nn;
+    auto at = [&](int ii, int jj, int kk) -> T {
+      if (periodic) {
+        ii = ii < 0 ? ii + n : (ii >= n ? ii - n : ii);
+        jj = jj < 0 ? jj + n : (jj >= n ? jj - n : jj);
+        kk = kk < 0 ? kk + n : (kk >= n ? kk - n : kk);
+      } else if (ii < 0 || ii >= n || jj < 0 || jj >= n || kk < 0 || kk >= n) {
+        return zero_v<T>();
+      }
+      return src.ld1(ii + (long)jj * nn + (long)kk * n2);
+    };
+    T zm = at(i, j, k0 - 1), x = at(i, j, k0);
+    for (int k = k0; k < k1; ++k) {
+      const T zp = at(i, j, k + 1);
+      const T v = point<T>(stencil, s, g, g2, x, at(i - 1, j, k), at(i + 1, j, k), at(i, j - 1, k), at(i, j + 1, k),
+                           zm, zp);
+      epi.s1(st, col + k * n2, v, x);
+      zm = x;
+      x = zp;
+    }
+  }
+  epi.finish(st);
+}
+
+// ---- vectorised kernel (real T, n % 4 == 0) -----------------------------------------
+constexpr int VX = 32, VY = 4, VKC = 16;
+
+template <class Src, class Epi>
+__global__ void __launch_bounds__(VX* VY)
+    k_stencil4(int n, int stencil, typename Src::type s, typename Src::type g, typename Src::type g2, Src src,
+               Epi epi) {
+  using T = typename Src::type;
+  const int lane = threadIdx.x;
+  const int i0 = (blockIdx.x * VX + lane) * 4;
+  const int j = blockIdx.y * VY + threadIdx.y;
+  const int k0 = blockIdx.z * VKC;
+  const int k1 = min(n, k0 + VKC);
+  const long nn = n, n2 = nn * nn;
+  const bool periodic = stencil != 0;
+  const bool act = i0 < n;
+  typename Epi::State st;
+  epi.init(st);
+  if (j < n) {  // warp-uniform: every lane of the warp shares j
+    auto wrap = [&](int v) { return v < 0 ? v + n : (v >= n ? v - n : v); };
+    auto row = [&](int jj, int kk) -> V4<T> {
+      if (periodic) {
+        jj = wrap(jj);
+        kk = wrap(kk);
+      } else if (jj < 0 || jj >= n || kk < 0 || kk >= n) {
+        return zero4<T>();
+      }
+      if (!act) return zero4<T>();
+      return src.ld4(i0 + (long)jj * nn + (long)kk * n2);
+    };
+    // i-neighbours that cross the lane's 4-vector: lane 0 needs i0-1,
+    // lane 31 / the last active lane needs i0+4 (loaded, everything else shuffled)
+    auto edge = [&](int ii, int kk) -> T {
+      if (periodic) {
+        ii = wrap(ii);
+        kk = wrap(kk);
+      } else if (ii < 0 || ii >= n || kk < 0 || kk >= n) {
+        return zero_v<T>();
+      }
+      if (!act) return zero_v<T>();
+      return src.ld1(ii + (long)j * nn + (long)kk * n2);
+    };
+    const bool need_l = lane == 0;
+    const bool need_r = lane == VX - 1 || i0 + 4 >= n;
+    V4<T> zm = row(j, k0 - 1), x = row(j, k0), zp = row(j, k0 + 1);
+    V4<T> ym = row(j - 1, k0), yp = row(j + 1, k0);
+    T el = need_l ? edge(i0 - 1, k0) : zero_v<T>();
+    T er = need_r ? edge(i0 + 4, k0) : zero_v<T>();
+    for (int k = k0; k < k1; ++k) {
+      // prefetch: plane k+2 centre, plane k+1 side rows and edges
+      const V4<T> zq = row(j, k + 2);
+      const V4<T> ymn = row(j - 1, k + 1), ypn = row(j + 1, k + 1);
+      const T eln = need_l ? edge(i0 - 1, k + 1) : zero_v<T>();
+      const T ern = need_r ? edge(i0 + 4, k + 1) : zero_v<T>();
+      T left = shfl_up1(x.x[3]);
+      T right = shfl_down1(x.x[0]);
+      if (need_l) left = el;
+      if (need_r) right = er;
+      V4<T> v;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const T xl = e == 0 ? left : x.x[e - 1];
+        const T xr = e == 3 ? right : x.x[e + 1];
+        v.x[e] = point<T>(stencil, s, g, g2, x.x[e], xl, xr, ym.x[e], yp.x[e], zm.x[e], zp.x[e]);
+      }
+      if (act) epi.v4(st, i0 + (long)j * nn + (long)k * n2, v, x);
+      zm = x;
+      x = zp;
+      zp = zq;
+      ym = ymn;
+      yp = ypn;
+      el = eln;
+      er = ern;
+    }
+  }
+  epi.finish(st);
+}
+
+template <class Src, class Epi>
+void launch(const StencilSpec& sp, Src src, Epi epi, cudaStream_t st, const char* name) {
+  using T = typename Src::type;
+  using R = real_t<T>;
+  const int n = sp.n;
+  if constexpr (!is_cplx<T>) {
+    if (n % 4 == 0) {
+      const dim3 grid((n / 4 + VX - 1) / VX, (n + VY - 1) / VY, (n + VKC - 1) / VKC);
+      k_stencil4<Src, Epi><<<grid, dim3(VX, VY), 0, st>>>(n, sp.stencil, (R)sp.sigma, (R)sp.gamma, (R)sp.gamma2, src,
+                                                          epi);
+      LAUNCHED(name);
+      return;
+    }
+  }
+  const dim3 grid((n + SBX - 1) / SBX, (n + SBY - 1) / SBY, (n + SKC - 1) / SKC);
+  k_stencil<Src, Epi><<<grid, dim3(SBX, SBY), 0, st>>>(n, sp.stencil, (R)sp.sigma, (R)sp.gamma, (R)sp.gamma2, src,
+                                                       epi);
+  LAUNCHED(name);
+}
+
+}  // namespace
+
+template <class T>
+void stencil_apply(const StencilSpec& s, const T* x, T* out, cudaStream_t st) {
+  launch(s, LdPlain<T>{x}, EpiStore<T>{out}, st, "stencil");
+}
+
+template <class T>
+void stencil_residual(const StencilSpec& s, const T* x, const T* b, T* r, const RedSlot* red, cudaStream_t st) {
+  if (red)
+    launch(s, LdPlain<T>{x}, EpiResidual<T, true>{b, r, *red}, st, "stencil_residual");
+  else
+    launch(s, LdPlain<T>{x}, EpiResidual<T, false>{b, r, RedSlot{}}, st, "stencil_residual");
+}
+
+template <class T>
+void stencil_apply_dot(const StencilSpec& s, const T* p, T* q, const RedSlot& red, cudaStream_t st) {
+  launch(s, LdPlain<T>{p}, EpiStoreDot<T>{q, red}, st, "stencil_dot");
+}
+
+void apply_f64(const StencilSpec& k, const double* y, const float* y32, const double* g, double* out,
+               cudaStream_t st) {
+  if (y32)
+    launch(k, LdF2D{y32}, EpiF64Forcing{g, out}, st, "apply_f64");
+  else
+    launch(k, LdPlain<double>{y}, EpiF64Forcing{g, out}, st, "apply_f64");
+}
+
+void apply_f32(const StencilSpec& k, const double* y, const float* y32, const float* g32, float* out32, int* flag,
+               cudaStream_t st) {
+  if (y32)
+    launch(k, LdPlain<float>{y32}, EpiF32Forcing{g32, out32}, st, "apply_f32");
+  else
+    launch(k, LdD2F{y, flag}, EpiF32Forcing{g32, out32}, st, "apply_f32");
+}
+
+#define INST_STENCIL(T)                                                                          \
+  template void stencil_apply<T>(const StencilSpec&, const T*, T*, cudaStream_t);               \
+  template void stencil_residual<T>(const StencilSpec&, const T*, const T*, T*, const RedSlot*, \
+                                    cudaStream_t);                                              \
+  template void stencil_apply_dot<T>(const StencilSpec&, const T*, T*, const RedSlot&, cudaStream_t);
+
+INST_STENCIL(float)
+INST_STENCIL(double)
+INST_STENCIL(c32)
+INST_STENCIL(c64)
+
+}  // namespace mprkb

@@ -1,0 +1,368 @@
+// FastDiag tensor contractions (apply_tensor<T>, precond.hpp:69-122).
+//
+// Each side is a GEMM with the n x n factor Q (x-fastest layout):
+//   R:  C[(j,k)][a] = sum_q X[(j,k)][q] Q[a][q]     (M = n^2, N = n, K = n)
+//   M:  C[k][a][i]  = sum_q Q[a][q] X[k][q][i]      (batched over k planes)
+//   L:  C[a][(i,j)] = sum_q Q[a][q] X[q][(i,j)]     (M = n, N = n^2)
+// 12 n flop per DOF per FastDiag apply: compute-bound on CUDA-core FMA.
+//
+// k_tensor       — generic register-tiled kernel; every output accumulates
+//                  q in ascending order from +0 (the reference's loop), with
+//                  separately rounded mul/add in PARITY (bitwise equal) or FMA.
+// k_tensor_fast  — FAST numerics, real T, n % 4 == 0: 2-stage smem pipeline
+//                  with register prefetch, 16-byte global loads, split 8x8
+//                  thread tiles.  FOLD (Dirichlet sine basis only, where
+//                  Q[n-1-a][q] = (-1)^q Q[a][q]): the CTA computes rows
+//                  a < ceil(n/2) from even-q and odd-q partial sums and
+//                  writes C[a] = E + O, C[n-1-a] = E - O — half the FLOPs.
+// Zero-filled K padding is harmless: an accumulator started at +0 never
+// becomes -0, so adding +-0 leaves it unchanged.
+#include "launch.hpp"
+#include "vec.cuh"
+
+namespace mprkb {
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// generic (bit-exact capable) kernel
+// ---------------------------------------------------------------------------
+template <class T, int BM, int BN, int BK, int TM, int TN, bool RIGHT, bool EXACT, bool DIAG>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN))
+    k_tensor(const T* __restrict__ Q, const T* __restrict__ X, T* __restrict__ C, const T* __restrict__ pd, int n,
+             long Mdim, long Ndim, long ldx, long bstride) {
+  constexpr int NT = (BM / TM) * (BN / TN);
+  constexpr int PAD = 16 / sizeof(T) > 0 ? 16 / sizeof(T) : 1;
+  __shared__ __align__(16) T As[BK][BM + PAD];
+  __shared__ __align__(16) T Bs[BK][BN + PAD];
+  const int tid = threadIdx.x;
+  const int tx = tid % (BN / TN), ty = tid / (BN / TN);
+  const long m0 = (long)blockIdx.y * BM;
+  const long c0 = (long)blockIdx.x * BN;
+  const long boff = (long)blockIdx.z * bstride;
+
+  T acc[TM][TN];
+#pragma unroll
+  for (int a = 0; a < TM; ++a)
+#pragma unroll
+    for (int b = 0; b < TN; ++b) acc[a][b] = zero_v<T>();
+
+  for (int k0 = 0; k0 < n; k0 += BK) {
+#pragma unroll
+    for (int e = tid; e < BM * BK; e += NT) {
+      const int kk = e % BK, mm = e / BK;
+      const long m = m0 + mm;
+      const int k = k0 + kk;
+      T v = zero_v<T>();
+      if (m < Mdim && k < n) v = RIGHT ? ldg(X + boff + m * n + k) : ldg(Q + m * n + k);
+      As[kk][mm] = v;
+    }
+    if (RIGHT) {
+#pragma unroll
+      for (int e = tid; e < BN * BK; e += NT) {
+        const int kk = e % BK, cc = e / BK;
+        const long c = c0 + cc;
+        const int k = k0 + kk;
+        Bs[kk][cc] = (c < Ndim && k < n) ? ldg(Q + c * n + k) : zero_v<T>();
+      }
+    } else {
+#pragma unroll
+      for (int e = tid; e < BN * BK; e += NT) {
+        const int cc = e % BN, kk = e / BN;
+        const long c = c0 + cc;
+        const int k = k0 + kk;
+        Bs[kk][cc] = (c < Ndim && k < n) ? ldg(X + boff + (long)k * ldx + c) : zero_v<T>();
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      T av[TM], bv[TN];
+#pragma unroll
+      for (int a = 0; a < TM; ++a) av[a] = As[kk][ty * TM + a];
+#pragma unroll
+      for (int b = 0; b < TN; ++b) bv[b] = Bs[kk][tx * TN + b];
+#pragma unroll
+      for (int a = 0; a < TM; ++a)
+#pragma unroll
+        for (int b = 0; b < TN; ++b) {
+          if (EXACT)
+            acc[a][b] = xadd(acc[a][b], xmul(av[a], bv[b]));
+          else
+            acc[a][b] = fma_(av[a], bv[b], acc[a][b]);
+        }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < TM; ++a) {
+    const long m = m0 + ty * TM + a;
+    if (m >= Mdim) continue;
+#pragma unroll
+    for (int b = 0; b < TN; ++b) {
+      const long c = c0 + tx * TN + b;
+      if (c >= Ndim) continue;
+      const long o = RIGHT ? m * n + c : boff + m * ldx + c;
+      T v = acc[a][b];
+      if (DIAG) v = xmul(v, ldg(pd + o));
+      C[o] = v;
+    }
+  }
+}
+
+template <class T, int BM, int BN, int BK, int TM, int TN, bool EXACT, bool DIAG>
+void launch_generic_cfg(int side, int n, const T* q, const T* x, T* out, const T* pd, cudaStream_t st) {
+  constexpr int NT = (BM / TM) * (BN / TN);
+  const long nn = n, n2 = nn * nn;
+  if (side == 2) {
+    dim3 grid((unsigned)((nn + BN - 1) / BN), (unsigned)((n2 + BM - 1) / BM), 1);
+    k_tensor<T, BM, BN, BK, TM, TN, true, EXACT, DIAG><<<grid, NT, 0, st>>>(q, x, out, pd, n, n2, nn, nn, 0);
+  } else if (side == 1) {
+    dim3 grid((unsigned)((nn + BN - 1) / BN), (unsigned)((nn + BM - 1) / BM), (unsigned)nn);
+    k_tensor<T, BM, BN, BK, TM, TN, false, EXACT, DIAG><<<grid, NT, 0, st>>>(q, x, out, pd, n, nn, nn, nn, n2);
+  } else {
+    dim3 grid((unsigned)((n2 + BN - 1) / BN), (unsigned)((nn + BM - 1) / BM), 1);
+    k_tensor<T, BM, BN, BK, TM, TN, false, EXACT, DIAG><<<grid, NT, 0, st>>>(q, x, out, pd, n, nn, n2, n2, 0);
+  }
+  LAUNCHED("tensor");
+}
+
+template <class T, bool EXACT, bool DIAG>
+void launch_generic(int side, int n, const T* q, const T* x, T* out, const T* pd, cudaStream_t st) {
+  if constexpr (sizeof(T) <= 4) {
+    if (n >= 128) return launch_generic_cfg<T, 128, 128, 8, 8, 8, EXACT, DIAG>(side, n, q, x, out, pd, st);
+  }
+  if (n >= 48) return launch_generic_cfg<T, 64, 64, 8, 4, 4, EXACT, DIAG>(side, n, q, x, out, pd, st);
+  launch_generic_cfg<T, 32, 32, 8, 2, 2, EXACT, DIAG>(side, n, q, x, out, pd, st);
+}
+
+// ---------------------------------------------------------------------------
+// FAST kernel (real T, n % 4 == 0)
+// ---------------------------------------------------------------------------
+template <class T>
+struct Vec4Ld;
+template <>
+struct Vec4Ld<float> {
+  static __device__ __forceinline__ V4<float> ld(const float* p) { return ld4(p); }
+};
+template <>
+struct Vec4Ld<double> {
+  static __device__ __forceinline__ V4<double> ld(const double* p) { return ld4(p); }
+};
+
+// Thread-tile row/col i of TM (TN): two halves of the CTA tile, so a warp's
+// fragment reads are 2 distinct (A) / 16-wide contiguous (B) smem vectors.
+template <int B, int TT>
+__device__ __forceinline__ int frag(int t, int i) {
+  return i < TT / 2 ? t * (TT / 2) + i : B / 2 + t * (TT / 2) + (i - TT / 2);
+}
+
+template <class T, int BM, int BN, int BK, int TM, int TN, bool RIGHT, bool DIAG, bool FOLD>
+__global__ void __launch_bounds__((BM / TM) * (BN / TN), sizeof(T) == 4 ? 2 : 1)
+    k_tensor_fast(const T* __restrict__ Q, const T* __restrict__ X, T* __restrict__ C, const T* __restrict__ pd,
+                  int n, long Mdim, long Ndim, long ldx, long bstride) {
+  constexpr int NT = (BM / TM) * (BN / TN);
+  constexpr int PAD = 4;
+  constexpr int ACH = BM * BK / 4 / NT;  // float4-chunks of A per thread per K step
+  constexpr int BCH = BN * BK / 4 / NT;
+  static_assert(ACH >= 1 && BCH >= 1, "tile too small for the CTA");
+  constexpr int NACC = FOLD ? 2 : 1;
+  __shared__ __align__(16) T As[2][BK][BM + PAD];
+  __shared__ __align__(16) T Bs[2][BK][BN + PAD];
+  const int tid = threadIdx.x;
+  const int tx = tid % (BN / TN), ty = tid / (BN / TN);
+  const long m0 = (long)blockIdx.y * BM;
+  const long c0 = (long)blockIdx.x * BN;
+  const long boff = (long)blockIdx.z * bstride;
+
+  T acc[NACC][TM][TN];
+#pragma unroll
+  for (int p = 0; p < NACC; ++p)
+#pragma unroll
+    for (int a = 0; a < TM; ++a)
+#pragma unroll
+      for (int b = 0; b < TN; ++b) acc[p][a][b] = T(0);
+
+  V4<T> ra[ACH], rb[BCH];
+  // A (K-contiguous): chunk c -> row c / (BK/4), k offset (c % (BK/4)) * 4
+  auto load_a = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < ACH; ++i) {
+      const int c = tid + i * NT;
+      const int row = c / (BK / 4), kq = (c % (BK / 4)) * 4;
+      const long m = m0 + row;
+      const int k = k0 + kq;
+      if (m < Mdim && k < n)
+        ra[i] = Vec4Ld<T>::ld(RIGHT ? X + boff + m * n + k : Q + m * n + k);
+      else
+        ra[i] = zero4<T>();
+    }
+  };
+  auto load_b = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < BCH; ++i) {
+      const int c = tid + i * NT;
+      if (RIGHT) {  // B[q][a] = Q[a][q]: K-contiguous rows of Q
+        const int col = c / (BK / 4), kq = (c % (BK / 4)) * 4;
+        const long a = c0 + col;
+        const int k = k0 + kq;
+        rb[i] = (a < Ndim && k < n) ? Vec4Ld<T>::ld(Q + a * n + k) : zero4<T>();
+      } else {  // B[q][c] = X[q][c]: N-contiguous rows of X
+        const int row = c / (BN / 4), col = (c % (BN / 4)) * 4;
+        const int k = k0 + row;
+        const long cc = c0 + col;
+        rb[i] = (k < n && cc < Ndim) ? Vec4Ld<T>::ld(X + boff + (long)k * ldx + cc) : zero4<T>();
+      }
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < ACH; ++i) {
+      const int c = tid + i * NT;
+      const int row = c / (BK / 4), kq = (c % (BK / 4)) * 4;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) As[buf][kq + e][row] = ra[i].x[e];
+    }
+#pragma unroll
+    for (int i = 0; i < BCH; ++i) {
+      const int c = tid + i * NT;
+      if (RIGHT) {
+        const int col = c / (BK / 4), kq = (c % (BK / 4)) * 4;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) Bs[buf][kq + e][col] = rb[i].x[e];
+      } else {
+        const int row = c / (BN / 4), col = (c % (BN / 4)) * 4;
+        st4(&Bs[buf][row][col], rb[i]);
+      }
+    }
+  };
+
+  load_a(0);
+  load_b(0);
+  store(0);
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = 0; k0 < n; k0 += BK) {
+    const bool more = k0 + BK < n;
+    if (more) {
+      load_a(k0 + BK);
+      load_b(k0 + BK);
+    }
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      T av[TM], bv[TN];
+#pragma unroll
+      for (int a = 0; a < TM; ++a) av[a] = As[buf][kk][frag<BM, TM>(ty, a)];
+#pragma unroll
+      for (int b = 0; b < TN; ++b) bv[b] = Bs[buf][kk][frag<BN, TN>(tx, b)];
+      constexpr int dummy = 0;
+      (void)dummy;
+      const int p = FOLD ? (kk & 1) : 0;  // BK and k0 are even: parity of q is kk's
+#pragma unroll
+      for (int a = 0; a < TM; ++a)
+#pragma unroll
+        for (int b = 0; b < TN; ++b) acc[p][a][b] = fma_(av[a], bv[b], acc[p][a][b]);
+    }
+    if (more) {
+      store(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+
+  // epilogue
+#pragma unroll
+  for (int a = 0; a < TM; ++a) {
+    const long m = m0 + frag<BM, TM>(ty, a);
+    if (m >= Mdim) continue;
+#pragma unroll
+    for (int b = 0; b < TN; ++b) {
+      const long c = c0 + frag<BN, TN>(tx, b);
+      if (c >= Ndim) continue;
+      if (!FOLD) {
+        const long o = RIGHT ? m * n + c : boff + m * ldx + c;
+        T v = acc[0][a][b];
+        if (DIAG) v *= ldg(pd + o);
+        C[o] = v;
+      } else {
+        // rows (LEFT) / columns (RIGHT) a and n-1-a from the q-parity sums
+        const T e = acc[0][a][b], od = acc[FOLD ? 1 : 0][a][b];
+        const long qa = RIGHT ? c : m;  // index into Q's rows (< ceil(n/2))
+        const long qb = n - 1 - qa;
+        const long o1 = RIGHT ? m * n + qa : boff + qa * ldx + c;
+        const long o2 = RIGHT ? m * n + qb : boff + qb * ldx + c;
+        T v1 = e + od;
+        if (DIAG) v1 *= ldg(pd + o1);
+        C[o1] = v1;
+        if (qb != qa) {
+          T v2 = e - od;
+          if (DIAG) v2 *= ldg(pd + o2);
+          C[o2] = v2;
+        }
+      }
+    }
+  }
+}
+
+template <class T, int BM, int BN, int BK, int TM, int TN, bool DIAG, bool FOLD>
+void launch_fast_cfg(int side, int n, const T* q, const T* x, T* out, const T* pd, cudaStream_t st) {
+  constexpr int NT = (BM / TM) * (BN / TN);
+  const long nn = n, n2 = nn * nn;
+  const long nq = FOLD ? (nn + 1) / 2 : nn;  // rows of Q actually used
+  if (side == 2) {
+    dim3 grid((unsigned)((nq + BN - 1) / BN), (unsigned)((n2 + BM - 1) / BM), 1);
+    k_tensor_fast<T, BM, BN, BK, TM, TN, true, DIAG, FOLD><<<grid, NT, 0, st>>>(q, x, out, pd, n, n2, nq, nn, 0);
+  } else if (side == 1) {
+    dim3 grid((unsigned)((nn + BN - 1) / BN), (unsigned)((nq + BM - 1) / BM), (unsigned)nn);
+    k_tensor_fast<T, BM, BN, BK, TM, TN, false, DIAG, FOLD><<<grid, NT, 0, st>>>(q, x, out, pd, n, nq, nn, nn, n2);
+  } else {
+    dim3 grid((unsigned)((n2 + BN - 1) / BN), (unsigned)((nq + BM - 1) / BM), 1);
+    k_tensor_fast<T, BM, BN, BK, TM, TN, false, DIAG, FOLD><<<grid, NT, 0, st>>>(q, x, out, pd, n, nq, n2, n2, 0);
+  }
+  LAUNCHED("tensor_fast");
+}
+
+template <class T, bool DIAG, bool FOLD>
+void launch_fast(int side, int n, const T* q, const T* x, T* out, const T* pd, cudaStream_t st) {
+  if constexpr (sizeof(T) == 4 && FOLD)  // two accumulator sets: halve the thread tile
+    launch_fast_cfg<T, 128, 64, 16, 8, 4, DIAG, FOLD>(side, n, q, x, out, pd, st);
+  else if constexpr (sizeof(T) == 4)
+    launch_fast_cfg<T, 128, 128, 8, 8, 8, DIAG, FOLD>(side, n, q, x, out, pd, st);
+  else
+    launch_fast_cfg<T, 64, 64, 16, 4, 4, DIAG, FOLD>(side, n, q, x, out, pd, st);
+}
+
+}  // namespace
+
+template <class T>
+void tensor_apply(int side, int n, const T* q, const T* x, T* out, const T* pd, Numerics num, cudaStream_t st,
+                  bool fold) {
+  if (num == Numerics::Parity) {
+    if (pd)
+      launch_generic<T, true, true>(side, n, q, x, out, pd, st);
+    else
+      launch_generic<T, true, false>(side, n, q, x, out, pd, st);
+    return;
+  }
+  if constexpr (!is_cplx<T>) {
+    if (n % 4 == 0 && n >= 64) {
+      if (fold) {
+        if (pd) return launch_fast<T, true, true>(side, n, q, x, out, pd, st);
+        return launch_fast<T, false, true>(side, n, q, x, out, pd, st);
+      }
+      if (pd) return launch_fast<T, true, false>(side, n, q, x, out, pd, st);
+      return launch_fast<T, false, false>(side, n, q, x, out, pd, st);
+    }
+  }
+  if (pd)
+    launch_generic<T, false, true>(side, n, q, x, out, pd, st);
+  else
+    launch_generic<T, false, false>(side, n, q, x, out, pd, st);
+}
+
+template void tensor_apply<float>(int, int, const float*, const float*, float*, const float*, Numerics, cudaStream_t, bool);
+template void tensor_apply<double>(int, int, const double*, const double*, double*, const double*, Numerics, cudaStream_t, bool);
+template void tensor_apply<c32>(int, int, const c32*, const c32*, c32*, const c32*, Numerics, cudaStream_t, bool);
+template void tensor_apply<c64>(int, int, const c64*, const c64*, c64*, const c64*, Numerics, cudaStream_t, bool);
+
+}  // namespace mprkb

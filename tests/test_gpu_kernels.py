@@ -86,10 +86,14 @@ def test_tensor_permutation_known_answer(gpu, mp):
 
 
 @pytest.mark.parametrize("kind", [0, 1, 2, 3])
-@pytest.mark.parametrize("n", [3, 8, 32])
+@pytest.mark.parametrize("n", [3, 8, 32, 64, 96])
 def test_fastdiag_stage_bitwise(gpu, mp, ref, kind, n):
+    """PARITY bitwise; FAST (incl. the pipelined and sine-folded kernels at
+    n % 4 == 0, n >= 64) within tolerance of the reference."""
     import torch
 
+    if n == 96 and kind >= 2:
+        pytest.skip("reference cost")
     rng = np.random.default_rng(3000 + n + kind)
     x = rnd(rng, kind, n ** 3)
     eq = "heat" if kind <= 1 else "advection"
