@@ -223,6 +223,22 @@ int mprkb_tensor_apply(int dtype, int side, int n, const void* q, const void* x,
   });
 }
 
+int mprkb_tensor_apply_tc(int side, int n, const float* q_host, const float* x, float* out, void* stream) {
+  return guarded([&] {
+    require_device();
+    if (side < 0 || side > 2) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "unknown tensor side");
+    if (!tensor_tc_supported(n)) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "tensor-core contraction needs n % 128 == 0");
+    const size_t nn = (size_t)n * n;
+    std::vector<float> hi(nn), lo(nn);
+    pack_tf32_split(n, q_host, hi.data(), lo.data());
+    DevBuf dh(nn * 4), dl(nn * 4);
+    CUDA_CHECK(cudaMemcpy(dh.get(), hi.data(), nn * 4, cudaMemcpyHostToDevice));
+    CUDA_CHECK(cudaMemcpy(dl.get(), lo.data(), nn * 4, cudaMemcpyHostToDevice));
+    tensor_apply_tc(side, n, dh.as<float>(), dl.as<float>(), x, out, nullptr, S(stream));
+    CUDA_CHECK(cudaStreamSynchronize(S(stream)));
+  });
+}
+
 int mprkb_dot(int dtype, size_t m, const void* a, const void* b, int conjugate_dot, int numerics, double* result,
               void* stream) {
   return guarded([&] {

@@ -45,6 +45,15 @@ void apply_f32(const StencilSpec& k, const double* y, const float* y32, const fl
 template <class T>
 void tensor_apply(int side, int n, const T* q, const T* x, T* out, const T* pd, Numerics num,
                   cudaStream_t st, bool fold = false);
+// Tensor-core (tcgen05, 3xTF32) contraction for fp32, FAST numerics
+// (tensor_tc.cu).  q_{hi,lo}_packed: Q split into tf32 hi/lo parts and packed
+// by pack_tf32_split() into the canonical UMMA K-major layout.
+bool tensor_tc_supported(int n);
+void tensor_apply_tc(int side, int n, const float* q_hi_packed, const float* q_lo_packed, const float* x,
+                     float* out, const float* pd, cudaStream_t st);
+// Host: split Q (n x n row-major) into tf32 hi/lo and pack as
+// [k-block of 32][row-group of 8][k-chunk of 4][8 rows][4].
+void pack_tf32_split(int n, const float* q, float* hi_packed, float* lo_packed);
 // pd_inv[i+jn+kn^2] = 1/(la_i + lb_j + lc_k) in T (precond.hpp:139-150); real
 // types only (IEEE division is correctly rounded on both sides).  *zero_flag
 // (initialised to INT_MAX by the caller) receives the smallest linear index

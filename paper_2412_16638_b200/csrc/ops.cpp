@@ -35,7 +35,31 @@ void upload(DevBuf& d, const void* host, size_t bytes) {
   CUDA_CHECK(cudaMemcpy(d.get(), host, bytes, cudaMemcpyHostToDevice));
 }
 
+// round to tf32 (10 explicit mantissa bits), ties away from zero (cvt.rna)
+float tf32_rna(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7f800000u) != 0x7f800000u) u = (u + 0x1000u) & 0xffffe000u;
+  float r;
+  std::memcpy(&r, &u, 4);
+  return r;
+}
+
 }  // namespace
+
+void pack_tf32_split(int n, const float* q, float* hi_packed, float* lo_packed) {
+  const size_t nn = (size_t)n;
+  for (size_t row = 0; row < nn; ++row)
+    for (size_t k = 0; k < nn; ++k) {
+      const float x = q[row * nn + k];
+      const float hi = tf32_rna(x);
+      const float lo = tf32_rna(x - hi);
+      const size_t kb = k / 32, c = (k % 32) / 4, j = k % 4, g = row / 8, r = row % 8;
+      const size_t o = (((kb * (nn / 8) + g) * 8 + c) * 8 + r) * 4 + j;
+      hi_packed[o] = hi;
+      lo_packed[o] = lo;
+    }
+}
 
 StencilOp::StencilOp(int dtype, const StencilSpec& s) : Op(dtype, (size_t)s.n * s.n * s.n), spec_(s) {
   if (s.n < 2) MPRKB_THROW(3, "KronSumOperator: n must be at least 2");
@@ -75,6 +99,20 @@ FastDiagOp<T>::FastDiagOp(int n, const T* qa, const T* qa_inv, const T* qb, cons
           }
         fold_[f] = scale > 0.0 && worst <= 1e-6 * scale;
       }
+  }
+  if constexpr (std::is_same_v<T, float>) {
+    // fp32 FAST numerics on the tensor cores (3xTF32, tensor_tc.cu) when
+    // MPRKB_TENSOR_CORES=1; default: the sine-folded CUDA-core kernels
+    const char* env = std::getenv("MPRKB_TENSOR_CORES");
+    tc_ = num == Numerics::Fast && tensor_tc_supported(n) && (env && env[0] == '1');
+    if (tc_) {
+      std::vector<float> hi(nn), lo(nn);
+      for (int f = 0; f < 6; ++f) {
+        pack_tf32_split(n, src[f], hi.data(), lo.data());
+        upload(qhp_[f], hi.data(), nn * sizeof(float));
+        upload(qlp_[f], lo.data(), nn * sizeof(float));
+      }
+    }
   }
   pd_.alloc(m * sizeof(T));
   t1_.alloc(m * sizeof(T));
@@ -128,6 +166,20 @@ void FastDiagOp<T>::apply(const void* xv, void* outv, cudaStream_t st) {
   T* out = static_cast<T*>(outv);
   T* t1 = t1_.as<T>();
   T* t2 = t2_.as<T>();
+  if constexpr (std::is_same_v<T, float>) {
+    if (tc_) {
+      auto tc = [&](int side, int f, const float* in, float* o, const float* pd) {
+        tensor_apply_tc(side, n_, qhp_[f].as<float>(), qlp_[f].as<float>(), in, o, pd, st);
+      };
+      tc(2, 1, x, t1, nullptr);
+      tc(1, 3, t1, t2, nullptr);
+      tc(0, 5, t2, t1, pd_.as<float>());
+      tc(2, 0, t1, t2, nullptr);
+      tc(1, 2, t2, t1, nullptr);
+      tc(0, 4, t1, out, nullptr);
+      return;
+    }
+  }
   tensor_apply<T>(2, n_, q_[1].as<T>(), x, t1, nullptr, num_, st, fold_[1]);
   tensor_apply<T>(1, n_, q_[3].as<T>(), t1, t2, nullptr, num_, st, fold_[3]);
   tensor_apply<T>(0, n_, q_[5].as<T>(), t2, t1, pd_.as<T>(), num_, st, fold_[5]);

@@ -54,7 +54,9 @@ class FastDiagOp final : public Op {
   int n_;
   Numerics num_;
   bool fold_[6] = {false, false, false, false, false, false};  // sine symmetry per factor
+  bool tc_ = false;  // fp32 FAST: tensor-core (3xTF32) contractions
   DevBuf q_[6];  // qa, qa_inv, qb, qb_inv, qc, qc_inv
+  DevBuf qhp_[6], qlp_[6];  // tf32 hi/lo split, UMMA-packed (tc_ only)
   DevBuf pd_, t1_, t2_;
 };
 
