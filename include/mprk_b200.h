@@ -99,7 +99,7 @@ int mprkb_stencil_apply(int dtype, int n, int stencil, double sigma, double gamm
 int mprkb_tensor_apply(int dtype, int side, int n, const void* q, const void* x, void* out,
                        int numerics, void* stream);
 /* apply_tensor for fp32 on the tcgen05 tensor cores (3xTF32 split, fp32
- * accumulation; FAST numerics; n % 128 == 0): q is a HOST n*n matrix (split
+ * accumulation; FAST numerics; n % 256 == 0): q is a HOST n*n matrix (split
  * and packed per call), x/out device vectors. */
 int mprkb_tensor_apply_tc(int side, int n, const float* q_host, const float* x, float* out, void* stream);
 /* detail::dot_real / dot (krylov.hpp:43-66) on device vectors; result written

@@ -227,7 +227,7 @@ int mprkb_tensor_apply_tc(int side, int n, const float* q_host, const float* x, 
   return guarded([&] {
     require_device();
     if (side < 0 || side > 2) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "unknown tensor side");
-    if (!tensor_tc_supported(n)) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "tensor-core contraction needs n % 128 == 0");
+    if (!tensor_tc_supported(n)) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "tensor-core contraction needs n % 256 == 0");
     const size_t nn = (size_t)n * n;
     std::vector<float> hi(nn), lo(nn);
     pack_tf32_split(n, q_host, hi.data(), lo.data());

@@ -29,14 +29,16 @@ template <class T>
 void stencil_apply_dot(const StencilSpec& s, const T* p, T* q, const RedSlot& red, cudaStream_t st);
 
 // apply_f (operators.cpp:81-96), F64 policy: out = K y + g, y read as double
-// or widened from float (`y32`), g may be null.
+// or widened from float (`y32`, the fp32 stage solution, exact), g may be
+// null.  finite_flag (nullable): set when the stage vector y holds a NaN or
+// infinity (check_finite, stepper.cpp:18-21, fused into this pass).
 void apply_f64(const StencilSpec& k, const double* y, const float* y32, const double* g, double* out,
-               cudaStream_t st);
+               int* finite_flag, cudaStream_t st);
 // apply_f F32 policy: out32 = K f32(y) + f32(g) in binary32 (stored as float;
 // widening to double is exact and deferred to the consumer).  Sets *flag when
-// |y| overflows binary32 (precision.hpp:100-104).
+// |y| overflows binary32 (precision.hpp:100-104); y32 = y already in fp32.
 void apply_f32(const StencilSpec& k, const double* y, const float* y32, const float* g32, float* out32,
-               int* flag, cudaStream_t st);
+               int* flag, int* finite_flag, cudaStream_t st);
 
 // ---- tensor contractions (precond.hpp:69-122) --------------------------------------
 // side 0 L (stride n^2), 1 M (stride n), 2 R (stride 1).  pd: fused diag scale
@@ -52,7 +54,7 @@ bool tensor_tc_supported(int n);
 void tensor_apply_tc(int side, int n, const float* q_hi_packed, const float* q_lo_packed, const float* x,
                      float* out, const float* pd, cudaStream_t st);
 // Host: split Q (n x n row-major) into tf32 hi/lo and pack as
-// [k-block of 32][row-group of 8][k-chunk of 4][8 rows][4].
+// [k-block of 16][row-group of 8][k-chunk of 4][8 rows][4].
 void pack_tf32_split(int n, const float* q, float* hi_packed, float* lo_packed);
 // pd_inv[i+jn+kn^2] = 1/(la_i + lb_j + lc_k) in T (precond.hpp:139-150); real
 // types only (IEEE division is correctly rounded on both sides).  *zero_flag

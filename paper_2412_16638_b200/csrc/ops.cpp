@@ -54,8 +54,9 @@ void pack_tf32_split(int n, const float* q, float* hi_packed, float* lo_packed) 
       const float x = q[row * nn + k];
       const float hi = tf32_rna(x);
       const float lo = tf32_rna(x - hi);
-      const size_t kb = k / 32, c = (k % 32) / 4, j = k % 4, g = row / 8, r = row % 8;
-      const size_t o = (((kb * (nn / 8) + g) * 8 + c) * 8 + r) * 4 + j;
+      // [k-block of 16][row-group of 8][k-chunk of 4 (4 per block)][8 rows][4]
+      const size_t kb = k / 16, c = (k % 16) / 4, j = k % 4, g = row / 8, r = row % 8;
+      const size_t o = (((kb * (nn / 8) + g) * 4 + c) * 8 + r) * 4 + j;
       hi_packed[o] = hi;
       lo_packed[o] = lo;
     }
@@ -101,10 +102,10 @@ FastDiagOp<T>::FastDiagOp(int n, const T* qa, const T* qa_inv, const T* qb, cons
       }
   }
   if constexpr (std::is_same_v<T, float>) {
-    // fp32 FAST numerics on the tensor cores (3xTF32, tensor_tc.cu) when
-    // MPRKB_TENSOR_CORES=1; default: the sine-folded CUDA-core kernels
+    // fp32 FAST numerics run on the tensor cores (3xTF32, tensor_tc.cu)
+    // unless MPRKB_TENSOR_CORES=0 selects the CUDA-core kernels
     const char* env = std::getenv("MPRKB_TENSOR_CORES");
-    tc_ = num == Numerics::Fast && tensor_tc_supported(n) && (env && env[0] == '1');
+    tc_ = num == Numerics::Fast && tensor_tc_supported(n) && !(env && env[0] == '0');
     if (tc_) {
       std::vector<float> hi(nn), lo(nn);
       for (int f = 0; f < 6; ++f) {

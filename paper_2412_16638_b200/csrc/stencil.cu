@@ -166,9 +166,12 @@ struct EpiStoreDot {
 struct EpiF64Forcing {
   const double* g;
   double* out;
+  int* finite_flag;  // check_finite(y) on the centre values (nullable)
   struct State {};
   __device__ void init(State&) const {}
-  __device__ __forceinline__ void v4(State&, long i, const V4<double>& v, const V4<double>&) const {
+  __device__ __forceinline__ void v4(State&, long i, const V4<double>& v, const V4<double>& xc) const {
+    if (finite_flag && !(isfinite(xc.x[0]) && isfinite(xc.x[1]) && isfinite(xc.x[2]) && isfinite(xc.x[3])))
+      *finite_flag = 1;
     if (g) {
       const V4<double> gv = ld4(g + i);
       V4<double> o;
@@ -179,7 +182,10 @@ struct EpiF64Forcing {
       st4(out + i, v);
     }
   }
-  __device__ __forceinline__ void s1(State&, long i, double v, double) const { out[i] = g ? xadd(v, ldg(g + i)) : v; }
+  __device__ __forceinline__ void s1(State&, long i, double v, double xc) const {
+    if (finite_flag && !isfinite(xc)) *finite_flag = 1;
+    out[i] = g ? xadd(v, ldg(g + i)) : v;
+  }
   __device__ void finish(State&) const {}
 };
 
@@ -187,9 +193,12 @@ struct EpiF64Forcing {
 struct EpiF32Forcing {
   const float* g32;
   float* out;
+  int* finite_flag;  // check_finite(y) on the centre values (nullable)
   struct State {};
   __device__ void init(State&) const {}
-  __device__ __forceinline__ void v4(State&, long i, const V4<float>& v, const V4<float>&) const {
+  __device__ __forceinline__ void v4(State&, long i, const V4<float>& v, const V4<float>& xc) const {
+    if (finite_flag && !(isfinite(xc.x[0]) && isfinite(xc.x[1]) && isfinite(xc.x[2]) && isfinite(xc.x[3])))
+      *finite_flag = 1;
     if (g32) {
       const V4<float> gv = ld4(g32 + i);
       V4<float> o;
@@ -200,7 +209,10 @@ struct EpiF32Forcing {
       st4(out + i, v);
     }
   }
-  __device__ __forceinline__ void s1(State&, long i, float v, float) const { out[i] = g32 ? xadd(v, ldg(g32 + i)) : v; }
+  __device__ __forceinline__ void s1(State&, long i, float v, float xc) const {
+    if (finite_flag && !isfinite(xc)) *finite_flag = 1;
+    out[i] = g32 ? xadd(v, ldg(g32 + i)) : v;
+  }
   __device__ void finish(State&) const {}
 };
 
@@ -364,19 +376,19 @@ void stencil_apply_dot(const StencilSpec& s, const T* p, T* q, const RedSlot& re
 }
 
 void apply_f64(const StencilSpec& k, const double* y, const float* y32, const double* g, double* out,
-               cudaStream_t st) {
+               int* finite_flag, cudaStream_t st) {
   if (y32)
-    launch(k, LdF2D{y32}, EpiF64Forcing{g, out}, st, "apply_f64");
+    launch(k, LdF2D{y32}, EpiF64Forcing{g, out, finite_flag}, st, "apply_f64");
   else
-    launch(k, LdPlain<double>{y}, EpiF64Forcing{g, out}, st, "apply_f64");
+    launch(k, LdPlain<double>{y}, EpiF64Forcing{g, out, finite_flag}, st, "apply_f64");
 }
 
 void apply_f32(const StencilSpec& k, const double* y, const float* y32, const float* g32, float* out32, int* flag,
-               cudaStream_t st) {
+               int* finite_flag, cudaStream_t st) {
   if (y32)
-    launch(k, LdPlain<float>{y32}, EpiF32Forcing{g32, out32}, st, "apply_f32");
+    launch(k, LdPlain<float>{y32}, EpiF32Forcing{g32, out32, finite_flag}, st, "apply_f32");
   else
-    launch(k, LdD2F{y, flag}, EpiF32Forcing{g32, out32}, st, "apply_f32");
+    launch(k, LdD2F{y, flag}, EpiF32Forcing{g32, out32, finite_flag}, st, "apply_f32");
 }
 
 #define INST_STENCIL(T)                                                                          \

@@ -153,6 +153,9 @@ void Stepper::step(double* u, StepTrace& trace) {
 
   for (int i = 0; i < q; ++i) {
     CombineTerms terms;
+    const double* ys = y_.as<double>();  // stage vector source (see below)
+    const float* ys32 = nullptr;
+    bool stage_checked = false;
     for (int j = 0; j < i; ++j) {
       if (t.ah(i, j) != 0.0) add_term(terms, tau * t.ah(i, j), fh[j], 0);
       if (t.ae(i, j) != 0.0) add_term(terms, tau * t.ae(i, j), fe[j], fe32[j]);
@@ -185,32 +188,56 @@ void Stepper::step(double* u, StepTrace& trace) {
           gmres_solve<c64>(*S.op, S.pre.get(), bsol_.as<c64>(), xsol_.as<c64>(), crit, cfg_.num, *wc64_, rep, st_, tm);
           break;
       }
-      extract_stage(m, solve_dtype_, xsol_.get(), y_.as<double>(), check_slot(9, kStage), st_);
+      // The stage vector y is the solver's iterate: heat stages read it in
+      // place (fp32 widening is exact and deferred into the f evaluations,
+      // which also carry check_finite); complex (advection) stages take the
+      // real part first.
+      if (solve_dtype_ == 0) {
+        ys32 = xsol_.as<float>();
+      } else if (solve_dtype_ == 1) {
+        ys = xsol_.as<double>();
+      } else {
+        extract_stage(m, solve_dtype_, xsol_.get(), y_.as<double>(), check_slot(9, kStage), st_);
+        stage_checked = true;
+      }
       if (!rep.converged) trace.solver_failure = true;
       trace.solves.push_back(std::move(rep));
     } else {
       Bracket br(timer_, "axpy", st_);
       combine(m, u, terms, 0, y_.get(), check_slot(9, kStage), st_);
+      stage_checked = true;
     }
+    if (!stage_checked && !need_f64_[i] && !need_feps_[i]) {
+      // no f evaluation to carry the check: run it on its own
+      extract_stage(m, ys32 ? 0 : 1, ys32 ? (const void*)ys32 : (const void*)ys, y_.as<double>(),
+                    check_slot(9, kStage), st_);
+      stage_checked = true;
+    }
+    auto finite_slot = [&]() -> int* {
+      if (stage_checked) return nullptr;
+      stage_checked = true;
+      return check_slot(9, kStage);
+    };
 
     const double* g = prob_.forcing.empty() ? nullptr : g64_.as<double>();
     if (need_f64_[i]) {
       Bracket br(timer_, "stencil", st_);
-      apply_f64(kspec_, y_.as<double>(), nullptr, g, f_hi_[i].as<double>(), st_);
+      apply_f64(kspec_, ys, ys32, g, f_hi_[i].as<double>(), finite_slot(), st_);
       fh[i] = f_hi_[i].get();
     }
     if (need_feps_[i]) {
       if (cfg_.f32) {
         Bracket br(timer_, "stencil", st_);
-        apply_f32(kspec_, y_.as<double>(), nullptr, g ? g32_.as<float>() : nullptr, f_eps_[i].as<float>(),
-                  check_slot(6, kOverflow), st_);
+        int* fin = finite_slot();
+        apply_f32(kspec_, ys, ys32, g ? g32_.as<float>() : nullptr, f_eps_[i].as<float>(),
+                  ys32 ? sink : check_slot(6, kOverflow), fin, st_);
         fe[i] = f_eps_[i].get();
         fe32[i] = 1;
       } else if (need_f64_[i]) {
         fe[i] = fh[i];  // f_eps aliases f_hi (stepper.cpp:191-192)
       } else {
         Bracket br(timer_, "stencil", st_);
-        apply_f64(kspec_, y_.as<double>(), nullptr, g, f_eps_[i].as<double>(), st_);
+        apply_f64(kspec_, ys, ys32, g, f_eps_[i].as<double>(), finite_slot(), st_);
         fe[i] = f_eps_[i].get();
       }
     }

@@ -108,7 +108,7 @@ def test_fastdiag_stage_bitwise(gpu, mp, ref, kind, n):
         assert np.abs(fast - want).max() <= 50 * FAST_TOL[kind] * max(1.0, np.abs(want).max())
 
 
-@pytest.mark.parametrize("n", [128, 256])
+@pytest.mark.parametrize("n", [256])
 def test_fastdiag_tensor_cores_match_reference(gpu, mp, ref, n):
     """fp32 FAST FastDiag on tcgen05 (3xTF32) vs the reference's fp32 apply and
     vs an fp64 apply: the tensor-core path must be as accurate as fp32 FMA."""

@@ -216,6 +216,26 @@ def test_integrate_fast_matches_reference_64(gpu, mp, ref):
         d[:] = a
 
 
+def test_step_fast_256_within_reference_noise(gpu, mp, ref):
+    """The bench workload (heat 256^3, 4s3pB, fp32 implicit, tol 1e-3) in
+    FAST numerics — tensor-core FastDiag, fused kernels — against the
+    reference: iteration counts equal, and one step's state within 2x the
+    reference's own fp32-vs-fp64 distance (SURVEY.md §8c fast-mode bar)."""
+    t = mp.builtin("4s3pB")
+    n, tau = 256, 0.01
+    u32 = np.zeros(n ** 3)
+    u64 = np.zeros(n ** 3)
+    r32 = ref.stepper(0, n, tabd(t), tau, 1e-3, "f32").step(u32)
+    ref.stepper(0, n, tabd(t), tau, 1e-5, "f64").step(u64)
+    g = mp.Stepper("heat", n, t, tau, 1e-3, "f32")
+    ug = np.zeros(n ** 3)
+    tg = g.step(ug)
+    assert tg["iterations"] == r32["iterations"]
+    own = np.linalg.norm(u32 - u64)
+    assert np.linalg.norm(ug - u32) <= 2 * own, (np.linalg.norm(ug - u32), own)
+    assert np.linalg.norm(ug - u64) <= 2 * own
+
+
 def test_stepper_errors(gpu, mp):
     """blow-up -> NonFiniteState (test_stepper.cpp:208-215); bad tau -> MprkError;
     small grid -> DimensionTooSmall; bad precision/equation -> ValueError."""
