@@ -16,11 +16,13 @@
 //       M side: col = i,  B[i][q] = X[k][q][i]                 (transposed while splitting)
 //       L side: col = (i,j), B[c][q] = X[q][c]                 (transposed while splitting)
 //       loaded raw by TMA tensor copies (2D/3D boxes of 256 x 16 fp32).
-// Warp roles (192 threads): warps 0-3 split raw X into tf32 hi/lo in the
-// canonical layout (conflict-free 16-byte smem stores) and later run the
-// epilogue; warp 4 is the TMA/bulk producer; warp 5 issues the MMAs.  A
-// 3-stage mbarrier ring (full -> converted -> empty) overlaps HBM loads,
-// splitting and MMAs.  Epilogue: tcgen05.ld 32x32b.x32 -> (x pd_inv for the
+// Persistent (one CTA per SM, tiles strided by the grid), warp roles (320
+// threads): warps 0-3 split raw X into tf32 hi/lo in the canonical layout
+// (conflict-free 16-byte smem stores); warps 4-7 run the epilogue; warp 8 is
+// the TMA/bulk producer; warp 9 issues the MMAs.  A 3-stage mbarrier ring
+// (full -> converted -> empty) overlaps HBM loads, splitting and MMAs across
+// tile boundaries, and two 256-column TMEM accumulators let the epilogue of
+// tile t drain while tile t+1 accumulates.  Epilogue: tcgen05.ld 32x32b.x32 -> (x pd_inv for the
 // fused diagonal) -> global; for the R side D is C transposed, and lane a
 // writing C[col][a] makes every store instruction a coalesced 128-byte row.
 #include <cuda.h>
@@ -38,8 +40,11 @@ constexpr int TC_BM = 128;      // MMA M (rows of Q per CTA)
 constexpr int TC_BN = 256;      // MMA N (columns of X per CTA)
 constexpr int TC_BK = 16;       // k-block: 2 MMA k-steps of 8
 constexpr int TC_STAGES = 3;
-constexpr int TC_CONV_WARPS = 4;
-constexpr int TC_THREADS = (TC_CONV_WARPS + 2) * 32;
+constexpr int TC_CONV_WARPS = 4;   // warps 0-3: raw -> tf32 hi/lo
+constexpr int TC_EPI_WARP0 = 4;    // warps 4-7: epilogue (TMEM lane quarter = warp % 4)
+constexpr int TC_PROD_WARP = 8;    // TMA / bulk producer
+constexpr int TC_MMA_WARP = 9;     // single-thread MMA issue
+constexpr int TC_THREADS = 10 * 32;
 
 constexpr int RAW_BYTES = TC_BN * TC_BK * 4;  // 16 KB raw fp32 X
 constexpr int XS_BYTES = TC_BN * TC_BK * 4;   // 16 KB per hi / lo
@@ -51,7 +56,8 @@ struct TcSmem {
   alignas(8) uint64_t full[TC_STAGES];
   alignas(8) uint64_t conv[TC_STAGES];
   alignas(8) uint64_t empty[TC_STAGES];
-  alignas(8) uint64_t tmem_full;
+  alignas(8) uint64_t tmem_full[2];   // accumulator buffer ready for the epilogue
+  alignas(8) uint64_t tmem_empty[2];  // accumulator buffer drained
   uint32_t tmem_base;
 };
 
@@ -155,37 +161,53 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// SIDE: 2 = R, 1 = M, 0 = L
+// SIDE: 2 = R, 1 = M, 0 = L.  Persistent: CTA b processes tiles b, b + grid, ...
+// Tile t -> (a-tile = t % a_tiles, column tile = t / a_tiles [, plane]) so the
+// two a-tiles of one X column block run on neighbouring CTAs (L2 reuse).
 template <int SIDE, bool DIAG>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_tensor_tc(const __grid_constant__ CUtensorMap xmap, float* __restrict__ C, const float* __restrict__ pd,
-                const float* __restrict__ qh_pack, const float* __restrict__ ql_pack, int n) {
+                const float* __restrict__ qh_pack, const float* __restrict__ ql_pack, int n, int col_tiles,
+                int num_tiles) {
   extern __shared__ unsigned char smem_raw[];
   TcSmem& S = *reinterpret_cast<TcSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int KB = n / TC_BK;
+  const int a_tiles = n / TC_BM;
   const long nn = n, n2 = nn * nn;
-  const int a0 = blockIdx.x * TC_BM;   // rows of Q (output a)
-  const long col0 = (long)blockIdx.y * TC_BN;  // columns of X
-  const int plane = blockIdx.z;        // M side: k plane
   auto RAW = [&](int s) { return S.stage[s]; };
   auto XH = [&](int s) { return S.stage[s] + RAW_BYTES; };
   auto XL = [&](int s) { return S.stage[s] + RAW_BYTES + XS_BYTES; };
   auto QH = [&](int s) { return S.stage[s] + RAW_BYTES + 2 * XS_BYTES; };
   auto QL = [&](int s) { return S.stage[s] + RAW_BYTES + 2 * XS_BYTES + QS_BYTES; };
+  struct Tile {
+    int a0, plane;
+    long col0;
+  };
+  auto tile_of = [&](int t) {
+    Tile T;
+    T.a0 = (t % a_tiles) * TC_BM;
+    const int ct = t / a_tiles;
+    T.col0 = (long)(ct % col_tiles) * TC_BN;
+    T.plane = ct / col_tiles;  // M side only
+    return T;
+  };
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
-                 "r"((uint32_t)TC_BN));
+                 "r"(2u * TC_BN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (tid == 32 * TC_CONV_WARPS) {
+  if (tid == 32 * TC_PROD_WARP) {
     for (int s = 0; s < TC_STAGES; ++s) {
       mbar_init(&S.full[s], 1);
       mbar_init(&S.conv[s], 32 * TC_CONV_WARPS);
       mbar_init(&S.empty[s], 1);
     }
-    mbar_init(&S.tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&S.tmem_full[b], 1);
+      mbar_init(&S.tmem_empty[b], 128);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -193,128 +215,151 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = S.tmem_base;
 
-  if (warp == TC_CONV_WARPS) {
+  if (warp == TC_PROD_WARP) {
     // ---------------- producer: TMA for X, bulk copies for the Q tiles ----------
     if (lane == 0) {
-      for (int kb = 0; kb < KB; ++kb) {
-        const int s = kb % TC_STAGES;
-        if (kb >= TC_STAGES) mbar_wait(&S.empty[s], ((kb / TC_STAGES) - 1) & 1);
-        mbar_expect_tx(&S.full[s], RAW_BYTES + 2 * QS_BYTES);
-        if (SIDE == 2)
-          tma_2d(RAW(s), &xmap, kb * TC_BK, (int)col0, &S.full[s]);
-        else if (SIDE == 1)
-          tma_3d(RAW(s), &xmap, (int)col0, kb * TC_BK, plane, &S.full[s]);
-        else
-          tma_2d(RAW(s), &xmap, (int)col0, kb * TC_BK, &S.full[s]);
-        const long qoff = ((long)kb * (n / 8) + a0 / 8) * 128;  // floats
-        bulk_g2s(QH(s), qh_pack + qoff, QS_BYTES, &S.full[s]);
-        bulk_g2s(QL(s), ql_pack + qoff, QS_BYTES, &S.full[s]);
+      long g = 0;  // global k-block counter across tiles
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const Tile T = tile_of(t);
+        for (int kb = 0; kb < KB; ++kb, ++g) {
+          const int s = (int)(g % TC_STAGES);
+          if (g >= TC_STAGES) mbar_wait(&S.empty[s], (uint32_t)((g / TC_STAGES) - 1) & 1);
+          mbar_expect_tx(&S.full[s], RAW_BYTES + 2 * QS_BYTES);
+          if (SIDE == 2)
+            tma_2d(RAW(s), &xmap, kb * TC_BK, (int)T.col0, &S.full[s]);
+          else if (SIDE == 1)
+            tma_3d(RAW(s), &xmap, (int)T.col0, kb * TC_BK, T.plane, &S.full[s]);
+          else
+            tma_2d(RAW(s), &xmap, (int)T.col0, kb * TC_BK, &S.full[s]);
+          const long qoff = ((long)kb * (n / 8) + T.a0 / 8) * 128;  // floats
+          bulk_g2s(QH(s), qh_pack + qoff, QS_BYTES, &S.full[s]);
+          bulk_g2s(QL(s), ql_pack + qoff, QS_BYTES, &S.full[s]);
+        }
       }
     }
-  } else if (warp == TC_CONV_WARPS + 1) {
+  } else if (warp == TC_MMA_WARP) {
     // ---------------- MMA issuer ---------------------------------------------------
     if (lane == 0) {
-      for (int kb = 0; kb < KB; ++kb) {
-        const int s = kb % TC_STAGES;
-        mbar_wait(&S.conv[s], (kb / TC_STAGES) & 1);
+      long g = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&S.tmem_empty[acc], (uint32_t)((it >> 1) & 1) ^ 1u);  // fresh barrier passes
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + (uint32_t)(acc * TC_BN);
+        for (int kb = 0; kb < KB; ++kb, ++g) {
+          const int s = (int)(g % TC_STAGES);
+          mbar_wait(&S.conv[s], (uint32_t)(g / TC_STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-        for (int ks = 0; ks < TC_BK / 8; ++ks) {
-          const uint64_t qh = kmajor_desc(QH(s) + ks * 256), ql = kmajor_desc(QL(s) + ks * 256);
-          const uint64_t xh = kmajor_desc(XH(s) + ks * 256), xl = kmajor_desc(XL(s) + ks * 256);
-          mma_tf32(tmem, ql, xh, (kb | ks) ? 1u : 0u);
-          mma_tf32(tmem, qh, xl, 1u);
-          mma_tf32(tmem, qh, xh, 1u);
+          for (int ks = 0; ks < TC_BK / 8; ++ks) {
+            const uint64_t qh = kmajor_desc(QH(s) + ks * 256), ql = kmajor_desc(QL(s) + ks * 256);
+            const uint64_t xh = kmajor_desc(XH(s) + ks * 256), xl = kmajor_desc(XL(s) + ks * 256);
+            mma_tf32(d, ql, xh, (kb | ks) ? 1u : 0u);
+            mma_tf32(d, qh, xl, 1u);
+            mma_tf32(d, qh, xh, 1u);
+          }
+          mma_commit(&S.empty[s]);
         }
-        mma_commit(&S.empty[s]);
+        mma_commit(&S.tmem_full[acc]);
       }
-      mma_commit(&S.tmem_full);
     }
-  } else {
+  } else if (warp < TC_CONV_WARPS) {
     // ---------------- converters: raw fp32 -> tf32 hi/lo, canonical K-major ----------
     const int ct = tid;  // 0..127
-    for (int kb = 0; kb < KB; ++kb) {
-      const int s = kb % TC_STAGES;
-      mbar_wait(&S.full[s], (kb / TC_STAGES) & 1);
-      const unsigned char* raw = RAW(s);
-      if (SIDE == 2) {
-        // raw [256 rows][16 fp32] (64 B rows) -> [row-group][chunk][8][16 B]
+    long g = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int kb = 0; kb < KB; ++kb, ++g) {
+        const int s = (int)(g % TC_STAGES);
+        mbar_wait(&S.full[s], (uint32_t)(g / TC_STAGES) & 1);
+        const unsigned char* raw = RAW(s);
+        if (SIDE == 2) {
+          // raw [256 rows][16 fp32] (64 B rows) -> [row-group][chunk][8][16 B]
 #pragma unroll
-        for (int i = 0; i < (TC_BN * TC_BK / 4) / (32 * TC_CONV_WARPS); ++i) {
-          const int e = ct + i * 32 * TC_CONV_WARPS;
-          const int r_in = e & 7, c = (e >> 3) & 3, g = e >> 5;
-          const float4 v = *reinterpret_cast<const float4*>(raw + (g * 8 + r_in) * 64 + c * 16);
-          const uint32_t h0 = tf32_rna(v.x), h1 = tf32_rna(v.y), h2 = tf32_rna(v.z), h3 = tf32_rna(v.w);
-          const uint32_t l0 = tf32_rna(v.x - __uint_as_float(h0)), l1 = tf32_rna(v.y - __uint_as_float(h1));
-          const uint32_t l2 = tf32_rna(v.z - __uint_as_float(h2)), l3 = tf32_rna(v.w - __uint_as_float(h3));
-          const int o = (g * 4 + c) * 128 + r_in * 16;
-          *reinterpret_cast<uint4*>(XH(s) + o) = make_uint4(h0, h1, h2, h3);
-          *reinterpret_cast<uint4*>(XL(s) + o) = make_uint4(l0, l1, l2, l3);
-        }
-      } else {
-        // raw [16 q][256 c] (1 KB rows) -> B[c][q]: each thread owns columns c, c+128
+          for (int i = 0; i < (TC_BN * TC_BK / 4) / (32 * TC_CONV_WARPS); ++i) {
+            const int e = ct + i * 32 * TC_CONV_WARPS;
+            const int r_in = e & 7, c = (e >> 3) & 3, gr = e >> 5;
+            const float4 v = *reinterpret_cast<const float4*>(raw + (gr * 8 + r_in) * 64 + c * 16);
+            const uint32_t h0 = tf32_rna(v.x), h1 = tf32_rna(v.y), h2 = tf32_rna(v.z), h3 = tf32_rna(v.w);
+            const uint32_t l0 = tf32_rna(v.x - __uint_as_float(h0)), l1 = tf32_rna(v.y - __uint_as_float(h1));
+            const uint32_t l2 = tf32_rna(v.z - __uint_as_float(h2)), l3 = tf32_rna(v.w - __uint_as_float(h3));
+            const int o = (gr * 4 + c) * 128 + r_in * 16;
+            *reinterpret_cast<uint4*>(XH(s) + o) = make_uint4(h0, h1, h2, h3);
+            *reinterpret_cast<uint4*>(XL(s) + o) = make_uint4(l0, l1, l2, l3);
+          }
+        } else {
+          // raw [16 q][256 c] (1 KB rows) -> B[c][q]: each thread owns columns c, c+128
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int c = ct + h * 128;
-          float v[TC_BK];
+          for (int h = 0; h < 2; ++h) {
+            const int c = ct + h * 128;
+            float v[TC_BK];
 #pragma unroll
-          for (int q = 0; q < TC_BK; ++q) v[q] = *reinterpret_cast<const float*>(raw + q * 1024 + c * 4);
+            for (int q = 0; q < TC_BK; ++q) v[q] = *reinterpret_cast<const float*>(raw + q * 1024 + c * 4);
 #pragma unroll
-          for (int ch = 0; ch < TC_BK / 4; ++ch) {
-            uint32_t hi[4], lo[4];
+            for (int ch = 0; ch < TC_BK / 4; ++ch) {
+              uint32_t hi[4], lo[4];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-              hi[t] = tf32_rna(v[ch * 4 + t]);
-              lo[t] = tf32_rna(v[ch * 4 + t] - __uint_as_float(hi[t]));
+              for (int u = 0; u < 4; ++u) {
+                hi[u] = tf32_rna(v[ch * 4 + u]);
+                lo[u] = tf32_rna(v[ch * 4 + u] - __uint_as_float(hi[u]));
+              }
+              const int o = ((c >> 3) * 4 + ch) * 128 + (c & 7) * 16;
+              *reinterpret_cast<uint4*>(XH(s) + o) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+              *reinterpret_cast<uint4*>(XL(s) + o) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
             }
-            const int o = ((c >> 3) * 4 + ch) * 128 + (c & 7) * 16;
-            *reinterpret_cast<uint4*>(XH(s) + o) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-            *reinterpret_cast<uint4*>(XL(s) + o) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
           }
         }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&S.conv[s]);
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_arrive(&S.conv[s]);
     }
-
-    // ---------------- epilogue: TMEM -> registers -> global -----------------------
-    mbar_wait(&S.tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const long a = a0 + 32 * warp + lane;  // this lane's row of D (TMEM lane)
-    for (int cc = 0; cc < TC_BN; cc += 32) {
-      uint32_t r[32];
-      tmem_ld32(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)cc, r);
-      if (SIDE == 2) {
-        // D[a][fibre] = C[fibre][a]: for fixed j the warp's lanes write 32 consecutive a
+  } else if (warp < TC_EPI_WARP0 + 4) {
+    // ---------------- epilogue: TMEM -> registers -> global (overlaps the next tile) ------
+    const int q4 = warp - TC_EPI_WARP0;  // TMEM lane quarter
+    int it = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      const Tile T = tile_of(t);
+      const int acc = it & 1;
+      mbar_wait(&S.tmem_full[acc], (uint32_t)(it >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const long a = T.a0 + 32 * q4 + lane;  // this lane's row of D
+      for (int cc = 0; cc < TC_BN; cc += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(32 * q4) << 16) + (uint32_t)(acc * TC_BN + cc), r);
+        if (SIDE == 2) {
+          // D[a][fibre] = C[fibre][a]: for fixed j the warp writes 32 consecutive a
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const long o = (col0 + cc + j) * nn + a;
-          float v = __uint_as_float(r[j]);
-          if (DIAG) v *= __ldg(pd + o);
-          C[o] = v;
-        }
-      } else {
-        const long base = SIDE == 1 ? (long)plane * n2 + a * nn + col0 + cc : a * n2 + col0 + cc;
-#pragma unroll
-        for (int j = 0; j < 32; j += 4) {
-          float4 v = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
-                                 __uint_as_float(r[j + 3]));
-          if (DIAG) {
-            const float4 p = __ldg(reinterpret_cast<const float4*>(pd + base + j));
-            v.x *= p.x;
-            v.y *= p.y;
-            v.z *= p.z;
-            v.w *= p.w;
+          for (int j = 0; j < 32; ++j) {
+            const long o = (T.col0 + cc + j) * nn + a;
+            float v = __uint_as_float(r[j]);
+            if (DIAG) v *= __ldg(pd + o);
+            C[o] = v;
           }
-          *reinterpret_cast<float4*>(C + base + j) = v;
+        } else {
+          const long base = SIDE == 1 ? (long)T.plane * n2 + a * nn + T.col0 + cc : a * n2 + T.col0 + cc;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            float4 v = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
+                                   __uint_as_float(r[j + 3]));
+            if (DIAG) {
+              const float4 p = __ldg(reinterpret_cast<const float4*>(pd + base + j));
+              v.x *= p.x;
+              v.y *= p.y;
+              v.z *= p.z;
+              v.w *= p.w;
+            }
+            *reinterpret_cast<float4*>(C + base + j) = v;
+          }
         }
       }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&S.tmem_empty[acc]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)TC_BN));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2u * TC_BN));
 }
 
 // ---- host: tensor maps ------------------------------------------------------------
@@ -354,24 +399,28 @@ void launch_tc(int n, const float* x, float* out, const float* pd, const float* 
   }
   const cuuint64_t nn = (cuuint64_t)n, n2 = nn * nn;
   CUtensorMap map;
-  dim3 grid;
+  int col_tiles;  // X column tiles per (plane)
+  int planes = 1;
   if (SIDE == 2) {  // X as [n^2 fibres][n q]
     const cuuint64_t dims[2] = {nn, n2}, strides[1] = {nn * 4};
     const cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)TC_BN};
     map = make_map(x, 2, dims, strides, box);
-    grid = dim3(n / TC_BM, (unsigned)(n2 / TC_BN), 1);
+    col_tiles = (int)(n2 / TC_BN);
   } else if (SIDE == 1) {  // X as [n k][n q][n i]
     const cuuint64_t dims[3] = {nn, nn, nn}, strides[2] = {nn * 4, n2 * 4};
     const cuuint32_t box[3] = {(cuuint32_t)TC_BN, (cuuint32_t)TC_BK, 1};
     map = make_map(x, 3, dims, strides, box);
-    grid = dim3(n / TC_BM, (unsigned)(nn / TC_BN), n);
+    col_tiles = (int)(nn / TC_BN);
+    planes = n;
   } else {  // X as [n q][n^2 c]
     const cuuint64_t dims[2] = {n2, nn}, strides[1] = {n2 * 4};
     const cuuint32_t box[2] = {(cuuint32_t)TC_BN, (cuuint32_t)TC_BK};
     map = make_map(x, 2, dims, strides, box);
-    grid = dim3(n / TC_BM, (unsigned)(n2 / TC_BN), 1);
+    col_tiles = (int)(n2 / TC_BN);
   }
-  k_tensor_tc<SIDE, DIAG><<<grid, TC_THREADS, smem, st>>>(map, out, pd, qh, ql, n);
+  const int num_tiles = (n / TC_BM) * col_tiles * planes;
+  const int grid = num_tiles < sm_count() ? num_tiles : sm_count();
+  k_tensor_tc<SIDE, DIAG><<<grid, TC_THREADS, smem, st>>>(map, out, pd, qh, ql, n, col_tiles, num_tiles);
   LAUNCHED("tensor_tc");
 }
 
