@@ -161,6 +161,12 @@ int mprkb_cg(int dtype, size_t m, mprkb_op* op, mprkb_op* precond, const void* b
 /* gmres<T>(...) — same conventions. */
 int mprkb_gmres(int dtype, size_t m, mprkb_op* op, mprkb_op* precond, const void* b, void* x,
                 double tol, int max_iter, int numerics, mprkb_solve_report* report, void* stream);
+/* gmres with the Krylov basis stored in `basis_storage` (-1 = dtype, as the
+ * reference; MPRKB_F16 = fp16 / 2 x fp16 for complex, fp64-accumulated MGS
+ * dots) — the accessor-style storage extension. */
+int mprkb_gmres_ex(int dtype, size_t m, mprkb_op* op, mprkb_op* precond, const void* b, void* x,
+                   double tol, int max_iter, int numerics, int basis_storage,
+                   mprkb_solve_report* report, void* stream);
 
 /* ---- coarse boundary: Stepper / integrate (stepper.hpp:20-99) --------------- */
 #define MPRKB_MAX_STAGES 16
@@ -182,6 +188,8 @@ typedef struct {
   int block_storage;       /* block-Jacobi storage precision (default = compute)        */
   double nu;               /* diffusion coefficient (advection-diffusion only)          */
   int record_timings;      /* 1: CUDA-event brackets under the reference's labels       */
+  int basis_storage;       /* GMRES Krylov-basis storage: -1 = working precision        */
+                           /* (reference), MPRKB_F16 = fp16 basis, fp64 dots (extension) */
 } mprkb_config;
 
 void mprkb_config_init(mprkb_config* cfg);

@@ -334,6 +334,42 @@ int ref_stage_solve(int dtype, int solver, int n, double tau, double a, int prec
   });
 }
 
+// Stage solve with a caller-supplied preconditioner callback (host vectors of
+// m scalars of the dtype): the block-Jacobi / fp16-storage oracle route —
+// a CPU ApplyFn plugged into the reference's own cg / gmres.
+typedef void (*ref_apply_cb)(void* ctx, const void* x, void* out);
+
+int ref_stage_solve_cb(int dtype, int solver, int n, double tau, double a, ref_apply_cb pre, void* ctx,
+                       const void* b, const void* x0, double tol, int max_iter, void* x_out, int* iters,
+                       int* converged, int* failure, double* true_res, double* hist, int hist_cap, int* hist_len) {
+  return guarded([&] {
+    const Equation eq = (dtype <= 1) ? Equation::Heat : Equation::Advection;
+    const ProblemSpec p = make_problem(eq, n);
+    const KronSumOperator op = stage_operator(p, tau, a);
+    const std::size_t m = p.size();
+    const StoppingCriterion crit{tol, max_iter};
+    SolveReport rep;
+    auto solve = [&](auto tag) {
+      using T = decltype(tag);
+      ApplyFn<T> A = [&](const std::vector<T>& v, std::vector<T>& o) { op.apply(v, o); };
+      ApplyFn<T> P = [&](const std::vector<T>& v, std::vector<T>& o) {
+        o.resize(v.size());
+        pre(ctx, v.data(), o.data());
+      };
+      std::vector<T> x = solver == 0 ? cg<T>(A, P, vec<T>(b, m), vec<T>(x0, m), crit, rep)
+                                     : gmres<T>(A, P, vec<T>(b, m), vec<T>(x0, m), crit, rep);
+      put(x, x_out);
+    };
+    switch (dtype) {
+      case 0: solve(float{}); break;
+      case 1: solve(double{}); break;
+      case 2: solve(cf{}); break;
+      default: solve(cd{}); break;
+    }
+    fill_report(rep, iters, converged, failure, true_res, hist, hist_cap, hist_len);
+  });
+}
+
 // --- Stepper / integrate ------------------------------------------------------
 
 struct RefStepper {

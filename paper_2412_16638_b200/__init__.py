@@ -147,7 +147,7 @@ def heat_exact(n: int, t: float) -> np.ndarray:
 
 
 def _config(tableau: Tableau, equation, n, tau, t_end, tol, precision, max_iter, numerics, preconditioner,
-            block_size, block_storage, nu, timings):
+            block_size, block_storage, nu, timings, basis_storage=None):
     cfg = _c.Config()
     _c.lib.mprkb_config_init(C.byref(cfg))
     cfg.equation = _parse(_EQ, equation, "equation", "heat or advection")
@@ -169,6 +169,7 @@ def _config(tableau: Tableau, equation, n, tau, t_end, tol, precision, max_iter,
     cfg.block_storage = _parse(_STORE, block_storage, "storage", "f16, f32 or f64")
     cfg.nu = float(nu)
     cfg.record_timings = 1 if timings else 0
+    cfg.basis_storage = _parse({None: -1, "f16": _c.F16}, basis_storage, "basis storage", "None or f16")
     return cfg, keep
 
 
@@ -183,9 +184,9 @@ class Stepper:
     def __init__(self, equation: str, n: int, tableau: Tableau, tau: float, tol: float = 1e-6,
                  precision: str = "f64", max_iter: int = 40, *, t_end: float = 0.1, numerics: str = "fast",
                  preconditioner: str = "fastdiag", block_size: int = 8, block_storage: Optional[str] = None,
-                 nu: float = 0.0, timings: bool = False):
+                 nu: float = 0.0, timings: bool = False, basis_storage: Optional[str] = None):
         cfg, keep = _config(tableau, equation, n, tau, t_end, tol, precision, max_iter, numerics,
-                            preconditioner, block_size, block_storage, nu, timings)
+                            preconditioner, block_size, block_storage, nu, timings, basis_storage)
         self._h = C.c_void_p()
         check(_c.lib.mprkb_stepper_create(C.byref(cfg), C.byref(self._h)))
         self.n = int(n)
@@ -266,7 +267,8 @@ def _result_dict(res, its, state):
 def integrate(tableau: Tableau, equation: str, n: int, tau: float, t_end: float, tol: float = 1e-6,
               precision: str = "f64", max_iter: int = 40, *, numerics: str = "fast",
               preconditioner: str = "fastdiag", block_size: int = 8, block_storage: Optional[str] = None,
-              nu: float = 0.0, reference: Optional[np.ndarray] = None) -> dict:
+              nu: float = 0.0, reference: Optional[np.ndarray] = None,
+              basis_storage: Optional[str] = None) -> dict:
     """mprk.integrate (bindings.cpp:130-147): run the split-tableau integrator
     on a built-in problem; returns the reference's result dict (steps,
     solver_failure, mean_iterations, total_iterations, solve_iterations,
@@ -283,7 +285,7 @@ def integrate(tableau: Tableau, equation: str, n: int, tau: float, t_end: float,
         raise MprkError("integrate: tau must divide t_end")
     st = Stepper(equation, n, tableau, tau, tol, precision, max_iter, t_end=t_end, numerics=numerics,
                  preconditioner=preconditioner, block_size=block_size, block_storage=block_storage, nu=nu,
-                 timings=True)
+                 timings=True, basis_storage=basis_storage)
     out = st.integrate(reference)
     out["timings"] = st.timings()
     return out
@@ -432,13 +434,13 @@ class Operator:
         return Operator(h, dtype, size, keep=cb)
 
 
-def _krylov(fn, op: Operator, precond: Optional[Operator], b, x0, tol, max_iter, numerics):
+def _krylov(fn, op: Operator, precond: Optional[Operator], b, x0, tol, max_iter, numerics, extra=()):
     dt = _dtype_code(b)
     x = x0.clone()
     hist = np.zeros(max_iter + 8)
     rep = _c.SolveReport(0, 0, 0, 0.0, hist.ctypes.data_as(C.POINTER(C.c_double)), len(hist), 0)
     check(fn(dt, b.numel(), op._h, precond._h if precond is not None else None, _ptr(b), _ptr(x), tol, max_iter,
-             _NUM[numerics], C.byref(rep), _stream()))
+             _NUM[numerics], *extra, C.byref(rep), _stream()))
     return x, dict(iterations=rep.iterations, converged=bool(rep.converged), failure=rep.failure,
                    true_residual=rep.true_residual, history=hist[: rep.history_length].copy())
 
@@ -450,9 +452,13 @@ def cg(op: Operator, precond: Optional[Operator], b, x0, tol: float = 1e-6, max_
 
 
 def gmres(op: Operator, precond: Optional[Operator], b, x0, tol: float = 1e-6, max_iter: int = 40,
-          numerics: str = "fast"):
-    """gmres<T>(op, precond, b, x0, crit, report) (krylov.hpp:181-311) -> (x, report)."""
-    return _krylov(_c.lib.mprkb_gmres, op, precond, b, x0, tol, max_iter, numerics)
+          numerics: str = "fast", basis_storage: Optional[str] = None):
+    """gmres<T>(op, precond, b, x0, crit, report) (krylov.hpp:181-311) -> (x, report).
+    basis_storage="f16" keeps the Krylov basis in fp16 (extension)."""
+    if basis_storage is None:
+        return _krylov(_c.lib.mprkb_gmres, op, precond, b, x0, tol, max_iter, numerics)
+    code = _parse({"f16": _c.F16}, basis_storage, "basis storage", "None or f16")
+    return _krylov(_c.lib.mprkb_gmres_ex, op, precond, b, x0, tol, max_iter, numerics, extra=(code,))
 
 
 def kernel_launches() -> int:

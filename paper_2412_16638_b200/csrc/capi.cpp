@@ -94,6 +94,9 @@ StepperConfig config_of(const mprkb_config* c) {
   s.block_storage = c->block_storage;
   s.nu = c->nu;
   s.timings = c->record_timings != 0;
+  s.basis_storage = c->basis_storage;
+  if (s.basis_storage != -1 && s.basis_storage != MPRKB_F16)
+    MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "basis storage must be -1 (working precision) or F16");
   return s;
 }
 
@@ -344,7 +347,8 @@ void mprkb_op_destroy(mprkb_op* op) { delete op; }
 
 // ---- Krylov -------------------------------------------------------------------------
 static int krylov(bool use_cg, int dtype, size_t m, mprkb_op* op, mprkb_op* precond, const void* b, void* x,
-                  double tol, int max_iter, int numerics, mprkb_solve_report* report, void* stream) {
+                  double tol, int max_iter, int numerics, mprkb_solve_report* report, void* stream,
+                  int basis_storage = -1) {
   return guarded([&] {
     require_device();
     check_dtype(dtype);
@@ -369,7 +373,7 @@ static int krylov(bool use_cg, int dtype, size_t m, mprkb_op* op, mprkb_op* prec
       } else {
         if (use_cg) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "cg: complex systems use gmres");
       }
-      gmres_solve<T>(*op->op, P, (const T*)b, (T*)x, crit, num, w, rep, st);
+      gmres_solve<T>(*op->op, P, (const T*)b, (T*)x, crit, num, w, rep, st, nullptr, basis_storage);
     };
     switch (dtype) {
       case 0: run(float{}); break;
@@ -392,6 +396,11 @@ int mprkb_gmres(int dtype, size_t m, mprkb_op* op, mprkb_op* precond, const void
   return krylov(false, dtype, m, op, precond, b, x, tol, max_iter, numerics, report, stream);
 }
 
+int mprkb_gmres_ex(int dtype, size_t m, mprkb_op* op, mprkb_op* precond, const void* b, void* x, double tol,
+                   int max_iter, int numerics, int basis_storage, mprkb_solve_report* report, void* stream) {
+  return krylov(false, dtype, m, op, precond, b, x, tol, max_iter, numerics, report, stream, basis_storage);
+}
+
 // ---- Stepper / integrate -------------------------------------------------------------
 void mprkb_config_init(mprkb_config* c) {
   std::memset(c, 0, sizeof *c);
@@ -405,6 +414,7 @@ void mprkb_config_init(mprkb_config* c) {
   c->block_size = 8;
   c->block_storage = -1;
   c->nu = 0.0;
+  c->basis_storage = -1;
 }
 
 int mprkb_stepper_create(const mprkb_config* cfg, mprkb_stepper** out) {

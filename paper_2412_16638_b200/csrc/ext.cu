@@ -1,0 +1,272 @@
+// North-star extensions (no reference counterpart):
+//   * block-Jacobi apply with per-block storage precision (Ginkgo-style
+//     accessor: blocks stored in fp16 / fp32 / fp64, arithmetic in the
+//     stage's compute precision),
+//   * CSR SpMV with fp16 / fp32 / fp64 value storage,
+//   * Krylov-basis storage in a lower precision (GMRES), fp64-accumulated dots.
+// All HBM-bound.  Algorithmic bytes per DOF: block-Jacobi (2 s + b s_b),
+// CSR (2 s + nnz_row (s_v + 4) + 4), basis ops 2-3 vector streams.
+#include "launch.hpp"
+#include "reduce.cuh"
+#include "vec.cuh"
+
+namespace mprkb {
+
+namespace {
+
+template <class S>
+__device__ __forceinline__ double widen(S v);
+template <>
+__device__ __forceinline__ double widen<__half>(__half v) {
+  return (double)__half2float(v);
+}
+template <>
+__device__ __forceinline__ double widen<float>(float v) {
+  return (double)v;
+}
+template <>
+__device__ __forceinline__ double widen<double>(double v) {
+  return v;
+}
+
+// storage value -> compute real type R (exact: fp16 and fp32 embed in fp32/fp64)
+template <class R, class S>
+__device__ __forceinline__ R ld_store(const S* p) {
+  if constexpr (std::is_same_v<S, __half>) {
+    return (R)__half2float(__ldg(p));
+  } else {
+    return (R)__ldg(p);
+  }
+}
+
+// real scalar (R) times value (T): exact product rounding
+__device__ __forceinline__ float rmul(float a, float x) { return xmul(a, x); }
+__device__ __forceinline__ double rmul(double a, double x) { return xmul(a, x); }
+template <class R>
+__device__ __forceinline__ cplx<R> rmul(R a, cplx<R> x) {
+  return {xmul(a, x.re), xmul(a, x.im)};
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------
+// block-Jacobi
+//   blocks: x-line segments [i0, i0 + bs) of each (j, k) line, bs = min(b, n - i0)
+//   inv: per block, column-major bs x bs inverse in storage S (block B at
+//   offset B * b * b), so for fixed j the rows of a block read consecutive
+//   addresses (coalesced).
+// ---------------------------------------------------------------------------------
+template <class T, class S>
+__global__ void __launch_bounds__(256) k_block_jacobi(int n, int b, const S* __restrict__ inv, const T* __restrict__ r,
+                                                      T* __restrict__ z) {
+  using R = real_t<T>;
+  const long nn = n, m = nn * nn * nn;
+  const int per_line = (n + b - 1) / b;
+  for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < m; idx += (long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx % nn);
+    const long line = idx / nn;
+    const int blk = i / b, i0 = blk * b, bs = min(b, n - i0), ii = i - i0;
+    const S* D = inv + (line * per_line + blk) * (long)b * b;
+    const T* rb = r + line * nn + i0;
+    T acc = zero_v<T>();
+    for (int jj = 0; jj < bs; ++jj) acc = xadd(acc, rmul(ld_store<R>(D + (long)jj * bs + ii), ldg(rb + jj)));
+    z[idx] = acc;
+  }
+}
+
+template <class S>
+__global__ void k_bj_fill(long nblocks_per_line, long lines, int n, int b, const double* __restrict__ full,
+                          const double* __restrict__ tail, S* __restrict__ inv) {
+  const long total = nblocks_per_line * lines * (long)b * b;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    const long blk = (e / ((long)b * b)) % nblocks_per_line;
+    const int off = (int)(e % ((long)b * b));
+    const int i0 = (int)blk * b, bs = min(b, n - i0);
+    const double* src = bs == b ? full : tail;
+    double v = off < bs * bs ? src[off] : 0.0;
+    if constexpr (std::is_same_v<S, __half>)
+      inv[e] = __double2half(v);
+    else
+      inv[e] = (S)v;
+  }
+}
+
+template <class T>
+void block_jacobi_apply(int n, int b, int storage, const void* inv, const T* r, T* z, cudaStream_t st) {
+  const size_t m = (size_t)n * n * n;
+  const unsigned g = grid_for(m, 256, 8);
+  switch (storage) {
+    case 4: k_block_jacobi<T, __half><<<g, 256, 0, st>>>(n, b, (const __half*)inv, r, z); break;
+    case 0: k_block_jacobi<T, float><<<g, 256, 0, st>>>(n, b, (const float*)inv, r, z); break;
+    default: k_block_jacobi<T, double><<<g, 256, 0, st>>>(n, b, (const double*)inv, r, z); break;
+  }
+  LAUNCHED("block_jacobi");
+}
+
+void block_jacobi_fill(int n, int b, int storage, const double* full_dev, const double* tail_dev, void* inv,
+                       cudaStream_t st) {
+  const long per_line = (n + b - 1) / b, lines = (long)n * n;
+  const size_t total = (size_t)per_line * lines * b * b;
+  const unsigned g = grid_for(total, 256, 8);
+  switch (storage) {
+    case 4: k_bj_fill<__half><<<g, 256, 0, st>>>(per_line, lines, n, b, full_dev, tail_dev, (__half*)inv); break;
+    case 0: k_bj_fill<float><<<g, 256, 0, st>>>(per_line, lines, n, b, full_dev, tail_dev, (float*)inv); break;
+    default: k_bj_fill<double><<<g, 256, 0, st>>>(per_line, lines, n, b, full_dev, tail_dev, (double*)inv); break;
+  }
+  LAUNCHED("block_jacobi_fill");
+}
+
+// ---------------------------------------------------------------------------------
+// CSR SpMV: y[i] = sum_k val[k] x[col[k]] in ascending k (compute precision T,
+// values widened exactly from storage S)
+// ---------------------------------------------------------------------------------
+template <class T, class S>
+__global__ void __launch_bounds__(256) k_csr(int rows, const int* __restrict__ rp, const int* __restrict__ cols,
+                                             const S* __restrict__ vals, const T* __restrict__ x, T* __restrict__ y) {
+  using R = real_t<T>;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x) {
+    T acc = zero_v<T>();
+    const int e = __ldg(rp + i + 1);
+    for (int k = __ldg(rp + i); k < e; ++k) acc = xadd(acc, rmul(ld_store<R>(vals + k), ldg(x + __ldg(cols + k))));
+    y[i] = acc;
+  }
+}
+
+template <class T>
+void csr_apply(int rows, const int* rp, const int* cols, const void* vals, int storage, const T* x, T* y,
+               cudaStream_t st) {
+  const unsigned g = grid_for((size_t)rows, 256, 8);
+  switch (storage) {
+    case 4: k_csr<T, __half><<<g, 256, 0, st>>>(rows, rp, cols, (const __half*)vals, x, y); break;
+    case 0: k_csr<T, float><<<g, 256, 0, st>>>(rows, rp, cols, (const float*)vals, x, y); break;
+    default: k_csr<T, double><<<g, 256, 0, st>>>(rows, rp, cols, (const double*)vals, x, y); break;
+  }
+  LAUNCHED("csr");
+}
+
+// ---------------------------------------------------------------------------------
+// low-precision Krylov-basis storage (GMRES): basis vectors kept in storage
+// type S (fp16: __half / __half2 for complex), arithmetic in T, dots in fp64.
+// ---------------------------------------------------------------------------------
+template <class T>
+struct Store16;
+template <>
+struct Store16<float> {
+  using type = __half;
+  static __device__ __forceinline__ type put(float v) { return __float2half_rn(v); }
+  static __device__ __forceinline__ float get(type v) { return __half2float(v); }
+};
+template <>
+struct Store16<double> {
+  using type = __half;
+  static __device__ __forceinline__ type put(double v) { return __double2half(v); }
+  static __device__ __forceinline__ double get(type v) { return (double)__half2float(v); }
+};
+template <>
+struct Store16<c32> {
+  using type = __half2;
+  static __device__ __forceinline__ type put(c32 v) { return __floats2half2_rn(v.re, v.im); }
+  static __device__ __forceinline__ c32 get(type v) {
+    const float2 f = __half22float2(v);
+    return {f.x, f.y};
+  }
+};
+template <>
+struct Store16<c64> {
+  using type = __half2;
+  static __device__ __forceinline__ type put(c64 v) { return __halves2half2(__double2half(v.re), __double2half(v.im)); }
+  static __device__ __forceinline__ c64 get(type v) {
+    const float2 f = __half22float2(v);
+    return {(double)f.x, (double)f.y};
+  }
+};
+
+// v16 = w * s  (basis normalisation, krylov.hpp:229-231, 298-300)
+template <class T>
+__global__ void __launch_bounds__(256) k_vscale16(size_t m, const T* w, T s, typename Store16<T>::type* v) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < m; i += (size_t)gridDim.x * blockDim.x)
+    v[i] = Store16<T>::put(xmul(ldg(w + i), s));
+}
+// conj(v16) . w  in fp64
+template <class T>
+__global__ void __launch_bounds__(256) k_dot16(size_t m, const typename Store16<T>::type* v, const T* w, RedSlot red) {
+  double acc[2] = {0.0, 0.0};
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < m; i += (size_t)gridDim.x * blockDim.x) {
+    const T a = Store16<T>::get(v[i]);
+    const T b = ldg(w + i);
+    if constexpr (is_cplx<T>) {
+      cdot_acc(acc, a, b);
+    } else {
+      acc[0] = __fma_rn((double)a, (double)b, acc[0]);
+    }
+  }
+  grid_reduce<2>(acc, red);
+}
+// w -= h * v16
+template <class T>
+__global__ void __launch_bounds__(256) k_vaxmy16(size_t m, T h, const typename Store16<T>::type* v, T* w) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < m; i += (size_t)gridDim.x * blockDim.x)
+    w[i] = xsub(w[i], xmul(h, Store16<T>::get(v[i])));
+}
+// xc += y_j * v16_j (one basis vector per launch)
+template <class T>
+__global__ void __launch_bounds__(256) k_axpy16(size_t m, T y, const typename Store16<T>::type* v, T* xc) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < m; i += (size_t)gridDim.x * blockDim.x)
+    xc[i] = xadd(xc[i], xmul(y, Store16<T>::get(v[i])));
+}
+
+template <class T>
+void basis16_scale(size_t m, const T* w, T s, void* v, cudaStream_t st) {
+  k_vscale16<T><<<grid_for(m, 256, 8), 256, 0, st>>>(m, w, s, (typename Store16<T>::type*)v);
+  LAUNCHED("basis16_scale");
+}
+template <class T>
+void basis16_dot(size_t m, const void* v, const T* w, const RedSlot& red, cudaStream_t st) {
+  k_dot16<T><<<grid_for(m, 256, 4), 256, 0, st>>>(m, (const typename Store16<T>::type*)v, w, red);
+  LAUNCHED("basis16_dot");
+}
+template <class T>
+void basis16_axmy(size_t m, T h, const void* v, T* w, cudaStream_t st) {
+  k_vaxmy16<T><<<grid_for(m, 256, 8), 256, 0, st>>>(m, h, (const typename Store16<T>::type*)v, w);
+  LAUNCHED("basis16_axmy");
+}
+template <class T>
+void basis16_axpy(size_t m, T y, const void* v, T* xc, cudaStream_t st) {
+  k_axpy16<T><<<grid_for(m, 256, 8), 256, 0, st>>>(m, y, (const typename Store16<T>::type*)v, xc);
+  LAUNCHED("basis16_axpy");
+}
+
+template <class S>
+__global__ void k_cast_storage(size_t m, const double* src, S* dst) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < m; i += (size_t)gridDim.x * blockDim.x) {
+    if constexpr (std::is_same_v<S, __half>)
+      dst[i] = __double2half(src[i]);
+    else
+      dst[i] = (S)src[i];
+  }
+}
+
+void cast_f64_to_storage(size_t m, const double* src, int storage, void* dst, cudaStream_t st) {
+  const unsigned g = grid_for(m, 256, 8);
+  switch (storage) {
+    case 4: k_cast_storage<__half><<<g, 256, 0, st>>>(m, src, (__half*)dst); break;
+    case 0: k_cast_storage<float><<<g, 256, 0, st>>>(m, src, (float*)dst); break;
+    default: k_cast_storage<double><<<g, 256, 0, st>>>(m, src, (double*)dst); break;
+  }
+  LAUNCHED("cast_storage");
+}
+
+#define INST_EXT(T)                                                                                      \
+  template void block_jacobi_apply<T>(int, int, int, const void*, const T*, T*, cudaStream_t);           \
+  template void csr_apply<T>(int, const int*, const int*, const void*, int, const T*, T*, cudaStream_t); \
+  template void basis16_scale<T>(size_t, const T*, T, void*, cudaStream_t);                              \
+  template void basis16_dot<T>(size_t, const void*, const T*, const RedSlot&, cudaStream_t);             \
+  template void basis16_axmy<T>(size_t, T, const void*, T*, cudaStream_t);                               \
+  template void basis16_axpy<T>(size_t, T, const void*, T*, cudaStream_t);
+
+INST_EXT(float)
+INST_EXT(double)
+INST_EXT(c32)
+INST_EXT(c64)
+
+}  // namespace mprkb

@@ -109,6 +109,12 @@ KrylovWork<T>::KrylovWork(size_t m) : red(2), m_(m) {
 }
 
 template <class T>
+void* KrylovWork<T>::basis16(int j) {
+  while ((int)basis16_.size() <= j) basis16_.emplace_back(m_ * (is_cplx<T> ? 4 : 2));
+  return basis16_[j].get();
+}
+
+template <class T>
 T* KrylovWork<T>::basis(int j) {
   while ((int)basis_.size() <= j) basis_.emplace_back(m_ * sizeof(T));
   return basis_[j].template as<T>();
@@ -230,7 +236,7 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
 // ---------------------------------------------------------------------------
 template <class T>
 void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, KrylovWork<T>& w,
-                 SolveReport& rep, cudaStream_t st, EventTimer* timer) {
+                 SolveReport& rep, cudaStream_t st, EventTimer* timer, int basis_storage) {
   using R = real_t<T>;
   using H = typename HostScalar<T>::type;
   const size_t m = w.size();
@@ -240,6 +246,8 @@ void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num,
   const bool fast = num == Numerics::Fast;
   const RedSlot s0 = w.red.slot(0);
   const int kmax = crit.max_iter;
+  const bool b16 = basis_storage == 4;
+  if (basis_storage != -1 && !b16) MPRKB_THROW(10, "gmres: basis storage must be the working precision or F16");
   T *t = w.v(0), *wv = w.v(1), *xc = w.v(2), *wt = w.v(3);
 
   auto fetch = [&]() -> R {
@@ -295,6 +303,16 @@ void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num,
     std::vector<H> sn(kmax, H{});
     std::vector<H> s(kmax + 1, H{});
     std::vector<T*> basis;
+    std::vector<void*> basis16;
+    auto push_basis = [&](int j, H scale) {  // basis_j = w * scale
+      if (b16) {
+        basis16.push_back(w.basis16(j));
+        basis16_scale<T>(m, wv, to_dev<T>(scale), basis16[j], st);
+      } else {
+        basis.push_back(w.basis(j));
+        vscale<T>(m, wv, to_dev<T>(scale), basis[j], st);
+      }
+    };
     s[0] = scast<H>(beta);
     bool x_built = false;
 
@@ -308,24 +326,45 @@ void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num,
       }
       std::vector<T> yd(cols);
       for (int j = 0; j < cols; ++j) yd[j] = to_dev<T>(y[j]);
-      candidate<T>(m, x, basis.data(), yd.data(), cols, dst, st);
+      if (b16) {
+        CUDA_CHECK(cudaMemcpyAsync(dst, x, m * sizeof(T), cudaMemcpyDeviceToDevice, st));
+        for (int j = 0; j < cols; ++j) basis16_axpy<T>(m, yd[j], basis16[j], dst, st);
+      } else {
+        candidate<T>(m, x, basis.data(), yd.data(), cols, dst, st);
+      }
     };
 
-    {
-      const H inv0 = scast<H>(1.0) / scast<H>(beta);
-      basis.push_back(w.basis(0));
-      vscale<T>(m, wv, to_dev<T>(inv0), basis[0], st);
-    }
+    push_basis(0, scast<H>(1.0) / scast<H>(beta));
 
     int k = 0;
     for (; k < kmax;) {
-      op(basis[k], t);
+      const T* vk;
+      if (b16) {  // the operator reads the basis vector widened to T (exact)
+        CUDA_CHECK(cudaMemsetAsync(wt, 0, m * sizeof(T), st));
+        basis16_axpy<T>(m, to_dev<T>(scast<H>(1.0)), basis16[k], wt, st);
+        vk = wt;
+      } else {
+        vk = basis[k];
+      }
+      op(vk, t);
       pre(t, wv);
       std::vector<H> h(k + 2, H{});
       for (int j = 0; j <= k; ++j) {  // modified Gram-Schmidt
-        const H hj = dotc(basis[j], wv);
-        h[j] = hj;
-        vaxmy<T>(m, to_dev<T>(hj), basis[j], wv, st);
+        H hj;
+        if (b16) {
+          basis16_dot<T>(m, basis16[j], wv, s0, st);
+          stream_sync(st);
+          if constexpr (is_cplx<T>)
+            hj = H((R)w.red.host(0)[0], (R)w.red.host(0)[1]);
+          else
+            hj = (R)w.red.host(0)[0];
+          h[j] = hj;
+          basis16_axmy<T>(m, to_dev<T>(hj), basis16[j], wv, st);
+        } else {
+          hj = dotc(basis[j], wv);
+          h[j] = hj;
+          vaxmy<T>(m, to_dev<T>(hj), basis[j], wv, st);
+        }
       }
       const R wnorm = norm2(wv);
       h[k + 1] = scast<H>(static_cast<double>(wnorm));
@@ -378,9 +417,7 @@ void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num,
         rep.history.back() = rt;
       }
       if (k == kmax) break;
-      const H inv = scast<H>(1.0) / scast<H>(static_cast<double>(wnorm));
-      basis.push_back(w.basis(k));
-      vscale<T>(m, wv, to_dev<T>(inv), basis[k], st);
+      push_basis(k, scast<H>(1.0) / scast<H>(static_cast<double>(wnorm)));
     }
     if (!rep.converged) rep.failure = 1;
     if (!x_built) {
@@ -402,13 +439,12 @@ template void cg_solve<float>(Op&, Op*, const float*, float*, const Crit&, Numer
                               SolveReport&, cudaStream_t, EventTimer*);
 template void cg_solve<double>(Op&, Op*, const double*, double*, const Crit&, Numerics, KrylovWork<double>&,
                                SolveReport&, cudaStream_t, EventTimer*);
-template void gmres_solve<float>(Op&, Op*, const float*, float*, const Crit&, Numerics, KrylovWork<float>&,
-                                 SolveReport&, cudaStream_t, EventTimer*);
-template void gmres_solve<double>(Op&, Op*, const double*, double*, const Crit&, Numerics,
-                                  KrylovWork<double>&, SolveReport&, cudaStream_t, EventTimer*);
-template void gmres_solve<c32>(Op&, Op*, const c32*, c32*, const Crit&, Numerics, KrylovWork<c32>&,
-                               SolveReport&, cudaStream_t, EventTimer*);
-template void gmres_solve<c64>(Op&, Op*, const c64*, c64*, const Crit&, Numerics, KrylovWork<c64>&,
-                               SolveReport&, cudaStream_t, EventTimer*);
+#define INST_GMRES(T)                                                                                      \
+  template void gmres_solve<T>(Op&, Op*, const T*, T*, const Crit&, Numerics, KrylovWork<T>&, SolveReport&, \
+                               cudaStream_t, EventTimer*, int);
+INST_GMRES(float)
+INST_GMRES(double)
+INST_GMRES(c32)
+INST_GMRES(c64)
 
 }  // namespace mprkb

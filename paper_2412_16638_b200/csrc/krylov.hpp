@@ -67,21 +67,24 @@ class KrylovWork {
   explicit KrylovWork(size_t m);
   T* v(int i) { return vecs_[i].template as<T>(); }
   T* basis(int j);
+  void* basis16(int j);  // fp16 storage (2 x fp16 for complex)
   size_t size() const { return m_; }
   Reducer red;
 
  private:
   size_t m_;
   DevBuf vecs_[4];
-  std::vector<DevBuf> basis_;
+  std::vector<DevBuf> basis_, basis16_;
 };
 
 template <class T>
 void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, KrylovWork<T>& w,
               SolveReport& rep, cudaStream_t st, EventTimer* timer = nullptr);
 
+// basis_storage: -1 = the working precision T (the reference), 4 = fp16
+// Krylov basis (accessor-style storage, fp64-accumulated dots; extension).
 template <class T>
 void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, KrylovWork<T>& w,
-                 SolveReport& rep, cudaStream_t st, EventTimer* timer = nullptr);
+                 SolveReport& rep, cudaStream_t st, EventTimer* timer = nullptr, int basis_storage = -1);
 
 }  // namespace mprkb

@@ -63,6 +63,28 @@ void pack_tf32_split(int n, const float* q, float* hi_packed, float* lo_packed);
 template <class T>
 void pd_inv_device(int n, const T* la, const T* lb, const T* lc, T* pd, int* zero_flag, cudaStream_t st);
 
+// ---- north-star extensions (ext.cu) ---------------------------------------------------
+// storage codes: 0 fp32, 1 fp64, 4 fp16
+template <class T>
+void block_jacobi_apply(int n, int b, int storage, const void* inv, const T* r, T* z, cudaStream_t st);
+// per-block inverse storage from the two distinct fp64 block inverses
+// (column-major b x b full blocks, n % b tail blocks)
+void block_jacobi_fill(int n, int b, int storage, const double* full_dev, const double* tail_dev, void* inv,
+                       cudaStream_t st);
+template <class T>
+void csr_apply(int rows, const int* rp, const int* cols, const void* vals, int storage, const T* x, T* y,
+               cudaStream_t st);
+// GMRES basis kept in fp16 (real) / 2 x fp16 (complex); dots fp64-accumulated
+template <class T>
+void basis16_scale(size_t m, const T* w, T s, void* v, cudaStream_t st);
+template <class T>
+void basis16_dot(size_t m, const void* v, const T* w, const RedSlot& red, cudaStream_t st);
+template <class T>
+void basis16_axmy(size_t m, T h, const void* v, T* w, cudaStream_t st);
+template <class T>
+void basis16_axpy(size_t m, T y, const void* v, T* xc, cudaStream_t st);
+void cast_f64_to_storage(size_t m, const double* src, int storage, void* dst, cudaStream_t st);
+
 // ---- reductions (krylov.hpp:43-71) --------------------------------------------------
 // dot_real(a, b): FAST -> fp64 tree into red.out[0]; PARITY -> sequential in real_t<T>
 template <class T>

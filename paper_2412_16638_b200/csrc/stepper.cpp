@@ -182,10 +182,10 @@ void Stepper::step(double* u, StepTrace& trace) {
           cg_solve<double>(*S.op, S.pre.get(), bsol_.as<double>(), xsol_.as<double>(), crit, cfg_.num, *w64_, rep, st_, tm);
           break;
         case 2:
-          gmres_solve<c32>(*S.op, S.pre.get(), bsol_.as<c32>(), xsol_.as<c32>(), crit, cfg_.num, *wc32_, rep, st_, tm);
+          gmres_solve<c32>(*S.op, S.pre.get(), bsol_.as<c32>(), xsol_.as<c32>(), crit, cfg_.num, *wc32_, rep, st_, tm, cfg_.basis_storage);
           break;
         default:
-          gmres_solve<c64>(*S.op, S.pre.get(), bsol_.as<c64>(), xsol_.as<c64>(), crit, cfg_.num, *wc64_, rep, st_, tm);
+          gmres_solve<c64>(*S.op, S.pre.get(), bsol_.as<c64>(), xsol_.as<c64>(), crit, cfg_.num, *wc64_, rep, st_, tm, cfg_.basis_storage);
           break;
       }
       // The stage vector y is the solver's iterate: heat stages read it in

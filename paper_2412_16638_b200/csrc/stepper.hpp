@@ -25,6 +25,7 @@ struct StepperConfig {
   int block_storage = -1;
   double nu = 0.0;
   bool timings = false;
+  int basis_storage = -1;  // GMRES basis storage (-1: working precision; 4: fp16)
 };
 
 struct StepTrace {
