@@ -39,6 +39,21 @@ def mp():
 
 
 @pytest.fixture(scope="session")
+def dropin_exe(tmp_path_factory, mp):
+    """tests/cpp/dropin_example.cpp built against include/mprk_b200.hpp and
+    linked to libmprk_b200.so (the C++ drop-in boundary)."""
+    import subprocess
+
+    exe = tmp_path_factory.mktemp("dropin") / "dropin"
+    libdir = os.path.join(ROOT, "paper_2412_16638_b200")
+    r = subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "tests", "cpp", "dropin_example.cpp"), "-o", str(exe),
+                        "-L", libdir, "-lmprk_b200", "-Wl,-rpath," + libdir], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    return exe
+
+
+@pytest.fixture(scope="session")
 def gpu(mp):
     # -m gpu runs on the B200 box: a missing device is a failure, not a skip
     assert mp.device_count() >= 1, "no CUDA device visible to libmprk_b200.so"

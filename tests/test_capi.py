@@ -76,3 +76,9 @@ def test_argument_errors_map_like_the_reference(mp):
     with pytest.raises(mp.MprkError):
         mp.builtin("4s3pD")
     assert issubclass(mp.DimensionTooSmall, mp.MprkError)
+
+
+def test_cpp_dropin_header_builds_and_links(dropin_exe):
+    """include/mprk_b200.hpp (the C++ drop-in for mprk::Stepper / integrate)
+    compiles against the C-ABI and links against libmprk_b200.so."""
+    assert dropin_exe.exists()

@@ -278,3 +278,17 @@ def test_solve_counts_and_precision_policy(gpu, mp):
         t = mp.midpoint_corrected(int(name[8:])) if name.startswith("midpoint") else mp.builtin(name)
         st = mp.Stepper("heat", 4, t, 0.01)
         assert len(st.step(st.initial_state())["iterations"]) == want
+
+
+def test_cpp_dropin_matches_reference(gpu, mp, ref, dropin_exe):
+    """The C++ drop-in (include/mprk_b200.hpp) reproduces the reference's
+    integrate() bit for bit with PARITY numerics (heat 16^3, 4s3pB, fp32)."""
+    import subprocess
+
+    out = subprocess.run([str(dropin_exe), "16", "parity"], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    first = out.stdout.split("\n")[0].split()
+    mean_it, emax, el2 = float(first[0]), float(first[1]), float(first[2])
+    want = ref.integrate(0, 16, tabd(mp.builtin("4s3pB")), 1.0 / 40.0, 0.1, 1e-4, "f32")
+    assert (mean_it, emax, el2) == (want["mean_iterations"], want["error_max"], want["error_l2"])
+    assert "solves 4" in out.stdout
