@@ -73,55 +73,57 @@ def dist_env():
 # clocks sampling during the timed region
 # ---------------------------------------------------------------------------------
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + throttle reasons sampled DURING the timed region: an NVML
+    poll every 2 ms on a side thread (nvidia-smi -lms cannot start inside a
+    sub-second timed region)."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
-        self.proc = None
-        self.lines = []
+        self.samples = []
+        self.err = None
+        self.run = False
         self.t = None
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
-        except (FileNotFoundError, OSError):
-            self.proc = None
+            import pynvml
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.idx)
+            self.smax = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # noqa: BLE001 - reported in the JSON line
+            self.err = f"nvml unavailable: {e}"
+            return
+        self.run = True
+        self.t = threading.Thread(target=self._poll, daemon=True)
+        self.t.start()
+        time.sleep(0.005)
+
+    def _poll(self):
+        nv = self.nv
+        while self.run:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((sm, rs))
+            except Exception as e:  # noqa: BLE001
+                self.err = str(e)
+                return
+            time.sleep(0.002)
 
     def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        if self.t:
-            self.t.join(timeout=2)
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                smax.append(float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[2:6]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        if self.t is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err or "not sampled"], "samples": 0}
+        self.run = False
+        self.t.join(timeout=2)
+        reasons = sorted(nm for nm, bit in self.REASONS.items() if any(rs & bit for _, rs in self.samples))
+        sm = [s for s, _ in self.samples]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(self.smax),
+                "reasons": reasons, "samples": len(sm), "source": "NVML every 2 ms during the timed region"}
 
 
 # ---------------------------------------------------------------------------------
@@ -188,8 +190,8 @@ def run_reference_arm(args):
 # ---------------------------------------------------------------------------------
 def load_traffic():
     """dram bytes per launch of the dominant kernel from the committed ncu
-    capture (profiles/ncu_summary_r01.json), if present."""
-    p = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+    capture (profiles/ncu_summary.json), if present."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
             d = json.load(f)
@@ -292,16 +294,23 @@ def run_cuda_arm(args):
 
     line = None
     if rank == 0:
-        # ---- roofline of the dominant kernel: the FastDiag contraction
-        # (CUDA-core FP32 FMA bound; 2 n^4 flop per launch = n^3 outputs x n MACs)
+        # ---- roofline of the dominant kernel: the FastDiag contraction on the
+        # tensor cores (3xTF32, tensor_tc.cu).  Algorithmic work = one fp32
+        # GEMM, 2 n^4 flop per launch (n^3 outputs x n MACs); the 3xTF32 split
+        # issues three TF32 MMAs per algorithmic MAC, so the fp32-accurate
+        # ceiling is the dense TF32 peak / 3 (TF32 dense = bf16 dense / 2).
         ms_launch = measure_contraction(mp, torch, st.stream)
         flops = 2.0 * n ** 4
         achieved = flops / (ms_launch * 1e-3) / 1e12
-        peak = mp_fma_peak(mp, 0)
+        peaks = load_peaks()
+        tf32 = peaks["bf16_tflops"] / 2.0
+        peak = tf32 / 3.0
+        # bytes the contraction must move: x in + out (fp32), + pd on the
+        # diagonal-fused launch (1 of 6): 8N x 6 + 4N per apply
+        bytes_launch = (8.0 * m * 6 + 4.0 * m) / 6.0
         # ---- HBM-bound companion: the fp64 stencil (K1), 2*8*N bytes per launch
         ms_sten = measure_stencil(mp, torch, st.stream)
         gbs = 16.0 * m / (ms_sten * 1e-3) / 1e9
-        peaks = load_peaks()
         line = {
             "metric": METRIC, "value": value, "unit": "DOF-updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "steps_per_s": 1e3 / ms_step,
@@ -312,10 +321,17 @@ def run_cuda_arm(args):
             "e2e": {"value": e2e_value, "unit": "DOF-updates/s", "h2d_bytes_per_step": 8 * m,
                     "d2h_bytes_per_step": 8 * m, "steps": e2e_steps,
                     "note": "Stepper.step(host pinned f64 state) through the C-ABI, wall clock"},
-            "roofline": {"kernel": "k_tensor (FastDiag contraction, fp32 FFMA)", "bound": "compute",
-                         "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
-                         "peak_source": "measured FP32 FMA peak (mprkb_measure_fma_peak, this run)",
-                         "flop_per_launch": flops, "ms_per_launch": ms_launch, "traffic": load_traffic()},
+            "roofline": {"kernel": "k_tensor_tc (FastDiag contraction, tcgen05 3xTF32, fp32 accumulate in TMEM)",
+                         "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                         "frac": achieved / peak,
+                         "peak_source": (f"{peaks['src_tc']}: dense TF32 = bf16 {peaks['bf16_tflops']:.0f} / 2 = "
+                                         f"{tf32:.0f} TFLOP/s, / 3 MMAs per fp32 MAC (3xTF32)"),
+                         "flop_per_launch": flops, "ms_per_launch": ms_launch,
+                         "executed_tf32_tflops": 3 * achieved,
+                         "hbm_gbs": bytes_launch / (ms_launch * 1e-3) / 1e9,
+                         "hbm_frac": bytes_launch / (ms_launch * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                         "traffic": load_traffic(),
+                         "traffic_note": "ncu --set full dram read+write of one launch (profiles/ncu_summary.json)"},
             "roofline_hbm": {"kernel": "k_stencil (fp64 7-point)", "bound": "hbm", "achieved": gbs,
                              "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"],
                              "peak_source": peaks["src"], "bytes_per_launch": 16.0 * m, "ms_per_launch": ms_sten},
@@ -366,18 +382,22 @@ def measure_stencil(mp, torch, stream_ptr, reps=20):
 
 
 def load_peaks():
+    out = {"hbm_gbs": 6650.0, "src": "B200_PROFILING.md fallback", "bf16_tflops": 2250.0,
+           "src_tc": "nominal bf16 dense (no MEASURED_PEAKS.json)"}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
-        return {"hbm_gbs": float(d["hbm_gbs"]), "src": "MEASURED_PEAKS.json hbm_gbs (measured copy)"}
+        out.update(hbm_gbs=float(d["hbm_gbs"]), src="MEASURED_PEAKS.json hbm_gbs (measured copy)")
+        out.update(bf16_tflops=float(d["bf16_tflops"]), src_tc="MEASURED_PEAKS.json bf16_tflops (burst)")
     except (OSError, ValueError, KeyError):
-        return {"hbm_gbs": 6650.0, "src": "B200_PROFILING.md fallback"}
+        pass
+    return out
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
