@@ -22,8 +22,15 @@ Arms
                     same workload, bounded sample of steps.
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
-Multi-GPU: launched under torch.distributed.run, one rank per GPU; every rank
-steps its own 256^3 grid (replicas, weak scaling), timing = max over ranks.
+Multi-GPU (--gpus N > 1, under torch.distributed.run, one rank per GPU):
+configs[2] — ONE 512^3 grid slab-decomposed across the N GPUs (rank r owns
+k-planes [r 512/N, (r+1) 512/N)), ghost planes exchanged with the
+k-neighbours before every stencil, FastDiag transposed k-slab <-> j-slab by
+an all-to-all around its contraction along k, Krylov dots summed across
+ranks — all over NCCL (libmprk_b200's own communicator; torch.distributed
+only broadcasts the NCCL id and takes the max-over-ranks time).  Fixed total
+work as N grows ("scaling": "strong"); at N = 8 each GPU holds 512*512*64 =
+256^3 DOF, the N = 1 line's per-GPU size.
 """
 from __future__ import annotations
 
@@ -43,6 +50,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "RK time-steps/s & DOF-updates/s, 3D heat 256³–512³ mixed DIRK; SpMV HBM GB/s"
 N_GRID = 256
+N_SPLIT = 512  # configs[2]: the grid split across N > 1 GPUs
 METHOD = "4s3pB"
 TAU = 0.01
 TOL = 1e-3
@@ -50,15 +58,21 @@ PREC = "f32"
 MAX_ITER = 40
 
 
+def grid_for_world(n_gpus: int) -> int:
+    return N_GRID if n_gpus == 1 else N_SPLIT
+
+
 def workload_config(n_gpus: int) -> dict:
+    n = grid_for_world(n_gpus)
     return {
-        "workload": f"heat {N_GRID}^3, {METHOD} (4-stage mixed DIRK: fp32 implicit CG + FastDiag, "
-                    f"fp64 explicit couplings/state), tau={TAU}, tol={TOL}",
-        "n": N_GRID, "dof": N_GRID ** 3, "method": METHOD, "implicit_precision": PREC,
+        "workload": f"heat {n}^3, {METHOD} (4-stage mixed DIRK: fp32 implicit CG + FastDiag, "
+                    f"fp64 explicit couplings/state), tau={TAU}, tol={TOL}"
+                    + ("" if n_gpus == 1 else f", k-slab decomposed over {n_gpus} GPUs (NCCL)"),
+        "n": n, "dof": n ** 3, "dof_per_gpu": n ** 3 // n_gpus, "method": METHOD, "implicit_precision": PREC,
         "preconditioner": "fastdiag", "tau": TAU, "tol": TOL, "max_iter": MAX_ITER,
         "state": "resident in HBM (f64)",
-        "l2": "no flush: one step streams ~3.5 GB through HBM (state alone 134 MB > 126 MB L2)",
-        "parallelism": "single" if n_gpus == 1 else f"replicas x{n_gpus}",
+        "l2": "no flush: one step streams >= 3.5 GB per GPU through HBM (state slab alone 134 MB > 126 MB L2)",
+        "parallelism": "single" if n_gpus == 1 else f"slab{n_gpus} (k-planes; halo + all-to-all + dot allreduce)",
     }
 
 
@@ -171,11 +185,19 @@ def run_reference_arm(args):
     value = N_GRID ** 3 / per_step
     sample = (f"{len(times)} of {args.steps} requested steps of the same workload "
               f"(+{len(warm)} warm-up), wall clock, {threads} OpenMP threads")
+    if world > 1:
+        # one 512^3 reference step takes minutes on the host (FastDiag is
+        # 12 n flop/DOF, 16x the 256^3 cost): the sample is the 256^3 step,
+        # whose DOF-updates/s bounds the 512^3 rate from above
+        sample = (f"{len(times)} step(s) of heat {N_GRID}^3 {METHOD} on {threads} OpenMP threads "
+                  f"(upper bound on the reference's {N_SPLIT}^3 DOF-updates/s; no multi-node/GPU path "
+                  f"exists in the reference)")
     line = {
         "metric": METRIC, "value": value, "unit": "DOF-updates/s", "n_gpus": args.gpus, "steps": len(times),
         "warmup": len(warm), "ms_per_step": per_step * 1e3, "steps_per_s": 1.0 / per_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64", "data": "synthetic",
-        "config": workload_config(1), "impl": "reference",
+        "higher_is_better": True, "scaling": "weak" if world == 1 else "strong", "vs_baseline": None,
+        "dtype": "f32/f64", "data": "synthetic",
+        "config": workload_config(world), "impl": "reference",
         "cpu_baseline": {"value": value, "unit": "DOF-updates/s", "cores": threads, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": "DOF-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -235,12 +257,20 @@ def run_cuda_arm(args):
         torch.cuda.set_device(0)
     import paper_2412_16638_b200 as mp
 
-    n = N_GRID
-    m = n ** 3
+    n = grid_for_world(world)
+    m = n ** 3  # DOF of the whole (possibly split) grid
     tab = mp.builtin(METHOD)
-    st = mp.Stepper("heat", n, tab, TAU, TOL, PREC, MAX_ITER)
+    comm = None
+    if world > 1:
+        # libmprk_b200's own NCCL communicator; torch.distributed only ships the id
+        mp.set_device(local)
+        obj = [mp.Comm.nccl_unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(obj, src=0)
+        comm = mp.Comm.nccl(rank, world, obj[0])
+    st = mp.Stepper("heat", n, tab, TAU, TOL, PREC, MAX_ITER, comm=comm)
     stream = torch.cuda.ExternalStream(st.stream)
-    u = torch.from_numpy(st.initial_state()).cuda()
+    u = torch.from_numpy(st.initial_state()).cuda()  # this rank's slab
+    m_local = st.size
     torch.cuda.synchronize()
 
     def barrier():
@@ -273,7 +303,7 @@ def run_cuda_arm(args):
         torch.distributed.all_reduce(t_local, op=torch.distributed.ReduceOp.MAX)
     ms_total = t_local.item()
     ms_step = ms_total / args.steps
-    value = world * m * args.steps / (ms_total * 1e-3)
+    value = m * args.steps / (ms_total * 1e-3)
 
     # ---- e2e: the public C-ABI call with a HOST (pinned) state buffer, H2D +
     # D2H inside the timed region every step
@@ -290,7 +320,7 @@ def run_cuda_arm(args):
     te = torch.tensor([t_e2e], dtype=torch.float64, device="cuda")
     if world > 1:
         torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
-    e2e_value = world * m * e2e_steps / te.item()
+    e2e_value = m * e2e_steps / te.item()
 
     line = None
     if rank == 0:
@@ -314,12 +344,13 @@ def run_cuda_arm(args):
         line = {
             "metric": METRIC, "value": value, "unit": "DOF-updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "steps_per_s": 1e3 / ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64",
+            "higher_is_better": True, "scaling": "weak" if world == 1 else "strong", "vs_baseline": None,
+            "dtype": "f32/f64",
             "data": "synthetic (make_problem: u0 = 0, g = sin sin sin)", "config": workload_config(world),
             "iterations_per_solve": sorted(set(i for it in iters for i in it)),
             "gpu_launches": launches,
-            "e2e": {"value": e2e_value, "unit": "DOF-updates/s", "h2d_bytes_per_step": 8 * m,
-                    "d2h_bytes_per_step": 8 * m, "steps": e2e_steps,
+            "e2e": {"value": e2e_value, "unit": "DOF-updates/s", "h2d_bytes_per_step": 8 * m_local * world,
+                    "d2h_bytes_per_step": 8 * m_local * world, "steps": e2e_steps,
                     "note": "Stepper.step(host pinned f64 state) through the C-ABI, wall clock"},
             "roofline": {"kernel": "k_tensor_tc (FastDiag contraction, tcgen05 3xTF32, fp32 accumulate in TMEM)",
                          "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

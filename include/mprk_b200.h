@@ -249,6 +249,44 @@ int mprkb_integrate(const mprkb_config* cfg, const double* reference_host, size_
 int mprkb_stepper_integrate(mprkb_stepper* s, const double* reference_host, size_t reference_len,
                             double* state_host, mprkb_result* result);
 
+/* ---- split grid: k-slab decomposition across ranks ----------
+ * Rank r of P owns k-planes [r n/P, (r+1) n/P): the contiguous slice
+ * [r n^3/P, (r+1) n^3/P) of the x-fastest state vector.  Stencils exchange
+ * one ghost plane with each k-neighbour (a ring for the periodic advection
+ * grid), FastDiag transposes k-slab <-> j-slab by an all-to-all around its
+ * contraction along k, and every Krylov dot/norm is completed across ranks
+ * (FAST: fp64 partials summed in rank order; PARITY: the reference's
+ * sequential accumulator continued rank after rank -> bitwise equal to the
+ * undivided grid).  The reference has no decomposition; its single-domain
+ * Stepper (stepper.hpp:53-65) is what a split run must reproduce. */
+typedef struct mprkb_comm mprkb_comm;
+typedef struct mprkb_comm_group mprkb_comm_group;
+
+/* Select the CUDA device of the calling thread (one process / thread per GPU). */
+int mprkb_set_device(int device);
+/* Slab of `rank` in a P-way split of an n-grid (host only, no device needed). */
+int mprkb_slab_plan(int n, int size, int rank, int* k0, int* nz, int* j0, int* ny);
+/* NCCL backend (one process per GPU): rank 0 draws the 128-byte id and the
+ * host side (e.g. torch.distributed) broadcasts it; every rank then creates
+ * its communicator on its current device. */
+int mprkb_nccl_unique_id(unsigned char* id);
+int mprkb_comm_create_nccl(int rank, int size, const unsigned char* id, mprkb_comm** out);
+/* In-process backend: `size` ranks as threads of one process sharing one
+ * device (runs every split code path on a single GPU).  Create the group
+ * once, then one communicator per rank thread. */
+int mprkb_comm_group_create(int size, mprkb_comm_group** out);
+int mprkb_comm_create_local(mprkb_comm_group* g, int rank, mprkb_comm** out);
+void mprkb_comm_group_destroy(mprkb_comm_group* g);
+void mprkb_comm_destroy(mprkb_comm* c);
+/* v[i] <- sum over ranks (added in rank order); collective. */
+int mprkb_comm_allreduce_sum(mprkb_comm* c, double* v, int count);
+/* Stepper on this rank's slab; `comm` must outlive the stepper (NULL = the
+ * undivided grid, same as mprkb_stepper_create).  Every rank calls every
+ * stepper entry point collectively; state buffers (step, initial_state,
+ * integrate) hold the local slab only. */
+int mprkb_stepper_create_split(const mprkb_config* cfg, mprkb_comm* comm, mprkb_stepper** out);
+int mprkb_stepper_slab(mprkb_stepper* s, int* k0, int* nz, size_t* local_size);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,7 +28,7 @@ __all__ = [
     "WrongEquation", "NonFiniteState", "CudaError", "NoDevice",
     "Tableau", "builtin", "midpoint_corrected", "validate", "integrate", "make_problem", "heat_exact",
     "Stepper", "Operator", "stencil_apply", "tensor_apply", "dot", "cg", "gmres", "kernel_launches",
-    "device_count",
+    "device_count", "Comm", "LocalGroup", "slab_plan", "run_ranks", "set_device",
 ]
 
 
@@ -179,23 +179,35 @@ class Stepper:
     ``step(u)`` takes a numpy float64 vector (host, updated in place, copied
     in/out each call); ``step_device(u)`` a torch CUDA float64 tensor that
     stays resident in HBM.
+
+    With ``comm`` (a :class:`Comm`) the grid is split into k-slabs across the
+    communicator's ranks: every vector argument is this rank's slab
+    (``size`` = n*n*nz elements starting at plane ``k0``) and all ranks must
+    call every method together.
     """
 
     def __init__(self, equation: str, n: int, tableau: Tableau, tau: float, tol: float = 1e-6,
                  precision: str = "f64", max_iter: int = 40, *, t_end: float = 0.1, numerics: str = "fast",
                  preconditioner: str = "fastdiag", block_size: int = 8, block_storage: Optional[str] = None,
-                 nu: float = 0.0, timings: bool = False, basis_storage: Optional[str] = None):
+                 nu: float = 0.0, timings: bool = False, basis_storage: Optional[str] = None,
+                 comm: Optional["Comm"] = None):
         cfg, keep = _config(tableau, equation, n, tau, t_end, tol, precision, max_iter, numerics,
                             preconditioner, block_size, block_storage, nu, timings, basis_storage)
         self._h = C.c_void_p()
-        check(_c.lib.mprkb_stepper_create(C.byref(cfg), C.byref(self._h)))
+        self._comm = comm  # keeps the communicator alive as long as the stepper
+        if comm is None:
+            check(_c.lib.mprkb_stepper_create(C.byref(cfg), C.byref(self._h)))
+        else:
+            check(_c.lib.mprkb_stepper_create_split(C.byref(cfg), comm._h, C.byref(self._h)))
         self.n = int(n)
-        self.size = self.n ** 3
+        k0, nz, m = C.c_int(), C.c_int(), C.c_size_t()
+        check(_c.lib.mprkb_stepper_slab(self._h, C.byref(k0), C.byref(nz), C.byref(m)))
+        self.k0, self.nz, self.size = k0.value, nz.value, m.value
         self._trace = _c.StepTrace()
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _c is not None and _c.lib is not None:  # (module globals are gone at shutdown)
             _c.lib.mprkb_stepper_destroy(h)
             self._h = None
 
@@ -217,7 +229,7 @@ class Stepper:
 
     def step(self, u: np.ndarray) -> dict:
         if u.dtype != np.float64 or not u.flags.c_contiguous or u.size != self.size:
-            raise LengthMismatch("step: u must be a contiguous float64 vector of length n^3")
+            raise LengthMismatch("step: u must be a contiguous float64 vector of length n^3 (split: the slab)")
         check(_c.lib.mprkb_stepper_step(self._h, _dp(u), C.byref(self._trace)))
         return self._trace_dict()
 
@@ -254,6 +266,106 @@ class Stepper:
         check(_c.lib.mprkb_stepper_integrate(self._h, None if ref is None else _dp(ref),
                                              0 if ref is None else ref.size, _dp(state), C.byref(res)))
         return _result_dict(res, its, state)
+
+
+# ---- split grid: communicators ----------------------------------------------------------
+def set_device(device: int) -> None:
+    """cudaSetDevice for the calling thread inside libmprk_b200."""
+    check(_c.lib.mprkb_set_device(int(device)))
+
+
+def slab_plan(n: int, size: int, rank: int) -> dict:
+    """k-slab (state) and j-slab (FastDiag transpose) of `rank` in a `size`-way split."""
+    k0, nz, j0, ny = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+    check(_c.lib.mprkb_slab_plan(int(n), int(size), int(rank), C.byref(k0), C.byref(nz), C.byref(j0),
+                                 C.byref(ny)))
+    return dict(k0=k0.value, nz=nz.value, j0=j0.value, ny=ny.value)
+
+
+class Comm:
+    """One rank's communicator: NCCL (one process per GPU) or the in-process
+    group (ranks = threads sharing one GPU)."""
+
+    def __init__(self, handle, rank: int, size: int, keep=None):
+        self._h = handle
+        self.rank, self.size = rank, size
+        self._keep = keep
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(_c.lib.mprkb_nccl_unique_id(buf))
+        return buf.raw
+
+    @classmethod
+    def nccl(cls, rank: int, size: int, unique_id: bytes) -> "Comm":
+        h = C.c_void_p()
+        check(_c.lib.mprkb_comm_create_nccl(int(rank), int(size), C.c_char_p(bytes(unique_id)), C.byref(h)))
+        return cls(h, rank, size)
+
+    def allreduce_sum(self, values) -> np.ndarray:
+        v = np.ascontiguousarray(values, dtype=np.float64).copy()
+        check(_c.lib.mprkb_comm_allreduce_sum(self._h, v.ctypes.data_as(C.POINTER(C.c_double)), v.size))
+        return v
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _c is not None and _c.lib is not None:  # (module globals are gone at shutdown)
+            _c.lib.mprkb_comm_destroy(h)
+            self._h = None
+
+
+class LocalGroup:
+    """`size` ranks in this process on one device (every split code path on a
+    single GPU); ``comm(rank)`` is called from that rank's thread."""
+
+    def __init__(self, size: int):
+        self._h = C.c_void_p()
+        check(_c.lib.mprkb_comm_group_create(int(size), C.byref(self._h)))
+        self.size = int(size)
+
+    def comm(self, rank: int) -> Comm:
+        h = C.c_void_p()
+        check(_c.lib.mprkb_comm_create_local(self._h, int(rank), C.byref(h)))
+        return Comm(h, rank, self.size, keep=self)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and _c is not None and _c.lib is not None:  # (module globals are gone at shutdown)
+            _c.lib.mprkb_comm_group_destroy(h)
+            self._h = None
+
+
+def run_ranks(size: int, fn, device: int = 0) -> list:
+    """Run fn(rank, comm) for `size` in-process ranks (one thread each, all on
+    `device`) and return the results in rank order; re-raises the first
+    rank's exception."""
+    import threading
+
+    group = LocalGroup(size)
+    out = [None] * size
+    errs = [None] * size
+
+    def body(r):
+        try:
+            set_device(device)
+            comm = group.comm(r)
+            try:
+                out[r] = fn(r, comm)
+            finally:
+                del comm
+        except BaseException as e:  # noqa: BLE001 - re-raised below
+            errs[r] = e
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(size)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for e in errs:
+        if e is not None:
+            raise e
+    return out
 
 
 def _result_dict(res, its, state):
@@ -360,7 +472,7 @@ class Operator:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and _c is not None and _c.lib is not None:  # (module globals are gone at shutdown)
             _c.lib.mprkb_op_destroy(h)
             self._h = None
 

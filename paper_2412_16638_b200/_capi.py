@@ -166,6 +166,18 @@ SIGNATURES = {
     "mprkb_stepper_destroy": (None, [vp]),
     "mprkb_integrate": (i32, [C.POINTER(Config), vp, sz, vp, C.POINTER(Result)]),
     "mprkb_stepper_integrate": (i32, [vp, vp, sz, vp, C.POINTER(Result)]),
+    # split grid (k-slab decomposition)
+    "mprkb_set_device": (i32, [i32]),
+    "mprkb_slab_plan": (i32, [i32, i32, i32, ip, ip, ip, ip]),
+    "mprkb_nccl_unique_id": (i32, [C.c_char_p]),
+    "mprkb_comm_create_nccl": (i32, [i32, i32, C.c_char_p, C.POINTER(vp)]),
+    "mprkb_comm_group_create": (i32, [i32, C.POINTER(vp)]),
+    "mprkb_comm_create_local": (i32, [vp, i32, C.POINTER(vp)]),
+    "mprkb_comm_group_destroy": (None, [vp]),
+    "mprkb_comm_destroy": (None, [vp]),
+    "mprkb_comm_allreduce_sum": (i32, [vp, dptr, i32]),
+    "mprkb_stepper_create_split": (i32, [C.POINTER(Config), vp, C.POINTER(vp)]),
+    "mprkb_stepper_slab": (i32, [vp, ip, ip, C.POINTER(sz)]),
 }
 
 for _name, (_res, _args) in SIGNATURES.items():

@@ -78,11 +78,13 @@ __device__ __forceinline__ R term_real(cplx<R> a, cplx<R> b) {
   return xadd(xmul(a.re, b.re), xmul(a.im, b.im));
 }
 
+// init: the running sum a split grid's previous rank handed over (0 on an
+// undivided grid) — rank r continues the reference's global index order.
 template <class T>
-__global__ void __launch_bounds__(256) k_dot_seq(size_t m, const T* a, const T* b, double* out) {
+__global__ void __launch_bounds__(256) k_dot_seq(size_t m, const T* a, const T* b, double init, double* out) {
   using R = real_t<T>;
   __shared__ R buf[SEQ_CHUNK];
-  R acc = R(0);
+  R acc = (R)init;
   for (size_t base = 0; base < m; base += SEQ_CHUNK) {
     const int cnt = (int)min((size_t)SEQ_CHUNK, m - base);
     for (int t = threadIdx.x; t < cnt; t += blockDim.x) buf[t] = term_real(ldg(a + base + t), ldg(b + base + t));
@@ -99,10 +101,11 @@ __global__ void __launch_bounds__(256) k_dot_seq(size_t m, const T* a, const T* 
 
 // acc += conj(a_i) * b_i, complex accumulator
 template <class R>
-__global__ void __launch_bounds__(256) k_cdot_seq(size_t m, const cplx<R>* a, const cplx<R>* b, double* out) {
+__global__ void __launch_bounds__(256) k_cdot_seq(size_t m, const cplx<R>* a, const cplx<R>* b, double init_re,
+                                                  double init_im, double* out) {
   constexpr int CH = SEQ_CHUNK / 2;
   __shared__ cplx<R> buf[CH];
-  cplx<R> acc{R(0), R(0)};
+  cplx<R> acc{(R)init_re, (R)init_im};
   for (size_t base = 0; base < m; base += CH) {
     const int cnt = (int)min((size_t)CH, m - base);
     for (int t = threadIdx.x; t < cnt; t += blockDim.x) {
@@ -122,24 +125,26 @@ __global__ void __launch_bounds__(256) k_cdot_seq(size_t m, const cplx<R>* a, co
 }
 
 template <class T>
-void dot_real(size_t m, const T* a, const T* b, const RedSlot& red, Numerics num, cudaStream_t st) {
+void dot_real(size_t m, const T* a, const T* b, const RedSlot& red, Numerics num, cudaStream_t st,
+              const double* init) {
   if (num == Numerics::Parity)
-    k_dot_seq<T><<<1, 256, 0, st>>>(m, a, b, red.out);
+    k_dot_seq<T><<<1, 256, 0, st>>>(m, a, b, init ? init[0] : 0.0, red.out);
   else
     k_dot_fast<T><<<wave(m), kBlock, 0, st>>>(m, a, b, red);
   LAUNCHED("dot");
 }
 
 template <class T>
-void dot_conj(size_t m, const T* a, const T* b, const RedSlot& red, Numerics num, cudaStream_t st) {
+void dot_conj(size_t m, const T* a, const T* b, const RedSlot& red, Numerics num, cudaStream_t st,
+              const double* init) {
   if constexpr (is_cplx<T>) {
     if (num == Numerics::Parity)
-      k_cdot_seq<real_t<T>><<<1, 256, 0, st>>>(m, a, b, red.out);
+      k_cdot_seq<real_t<T>><<<1, 256, 0, st>>>(m, a, b, init ? init[0] : 0.0, init ? init[1] : 0.0, red.out);
     else
       k_cdot_fast<T><<<wave(m), kBlock, 0, st>>>(m, a, b, red);
     LAUNCHED("dot");
   } else {
-    dot_real<T>(m, a, b, red, num, st);
+    dot_real<T>(m, a, b, red, num, st, init);
   }
 }
 
@@ -506,29 +511,70 @@ void narrow_f64(size_t m, const double* x, float* y, int* flag, cudaStream_t st)
 __device__ __forceinline__ float rcp_exact(float s) { return __fdiv_rn(1.0f, s); }
 __device__ __forceinline__ double rcp_exact(double s) { return __ddiv_rn(1.0, s); }
 
+// Box j in [j0, j0 + ny) stored [k][jl][i] (ny = n: the whole grid; else the
+// j-slab FastDiag works in).  zero_flag gets the smallest GLOBAL linear index.
 template <class T>
-__global__ void k_pd_inv(int n, const T* la, const T* lb, const T* lc, T* pd, int* zero_flag) {
-  const long nn = n, m = nn * nn * nn;
+__global__ void k_pd_inv(int n, int ny, int j0, const T* la, const T* lb, const T* lc, T* pd, int* zero_flag) {
+  const long nn = n, m = nn * ny * nn;
   for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < m; idx += (long)gridDim.x * blockDim.x) {
-    const int i = (int)(idx % nn), j = (int)((idx / nn) % nn), k = (int)(idx / (nn * nn));
+    const int i = (int)(idx % nn), j = j0 + (int)((idx / nn) % ny), k = (int)(idx / (nn * ny));
     const T sum = xadd(xadd(la[i], lb[j]), lc[k]);
     // smallest offending linear index = the reference's first throw (k, j, i loop order)
-    if (sum == T(0)) atomicMin(zero_flag, (int)(idx < 0x7ffffffeL ? idx : 0x7ffffffeL));
+    const long g = i + (long)j * nn + (long)k * nn * nn;
+    if (sum == T(0)) atomicMin(zero_flag, (int)(g < 0x7ffffffeL ? g : 0x7ffffffeL));
     pd[idx] = rcp_exact(sum);
   }
 }
 
 template <class T>
-void pd_inv_device(int n, const T* la, const T* lb, const T* lc, T* pd, int* zero_flag, cudaStream_t st) {
-  const size_t m = (size_t)n * n * n;
-  k_pd_inv<T><<<grid_for(m, 256), 256, 0, st>>>(n, la, lb, lc, pd, zero_flag);
+void pd_inv_device(int n, const T* la, const T* lb, const T* lc, T* pd, int* zero_flag, cudaStream_t st, int ny,
+                   int j0) {
+  if (ny <= 0) ny = n;
+  const size_t m = (size_t)n * n * ny;
+  k_pd_inv<T><<<grid_for(m, 256), 256, 0, st>>>(n, ny, j0, la, lb, lc, pd, zero_flag);
   LAUNCHED("pd_inv");
 }
 
 // ============================================================================
+// slab transposes around the all-to-all (FastDiag's contraction along k)
+// ============================================================================
+// Rows of n contiguous elements move between the k-slab [kl][j][i] and the
+// peer-blocked buffer [s][kl][jl][i] (j = s ny + jl): a row permutation.
+__global__ void __launch_bounds__(256) k_slab_rows(long rows, int row_vecs, int n, int nz, int ny, int P,
+                                                   const uint4* __restrict__ src, uint4* __restrict__ dst,
+                                                   int to_blocked) {
+  const long total = rows * row_vecs;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    const long r = e / row_vecs;
+    const int v = (int)(e - r * row_vecs);
+    // r enumerates the k-slab rows: kl = r / n, j = r % n
+    const long kl = r / n;
+    const int j = (int)(r - kl * n);
+    const int s = j / ny, jl = j - s * ny;
+    const long rb = ((long)s * nz + kl) * ny + jl;
+    if (to_blocked)
+      dst[rb * row_vecs + v] = __ldcs(src + r * row_vecs + v);
+    else
+      dst[r * row_vecs + v] = __ldcs(src + rb * row_vecs + v);
+  }
+  (void)P;
+}
+
+void slab_transpose_rows(int n, int nz, int ny, int P, size_t elem, const void* src, void* dst, bool to_blocked,
+                         cudaStream_t st) {
+  const size_t row_bytes = (size_t)n * elem;
+  if (row_bytes % 16) MPRKB_THROW(10, "slab transpose: rows must be 16-byte multiples");
+  const int row_vecs = (int)(row_bytes / 16);
+  const long rows = (long)nz * n;
+  k_slab_rows<<<grid_for((size_t)rows * row_vecs, 256), 256, 0, st>>>(
+      rows, row_vecs, n, nz, ny, P, static_cast<const uint4*>(src), static_cast<uint4*>(dst), to_blocked ? 1 : 0);
+  LAUNCHED("slab_transpose");
+}
+
+// ============================================================================
 #define INST_BLAS(T)                                                                                  \
-  template void dot_real<T>(size_t, const T*, const T*, const RedSlot&, Numerics, cudaStream_t);     \
-  template void dot_conj<T>(size_t, const T*, const T*, const RedSlot&, Numerics, cudaStream_t);     \
+  template void dot_real<T>(size_t, const T*, const T*, const RedSlot&, Numerics, cudaStream_t, const double*); \
+  template void dot_conj<T>(size_t, const T*, const T*, const RedSlot&, Numerics, cudaStream_t, const double*); \
   template void vsub<T>(size_t, const T*, const T*, T*, const RedSlot*, cudaStream_t);               \
   template void vscale<T>(size_t, const T*, T, T*, cudaStream_t);                                    \
   template void vaxmy<T>(size_t, T, const T*, T*, cudaStream_t);                                     \
@@ -543,7 +589,8 @@ template void cg_update<float>(size_t, float, float*, const float*, float*, cons
 template void cg_update<double>(size_t, double, double*, const double*, double*, const double*, const RedSlot*, cudaStream_t);
 template void xpby<float>(size_t, const float*, float, float*, cudaStream_t);
 template void xpby<double>(size_t, const double*, double, double*, cudaStream_t);
-template void pd_inv_device<float>(int, const float*, const float*, const float*, float*, int*, cudaStream_t);
-template void pd_inv_device<double>(int, const double*, const double*, const double*, double*, int*, cudaStream_t);
+template void pd_inv_device<float>(int, const float*, const float*, const float*, float*, int*, cudaStream_t, int, int);
+template void pd_inv_device<double>(int, const double*, const double*, const double*, double*, int*, cudaStream_t, int,
+                                    int);
 
 }  // namespace mprkb

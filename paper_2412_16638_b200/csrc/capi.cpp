@@ -8,6 +8,7 @@
 #include <limits>
 #include <string>
 
+#include "comm.hpp"
 #include "krylov.hpp"
 #include "stepper.hpp"
 
@@ -415,6 +416,105 @@ void mprkb_config_init(mprkb_config* c) {
   c->block_storage = -1;
   c->nu = 0.0;
   c->basis_storage = -1;
+}
+
+// ---- split grid ---------------------------------------------------------------------
+struct mprkb_comm {
+  std::unique_ptr<Comm> c;
+};
+struct mprkb_comm_group {
+  std::shared_ptr<LocalGroup> g;
+};
+
+int mprkb_set_device(int device) {
+  return guarded([&] {
+    require_device();
+    CUDA_CHECK(cudaSetDevice(device));
+  });
+}
+
+int mprkb_slab_plan(int n, int size, int rank, int* k0, int* nz, int* j0, int* ny) {
+  return guarded([&] {
+    if (size < 1 || rank < 0 || rank >= size) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "slab plan: bad rank/size");
+    if (n < 1 || n % size) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "slab plan: n must split into equal k-slabs");
+    const int z = n / size;
+    if (k0) *k0 = rank * z;
+    if (nz) *nz = z;
+    if (j0) *j0 = rank * z;
+    if (ny) *ny = z;
+  });
+}
+
+int mprkb_nccl_unique_id(unsigned char* id) {
+  return guarded([&] { nccl_unique_id(id); });
+}
+
+int mprkb_comm_create_nccl(int rank, int size, const unsigned char* id, mprkb_comm** out) {
+  return guarded([&] {
+    require_device();
+    auto* h = new mprkb_comm;
+    try {
+      h->c = make_nccl_comm(rank, size, id);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int mprkb_comm_group_create(int size, mprkb_comm_group** out) {
+  return guarded([&] {
+    auto* h = new mprkb_comm_group;
+    h->g = make_local_group(size);
+    *out = h;
+  });
+}
+
+int mprkb_comm_create_local(mprkb_comm_group* g, int rank, mprkb_comm** out) {
+  return guarded([&] {
+    require_device();
+    if (!g) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "null comm group");
+    auto* h = new mprkb_comm;
+    try {
+      h->c = make_local_comm(g->g, rank);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+void mprkb_comm_group_destroy(mprkb_comm_group* g) { delete g; }
+void mprkb_comm_destroy(mprkb_comm* c) { delete c; }
+
+int mprkb_comm_allreduce_sum(mprkb_comm* c, double* v, int count) {
+  return guarded([&] { c->c->allreduce_sum(v, count); });
+}
+
+int mprkb_stepper_create_split(const mprkb_config* cfg, mprkb_comm* comm, mprkb_stepper** out) {
+  return guarded([&] {
+    StepperConfig c = config_of(cfg);
+    c.comm = comm ? comm->c.get() : nullptr;
+    auto* h = new mprkb_stepper;
+    try {
+      h->s = std::make_unique<Stepper>(c);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int mprkb_stepper_slab(mprkb_stepper* s, int* k0, int* nz, size_t* local_size) {
+  return guarded([&] {
+    if (!s) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "null stepper");
+    if (k0) *k0 = s->s->slab().k0;
+    if (nz) *nz = s->s->slab().nz;
+    if (local_size) *local_size = s->s->size();
+  });
 }
 
 int mprkb_stepper_create(const mprkb_config* cfg, mprkb_stepper** out) {

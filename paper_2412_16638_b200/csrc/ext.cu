@@ -57,10 +57,10 @@ __device__ __forceinline__ cplx<R> rmul(R a, cplx<R> x) {
 //   addresses (coalesced).
 // ---------------------------------------------------------------------------------
 template <class T, class S>
-__global__ void __launch_bounds__(256) k_block_jacobi(int n, int b, const S* __restrict__ inv, const T* __restrict__ r,
-                                                      T* __restrict__ z) {
+__global__ void __launch_bounds__(256) k_block_jacobi(int n, long lines, int b, const S* __restrict__ inv,
+                                                      const T* __restrict__ r, T* __restrict__ z) {
   using R = real_t<T>;
-  const long nn = n, m = nn * nn * nn;
+  const long nn = n, m = nn * lines;
   const int per_line = (n + b - 1) / b;
   for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < m; idx += (long)gridDim.x * blockDim.x) {
     const int i = (int)(idx % nn);
@@ -92,20 +92,22 @@ __global__ void k_bj_fill(long nblocks_per_line, long lines, int n, int b, const
 }
 
 template <class T>
-void block_jacobi_apply(int n, int b, int storage, const void* inv, const T* r, T* z, cudaStream_t st) {
-  const size_t m = (size_t)n * n * n;
+void block_jacobi_apply(int n, int b, int storage, const void* inv, const T* r, T* z, cudaStream_t st, long lines) {
+  if (lines <= 0) lines = (long)n * n;
+  const size_t m = (size_t)n * lines;
   const unsigned g = grid_for(m, 256, 8);
   switch (storage) {
-    case 4: k_block_jacobi<T, __half><<<g, 256, 0, st>>>(n, b, (const __half*)inv, r, z); break;
-    case 0: k_block_jacobi<T, float><<<g, 256, 0, st>>>(n, b, (const float*)inv, r, z); break;
-    default: k_block_jacobi<T, double><<<g, 256, 0, st>>>(n, b, (const double*)inv, r, z); break;
+    case 4: k_block_jacobi<T, __half><<<g, 256, 0, st>>>(n, lines, b, (const __half*)inv, r, z); break;
+    case 0: k_block_jacobi<T, float><<<g, 256, 0, st>>>(n, lines, b, (const float*)inv, r, z); break;
+    default: k_block_jacobi<T, double><<<g, 256, 0, st>>>(n, lines, b, (const double*)inv, r, z); break;
   }
   LAUNCHED("block_jacobi");
 }
 
 void block_jacobi_fill(int n, int b, int storage, const double* full_dev, const double* tail_dev, void* inv,
-                       cudaStream_t st) {
-  const long per_line = (n + b - 1) / b, lines = (long)n * n;
+                       cudaStream_t st, long lines) {
+  if (lines <= 0) lines = (long)n * n;
+  const long per_line = (n + b - 1) / b;
   const size_t total = (size_t)per_line * lines * b * b;
   const unsigned g = grid_for(total, 256, 8);
   switch (storage) {
@@ -257,7 +259,7 @@ void cast_f64_to_storage(size_t m, const double* src, int storage, void* dst, cu
 }
 
 #define INST_EXT(T)                                                                                      \
-  template void block_jacobi_apply<T>(int, int, int, const void*, const T*, T*, cudaStream_t);           \
+  template void block_jacobi_apply<T>(int, int, int, const void*, const T*, T*, cudaStream_t, long);     \
   template void csr_apply<T>(int, const int*, const int*, const void*, int, const T*, T*, cudaStream_t); \
   template void basis16_scale<T>(size_t, const T*, T, void*, cudaStream_t);                              \
   template void basis16_dot<T>(size_t, const void*, const T*, const RedSlot&, cudaStream_t);             \

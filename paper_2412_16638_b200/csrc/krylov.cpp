@@ -1,5 +1,6 @@
 #include "krylov.hpp"
 
+#include <array>
 #include <cmath>
 #include <complex>
 #include <cstring>
@@ -101,6 +102,49 @@ T to_dev(const H& h) {
   return t;
 }
 
+// Finish the slot-0 reduction a FAST kernel just produced: this rank's fp64
+// partial(s), summed across a split grid's ranks in rank order.
+template <class T>
+std::array<double, 2> finish_red(KrylovWork<T>& w, int nv, cudaStream_t st) {
+  stream_sync(st);
+  std::array<double, 2> v{w.red.host(0)[0], w.red.host(0)[1]};
+  if (w.comm && w.comm->size() > 1) w.comm->allreduce_sum(v.data(), nv);
+  return v;
+}
+
+// detail::dot_real / dot (krylov.hpp:43-67) over the whole (possibly split)
+// vector.  PARITY on a split grid keeps the reference's single accumulator
+// in global index order: rank r continues from rank r-1's partial sum, handed
+// on by one broadcast per rank.
+template <class T>
+std::array<double, 2> global_dot(KrylovWork<T>& w, bool conj, const T* a, const T* b, Numerics num,
+                                 cudaStream_t st) {
+  const size_t m = w.size();
+  const RedSlot s0 = w.red.slot(0);
+  const int nv = conj && is_cplx<T> ? 2 : 1;
+  Comm* c = w.comm;
+  auto launch = [&](const double* init) {
+    if (conj)
+      dot_conj<T>(m, a, b, s0, num, st, init);
+    else
+      dot_real<T>(m, a, b, s0, num, st, init);
+  };
+  if (num == Numerics::Fast || !c || c->size() == 1) {
+    launch(nullptr);
+    return finish_red(w, nv, st);
+  }
+  std::array<double, 2> acc{0.0, 0.0};
+  for (int r = 0; r < c->size(); ++r) {
+    if (r == c->rank()) {
+      launch(acc.data());
+      stream_sync(st);
+      acc = {w.red.host(0)[0], w.red.host(0)[1]};
+    }
+    c->bcast_host(acc.data(), nv, r);
+  }
+  return acc;
+}
+
 }  // namespace
 
 template <class T>
@@ -136,14 +180,8 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
   const RedSlot s0 = w.red.slot(0);
   T *r = w.v(0), *z = w.v(1), *p = w.v(2), *q = w.v(3);
 
-  auto fetch = [&]() -> R {
-    stream_sync(st);
-    return (R)w.red.host(0)[0];
-  };
-  auto rdot = [&](const T* a, const T* c) -> R {
-    dot_real<T>(m, a, c, s0, num, st);
-    return fetch();
-  };
+  auto fetch = [&]() -> R { return (R)finish_red(w, 1, st)[0]; };
+  auto rdot = [&](const T* a, const T* c) -> R { return (R)global_dot(w, false, a, c, num, st)[0]; };
   auto op = [&](const T* in, T* out) {
     Bracket br(timer, "stencil", st);
     A.apply(in, out, st);
@@ -250,21 +288,13 @@ void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num,
   if (basis_storage != -1 && !b16) MPRKB_THROW(10, "gmres: basis storage must be the working precision or F16");
   T *t = w.v(0), *wv = w.v(1), *xc = w.v(2), *wt = w.v(3);
 
-  auto fetch = [&]() -> R {
-    stream_sync(st);
-    return (R)w.red.host(0)[0];
-  };
-  auto norm2 = [&](const T* v) -> R {
-    dot_real<T>(m, v, v, s0, num, st);
-    return std::sqrt(fetch());
-  };
+  auto norm2 = [&](const T* v) -> R { return std::sqrt((R)global_dot(w, false, v, v, num, st)[0]); };
   auto dotc = [&](const T* a, const T* c) -> H {
-    dot_conj<T>(m, a, c, s0, num, st);
-    stream_sync(st);
+    const auto v = global_dot(w, true, a, c, num, st);
     if constexpr (is_cplx<T>)
-      return H((R)w.red.host(0)[0], (R)w.red.host(0)[1]);
+      return H((R)v[0], (R)v[1]);
     else
-      return (R)w.red.host(0)[0];
+      return (R)v[0];
   };
   auto op = [&](const T* in, T* out) {
     Bracket br(timer, "stencil", st);
@@ -353,11 +383,11 @@ void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num,
         H hj;
         if (b16) {
           basis16_dot<T>(m, basis16[j], wv, s0, st);
-          stream_sync(st);
+          const auto v = finish_red(w, is_cplx<T> ? 2 : 1, st);
           if constexpr (is_cplx<T>)
-            hj = H((R)w.red.host(0)[0], (R)w.red.host(0)[1]);
+            hj = H((R)v[0], (R)v[1]);
           else
-            hj = (R)w.red.host(0)[0];
+            hj = (R)v[0];
           h[j] = hj;
           basis16_axmy<T>(m, to_dev<T>(hj), basis16[j], wv, st);
         } else {

@@ -70,6 +70,9 @@ class KrylovWork {
   void* basis16(int j);  // fp16 storage (2 x fp16 for complex)
   size_t size() const { return m_; }
   Reducer red;
+  // split grid: the vectors are this rank's slab and every dot/norm is
+  // completed across ranks (null: undivided grid)
+  Comm* comm = nullptr;
 
  private:
   size_t m_;

@@ -9,12 +9,21 @@
 namespace mprkb {
 
 // ---- stencil family (operators.hpp:113-161) ------------------------------------
+struct Halo;  // comm.hpp: slab + ghost-plane scratch of a split grid
+// Exchange the boundary planes of the local slab `x` (elements of `elem`
+// bytes) with the k-neighbours; g[0]/g[1] receive the lo/hi ghost planes
+// (null where the domain ends: Dirichlet zero).  Stream-ordered on st.
+void halo_exchange(const Halo& h, const void* x, size_t elem, bool periodic, cudaStream_t st, const void* g[2]);
+
 struct StencilSpec {
   int n = 0;
   int stencil = 0;      // 0 Dirichlet Laplace, 1 periodic central, 2 adv-diff (central + periodic Laplace)
   double sigma = 0.0;   // identity shift
   double gamma = 0.0;   // stencil scale
   double gamma2 = 0.0;  // second (diffusion) scale for stencil 2
+  int nz = 0;           // local k-planes (0: the whole grid, n)
+  const Halo* halo = nullptr;  // split grid: exchange ghost planes before every apply
+  size_t size() const { return (size_t)n * n * (nz > 0 ? nz : n); }
 };
 
 // out = sigma x + gamma K3 x
@@ -44,15 +53,19 @@ void apply_f32(const StencilSpec& k, const double* y, const float* y32, const fl
 // side 0 L (stride n^2), 1 M (stride n), 2 R (stride 1).  pd: fused diag scale
 // of the output (precond.hpp:172) or null.  fold: Q has the Dirichlet sine
 // symmetry Q[n-1-a][q] = (-1)^q Q[a][q] (FAST numerics may halve the flops).
+// cols: the non-contracted extent — n^2 for the undivided grid; n * nz for
+// R / M on a k-slab (nz planes), n * ny for L on a j-slab ([k][jl][i] layout,
+// column stride n * ny).
 template <class T>
 void tensor_apply(int side, int n, const T* q, const T* x, T* out, const T* pd, Numerics num,
-                  cudaStream_t st, bool fold = false);
+                  cudaStream_t st, bool fold = false, long cols = 0);
 // Tensor-core (tcgen05, 3xTF32) contraction for fp32, FAST numerics
 // (tensor_tc.cu).  q_{hi,lo}_packed: Q split into tf32 hi/lo parts and packed
 // by pack_tf32_split() into the canonical UMMA K-major layout.
 bool tensor_tc_supported(int n);
 void tensor_apply_tc(int side, int n, const float* q_hi_packed, const float* q_lo_packed, const float* x,
-                     float* out, const float* pd, cudaStream_t st);
+                     float* out, const float* pd, cudaStream_t st, long cols = 0);
+bool tensor_tc_supported_cols(int n, long cols);
 // Host: split Q (n x n row-major) into tf32 hi/lo and pack as
 // [k-block of 16][row-group of 8][k-chunk of 4][8 rows][4].
 void pack_tf32_split(int n, const float* q, float* hi_packed, float* lo_packed);
@@ -60,17 +73,26 @@ void pack_tf32_split(int n, const float* q, float* hi_packed, float* lo_packed);
 // types only (IEEE division is correctly rounded on both sides).  *zero_flag
 // (initialised to INT_MAX by the caller) receives the smallest linear index
 // whose eigenvalue sum is exactly zero.
+// ny/j0: only the j-box [j0, j0 + ny), stored [k][jl][i] (the j-slab layout
+// of a split grid); ny = 0 means the whole grid.
 template <class T>
-void pd_inv_device(int n, const T* la, const T* lb, const T* lc, T* pd, int* zero_flag, cudaStream_t st);
+void pd_inv_device(int n, const T* la, const T* lb, const T* lc, T* pd, int* zero_flag, cudaStream_t st, int ny = 0,
+                   int j0 = 0);
+// k-slab [kl][j][i] (nz planes) <-> peer-blocked [s][kl][jl][i] (j = s ny + jl),
+// the send/receive layout of the FastDiag all-to-all.
+void slab_transpose_rows(int n, int nz, int ny, int P, size_t elem, const void* src, void* dst, bool to_blocked,
+                         cudaStream_t st);
 
 // ---- north-star extensions (ext.cu) ---------------------------------------------------
 // storage codes: 0 fp32, 1 fp64, 4 fp16
+// lines: x-lines held (n^2 for the whole grid, n * nz on a k-slab; 0 = n^2)
 template <class T>
-void block_jacobi_apply(int n, int b, int storage, const void* inv, const T* r, T* z, cudaStream_t st);
+void block_jacobi_apply(int n, int b, int storage, const void* inv, const T* r, T* z, cudaStream_t st,
+                        long lines = 0);
 // per-block inverse storage from the two distinct fp64 block inverses
 // (column-major b x b full blocks, n % b tail blocks)
 void block_jacobi_fill(int n, int b, int storage, const double* full_dev, const double* tail_dev, void* inv,
-                       cudaStream_t st);
+                       cudaStream_t st, long lines = 0);
 template <class T>
 void csr_apply(int rows, const int* rp, const int* cols, const void* vals, int storage, const T* x, T* y,
                cudaStream_t st);
@@ -87,11 +109,15 @@ void cast_f64_to_storage(size_t m, const double* src, int storage, void* dst, cu
 
 // ---- reductions (krylov.hpp:43-71) --------------------------------------------------
 // dot_real(a, b): FAST -> fp64 tree into red.out[0]; PARITY -> sequential in real_t<T>
+// init (PARITY, nullable): starting value(s) of the sequential accumulator —
+// a split grid's rank r continues from rank r-1's partial sum.
 template <class T>
-void dot_real(size_t m, const T* a, const T* b, const RedSlot& red, Numerics num, cudaStream_t st);
+void dot_real(size_t m, const T* a, const T* b, const RedSlot& red, Numerics num, cudaStream_t st,
+              const double* init = nullptr);
 // complex dot with conjugated first argument -> red.out[0..1]
 template <class T>
-void dot_conj(size_t m, const T* a, const T* b, const RedSlot& red, Numerics num, cudaStream_t st);
+void dot_conj(size_t m, const T* a, const T* b, const RedSlot& red, Numerics num, cudaStream_t st,
+              const double* init = nullptr);
 
 // ---- vector updates (krylov.hpp:111-158, 191-301) ------------------------------------
 template <class T>

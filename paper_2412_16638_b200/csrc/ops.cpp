@@ -62,7 +62,7 @@ void pack_tf32_split(int n, const float* q, float* hi_packed, float* lo_packed) 
     }
 }
 
-StencilOp::StencilOp(int dtype, const StencilSpec& s) : Op(dtype, (size_t)s.n * s.n * s.n), spec_(s) {
+StencilOp::StencilOp(int dtype, const StencilSpec& s) : Op(dtype, s.size()), spec_(s) {
   if (s.n < 2) MPRKB_THROW(3, "KronSumOperator: n must be at least 2");
 }
 
@@ -78,10 +78,16 @@ void StencilOp::apply(const void* x, void* out, cudaStream_t st) {
 
 template <class T>
 FastDiagOp<T>::FastDiagOp(int n, const T* qa, const T* qa_inv, const T* qb, const T* qb_inv, const T* qc,
-                          const T* qc_inv, const T* la, const T* lb, const T* lc, Numerics num)
-    : Op(dtype_of<T>::v, (size_t)n * n * n), n_(n), num_(num) {
+                          const T* qc_inv, const T* la, const T* lb, const T* lc, Numerics num, const Halo* halo)
+    : Op(dtype_of<T>::v, halo ? halo->slab.local() : (size_t)n * n * n),
+      n_(n),
+      num_(num),
+      halo_(halo && halo->slab.split() ? halo : nullptr) {
   if (n < 2) MPRKB_THROW(3, "FastDiagPreconditioner: n must be at least 2");
-  const size_t nn = (size_t)n * n, m = nn * n;
+  const size_t nn = (size_t)n * n, m = size();
+  nz_ = halo_ ? halo_->slab.nz : n;
+  ny_ = halo_ ? halo_->slab.ny : n;
+  P_ = halo_ ? halo_->slab.P : 1;
   const T* src[6] = {qa, qa_inv, qb, qb_inv, qc, qc_inv};
   for (int i = 0; i < 6; ++i) upload(q_[i], src[i], nn * sizeof(T));
   if constexpr (!is_cplx<T>) {
@@ -106,6 +112,7 @@ FastDiagOp<T>::FastDiagOp(int n, const T* qa, const T* qa_inv, const T* qb, cons
     // unless MPRKB_TENSOR_CORES=0 selects the CUDA-core kernels
     const char* env = std::getenv("MPRKB_TENSOR_CORES");
     tc_ = num == Numerics::Fast && tensor_tc_supported(n) && !(env && env[0] == '0');
+    tc_split_ = tc_ && tensor_tc_supported_cols(n, (long)n * nz_) && tensor_tc_supported_cols(n, (long)n * ny_);
     if (tc_) {
       std::vector<float> hi(nn), lo(nn);
       for (int f = 0; f < 6; ++f) {
@@ -122,6 +129,7 @@ FastDiagOp<T>::FastDiagOp(int n, const T* qa, const T* qa_inv, const T* qb, cons
   if constexpr (!is_cplx<T>) {
     // pd_inv[i+jn+kn^2] = 1/(la_i+lb_j+lc_k) in T on the device: IEEE
     // division and the same left-to-right sum => bitwise the reference's.
+    // (split grid: this rank's j-box, the layout the diagonal is applied in)
     DevBuf dl, flag(sizeof(int));
     std::vector<T> lam(3 * (size_t)n);
     std::memcpy(lam.data(), la, n * sizeof(T));
@@ -129,7 +137,8 @@ FastDiagOp<T>::FastDiagOp(int n, const T* qa, const T* qa_inv, const T* qb, cons
     std::memcpy(lam.data() + 2 * n, lc, n * sizeof(T));
     upload(dl, lam.data(), lam.size() * sizeof(T));
     CUDA_CHECK(cudaMemcpy(flag.get(), &zi, sizeof(int), cudaMemcpyHostToDevice));
-    pd_inv_device<T>(n, dl.as<T>(), dl.as<T>() + n, dl.as<T>() + 2 * n, pd_.as<T>(), flag.as<int>(), 0);
+    pd_inv_device<T>(n, dl.as<T>(), dl.as<T>() + n, dl.as<T>() + 2 * n, pd_.as<T>(), flag.as<int>(), 0,
+                     halo_ ? ny_ : 0, halo_ ? halo_->slab.j0 : 0);
     CUDA_CHECK(cudaMemcpy(&zi, flag.get(), sizeof(int), cudaMemcpyDeviceToHost));
   } else {
     // complex: 1/sum through libgcc's complex division on the host, exactly
@@ -138,19 +147,31 @@ FastDiagOp<T>::FastDiagOp(int n, const T* qa, const T* qa_inv, const T* qb, cons
     const H* A = reinterpret_cast<const H*>(la);
     const H* B = reinterpret_cast<const H*>(lb);
     const H* C = reinterpret_cast<const H*>(lc);
+    // j-box [j0, j0 + ny) in [k][jl][i] order (the whole grid when undivided)
+    const size_t ny = (size_t)ny_, j0 = halo_ ? (size_t)halo_->slab.j0 : 0;
     std::vector<H> pd(m);
     const H one = static_cast<H>(static_cast<typename H::value_type>(1.0));
     for (size_t k = 0; k < (size_t)n && zi == INT_MAX; ++k)
-      for (size_t j = 0; j < (size_t)n && zi == INT_MAX; ++j)
+      for (size_t jl = 0; jl < ny && zi == INT_MAX; ++jl)
         for (size_t i = 0; i < (size_t)n; ++i) {
+          const size_t j = j0 + jl;
           const H sum = A[i] + B[j] + C[k];
           if (sum == H{}) {
             zi = (int)(i + j * n + k * nn);
             break;
           }
-          pd[i + j * n + k * nn] = one / sum;
+          pd[i + jl * n + k * n * ny] = one / sum;
         }
     if (zi == INT_MAX) CUDA_CHECK(cudaMemcpy(pd_.get(), pd.data(), m * sizeof(T), cudaMemcpyHostToDevice));
+  }
+  if (halo_) {
+    // every rank reports the globally first zero sum (the reference's throw)
+    double v = -(double)zi;
+    halo_->slab.comm->allreduce_max(&v, 1);
+    zi = (int)-v;
+  }
+  if (halo_) {
+    t3_.alloc(m * sizeof(T));
   }
   if (zi != INT_MAX) {
     const int i = zi % n, j = (zi / n) % n, k = zi / (int)nn;
@@ -162,9 +183,63 @@ FastDiagOp<T>::FastDiagOp(int n, const T* qa, const T* qa_inv, const T* qb, cons
 // apply_inverse (precond.hpp:153-186): R, M, L with the inverse factors, the
 // diagonal scale fused into the L pass, then R, M, L with the forward factors.
 template <class T>
+void FastDiagOp<T>::contract(int side, int f, const T* in, T* o, const T* pd, long cols, cudaStream_t st) {
+  if constexpr (std::is_same_v<T, float>) {
+    if (tc_split_) {
+      tensor_apply_tc(side, n_, qhp_[f].template as<float>(), qlp_[f].template as<float>(), in, o, pd, st, cols);
+      return;
+    }
+  }
+  tensor_apply<T>(side, n_, q_[f].template as<T>(), in, o, pd, num_, st, fold_[f], cols);
+}
+
+template <class T>
+void FastDiagOp<T>::apply_split(const T* x, T* out, cudaStream_t st) {
+  const int n = n_;
+  const long ck = (long)n * nz_, cj = (long)n * ny_;
+  const size_t blk = (size_t)nz_ * ny_ * n * sizeof(T);  // bytes per peer
+  Comm* comm = halo_->slab.comm;
+  T* t1 = t1_.as<T>();
+  T* t2 = t2_.as<T>();
+  T* t3 = t3_.as<T>();
+  const T* pd = pd_.as<T>();
+  // k-slab -> j-slab: pack peer blocks, exchange (lands as [k][jl][i])
+  auto to_j = [&](const T* src, T* scratch, T* dst) {
+    slab_transpose_rows(n, nz_, ny_, P_, sizeof(T), src, scratch, true, st);
+    comm->alltoall(scratch, dst, blk, st);
+  };
+  // j-slab -> k-slab: contiguous peer blocks out, unpack on arrival
+  auto to_k = [&](const T* src, T* scratch, T* dst) {
+    comm->alltoall(src, scratch, blk, st);
+    slab_transpose_rows(n, nz_, ny_, P_, sizeof(T), scratch, dst, false, st);
+  };
+  contract(2, 1, x, t1, nullptr, ck, st);   // R: Qa^-1
+  contract(1, 3, t1, t2, nullptr, ck, st);  // M: Qb^-1
+  to_j(t2, t1, t3);
+  contract(0, 5, t3, t1, pd, cj, st);       // L: Qc^-1, then * pd_inv
+  if (num_ == Numerics::Parity) {
+    to_k(t1, t2, t3);
+    contract(2, 0, t3, t1, nullptr, ck, st);  // R: Qa
+    contract(1, 2, t1, t2, nullptr, ck, st);  // M: Qb
+    to_j(t2, t1, t3);
+    contract(0, 4, t3, t1, nullptr, cj, st);  // L: Qc
+    to_k(t1, t2, out);
+  } else {
+    contract(0, 4, t1, t2, nullptr, cj, st);  // L: Qc (the factors commute exactly)
+    to_k(t2, t1, t3);
+    contract(1, 2, t3, t1, nullptr, ck, st);  // M: Qb
+    contract(2, 0, t1, out, nullptr, ck, st); // R: Qa
+  }
+}
+
+template <class T>
 void FastDiagOp<T>::apply(const void* xv, void* outv, cudaStream_t st) {
   const T* x = static_cast<const T*>(xv);
   T* out = static_cast<T*>(outv);
+  if (halo_) {
+    apply_split(x, out, st);
+    return;
+  }
   T* t1 = t1_.as<T>();
   T* t2 = t2_.as<T>();
   if constexpr (std::is_same_v<T, float>) {
@@ -199,9 +274,11 @@ void CallbackOp::apply(const void* x, void* out, cudaStream_t st) {
   if (rc != 0) MPRKB_THROW(rc, "ApplyFn callback returned an error");
 }
 
-StencilSpec stage_spec(const Problem& p, double tau, double a) {
+StencilSpec stage_spec(const Problem& p, double tau, double a, const Halo* halo) {
   StencilSpec s;
   s.n = p.n;
+  s.nz = p.nz;
+  s.halo = halo && halo->slab.split() ? halo : nullptr;
   s.stencil = p.eq == Equation::Heat ? 0 : (p.eq == Equation::Advection ? 1 : 2);
   s.sigma = 1.0;
   s.gamma = -tau * a * p.gamma_k;
@@ -209,9 +286,11 @@ StencilSpec stage_spec(const Problem& p, double tau, double a) {
   return s;
 }
 
-StencilSpec rhs_spec(const Problem& p) {
+StencilSpec rhs_spec(const Problem& p, const Halo* halo) {
   StencilSpec s;
   s.n = p.n;
+  s.nz = p.nz;
+  s.halo = halo && halo->slab.split() ? halo : nullptr;
   s.stencil = p.eq == Equation::Heat ? 0 : (p.eq == Equation::Advection ? 1 : 2);
   s.sigma = 0.0;
   s.gamma = p.gamma_k;
@@ -219,7 +298,8 @@ StencilSpec rhs_spec(const Problem& p) {
   return s;
 }
 
-std::unique_ptr<Op> make_stage_fastdiag(int dtype, const Problem& p, double tau, double a, Numerics num) {
+std::unique_ptr<Op> make_stage_fastdiag(int dtype, const Problem& p, double tau, double a, Numerics num,
+                                        const Halo* halo) {
   const double g = -tau * a * p.gamma_k;  // stage_gamma (precond.cpp:10-12)
   const int n = p.n;
   if (p.eq == Equation::Heat) {
@@ -228,7 +308,7 @@ std::unique_ptr<Op> make_stage_fastdiag(int dtype, const Problem& p, double tau,
     spectral_dirichlet(n, 0.0, g, qb, qbi, lb);
     if (dtype == 1)
       return std::make_unique<FastDiagOp<double>>(n, qa.data(), qai.data(), qb.data(), qbi.data(), qb.data(),
-                                                  qbi.data(), la.data(), lb.data(), lb.data(), num);
+                                                  qbi.data(), la.data(), lb.data(), lb.data(), num, halo);
     if (dtype != 0) MPRKB_THROW(10, "heat preconditioner: dtype must be F32 or F64");
     auto nar = [](const std::vector<double>& v) {
       std::vector<float> o(v.size());
@@ -237,7 +317,7 @@ std::unique_ptr<Op> make_stage_fastdiag(int dtype, const Problem& p, double tau,
     };
     const auto fa = nar(qa), fai = nar(qai), fla = nar(la), fb = nar(qb), fbi = nar(qbi), flb = nar(lb);
     return std::make_unique<FastDiagOp<float>>(n, fa.data(), fai.data(), fb.data(), fbi.data(), fb.data(),
-                                               fbi.data(), fla.data(), flb.data(), flb.data(), num);
+                                               fbi.data(), fla.data(), flb.data(), flb.data(), num, halo);
   }
   const double g2 = -tau * a * p.gamma_d;
   std::vector<std::complex<double>> qa, qai, la, qb, qbi, lb;
@@ -249,7 +329,7 @@ std::unique_ptr<Op> make_stage_fastdiag(int dtype, const Problem& p, double tau,
         reinterpret_cast<const c64*>(qb.data()), reinterpret_cast<const c64*>(qbi.data()),
         reinterpret_cast<const c64*>(qb.data()), reinterpret_cast<const c64*>(qbi.data()),
         reinterpret_cast<const c64*>(la.data()), reinterpret_cast<const c64*>(lb.data()),
-        reinterpret_cast<const c64*>(lb.data()), num);
+        reinterpret_cast<const c64*>(lb.data()), num, halo);
   if (dtype != 2) MPRKB_THROW(10, "advection preconditioner: dtype must be C32 or C64");
   auto nar = [](const std::vector<std::complex<double>>& v) {
     std::vector<std::complex<float>> o(v.size());
@@ -259,7 +339,7 @@ std::unique_ptr<Op> make_stage_fastdiag(int dtype, const Problem& p, double tau,
   const auto fa = nar(qa), fai = nar(qai), fla = nar(la), fb = nar(qb), fbi = nar(qbi), flb = nar(lb);
   auto C = [](const std::vector<std::complex<float>>& v) { return reinterpret_cast<const c32*>(v.data()); };
   return std::make_unique<FastDiagOp<c32>>(n, C(fa), C(fai), C(fb), C(fbi), C(fb), C(fbi), C(fla), C(flb),
-                                           C(flb), num);
+                                           C(flb), num, halo);
 }
 
 std::unique_ptr<Op> make_fastdiag(int dtype, int n, const void* qa, const void* qa_inv, const void* qb,

@@ -7,6 +7,7 @@
 
 #include "launch.hpp"
 #include "problem.hpp"
+#include "comm.hpp"
 #include "runtime.hpp"
 
 namespace mprkb {
@@ -41,23 +42,37 @@ class StencilOp final : public Op {
 // FastDiagPreconditioner<T> (precond.hpp:30-53): P^-1 = (Qc(x)Qb(x)Qa) diag(pd)
 // (Qc^-1 (x) Qb^-1 (x) Qa^-1).  Device-resident factors, pd_inv and two
 // scratch vectors (not re-entrant, like the reference's mutable t1_/t2_).
+//
+// On a split grid (halo != null, P > 1) the operand is this rank's k-slab.
+// The contractions along i and j are slab-local; the one along k needs every
+// k, so the vector is transposed to a j-slab ([k][jl][i], ny = n/P rows of j)
+// by an all-to-all around it:
+//   FAST    R^-1 M^-1 | T | L^-1 pd L | T^-1 | M R          (2 all-to-alls)
+//   PARITY  R^-1 M^-1 | T | L^-1 pd | T^-1 | R M | T | L | T^-1
+// PARITY keeps the reference's contraction order, so every output is the
+// same sequence of roundings as on the undivided grid (bitwise equal).
 template <class T>
 class FastDiagOp final : public Op {
  public:
   // Host arrays in T layout: q* (n*n row-major), lambda_* (n).
   FastDiagOp(int n, const T* qa, const T* qa_inv, const T* qb, const T* qb_inv, const T* qc, const T* qc_inv,
-             const T* la, const T* lb, const T* lc, Numerics num);
+             const T* la, const T* lb, const T* lc, Numerics num, const Halo* halo = nullptr);
   void apply(const void* x, void* out, cudaStream_t st) override;
   int n() const { return n_; }
 
  private:
+  void apply_split(const T* x, T* out, cudaStream_t st);
+  void contract(int side, int f, const T* in, T* out, const T* pd, long cols, cudaStream_t st);
   int n_;
   Numerics num_;
+  const Halo* halo_ = nullptr;
+  int P_ = 1, nz_ = 0, ny_ = 0;
+  bool tc_split_ = false;  // tensor cores usable on both slab layouts
   bool fold_[6] = {false, false, false, false, false, false};  // sine symmetry per factor
   bool tc_ = false;  // fp32 FAST: tensor-core (3xTF32) contractions
   DevBuf q_[6];  // qa, qa_inv, qb, qb_inv, qc, qc_inv
   DevBuf qhp_[6], qlp_[6];  // tf32 hi/lo split, UMMA-packed (tc_ only)
-  DevBuf pd_, t1_, t2_;
+  DevBuf pd_, t1_, t2_, t3_;  // t3_: split grid only
 };
 
 // User callback (the literal ApplyFn slot across the C-ABI).
@@ -73,13 +88,15 @@ class CallbackOp final : public Op {
 };
 
 // Stage operator I - tau a K of a problem (stage_operator, operators.cpp:77-79).
-StencilSpec stage_spec(const Problem& p, double tau, double a);
+// halo: the split grid's ghost exchange (null: undivided grid).
+StencilSpec stage_spec(const Problem& p, double tau, double a, const Halo* halo = nullptr);
 // The problem's own K (sigma 0) for f evaluations.
-StencilSpec rhs_spec(const Problem& p);
+StencilSpec rhs_spec(const Problem& p, const Halo* halo = nullptr);
 
 // build_heat_precond(_f32) / build_advection_precond(_f32) (precond.cpp:14-42),
 // dtype selects the arithmetic (F32/F64 heat, C32/C64 advection).
-std::unique_ptr<Op> make_stage_fastdiag(int dtype, const Problem& p, double tau, double a, Numerics num);
+std::unique_ptr<Op> make_stage_fastdiag(int dtype, const Problem& p, double tau, double a, Numerics num,
+                                        const Halo* halo = nullptr);
 // FastDiag from caller-provided factors (the public FastDiagPreconditioner ctor).
 std::unique_ptr<Op> make_fastdiag(int dtype, int n, const void* qa, const void* qa_inv, const void* qb,
                                   const void* qb_inv, const void* qc, const void* qc_inv, const void* la,

@@ -90,8 +90,10 @@ std::vector<double> col_major(const std::vector<double>& rm, int k) {
 template <class T>
 class BlockJacobiOp final : public Op {
  public:
+  // x-line blocks never cross a k-slab: a split grid's rank holds its own
+  // lines (size() / n of them) and the operator stays communication-free
   BlockJacobiOp(const StencilSpec& s, int block, int storage)
-      : Op(dtype_of<T>::v, (size_t)s.n * s.n * s.n), n_(s.n), b_(block), storage_(storage) {
+      : Op(dtype_of<T>::v, s.size()), n_(s.n), lines_((long)(s.size() / s.n)), b_(block), storage_(storage) {
     if (block < 1) MPRKB_THROW(10, "block-Jacobi: block size must be >= 1");
     if (block > s.n) b_ = s.n;
     const int tail = n_ % b_;
@@ -105,16 +107,18 @@ class BlockJacobiOp final : public Op {
     CUDA_CHECK(cudaMemcpy(df.get(), full.data(), full.size() * 8, cudaMemcpyHostToDevice));
     CUDA_CHECK(cudaMemcpy(dt.get(), tl.data(), tl.size() * 8, cudaMemcpyHostToDevice));
     const size_t per_line = (n_ + b_ - 1) / b_;
-    inv_.alloc(per_line * (size_t)n_ * n_ * b_ * b_ * storage_size(storage));
-    block_jacobi_fill(n_, b_, storage_, df.as<double>(), dt.as<double>(), inv_.get(), 0);
+    inv_.alloc(per_line * (size_t)lines_ * b_ * b_ * storage_size(storage));
+    block_jacobi_fill(n_, b_, storage_, df.as<double>(), dt.as<double>(), inv_.get(), 0, lines_);
     CUDA_CHECK(cudaDeviceSynchronize());
   }
   void apply(const void* x, void* out, cudaStream_t st) override {
-    block_jacobi_apply<T>(n_, b_, storage_, inv_.get(), static_cast<const T*>(x), static_cast<T*>(out), st);
+    block_jacobi_apply<T>(n_, b_, storage_, inv_.get(), static_cast<const T*>(x), static_cast<T*>(out), st, lines_);
   }
 
  private:
-  int n_, b_, storage_;
+  int n_;
+  long lines_;
+  int b_, storage_;
   DevBuf inv_;
 };
 

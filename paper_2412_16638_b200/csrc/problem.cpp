@@ -8,13 +8,17 @@
 
 namespace mprkb {
 
-Problem make_problem(Equation eq, int n, double nu) {
+Problem make_problem(Equation eq, int n, double nu, int k0, int nz) {
   const bool heat = eq == Equation::Heat;
   if (n < (heat ? 2 : 3)) MPRKB_THROW(3, "make_problem: grid too small for the requested equation");
+  if (nz <= 0) nz = n;
+  if (k0 < 0 || k0 + nz > n) MPRKB_THROW(10, "make_problem: k-slab outside the grid");
   Problem p;
   p.eq = eq;
   p.n = n;
-  const size_t m = (size_t)n * n * n;
+  p.k0 = k0;
+  p.nz = nz;
+  const size_t m = (size_t)n * n * nz;
   const double pi = std::numbers::pi;
   if (heat) {
     // nodes at i*h, h = 1/(n-1); boundary nodes are unknowns with zero ghosts
@@ -22,10 +26,10 @@ Problem make_problem(Equation eq, int n, double nu) {
     p.gamma_k = -1.0 / (p.h * p.h);
     p.u0.assign(m, 0.0);
     p.forcing.resize(m);
-    for (int k = 0; k < n; ++k)
+    for (int k = k0; k < k0 + nz; ++k)
       for (int j = 0; j < n; ++j)
         for (int i = 0; i < n; ++i)
-          p.forcing[i + (size_t)j * n + (size_t)k * n * n] =
+          p.forcing[i + (size_t)j * n + (size_t)(k - k0) * n * n] =
               std::sin(pi * i * p.h) * std::sin(pi * j * p.h) * std::sin(pi * k * p.h);
   } else {
     // periodic unit cube, h = 1/n, Gaussian pulse
@@ -33,11 +37,11 @@ Problem make_problem(Equation eq, int n, double nu) {
     p.gamma_k = -1.0 / (2.0 * p.h);
     if (eq == Equation::AdvectionDiffusion) p.gamma_d = -nu / (p.h * p.h);
     p.u0.resize(m);
-    for (int k = 0; k < n; ++k)
+    for (int k = k0; k < k0 + nz; ++k)
       for (int j = 0; j < n; ++j)
         for (int i = 0; i < n; ++i) {
           const double dx = i * p.h - 0.5, dy = j * p.h - 0.5, dz = k * p.h - 0.5;
-          p.u0[i + (size_t)j * n + (size_t)k * n * n] = std::exp(-100.0 * (dx * dx + dy * dy + dz * dz));
+          p.u0[i + (size_t)j * n + (size_t)(k - k0) * n * n] = std::exp(-100.0 * (dx * dx + dy * dy + dz * dz));
         }
   }
   return p;

@@ -17,14 +17,17 @@ struct Problem {
   double h = 0.0;
   double gamma_k = 0.0;   // stencil scale of K (operators.cpp:37, 52)
   double gamma_d = 0.0;   // diffusion scale (advection-diffusion extension)
-  std::vector<double> u0;
-  std::vector<double> forcing;  // empty unless heat
-  size_t size() const { return (size_t)n * n * n; }
+  int k0 = 0, nz = 0;     // this rank's k-slab [k0, k0 + nz) (the whole grid: 0, n)
+  std::vector<double> u0;       // local slab
+  std::vector<double> forcing;  // local slab; empty unless heat
+  size_t size() const { return (size_t)n * n * nz; }
 };
 
 // make_problem (operators.cpp:29-65).  nu: diffusion coefficient of the
-// advection-diffusion extension (K_d = nu/h^2 * periodic Laplacian).
-Problem make_problem(Equation eq, int n, double nu = 0.0);
+// advection-diffusion extension (K_d = nu/h^2 * periodic Laplacian).  k0/nz
+// restrict u0 and forcing to one k-slab of a split grid (nz = 0: all of it);
+// every value is the one the undivided grid holds at that point.
+Problem make_problem(Equation eq, int n, double nu = 0.0, int k0 = 0, int nz = 0);
 // heat_exact (operators.cpp:67-75)
 std::vector<double> heat_exact(const Problem& p, double t);
 

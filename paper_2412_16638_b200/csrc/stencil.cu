@@ -24,38 +24,56 @@ __device__ __forceinline__ bool f32_overflows(double x) {
 }
 
 // ---- loaders ------------------------------------------------------------------
+// Every loader reads a raw vector `p` (local slab) and, on a split grid, the
+// two ghost planes the halo exchange filled (`glo` = plane k0-1, `ghi` =
+// plane k0+nz; null = Dirichlet zero / undivided grid).
 template <class T>
 struct LdPlain {
   using type = T;
+  using raw = T;
   const T* p;
-  __device__ __forceinline__ T ld1(long i) const { return ldg(p + i); }
-  __device__ __forceinline__ V4<T> ld4(long i) const { return ::mprkb::ld4(p + i); }
+  const T* glo = nullptr;
+  const T* ghi = nullptr;
+  __device__ __forceinline__ T ld1f(const T* b, long i) const { return ldg(b + i); }
+  __device__ __forceinline__ V4<T> ld4f(const T* b, long i) const { return ::mprkb::ld4(b + i); }
+  __device__ __forceinline__ T ld1(long i) const { return ld1f(p, i); }
+  __device__ __forceinline__ V4<T> ld4(long i) const { return ld4f(p, i); }
 };
 // double vector read in binary32 (apply_f F32: downcast(u), operators.cpp:88);
 // flags |u| past the binary32 range (precision.hpp:100-104)
 struct LdD2F {
   using type = float;
+  using raw = double;
   const double* p;
   int* flag;
+  const double* glo = nullptr;
+  const double* ghi = nullptr;
   __device__ __forceinline__ float cvt(double x) const {
     if (f32_overflows(x)) *flag = 1;
     return __double2float_rn(x);
   }
-  __device__ __forceinline__ float ld1(long i) const { return cvt(ldg(p + i)); }
-  __device__ __forceinline__ V4<float> ld4(long i) const {
-    const V4<double> d = ::mprkb::ld4(p + i);
+  __device__ __forceinline__ float ld1f(const double* b, long i) const { return cvt(ldg(b + i)); }
+  __device__ __forceinline__ V4<float> ld4f(const double* b, long i) const {
+    const V4<double> d = ::mprkb::ld4(b + i);
     return {{cvt(d.x[0]), cvt(d.x[1]), cvt(d.x[2]), cvt(d.x[3])}};
   }
+  __device__ __forceinline__ float ld1(long i) const { return ld1f(p, i); }
+  __device__ __forceinline__ V4<float> ld4(long i) const { return ld4f(p, i); }
 };
 // float vector widened to double (exact)
 struct LdF2D {
   using type = double;
+  using raw = float;
   const float* p;
-  __device__ __forceinline__ double ld1(long i) const { return (double)ldg(p + i); }
-  __device__ __forceinline__ V4<double> ld4(long i) const {
-    const V4<float> f = ::mprkb::ld4(p + i);
+  const float* glo = nullptr;
+  const float* ghi = nullptr;
+  __device__ __forceinline__ double ld1f(const float* b, long i) const { return (double)ldg(b + i); }
+  __device__ __forceinline__ V4<double> ld4f(const float* b, long i) const {
+    const V4<float> f = ::mprkb::ld4(b + i);
     return {{(double)f.x[0], (double)f.x[1], (double)f.x[2], (double)f.x[3]}};
   }
+  __device__ __forceinline__ double ld1(long i) const { return ld1f(p, i); }
+  __device__ __forceinline__ V4<double> ld4(long i) const { return ld4f(p, i); }
 };
 
 template <class T>
@@ -221,13 +239,13 @@ constexpr int SBX = 32, SBY = 8, SKC = 16;
 
 template <class Src, class Epi>
 __global__ void __launch_bounds__(SBX* SBY)
-    k_stencil(int n, int stencil, real_t<typename Src::type> s, real_t<typename Src::type> g,
+    k_stencil(int n, int nz, int stencil, real_t<typename Src::type> s, real_t<typename Src::type> g,
               real_t<typename Src::type> g2, Src src, Epi epi) {
   using T = typename Src::type;
   const int i = blockIdx.x * SBX + threadIdx.x;
   const int j = blockIdx.y * SBY + threadIdx.y;
   const int k0 = blockIdx.z * SKC;
-  const int k1 = min(n, k0 + SKC);
+  const int k1 = min(nz, k0 + SKC);
   const long nn = n, n2 = nn * nn;
   typename Epi::State st;
   epi.init(st);
@@ -238,11 +256,20 @@ __global__ void __launch_bounds__(SBX* SBY)
       if (periodic) {
         ii = ii < 0 ? ii + n : (ii >= n ? ii - n : ii);
         jj = jj < 0 ? jj + n : (jj >= n ? jj - n : jj);
-        kk = kk < 0 ? kk + n : (kk >= n ? kk - n : kk);
-      } else if (ii < 0 || ii >= n || jj < 0 || jj >= n || kk < 0 || kk >= n) {
+      } else if (ii < 0 || ii >= n || jj < 0 || jj >= n) {
         return zero_v<T>();
       }
-      return src.ld1(ii + (long)jj * nn + (long)kk * n2);
+      const long off = ii + (long)jj * nn;
+      if (kk < 0) {
+        if (src.glo) return src.ld1f(src.glo, off);
+        if (!periodic) return zero_v<T>();
+        kk += nz;
+      } else if (kk >= nz) {
+        if (src.ghi) return src.ld1f(src.ghi, off);
+        if (!periodic) return zero_v<T>();
+        kk -= nz;
+      }
+      return src.ld1(off + (long)kk * n2);
     };
     T zm = at(i, j, k0 - 1), x = at(i, j, k0);
     for (int k = k0; k < k1; ++k) {
@@ -262,14 +289,14 @@ constexpr int VX = 32, VY = 4, VKC = 16;
 
 template <class Src, class Epi>
 __global__ void __launch_bounds__(VX* VY)
-    k_stencil4(int n, int stencil, typename Src::type s, typename Src::type g, typename Src::type g2, Src src,
-               Epi epi) {
+    k_stencil4(int n, int nz, int stencil, typename Src::type s, typename Src::type g, typename Src::type g2,
+               Src src, Epi epi) {
   using T = typename Src::type;
   const int lane = threadIdx.x;
   const int i0 = (blockIdx.x * VX + lane) * 4;
   const int j = blockIdx.y * VY + threadIdx.y;
   const int k0 = blockIdx.z * VKC;
-  const int k1 = min(n, k0 + VKC);
+  const int k1 = min(nz, k0 + VKC);
   const long nn = n, n2 = nn * nn;
   const bool periodic = stencil != 0;
   const bool act = i0 < n;
@@ -277,26 +304,38 @@ __global__ void __launch_bounds__(VX* VY)
   epi.init(st);
   if (j < n) {  // warp-uniform: every lane of the warp shares j
     auto wrap = [&](int v) { return v < 0 ? v + n : (v >= n ? v - n : v); };
+    // plane kk in [-1, nz]: the local slab, or a ghost plane / the
+    // undivided grid's wrap-around / a Dirichlet zero outside it
     auto row = [&](int jj, int kk) -> V4<T> {
       if (periodic) {
         jj = wrap(jj);
-        kk = wrap(kk);
-      } else if (jj < 0 || jj >= n || kk < 0 || kk >= n) {
+      } else if (jj < 0 || jj >= n) {
         return zero4<T>();
       }
       if (!act) return zero4<T>();
-      return src.ld4(i0 + (long)jj * nn + (long)kk * n2);
+      const long off = i0 + (long)jj * nn;
+      if (kk < 0) {
+        if (src.glo) return src.ld4f(src.glo, off);
+        if (!periodic) return zero4<T>();
+        kk += nz;
+      } else if (kk >= nz) {
+        if (src.ghi) return src.ld4f(src.ghi, off);
+        if (!periodic) return zero4<T>();
+        kk -= nz;
+      }
+      return src.ld4(off + (long)kk * n2);
     };
     // i-neighbours that cross the lane's 4-vector: lane 0 needs i0-1,
     // lane 31 / the last active lane needs i0+4 (loaded, everything else shuffled)
+    // (only ever needed for planes inside the slab; the k+1 prefetch past the
+    // last plane is never consumed)
     auto edge = [&](int ii, int kk) -> T {
       if (periodic) {
         ii = wrap(ii);
-        kk = wrap(kk);
-      } else if (ii < 0 || ii >= n || kk < 0 || kk >= n) {
+      } else if (ii < 0 || ii >= n) {
         return zero_v<T>();
       }
-      if (!act) return zero_v<T>();
+      if (!act || kk < 0 || kk >= nz) return zero_v<T>();
       return src.ld1(ii + (long)j * nn + (long)kk * n2);
     };
     const bool need_l = lane == 0;
@@ -340,18 +379,26 @@ void launch(const StencilSpec& sp, Src src, Epi epi, cudaStream_t st, const char
   using T = typename Src::type;
   using R = real_t<T>;
   const int n = sp.n;
+  const int nz = sp.nz > 0 ? sp.nz : n;
+  if (sp.halo) {
+    // split grid: the neighbours' boundary planes of the raw source vector
+    const void* g[2];
+    halo_exchange(*sp.halo, src.p, sizeof(typename Src::raw), sp.stencil != 0, st, g);
+    src.glo = static_cast<const typename Src::raw*>(g[0]);
+    src.ghi = static_cast<const typename Src::raw*>(g[1]);
+  }
   if constexpr (!is_cplx<T>) {
     if (n % 4 == 0) {
-      const dim3 grid((n / 4 + VX - 1) / VX, (n + VY - 1) / VY, (n + VKC - 1) / VKC);
-      k_stencil4<Src, Epi><<<grid, dim3(VX, VY), 0, st>>>(n, sp.stencil, (R)sp.sigma, (R)sp.gamma, (R)sp.gamma2, src,
-                                                          epi);
+      const dim3 grid((n / 4 + VX - 1) / VX, (n + VY - 1) / VY, (nz + VKC - 1) / VKC);
+      k_stencil4<Src, Epi><<<grid, dim3(VX, VY), 0, st>>>(n, nz, sp.stencil, (R)sp.sigma, (R)sp.gamma, (R)sp.gamma2,
+                                                          src, epi);
       LAUNCHED(name);
       return;
     }
   }
-  const dim3 grid((n + SBX - 1) / SBX, (n + SBY - 1) / SBY, (n + SKC - 1) / SKC);
-  k_stencil<Src, Epi><<<grid, dim3(SBX, SBY), 0, st>>>(n, sp.stencil, (R)sp.sigma, (R)sp.gamma, (R)sp.gamma2, src,
-                                                       epi);
+  const dim3 grid((n + SBX - 1) / SBX, (n + SBY - 1) / SBY, (nz + SKC - 1) / SKC);
+  k_stencil<Src, Epi><<<grid, dim3(SBX, SBY), 0, st>>>(n, nz, sp.stencil, (R)sp.sigma, (R)sp.gamma, (R)sp.gamma2,
+                                                       src, epi);
   LAUNCHED(name);
 }
 

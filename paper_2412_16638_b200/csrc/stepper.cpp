@@ -36,7 +36,12 @@ static const StepperConfig& device_checked(const StepperConfig& cfg) {
 }
 
 Stepper::Stepper(const StepperConfig& cfg)
-    : cfg_(device_checked(cfg)), prob_(make_problem(cfg.eq, cfg.n, cfg.nu)), m_(prob_.size()), flags_(256),
+    : cfg_(device_checked(cfg)),
+      slab_(make_slab(cfg.n, cfg.comm)),
+      halo_(slab_.split() ? std::make_unique<Halo>(slab_) : nullptr),
+      prob_(make_problem(cfg.eq, cfg.n, cfg.nu, slab_.k0, slab_.nz)),
+      m_(prob_.size()),
+      flags_(256),
       timer_(cfg.timings) {
   const Tableau& t = cfg_.tab;
   const int q = t.q;
@@ -44,7 +49,8 @@ Stepper::Stepper(const StepperConfig& cfg)
   CUDA_CHECK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
   const bool heat = cfg_.eq == Equation::Heat;
   solve_dtype_ = (heat ? 0 : 2) + (cfg_.f32 ? 0 : 1);
-  kspec_ = rhs_spec(prob_);
+  const Halo* halo = halo_.get();
+  kspec_ = rhs_spec(prob_, halo);
 
   // need_f64 / need_feps masks (stepper.cpp:60-66)
   need_f64_.assign(q, 0);
@@ -69,9 +75,9 @@ Stepper::Stepper(const StepperConfig& cfg)
     if (idx < 0) {
       StageSolver s;
       s.a = a;
-      s.op = std::make_unique<StencilOp>(solve_dtype_, stage_spec(prob_, cfg_.tau, a));
+      s.op = std::make_unique<StencilOp>(solve_dtype_, stage_spec(prob_, cfg_.tau, a, halo));
       if (cfg_.precond == 0)
-        s.pre = make_stage_fastdiag(solve_dtype_, prob_, cfg_.tau, a, num);
+        s.pre = make_stage_fastdiag(solve_dtype_, prob_, cfg_.tau, a, num, halo);
       else if (cfg_.precond == 2)
         s.pre = make_block_jacobi(solve_dtype_, prob_, cfg_.tau, a, cfg_.block,
                                   cfg_.block_storage < 0 ? solve_dtype_ % 2 : cfg_.block_storage);
@@ -102,11 +108,12 @@ Stepper::Stepper(const StepperConfig& cfg)
     const size_t s = dtype_size(solve_dtype_);
     bsol_.alloc(m * s);
     xsol_.alloc(m * s);
+    Comm* comm = slab_.split() ? slab_.comm : nullptr;
     switch (solve_dtype_) {
-      case 0: w32_ = std::make_unique<KrylovWork<float>>(m); break;
-      case 1: w64_ = std::make_unique<KrylovWork<double>>(m); break;
-      case 2: wc32_ = std::make_unique<KrylovWork<c32>>(m); break;
-      default: wc64_ = std::make_unique<KrylovWork<c64>>(m); break;
+      case 0: w32_ = std::make_unique<KrylovWork<float>>(m); w32_->comm = comm; break;
+      case 1: w64_ = std::make_unique<KrylovWork<double>>(m); w64_->comm = comm; break;
+      case 2: wc32_ = std::make_unique<KrylovWork<c32>>(m); wc32_->comm = comm; break;
+      default: wc64_ = std::make_unique<KrylovWork<c64>>(m); wc64_->comm = comm; break;
     }
   }
   stream_sync(st_);
@@ -135,10 +142,15 @@ void Stepper::step(double* u, StepTrace& trace) {
     return flags_.dev(next++);
   };
   int* sink = flags_.dev(0);
+  // a split grid raises a check on every rank when any rank saw it, so all
+  // ranks throw the same (first) error and none is left waiting
   auto raise_flags = [&]() {
     stream_sync(st_);
-    for (const Check& c : checks)
-      if (flags_.value(c.slot)) MPRKB_THROW(c.code, c.msg);
+    std::vector<double> v(checks.size());
+    for (size_t i = 0; i < checks.size(); ++i) v[i] = flags_.value(checks[i].slot) ? 1.0 : 0.0;
+    if (slab_.split() && !v.empty()) slab_.comm->allreduce_max(v.data(), (int)v.size());
+    for (size_t i = 0; i < checks.size(); ++i)
+      if (v[i] != 0.0) MPRKB_THROW(checks[i].code, checks[i].msg);
   };
 
   const Tableau& t = cfg_.tab;
@@ -305,6 +317,8 @@ IntegrationResult integrate_with(Stepper& stepper, const std::vector<double>* re
     target = &exact;
   }
   if (target != nullptr) {
+    // (split grid: state and reference are this rank's slab; the norms are
+    // completed across ranks, the sum of squares in rank order)
     if (target->size() != res.state.size()) MPRKB_THROW(2, "integrate: reference state has the wrong length");
     double worst = 0.0, sq = 0.0;
     for (size_t i = 0; i < res.state.size(); ++i) {
@@ -312,8 +326,15 @@ IntegrationResult integrate_with(Stepper& stepper, const std::vector<double>* re
       worst = std::max(worst, std::abs(e));
       sq += e * e;
     }
+    double total = static_cast<double>(res.state.size());
+    if (stepper.slab().split()) {
+      Comm* c = stepper.slab().comm;
+      c->allreduce_max(&worst, 1);
+      c->allreduce_sum(&sq, 1);
+      total = static_cast<double>(stepper.slab().n) * stepper.slab().n * stepper.slab().n;
+    }
     res.error_max = worst;
-    res.error_l2 = std::sqrt(sq / static_cast<double>(res.state.size()));
+    res.error_l2 = std::sqrt(sq / total);
   }
   res.wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - wall_start).count();
   return res;

@@ -26,6 +26,9 @@ struct StepperConfig {
   double nu = 0.0;
   bool timings = false;
   int basis_storage = -1;  // GMRES basis storage (-1: working precision; 4: fp16)
+  // Split grid: this rank steps k-planes [rank n/P, (rank+1) n/P)
+  // and exchanges halos / transposes / scalars through comm (null: undivided).
+  Comm* comm = nullptr;
 };
 
 struct StepTrace {
@@ -40,6 +43,7 @@ class Stepper {
   // one step on device state u (n^3 doubles), in place
   void step(double* u_dev, StepTrace& trace);
   const Problem& problem() const { return prob_; }
+  const Slab& slab() const { return slab_; }
   cudaStream_t stream() const { return st_; }
   size_t size() const { return m_; }
   EventTimer& timer() { return timer_; }
@@ -52,6 +56,8 @@ class Stepper {
     std::unique_ptr<Op> pre;
   };
   StepperConfig cfg_;
+  Slab slab_;
+  std::unique_ptr<Halo> halo_;  // split grid only
   Problem prob_;
   size_t m_;
   cudaStream_t st_ = nullptr;

@@ -110,30 +110,34 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN))
   }
 }
 
+// cols = elements per contracted fibre set: R -> fibres (j,k), M -> (i, planes)
+// with cols / n planes, L -> columns (i,j) of one k-plane (= its stride).
+// The undivided grid has cols = n^2; a k-slab (R, M) has n * nz, a j-slab (L)
+// n * ny.
 template <class T, int BM, int BN, int BK, int TM, int TN, bool EXACT, bool DIAG>
-void launch_generic_cfg(int side, int n, const T* q, const T* x, T* out, const T* pd, cudaStream_t st) {
+void launch_generic_cfg(int side, int n, long cols, const T* q, const T* x, T* out, const T* pd, cudaStream_t st) {
   constexpr int NT = (BM / TM) * (BN / TN);
   const long nn = n, n2 = nn * nn;
   if (side == 2) {
-    dim3 grid((unsigned)((nn + BN - 1) / BN), (unsigned)((n2 + BM - 1) / BM), 1);
-    k_tensor<T, BM, BN, BK, TM, TN, true, EXACT, DIAG><<<grid, NT, 0, st>>>(q, x, out, pd, n, n2, nn, nn, 0);
+    dim3 grid((unsigned)((nn + BN - 1) / BN), (unsigned)((cols + BM - 1) / BM), 1);
+    k_tensor<T, BM, BN, BK, TM, TN, true, EXACT, DIAG><<<grid, NT, 0, st>>>(q, x, out, pd, n, cols, nn, nn, 0);
   } else if (side == 1) {
-    dim3 grid((unsigned)((nn + BN - 1) / BN), (unsigned)((nn + BM - 1) / BM), (unsigned)nn);
+    dim3 grid((unsigned)((nn + BN - 1) / BN), (unsigned)((nn + BM - 1) / BM), (unsigned)(cols / nn));
     k_tensor<T, BM, BN, BK, TM, TN, false, EXACT, DIAG><<<grid, NT, 0, st>>>(q, x, out, pd, n, nn, nn, nn, n2);
   } else {
-    dim3 grid((unsigned)((n2 + BN - 1) / BN), (unsigned)((nn + BM - 1) / BM), 1);
-    k_tensor<T, BM, BN, BK, TM, TN, false, EXACT, DIAG><<<grid, NT, 0, st>>>(q, x, out, pd, n, nn, n2, n2, 0);
+    dim3 grid((unsigned)((cols + BN - 1) / BN), (unsigned)((nn + BM - 1) / BM), 1);
+    k_tensor<T, BM, BN, BK, TM, TN, false, EXACT, DIAG><<<grid, NT, 0, st>>>(q, x, out, pd, n, nn, cols, cols, 0);
   }
   LAUNCHED("tensor");
 }
 
 template <class T, bool EXACT, bool DIAG>
-void launch_generic(int side, int n, const T* q, const T* x, T* out, const T* pd, cudaStream_t st) {
+void launch_generic(int side, int n, long cols, const T* q, const T* x, T* out, const T* pd, cudaStream_t st) {
   if constexpr (sizeof(T) <= 4) {
-    if (n >= 128) return launch_generic_cfg<T, 128, 128, 8, 8, 8, EXACT, DIAG>(side, n, q, x, out, pd, st);
+    if (n >= 128) return launch_generic_cfg<T, 128, 128, 8, 8, 8, EXACT, DIAG>(side, n, cols, q, x, out, pd, st);
   }
-  if (n >= 48) return launch_generic_cfg<T, 64, 64, 8, 4, 4, EXACT, DIAG>(side, n, q, x, out, pd, st);
-  launch_generic_cfg<T, 32, 32, 8, 2, 2, EXACT, DIAG>(side, n, q, x, out, pd, st);
+  if (n >= 48) return launch_generic_cfg<T, 64, 64, 8, 4, 4, EXACT, DIAG>(side, n, cols, q, x, out, pd, st);
+  launch_generic_cfg<T, 32, 32, 8, 2, 2, EXACT, DIAG>(side, n, cols, q, x, out, pd, st);
 }
 
 // ---------------------------------------------------------------------------
@@ -305,64 +309,65 @@ __global__ void __launch_bounds__((BM / TM) * (BN / TN), sizeof(T) == 4 ? 2 : 1)
 }
 
 template <class T, int BM, int BN, int BK, int TM, int TN, bool DIAG, bool FOLD>
-void launch_fast_cfg(int side, int n, const T* q, const T* x, T* out, const T* pd, cudaStream_t st) {
+void launch_fast_cfg(int side, int n, long cols, const T* q, const T* x, T* out, const T* pd, cudaStream_t st) {
   constexpr int NT = (BM / TM) * (BN / TN);
   const long nn = n, n2 = nn * nn;
   const long nq = FOLD ? (nn + 1) / 2 : nn;  // rows of Q actually used
   if (side == 2) {
-    dim3 grid((unsigned)((nq + BN - 1) / BN), (unsigned)((n2 + BM - 1) / BM), 1);
-    k_tensor_fast<T, BM, BN, BK, TM, TN, true, DIAG, FOLD><<<grid, NT, 0, st>>>(q, x, out, pd, n, n2, nq, nn, 0);
+    dim3 grid((unsigned)((nq + BN - 1) / BN), (unsigned)((cols + BM - 1) / BM), 1);
+    k_tensor_fast<T, BM, BN, BK, TM, TN, true, DIAG, FOLD><<<grid, NT, 0, st>>>(q, x, out, pd, n, cols, nq, nn, 0);
   } else if (side == 1) {
-    dim3 grid((unsigned)((nn + BN - 1) / BN), (unsigned)((nq + BM - 1) / BM), (unsigned)nn);
+    dim3 grid((unsigned)((nn + BN - 1) / BN), (unsigned)((nq + BM - 1) / BM), (unsigned)(cols / nn));
     k_tensor_fast<T, BM, BN, BK, TM, TN, false, DIAG, FOLD><<<grid, NT, 0, st>>>(q, x, out, pd, n, nq, nn, nn, n2);
   } else {
-    dim3 grid((unsigned)((n2 + BN - 1) / BN), (unsigned)((nq + BM - 1) / BM), 1);
-    k_tensor_fast<T, BM, BN, BK, TM, TN, false, DIAG, FOLD><<<grid, NT, 0, st>>>(q, x, out, pd, n, nq, n2, n2, 0);
+    dim3 grid((unsigned)((cols + BN - 1) / BN), (unsigned)((nq + BM - 1) / BM), 1);
+    k_tensor_fast<T, BM, BN, BK, TM, TN, false, DIAG, FOLD><<<grid, NT, 0, st>>>(q, x, out, pd, n, nq, cols, cols, 0);
   }
   LAUNCHED("tensor_fast");
 }
 
 template <class T, bool DIAG, bool FOLD>
-void launch_fast(int side, int n, const T* q, const T* x, T* out, const T* pd, cudaStream_t st) {
+void launch_fast(int side, int n, long cols, const T* q, const T* x, T* out, const T* pd, cudaStream_t st) {
   if constexpr (sizeof(T) == 4 && FOLD)  // two accumulator sets: halve the thread tile
-    launch_fast_cfg<T, 128, 64, 16, 8, 4, DIAG, FOLD>(side, n, q, x, out, pd, st);
+    launch_fast_cfg<T, 128, 64, 16, 8, 4, DIAG, FOLD>(side, n, cols, q, x, out, pd, st);
   else if constexpr (sizeof(T) == 4)
-    launch_fast_cfg<T, 128, 128, 8, 8, 8, DIAG, FOLD>(side, n, q, x, out, pd, st);
+    launch_fast_cfg<T, 128, 128, 8, 8, 8, DIAG, FOLD>(side, n, cols, q, x, out, pd, st);
   else
-    launch_fast_cfg<T, 64, 64, 16, 4, 4, DIAG, FOLD>(side, n, q, x, out, pd, st);
+    launch_fast_cfg<T, 64, 64, 16, 4, 4, DIAG, FOLD>(side, n, cols, q, x, out, pd, st);
 }
 
 }  // namespace
 
 template <class T>
 void tensor_apply(int side, int n, const T* q, const T* x, T* out, const T* pd, Numerics num, cudaStream_t st,
-                  bool fold) {
+                  bool fold, long cols) {
+  if (cols <= 0) cols = (long)n * n;
   if (num == Numerics::Parity) {
     if (pd)
-      launch_generic<T, true, true>(side, n, q, x, out, pd, st);
+      launch_generic<T, true, true>(side, n, cols, q, x, out, pd, st);
     else
-      launch_generic<T, true, false>(side, n, q, x, out, pd, st);
+      launch_generic<T, true, false>(side, n, cols, q, x, out, pd, st);
     return;
   }
   if constexpr (!is_cplx<T>) {
     if (n % 4 == 0 && n >= 64) {
       if (fold) {
-        if (pd) return launch_fast<T, true, true>(side, n, q, x, out, pd, st);
-        return launch_fast<T, false, true>(side, n, q, x, out, pd, st);
+        if (pd) return launch_fast<T, true, true>(side, n, cols, q, x, out, pd, st);
+        return launch_fast<T, false, true>(side, n, cols, q, x, out, pd, st);
       }
-      if (pd) return launch_fast<T, true, false>(side, n, q, x, out, pd, st);
-      return launch_fast<T, false, false>(side, n, q, x, out, pd, st);
+      if (pd) return launch_fast<T, true, false>(side, n, cols, q, x, out, pd, st);
+      return launch_fast<T, false, false>(side, n, cols, q, x, out, pd, st);
     }
   }
   if (pd)
-    launch_generic<T, false, true>(side, n, q, x, out, pd, st);
+    launch_generic<T, false, true>(side, n, cols, q, x, out, pd, st);
   else
-    launch_generic<T, false, false>(side, n, q, x, out, pd, st);
+    launch_generic<T, false, false>(side, n, cols, q, x, out, pd, st);
 }
 
-template void tensor_apply<float>(int, int, const float*, const float*, float*, const float*, Numerics, cudaStream_t, bool);
-template void tensor_apply<double>(int, int, const double*, const double*, double*, const double*, Numerics, cudaStream_t, bool);
-template void tensor_apply<c32>(int, int, const c32*, const c32*, c32*, const c32*, Numerics, cudaStream_t, bool);
-template void tensor_apply<c64>(int, int, const c64*, const c64*, c64*, const c64*, Numerics, cudaStream_t, bool);
+template void tensor_apply<float>(int, int, const float*, const float*, float*, const float*, Numerics, cudaStream_t, bool, long);
+template void tensor_apply<double>(int, int, const double*, const double*, double*, const double*, Numerics, cudaStream_t, bool, long);
+template void tensor_apply<c32>(int, int, const c32*, const c32*, c32*, const c32*, Numerics, cudaStream_t, bool, long);
+template void tensor_apply<c64>(int, int, const c64*, const c64*, c64*, const c64*, Numerics, cudaStream_t, bool, long);
 
 }  // namespace mprkb

@@ -168,7 +168,7 @@ template <int SIDE, bool DIAG>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_tensor_tc(const __grid_constant__ CUtensorMap xmap, float* __restrict__ C, const float* __restrict__ pd,
                 const float* __restrict__ qh_pack, const float* __restrict__ ql_pack, int n, int col_tiles,
-                int num_tiles) {
+                int num_tiles, long ldc) {
   extern __shared__ unsigned char smem_raw[];
   TcSmem& S = *reinterpret_cast<TcSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -336,7 +336,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             C[o] = v;
           }
         } else {
-          const long base = SIDE == 1 ? (long)T.plane * n2 + a * nn + T.col0 + cc : a * n2 + T.col0 + cc;
+          const long base = SIDE == 1 ? (long)T.plane * n2 + a * nn + T.col0 + cc : a * ldc + T.col0 + cc;
 #pragma unroll
           for (int j = 0; j < 32; j += 4) {
             float4 v = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]), __uint_as_float(r[j + 2]),
@@ -390,7 +390,8 @@ CUtensorMap make_map(const float* x, int rank, const cuuint64_t* dims, const cuu
 }
 
 template <int SIDE, bool DIAG>
-void launch_tc(int n, const float* x, float* out, const float* pd, const float* qh, const float* ql, cudaStream_t st) {
+void launch_tc(int n, long cols, const float* x, float* out, const float* pd, const float* qh, const float* ql,
+               cudaStream_t st) {
   const size_t smem = sizeof(TcSmem) + 1024;
   static bool configured = false;
   if (!configured) {
@@ -401,26 +402,27 @@ void launch_tc(int n, const float* x, float* out, const float* pd, const float* 
   CUtensorMap map;
   int col_tiles;  // X column tiles per (plane)
   int planes = 1;
-  if (SIDE == 2) {  // X as [n^2 fibres][n q]
-    const cuuint64_t dims[2] = {nn, n2}, strides[1] = {nn * 4};
+  const cuuint64_t cc = (cuuint64_t)cols;
+  if (SIDE == 2) {  // X as [cols fibres][n q]
+    const cuuint64_t dims[2] = {nn, cc}, strides[1] = {nn * 4};
     const cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)TC_BN};
     map = make_map(x, 2, dims, strides, box);
-    col_tiles = (int)(n2 / TC_BN);
-  } else if (SIDE == 1) {  // X as [n k][n q][n i]
-    const cuuint64_t dims[3] = {nn, nn, nn}, strides[2] = {nn * 4, n2 * 4};
+    col_tiles = (int)(cc / TC_BN);
+  } else if (SIDE == 1) {  // X as [cols/n k][n q][n i]
+    const cuuint64_t dims[3] = {nn, nn, cc / nn}, strides[2] = {nn * 4, n2 * 4};
     const cuuint32_t box[3] = {(cuuint32_t)TC_BN, (cuuint32_t)TC_BK, 1};
     map = make_map(x, 3, dims, strides, box);
     col_tiles = (int)(nn / TC_BN);
-    planes = n;
-  } else {  // X as [n q][n^2 c]
-    const cuuint64_t dims[2] = {n2, nn}, strides[1] = {n2 * 4};
+    planes = (int)(cc / nn);
+  } else {  // X as [n q][cols c]
+    const cuuint64_t dims[2] = {cc, nn}, strides[1] = {cc * 4};
     const cuuint32_t box[2] = {(cuuint32_t)TC_BN, (cuuint32_t)TC_BK};
     map = make_map(x, 2, dims, strides, box);
-    col_tiles = (int)(n2 / TC_BN);
+    col_tiles = (int)(cc / TC_BN);
   }
   const int num_tiles = (n / TC_BM) * col_tiles * planes;
   const int grid = num_tiles < sm_count() ? num_tiles : sm_count();
-  k_tensor_tc<SIDE, DIAG><<<grid, TC_THREADS, smem, st>>>(map, out, pd, qh, ql, n, col_tiles, num_tiles);
+  k_tensor_tc<SIDE, DIAG><<<grid, TC_THREADS, smem, st>>>(map, out, pd, qh, ql, n, col_tiles, num_tiles, cols);
   LAUNCHED("tensor_tc");
 }
 
@@ -428,21 +430,24 @@ void launch_tc(int n, const float* x, float* out, const float* pd, const float* 
 
 // N = 256 columns per CTA and 128 Q rows: n % 256 == 0 for the M side's i tiles.
 bool tensor_tc_supported(int n) { return n >= 256 && n % 256 == 0 && n <= 2048; }
+// slab layouts: every column extent must hold whole 256-column tiles
+bool tensor_tc_supported_cols(int n, long cols) { return tensor_tc_supported(n) && cols % TC_BN == 0 && cols % n == 0; }
 
 void tensor_apply_tc(int side, int n, const float* q_hi_packed, const float* q_lo_packed, const float* x, float* out,
-                     const float* pd, cudaStream_t st) {
+                     const float* pd, cudaStream_t st, long cols) {
+  if (cols <= 0) cols = (long)n * n;
   switch (side) {
     case 2:
-      pd ? launch_tc<2, true>(n, x, out, pd, q_hi_packed, q_lo_packed, st)
-         : launch_tc<2, false>(n, x, out, pd, q_hi_packed, q_lo_packed, st);
+      pd ? launch_tc<2, true>(n, cols, x, out, pd, q_hi_packed, q_lo_packed, st)
+         : launch_tc<2, false>(n, cols, x, out, pd, q_hi_packed, q_lo_packed, st);
       break;
     case 1:
-      pd ? launch_tc<1, true>(n, x, out, pd, q_hi_packed, q_lo_packed, st)
-         : launch_tc<1, false>(n, x, out, pd, q_hi_packed, q_lo_packed, st);
+      pd ? launch_tc<1, true>(n, cols, x, out, pd, q_hi_packed, q_lo_packed, st)
+         : launch_tc<1, false>(n, cols, x, out, pd, q_hi_packed, q_lo_packed, st);
       break;
     default:
-      pd ? launch_tc<0, true>(n, x, out, pd, q_hi_packed, q_lo_packed, st)
-         : launch_tc<0, false>(n, x, out, pd, q_hi_packed, q_lo_packed, st);
+      pd ? launch_tc<0, true>(n, cols, x, out, pd, q_hi_packed, q_lo_packed, st)
+         : launch_tc<0, false>(n, cols, x, out, pd, q_hi_packed, q_lo_packed, st);
       break;
   }
 }
