@@ -29,6 +29,19 @@ Slab make_slab(int n, Comm* comm) {
   return s;
 }
 
+Halo::Halo(const Slab& s) : slab(s) {
+  ghost.alloc((size_t)2 * s.n * s.n * 16);
+  CUDA_CHECK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+  CUDA_CHECK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  CUDA_CHECK(cudaEventCreateWithFlags(&arrived, cudaEventDisableTiming));
+}
+
+Halo::~Halo() {
+  if (cs) cudaStreamDestroy(cs);
+  if (ready) cudaEventDestroy(ready);
+  if (arrived) cudaEventDestroy(arrived);
+}
+
 void halo_exchange(const Halo& h, const void* x, size_t elem, bool periodic, cudaStream_t st, const void* g[2]) {
   const Slab& s = h.slab;
   const size_t plane = (size_t)s.n * s.n * elem;

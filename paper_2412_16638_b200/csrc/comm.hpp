@@ -89,10 +89,18 @@ Slab make_slab(int n, Comm* comm);
 
 // Slab + the ghost-plane scratch its stencils share (2 planes of the widest
 // scalar).  All users run on one stream, so one pair of planes suffices.
+// The exchange runs on its own stream `cs` so the interior planes of a
+// stencil (which need no ghost) overlap it; `ready` / `arrived` order it
+// against the compute stream.
 struct Halo {
   Slab slab;
   DevBuf ghost;
-  explicit Halo(const Slab& s) : slab(s) { ghost.alloc((size_t)2 * s.n * s.n * 16); }
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ready = nullptr, arrived = nullptr;
+  explicit Halo(const Slab& s);
+  ~Halo();
+  Halo(const Halo&) = delete;
+  Halo& operator=(const Halo&) = delete;
 };
 
 }  // namespace mprkb

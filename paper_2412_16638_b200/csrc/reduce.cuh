@@ -52,8 +52,8 @@ __device__ __forceinline__ void grid_reduce(double (&v)[NV], const RedSlot& s) {
   __shared__ bool last;
   const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
   const int nth = blockDim.x * blockDim.y * blockDim.z;
-  const unsigned bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-  const unsigned nb = gridDim.x * gridDim.y * gridDim.z;
+  const unsigned bid = s.base + blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+  const unsigned nb = s.total ? s.total : gridDim.x * gridDim.y * gridDim.z;
   block_sum<NV>(v);
   if (tid == 0) {
 #pragma unroll

@@ -11,6 +11,10 @@
 // Ghost values outside a Dirichlet domain are +0 and are always subtracted:
 // x - (+0) == x exactly (including -0), so the branch-free form is
 // bit-identical to the reference's conditional subtractions.
+#include <type_traits>
+#include <utility>
+
+#include "comm.hpp"
 #include "launch.hpp"
 #include "reduce.cuh"
 #include "vec.cuh"
@@ -234,18 +238,31 @@ struct EpiF32Forcing {
   __device__ void finish(State&) const {}
 };
 
+// Planes a CTA marches over.  kb < ke: chunks of `chunk` planes of [kb, ke)
+// by blockIdx.z.  kb < 0: the two boundary planes of a split slab (z = 0 ->
+// plane 0, z = 1 -> plane nz - 1), the part that waits for the ghosts.
+__device__ __forceinline__ void plane_range(int nz, int kb, int ke, int chunk, int& k0, int& k1) {
+  if (kb < 0) {
+    k0 = blockIdx.z == 0 ? 0 : nz - 1;
+    k1 = k0 + 1;
+  } else {
+    k0 = kb + (int)blockIdx.z * chunk;
+    k1 = min(ke, k0 + chunk);
+  }
+}
+
 // ---- scalar kernel -----------------------------------------------------------------
 constexpr int SBX = 32, SBY = 8, SKC = 16;
 
 template <class Src, class Epi>
 __global__ void __launch_bounds__(SBX* SBY)
-    k_stencil(int n, int nz, int stencil, real_t<typename Src::type> s, real_t<typename Src::type> g,
+    k_stencil(int n, int nz, int kb, int ke, int stencil, real_t<typename Src::type> s, real_t<typename Src::type> g,
               real_t<typename Src::type> g2, Src src, Epi epi) {
   using T = typename Src::type;
   const int i = blockIdx.x * SBX + threadIdx.x;
   const int j = blockIdx.y * SBY + threadIdx.y;
-  const int k0 = blockIdx.z * SKC;
-  const int k1 = min(nz, k0 + SKC);
+  int k0, k1;
+  plane_range(nz, kb, ke, SKC, k0, k1);
   const long nn = n, n2 = nn * nn;
   typename Epi::State st;
   epi.init(st);
@@ -289,14 +306,14 @@ constexpr int VX = 32, VY = 4, VKC = 16;
 
 template <class Src, class Epi>
 __global__ void __launch_bounds__(VX* VY)
-    k_stencil4(int n, int nz, int stencil, typename Src::type s, typename Src::type g, typename Src::type g2,
-               Src src, Epi epi) {
+    k_stencil4(int n, int nz, int kb, int ke, int stencil, typename Src::type s, typename Src::type g,
+               typename Src::type g2, Src src, Epi epi) {
   using T = typename Src::type;
   const int lane = threadIdx.x;
   const int i0 = (blockIdx.x * VX + lane) * 4;
   const int j = blockIdx.y * VY + threadIdx.y;
-  const int k0 = blockIdx.z * VKC;
-  const int k1 = min(nz, k0 + VKC);
+  int k0, k1;
+  plane_range(nz, kb, ke, VKC, k0, k1);
   const long nn = n, n2 = nn * nn;
   const bool periodic = stencil != 0;
   const bool act = i0 < n;
@@ -374,32 +391,72 @@ __global__ void __launch_bounds__(VX* VY)
   epi.finish(st);
 }
 
+// epilogues that fold a reduction: split it over several launches
+template <class E, class = void>
+struct has_red : std::false_type {};
+template <class E>
+struct has_red<E, std::void_t<decltype(std::declval<E&>().red)>> : std::true_type {};
+
+template <class Epi>
+void set_red_part(Epi& e, unsigned base, unsigned total) {
+  if constexpr (has_red<Epi>::value) {
+    e.red.base = base;
+    e.red.total = total;
+  }
+}
+
 template <class Src, class Epi>
 void launch(const StencilSpec& sp, Src src, Epi epi, cudaStream_t st, const char* name) {
   using T = typename Src::type;
   using R = real_t<T>;
   const int n = sp.n;
   const int nz = sp.nz > 0 ? sp.nz : n;
-  if (sp.halo) {
-    // split grid: the neighbours' boundary planes of the raw source vector
-    const void* g[2];
-    halo_exchange(*sp.halo, src.p, sizeof(typename Src::raw), sp.stencil != 0, st, g);
-    src.glo = static_cast<const typename Src::raw*>(g[0]);
-    src.ghi = static_cast<const typename Src::raw*>(g[1]);
-  }
-  if constexpr (!is_cplx<T>) {
-    if (n % 4 == 0) {
-      const dim3 grid((n / 4 + VX - 1) / VX, (n + VY - 1) / VY, (nz + VKC - 1) / VKC);
-      k_stencil4<Src, Epi><<<grid, dim3(VX, VY), 0, st>>>(n, nz, sp.stencil, (R)sp.sigma, (R)sp.gamma, (R)sp.gamma2,
-                                                          src, epi);
-      LAUNCHED(name);
-      return;
+  const bool vec = !is_cplx<T> && n % 4 == 0;
+  const dim3 block = vec ? dim3(VX, VY) : dim3(SBX, SBY);
+  const int chunk = vec ? VKC : SKC;
+  const unsigned gx = vec ? (n / 4 + VX - 1) / VX : (n + SBX - 1) / SBX;
+  const unsigned gy = vec ? (n + VY - 1) / VY : (n + SBY - 1) / SBY;
+  auto go = [&](int kb, int ke, unsigned gz, const Epi& e) {
+    if constexpr (!is_cplx<T>) {
+      if (vec) {
+        k_stencil4<Src, Epi><<<dim3(gx, gy, gz), block, 0, st>>>(n, nz, kb, ke, sp.stencil, (R)sp.sigma,
+                                                                (R)sp.gamma, (R)sp.gamma2, src, e);
+        LAUNCHED(name);
+        return;
+      }
     }
+    k_stencil<Src, Epi><<<dim3(gx, gy, gz), block, 0, st>>>(n, nz, kb, ke, sp.stencil, (R)sp.sigma, (R)sp.gamma,
+                                                             (R)sp.gamma2, src, e);
+    LAUNCHED(name);
+  };
+  if (!sp.halo) {
+    go(0, nz, (unsigned)((nz + chunk - 1) / chunk), epi);
+    return;
   }
-  const dim3 grid((n + SBX - 1) / SBX, (n + SBY - 1) / SBY, (nz + SKC - 1) / SKC);
-  k_stencil<Src, Epi><<<grid, dim3(SBX, SBY), 0, st>>>(n, nz, sp.stencil, (R)sp.sigma, (R)sp.gamma, (R)sp.gamma2,
-                                                       src, epi);
-  LAUNCHED(name);
+  // Split grid: the neighbours' boundary planes travel on the halo stream
+  // while the interior planes [1, nz - 1) — which need no ghost — compute;
+  // the two boundary planes follow once the ghosts arrived.
+  const Halo& h = *sp.halo;
+  CUDA_CHECK(cudaEventRecord(h.ready, st));  // x written; previous ghost readers done
+  CUDA_CHECK(cudaStreamWaitEvent(h.cs, h.ready, 0));
+  const void* g[2];
+  halo_exchange(h, src.p, sizeof(typename Src::raw), sp.stencil != 0, h.cs, g);
+  CUDA_CHECK(cudaEventRecord(h.arrived, h.cs));
+  src.glo = static_cast<const typename Src::raw*>(g[0]);
+  src.ghi = static_cast<const typename Src::raw*>(g[1]);
+  if (nz <= 2) {
+    CUDA_CHECK(cudaStreamWaitEvent(st, h.arrived, 0));
+    go(0, nz, 1, epi);
+    return;
+  }
+  const unsigned gz_in = (unsigned)((nz - 2 + chunk - 1) / chunk);
+  const unsigned nb_in = gx * gy * gz_in, nb_bd = gx * gy * 2;
+  Epi ein = epi, ebd = epi;
+  set_red_part(ein, 0, nb_in + nb_bd);
+  set_red_part(ebd, nb_in, nb_in + nb_bd);
+  go(1, nz - 1, gz_in, ein);
+  CUDA_CHECK(cudaStreamWaitEvent(st, h.arrived, 0));
+  go(-1, -1, 2, ebd);
 }
 
 }  // namespace

@@ -85,6 +85,10 @@ struct RedSlot {
   double* partial = nullptr;   // >= gridDim * NV doubles (device)
   unsigned* ticket = nullptr;  // zero between uses (device)
   double* out = nullptr;       // NV doubles, host-mapped pinned memory
+  // one reduction spread over several launches (interior + boundary planes of
+  // a split-grid stencil): this launch's CTAs are partials [base, base +
+  // gridDim) of `total`; the last CTA of ALL launches writes out (0: one launch)
+  unsigned base = 0, total = 0;
 };
 constexpr int kMaxPartials = 1 << 16;
 
