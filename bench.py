@@ -367,6 +367,9 @@ def run_cuda_arm(args):
                              "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"],
                              "peak_source": peaks["src"], "bytes_per_launch": 16.0 * m, "ms_per_launch": ms_sten},
             "clocks": clk,
+            "kernels": kernel_table(mp, N_GRID, peaks["hbm_gbs"]),
+            "kernels_note": (f"each kernel alone on {N_GRID}^3 vectors, CUDA events, algorithmic bytes "
+                             "(SURVEY.md §8d) / time vs MEASURED_PEAKS hbm_gbs"),
         }
         if not args.no_cpu_baseline and world == 1:
             budget = float(os.environ.get("MPRKB_CPU_BASELINE_S", "30"))
@@ -383,6 +386,26 @@ def run_cuda_arm(args):
     if line is not None:
         print(json.dumps(line))
     return 0
+
+
+KERNELS = ["copy_f32", "stencil_f64", "stencil_f32", "residual_f32", "apply_dot_f32", "apply_f64", "apply_f32",
+           "dot_f32", "cg_update_f32", "combine_7", "final_4", "block_jacobi_f16", "csr_f32", "csr_f16"]
+
+
+def kernel_table(mp, n, peak_gbs, reps=20):
+    """HBM-bound kernels of the step (and the SpMV / block-Jacobi extensions)
+    timed alone on n^3 vectors: achieved algorithmic GB/s and fraction of the
+    measured copy peak — the 'SpMV HBM GB/s' half of BASELINE.json's metric."""
+    import ctypes as C
+
+    out = {}
+    for k in KERNELS:
+        ms, by = C.c_double(), C.c_double()
+        mp.check(mp._c.lib.mprkb_kernel_bench(k.encode(), n, reps, C.byref(ms), C.byref(by)))
+        gbs = by.value / (ms.value * 1e-3) / 1e9
+        out[k] = {"us": round(ms.value * 1e3, 2), "bytes": by.value, "gbs": round(gbs, 1),
+                  "frac": round(gbs / peak_gbs, 4)}
+    return out
 
 
 def mp_fma_peak(mp, dtype):

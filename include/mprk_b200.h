@@ -76,6 +76,13 @@ long long mprkb_kernel_launches(void);
 /* Measured CUDA-core FMA throughput (TFLOP/s) for F32 or F64: the roofline
  * denominator of the FastDiag contractions (instrumentation). */
 int mprkb_measure_fma_peak(int dtype, double* tflops);
+/* Roofline helper: time one HBM-bound kernel of the step alone on n^3
+ * vectors (CUDA events, `reps` back-to-back launches after warm-up) and
+ * report ms per launch and the algorithmic bytes per launch.  `which`:
+ * copy_f32, stencil_f64, stencil_f32, residual_f32, apply_dot_f32, apply_f64,
+ * apply_f32, dot_f32, cg_update_f32, combine_7, final_4, block_jacobi_f16,
+ * csr_f32, csr_f16. */
+int mprkb_kernel_bench(const char* which, int n, int reps, double* ms_per_launch, double* bytes_per_launch);
 
 /* ---- problem setup (operators.cpp:29-79), host ------------------------------ */
 /* make_problem(eq, n): u0 (n^3), forcing (n^3; heat only, may be NULL),

@@ -136,6 +136,7 @@ SIGNATURES = {
     "mprkb_device_synchronize": (i32, []),
     "mprkb_kernel_launches": (C.c_longlong, []),
     "mprkb_measure_fma_peak": (i32, [i32, dptr]),
+    "mprkb_kernel_bench": (i32, [C.c_char_p, i32, i32, dptr, dptr]),
     "mprkb_make_problem": (i32, [i32, i32, vp, vp, dptr, dptr]),
     "mprkb_heat_exact": (i32, [i32, f64, vp]),
     "mprkb_builtin_tableau": (i32, [C.c_char_p, i32, ip, vp, vp, vp, vp]),

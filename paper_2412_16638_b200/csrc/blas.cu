@@ -131,6 +131,7 @@ void dot_real(size_t m, const T* a, const T* b, const RedSlot& red, Numerics num
     k_dot_seq<T><<<1, 256, 0, st>>>(m, a, b, init ? init[0] : 0.0, red.out);
   else
     k_dot_fast<T><<<wave(m), kBlock, 0, st>>>(m, a, b, red);
+  note_partials(red, num == Numerics::Parity ? 0 : wave(m));
   LAUNCHED("dot");
 }
 
@@ -142,6 +143,7 @@ void dot_conj(size_t m, const T* a, const T* b, const RedSlot& red, Numerics num
       k_cdot_seq<real_t<T>><<<1, 256, 0, st>>>(m, a, b, init ? init[0] : 0.0, init ? init[1] : 0.0, red.out);
     else
       k_cdot_fast<T><<<wave(m), kBlock, 0, st>>>(m, a, b, red);
+    note_partials(red, num == Numerics::Parity ? 0 : wave(m));
     LAUNCHED("dot");
   } else {
     dot_real<T>(m, a, b, red, num, st, init);
@@ -177,9 +179,10 @@ __global__ void __launch_bounds__(kBlock) k_vsub(size_t m, const T* b, const T* 
 
 template <class T>
 void vsub(size_t m, const T* b, const T* q, T* r, const RedSlot* red, cudaStream_t st) {
-  if (red)
+  if (red) {
     k_vsub<T, true><<<wave(m), kBlock, 0, st>>>(m, b, q, r, *red);
-  else
+    note_partials(*red, wave(m));
+  } else
     k_vsub<T, false><<<wave(m), kBlock, 0, st>>>(m, b, q, r, RedSlot{});
   LAUNCHED("vsub");
 }
@@ -215,9 +218,10 @@ __global__ void __launch_bounds__(kBlock) k_cg_update(size_t m, real_t<T> alpha,
 template <class T>
 void cg_update(size_t m, real_t<T> alpha, T* x, const T* p, T* r, const T* q, const RedSlot* red,
                cudaStream_t st) {
-  if (red)
+  if (red) {
     k_cg_update<T, true><<<wave(m), kBlock, 0, st>>>(m, alpha, x, p, r, q, *red);
-  else
+    note_partials(*red, wave(m));
+  } else
     k_cg_update<T, false><<<wave(m), kBlock, 0, st>>>(m, alpha, x, p, r, q, RedSlot{});
   LAUNCHED("cg_update");
 }

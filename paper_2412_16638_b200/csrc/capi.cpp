@@ -266,8 +266,10 @@ int mprkb_dot(int dtype, size_t m, const void* a, const void* b, int conjugate_d
         break;
     }
     stream_sync(st);
-    result[0] = red.host(0)[0];
-    if (cplx && conjugate_dot) result[1] = red.host(0)[1];
+    double v[2] = {0.0, 0.0};
+    red.result(0, cplx && conjugate_dot ? 2 : 1, v);
+    result[0] = v[0];
+    if (cplx && conjugate_dot) result[1] = v[1];
   });
 }
 
@@ -636,6 +638,12 @@ int mprkb_stepper_integrate(mprkb_stepper* s, const double* reference_host, size
 
 namespace mprkb {
 double fma_peak_tflops(int dtype);
+void kernel_bench(const std::string& which, int n, int reps, double* ms, double* bytes);
+}
+
+extern "C" int mprkb_kernel_bench(const char* which, int n, int reps, double* ms_per_launch,
+                                  double* bytes_per_launch) {
+  return guarded([&] { mprkb::kernel_bench(which ? which : "", n, reps, ms_per_launch, bytes_per_launch); });
 }
 
 extern "C" int mprkb_measure_fma_peak(int dtype, double* tflops) {

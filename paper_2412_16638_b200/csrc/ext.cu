@@ -225,6 +225,7 @@ void basis16_scale(size_t m, const T* w, T s, void* v, cudaStream_t st) {
 template <class T>
 void basis16_dot(size_t m, const void* v, const T* w, const RedSlot& red, cudaStream_t st) {
   k_dot16<T><<<grid_for(m, 256, 4), 256, 0, st>>>(m, (const typename Store16<T>::type*)v, w, red);
+  note_partials(red, grid_for(m, 256, 4));
   LAUNCHED("basis16_dot");
 }
 template <class T>

@@ -107,7 +107,8 @@ T to_dev(const H& h) {
 template <class T>
 std::array<double, 2> finish_red(KrylovWork<T>& w, int nv, cudaStream_t st) {
   stream_sync(st);
-  std::array<double, 2> v{w.red.host(0)[0], w.red.host(0)[1]};
+  std::array<double, 2> v{0.0, 0.0};
+  w.red.result(0, nv, v.data());
   if (w.comm && w.comm->size() > 1) w.comm->allreduce_sum(v.data(), nv);
   return v;
 }
@@ -138,7 +139,7 @@ std::array<double, 2> global_dot(KrylovWork<T>& w, bool conj, const T* a, const 
     if (r == c->rank()) {
       launch(acc.data());
       stream_sync(st);
-      acc = {w.red.host(0)[0], w.red.host(0)[1]};
+      w.red.result(0, nv, acc.data());
     }
     c->bcast_host(acc.data(), nv, r);
   }

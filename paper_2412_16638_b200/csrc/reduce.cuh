@@ -2,10 +2,11 @@
 //
 // FAST numerics: every kernel that produces a vector can also fold a dot
 // product into its epilogue.  Each CTA reduces its fp64 partial with warp
-// shuffles, writes it to `partial[cta]`, and the last CTA to finish (atomic
-// ticket) sums all partials in a FIXED order and writes the scalar straight to
-// host-mapped pinned memory.  One launch, no second pass over HBM, bitwise
-// reproducible run to run.  fp32 products are formed exactly in fp64
+// shuffles and writes it straight to host-mapped pinned memory; the host adds
+// the per-CTA partials in CTA order after the stream synchronize it needs
+// anyway (the Krylov scalars drive host control flow).  One launch, no second
+// pass over HBM, no fences or atomics in the kernel, bitwise reproducible run
+// to run.  fp32 products are formed exactly in fp64
 // (24+24 < 53 bits), so the result is far more accurate than the reference's
 // sequential fp32 sum (SURVEY.md §0 finding 2).
 //
@@ -46,38 +47,17 @@ __device__ __forceinline__ void block_sum(double (&v)[NV]) {
   }
 }
 
-// Finish a grid-wide reduction: every thread passes its private partial.
+// Finish a grid-wide reduction: every thread passes its private partial; the
+// CTA's tuple goes to host-mapped memory (RedSlot protocol, types.hpp).
 template <int NV>
 __device__ __forceinline__ void grid_reduce(double (&v)[NV], const RedSlot& s) {
-  __shared__ bool last;
+  static_assert(NV <= 2, "RedSlot tuples hold 2 doubles");
   const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
-  const int nth = blockDim.x * blockDim.y * blockDim.z;
   const unsigned bid = s.base + blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
-  const unsigned nb = s.total ? s.total : gridDim.x * gridDim.y * gridDim.z;
   block_sum<NV>(v);
-  if (tid == 0) {
+  if (tid == 0)
 #pragma unroll
-    for (int c = 0; c < NV; ++c) s.partial[(size_t)bid * NV + c] = v[c];
-    __threadfence();
-    const unsigned t = atomicAdd(s.ticket, 1u);
-    last = (t == nb - 1);
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  double w[NV];
-#pragma unroll
-  for (int c = 0; c < NV; ++c) w[c] = 0.0;
-  for (unsigned b = tid; b < nb; b += nth)
-#pragma unroll
-    for (int c = 0; c < NV; ++c) w[c] += __ldcg(s.partial + (size_t)b * NV + c);
-  block_sum<NV>(w);
-  if (tid == 0) {
-#pragma unroll
-    for (int c = 0; c < NV; ++c) s.out[c] = w[c];
-    *s.ticket = 0u;
-    __threadfence_system();
-  }
+    for (int c = 0; c < NV; ++c) s.partial[(size_t)bid * 2 + c] = v[c];
 }
 
 // ---- per-element dot contributions in fp64 --------------------------------------

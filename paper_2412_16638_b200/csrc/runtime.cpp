@@ -68,25 +68,42 @@ void DevBuf::release() {
 }
 
 Reducer::Reducer(int slots) : slots_(slots) {
-  partial_.alloc(sizeof(double) * 2 * kMaxPartials * slots);
-  ticket_.alloc(sizeof(unsigned) * slots);
-  CUDA_CHECK(cudaMemset(ticket_.get(), 0, sizeof(unsigned) * slots));
+  CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&partial_), sizeof(double) * 2 * kMaxPartials * slots,
+                           cudaHostAllocMapped));
   CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&host_), sizeof(double) * 2 * slots, cudaHostAllocMapped));
   std::memset(host_, 0, sizeof(double) * 2 * slots);
+  count_ = new int[slots]();
 }
 
 Reducer::~Reducer() {
+  if (partial_) cudaFreeHost(partial_);
   if (host_) cudaFreeHost(host_);
+  delete[] count_;
 }
 
 RedSlot Reducer::slot(int i) const {
   RedSlot s;
-  s.partial = partial_.as<double>() + (size_t)2 * kMaxPartials * i;
-  s.ticket = ticket_.as<unsigned>() + i;
   double* dptr = nullptr;
+  CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dptr), partial_ + (size_t)2 * kMaxPartials * i, 0));
+  s.partial = dptr;
   CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dptr), host_ + 2 * i, 0));
   s.out = dptr;
+  s.count = count_ + i;
   return s;
+}
+
+void Reducer::result(int i, int nv, double* v) const {
+  const int n = count_[i];
+  if (n <= 0) {
+    for (int c = 0; c < nv; ++c) v[c] = ((volatile double*)host_)[2 * i + c];
+    return;
+  }
+  const volatile double* p = partial_ + (size_t)2 * kMaxPartials * i;
+  for (int c = 0; c < nv; ++c) {
+    double s = 0.0;
+    for (int b = 0; b < n; ++b) s += p[(size_t)2 * b + c];
+    v[c] = s;
+  }
 }
 
 Flags::Flags(int count) : count_(count) {

@@ -41,8 +41,8 @@ class DevBuf {
   size_t bytes_ = 0;
 };
 
-// Grid-reduction targets: per slot a partial buffer + ticket on the device and
-// a host-mapped pinned result (read after a stream synchronize).
+// Grid-reduction targets (RedSlot protocol, types.hpp): per slot host-mapped
+// partial tuples + a result pair, and the host-side tuple count.
 class Reducer {
  public:
   explicit Reducer(int slots = 4);
@@ -50,12 +50,15 @@ class Reducer {
   Reducer(const Reducer&) = delete;
   Reducer& operator=(const Reducer&) = delete;
   RedSlot slot(int i) const;
-  const double* host(int i) const { return host_ + 2 * i; }
+  // after a stream synchronize: the reduction's nv value(s), partial tuples
+  // added in CTA order
+  void result(int i, int nv, double* v) const;
 
  private:
   int slots_;
-  DevBuf partial_, ticket_;
-  double* host_ = nullptr;
+  double* partial_ = nullptr;  // host pointer (mapped)
+  double* host_ = nullptr;     // result pairs (mapped)
+  int* count_ = nullptr;       // host only
 };
 
 // Device error flags (non-finite / overflow) with host-mapped mirror.

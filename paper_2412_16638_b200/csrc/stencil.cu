@@ -14,14 +14,27 @@
 #include <type_traits>
 #include <utility>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "comm.hpp"
 #include "launch.hpp"
 #include "reduce.cuh"
+#include "tma.cuh"
 #include "vec.cuh"
 
 namespace mprkb {
 
 namespace {
+
+// MPRKB_STENCIL_TMA=0 selects the register-marching kernel everywhere (A/B runs)
+bool tma_stencil_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("MPRKB_STENCIL_TMA");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
 
 __device__ __forceinline__ bool f32_overflows(double x) {
   return !isnan(x) && fabs(x) >= 3.402823669209384634633746074317e+38;
@@ -42,6 +55,7 @@ struct LdPlain {
   __device__ __forceinline__ V4<T> ld4f(const T* b, long i) const { return ::mprkb::ld4(b + i); }
   __device__ __forceinline__ T ld1(long i) const { return ld1f(p, i); }
   __device__ __forceinline__ V4<T> ld4(long i) const { return ld4f(p, i); }
+  __device__ __forceinline__ T cv(T r) const { return r; }
 };
 // double vector read in binary32 (apply_f F32: downcast(u), operators.cpp:88);
 // flags |u| past the binary32 range (precision.hpp:100-104)
@@ -63,6 +77,7 @@ struct LdD2F {
   }
   __device__ __forceinline__ float ld1(long i) const { return ld1f(p, i); }
   __device__ __forceinline__ V4<float> ld4(long i) const { return ld4f(p, i); }
+  __device__ __forceinline__ float cv(double r) const { return cvt(r); }
 };
 // float vector widened to double (exact)
 struct LdF2D {
@@ -78,6 +93,7 @@ struct LdF2D {
   }
   __device__ __forceinline__ double ld1(long i) const { return ld1f(p, i); }
   __device__ __forceinline__ V4<double> ld4(long i) const { return ld4f(p, i); }
+  __device__ __forceinline__ double cv(float r) const { return (double)r; }
 };
 
 template <class T>
@@ -125,12 +141,24 @@ __device__ __forceinline__ T point(int stencil, real_t<T> s, real_t<T> g, real_t
 }
 
 // ---- epilogues (vector form: 4 consecutive points; scalar form: 1) ---------------
+// Pre / pre4(i): the epilogue's own pointwise operand (b of a residual, g of
+// apply_f) for 4 points, loaded ahead of time by the pipelined kernel so its
+// latency overlaps the previous plane; v4() = v4p(pre4(i)).
+struct NoPre {};
+
 template <class T>
 struct EpiStore {
   T* out;
   struct State {};
+  using Pre = NoPre;
   __device__ void init(State&) const {}
-  __device__ __forceinline__ void v4(State&, long i, const V4<T>& v, const V4<T>&) const { st4(out + i, v); }
+  __device__ __forceinline__ Pre pre4(long) const { return {}; }
+  __device__ __forceinline__ void v4p(State&, long i, const V4<T>& v, const V4<T>&, const Pre&) const {
+    st4(out + i, v);
+  }
+  __device__ __forceinline__ void v4(State& s, long i, const V4<T>& v, const V4<T>& xc) const {
+    v4p(s, i, v, xc, pre4(i));
+  }
   __device__ __forceinline__ void s1(State&, long i, T v, T) const { out[i] = v; }
   __device__ void finish(State&) const {}
 };
@@ -143,9 +171,10 @@ struct EpiResidual {
   struct State {
     double v[1];
   };
+  using Pre = V4<T>;
   __device__ void init(State& s) const { s.v[0] = 0.0; }
-  __device__ __forceinline__ void v4(State& s, long i, const V4<T>& v, const V4<T>&) const {
-    const V4<T> bv = ld4rw(b + i);
+  __device__ __forceinline__ Pre pre4(long i) const { return ld4rw(b + i); }
+  __device__ __forceinline__ void v4p(State& s, long i, const V4<T>& v, const V4<T>&, const Pre& bv) const {
     V4<T> o;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -153,6 +182,9 @@ struct EpiResidual {
       if (RED) dot_acc(s.v, o.x[e], o.x[e]);
     }
     if (r) st4(r + i, o);
+  }
+  __device__ __forceinline__ void v4(State& s, long i, const V4<T>& v, const V4<T>& xc) const {
+    v4p(s, i, v, xc, pre4(i));
   }
   __device__ __forceinline__ void s1(State& s, long i, T v, T) const {
     const T o = xsub(b[i], v);
@@ -171,11 +203,16 @@ struct EpiStoreDot {
   struct State {
     double v[1];
   };
+  using Pre = NoPre;
   __device__ void init(State& s) const { s.v[0] = 0.0; }
-  __device__ __forceinline__ void v4(State& s, long i, const V4<T>& v, const V4<T>& xc) const {
+  __device__ __forceinline__ Pre pre4(long) const { return {}; }
+  __device__ __forceinline__ void v4p(State& s, long i, const V4<T>& v, const V4<T>& xc, const Pre&) const {
     st4(out + i, v);
 #pragma unroll
     for (int e = 0; e < 4; ++e) dot_acc(s.v, xc.x[e], v.x[e]);
+  }
+  __device__ __forceinline__ void v4(State& s, long i, const V4<T>& v, const V4<T>& xc) const {
+    v4p(s, i, v, xc, pre4(i));
   }
   __device__ __forceinline__ void s1(State& s, long i, T v, T xc) const {
     out[i] = v;
@@ -190,12 +227,14 @@ struct EpiF64Forcing {
   double* out;
   int* finite_flag;  // check_finite(y) on the centre values (nullable)
   struct State {};
+  using Pre = V4<double>;
   __device__ void init(State&) const {}
-  __device__ __forceinline__ void v4(State&, long i, const V4<double>& v, const V4<double>& xc) const {
+  __device__ __forceinline__ Pre pre4(long i) const { return g ? ld4(g + i) : zero4<double>(); }
+  __device__ __forceinline__ void v4p(State&, long i, const V4<double>& v, const V4<double>& xc,
+                                      const Pre& gv) const {
     if (finite_flag && !(isfinite(xc.x[0]) && isfinite(xc.x[1]) && isfinite(xc.x[2]) && isfinite(xc.x[3])))
       *finite_flag = 1;
     if (g) {
-      const V4<double> gv = ld4(g + i);
       V4<double> o;
 #pragma unroll
       for (int e = 0; e < 4; ++e) o.x[e] = xadd(v.x[e], gv.x[e]);
@@ -203,6 +242,9 @@ struct EpiF64Forcing {
     } else {
       st4(out + i, v);
     }
+  }
+  __device__ __forceinline__ void v4(State& s, long i, const V4<double>& v, const V4<double>& xc) const {
+    v4p(s, i, v, xc, pre4(i));
   }
   __device__ __forceinline__ void s1(State&, long i, double v, double xc) const {
     if (finite_flag && !isfinite(xc)) *finite_flag = 1;
@@ -217,12 +259,14 @@ struct EpiF32Forcing {
   float* out;
   int* finite_flag;  // check_finite(y) on the centre values (nullable)
   struct State {};
+  using Pre = V4<float>;
   __device__ void init(State&) const {}
-  __device__ __forceinline__ void v4(State&, long i, const V4<float>& v, const V4<float>& xc) const {
+  __device__ __forceinline__ Pre pre4(long i) const { return g32 ? ld4(g32 + i) : zero4<float>(); }
+  __device__ __forceinline__ void v4p(State&, long i, const V4<float>& v, const V4<float>& xc,
+                                      const Pre& gv) const {
     if (finite_flag && !(isfinite(xc.x[0]) && isfinite(xc.x[1]) && isfinite(xc.x[2]) && isfinite(xc.x[3])))
       *finite_flag = 1;
     if (g32) {
-      const V4<float> gv = ld4(g32 + i);
       V4<float> o;
 #pragma unroll
       for (int e = 0; e < 4; ++e) o.x[e] = xadd(v.x[e], gv.x[e]);
@@ -230,6 +274,9 @@ struct EpiF32Forcing {
     } else {
       st4(out + i, v);
     }
+  }
+  __device__ __forceinline__ void v4(State& s, long i, const V4<float>& v, const V4<float>& xc) const {
+    v4p(s, i, v, xc, pre4(i));
   }
   __device__ __forceinline__ void s1(State&, long i, float v, float xc) const {
     if (finite_flag && !isfinite(xc)) *finite_flag = 1;
@@ -391,6 +438,193 @@ __global__ void __launch_bounds__(VX* VY)
   epi.finish(st);
 }
 
+
+// ---- plane-pipelined TMA kernel (Dirichlet, real T, n % 128 == 0) --------------------
+// A CTA owns a 128 (i) x 8 (j) column of the grid over TKC planes.  Each
+// plane tile arrives once by a TMA tensor copy — (8 + 2) rows x (128 + 8)
+// columns including the j/i halo, out-of-range rows/columns/planes zero-filled
+// by the TMA unit, which IS the Dirichlet ghost — into a 5-deep smem ring:
+// while plane k is computed (it needs k-1, k, k+1 resident) the copies of
+// planes k+2, k+3 are in flight, and the epilogue's own operand (b / g) for
+// plane k+1 is loaded into registers ahead of use.  27.5 KB (fp32) of smem
+// per CTA keeps 8 CTAs on an SM; the host sizes the k-chunk so the grid is
+// one full wave (or many), never a ragged second wave.
+// Every input element crosses HBM once; neighbours come from smem (j, k) and
+// warp shuffles (i).  On a split grid planes -1 / nz come from the ghost
+// planes (their own 2D tensor maps).
+constexpr int TI = 128, TJ = 8, TST = 5, TW = TI + 8, TTHREADS = 128;
+constexpr int TROWS = TJ / (TTHREADS / 32);  // tile rows per warp
+
+// ring slot stride: TMA destinations must be 128-byte aligned
+template <class Raw>
+constexpr int tma_slot_elems() {
+  return (int)((((size_t)(TJ + 2) * TW * sizeof(Raw) + 127) / 128) * 128 / sizeof(Raw));
+}
+template <class Raw>
+constexpr size_t tma_stencil_smem() {
+  return (size_t)TST * tma_slot_elems<Raw>() * sizeof(Raw) + TST * sizeof(uint64_t) + 128;
+}
+
+template <class Src, class Epi>
+__global__ void __launch_bounds__(TTHREADS)
+    k_stencil_tma(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap lomap,
+                  const __grid_constant__ CUtensorMap himap, int has_lo, int has_hi, int n, int nz, int kb, int ke,
+                  int kc, typename Src::type s, typename Src::type g, Src src, Epi epi) {
+  using T = typename Src::type;
+  using Raw = typename Src::raw;
+  constexpr int PLANE = tma_slot_elems<Raw>();
+  extern __shared__ unsigned char smem_raw[];
+  Raw* buf = reinterpret_cast<Raw*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(buf + TST * PLANE);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int i0 = blockIdx.x * TI, j0 = blockIdx.y * TJ;
+  int k0, k1;
+  plane_range(nz, kb, ke, kc, k0, k1);
+  const int planes = k1 - k0 + 2;  // k0 - 1 ... k1
+  constexpr uint32_t bytes = (TJ + 2) * TW * sizeof(Raw);
+  if (tid == 0) {
+    for (int b = 0; b < TST; ++b) mbar_init(&full[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // (the maps' addresses are taken here, in the kernel body: a lambda
+  // capturing a __grid_constant__ parameter would copy it to local memory,
+  // which TMA cannot read)
+  const CUtensorMap* xm = &xmap;
+  const CUtensorMap* lm = &lomap;
+  const CUtensorMap* hm = &himap;
+  auto issue = [&](int q) {  // plane k0 - 1 + q into ring slot q % TST
+    const int k = k0 - 1 + q, b = q % TST;
+    Raw* dst = buf + b * PLANE;
+    mbar_expect_tx(&full[b], bytes);
+    if (k < 0 && has_lo)
+      tma_2d(dst, lm, i0 - 4, j0 - 1, &full[b]);
+    else if (k >= nz && has_hi)
+      tma_2d(dst, hm, i0 - 4, j0 - 1, &full[b]);
+    else
+      tma_3d(dst, xm, i0 - 4, j0 - 1, k, &full[b]);  // k = -1 / nz: out of range -> zeros
+  };
+  if (tid == 0)
+    for (int q = 0; q < TST && q < planes; ++q) issue(q);
+  auto wait = [&](int q) { mbar_wait(&full[q % TST], (uint32_t)(q / TST) & 1u); };
+  auto ld = [&](const Raw* p) -> V4<T> {
+    V4<T> v;
+    if constexpr (sizeof(Raw) == 4) {
+      const float4 f = *reinterpret_cast<const float4*>(p);
+      v.x[0] = src.cv(f.x); v.x[1] = src.cv(f.y); v.x[2] = src.cv(f.z); v.x[3] = src.cv(f.w);
+    } else {
+      const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
+      v.x[0] = src.cv(a.x); v.x[1] = src.cv(a.y); v.x[2] = src.cv(b.x); v.x[3] = src.cv(b.y);
+    }
+    return v;
+  };
+  typename Epi::State st;
+  epi.init(st);
+  const long nn = n, n2 = nn * nn;
+  const int col = 4 + 4 * lane;  // this lane's 4 columns inside a smem row
+  auto gidx = [&](int r, int k) { return (i0 + 4 * lane) + (long)(j0 + r) * nn + (long)k * n2; };
+  typename Epi::Pre pre[TROWS];
+#pragma unroll
+  for (int rr = 0; rr < TROWS; ++rr) pre[rr] = epi.pre4(gidx(warp * TROWS + rr, k0));
+  for (int k = k0; k < k1; ++k) {
+    const int q = k - k0 + 1;
+    if (k == k0) {
+      wait(0);
+      wait(1);
+    }
+    wait(q + 1);
+    const Raw* pm = buf + ((q - 1) % TST) * PLANE;
+    const Raw* pc = buf + (q % TST) * PLANE;
+    const Raw* pp = buf + ((q + 1) % TST) * PLANE;
+    typename Epi::Pre nxt[TROWS];
+#pragma unroll
+    for (int rr = 0; rr < TROWS; ++rr)
+      if (k + 1 < k1) nxt[rr] = epi.pre4(gidx(warp * TROWS + rr, k + 1));
+#pragma unroll
+    for (int rr = 0; rr < TROWS; ++rr) {
+      const int r = warp * TROWS + rr;  // tile row
+      const int o = (r + 1) * TW + col;
+      const V4<T> c = ld(pc + o);
+      const V4<T> ym = ld(pc + o - TW), yp = ld(pc + o + TW);
+      const V4<T> zm = ld(pm + o), zp = ld(pp + o);
+      T left = shfl_up1(c.x[3]);
+      T right = shfl_down1(c.x[0]);
+      if (lane == 0) left = src.cv(pc[o - 1]);
+      if (lane == 31) right = src.cv(pc[o + 4]);
+      V4<T> v;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const T xl = e == 0 ? left : c.x[e - 1];
+        const T xr = e == 3 ? right : c.x[e + 1];
+        v.x[e] = point<T>(0, s, g, T(0), c.x[e], xl, xr, ym.x[e], yp.x[e], zm.x[e], zp.x[e]);
+      }
+      epi.v4p(st, gidx(r, k), v, c, pre[rr]);
+    }
+#pragma unroll
+    for (int rr = 0; rr < TROWS; ++rr) pre[rr] = nxt[rr];
+    __syncthreads();  // ring slot of plane q - 1 is free
+    if (tid == 0 && q - 1 + TST < planes) issue(q - 1 + TST);
+  }
+  epi.finish(st);
+}
+
+// k-chunk for `planes` planes over `cols` tile columns: the smallest
+// (waves x planes per CTA incl. the 2-plane halo) for the resident capacity
+template <class Src, class Epi>
+int tma_chunk(long cols, int planes) {
+  static int resident = 0;
+  if (!resident) {
+    int per_sm = 0;
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stencil_tma<Src, Epi>, TTHREADS,
+                                                             tma_stencil_smem<typename Src::raw>()));
+    resident = std::max(1, per_sm) * sm_count();
+  }
+  int best = 8;
+  long best_cost = -1;
+  for (int kc = 4; kc <= 64; kc *= 2) {
+    const long units = cols * ((planes + kc - 1) / kc);
+    const long cost = ((units + resident - 1) / resident) * (std::min(kc, planes) + 2);
+    if (best_cost < 0 || cost < best_cost) {
+      best = kc;
+      best_cost = cost;
+    }
+  }
+  return best;
+}
+
+template <class Src, class Epi>
+void tma_configure() {
+  static bool configured = false;
+  if (!configured) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_stencil_tma<Src, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)tma_stencil_smem<typename Src::raw>()));
+    configured = true;
+  }
+}
+
+template <class Src, class Epi>
+void launch_tma(const StencilSpec& sp, const Src& src, const Epi& epi, int kb, int ke, int kc, unsigned gz,
+                cudaStream_t st, const char* name) {
+  using T = typename Src::type;
+  using Raw = typename Src::raw;
+  const int n = sp.n, nz = sp.nz > 0 ? sp.nz : n;
+  constexpr size_t smem = tma_stencil_smem<Raw>();
+  tma_configure<Src, Epi>();
+  const CUtensorMapDataType dt = sizeof(Raw) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  const cuuint64_t nn = (cuuint64_t)n;
+  const cuuint64_t dims3[3] = {nn, nn, (cuuint64_t)nz}, str3[2] = {nn * sizeof(Raw), nn * nn * sizeof(Raw)};
+  const cuuint32_t box3[3] = {(cuuint32_t)TW, (cuuint32_t)(TJ + 2), 1};
+  const CUtensorMap xmap = make_map(dt, src.p, 3, dims3, str3, box3);
+  const cuuint64_t dims2[2] = {nn, nn}, str2[1] = {nn * sizeof(Raw)};
+  const cuuint32_t box2[2] = {(cuuint32_t)TW, (cuuint32_t)(TJ + 2)};
+  const CUtensorMap lomap = src.glo ? make_map(dt, src.glo, 2, dims2, str2, box2) : xmap;
+  const CUtensorMap himap = src.ghi ? make_map(dt, src.ghi, 2, dims2, str2, box2) : xmap;
+  const dim3 grid((unsigned)(n / TI), (unsigned)(n / TJ), gz);
+  k_stencil_tma<Src, Epi><<<grid, TTHREADS, smem, st>>>(xmap, lomap, himap, src.glo ? 1 : 0, src.ghi ? 1 : 0, n, nz, kb,
+                                                        ke, kc, (T)sp.sigma, (T)sp.gamma, src, epi);
+  LAUNCHED(name);
+}
+
 // epilogues that fold a reduction: split it over several launches
 template <class E, class = void>
 struct has_red : std::false_type {};
@@ -404,6 +638,10 @@ void set_red_part(Epi& e, unsigned base, unsigned total) {
     e.red.total = total;
   }
 }
+template <class Epi>
+void note_red(const Epi& e, unsigned tuples) {
+  if constexpr (has_red<Epi>::value) note_partials(e.red, tuples);
+}
 
 template <class Src, class Epi>
 void launch(const StencilSpec& sp, Src src, Epi epi, cudaStream_t st, const char* name) {
@@ -412,12 +650,24 @@ void launch(const StencilSpec& sp, Src src, Epi epi, cudaStream_t st, const char
   const int n = sp.n;
   const int nz = sp.nz > 0 ? sp.nz : n;
   const bool vec = !is_cplx<T> && n % 4 == 0;
+  // the TMA plane pipeline covers the bench path: Dirichlet heat, real T, n % 128 == 0
+  const bool tma = !is_cplx<T> && sp.stencil == 0 && n % TI == 0 && tma_stencil_enabled();
   const dim3 block = vec ? dim3(VX, VY) : dim3(SBX, SBY);
-  const int chunk = vec ? VKC : SKC;
-  const unsigned gx = vec ? (n / 4 + VX - 1) / VX : (n + SBX - 1) / SBX;
-  const unsigned gy = vec ? (n + VY - 1) / VY : (n + SBY - 1) / SBY;
+  int chunk = vec ? VKC : SKC;
+  if constexpr (!is_cplx<T>) {
+    if (tma) {
+      tma_configure<Src, Epi>();
+      chunk = tma_chunk<Src, Epi>((long)(n / TI) * (n / TJ), sp.halo && nz > 2 ? nz - 2 : nz);
+    }
+  }
+  const unsigned gx = tma ? n / TI : vec ? (n / 4 + VX - 1) / VX : (n + SBX - 1) / SBX;
+  const unsigned gy = tma ? n / TJ : vec ? (n + VY - 1) / VY : (n + SBY - 1) / SBY;
   auto go = [&](int kb, int ke, unsigned gz, const Epi& e) {
     if constexpr (!is_cplx<T>) {
+      if (tma) {
+        launch_tma(sp, src, e, kb, ke, chunk, gz, st, name);
+        return;
+      }
       if (vec) {
         k_stencil4<Src, Epi><<<dim3(gx, gy, gz), block, 0, st>>>(n, nz, kb, ke, sp.stencil, (R)sp.sigma,
                                                                 (R)sp.gamma, (R)sp.gamma2, src, e);
@@ -430,7 +680,9 @@ void launch(const StencilSpec& sp, Src src, Epi epi, cudaStream_t st, const char
     LAUNCHED(name);
   };
   if (!sp.halo) {
-    go(0, nz, (unsigned)((nz + chunk - 1) / chunk), epi);
+    const unsigned gz = (unsigned)((nz + chunk - 1) / chunk);
+    go(0, nz, gz, epi);
+    note_red(epi, gx * gy * gz);
     return;
   }
   // Split grid: the neighbours' boundary planes travel on the halo stream
@@ -447,6 +699,7 @@ void launch(const StencilSpec& sp, Src src, Epi epi, cudaStream_t st, const char
   if (nz <= 2) {
     CUDA_CHECK(cudaStreamWaitEvent(st, h.arrived, 0));
     go(0, nz, 1, epi);
+    note_red(epi, gx * gy);
     return;
   }
   const unsigned gz_in = (unsigned)((nz - 2 + chunk - 1) / chunk);
@@ -457,6 +710,7 @@ void launch(const StencilSpec& sp, Src src, Epi epi, cudaStream_t st, const char
   go(1, nz - 1, gz_in, ein);
   CUDA_CHECK(cudaStreamWaitEvent(st, h.arrived, 0));
   go(-1, -1, 2, ebd);
+  note_red(epi, nb_in + nb_bd);
 }
 
 }  // namespace

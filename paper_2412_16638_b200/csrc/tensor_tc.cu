@@ -30,6 +30,7 @@
 #include <cstdlib>
 
 #include "launch.hpp"
+#include "tma.cuh"
 #include "vec.cuh"
 
 namespace mprkb {
@@ -61,62 +62,10 @@ struct TcSmem {
   uint32_t tmem_base;
 };
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
 __device__ __forceinline__ uint32_t tf32_rna(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
   return r;
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-// Bounded wait: a protocol bug traps (error surfaces to the host) instead of
-// spinning the GPU forever.
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = smem_u32(bar);
-  for (long long spin = 0;; ++spin) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, P1;\n\t}"
-        : "=r"(ok)
-        : "r"(a), "r"(parity)
-        : "memory");
-    if (ok) return;
-    if (spin > (1ll << 26)) __trap();
-  }
-}
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(dst)),
-               "l"(src), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-          smem_u32(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-      "[%5];" ::"r"(smem_u32(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-      : "memory");
 }
 
 // UMMA shared-memory descriptor: SWIZZLE_NONE, sm_100 version bit, K-major
@@ -362,33 +311,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2u * TC_BN));
 }
 
-// ---- host: tensor maps ------------------------------------------------------------
-using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeFn encode_fn() {
-  static EncodeFn fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    CUDA_CHECK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
-    if (q != cudaDriverEntryPointSuccess || !p) MPRKB_THROW(20, "cuTensorMapEncodeTiled unavailable");
-    return reinterpret_cast<EncodeFn>(p);
-  }();
-  return fn;
-}
-
-CUtensorMap make_map(const float* x, int rank, const cuuint64_t* dims, const cuuint64_t* strides_bytes,
-                     const cuuint32_t* box) {
-  CUtensorMap m;
-  const cuuint32_t estr[3] = {1, 1, 1};
-  const CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, (cuuint32_t)rank, const_cast<float*>(x), dims,
-                                 strides_bytes, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) MPRKB_THROW(20, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
-  return m;
-}
-
 template <int SIDE, bool DIAG>
 void launch_tc(int n, long cols, const float* x, float* out, const float* pd, const float* qh, const float* ql,
                cudaStream_t st) {
@@ -406,18 +328,18 @@ void launch_tc(int n, long cols, const float* x, float* out, const float* pd, co
   if (SIDE == 2) {  // X as [cols fibres][n q]
     const cuuint64_t dims[2] = {nn, cc}, strides[1] = {nn * 4};
     const cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)TC_BN};
-    map = make_map(x, 2, dims, strides, box);
+    map = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, x, 2, dims, strides, box);
     col_tiles = (int)(cc / TC_BN);
   } else if (SIDE == 1) {  // X as [cols/n k][n q][n i]
     const cuuint64_t dims[3] = {nn, nn, cc / nn}, strides[2] = {nn * 4, n2 * 4};
     const cuuint32_t box[3] = {(cuuint32_t)TC_BN, (cuuint32_t)TC_BK, 1};
-    map = make_map(x, 3, dims, strides, box);
+    map = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, x, 3, dims, strides, box);
     col_tiles = (int)(nn / TC_BN);
     planes = (int)(cc / nn);
   } else {  // X as [n q][cols c]
     const cuuint64_t dims[2] = {cc, nn}, strides[1] = {cc * 4};
     const cuuint32_t box[2] = {(cuuint32_t)TC_BN, (cuuint32_t)TC_BK};
-    map = make_map(x, 2, dims, strides, box);
+    map = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, x, 2, dims, strides, box);
     col_tiles = (int)(cc / TC_BN);
   }
   const int num_tiles = (n / TC_BM) * col_tiles * planes;

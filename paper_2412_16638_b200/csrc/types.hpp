@@ -81,15 +81,23 @@ inline unsigned grid_for(size_t work, unsigned block, unsigned per_sm = 8) {
 enum class Numerics { Fast = 0, Parity = 1 };
 
 // One grid-wide reduction target (see reduce.cuh).
+// Protocol: every CTA of a reducing kernel writes its fp64 partial tuple to
+// partial[(base + cta) * 2 + c] (host-mapped pinned memory) with plain stores
+// — no fences, no atomics; the launcher records how many tuples it launched in
+// *count (host memory), and after the stream synchronize the host adds them
+// in CTA order (Reducer::result) — deterministic run to run.  Single-CTA
+// sequential kernels (PARITY dots) write `out` and set *count = 0.
 struct RedSlot {
-  double* partial = nullptr;   // >= gridDim * NV doubles (device)
-  unsigned* ticket = nullptr;  // zero between uses (device)
-  double* out = nullptr;       // NV doubles, host-mapped pinned memory
+  double* partial = nullptr;   // device alias of host-mapped memory, kMaxPartials x 2 doubles
+  double* out = nullptr;       // device alias of host-mapped memory, 2 doubles
+  int* count = nullptr;        // HOST pointer: tuples written by the last launch(es)
   // one reduction spread over several launches (interior + boundary planes of
-  // a split-grid stencil): this launch's CTAs are partials [base, base +
-  // gridDim) of `total`; the last CTA of ALL launches writes out (0: one launch)
+  // a split-grid stencil): this launch's CTAs are tuples [base, base + gridDim)
   unsigned base = 0, total = 0;
 };
+inline void note_partials(const RedSlot& r, unsigned tuples) {
+  if (r.count) *r.count = (int)tuples;
+}
 constexpr int kMaxPartials = 1 << 16;
 
 }  // namespace mprkb
