@@ -109,6 +109,10 @@ int mprkb_tensor_apply(int dtype, int side, int n, const void* q, const void* x,
  * accumulation; FAST numerics; n % 256 == 0): q is a HOST n*n matrix (split
  * and packed per call), x/out device vectors. */
 int mprkb_tensor_apply_tc(int side, int n, const float* q_host, const float* x, float* out, void* stream);
+/* The same for a Q with the Dirichlet sine symmetry Q[n-1-a][q] = (-1)^q Q[a][q]
+ * (spectral_dirichlet, spectral.cpp:11-29): even/odd-q partial sums for
+ * a < n/2, half the MMAs (MPRKB_INVALID_ARGUMENT if Q lacks the symmetry). */
+int mprkb_tensor_apply_tc_fold(int side, int n, const float* q_host, const float* x, float* out, void* stream);
 /* detail::dot_real / dot (krylov.hpp:43-66) on device vectors; result written
  * to host memory (`result` = 1 real, or 2 doubles re,im for a complex dot). */
 int mprkb_dot(int dtype, size_t m, const void* a, const void* b, int conjugate_dot, int numerics,

@@ -144,6 +144,7 @@ SIGNATURES = {
     "mprkb_tensor_apply": (i32, [i32, i32, i32, vp, vp, vp, i32, vp]),
     "mprkb_dot": (i32, [i32, sz, vp, vp, i32, i32, dptr, vp]),
     "mprkb_tensor_apply_tc": (i32, [i32, i32, vp, vp, vp, vp]),
+    "mprkb_tensor_apply_tc_fold": (i32, [i32, i32, vp, vp, vp, vp]),
     "mprkb_op_stencil": (i32, [i32, i32, i32, f64, f64, C.POINTER(vp)]),
     "mprkb_op_fastdiag": (i32, [i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, C.POINTER(vp)]),
     "mprkb_op_fastdiag_stage": (i32, [i32, i32, i32, f64, f64, i32, C.POINTER(vp)]),

@@ -227,6 +227,27 @@ int mprkb_tensor_apply(int dtype, int side, int n, const void* q, const void* x,
   });
 }
 
+int mprkb_tensor_apply_tc_fold(int side, int n, const float* q_host, const float* x, float* out, void* stream) {
+  return guarded([&] {
+    require_device();
+    if (side < 0 || side > 2) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "unknown tensor side");
+    if (!tensor_tc_supported(n)) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "tensor-core contraction needs n % 256 == 0");
+    const size_t nn = (size_t)n * n;
+    for (size_t a = 0; a < (size_t)n; ++a)
+      for (size_t q = 0; q < (size_t)n; ++q) {
+        const float want = (q % 2 ? -1.0f : 1.0f) * q_host[a * n + q];
+        if (std::abs(q_host[(n - 1 - a) * n + q] - want) > 1e-6f * (std::abs(want) + 1e-30f))
+          MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "folded contraction: Q lacks the sine symmetry Q[n-1-a][q] = (-1)^q Q[a][q]");
+      }
+    std::vector<float> pk(nn);
+    pack_tf32_fold(n, q_host, pk.data());
+    DevBuf dq(nn * 4);
+    CUDA_CHECK(cudaMemcpy(dq.get(), pk.data(), nn * 4, cudaMemcpyHostToDevice));
+    tensor_apply_tc_fold(side, n, dq.as<float>(), x, out, nullptr, S(stream));
+    CUDA_CHECK(cudaStreamSynchronize(S(stream)));
+  });
+}
+
 int mprkb_tensor_apply_tc(int side, int n, const float* q_host, const float* x, float* out, void* stream) {
   return guarded([&] {
     require_device();

@@ -66,6 +66,12 @@ bool tensor_tc_supported(int n);
 void tensor_apply_tc(int side, int n, const float* q_hi_packed, const float* q_lo_packed, const float* x,
                      float* out, const float* pd, cudaStream_t st, long cols = 0);
 bool tensor_tc_supported_cols(int n, long cols);
+// Folded variant for factors with the Dirichlet sine symmetry
+// Q[n-1-a][q] = (-1)^q Q[a][q]: half the MMAs.  qpack = pack_tf32_fold(): four
+// (n/2)^2 blocks {even hi, even lo, odd hi, odd lo} of Q's rows a < n/2.
+void tensor_apply_tc_fold(int side, int n, const float* qpack, const float* x, float* out, const float* pd,
+                          cudaStream_t st, long cols = 0);
+void pack_tf32_fold(int n, const float* q, float* qpack);
 // Host: split Q (n x n row-major) into tf32 hi/lo and pack as
 // [k-block of 16][row-group of 8][k-chunk of 4][8 rows][4].
 void pack_tf32_split(int n, const float* q, float* hi_packed, float* lo_packed);

@@ -62,6 +62,24 @@ void pack_tf32_split(int n, const float* q, float* hi_packed, float* lo_packed) 
     }
 }
 
+// rows a < n/2, columns split by parity of q: E[a][q'] = Q[a][2q'],
+// O[a][q'] = Q[a][2q'+1], each tf32 hi/lo, packed
+// [k-block of 8][row-group of 8][k-chunk of 4 (2 per block)][8 rows][4]
+void pack_tf32_fold(int n, const float* q, float* qpack) {
+  const size_t h = (size_t)n / 2, blk = h * h;
+  for (size_t row = 0; row < h; ++row)
+    for (size_t k = 0; k < h; ++k)
+      for (int p = 0; p < 2; ++p) {
+        const float x = q[row * n + 2 * k + p];
+        const float hi = tf32_rna(x);
+        const float lo = tf32_rna(x - hi);
+        const size_t kb = k / 8, c = (k % 8) / 4, j = k % 4, g = row / 8, r = row % 8;
+        const size_t o = (((kb * (h / 8) + g) * 2 + c) * 8 + r) * 4 + j;
+        qpack[(size_t)(p * 2 + 0) * blk + o] = hi;
+        qpack[(size_t)(p * 2 + 1) * blk + o] = lo;
+      }
+}
+
 StencilOp::StencilOp(int dtype, const StencilSpec& s) : Op(dtype, s.size()), spec_(s) {
   if (s.n < 2) MPRKB_THROW(3, "KronSumOperator: n must be at least 2");
 }
@@ -115,10 +133,17 @@ FastDiagOp<T>::FastDiagOp(int n, const T* qa, const T* qa_inv, const T* qb, cons
     tc_split_ = tc_ && tensor_tc_supported_cols(n, (long)n * nz_) && tensor_tc_supported_cols(n, (long)n * ny_);
     if (tc_) {
       std::vector<float> hi(nn), lo(nn);
+      const char* fenv = std::getenv("MPRKB_TC_FOLD");
       for (int f = 0; f < 6; ++f) {
-        pack_tf32_split(n, src[f], hi.data(), lo.data());
-        upload(qhp_[f], hi.data(), nn * sizeof(float));
-        upload(qlp_[f], lo.data(), nn * sizeof(float));
+        tcf_[f] = fold_[f] && !(fenv && fenv[0] == '0');
+        if (tcf_[f]) {  // folded: four (n/2)^2 blocks = n^2 floats
+          pack_tf32_fold(n, src[f], hi.data());
+          upload(qhp_[f], hi.data(), nn * sizeof(float));
+        } else {
+          pack_tf32_split(n, src[f], hi.data(), lo.data());
+          upload(qhp_[f], hi.data(), nn * sizeof(float));
+          upload(qlp_[f], lo.data(), nn * sizeof(float));
+        }
       }
     }
   }
@@ -186,7 +211,10 @@ template <class T>
 void FastDiagOp<T>::contract(int side, int f, const T* in, T* o, const T* pd, long cols, cudaStream_t st) {
   if constexpr (std::is_same_v<T, float>) {
     if (tc_split_) {
-      tensor_apply_tc(side, n_, qhp_[f].template as<float>(), qlp_[f].template as<float>(), in, o, pd, st, cols);
+      if (tcf_[f])
+        tensor_apply_tc_fold(side, n_, qhp_[f].template as<float>(), in, o, pd, st, cols);
+      else
+        tensor_apply_tc(side, n_, qhp_[f].template as<float>(), qlp_[f].template as<float>(), in, o, pd, st, cols);
       return;
     }
   }
@@ -245,7 +273,10 @@ void FastDiagOp<T>::apply(const void* xv, void* outv, cudaStream_t st) {
   if constexpr (std::is_same_v<T, float>) {
     if (tc_) {
       auto tc = [&](int side, int f, const float* in, float* o, const float* pd) {
-        tensor_apply_tc(side, n_, qhp_[f].as<float>(), qlp_[f].as<float>(), in, o, pd, st);
+        if (tcf_[f])
+          tensor_apply_tc_fold(side, n_, qhp_[f].as<float>(), in, o, pd, st);
+        else
+          tensor_apply_tc(side, n_, qhp_[f].as<float>(), qlp_[f].as<float>(), in, o, pd, st);
       };
       tc(2, 1, x, t1, nullptr);
       tc(1, 3, t1, t2, nullptr);

@@ -71,7 +71,8 @@ class FastDiagOp final : public Op {
   bool fold_[6] = {false, false, false, false, false, false};  // sine symmetry per factor
   bool tc_ = false;  // fp32 FAST: tensor-core (3xTF32) contractions
   DevBuf q_[6];  // qa, qa_inv, qb, qb_inv, qc, qc_inv
-  DevBuf qhp_[6], qlp_[6];  // tf32 hi/lo split, UMMA-packed (tc_ only)
+  DevBuf qhp_[6], qlp_[6];  // tf32 hi/lo split, UMMA-packed (tc_ only; folded: qhp_ holds all four blocks)
+  bool tcf_[6] = {false, false, false, false, false, false};  // folded tcgen05 contraction per factor
   DevBuf pd_, t1_, t2_, t3_;  // t3_: split grid only
 };
 

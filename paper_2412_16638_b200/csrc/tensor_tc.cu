@@ -348,7 +348,323 @@ void launch_tc(int n, long cols, const float* x, float* out, const float* pd, co
   LAUNCHED("tensor_tc");
 }
 
+
+// ===================================================================================
+// Folded contraction: the Dirichlet sine basis has Q[n-1-a][q] = (-1)^q Q[a][q]
+// (spectral.cpp:17-20), so for a < n/2
+//     D[a] = E[a] + O[a],   D[n-1-a] = E[a] - O[a],
+//     E[a] = sum_{q even} Q[a][q] X[q],   O[a] = sum_{q odd} Q[a][q] X[q].
+// One CTA tile = all a < n/2 rows (M = 128 per a-tile) x 128 columns; each
+// k-block of 16 q feeds E with its 8 even q and O with its 8 odd q (3xTF32 each:
+// 6 MMAs, M = 128, N = 128, K = 8), E and O accumulate in two 128-column TMEM
+// blocks, double-buffered across tiles (512 columns).  Half the MMAs and half
+// the splitting work of the unfolded kernel per output; the epilogue writes
+// both rows a and n-1-a.  The converter de-interleaves even/odd q while it
+// splits, and the host packs Q's even/odd columns (pack_tf32_fold).
+constexpr int TF_BM = 128, TF_BN = 128, TF_BK = 16, TF_STAGES = 5;
+constexpr int TF_RAW = TF_BN * TF_BK * 4;      // 8 KB raw X
+constexpr int TF_X = TF_BN * (TF_BK / 2) * 4;  // 4 KB per {even, odd} x {hi, lo}
+constexpr int TF_Q = TF_BM * (TF_BK / 2) * 4;  // 4 KB per {even, odd} x {hi, lo}
+constexpr int TF_STAGE = TF_RAW + 4 * TF_X + 4 * TF_Q;
+
+struct TfSmem {
+  alignas(1024) unsigned char stage[TF_STAGES][TF_STAGE];
+  alignas(8) uint64_t full[TF_STAGES];
+  alignas(8) uint64_t conv[TF_STAGES];
+  alignas(8) uint64_t empty[TF_STAGES];
+  alignas(8) uint64_t tmem_full[2];
+  alignas(8) uint64_t tmem_empty[2];
+  uint32_t tmem_base;
+};
+
+// K-major no-swizzle canonical layout of an 8-wide k-block:
+// [row-group of 8][k-chunk of 4 (2 per block)][8 rows][16 B] -> LBO 128 B, SBO 256 B
+__device__ __forceinline__ uint64_t kmajor_desc8(const void* p) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_u32(p) >> 4) & 0x3FFF);
+  d |= (uint64_t)(128 >> 4) << 16;
+  d |= (uint64_t)(256 >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  return d;
+}
+constexpr uint32_t kIdescF = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TF_BN >> 3) << 17) |
+                             ((uint32_t)(TF_BM >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32f(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(kIdescF), "r"(acc), "r"(0u), "r"(0u), "r"(0u), "r"(0u)
+      : "memory");
+}
+
+// canonical byte offset of (row, 4-chunk ch) in an 8-wide K-major block
+__device__ __forceinline__ int kofs8(int row, int ch) { return ((row >> 3) * 2 + ch) * 128 + (row & 7) * 16; }
+
+template <int SIDE, bool DIAG>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    k_tensor_tcf(const __grid_constant__ CUtensorMap xmap, float* __restrict__ C, const float* __restrict__ pd,
+                 const float* __restrict__ qpack, int n, int col_tiles, int num_tiles, long ldc) {
+  extern __shared__ unsigned char smem_raw[];
+  TfSmem& S = *reinterpret_cast<TfSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int KB = n / TF_BK;
+  const int h = n / 2;            // folded rows
+  const int a_tiles = h / TF_BM;  // 1 for n = 256
+  const long nn = n, n2 = nn * nn;
+  const size_t qh2 = (size_t)h * h;  // floats per packed half
+  auto RAW = [&](int s) { return S.stage[s]; };
+  // X{E,O}{H,L}: p = 0 even, 1 odd; l = 0 hi, 1 lo
+  auto XS = [&](int s, int p, int l) { return S.stage[s] + TF_RAW + (p * 2 + l) * TF_X; };
+  auto QS = [&](int s, int p, int l) { return S.stage[s] + TF_RAW + 4 * TF_X + (p * 2 + l) * TF_Q; };
+  struct Tile {
+    int a0, plane;
+    long col0;
+  };
+  auto tile_of = [&](int t) {
+    Tile T;
+    T.a0 = (t % a_tiles) * TF_BM;
+    const int ct = t / a_tiles;
+    T.col0 = (long)(ct % col_tiles) * TF_BN;
+    T.plane = ct / col_tiles;
+    return T;
+  };
+  const CUtensorMap* xm = &xmap;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
+                 "r"(512u));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 32 * TC_PROD_WARP) {
+    for (int s = 0; s < TF_STAGES; ++s) {
+      mbar_init(&S.full[s], 1);
+      mbar_init(&S.conv[s], 32 * TC_CONV_WARPS);
+      mbar_init(&S.empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&S.tmem_full[b], 1);
+      mbar_init(&S.tmem_empty[b], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = S.tmem_base;
+
+  if (warp == TC_PROD_WARP) {
+    if (lane == 0) {
+      long g = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const Tile T = tile_of(t);
+        for (int kb = 0; kb < KB; ++kb, ++g) {
+          const int s = (int)(g % TF_STAGES);
+          if (g >= TF_STAGES) mbar_wait(&S.empty[s], (uint32_t)((g / TF_STAGES) - 1) & 1);
+          mbar_expect_tx(&S.full[s], TF_RAW + 4 * TF_Q);
+          if (SIDE == 2)
+            tma_2d(RAW(s), xm, kb * TF_BK, (int)T.col0, &S.full[s]);
+          else if (SIDE == 1)
+            tma_3d(RAW(s), xm, (int)T.col0, kb * TF_BK, T.plane, &S.full[s]);
+          else
+            tma_2d(RAW(s), xm, (int)T.col0, kb * TF_BK, &S.full[s]);
+          // packed Q halves: [k-block of 8][row-group][2 chunks][8 rows][4]
+          const size_t qoff = ((size_t)kb * (h / 8) + T.a0 / 8) * 64;
+          for (int p = 0; p < 2; ++p)
+            for (int l = 0; l < 2; ++l)
+              bulk_g2s(QS(s, p, l), qpack + (size_t)(p * 2 + l) * qh2 + qoff, TF_Q, &S.full[s]);
+        }
+      }
+    }
+  } else if (warp == TC_MMA_WARP) {
+    if (lane == 0) {
+      long g = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        mbar_wait(&S.tmem_empty[acc], (uint32_t)((it >> 1) & 1) ^ 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t dE = tmem + (uint32_t)(acc * 256), dO = dE + 128;
+        for (int kb = 0; kb < KB; ++kb, ++g) {
+          const int s = (int)(g % TF_STAGES);
+          mbar_wait(&S.conv[s], (uint32_t)(g / TF_STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t first = kb ? 1u : 0u;
+#pragma unroll
+          for (int p = 0; p < 2; ++p) {
+            const uint32_t d = p ? dO : dE;
+            const uint64_t qh = kmajor_desc8(QS(s, p, 0)), ql = kmajor_desc8(QS(s, p, 1));
+            const uint64_t xh = kmajor_desc8(XS(s, p, 0)), xl = kmajor_desc8(XS(s, p, 1));
+            mma_tf32f(d, ql, xh, first);
+            mma_tf32f(d, qh, xl, 1u);
+            mma_tf32f(d, qh, xh, 1u);
+          }
+          mma_commit(&S.empty[s]);
+        }
+        mma_commit(&S.tmem_full[acc]);
+      }
+    }
+  } else if (warp < TC_CONV_WARPS) {
+    // raw fp32 -> tf32 hi/lo, even q -> E block, odd q -> O block
+    const int ct = tid;  // 0..127: one X column (B row) per thread
+    long g = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int kb = 0; kb < KB; ++kb, ++g) {
+        const int s = (int)(g % TF_STAGES);
+        mbar_wait(&S.full[s], (uint32_t)(g / TF_STAGES) & 1);
+        const uint32_t raw = smem_u32(RAW(s));
+        float v[TF_BK];
+        if (SIDE == 2) {
+          // raw [128 columns][16 q] (64 B rows)
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(v[4 * j]), "=f"(v[4 * j + 1]), "=f"(v[4 * j + 2]), "=f"(v[4 * j + 3])
+                         : "r"(raw + ct * 64 + j * 16));
+        } else {
+          // raw [16 q][128 columns] (512 B rows)
+#pragma unroll
+          for (int q = 0; q < TF_BK; ++q)
+            asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[q]) : "r"(raw + q * 512 + ct * 4));
+        }
+#pragma unroll
+        for (int p = 0; p < 2; ++p)
+#pragma unroll
+          for (int ch = 0; ch < 2; ++ch) {
+            uint32_t hi[4], lo[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float x = v[2 * (ch * 4 + u) + p];
+              hi[u] = tf32_rna(x);
+              lo[u] = tf32_rna(x - __uint_as_float(hi[u]));
+            }
+            const int o = kofs8(ct, ch);
+            const uint32_t dh = smem_u32(XS(s, p, 0)) + o, dl = smem_u32(XS(s, p, 1)) + o;
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dh), "r"(hi[0]), "r"(hi[1]), "r"(hi[2]),
+                         "r"(hi[3])
+                         : "memory");
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dl), "r"(lo[0]), "r"(lo[1]), "r"(lo[2]),
+                         "r"(lo[3])
+                         : "memory");
+          }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&S.conv[s]);
+      }
+    }
+  } else if (warp < TC_EPI_WARP0 + 4) {
+    const int q4 = warp - TC_EPI_WARP0;
+    int it = 0;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
+      const Tile T = tile_of(t);
+      const int acc = it & 1;
+      mbar_wait(&S.tmem_full[acc], (uint32_t)(it >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const long a = T.a0 + 32 * q4 + lane;  // folded row; its mirror is n-1-a
+      const long am = n - 1 - a;
+      const uint32_t lanebase = tmem + ((uint32_t)(32 * q4) << 16) + (uint32_t)(acc * 256);
+      for (int cc = 0; cc < TF_BN; cc += 32) {
+        uint32_t e[32], o[32];
+        tmem_ld32(lanebase + (uint32_t)cc, e);
+        tmem_ld32(lanebase + 128u + (uint32_t)cc, o);
+        if (SIDE == 2) {
+          // D[a][fibre] = C[fibre][a]: for fixed j the warp writes 32 consecutive a
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const long f = (T.col0 + cc + j) * nn;
+            float v1 = __uint_as_float(e[j]) + __uint_as_float(o[j]);
+            float v2 = __uint_as_float(e[j]) - __uint_as_float(o[j]);
+            if (DIAG) {
+              v1 *= __ldg(pd + f + a);
+              v2 *= __ldg(pd + f + am);
+            }
+            C[f + a] = v1;
+            C[f + am] = v2;
+          }
+        } else {
+          const long b1 = SIDE == 1 ? (long)T.plane * n2 + a * nn + T.col0 + cc : a * ldc + T.col0 + cc;
+          const long b2 = SIDE == 1 ? (long)T.plane * n2 + am * nn + T.col0 + cc : am * ldc + T.col0 + cc;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            float4 v1, v2;
+            float* p1 = &v1.x;
+            float* p2 = &v2.x;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              p1[u] = __uint_as_float(e[j + u]) + __uint_as_float(o[j + u]);
+              p2[u] = __uint_as_float(e[j + u]) - __uint_as_float(o[j + u]);
+            }
+            if (DIAG) {
+              const float4 d1 = __ldg(reinterpret_cast<const float4*>(pd + b1 + j));
+              const float4 d2 = __ldg(reinterpret_cast<const float4*>(pd + b2 + j));
+              v1.x *= d1.x; v1.y *= d1.y; v1.z *= d1.z; v1.w *= d1.w;
+              v2.x *= d2.x; v2.y *= d2.y; v2.z *= d2.z; v2.w *= d2.w;
+            }
+            *reinterpret_cast<float4*>(C + b1 + j) = v1;
+            *reinterpret_cast<float4*>(C + b2 + j) = v2;
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&S.tmem_empty[acc]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
+}
+
+template <int SIDE, bool DIAG>
+void launch_tcf(int n, long cols, const float* x, float* out, const float* pd, const float* qpack, cudaStream_t st) {
+  const size_t smem = sizeof(TfSmem) + 1024;
+  static bool configured = false;
+  if (!configured) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_tensor_tcf<SIDE, DIAG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  const cuuint64_t nn = (cuuint64_t)n, n2 = nn * nn, cc = (cuuint64_t)cols;
+  CUtensorMap map;
+  int col_tiles, planes = 1;
+  if (SIDE == 2) {
+    const cuuint64_t dims[2] = {nn, cc}, strides[1] = {nn * 4};
+    const cuuint32_t box[2] = {(cuuint32_t)TF_BK, (cuuint32_t)TF_BN};
+    map = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, x, 2, dims, strides, box);
+    col_tiles = (int)(cc / TF_BN);
+  } else if (SIDE == 1) {
+    const cuuint64_t dims[3] = {nn, nn, cc / nn}, strides[2] = {nn * 4, n2 * 4};
+    const cuuint32_t box[3] = {(cuuint32_t)TF_BN, (cuuint32_t)TF_BK, 1};
+    map = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, x, 3, dims, strides, box);
+    col_tiles = (int)(nn / TF_BN);
+    planes = (int)(cc / nn);
+  } else {
+    const cuuint64_t dims[2] = {cc, nn}, strides[1] = {cc * 4};
+    const cuuint32_t box[2] = {(cuuint32_t)TF_BN, (cuuint32_t)TF_BK};
+    map = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, x, 2, dims, strides, box);
+    col_tiles = (int)(cc / TF_BN);
+  }
+  const int num_tiles = (n / 2 / TF_BM) * col_tiles * planes;
+  const int grid = num_tiles < sm_count() ? num_tiles : sm_count();
+  k_tensor_tcf<SIDE, DIAG><<<grid, TC_THREADS, smem, st>>>(map, out, pd, qpack, n, col_tiles, num_tiles, cols);
+  LAUNCHED("tensor_tc_fold");
+}
+
 }  // namespace
+
+void tensor_apply_tc_fold(int side, int n, const float* qpack, const float* x, float* out, const float* pd,
+                          cudaStream_t st, long cols) {
+  if (cols <= 0) cols = (long)n * n;
+  switch (side) {
+    case 2:
+      pd ? launch_tcf<2, true>(n, cols, x, out, pd, qpack, st) : launch_tcf<2, false>(n, cols, x, out, pd, qpack, st);
+      break;
+    case 1:
+      pd ? launch_tcf<1, true>(n, cols, x, out, pd, qpack, st) : launch_tcf<1, false>(n, cols, x, out, pd, qpack, st);
+      break;
+    default:
+      pd ? launch_tcf<0, true>(n, cols, x, out, pd, qpack, st) : launch_tcf<0, false>(n, cols, x, out, pd, qpack, st);
+      break;
+  }
+}
 
 // N = 256 columns per CTA and 128 Q rows: n % 256 == 0 for the M side's i tiles.
 bool tensor_tc_supported(int n) { return n >= 256 && n % 256 == 0 && n <= 2048; }

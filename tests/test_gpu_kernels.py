@@ -108,6 +108,38 @@ def test_fastdiag_stage_bitwise(gpu, mp, ref, kind, n):
         assert np.abs(fast - want).max() <= 50 * FAST_TOL[kind] * max(1.0, np.abs(want).max())
 
 
+@pytest.mark.parametrize("side", [0, 1, 2])
+def test_tensor_tc_fold_each_side(gpu, mp, side):
+    """The folded tcgen05 contraction (even/odd q sums, rows a and n-1-a from
+    E +- O) on each side with the Dirichlet sine basis, against an fp64
+    contraction and the unfolded 3xTF32 kernel."""
+    import ctypes as C
+
+    import torch
+
+    n = 256
+    j = np.arange(n)
+    q = (np.sqrt(2.0 / (n + 1)) * np.sin(np.outer(j + 1, j + 1) * np.pi / (n + 1))).astype(np.float32)
+    rng = np.random.default_rng(91 + side)
+    x = rng.uniform(-1, 1, n ** 3).astype(np.float32)
+    X = x.reshape(n, n, n).astype(np.float64)  # [k][j][i]
+    Q = q.astype(np.float64)
+    want = {2: np.einsum("ai,kji->kja", Q, X), 1: np.einsum("aj,kji->kai", Q, X),
+            0: np.einsum("ak,kji->aji", Q, X)}[side].ravel()
+    xd = torch.from_numpy(x).cuda()
+    outs = {}
+    for name in ("mprkb_tensor_apply_tc_fold", "mprkb_tensor_apply_tc"):
+        out = torch.empty_like(xd)
+        mp.check(getattr(mp._c.lib, name)(side, n, q.ctypes.data_as(C.c_void_p), C.c_void_p(xd.data_ptr()),
+                                          C.c_void_p(out.data_ptr()), None))
+        outs[name] = out.cpu().numpy().astype(np.float64)
+    scale = np.abs(want).max()
+    err_f = np.abs(outs["mprkb_tensor_apply_tc_fold"] - want).max() / scale
+    err_u = np.abs(outs["mprkb_tensor_apply_tc"] - want).max() / scale
+    assert err_f <= 4e-6, (err_f, err_u)
+    assert err_u <= 4e-6, err_u
+
+
 @pytest.mark.parametrize("n", [256])
 def test_fastdiag_tensor_cores_match_reference(gpu, mp, ref, n):
     """fp32 FAST FastDiag on tcgen05 (3xTF32) vs the reference's fp32 apply and
@@ -123,6 +155,9 @@ def test_fastdiag_tensor_cores_match_reference(gpu, mp, ref, n):
     xd = torch.from_numpy(x).cuda()
     os.environ["MPRKB_TENSOR_CORES"] = "1"
     tc = mp.Operator.fastdiag_stage(0, "heat", n, 0.01, 0.5, "fast").apply(xd).cpu().numpy()
+    os.environ["MPRKB_TC_FOLD"] = "0"
+    tcu = mp.Operator.fastdiag_stage(0, "heat", n, 0.01, 0.5, "fast").apply(xd).cpu().numpy()
+    del os.environ["MPRKB_TC_FOLD"]
     os.environ["MPRKB_TENSOR_CORES"] = "0"
     cc = mp.Operator.fastdiag_stage(0, "heat", n, 0.01, 0.5, "fast").apply(xd).cpu().numpy()
     del os.environ["MPRKB_TENSOR_CORES"]
@@ -136,6 +171,7 @@ def test_fastdiag_tensor_cores_match_reference(gpu, mp, ref, n):
     # The stage solve's accuracy is set by CG's fp32 true-residual check, not
     # by the preconditioner, so this only has to stay far below the solve tol.
     assert err_tc <= 2e-5, (err_tc, err_cc, err_ref)
+    assert np.abs(tcu - want64).max() / scale <= 2e-5  # unfolded tcgen05 kernel
     assert err_cc <= 4 * err_ref + 1e-7
 
 
