@@ -10,6 +10,7 @@
 
 #include "comm.hpp"
 #include "ops.hpp"
+#include "problem.hpp"
 
 namespace mprkb {
 
@@ -117,6 +118,34 @@ void kernel_bench(const std::string& which, int n, int reps, double* ms, double*
   } else if (which == "csr_f16") {
     auto op = make_csr_stencil(0, sp, 4);
     t = time_it(st, reps, (8 + 7 * (2 + 4) + 4) * D, [&] { op->apply(f32(0), f32(1), st); });
+  } else if (which.rfind("tc_", 0) == 0) {
+    // FastDiag contractions on tcgen05: tc_{fold,split}_{R,M,L,Lpd}; bytes =
+    // x in + out (+ pd: the folded kernel scales its input, the unfolded its
+    // output), flops reported by the caller as 2 n^4
+    const bool fold = which.find("fold") != std::string::npos;
+    const char sd = which.back() == 'd' ? 'D' : which.back();
+    const int side = sd == 'R' ? 2 : sd == 'M' ? 1 : 0;
+    const bool diag = sd == 'D';
+    std::vector<double> q64, qi, lam;
+    spectral_dirichlet(n, 1.0, 0.3, q64, qi, lam);
+    std::vector<float> q(q64.begin(), q64.end());
+    const size_t nn = (size_t)n * n;
+    std::vector<float> a(nn), b(nn);
+    DevBuf qa(nn * 4), qb(nn * 4);
+    if (fold) {
+      pack_tf32_fold(n, q.data(), a.data());
+    } else {
+      pack_tf32_split(n, q.data(), a.data(), b.data());
+      CUDA_CHECK(cudaMemcpy(qb.get(), b.data(), nn * 4, cudaMemcpyHostToDevice));
+    }
+    CUDA_CHECK(cudaMemcpy(qa.get(), a.data(), nn * 4, cudaMemcpyHostToDevice));
+    const float* pd = diag ? f32(2) : nullptr;
+    t = time_it(st, reps, (diag ? 12 : 8) * D, [&] {
+      if (fold)
+        tensor_apply_tc_fold(side, n, qa.as<float>(), f32(0), f32(1), pd, st);
+      else
+        tensor_apply_tc(side, n, qa.as<float>(), qb.as<float>(), f32(0), f32(1), pd, st);
+    });
   } else {
     MPRKB_THROW(10, "kernel_bench: unknown kernel '" + which + "'");
   }

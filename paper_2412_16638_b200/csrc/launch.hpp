@@ -69,7 +69,10 @@ bool tensor_tc_supported_cols(int n, long cols);
 // Folded variant for factors with the Dirichlet sine symmetry
 // Q[n-1-a][q] = (-1)^q Q[a][q]: half the MMAs.  qpack = pack_tf32_fold(): four
 // (n/2)^2 blocks {even hi, even lo, odd hi, odd lo} of Q's rows a < n/2.
-void tensor_apply_tc_fold(int side, int n, const float* qpack, const float* x, float* out, const float* pd,
+// pd_in (nullable) scales the INPUT: out = contract(pd_in * x) — the FastDiag
+// diagonal of the previous contraction, applied where its load can be
+// pipelined (the product rounds exactly like an output scaling would).
+void tensor_apply_tc_fold(int side, int n, const float* qpack, const float* x, float* out, const float* pd_in,
                           cudaStream_t st, long cols = 0);
 void pack_tf32_fold(int n, const float* q, float* qpack);
 // Host: split Q (n x n row-major) into tf32 hi/lo and pack as

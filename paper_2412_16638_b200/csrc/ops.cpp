@@ -133,9 +133,13 @@ FastDiagOp<T>::FastDiagOp(int n, const T* qa, const T* qa_inv, const T* qb, cons
     tc_split_ = tc_ && tensor_tc_supported_cols(n, (long)n * nz_) && tensor_tc_supported_cols(n, (long)n * ny_);
     if (tc_) {
       std::vector<float> hi(nn), lo(nn);
+      // folded kernels for all six factors or none (the folded kernel takes
+      // the diagonal on its input, the unfolded one on its output)
       const char* fenv = std::getenv("MPRKB_TC_FOLD");
+      bool all = !(fenv && fenv[0] == '0');
+      for (int f = 0; f < 6; ++f) all = all && fold_[f];
       for (int f = 0; f < 6; ++f) {
-        tcf_[f] = fold_[f] && !(fenv && fenv[0] == '0');
+        tcf_[f] = all;
         if (tcf_[f]) {  // folded: four (n/2)^2 blocks = n^2 floats
           pack_tf32_fold(n, src[f], hi.data());
           upload(qhp_[f], hi.data(), nn * sizeof(float));
@@ -244,7 +248,10 @@ void FastDiagOp<T>::apply_split(const T* x, T* out, cudaStream_t st) {
   contract(2, 1, x, t1, nullptr, ck, st);   // R: Qa^-1
   contract(1, 3, t1, t2, nullptr, ck, st);  // M: Qb^-1
   to_j(t2, t1, t3);
-  contract(0, 5, t3, t1, pd, cj, st);       // L: Qc^-1, then * pd_inv
+  // (folded tensor-core kernels take the diagonal on the next contraction's
+  // input instead: FAST only, where L follows directly)
+  const bool pd_next = tc_split_ && tcf_[0] && num_ == Numerics::Fast;
+  contract(0, 5, t3, t1, pd_next ? nullptr : pd, cj, st);  // L: Qc^-1, then * pd_inv
   if (num_ == Numerics::Parity) {
     to_k(t1, t2, t3);
     contract(2, 0, t3, t1, nullptr, ck, st);  // R: Qa
@@ -253,7 +260,7 @@ void FastDiagOp<T>::apply_split(const T* x, T* out, cudaStream_t st) {
     contract(0, 4, t3, t1, nullptr, cj, st);  // L: Qc
     to_k(t1, t2, out);
   } else {
-    contract(0, 4, t1, t2, nullptr, cj, st);  // L: Qc (the factors commute exactly)
+    contract(0, 4, t1, t2, pd_next ? pd : nullptr, cj, st);  // L: Qc (the factors commute exactly)
     to_k(t2, t1, t3);
     contract(1, 2, t3, t1, nullptr, ck, st);  // M: Qb
     contract(2, 0, t1, out, nullptr, ck, st); // R: Qa
@@ -278,10 +285,13 @@ void FastDiagOp<T>::apply(const void* xv, void* outv, cudaStream_t st) {
         else
           tensor_apply_tc(side, n_, qhp_[f].as<float>(), qlp_[f].as<float>(), in, o, pd, st);
       };
+      // folded: the diagonal rides on the input of the 4th contraction
+      const float* pd = pd_.as<float>();
+      const bool f = tcf_[0];
       tc(2, 1, x, t1, nullptr);
       tc(1, 3, t1, t2, nullptr);
-      tc(0, 5, t2, t1, pd_.as<float>());
-      tc(2, 0, t1, t2, nullptr);
+      tc(0, 5, t2, t1, f ? nullptr : pd);
+      tc(2, 0, t1, t2, f ? pd : nullptr);
       tc(1, 2, t2, t1, nullptr);
       tc(0, 4, t1, out, nullptr);
       return;

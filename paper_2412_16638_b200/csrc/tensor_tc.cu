@@ -354,24 +354,36 @@ void launch_tc(int n, long cols, const float* x, float* out, const float* pd, co
 // (spectral.cpp:17-20), so for a < n/2
 //     D[a] = E[a] + O[a],   D[n-1-a] = E[a] - O[a],
 //     E[a] = sum_{q even} Q[a][q] X[q],   O[a] = sum_{q odd} Q[a][q] X[q].
-// One CTA tile = all a < n/2 rows (M = 128 per a-tile) x 128 columns; each
-// k-block of 16 q feeds E with its 8 even q and O with its 8 odd q (3xTF32 each:
-// 6 MMAs, M = 128, N = 128, K = 8), E and O accumulate in two 128-column TMEM
-// blocks, double-buffered across tiles (512 columns).  Half the MMAs and half
-// the splitting work of the unfolded kernel per output; the epilogue writes
-// both rows a and n-1-a.  The converter de-interleaves even/odd q while it
-// splits, and the host packs Q's even/odd columns (pack_tf32_fold).
-constexpr int TF_BM = 128, TF_BN = 128, TF_BK = 16, TF_STAGES = 5;
-constexpr int TF_RAW = TF_BN * TF_BK * 4;      // 8 KB raw X
+// One CTA tile = 128 folded rows a (M = 128) x 128 columns; each k-block of
+// 16 q feeds E with its 8 even q and O with its 8 odd q (3xTF32 each: 6 MMAs,
+// M = 128, N = 128, K = 8); E and O accumulate in two 128-column TMEM blocks,
+// double-buffered across tiles (512 columns).  Half the MMAs and half the
+// splitting work of the unfolded kernel per output; the epilogue writes rows
+// a and n-1-a.  The converter de-interleaves even/odd q while it splits; the
+// host packs Q's even/odd columns (pack_tf32_fold).
+//
+// PDIN: the FastDiag diagonal is applied to the INPUT, x <- pd * x, by the
+// converter (pd arrives by its own TMA copy in the same pipeline stage as x,
+// so its latency is hidden like x's); the product pd*x rounds exactly like
+// the reference's epilogue scaling of the previous contraction's output.
+constexpr int TF_BM = 128, TF_BN = 128, TF_BK = 16;
+constexpr int TF_RAW = TF_BN * TF_BK * 4;      // 8 KB raw X (and raw pd)
 constexpr int TF_X = TF_BN * (TF_BK / 2) * 4;  // 4 KB per {even, odd} x {hi, lo}
 constexpr int TF_Q = TF_BM * (TF_BK / 2) * 4;  // 4 KB per {even, odd} x {hi, lo}
-constexpr int TF_STAGE = TF_RAW + 4 * TF_X + 4 * TF_Q;
 
+template <bool PDIN>
+struct TfCfg {
+  static constexpr int STAGES = PDIN ? 4 : 5;
+  static constexpr int STAGE = TF_RAW * (PDIN ? 2 : 1) + 4 * TF_X + 4 * TF_Q;
+};
+
+template <bool PDIN>
 struct TfSmem {
-  alignas(1024) unsigned char stage[TF_STAGES][TF_STAGE];
-  alignas(8) uint64_t full[TF_STAGES];
-  alignas(8) uint64_t conv[TF_STAGES];
-  alignas(8) uint64_t empty[TF_STAGES];
+  alignas(1024) unsigned char stage[TfCfg<PDIN>::STAGES][TfCfg<PDIN>::STAGE];
+  alignas(16) float stagec[4][32 * 32];  // epilogue transpose, one 32x32 block per epilogue warp
+  alignas(8) uint64_t full[TfCfg<PDIN>::STAGES];
+  alignas(8) uint64_t conv[TfCfg<PDIN>::STAGES];
+  alignas(8) uint64_t empty[TfCfg<PDIN>::STAGES];
   alignas(8) uint64_t tmem_full[2];
   alignas(8) uint64_t tmem_empty[2];
   uint32_t tmem_base;
@@ -402,12 +414,40 @@ __device__ __forceinline__ void mma_tf32f(uint32_t tmem_d, uint64_t da, uint64_t
 // canonical byte offset of (row, 4-chunk ch) in an 8-wide K-major block
 __device__ __forceinline__ int kofs8(int row, int ch) { return ((row >> 3) * 2 + ch) * 128 + (row & 7) * 16; }
 
-template <int SIDE, bool DIAG>
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a)
+               : "memory");
+  return v;
+}
+
+// ring position: stage index and its mbarrier phase, advanced without divisions
+template <int N>
+struct Ring {
+  int s = 0;
+  uint32_t ph = 0;
+  __device__ __forceinline__ void next() {
+    if (++s == N) {
+      s = 0;
+      ph ^= 1u;
+    }
+  }
+};
+
+template <int SIDE, bool PDIN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    k_tensor_tcf(const __grid_constant__ CUtensorMap xmap, float* __restrict__ C, const float* __restrict__ pd,
-                 const float* __restrict__ qpack, int n, int col_tiles, int num_tiles, long ldc) {
+    k_tensor_tcf(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap pmap,
+                 float* __restrict__ C, const float* __restrict__ qpack, int n, int col_tiles, int num_tiles,
+                 long ldc) {
+  using Cfg = TfCfg<PDIN>;
+  constexpr int NS = Cfg::STAGES;
   extern __shared__ unsigned char smem_raw[];
-  TfSmem& S = *reinterpret_cast<TfSmem*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  TfSmem<PDIN>& S =
+      *reinterpret_cast<TfSmem<PDIN>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int KB = n / TF_BK;
   const int h = n / 2;            // folded rows
@@ -415,9 +455,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const long nn = n, n2 = nn * nn;
   const size_t qh2 = (size_t)h * h;  // floats per packed half
   auto RAW = [&](int s) { return S.stage[s]; };
+  auto PDR = [&](int s) { return S.stage[s] + TF_RAW; };  // PDIN only
+  constexpr int XOFF = TF_RAW * (PDIN ? 2 : 1);
   // X{E,O}{H,L}: p = 0 even, 1 odd; l = 0 hi, 1 lo
-  auto XS = [&](int s, int p, int l) { return S.stage[s] + TF_RAW + (p * 2 + l) * TF_X; };
-  auto QS = [&](int s, int p, int l) { return S.stage[s] + TF_RAW + 4 * TF_X + (p * 2 + l) * TF_Q; };
+  auto XS = [&](int s, int p, int l) { return S.stage[s] + XOFF + (p * 2 + l) * TF_X; };
+  auto QS = [&](int s, int p, int l) { return S.stage[s] + XOFF + 4 * TF_X + (p * 2 + l) * TF_Q; };
   struct Tile {
     int a0, plane;
     long col0;
@@ -431,6 +473,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     return T;
   };
   const CUtensorMap* xm = &xmap;
+  const CUtensorMap* pm = &pmap;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
@@ -438,7 +481,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 32 * TC_PROD_WARP) {
-    for (int s = 0; s < TF_STAGES; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(&S.full[s], 1);
       mbar_init(&S.conv[s], 32 * TC_CONV_WARPS);
       mbar_init(&S.empty[s], 1);
@@ -456,19 +499,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   if (warp == TC_PROD_WARP) {
     if (lane == 0) {
+      Ring<NS> r;
       long g = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         const Tile T = tile_of(t);
-        for (int kb = 0; kb < KB; ++kb, ++g) {
-          const int s = (int)(g % TF_STAGES);
-          if (g >= TF_STAGES) mbar_wait(&S.empty[s], (uint32_t)((g / TF_STAGES) - 1) & 1);
-          mbar_expect_tx(&S.full[s], TF_RAW + 4 * TF_Q);
-          if (SIDE == 2)
+        for (int kb = 0; kb < KB; ++kb, ++g, r.next()) {
+          const int s = r.s;
+          if (g >= NS) mbar_wait(&S.empty[s], r.ph ^ 1u);
+          mbar_expect_tx(&S.full[s], TF_RAW * (PDIN ? 2 : 1) + 4 * TF_Q);
+          if (SIDE == 2) {
             tma_2d(RAW(s), xm, kb * TF_BK, (int)T.col0, &S.full[s]);
-          else if (SIDE == 1)
+            if (PDIN) tma_2d(PDR(s), pm, kb * TF_BK, (int)T.col0, &S.full[s]);
+          } else if (SIDE == 1) {
             tma_3d(RAW(s), xm, (int)T.col0, kb * TF_BK, T.plane, &S.full[s]);
-          else
+            if (PDIN) tma_3d(PDR(s), pm, (int)T.col0, kb * TF_BK, T.plane, &S.full[s]);
+          } else {
             tma_2d(RAW(s), xm, (int)T.col0, kb * TF_BK, &S.full[s]);
+            if (PDIN) tma_2d(PDR(s), pm, (int)T.col0, kb * TF_BK, &S.full[s]);
+          }
           // packed Q halves: [k-block of 8][row-group][2 chunks][8 rows][4]
           const size_t qoff = ((size_t)kb * (h / 8) + T.a0 / 8) * 64;
           for (int p = 0; p < 2; ++p)
@@ -479,16 +527,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   } else if (warp == TC_MMA_WARP) {
     if (lane == 0) {
-      long g = 0;
+      Ring<NS> r;
       int it = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
         const int acc = it & 1;
         mbar_wait(&S.tmem_empty[acc], (uint32_t)((it >> 1) & 1) ^ 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t dE = tmem + (uint32_t)(acc * 256), dO = dE + 128;
-        for (int kb = 0; kb < KB; ++kb, ++g) {
-          const int s = (int)(g % TF_STAGES);
-          mbar_wait(&S.conv[s], (uint32_t)(g / TF_STAGES) & 1);
+        for (int kb = 0; kb < KB; ++kb, r.next()) {
+          const int s = r.s;
+          mbar_wait(&S.conv[s], r.ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t first = kb ? 1u : 0u;
 #pragma unroll
@@ -506,27 +554,44 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
   } else if (warp < TC_CONV_WARPS) {
-    // raw fp32 -> tf32 hi/lo, even q -> E block, odd q -> O block
+    // raw fp32 (x pd) -> tf32 hi/lo, even q -> E block, odd q -> O block
     const int ct = tid;  // 0..127: one X column (B row) per thread
-    long g = 0;
+    Ring<NS> r;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      for (int kb = 0; kb < KB; ++kb, ++g) {
-        const int s = (int)(g % TF_STAGES);
-        mbar_wait(&S.full[s], (uint32_t)(g / TF_STAGES) & 1);
+      for (int kb = 0; kb < KB; ++kb, r.next()) {
+        const int s = r.s;
+        mbar_wait(&S.full[s], r.ph);
         const uint32_t raw = smem_u32(RAW(s));
         float v[TF_BK];
         if (SIDE == 2) {
           // raw [128 columns][16 q] (64 B rows)
 #pragma unroll
-          for (int j = 0; j < 4; ++j)
-            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                         : "=f"(v[4 * j]), "=f"(v[4 * j + 1]), "=f"(v[4 * j + 2]), "=f"(v[4 * j + 3])
-                         : "r"(raw + ct * 64 + j * 16));
+          for (int j = 0; j < 4; ++j) {
+            const float4 w = lds128(raw + ct * 64 + j * 16);
+            v[4 * j] = w.x; v[4 * j + 1] = w.y; v[4 * j + 2] = w.z; v[4 * j + 3] = w.w;
+          }
+          if (PDIN) {
+            const uint32_t pr = smem_u32(PDR(s));
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float4 w = lds128(pr + ct * 64 + j * 16);
+              v[4 * j] *= w.x; v[4 * j + 1] *= w.y; v[4 * j + 2] *= w.z; v[4 * j + 3] *= w.w;
+            }
+          }
         } else {
           // raw [16 q][128 columns] (512 B rows)
 #pragma unroll
           for (int q = 0; q < TF_BK; ++q)
             asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[q]) : "r"(raw + q * 512 + ct * 4));
+          if (PDIN) {
+            const uint32_t pr = smem_u32(PDR(s));
+#pragma unroll
+            for (int q = 0; q < TF_BK; ++q) {
+              float w;
+              asm volatile("ld.shared.f32 %0, [%1];" : "=f"(w) : "r"(pr + q * 512 + ct * 4));
+              v[q] *= w;
+            }
+          }
         }
 #pragma unroll
         for (int p = 0; p < 2; ++p)
@@ -554,6 +619,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
   } else if (warp < TC_EPI_WARP0 + 4) {
     const int q4 = warp - TC_EPI_WARP0;
+    const uint32_t sb = smem_u32(S.stagec[q4]);
+    const int rr = lane >> 3, c4 = lane & 7;  // transposed read-back: 4 rows x 8 chunks
     int it = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
       const Tile T = tile_of(t);
@@ -572,36 +639,36 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
             const long f = (T.col0 + cc + j) * nn;
-            float v1 = __uint_as_float(e[j]) + __uint_as_float(o[j]);
-            float v2 = __uint_as_float(e[j]) - __uint_as_float(o[j]);
-            if (DIAG) {
-              v1 *= __ldg(pd + f + a);
-              v2 *= __ldg(pd + f + am);
-            }
-            C[f + a] = v1;
-            C[f + am] = v2;
+            C[f + a] = __uint_as_float(e[j]) + __uint_as_float(o[j]);
+            C[f + am] = __uint_as_float(e[j]) - __uint_as_float(o[j]);
           }
         } else {
-          const long b1 = SIDE == 1 ? (long)T.plane * n2 + a * nn + T.col0 + cc : a * ldc + T.col0 + cc;
-          const long b2 = SIDE == 1 ? (long)T.plane * n2 + am * nn + T.col0 + cc : am * ldc + T.col0 + cc;
+          // rows a (E+O) and n-1-a (E-O) are row-major outputs: transpose each
+          // 32x32 block through smem (16-byte chunks XOR-swizzled by row) so
+          // every store instruction covers 4 full 128-byte rows
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            float4 v1, v2;
-            float* p1 = &v1.x;
-            float* p2 = &v2.x;
+          for (int half = 0; half < 2; ++half) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              p1[u] = __uint_as_float(e[j + u]) + __uint_as_float(o[j + u]);
-              p2[u] = __uint_as_float(e[j + u]) - __uint_as_float(o[j + u]);
+            for (int c = 0; c < 8; ++c) {
+              float4 w;
+              float* pw = &w.x;
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                const float ev = __uint_as_float(e[4 * c + u]), ov = __uint_as_float(o[4 * c + u]);
+                pw[u] = half ? ev - ov : ev + ov;
+              }
+              sts128(sb + (uint32_t)(lane * 128 + ((c ^ (lane & 7)) << 4)), w);
             }
-            if (DIAG) {
-              const float4 d1 = __ldg(reinterpret_cast<const float4*>(pd + b1 + j));
-              const float4 d2 = __ldg(reinterpret_cast<const float4*>(pd + b2 + j));
-              v1.x *= d1.x; v1.y *= d1.y; v1.z *= d1.z; v1.w *= d1.w;
-              v2.x *= d2.x; v2.y *= d2.y; v2.z *= d2.z; v2.w *= d2.w;
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              const int r = 4 * i + rr;  // local row = TMEM lane of the writer
+              const float4 w = lds128(sb + (uint32_t)(r * 128 + ((c4 ^ (r & 7)) << 4)));
+              const long row = half ? n - 1 - (T.a0 + 32 * q4 + r) : T.a0 + 32 * q4 + r;
+              const long off = (SIDE == 1 ? (long)T.plane * n2 + row * nn : row * ldc) + T.col0 + cc + 4 * c4;
+              *reinterpret_cast<float4*>(C + off) = w;
             }
-            *reinterpret_cast<float4*>(C + b1 + j) = v1;
-            *reinterpret_cast<float4*>(C + b2 + j) = v2;
+            __syncwarp();
           }
         }
       }
@@ -614,44 +681,51 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
 }
 
-template <int SIDE, bool DIAG>
+template <int SIDE, bool PDIN>
 void launch_tcf(int n, long cols, const float* x, float* out, const float* pd, const float* qpack, cudaStream_t st) {
-  const size_t smem = sizeof(TfSmem) + 1024;
+  const size_t smem = sizeof(TfSmem<PDIN>) + 1024;
   static bool configured = false;
   if (!configured) {
-    CUDA_CHECK(cudaFuncSetAttribute(k_tensor_tcf<SIDE, DIAG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_CHECK(cudaFuncSetAttribute(k_tensor_tcf<SIDE, PDIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
   }
   const cuuint64_t nn = (cuuint64_t)n, n2 = nn * nn, cc = (cuuint64_t)cols;
-  CUtensorMap map;
+  CUtensorMap map, pmap;
   int col_tiles, planes = 1;
+  auto mk = [&](const float* p, int rank, const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box) {
+    return make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, p, rank, dims, strides, box);
+  };
   if (SIDE == 2) {
     const cuuint64_t dims[2] = {nn, cc}, strides[1] = {nn * 4};
     const cuuint32_t box[2] = {(cuuint32_t)TF_BK, (cuuint32_t)TF_BN};
-    map = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, x, 2, dims, strides, box);
+    map = mk(x, 2, dims, strides, box);
+    pmap = PDIN ? mk(pd, 2, dims, strides, box) : map;
     col_tiles = (int)(cc / TF_BN);
   } else if (SIDE == 1) {
     const cuuint64_t dims[3] = {nn, nn, cc / nn}, strides[2] = {nn * 4, n2 * 4};
     const cuuint32_t box[3] = {(cuuint32_t)TF_BN, (cuuint32_t)TF_BK, 1};
-    map = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, x, 3, dims, strides, box);
+    map = mk(x, 3, dims, strides, box);
+    pmap = PDIN ? mk(pd, 3, dims, strides, box) : map;
     col_tiles = (int)(nn / TF_BN);
     planes = (int)(cc / nn);
   } else {
     const cuuint64_t dims[2] = {cc, nn}, strides[1] = {cc * 4};
     const cuuint32_t box[2] = {(cuuint32_t)TF_BN, (cuuint32_t)TF_BK};
-    map = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, x, 2, dims, strides, box);
+    map = mk(x, 2, dims, strides, box);
+    pmap = PDIN ? mk(pd, 2, dims, strides, box) : map;
     col_tiles = (int)(cc / TF_BN);
   }
   const int num_tiles = (n / 2 / TF_BM) * col_tiles * planes;
   const int grid = num_tiles < sm_count() ? num_tiles : sm_count();
-  k_tensor_tcf<SIDE, DIAG><<<grid, TC_THREADS, smem, st>>>(map, out, pd, qpack, n, col_tiles, num_tiles, cols);
+  k_tensor_tcf<SIDE, PDIN><<<grid, TC_THREADS, smem, st>>>(map, pmap, out, qpack, n, col_tiles, num_tiles, cols);
   LAUNCHED("tensor_tc_fold");
 }
 
 }  // namespace
 
-void tensor_apply_tc_fold(int side, int n, const float* qpack, const float* x, float* out, const float* pd,
+void tensor_apply_tc_fold(int side, int n, const float* qpack, const float* x, float* out, const float* pd_in,
                           cudaStream_t st, long cols) {
+  const float* pd = pd_in;
   if (cols <= 0) cols = (long)n * n;
   switch (side) {
     case 2:
