@@ -345,22 +345,28 @@ __device__ __forceinline__ double term1(const CombineTerms& t, int c, size_t i) 
 
 // rhs = u; rhs += (tau a_ij) f_j ...; rhs += (tau a_ii) g   (stepper.cpp:157-172)
 // out_kind 0 double (+finite flag), 1 float (overflow flag), 2 c32, 3 c64
+// out2 (nullable): a second copy of the result — the solver's initial guess
+// x0 = rhs (stepper.cpp:111), written in the same pass instead of a copy.
 template <int KIND>
 __global__ void __launch_bounds__(kBlock) k_combine(size_t m, const double* u, CombineTerms t, void* out,
-                                                    int* flag) {
+                                                    void* out2, int* flag) {
   bool bad = false;
   auto emit = [&](size_t i, double r) {
     if (KIND == 0) {
       static_cast<double*>(out)[i] = r;
+      if (out2) static_cast<double*>(out2)[i] = r;
       bad |= !isfinite(r);
     } else if (KIND == 1) {
       bad |= f32_overflows(r);
       static_cast<float*>(out)[i] = __double2float_rn(r);
+      if (out2) static_cast<float*>(out2)[i] = __double2float_rn(r);
     } else if (KIND == 2) {
       bad |= f32_overflows(r);
       static_cast<c32*>(out)[i] = c32{__double2float_rn(r), 0.0f};
+      if (out2) static_cast<c32*>(out2)[i] = c32{__double2float_rn(r), 0.0f};
     } else {
       static_cast<c64*>(out)[i] = c64{r, 0.0};
+      if (out2) static_cast<c64*>(out2)[i] = c64{r, 0.0};
     }
   };
   for_each4(
@@ -374,6 +380,7 @@ __global__ void __launch_bounds__(kBlock) k_combine(size_t m, const double* u, C
         }
         if (KIND == 0) {
           st4(static_cast<double*>(out) + i, r);
+          if (out2) st4(static_cast<double*>(out2) + i, r);
 #pragma unroll
           for (int e = 0; e < 4; ++e) bad |= !isfinite(r.x[e]);
         } else if (KIND == 1) {
@@ -384,6 +391,7 @@ __global__ void __launch_bounds__(kBlock) k_combine(size_t m, const double* u, C
             f.x[e] = __double2float_rn(r.x[e]);
           }
           st4(static_cast<float*>(out) + i, f);
+          if (out2) st4(static_cast<float*>(out2) + i, f);
         } else {
 #pragma unroll
           for (int e = 0; e < 4; ++e) emit(i + e, r.x[e]);
@@ -398,12 +406,12 @@ __global__ void __launch_bounds__(kBlock) k_combine(size_t m, const double* u, C
 }
 
 void combine(size_t m, const double* u, const CombineTerms& t, int out_kind, void* out, int* flag,
-             cudaStream_t st) {
+             cudaStream_t st, void* out2) {
   switch (out_kind) {
-    case 0: k_combine<0><<<wave(m), kBlock, 0, st>>>(m, u, t, out, flag); break;
-    case 1: k_combine<1><<<wave(m), kBlock, 0, st>>>(m, u, t, out, flag); break;
-    case 2: k_combine<2><<<wave(m), kBlock, 0, st>>>(m, u, t, out, flag); break;
-    default: k_combine<3><<<wave(m), kBlock, 0, st>>>(m, u, t, out, flag); break;
+    case 0: k_combine<0><<<wave(m), kBlock, 0, st>>>(m, u, t, out, out2, flag); break;
+    case 1: k_combine<1><<<wave(m), kBlock, 0, st>>>(m, u, t, out, out2, flag); break;
+    case 2: k_combine<2><<<wave(m), kBlock, 0, st>>>(m, u, t, out, out2, flag); break;
+    default: k_combine<3><<<wave(m), kBlock, 0, st>>>(m, u, t, out, out2, flag); break;
   }
   LAUNCHED("combine");
 }

@@ -113,6 +113,17 @@ std::array<double, 2> finish_red(KrylovWork<T>& w, int nv, cudaStream_t st) {
   return v;
 }
 
+// Several single-value FAST reductions in one round trip: one stream
+// synchronize, one cross-rank all-reduce of the whole batch.
+template <class T, size_t K>
+std::array<double, K> finish_slots(KrylovWork<T>& w, const std::array<int, K>& slots, cudaStream_t st) {
+  stream_sync(st);
+  std::array<double, K> v{};
+  for (size_t i = 0; i < K; ++i) w.red.result(slots[i], 1, &v[i]);
+  if (w.comm && w.comm->size() > 1) w.comm->allreduce_sum(v.data(), (int)K);
+  return v;
+}
+
 // detail::dot_real / dot (krylov.hpp:43-67) over the whole (possibly split)
 // vector.  PARITY on a split grid keeps the reference's single accumulator
 // in global index order: rank r continues from rank r-1's partial sum, handed
@@ -149,7 +160,7 @@ std::array<double, 2> global_dot(KrylovWork<T>& w, bool conj, const T* a, const 
 }  // namespace
 
 template <class T>
-KrylovWork<T>::KrylovWork(size_t m) : red(2), m_(m) {
+KrylovWork<T>::KrylovWork(size_t m) : red(4), m_(m) {
   for (auto& v : vecs_) v.alloc(m * sizeof(T));
 }
 
@@ -207,7 +218,38 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
     return fast ? fetch() : rdot(dst, dst);
   };
 
-  const double r0 = (double)std::sqrt(residual(r));
+  // FAST with the fused stencil: the scalars the reference needs one at a time
+  // are produced speculatively and read in batches — r0, r.z and p.Ap of the
+  // first iteration in ONE round trip, and (for an exact-inverse
+  // preconditioner such as FastDiag, where the first update normally
+  // converges) ||r|| with the true residual in another.  Every decision is
+  // still taken in the reference's order on the same values; work the
+  // reference would have skipped only touches scratch vectors (never x).
+  const bool batch = fast && S != nullptr;
+  const bool spec_true = batch && P != nullptr && P->exact_inverse();
+  const RedSlot s1 = w.red.slot(1), s2 = w.red.slot(2), s3 = w.red.slot(3);
+  double r0;
+  R rz{}, pq_first{};
+  bool have_pq = false;
+  if (batch) {
+    {
+      Bracket br(timer, "stencil", st);
+      stencil_residual<T>(*S, x, b, r, &s0, st);
+    }
+    pre(r, z);
+    dot_real<T>(m, r, z, s1, num, st);
+    {
+      Bracket br(timer, "stencil", st);
+      stencil_apply_dot<T>(*S, z, q, s2, st);
+    }
+    const auto v = finish_slots<T, 3>(w, {0, 1, 2}, st);
+    r0 = (double)std::sqrt((R)v[0]);
+    rz = (R)v[1];
+    pq_first = (R)v[2];
+    have_pq = true;
+  } else {
+    r0 = (double)std::sqrt(residual(r));
+  }
   rep.history.push_back(r0);
   double rnorm = r0;
   bool x_clean = true;  // ||b - A x|| of the current x is known
@@ -215,16 +257,23 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
   if (crit.satisfied(rnorm, r0)) {
     rep.converged = true;
   } else {
-    pre(r, z);
-    std::swap(p, z);  // p = z
-    R rz = rdot(r, p);
+    if (!batch) {
+      pre(r, z);
+      std::swap(p, z);  // p = z
+      rz = rdot(r, p);
+    } else {
+      std::swap(p, z);  // p = z (q = A p already formed)
+    }
     for (int k = 0; k < crit.max_iter; ++k) {
       if (!(rz > R{})) {
         rep.failure = 2;
         break;
       }
       R pq;
-      if (S) {
+      if (have_pq) {
+        pq = pq_first;
+        have_pq = false;
+      } else if (S) {
         Bracket br(timer, "stencil", st);
         stencil_apply_dot<T>(*S, p, q, s0, st);
         pq = fetch();
@@ -240,10 +289,21 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
       cg_update<T>(m, alpha, x, p, r, q, fast ? &s0 : nullptr, st);
       x_clean = false;
       ++rep.iterations;
-      rnorm = (double)std::sqrt(fast ? fetch() : rdot(r, r));
+      double rt_spec = -1.0;
+      if (spec_true) {
+        {
+          Bracket br(timer, "stencil", st);
+          stencil_residual<T>(*S, x, b, q, &s3, st);  // q is free after the update
+        }
+        const auto v = finish_slots<T, 2>(w, {0, 3}, st);
+        rnorm = (double)std::sqrt((R)v[0]);
+        rt_spec = (double)std::sqrt((R)v[1]);
+      } else {
+        rnorm = (double)std::sqrt(fast ? fetch() : rdot(r, r));
+      }
       rep.history.push_back(rnorm);
       if (crit.satisfied(rnorm, r0)) {
-        const double rt = (double)std::sqrt(residual(q));
+        const double rt = rt_spec >= 0.0 ? rt_spec : (double)std::sqrt(residual(q));
         x_clean = true;
         clean_true = rt;
         if (crit.satisfied(rt, r0)) {

@@ -156,8 +156,9 @@ struct CombineTerms {
 // rhs = u + sum_t coef_t * v_t (one axpy per term, in order), written as:
 // out_kind 0: double (+ finite flag), 1: float (downcast, overflow flag),
 // 2: c32 (float, 0), 3: c64 (double, 0).
+// out2 (nullable): second copy of the result (the stage solve's x0).
 void combine(size_t m, const double* u, const CombineTerms& t, int out_kind, void* out, int* flag,
-             cudaStream_t st);
+             cudaStream_t st, void* out2 = nullptr);
 // y = widen(x) / real_part(x) of the solver output, + non-finite flag.
 void extract_stage(size_t m, int src_kind, const void* x, double* y, int* flag, cudaStream_t st);
 // u += sum_t coef_t * v_t, + non-finite flag on u.

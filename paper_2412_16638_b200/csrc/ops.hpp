@@ -22,6 +22,10 @@ class Op {
   // Non-null when the operator is a built-in KronSum stencil: lets the FAST
   // solvers fuse residual / dot epilogues into the stencil pass.
   virtual const StencilSpec* stencil() const { return nullptr; }
+  // True for a preconditioner that inverts the stage operator exactly in
+  // exact arithmetic (FastDiag): CG then normally converges after one update,
+  // which the FAST solver exploits to batch its scalar round trips.
+  virtual bool exact_inverse() const { return false; }
 
  private:
   int dtype_;
@@ -58,6 +62,7 @@ class FastDiagOp final : public Op {
   FastDiagOp(int n, const T* qa, const T* qa_inv, const T* qb, const T* qb_inv, const T* qc, const T* qc_inv,
              const T* la, const T* lb, const T* lc, Numerics num, const Halo* halo = nullptr);
   void apply(const void* x, void* out, cudaStream_t st) override;
+  bool exact_inverse() const override { return true; }
   int n() const { return n_; }
 
  private:

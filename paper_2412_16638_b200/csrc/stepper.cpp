@@ -179,11 +179,10 @@ void Stepper::step(double* u, StepTrace& trace) {
       const int out_kind = solve_dtype_ == 0 ? 1 : solve_dtype_ == 1 ? 0 : solve_dtype_;
       int* flag = (solve_dtype_ == 0 || solve_dtype_ == 2) ? check_slot(6, kOverflow) : sink;
       {
+        // x0 = narrowed rhs (stepper.cpp:111, 120, 135, 146), written by the same pass
         Bracket br(timer_, "axpy", st_);
-        combine(m, u, terms, out_kind, bsol_.get(), flag, st_);
+        combine(m, u, terms, out_kind, bsol_.get(), flag, st_, xsol_.get());
       }
-      // x0 = narrowed rhs (stepper.cpp:111, 120, 135, 146)
-      CUDA_CHECK(cudaMemcpyAsync(xsol_.get(), bsol_.get(), m * dtype_size(solve_dtype_), cudaMemcpyDeviceToDevice, st_));
       SolveReport rep;
       EventTimer* tm = timer_.enabled() ? &timer_ : nullptr;
       switch (solve_dtype_) {
