@@ -64,7 +64,7 @@ void pack_tf32_split(int n, const float* q, float* hi_packed, float* lo_packed) 
 
 // rows a < n/2, columns split by parity of q: E[a][q'] = Q[a][2q'],
 // O[a][q'] = Q[a][2q'+1], each tf32 hi/lo, packed
-// [k-block of 8][row-group of 8][k-chunk of 4 (2 per block)][8 rows][4]
+// [k-block of 16][row-group of 8][k-chunk of 4 (4 per block)][8 rows][4]
 void pack_tf32_fold(int n, const float* q, float* qpack) {
   const size_t h = (size_t)n / 2, blk = h * h;
   for (size_t row = 0; row < h; ++row)
@@ -73,8 +73,8 @@ void pack_tf32_fold(int n, const float* q, float* qpack) {
         const float x = q[row * n + 2 * k + p];
         const float hi = tf32_rna(x);
         const float lo = tf32_rna(x - hi);
-        const size_t kb = k / 8, c = (k % 8) / 4, j = k % 4, g = row / 8, r = row % 8;
-        const size_t o = (((kb * (h / 8) + g) * 2 + c) * 8 + r) * 4 + j;
+        const size_t kb = k / 16, c = (k % 16) / 4, j = k % 4, g = row / 8, r = row % 8;
+        const size_t o = (((kb * (h / 8) + g) * 4 + c) * 8 + r) * 4 + j;
         qpack[(size_t)(p * 2 + 0) * blk + o] = hi;
         qpack[(size_t)(p * 2 + 1) * blk + o] = lo;
       }

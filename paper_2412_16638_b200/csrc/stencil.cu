@@ -562,7 +562,10 @@ __global__ void __launch_bounds__(TTHREADS)
     }
 #pragma unroll
     for (int rr = 0; rr < TROWS; ++rr) pre[rr] = nxt[rr];
-    __syncthreads();  // ring slot of plane q - 1 is free
+    // ring slot of plane q - 1 is free: order this thread's generic reads of it
+    // before the async-proxy (TMA) refill, then let thread 0 issue it
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
     if (tid == 0 && q - 1 + TST < planes) issue(q - 1 + TST);
   }
   epi.finish(st);

@@ -366,36 +366,49 @@ void launch_tc(int n, long cols, const float* x, float* out, const float* pd, co
 // converter (pd arrives by its own TMA copy in the same pipeline stage as x,
 // so its latency is hidden like x's); the product pd*x rounds exactly like
 // the reference's epilogue scaling of the previous contraction's output.
-constexpr int TF_BM = 128, TF_BN = 128, TF_BK = 16;
-constexpr int TF_RAW = TF_BN * TF_BK * 4;      // 8 KB raw X (and raw pd)
-constexpr int TF_X = TF_BN * (TF_BK / 2) * 4;  // 4 KB per {even, odd} x {hi, lo}
-constexpr int TF_Q = TF_BM * (TF_BK / 2) * 4;  // 4 KB per {even, odd} x {hi, lo}
+constexpr int TF_BM = 128, TF_BN = 128, TF_BK = 32;  // 32 q per k-block: 16 even + 16 odd
+constexpr int TF_KH = TF_BK / 2;                    // K per parity per k-block (2 MMA k-steps)
+constexpr int TF_RAW = TF_BN * TF_BK * 4;           // 16 KB raw X (and raw pd)
+constexpr int TF_X = TF_BN * TF_KH * 4;             // 8 KB per {even, odd} x {hi, lo}
+constexpr int TF_Q = TF_BM * TF_KH * 4;             // 8 KB per {even, odd} x {hi, lo}
 
+// Three decoupled rings: raw X (+ pd) tiles, released by the converters as
+// soon as they are read, so the TMA runs up to RS k-blocks ahead; the packed
+// Q tiles (L2-resident), released by the MMA; the split X hi/lo operands.
 template <bool PDIN>
 struct TfCfg {
-  static constexpr int STAGES = PDIN ? 4 : 5;
-  static constexpr int STAGE = TF_RAW * (PDIN ? 2 : 1) + 4 * TF_X + 4 * TF_Q;
+  static constexpr int RAWB = TF_RAW * (PDIN ? 2 : 1);
+  static constexpr int RS = PDIN ? 2 : 3;  // raw ring
+  static constexpr int QS = 2;             // Q ring
+  static constexpr int CS = PDIN ? 2 : 3;  // converted ring
 };
 
 template <bool PDIN>
 struct TfSmem {
-  alignas(1024) unsigned char stage[TfCfg<PDIN>::STAGES][TfCfg<PDIN>::STAGE];
+  using Cfg = TfCfg<PDIN>;
+  alignas(1024) unsigned char raw[Cfg::RS][Cfg::RAWB];
+  alignas(1024) unsigned char q[Cfg::QS][4 * TF_Q];
+  alignas(1024) unsigned char x[Cfg::CS][4 * TF_X];
   alignas(16) float stagec[4][32 * 32];  // epilogue transpose, one 32x32 block per epilogue warp
-  alignas(8) uint64_t full[TfCfg<PDIN>::STAGES];
-  alignas(8) uint64_t conv[TfCfg<PDIN>::STAGES];
-  alignas(8) uint64_t empty[TfCfg<PDIN>::STAGES];
+  alignas(8) uint64_t rawfull[Cfg::RS];
+  alignas(8) uint64_t rawfree[Cfg::RS];
+  alignas(8) uint64_t qfull[Cfg::QS];
+  alignas(8) uint64_t qfree[Cfg::QS];
+  alignas(8) uint64_t xfull[Cfg::CS];
+  alignas(8) uint64_t xfree[Cfg::CS];
   alignas(8) uint64_t tmem_full[2];
   alignas(8) uint64_t tmem_empty[2];
   uint32_t tmem_base;
 };
 
-// K-major no-swizzle canonical layout of an 8-wide k-block:
-// [row-group of 8][k-chunk of 4 (2 per block)][8 rows][16 B] -> LBO 128 B, SBO 256 B
-__device__ __forceinline__ uint64_t kmajor_desc8(const void* p) {
+// K-major no-swizzle canonical layout of a 16-wide (per parity) k-block:
+// [row-group of 8][k-chunk of 4 (4 per block)][8 rows][16 B] -> LBO 128 B,
+// SBO 512 B; MMA k-step ks (8 k) starts 256 B further.
+__device__ __forceinline__ uint64_t kmajor_desc16(const void* p) {
   uint64_t d = 0;
   d |= (uint64_t)((smem_u32(p) >> 4) & 0x3FFF);
   d |= (uint64_t)(128 >> 4) << 16;
-  d |= (uint64_t)(256 >> 4) << 32;
+  d |= (uint64_t)(512 >> 4) << 32;
   d |= (uint64_t)1 << 46;
   return d;
 }
@@ -411,8 +424,8 @@ __device__ __forceinline__ void mma_tf32f(uint32_t tmem_d, uint64_t da, uint64_t
       : "memory");
 }
 
-// canonical byte offset of (row, 4-chunk ch) in an 8-wide K-major block
-__device__ __forceinline__ int kofs8(int row, int ch) { return ((row >> 3) * 2 + ch) * 128 + (row & 7) * 16; }
+// canonical byte offset of (row, 4-chunk ch) in a 16-wide K-major block
+__device__ __forceinline__ int kofs16(int row, int ch) { return ((row >> 3) * 4 + ch) * 128 + (row & 7) * 16; }
 
 __device__ __forceinline__ void sts128(uint32_t a, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
@@ -442,9 +455,9 @@ template <int SIDE, bool PDIN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_tensor_tcf(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap pmap,
                  float* __restrict__ C, const float* __restrict__ qpack, int n, int col_tiles, int num_tiles,
-                 long ldc) {
+                 long ldc, int dbg) {
   using Cfg = TfCfg<PDIN>;
-  constexpr int NS = Cfg::STAGES;
+  constexpr int RS = Cfg::RS, QS = Cfg::QS, CS = Cfg::CS;
   extern __shared__ unsigned char smem_raw[];
   TfSmem<PDIN>& S =
       *reinterpret_cast<TfSmem<PDIN>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -454,12 +467,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const int a_tiles = h / TF_BM;  // 1 for n = 256
   const long nn = n, n2 = nn * nn;
   const size_t qh2 = (size_t)h * h;  // floats per packed half
-  auto RAW = [&](int s) { return S.stage[s]; };
-  auto PDR = [&](int s) { return S.stage[s] + TF_RAW; };  // PDIN only
-  constexpr int XOFF = TF_RAW * (PDIN ? 2 : 1);
-  // X{E,O}{H,L}: p = 0 even, 1 odd; l = 0 hi, 1 lo
-  auto XS = [&](int s, int p, int l) { return S.stage[s] + XOFF + (p * 2 + l) * TF_X; };
-  auto QS = [&](int s, int p, int l) { return S.stage[s] + XOFF + 4 * TF_X + (p * 2 + l) * TF_Q; };
+  auto RAW = [&](int s) { return S.raw[s]; };
+  auto PDR = [&](int s) { return S.raw[s] + TF_RAW; };  // PDIN only
+  // X{E,O}{H,L} / Q{E,O}{H,L}: p = 0 even, 1 odd; l = 0 hi, 1 lo
+  auto XS = [&](int s, int p, int l) { return S.x[s] + (p * 2 + l) * TF_X; };
+  auto QT = [&](int s, int p, int l) { return S.q[s] + (p * 2 + l) * TF_Q; };
   struct Tile {
     int a0, plane;
     long col0;
@@ -481,10 +493,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 32 * TC_PROD_WARP) {
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&S.full[s], 1);
-      mbar_init(&S.conv[s], 32 * TC_CONV_WARPS);
-      mbar_init(&S.empty[s], 1);
+    for (int s = 0; s < RS; ++s) {
+      mbar_init(&S.rawfull[s], 1);
+      mbar_init(&S.rawfree[s], 32 * TC_CONV_WARPS);
+    }
+    for (int s = 0; s < QS; ++s) {
+      mbar_init(&S.qfull[s], 1);
+      mbar_init(&S.qfree[s], 1);
+    }
+    for (int s = 0; s < CS; ++s) {
+      mbar_init(&S.xfull[s], 32 * TC_CONV_WARPS);
+      mbar_init(&S.xfree[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&S.tmem_full[b], 1);
@@ -498,57 +517,80 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t tmem = S.tmem_base;
 
   if (warp == TC_PROD_WARP) {
+    // lane 0: raw X (+ pd) tiles; lane 1: the packed Q tiles — two
+    // independent producers so neither ring throttles the other
     if (lane == 0) {
-      Ring<NS> r;
+      Ring<RS> r;
       long g = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
         const Tile T = tile_of(t);
         for (int kb = 0; kb < KB; ++kb, ++g, r.next()) {
           const int s = r.s;
-          if (g >= NS) mbar_wait(&S.empty[s], r.ph ^ 1u);
-          mbar_expect_tx(&S.full[s], TF_RAW * (PDIN ? 2 : 1) + 4 * TF_Q);
-          if (SIDE == 2) {
-            tma_2d(RAW(s), xm, kb * TF_BK, (int)T.col0, &S.full[s]);
-            if (PDIN) tma_2d(PDR(s), pm, kb * TF_BK, (int)T.col0, &S.full[s]);
-          } else if (SIDE == 1) {
-            tma_3d(RAW(s), xm, (int)T.col0, kb * TF_BK, T.plane, &S.full[s]);
-            if (PDIN) tma_3d(PDR(s), pm, (int)T.col0, kb * TF_BK, T.plane, &S.full[s]);
-          } else {
-            tma_2d(RAW(s), xm, (int)T.col0, kb * TF_BK, &S.full[s]);
-            if (PDIN) tma_2d(PDR(s), pm, (int)T.col0, kb * TF_BK, &S.full[s]);
+          if (g >= RS) mbar_wait(&S.rawfree[s], r.ph ^ 1u);
+          if (dbg & 16) {  // (profiling knob: no X loads)
+            mbar_expect_tx(&S.rawfull[s], 0);
+            continue;
           }
-          // packed Q halves: [k-block of 8][row-group][2 chunks][8 rows][4]
-          const size_t qoff = ((size_t)kb * (h / 8) + T.a0 / 8) * 64;
-          for (int p = 0; p < 2; ++p)
-            for (int l = 0; l < 2; ++l)
-              bulk_g2s(QS(s, p, l), qpack + (size_t)(p * 2 + l) * qh2 + qoff, TF_Q, &S.full[s]);
+          mbar_expect_tx(&S.rawfull[s], Cfg::RAWB);
+          if (SIDE == 2) {
+            tma_2d(RAW(s), xm, kb * TF_BK, (int)T.col0, &S.rawfull[s]);
+            if (PDIN) tma_2d(PDR(s), pm, kb * TF_BK, (int)T.col0, &S.rawfull[s]);
+          } else if (SIDE == 1) {
+            tma_3d(RAW(s), xm, (int)T.col0, kb * TF_BK, T.plane, &S.rawfull[s]);
+            if (PDIN) tma_3d(PDR(s), pm, (int)T.col0, kb * TF_BK, T.plane, &S.rawfull[s]);
+          } else {
+            tma_2d(RAW(s), xm, (int)T.col0, kb * TF_BK, &S.rawfull[s]);
+            if (PDIN) tma_2d(PDR(s), pm, (int)T.col0, kb * TF_BK, &S.rawfull[s]);
+          }
+        }
+      }
+    } else if (lane == 1) {
+      Ring<QS> r;
+      long g = 0;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        const Tile T = tile_of(t);
+        for (int kb = 0; kb < KB; ++kb, ++g, r.next()) {
+          const int s = r.s;
+          if (g >= QS) mbar_wait(&S.qfree[s], r.ph ^ 1u);
+          mbar_expect_tx(&S.qfull[s], (dbg & 2) ? 0 : 4 * TF_Q);
+          // packed Q halves: [k-block of 16][row-group][4 chunks][8 rows][4]
+          const size_t qoff = ((size_t)kb * (h / 8) + T.a0 / 8) * 128;
+          if (!(dbg & 2))
+            for (int p = 0; p < 2; ++p)
+              for (int l = 0; l < 2; ++l)
+                bulk_g2s(QT(s, p, l), qpack + (size_t)(p * 2 + l) * qh2 + qoff, TF_Q, &S.qfull[s]);
         }
       }
     }
   } else if (warp == TC_MMA_WARP) {
     if (lane == 0) {
-      Ring<NS> r;
+      Ring<CS> rx;
+      Ring<QS> rq;
       int it = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
         const int acc = it & 1;
         mbar_wait(&S.tmem_empty[acc], (uint32_t)((it >> 1) & 1) ^ 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t dE = tmem + (uint32_t)(acc * 256), dO = dE + 128;
-        for (int kb = 0; kb < KB; ++kb, r.next()) {
-          const int s = r.s;
-          mbar_wait(&S.conv[s], r.ph);
+        for (int kb = 0; kb < KB; ++kb, rx.next(), rq.next()) {
+          mbar_wait(&S.qfull[rq.s], rq.ph);
+          mbar_wait(&S.xfull[rx.s], rx.ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t first = kb ? 1u : 0u;
 #pragma unroll
-          for (int p = 0; p < 2; ++p) {
+          for (int p = 0; p < 2 && !(dbg & 8); ++p) {  // (dbg 8: profiling knob, no MMAs)
             const uint32_t d = p ? dO : dE;
-            const uint64_t qh = kmajor_desc8(QS(s, p, 0)), ql = kmajor_desc8(QS(s, p, 1));
-            const uint64_t xh = kmajor_desc8(XS(s, p, 0)), xl = kmajor_desc8(XS(s, p, 1));
-            mma_tf32f(d, ql, xh, first);
-            mma_tf32f(d, qh, xl, 1u);
-            mma_tf32f(d, qh, xh, 1u);
+#pragma unroll
+            for (int ks = 0; ks < TF_KH / 8; ++ks) {
+              const uint64_t qh = kmajor_desc16(QT(rq.s, p, 0) + ks * 256), ql = kmajor_desc16(QT(rq.s, p, 1) + ks * 256);
+              const uint64_t xh = kmajor_desc16(XS(rx.s, p, 0) + ks * 256), xl = kmajor_desc16(XS(rx.s, p, 1) + ks * 256);
+              mma_tf32f(d, ql, xh, (first | ks) ? 1u : 0u);
+              mma_tf32f(d, qh, xl, 1u);
+              mma_tf32f(d, qh, xh, 1u);
+            }
           }
-          mma_commit(&S.empty[s]);
+          mma_commit(&S.xfree[rx.s]);
+          mma_commit(&S.qfree[rq.s]);
         }
         mma_commit(&S.tmem_full[acc]);
       }
@@ -556,30 +598,41 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else if (warp < TC_CONV_WARPS) {
     // raw fp32 (x pd) -> tf32 hi/lo, even q -> E block, odd q -> O block
     const int ct = tid;  // 0..127: one X column (B row) per thread
-    Ring<NS> r;
+    Ring<RS> r;
+    Ring<CS> rx;
+    long g = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-      for (int kb = 0; kb < KB; ++kb, r.next()) {
+      for (int kb = 0; kb < KB; ++kb, ++g, r.next(), rx.next()) {
         const int s = r.s;
-        mbar_wait(&S.full[s], r.ph);
+        mbar_wait(&S.rawfull[s], r.ph);
+        if (dbg & 1) {  // (profiling knob: skip the split)
+          mbar_arrive(&S.rawfree[s]);
+          if (g >= CS) mbar_wait(&S.xfree[rx.s], rx.ph ^ 1u);
+          mbar_arrive(&S.xfull[rx.s]);
+          continue;
+        }
         const uint32_t raw = smem_u32(RAW(s));
         float v[TF_BK];
         if (SIDE == 2) {
-          // raw [128 columns][16 q] (64 B rows)
+          // raw [128 columns][32 q] (128 B rows, TMA 128-byte swizzle: chunk j
+          // of row ct sits at j ^ (ct % 8), so a warp's 16-byte loads are
+          // conflict-free)
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const float4 w = lds128(raw + ct * 64 + j * 16);
+          for (int j = 0; j < TF_BK / 4; ++j) {
+            const int jp = (dbg & 32) ? j : (j ^ (ct & 7));
+            const float4 w = lds128(raw + ct * (TF_BK * 4) + (jp << 4));
             v[4 * j] = w.x; v[4 * j + 1] = w.y; v[4 * j + 2] = w.z; v[4 * j + 3] = w.w;
           }
           if (PDIN) {
             const uint32_t pr = smem_u32(PDR(s));
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              const float4 w = lds128(pr + ct * 64 + j * 16);
+            for (int j = 0; j < TF_BK / 4; ++j) {
+              const float4 w = lds128(pr + ct * (TF_BK * 4) + ((j ^ (ct & 7)) << 4));
               v[4 * j] *= w.x; v[4 * j + 1] *= w.y; v[4 * j + 2] *= w.z; v[4 * j + 3] *= w.w;
             }
           }
         } else {
-          // raw [16 q][128 columns] (512 B rows)
+          // raw [32 q][128 columns] (512 B rows)
 #pragma unroll
           for (int q = 0; q < TF_BK; ++q)
             asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v[q]) : "r"(raw + q * 512 + ct * 4));
@@ -593,10 +646,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
           }
         }
+        if (g >= CS) mbar_wait(&S.xfree[rx.s], rx.ph ^ 1u);
 #pragma unroll
         for (int p = 0; p < 2; ++p)
 #pragma unroll
-          for (int ch = 0; ch < 2; ++ch) {
+          for (int ch = 0; ch < TF_KH / 4; ++ch) {
             uint32_t hi[4], lo[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -604,8 +658,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               hi[u] = tf32_rna(x);
               lo[u] = tf32_rna(x - __uint_as_float(hi[u]));
             }
-            const int o = kofs8(ct, ch);
-            const uint32_t dh = smem_u32(XS(s, p, 0)) + o, dl = smem_u32(XS(s, p, 1)) + o;
+            const int o = kofs16(ct, ch);
+            const uint32_t dh = smem_u32(XS(rx.s, p, 0)) + o, dl = smem_u32(XS(rx.s, p, 1)) + o;
             asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dh), "r"(hi[0]), "r"(hi[1]), "r"(hi[2]),
                          "r"(hi[3])
                          : "memory");
@@ -613,8 +667,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                          "r"(lo[3])
                          : "memory");
           }
+        // the proxy fence also orders this thread's raw-tile reads before the
+        // TMA refill of the slot (releasing it straight after the loads let
+        // the async-proxy write overtake them)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&S.conv[s]);
+        mbar_arrive(&S.rawfree[s]);
+        mbar_arrive(&S.xfull[rx.s]);
       }
     }
   } else if (warp < TC_EPI_WARP0 + 4) {
@@ -630,7 +688,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const long a = T.a0 + 32 * q4 + lane;  // folded row; its mirror is n-1-a
       const long am = n - 1 - a;
       const uint32_t lanebase = tmem + ((uint32_t)(32 * q4) << 16) + (uint32_t)(acc * 256);
-      for (int cc = 0; cc < TF_BN; cc += 32) {
+      for (int cc = 0; cc < TF_BN && !(dbg & 4); cc += 32) {
         uint32_t e[32], o[32];
         tmem_ld32(lanebase + (uint32_t)cc, e);
         tmem_ld32(lanebase + 128u + (uint32_t)cc, o);
@@ -689,11 +747,16 @@ void launch_tcf(int n, long cols, const float* x, float* out, const float* pd, c
     CUDA_CHECK(cudaFuncSetAttribute(k_tensor_tcf<SIDE, PDIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
   }
+  static const int dbg = [] {
+    const char* e = std::getenv("MPRKB_TC_DBG");  // profiling knobs only (results are garbage when set)
+    return e ? std::atoi(e) : 0;
+  }();
   const cuuint64_t nn = (cuuint64_t)n, n2 = nn * nn, cc = (cuuint64_t)cols;
   CUtensorMap map, pmap;
   int col_tiles, planes = 1;
   auto mk = [&](const float* p, int rank, const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box) {
-    return make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, p, rank, dims, strides, box);
+    return make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, p, rank, dims, strides, box,
+                    SIDE == 2 && !(dbg & 32) ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
   };
   if (SIDE == 2) {
     const cuuint64_t dims[2] = {nn, cc}, strides[1] = {nn * 4};
@@ -717,7 +780,8 @@ void launch_tcf(int n, long cols, const float* x, float* out, const float* pd, c
   }
   const int num_tiles = (n / 2 / TF_BM) * col_tiles * planes;
   const int grid = num_tiles < sm_count() ? num_tiles : sm_count();
-  k_tensor_tcf<SIDE, PDIN><<<grid, TC_THREADS, smem, st>>>(map, pmap, out, qpack, n, col_tiles, num_tiles, cols);
+  k_tensor_tcf<SIDE, PDIN><<<grid, TC_THREADS, smem, st>>>(map, pmap, out, qpack, n, col_tiles, num_tiles, cols,
+                                                           dbg);
   LAUNCHED("tensor_tc_fold");
 }
 

@@ -84,11 +84,12 @@ inline EncodeFn encode_fn() {
 }
 
 inline CUtensorMap make_map(CUtensorMapDataType dt, const void* x, int rank, const cuuint64_t* dims,
-                            const cuuint64_t* strides_bytes, const cuuint32_t* box) {
+                            const cuuint64_t* strides_bytes, const cuuint32_t* box,
+                            CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_NONE) {
   CUtensorMap m;
   const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
   const CUresult r = encode_fn()(&m, dt, (cuuint32_t)rank, const_cast<void*>(x), dims,
-                                 strides_bytes, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                 strides_bytes, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
                                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) MPRKB_THROW(20, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return m;
