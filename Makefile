@@ -27,7 +27,14 @@ CU_OBJS  := $(patsubst $(SRC)/%.cu,$(OBJ)/%.cu.o,$(CU_SRCS))
 CPP_OBJS := $(patsubst $(SRC)/%.cpp,$(OBJ)/%.cpp.o,$(CPP_SRCS))
 HDRS     := $(wildcard $(SRC)/*.hpp) $(wildcard $(SRC)/*.cuh) include/mprk_b200.h
 
-all: $(LIB) oracle
+CLI      := tools/mprk-b200
+
+all: $(LIB) oracle $(CLI)
+
+# the reference's benchmark harness (tools/main.cpp) over the C-ABI
+$(CLI): tools/mprk_cli.cpp include/mprk_b200.h $(LIB)
+	$(CXX) -O2 -std=c++17 -Wall -Iinclude $< -o $@ -L$(PKG) -lmprk_b200 -Wl,-rpath,'$$ORIGIN/../$(PKG)'
+
 
 $(OBJ)/%.cu.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJ)
@@ -47,6 +54,6 @@ ref:
 	$(MAKE) -C oracle ref
 
 clean:
-	rm -rf $(OBJ) $(LIB)
+	rm -rf $(OBJ) $(LIB) $(CLI)
 
 .PHONY: all oracle ref clean

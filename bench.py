@@ -325,22 +325,25 @@ def run_cuda_arm(args):
     line = None
     if rank == 0:
         # ---- roofline of the dominant kernel: the FastDiag contraction on the
-        # tensor cores (3xTF32, tensor_tc.cu).  Algorithmic work = one fp32
-        # GEMM, 2 n^4 flop per launch (n^3 outputs x n MACs); the 3xTF32 split
-        # issues three TF32 MMAs per algorithmic MAC, so the fp32-accurate
-        # ceiling is the dense TF32 peak / 3 (TF32 dense = bf16 dense / 2).
+        # tensor cores (folded 3xTF32, tensor_tc.cu).  Algorithmic work per
+        # launch = the reference's contraction: 2 n^4 flop (n^3 outputs x n
+        # MACs) and 8 N bytes (x in, out; the diagonal adds 4 N on 1 of 6).
+        # Executed: the sine fold halves the MACs and 3xTF32 triples them ->
+        # 3 n^4 TF32 flop.  Floors: HBM 8N / peak vs TF32 3n^4 / (bf16 dense / 2);
+        # the larger one is the bound reported.
         ms_launch = measure_contraction(mp, torch, st.stream)
-        flops = 2.0 * n ** 4
-        achieved = flops / (ms_launch * 1e-3) / 1e12
         peaks = load_peaks()
-        tf32 = peaks["bf16_tflops"] / 2.0
-        peak = tf32 / 3.0
-        # bytes the contraction must move: x in + out (fp32), + pd on the
-        # diagonal-fused launch (1 of 6): 8N x 6 + 4N per apply
+        flops = 2.0 * n ** 4
         bytes_launch = (8.0 * m * 6 + 4.0 * m) / 6.0
-        # ---- HBM-bound companion: the fp64 stencil (K1), 2*8*N bytes per launch
-        ms_sten = measure_stencil(mp, torch, st.stream)
-        gbs = 16.0 * m / (ms_sten * 1e-3) / 1e9
+        tf32 = peaks["bf16_tflops"] / 2.0
+        t_hbm = bytes_launch / (peaks["hbm_gbs"] * 1e9)
+        t_tc = 3.0 * n ** 4 / (tf32 * 1e12)
+        hbm_gbs_c = bytes_launch / (ms_launch * 1e-3) / 1e9
+        tc_exec = 3.0 * n ** 4 / (ms_launch * 1e-3) / 1e12
+        # ---- HBM-bound companion: the step's most frequent stencil, the fused
+        # fp32 residual r = b - A x with ||r||^2 (TMA plane pipeline), 12 N bytes
+        ktab = kernel_table(mp, N_GRID, peaks["hbm_gbs"])
+        sten = ktab["residual_f32"]
         line = {
             "metric": METRIC, "value": value, "unit": "DOF-updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "steps_per_s": 1e3 / ms_step,
@@ -352,22 +355,28 @@ def run_cuda_arm(args):
             "e2e": {"value": e2e_value, "unit": "DOF-updates/s", "h2d_bytes_per_step": 8 * m_local * world,
                     "d2h_bytes_per_step": 8 * m_local * world, "steps": e2e_steps,
                     "note": "Stepper.step(host pinned f64 state) through the C-ABI, wall clock"},
-            "roofline": {"kernel": "k_tensor_tc (FastDiag contraction, tcgen05 3xTF32, fp32 accumulate in TMEM)",
-                         "bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak,
-                         "peak_source": (f"{peaks['src_tc']}: dense TF32 = bf16 {peaks['bf16_tflops']:.0f} / 2 = "
-                                         f"{tf32:.0f} TFLOP/s, / 3 MMAs per fp32 MAC (3xTF32)"),
-                         "flop_per_launch": flops, "ms_per_launch": ms_launch,
-                         "executed_tf32_tflops": 3 * achieved,
-                         "hbm_gbs": bytes_launch / (ms_launch * 1e-3) / 1e9,
-                         "hbm_frac": bytes_launch / (ms_launch * 1e-3) / 1e9 / peaks["hbm_gbs"],
+            "roofline": {"kernel": "k_tensor_tcf (FastDiag contraction, folded 3xTF32 tcgen05, fp32 accumulate "
+                                   "in TMEM)",
+                         "bound": "hbm" if t_hbm >= t_tc else "tensor",
+                         "achieved": hbm_gbs_c if t_hbm >= t_tc else tc_exec,
+                         "peak": peaks["hbm_gbs"] if t_hbm >= t_tc else tf32,
+                         "unit": "GB/s" if t_hbm >= t_tc else "TFLOP/s",
+                         "frac": hbm_gbs_c / peaks["hbm_gbs"] if t_hbm >= t_tc else tc_exec / tf32,
+                         "peak_source": peaks["src"] if t_hbm >= t_tc else peaks["src_tc"] + " / 2 (TF32)",
+                         "bytes_per_launch": bytes_launch, "flop_per_launch_algorithmic": flops,
+                         "ms_per_launch": ms_launch,
+                         "floors_us": {"hbm": t_hbm * 1e6, "tf32_executed": t_tc * 1e6},
+                         "tensor_view": {"executed_tf32_tflops": tc_exec, "tf32_dense_peak": tf32,
+                                         "frac": tc_exec / tf32,
+                                         "algorithmic_fp32_tflops": flops / (ms_launch * 1e-3) / 1e12},
                          "traffic": load_traffic(),
                          "traffic_note": "ncu --set full dram read+write of one launch (profiles/ncu_summary.json)"},
-            "roofline_hbm": {"kernel": "k_stencil (fp64 7-point)", "bound": "hbm", "achieved": gbs,
-                             "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": gbs / peaks["hbm_gbs"],
-                             "peak_source": peaks["src"], "bytes_per_launch": 16.0 * m, "ms_per_launch": ms_sten},
+            "roofline_hbm": {"kernel": "k_stencil_tma<LdPlain<float>, EpiResidual> (fp32 7-point residual + norm)",
+                             "bound": "hbm", "achieved": sten["gbs"], "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                             "frac": sten["frac"], "peak_source": peaks["src"], "bytes_per_launch": sten["bytes"],
+                             "ms_per_launch": sten["us"] * 1e-3},
             "clocks": clk,
-            "kernels": kernel_table(mp, N_GRID, peaks["hbm_gbs"]),
+            "kernels": ktab,
             "kernels_note": (f"each kernel alone on {N_GRID}^3 vectors, CUDA events, algorithmic bytes "
                              "(SURVEY.md §8d) / time vs MEASURED_PEAKS hbm_gbs"),
         }

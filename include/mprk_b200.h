@@ -260,6 +260,13 @@ int mprkb_integrate(const mprkb_config* cfg, const double* reference_host, size_
 int mprkb_stepper_integrate(mprkb_stepper* s, const double* reference_host, size_t reference_len,
                             double* state_host, mprkb_result* result);
 
+/* temporal_order(problem, cfg, taus) (stepper.cpp:271-310): every tau run
+ * against one tiny-tau reference (tau_min / 16, tol 1e-12, fp64 implicit);
+ * errors_* receive `count` values, slope the least-squares log-log slope of
+ * error_l2 on tau.  cfg->tau is ignored. */
+int mprkb_temporal_order(const mprkb_config* cfg, const double* taus, int count, double* errors_max,
+                         double* errors_l2, double* slope, int* solver_failure);
+
 /* ---- split grid: k-slab decomposition across ranks ----------
  * Rank r of P owns k-planes [r n/P, (r+1) n/P): the contiguous slice
  * [r n^3/P, (r+1) n^3/P) of the x-fastest state vector.  Stencils exchange

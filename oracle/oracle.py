@@ -177,6 +177,21 @@ class Reference:
                     steps=st.value, solver_failure=bool(sf.value), wall_seconds=ws.value)
 
 
+def _ref_temporal_order(self, eq, n, tab, taus, t_end, tol, precision, max_iter=40):
+    taus = np.ascontiguousarray(taus, np.float64)
+    em = np.zeros(taus.size); el = np.zeros(taus.size); slope = C.c_double(); sf = C.c_int()
+    self._chk(self.lib.ref_temporal_order(eq, n, tab["q"], _p(np.ascontiguousarray(tab["a_high"], np.float64)),
+                                          _p(np.ascontiguousarray(tab["a_eps"], np.float64)),
+                                          _p(np.ascontiguousarray(tab["b"], np.float64)), C.c_double(t_end),
+                                          C.c_double(tol), 0 if precision == "f32" else 1, max_iter, _p(taus),
+                                          taus.size, _p(em), _p(el), C.byref(slope), C.byref(sf)))
+    return dict(taus=taus.tolist(), errors_max=em.tolist(), errors_l2=el.tolist(), slope=slope.value,
+                solver_failure=bool(sf.value))
+
+
+Reference.temporal_order = _ref_temporal_order
+
+
 class RefStepper:
     def __init__(self, R: Reference, eq, n, tab, tau, tol, precision, max_iter, t_end):
         self.R = R

@@ -470,4 +470,27 @@ int ref_integrate(int eq, int n, int q, const double* a_high, const double* a_ep
   });
 }
 
+// temporal_order(): errors of each tau against a tiny-tau fp64 reference run,
+// and the least-squares log-log slope (stepper.cpp:271-310).
+int ref_temporal_order(int eq, int n, int q, const double* a_high, const double* a_eps, const double* b,
+                       double t_end, double tol, int precision, int max_iter, const double* taus, int count,
+                       double* errors_max, double* errors_l2, double* slope, int* solver_failure) {
+  return guarded([&] {
+    const ProblemSpec p = make_problem(eq_of(eq), n);
+    IntegrationConfig cfg;
+    cfg.tableau = tableau_from(q, a_high, a_eps, b);
+    cfg.t_end = t_end;
+    cfg.tol = tol;
+    cfg.policy.implicit = precision == 0 ? Precision::F32 : Precision::F64;
+    cfg.max_iter = max_iter;
+    const TemporalOrderResult r = temporal_order(p, cfg, std::vector<double>(taus, taus + count));
+    for (int i = 0; i < count; ++i) {
+      errors_max[i] = r.errors_max[i];
+      errors_l2[i] = r.errors_l2[i];
+    }
+    *slope = r.slope;
+    *solver_failure = r.solver_failure ? 1 : 0;
+  });
+}
+
 }  // extern "C"

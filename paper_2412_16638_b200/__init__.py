@@ -28,7 +28,8 @@ __all__ = [
     "WrongEquation", "NonFiniteState", "CudaError", "NoDevice",
     "Tableau", "builtin", "midpoint_corrected", "validate", "integrate", "make_problem", "heat_exact",
     "Stepper", "Operator", "stencil_apply", "tensor_apply", "dot", "cg", "gmres", "kernel_launches",
-    "device_count", "Comm", "LocalGroup", "slab_plan", "run_ranks", "set_device",
+    "device_count", "Comm", "LocalGroup", "slab_plan", "run_ranks", "set_device", "temporal_order",
+    "tableau_from_json", "tableau_to_json",
 ]
 
 
@@ -80,6 +81,49 @@ def midpoint_corrected(p: int) -> Tableau:
     if p < 0:
         raise MprkError("midpoint_corrected: corrector count must be nonnegative")
     return _tableau_from_lib(f"midpoint{int(p)}")
+
+
+def _derive_c(a_high, a_eps):
+    return [sum(a_high[i][j] + a_eps[i][j] for j in range(len(a_high[i]))) for i in range(len(a_high))]
+
+
+def tableau_to_json(t: Tableau) -> str:
+    """tableau_to_json (tableau.cpp:192-201): name, q, c, A_high, A_eps, b."""
+    import json
+
+    return json.dumps({"name": t.name, "q": t.q, "c": list(t.c), "A_high": [list(r) for r in t.a_high],
+                       "A_eps": [list(r) for r in t.a_eps], "b": list(t.b)}, indent=2)
+
+
+def tableau_from_json(text: str) -> Tableau:
+    """tableau_from_json (tableau.cpp:203-233): a user tableau for the stepper;
+    "c" is optional (row sums of A_high + A_eps).  Errors are MprkError with
+    the reference's messages."""
+    import json
+
+    try:
+        j = json.loads(text)
+    except ValueError as e:
+        raise MprkError(f"tableau JSON does not parse: {e}") from None
+    try:
+        name, q = str(j["name"]), j["q"]
+        if not isinstance(q, int) or isinstance(q, bool):
+            raise TypeError("q must be an integer")
+        ah = [[float(v) for v in r] for r in j["A_high"]]
+        ae = [[float(v) for v in r] for r in j["A_eps"]]
+        b = [float(v) for v in j["b"]]
+        c = [float(v) for v in j["c"]] if "c" in j else _derive_c(ah, ae)
+    except (KeyError, TypeError, ValueError) as e:
+        raise MprkError(f"tableau JSON has a wrong field: {e}") from None
+    if q <= 0 or len(b) != q or len(ah) != q or len(ae) != q:
+        raise MprkError("tableau JSON dimensions are inconsistent with q")
+    if any(len(r) != q for r in ah):
+        raise MprkError("A_high rows must have length q")
+    if any(len(r) != q for r in ae):
+        raise MprkError("A_eps rows must have length q")
+    if len(c) != q:
+        raise MprkError("c must have length q")
+    return Tableau(name, q, c, ah, ae, b)
 
 
 def validate(t: Tableau) -> list:
@@ -401,6 +445,26 @@ def integrate(tableau: Tableau, equation: str, n: int, tau: float, t_end: float,
     out = st.integrate(reference)
     out["timings"] = st.timings()
     return out
+
+
+def temporal_order(tableau: Tableau, equation: str, n: int, taus, t_end: float = 0.1, tol: float = 1e-6,
+                   precision: str = "f64", max_iter: int = 40, *, numerics: str = "fast",
+                   preconditioner: str = "fastdiag", nu: float = 0.0) -> dict:
+    """temporal_order(problem, cfg, taus) (stepper.cpp:271-310) on the GPU:
+    errors of each tau against one tiny-tau fp64 run and the least-squares
+    log-log slope.  Returns dict(taus, errors_max, errors_l2, slope,
+    solver_failure)."""
+    taus = np.ascontiguousarray(list(taus), dtype=np.float64)
+    if taus.size == 0:
+        raise MprkError("temporal_order: tau list must not be empty")
+    cfg, keep = _config(tableau, equation, n, float(taus[0]), t_end, tol, precision, max_iter, numerics,
+                        preconditioner, 8, None, nu, False)
+    em = np.zeros(taus.size); el = np.zeros(taus.size); slope = C.c_double(); sf = C.c_int()
+    check(_c.lib.mprkb_temporal_order(C.byref(cfg), taus.ctypes.data_as(C.POINTER(C.c_double)), taus.size,
+                                      em.ctypes.data_as(C.POINTER(C.c_double)),
+                                      el.ctypes.data_as(C.POINTER(C.c_double)), C.byref(slope), C.byref(sf)))
+    return dict(taus=taus.tolist(), errors_max=em.tolist(), errors_l2=el.tolist(), slope=slope.value,
+                solver_failure=bool(sf.value))
 
 
 # ---- device-level entry points (torch CUDA tensors) ---------------------------------

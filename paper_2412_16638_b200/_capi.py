@@ -168,6 +168,7 @@ SIGNATURES = {
     "mprkb_stepper_destroy": (None, [vp]),
     "mprkb_integrate": (i32, [C.POINTER(Config), vp, sz, vp, C.POINTER(Result)]),
     "mprkb_stepper_integrate": (i32, [vp, vp, sz, vp, C.POINTER(Result)]),
+    "mprkb_temporal_order": (i32, [C.POINTER(Config), dptr, i32, dptr, dptr, dptr, ip]),
     # split grid (k-slab decomposition)
     "mprkb_set_device": (i32, [i32]),
     "mprkb_slab_plan": (i32, [i32, i32, i32, ip, ip, ip, ip]),

@@ -645,6 +645,21 @@ int mprkb_integrate(const mprkb_config* cfg, const double* reference_host, size_
   });
 }
 
+int mprkb_temporal_order(const mprkb_config* cfg, const double* taus, int count, double* errors_max,
+                         double* errors_l2, double* slope, int* solver_failure) {
+  return guarded([&] {
+    if (!taus || count <= 0) MPRKB_THROW(MPRKB_ERROR, "temporal_order: tau list must not be empty");
+    const StepperConfig c = config_of(cfg);
+    const TemporalOrderResult r = temporal_order(c, std::vector<double>(taus, taus + count));
+    for (int i = 0; i < count; ++i) {
+      errors_max[i] = r.errors_max[i];
+      errors_l2[i] = r.errors_l2[i];
+    }
+    *slope = r.slope;
+    *solver_failure = r.solver_failure ? 1 : 0;
+  });
+}
+
 int mprkb_stepper_integrate(mprkb_stepper* s, const double* reference_host, size_t reference_len,
                             double* state_host, mprkb_result* result) {
   return guarded([&] {

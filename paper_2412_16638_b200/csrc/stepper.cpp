@@ -339,4 +339,40 @@ IntegrationResult integrate_with(Stepper& stepper, const std::vector<double>* re
   return res;
 }
 
+TemporalOrderResult temporal_order(StepperConfig cfg, std::vector<double> taus) {
+  if (taus.empty()) MPRKB_THROW(1, "temporal_order: tau list must not be empty");
+  double tau_min = taus.front();
+  for (const double t : taus) tau_min = std::min(tau_min, t);
+  StepperConfig ref_cfg = cfg;
+  ref_cfg.tau = tau_min / 16.0;
+  ref_cfg.tol = 1e-12;
+  ref_cfg.f32 = false;
+  const IntegrationResult ref = integrate(ref_cfg, nullptr);
+
+  TemporalOrderResult out;
+  out.solver_failure = ref.solver_failure;
+  out.taus = std::move(taus);
+  for (const double tau : out.taus) {
+    cfg.tau = tau;
+    const IntegrationResult r = integrate(cfg, &ref.state);
+    out.errors_max.push_back(*r.error_max);
+    out.errors_l2.push_back(*r.error_l2);
+    out.solver_failure = out.solver_failure || r.solver_failure;
+  }
+  // least-squares slope of log(error_l2) on log(tau), the reference's sums
+  const size_t m = out.taus.size();
+  double sx = 0, sy = 0, sxx = 0, sxy = 0;
+  for (size_t i = 0; i < m; ++i) {
+    const double x = std::log(out.taus[i]);
+    const double y = std::log(out.errors_l2[i]);
+    sx += x;
+    sy += y;
+    sxx += x * x;
+    sxy += x * y;
+  }
+  const double denom = m * sxx - sx * sx;
+  out.slope = denom != 0.0 ? (m * sxy - sx * sy) / denom : 0.0;
+  return out;
+}
+
 }  // namespace mprkb

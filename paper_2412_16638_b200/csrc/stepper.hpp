@@ -89,6 +89,16 @@ struct IntegrationResult {
 };
 
 IntegrationResult integrate(const StepperConfig& cfg, const std::vector<double>* reference);
+
+// temporal_order (stepper.cpp:271-310): each tau's errors against one
+// tiny-tau run (tau_min / 16, tol 1e-12, fp64 implicit stages) and the
+// least-squares slope of log(error_l2) against log(tau).
+struct TemporalOrderResult {
+  std::vector<double> taus, errors_max, errors_l2;
+  double slope = 0.0;
+  bool solver_failure = false;
+};
+TemporalOrderResult temporal_order(StepperConfig cfg, std::vector<double> taus);
 // integrate on an existing stepper (its timing registry then holds the run's labels)
 IntegrationResult integrate_with(Stepper& stepper, const std::vector<double>* reference,
                                  std::chrono::steady_clock::time_point wall_start);
