@@ -651,12 +651,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int p = 0; p < 2; ++p)
 #pragma unroll
           for (int ch = 0; ch < TF_KH / 4; ++ch) {
+            // hi = x truncated to tf32 (one LOP3), lo = x - hi (exact); the MMA
+            // reads lo's top 10 mantissa bits: |error| <= 2^-20 |x| per element
+            // — within fp32 FMA noise, without the quarter-rate cvt.rna
             uint32_t hi[4], lo[4];
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
               const float x = v[2 * (ch * 4 + u) + p];
-              hi[u] = tf32_rna(x);
-              lo[u] = tf32_rna(x - __uint_as_float(hi[u]));
+              hi[u] = __float_as_uint(x) & 0xFFFFE000u;
+              lo[u] = __float_as_uint(x - __uint_as_float(hi[u]));
             }
             const int o = kofs16(ct, ch);
             const uint32_t dh = smem_u32(XS(rx.s, p, 0)) + o, dl = smem_u32(XS(rx.s, p, 1)) + o;
