@@ -74,6 +74,95 @@ __global__ void __launch_bounds__(256) k_block_jacobi(int n, long lines, int b, 
   }
 }
 
+// One thread per block (n % B == 0, real T): the block's inverse (B columns
+// of B contiguous entries) and its r segment are read with 16-byte vector
+// loads, outputs accumulate over jj in the same ascending order as the
+// per-element kernel (bitwise identical), B outputs stored contiguously.
+template <class S, int CNT>
+__device__ __forceinline__ void ld_col(const S* p, float (&o)[CNT]) {
+  if constexpr (std::is_same_v<S, __half>) {
+    static_assert(CNT % 8 == 0 || CNT == 4, "fp16 columns load in 8- or 4-wide chunks");
+    if constexpr (CNT == 4) {
+      const uint2 w = __ldg(reinterpret_cast<const uint2*>(p));
+      const __half2 a = *reinterpret_cast<const __half2*>(&w.x), b = *reinterpret_cast<const __half2*>(&w.y);
+      o[0] = __low2float(a); o[1] = __high2float(a); o[2] = __low2float(b); o[3] = __high2float(b);
+    } else {
+#pragma unroll
+      for (int c = 0; c < CNT / 8; ++c) {
+        const uint4 w = __ldg(reinterpret_cast<const uint4*>(p) + c);
+        const __half2* h = reinterpret_cast<const __half2*>(&w);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          o[8 * c + 2 * u] = __low2float(h[u]);
+          o[8 * c + 2 * u + 1] = __high2float(h[u]);
+        }
+      }
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < CNT / 4; ++c) {
+      const float4 w = __ldg(reinterpret_cast<const float4*>(p) + c);
+      o[4 * c] = w.x; o[4 * c + 1] = w.y; o[4 * c + 2] = w.z; o[4 * c + 3] = w.w;
+    }
+  }
+}
+
+template <class T, class S, int B>
+__global__ void __launch_bounds__(128) k_block_jacobi_row(long blocks, const S* __restrict__ inv,
+                                                          const T* __restrict__ r, T* __restrict__ z) {
+  using R = real_t<T>;
+  for (long blk = blockIdx.x * (long)blockDim.x + threadIdx.x; blk < blocks; blk += (long)gridDim.x * blockDim.x) {
+    const S* D = inv + blk * (long)B * B;
+    const T* rb = r + blk * B;
+    R rv[B];
+#pragma unroll
+    for (int c = 0; c < B / 4; ++c) {
+      const V4<T> w = ld4(rb + 4 * c);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) rv[4 * c + u] = w.x[u];
+    }
+    R acc[B];
+#pragma unroll
+    for (int ii = 0; ii < B; ++ii) acc[ii] = R(0);
+#pragma unroll
+    for (int jj = 0; jj < B; ++jj) {
+      if constexpr (std::is_same_v<S, double>) {
+#pragma unroll
+        for (int ii = 0; ii < B; ++ii) acc[ii] = xadd(acc[ii], rmul((R)__ldg(D + jj * B + ii), rv[jj]));
+      } else {
+        float col[B];
+        ld_col<S, B>(D + jj * B, col);
+#pragma unroll
+        for (int ii = 0; ii < B; ++ii) acc[ii] = xadd(acc[ii], rmul((R)col[ii], rv[jj]));
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < B / 4; ++c) {
+      V4<T> w;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) w.x[u] = acc[4 * c + u];
+      st4(z + blk * B + 4 * c, w);
+    }
+  }
+}
+
+template <class T, class S>
+bool bj_row(int n, long lines, int b, const S* inv, const T* r, T* z, cudaStream_t st) {
+  if constexpr (is_cplx<T>) {
+    return false;
+  } else {
+    if (n % b) return false;
+    const long blocks = lines * (n / b);
+    const unsigned g = grid_for((size_t)blocks, 128, 16);
+    switch (b) {
+      case 4: k_block_jacobi_row<T, S, 4><<<g, 128, 0, st>>>(blocks, inv, r, z); return true;
+      case 8: k_block_jacobi_row<T, S, 8><<<g, 128, 0, st>>>(blocks, inv, r, z); return true;
+      case 16: k_block_jacobi_row<T, S, 16><<<g, 128, 0, st>>>(blocks, inv, r, z); return true;
+      default: return false;
+    }
+  }
+}
+
 template <class S>
 __global__ void k_bj_fill(long nblocks_per_line, long lines, int n, int b, const double* __restrict__ full,
                           const double* __restrict__ tail, S* __restrict__ inv) {
@@ -96,6 +185,16 @@ void block_jacobi_apply(int n, int b, int storage, const void* inv, const T* r, 
   if (lines <= 0) lines = (long)n * n;
   const size_t m = (size_t)n * lines;
   const unsigned g = grid_for(m, 256, 8);
+  bool done = false;
+  switch (storage) {
+    case 4: done = bj_row<T, __half>(n, lines, b, (const __half*)inv, r, z, st); break;
+    case 0: done = bj_row<T, float>(n, lines, b, (const float*)inv, r, z, st); break;
+    default: done = bj_row<T, double>(n, lines, b, (const double*)inv, r, z, st); break;
+  }
+  if (done) {
+    LAUNCHED("block_jacobi");
+    return;
+  }
   switch (storage) {
     case 4: k_block_jacobi<T, __half><<<g, 256, 0, st>>>(n, lines, b, (const __half*)inv, r, z); break;
     case 0: k_block_jacobi<T, float><<<g, 256, 0, st>>>(n, lines, b, (const float*)inv, r, z); break;
