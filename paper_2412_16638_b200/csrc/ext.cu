@@ -128,7 +128,11 @@ __global__ void __launch_bounds__(128) k_block_jacobi_row(long blocks, const S* 
     for (int jj = 0; jj < B; ++jj) {
       if constexpr (std::is_same_v<S, double>) {
 #pragma unroll
-        for (int ii = 0; ii < B; ++ii) acc[ii] = xadd(acc[ii], rmul((R)__ldg(D + jj * B + ii), rv[jj]));
+        for (int c = 0; c < B / 2; ++c) {
+          const double2 w = __ldg(reinterpret_cast<const double2*>(D + jj * B) + c);
+          acc[2 * c] = xadd(acc[2 * c], rmul((R)w.x, rv[jj]));
+          acc[2 * c + 1] = xadd(acc[2 * c + 1], rmul((R)w.y, rv[jj]));
+        }
       } else {
         float col[B];
         ld_col<S, B>(D + jj * B, col);
@@ -158,6 +162,12 @@ bool bj_row(int n, long lines, int b, const S* inv, const T* r, T* z, cudaStream
       case 4: k_block_jacobi_row<T, S, 4><<<g, 128, 0, st>>>(blocks, inv, r, z); return true;
       case 8: k_block_jacobi_row<T, S, 8><<<g, 128, 0, st>>>(blocks, inv, r, z); return true;
       case 16: k_block_jacobi_row<T, S, 16><<<g, 128, 0, st>>>(blocks, inv, r, z); return true;
+      case 32:
+        if constexpr (sizeof(T) == 4) {  // (fp64 accumulators would not fit the register budget)
+          k_block_jacobi_row<T, S, 32><<<g, 128, 0, st>>>(blocks, inv, r, z);
+          return true;
+        }
+        return false;
       default: return false;
     }
   }
