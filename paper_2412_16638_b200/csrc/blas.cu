@@ -463,7 +463,22 @@ void extract_stage(size_t m, int src_kind, const void* x, double* y, int* flag, 
 }
 
 // u += (tau b_i) f_i ...; check_finite(u)   (stepper.cpp:200-205)
-__global__ void __launch_bounds__(kBlock) k_final(size_t m, double* u, CombineTerms t, int* flag) {
+// gate (nullable, host-mapped): the step's earlier error checks; when any is
+// raised the reference leaves u untouched, so the update is skipped (the host
+// then throws the first one) — no synchronize needed between the stages and
+// the update.
+__global__ void __launch_bounds__(kBlock) k_final(size_t m, double* u, CombineTerms t, int* flag, const int* gate,
+                                                  int gate_count) {
+  if (gate_count) {  // one thread per CTA reads the flags (device memory)
+    __shared__ int skip;
+    if (threadIdx.x == 0) {
+      int any = 0;
+      for (int g = 0; g < gate_count; ++g) any |= gate[g];
+      skip = any;
+    }
+    __syncthreads();
+    if (skip) return;
+  }
   bool bad = false;
   for_each4(
       m,
@@ -487,8 +502,9 @@ __global__ void __launch_bounds__(kBlock) k_final(size_t m, double* u, CombineTe
   if (bad) *flag = 1;
 }
 
-void final_update(size_t m, double* u, const CombineTerms& t, int* flag, cudaStream_t st) {
-  k_final<<<wave(m), kBlock, 0, st>>>(m, u, t, flag);
+void final_update(size_t m, double* u, const CombineTerms& t, int* flag, cudaStream_t st, const int* gate,
+                  int gate_count) {
+  k_final<<<wave(m), kBlock, 0, st>>>(m, u, t, flag, gate, gate ? gate_count : 0);
   LAUNCHED("final_update");
 }
 

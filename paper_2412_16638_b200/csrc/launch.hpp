@@ -162,7 +162,10 @@ void combine(size_t m, const double* u, const CombineTerms& t, int out_kind, voi
 // y = widen(x) / real_part(x) of the solver output, + non-finite flag.
 void extract_stage(size_t m, int src_kind, const void* x, double* y, int* flag, cudaStream_t st);
 // u += sum_t coef_t * v_t, + non-finite flag on u.
-void final_update(size_t m, double* u, const CombineTerms& t, int* flag, cudaStream_t st);
+// gate: gate_count error flags of the step so far (DEVICE memory); if any is
+// set the update is skipped (u untouched, as the reference's throw leaves it).
+void final_update(size_t m, double* u, const CombineTerms& t, int* flag, cudaStream_t st,
+                  const int* gate = nullptr, int gate_count = 0);
 // element casts for the op-level API: narrow (overflow flag) / widen / promote
 void narrow_f64(size_t m, const double* x, float* y, int* flag, cudaStream_t st);
 

@@ -104,6 +104,7 @@ Stepper::Stepper(const StepperConfig& cfg)
     if (need_feps_[i] && (cfg_.f32 || !need_f64_[i])) f_eps_[i].alloc(m * (cfg_.f32 ? sizeof(float) : sizeof(double)));
   }
   y_.alloc(m * sizeof(double));
+  gate_dev_.alloc(sizeof(int) * 256);
   if (!solvers_.empty()) {
     const size_t s = dtype_size(solve_dtype_);
     bsol_.alloc(m * s);
@@ -253,14 +254,28 @@ void Stepper::step(double* u, StepTrace& trace) {
       }
     }
   }
-  raise_flags();
+  // The stage checks gate the final update on the device (a raised one skips
+  // it, leaving u untouched as the reference's throw does) so the step needs
+  // no synchronize here; on a split grid every rank must see every rank's
+  // checks first, which takes the collective.
+  const int stage_checks = next - 1;
+  if (slab_.split()) raise_flags();
 
   CombineTerms fin;
   for (int i = 0; i < q; ++i)
     if (t.b[i] != 0.0) add_term(fin, tau * t.b[i], fh[i], 0);
   {
     Bracket br(timer_, "axpy", st_);
-    final_update(m, u, fin, check_slot(9, "updated state picked up a NaN or infinity"), st_);
+    int* fin_flag = check_slot(9, "updated state picked up a NaN or infinity");
+    const int* gate = nullptr;
+    if (!slab_.split() && stage_checks > 0) {
+      // stream-ordered copy of the (host-mapped) check flags to device memory:
+      // the update's CTAs read it from L2, not across PCIe
+      CUDA_CHECK(cudaMemcpyAsync(gate_dev_.get(), flags_.dev(1), sizeof(int) * stage_checks, cudaMemcpyHostToDevice,
+                                 st_));
+      gate = gate_dev_.as<int>();
+    }
+    final_update(m, u, fin, fin_flag, st_, gate, stage_checks);
   }
   raise_flags();
   if (timer_.enabled()) timer_.resolve();

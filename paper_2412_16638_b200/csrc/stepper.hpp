@@ -69,6 +69,7 @@ class Stepper {
   std::vector<char> need_f64_, need_feps_;
   std::vector<DevBuf> f_hi_, f_eps_;
   DevBuf y_, bsol_, xsol_;
+  DevBuf gate_dev_;  // device copy of the stage checks gating the final update
   std::unique_ptr<KrylovWork<float>> w32_;
   std::unique_ptr<KrylovWork<double>> w64_;
   std::unique_ptr<KrylovWork<c32>> wc32_;
