@@ -389,7 +389,9 @@ struct TfSmem {
   alignas(1024) unsigned char raw[Cfg::RS][Cfg::RAWB];
   alignas(1024) unsigned char q[Cfg::QS][4 * TF_Q];
   alignas(1024) unsigned char x[Cfg::CS][4 * TF_X];
-  alignas(16) float stagec[4][32 * 32];  // epilogue transpose, one 32x32 block per epilogue warp
+  // epilogue: per epilogue warp one 32x32 fp32 staging block (128B-swizzled
+  // rows), drained by a TMA tensor store
+  alignas(1024) float stagec[4][1][32 * 32];
   alignas(8) uint64_t rawfull[Cfg::RS];
   alignas(8) uint64_t rawfree[Cfg::RS];
   alignas(8) uint64_t qfull[Cfg::QS];
@@ -454,8 +456,8 @@ struct Ring {
 template <int SIDE, bool PDIN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_tensor_tcf(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap pmap,
-                 float* __restrict__ C, const float* __restrict__ qpack, int n, int col_tiles, int num_tiles,
-                 long ldc, int dbg) {
+                 const __grid_constant__ CUtensorMap omap, float* __restrict__ C, const float* __restrict__ qpack,
+                 int n, int col_tiles, int num_tiles, long ldc, int dbg) {
   using Cfg = TfCfg<PDIN>;
   constexpr int RS = Cfg::RS, QS = Cfg::QS, CS = Cfg::CS;
   extern __shared__ unsigned char smem_raw[];
@@ -486,6 +488,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   };
   const CUtensorMap* xm = &xmap;
   const CUtensorMap* pm = &pmap;
+  const CUtensorMap* om = &omap;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&S.tmem_base)),
@@ -679,36 +682,44 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       }
     }
   } else if (warp < TC_EPI_WARP0 + 4) {
+    // TMEM -> E +- O -> swizzled smem block -> TMA tensor store.  Each 32x32
+    // block of the output (rows a, and the mirrored rows n-1-a written with
+    // the row order reversed so the block is ascending) goes out as one bulk
+    // store, asynchronous to the warp.
     const int q4 = warp - TC_EPI_WARP0;
-    const uint32_t sb = smem_u32(S.stagec[q4]);
-    const int rr = lane >> 3, c4 = lane & 7;  // transposed read-back: 4 rows x 8 chunks
     int it = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
       const Tile T = tile_of(t);
       const int acc = it & 1;
       mbar_wait(&S.tmem_full[acc], (uint32_t)(it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const long a = T.a0 + 32 * q4 + lane;  // folded row; its mirror is n-1-a
-      const long am = n - 1 - a;
+      const int arow = T.a0 + 32 * q4;  // first folded row of this warp's lane quarter
       const uint32_t lanebase = tmem + ((uint32_t)(32 * q4) << 16) + (uint32_t)(acc * 256);
       for (int cc = 0; cc < TF_BN && !(dbg & 4); cc += 32) {
         uint32_t e[32], o[32];
         tmem_ld32(lanebase + (uint32_t)cc, e);
         tmem_ld32(lanebase + 128u + (uint32_t)cc, o);
-        if (SIDE == 2) {
-          // D[a][fibre] = C[fibre][a]: for fixed j the warp writes 32 consecutive a
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const long f = (T.col0 + cc + j) * nn;
-            C[f + a] = __uint_as_float(e[j]) + __uint_as_float(o[j]);
-            C[f + am] = __uint_as_float(e[j]) - __uint_as_float(o[j]);
-          }
-        } else {
-          // rows a (E+O) and n-1-a (E-O) are row-major outputs: transpose each
-          // 32x32 block through smem (16-byte chunks XOR-swizzled by row) so
-          // every store instruction covers 4 full 128-byte rows
+        for (int half = 0; half < 2; ++half) {
+          const uint32_t sb = smem_u32(S.stagec[q4][0]);
+          // the previous block's store must have read the staging buffer
+          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          __syncwarp();
+          if (SIDE == 2) {
+            // block [32 fibres][32 a]: row j = fibre, column = a (lane; reversed for n-1-a)
+            const int col = half ? 31 - lane : lane;
 #pragma unroll
-          for (int half = 0; half < 2; ++half) {
+            for (int j = 0; j < 32; ++j) {
+              const float v = half ? __uint_as_float(e[j]) - __uint_as_float(o[j])
+                                   : __uint_as_float(e[j]) + __uint_as_float(o[j]);
+              asm volatile("st.shared.f32 [%0], %1;" ::"r"(sb + (uint32_t)(j * 128 + (((col >> 2) ^ (j & 7)) << 4) +
+                                                                           (col & 3) * 4)),
+                           "f"(v)
+                           : "memory");
+            }
+          } else {
+            // block [32 rows][32 columns]: row = lane (reversed for n-1-a)
+            const int row = half ? 31 - lane : lane;
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
               float4 w;
@@ -718,24 +729,33 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const float ev = __uint_as_float(e[4 * c + u]), ov = __uint_as_float(o[4 * c + u]);
                 pw[u] = half ? ev - ov : ev + ov;
               }
-              sts128(sb + (uint32_t)(lane * 128 + ((c ^ (lane & 7)) << 4)), w);
+              sts128(sb + (uint32_t)(row * 128 + ((c ^ (row & 7)) << 4)), w);
             }
-            __syncwarp();
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const int r = 4 * i + rr;  // local row = TMEM lane of the writer
-              const float4 w = lds128(sb + (uint32_t)(r * 128 + ((c4 ^ (r & 7)) << 4)));
-              const long row = half ? n - 1 - (T.a0 + 32 * q4 + r) : T.a0 + 32 * q4 + r;
-              const long off = (SIDE == 1 ? (long)T.plane * n2 + row * nn : row * ldc) + T.col0 + cc + 4 * c4;
-              *reinterpret_cast<float4*>(C + off) = w;
-            }
-            __syncwarp();
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            const int r0 = half ? n - 32 - arow : arow;  // first output row (a) of the block
+            if (SIDE == 2)
+              asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(om),
+                           "r"(r0), "r"((int)(T.col0 + cc)), "r"(sb)
+                           : "memory");
+            else if (SIDE == 1)
+              asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(om),
+                           "r"((int)(T.col0 + cc)), "r"(r0), "r"(T.plane), "r"(sb)
+                           : "memory");
+            else
+              asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(om),
+                           "r"((int)(T.col0 + cc)), "r"(r0), "r"(sb)
+                           : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
           }
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(&S.tmem_empty[acc]);
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores done before exit
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -781,10 +801,26 @@ void launch_tcf(int n, long cols, const float* x, float* out, const float* pd, c
     pmap = PDIN ? mk(pd, 2, dims, strides, box) : map;
     col_tiles = (int)(cc / TF_BN);
   }
+  // output tensor map: 32x32 fp32 boxes, 128-byte swizzle (the staging layout)
+  CUtensorMap omap;
+  {
+    const cuuint32_t ob2[2] = {32, 32};
+    const cuuint32_t ob3[3] = {32, 32, 1};
+    if (SIDE == 2) {  // C[fibre][a]
+      const cuuint64_t dims[2] = {nn, cc}, strides[1] = {nn * 4};
+      omap = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, out, 2, dims, strides, ob2, CU_TENSOR_MAP_SWIZZLE_128B);
+    } else if (SIDE == 1) {  // C[plane][a][i]
+      const cuuint64_t dims[3] = {nn, nn, cc / nn}, strides[2] = {nn * 4, n2 * 4};
+      omap = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, out, 3, dims, strides, ob3, CU_TENSOR_MAP_SWIZZLE_128B);
+    } else {  // C[a][col]
+      const cuuint64_t dims[2] = {cc, nn}, strides[1] = {cc * 4};
+      omap = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, out, 2, dims, strides, ob2, CU_TENSOR_MAP_SWIZZLE_128B);
+    }
+  }
   const int num_tiles = (n / 2 / TF_BM) * col_tiles * planes;
   const int grid = num_tiles < sm_count() ? num_tiles : sm_count();
-  k_tensor_tcf<SIDE, PDIN><<<grid, TC_THREADS, smem, st>>>(map, pmap, out, qpack, n, col_tiles, num_tiles, cols,
-                                                           dbg);
+  k_tensor_tcf<SIDE, PDIN><<<grid, TC_THREADS, smem, st>>>(map, pmap, omap, out, qpack, n, col_tiles, num_tiles,
+                                                           cols, dbg);
   LAUNCHED("tensor_tc_fold");
 }
 
