@@ -378,9 +378,9 @@ constexpr int TF_Q = TF_BM * TF_KH * 4;             // 8 KB per {even, odd} x {h
 template <bool PDIN>
 struct TfCfg {
   static constexpr int RAWB = TF_RAW * (PDIN ? 2 : 1);
-  static constexpr int RS = PDIN ? 2 : 3;  // raw ring
+  static constexpr int RS = PDIN ? 2 : 5;  // raw ring
   static constexpr int QS = 2;             // Q ring
-  static constexpr int CS = PDIN ? 2 : 3;  // converted ring
+  static constexpr int CS = 2;             // converted ring
 };
 
 template <bool PDIN>
