@@ -58,21 +58,22 @@ PREC = "f32"
 MAX_ITER = 40
 
 
-def grid_for_world(n_gpus: int) -> int:
-    return N_GRID if n_gpus == 1 else N_SPLIT
+def grid_for_world(n_gpus: int, split: bool = False) -> int:
+    return N_SPLIT if (n_gpus > 1 or split) else N_GRID
 
 
-def workload_config(n_gpus: int) -> dict:
-    n = grid_for_world(n_gpus)
+def workload_config(n_gpus: int, split: bool = False) -> dict:
+    n = grid_for_world(n_gpus, split)
+    split = split or n_gpus > 1
     return {
         "workload": f"heat {n}^3, {METHOD} (4-stage mixed DIRK: fp32 implicit CG + FastDiag, "
                     f"fp64 explicit couplings/state), tau={TAU}, tol={TOL}"
-                    + ("" if n_gpus == 1 else f", k-slab decomposed over {n_gpus} GPUs (NCCL)"),
+                    + (f", k-slab decomposed over {n_gpus} GPU(s) (NCCL)" if split else ""),
         "n": n, "dof": n ** 3, "dof_per_gpu": n ** 3 // n_gpus, "method": METHOD, "implicit_precision": PREC,
         "preconditioner": "fastdiag", "tau": TAU, "tol": TOL, "max_iter": MAX_ITER,
         "state": "resident in HBM (f64)",
         "l2": "no flush: one step streams >= 3.5 GB per GPU through HBM (state slab alone 134 MB > 126 MB L2)",
-        "parallelism": "single" if n_gpus == 1 else f"slab{n_gpus} (k-planes; halo + all-to-all + dot allreduce)",
+        "parallelism": (f"slab{n_gpus} (k-planes; halo + all-to-all + dot allreduce)" if split else "single"),
     }
 
 
@@ -257,16 +258,23 @@ def run_cuda_arm(args):
         torch.cuda.set_device(0)
     import paper_2412_16638_b200 as mp
 
-    n = grid_for_world(world)
+    split = world > 1 or args.split
+    n = N_SPLIT if split else N_GRID
     m = n ** 3  # DOF of the whole (possibly split) grid
     tab = mp.builtin(METHOD)
     comm = None
-    if world > 1:
-        # libmprk_b200's own NCCL communicator; torch.distributed only ships the id
+    if split:
+        # libmprk_b200's own NCCL communicator; torch.distributed only ships the
+        # id (--split at one GPU: a 1-rank communicator, every exchange path
+        # against itself — the N > 1 code path on a single-GPU box)
         mp.set_device(local)
-        obj = [mp.Comm.nccl_unique_id() if rank == 0 else None]
-        torch.distributed.broadcast_object_list(obj, src=0)
-        comm = mp.Comm.nccl(rank, world, obj[0])
+        if world > 1:
+            obj = [mp.Comm.nccl_unique_id() if rank == 0 else None]
+            torch.distributed.broadcast_object_list(obj, src=0)
+            uid = obj[0]
+        else:
+            uid = mp.Comm.nccl_unique_id()
+        comm = mp.Comm.nccl(rank, world, uid)
     st = mp.Stepper("heat", n, tab, TAU, TOL, PREC, MAX_ITER, comm=comm)
     stream = torch.cuda.ExternalStream(st.stream)
     u = torch.from_numpy(st.initial_state()).cuda()  # this rank's slab
@@ -331,15 +339,16 @@ def run_cuda_arm(args):
         # Executed: the sine fold halves the MACs and 3xTF32 triples them ->
         # 3 n^4 TF32 flop.  Floors: HBM 8N / peak vs TF32 3n^4 / (bf16 dense / 2);
         # the larger one is the bound reported.
-        ms_launch = measure_contraction(mp, torch, st.stream)
+        ms_launch = measure_contraction(mp, torch, st.stream)  # (on a 256^3 grid)
         peaks = load_peaks()
-        flops = 2.0 * n ** 4
-        bytes_launch = (8.0 * m * 6 + 4.0 * m) / 6.0
+        nk, mk = N_GRID, N_GRID ** 3
+        flops = 2.0 * nk ** 4
+        bytes_launch = (8.0 * mk * 6 + 4.0 * mk) / 6.0
         tf32 = peaks["bf16_tflops"] / 2.0
         t_hbm = bytes_launch / (peaks["hbm_gbs"] * 1e9)
-        t_tc = 3.0 * n ** 4 / (tf32 * 1e12)
+        t_tc = 3.0 * nk ** 4 / (tf32 * 1e12)
         hbm_gbs_c = bytes_launch / (ms_launch * 1e-3) / 1e9
-        tc_exec = 3.0 * n ** 4 / (ms_launch * 1e-3) / 1e12
+        tc_exec = 3.0 * nk ** 4 / (ms_launch * 1e-3) / 1e12
         # ---- HBM-bound companion: the step's most frequent stencil, the fused
         # fp32 residual r = b - A x with ||r||^2 (TMA plane pipeline), 12 N bytes
         ktab = kernel_table(mp, N_GRID, peaks["hbm_gbs"])
@@ -347,9 +356,10 @@ def run_cuda_arm(args):
         line = {
             "metric": METRIC, "value": value, "unit": "DOF-updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "steps_per_s": 1e3 / ms_step,
-            "higher_is_better": True, "scaling": "weak" if world == 1 else "strong", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if split else "weak", "vs_baseline": None,
             "dtype": "f32/f64",
-            "data": "synthetic (make_problem: u0 = 0, g = sin sin sin)", "config": workload_config(world),
+            "data": "synthetic (make_problem: u0 = 0, g = sin sin sin)",
+            "config": workload_config(world, split),
             "iterations_per_solve": sorted(set(i for it in iters for i in it)),
             "gpu_launches": launches,
             "e2e": {"value": e2e_value, "unit": "DOF-updates/s", "h2d_bytes_per_step": 8 * m_local * world,
@@ -380,7 +390,7 @@ def run_cuda_arm(args):
             "kernels_note": (f"each kernel alone on {N_GRID}^3 vectors, CUDA events, algorithmic bytes "
                              "(SURVEY.md §8d) / time vs MEASURED_PEAKS hbm_gbs"),
         }
-        if not args.no_cpu_baseline and world == 1:
+        if not args.no_cpu_baseline and world == 1 and not split:
             budget = float(os.environ.get("MPRKB_CPU_BASELINE_S", "30"))
             threads = os.cpu_count() or 1
             times = reference_steps(N_GRID, 1, budget, threads)
@@ -464,6 +474,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--split", action="store_true",
+                    help="configs[2] path (512^3 through the NCCL split stepper) even on one GPU")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference_arm(args)
