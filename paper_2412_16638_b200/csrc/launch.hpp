@@ -49,6 +49,30 @@ void apply_f64(const StencilSpec& k, const double* y, const float* y32, const do
 void apply_f32(const StencilSpec& k, const double* y, const float* y32, const float* g32, float* out32,
                int* flag, int* finite_flag, cudaStream_t st);
 
+// Stage i's f evaluations fused with stage i+1's right-hand side (F32 policy,
+// fp32 stage vector y32, Dirichlet stencil on the TMA path): see
+// EpiFevalCombine in stencil.cu.  All pointers are device vectors of the local
+// grid; `sin` / `ain[a]` may alias `aout[a]` (read-modify-write in place).
+struct FevalCombine {
+  const double* g = nullptr;
+  const float* g32 = nullptr;
+  double* fhi = nullptr;
+  int* finite_flag = nullptr;
+  const double* sin = nullptr;
+  double ch = 0, ce = 0, cg = 0;
+  int hh = 0, he = 0, hg = 0;
+  float* bout = nullptr;
+  float* xout = nullptr;
+  int* ovf_flag = nullptr;
+  int nacc = 0;
+  const double* ain[6] = {};
+  double* aout[6] = {};
+  double ah[6] = {}, ae[6] = {};
+  int hah[6] = {}, hae[6] = {};
+};
+bool feval_combine_supported(const StencilSpec& k);
+void feval_combine(const StencilSpec& k, const float* y32, const FevalCombine& f, cudaStream_t st);
+
 // ---- tensor contractions (precond.hpp:69-122) --------------------------------------
 // side 0 L (stride n^2), 1 M (stride n), 2 R (stride 1).  pd: fused diag scale
 // of the output (precond.hpp:172) or null.  fold: Q has the Dirichlet sine

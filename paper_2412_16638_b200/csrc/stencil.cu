@@ -285,6 +285,82 @@ struct EpiF32Forcing {
   __device__ void finish(State&) const {}
 };
 
+// f evaluations of stage i fused with the next stage's right-hand side
+// (stepper.cpp:157-192), F32 policy, fp32 stage vector y (read once, raw):
+//   f_hi  = K widen(y) + g            (fp64; stored when b_i != 0)
+//   f_eps = K y + g32                 (binary32 arithmetic; consumed here)
+//   rhs_{i+1} = S_{i+1} + c_h f_hi + c_e f_eps (+ c_g g)  -> narrowed b, x0
+//   S_k     += a_h f_hi + a_e f_eps   for the later stages k
+// S_k holds u plus stage k's couplings to stages < i, accumulated in the
+// reference's term order (j ascending, the fp64 term before the eps term, the
+// forcing last), so every value is rounded exactly as the per-stage
+// combination would round it; f_eps never touches HBM.
+constexpr int kMaxAcc = 6;
+struct EpiFevalCombine {
+  static constexpr bool kDual = true;
+  float s32 = 0.f, g32k = 0.f;    // the binary32 stencil's sigma / gamma
+  const double* g = nullptr;      // forcing
+  const float* g32 = nullptr;     // narrowed forcing
+  double* fhi = nullptr;          // f_hi output (nullable)
+  int* finite_flag = nullptr;     // check_finite(y) (nullable)
+  const double* sin = nullptr;    // S_{i+1} (u on the first stage)
+  double ch = 0, ce = 0, cg = 0;  // rhs couplings to f_hi, f_eps, g
+  int hh = 0, he = 0, hg = 0;     // which are present (nonzero in the tableau)
+  float* bout = nullptr;
+  float* xout = nullptr;
+  int* ovf_flag = nullptr;        // downcast overflow of rhs_{i+1}
+  int nacc = 0;
+  const double* ain[kMaxAcc] = {};
+  double* aout[kMaxAcc] = {};
+  double ah[kMaxAcc] = {}, ae[kMaxAcc] = {};
+  int hah[kMaxAcc] = {}, hae[kMaxAcc] = {};
+  struct State {};
+  struct Pre {
+    V4<double> g, s;
+    V4<float> g32;
+  };
+  __device__ void init(State&) const {}
+  __device__ __forceinline__ Pre pre4(long i) const { return Pre{ld4(g + i), ld4(sin + i), ld4(g32 + i)}; }
+  __device__ __forceinline__ void v4dual(State&, long i, const V4<double>& v64, const V4<float>& v32,
+                                         const V4<double>& xc, const Pre& p) const {
+    if (finite_flag && !(isfinite(xc.x[0]) && isfinite(xc.x[1]) && isfinite(xc.x[2]) && isfinite(xc.x[3])))
+      *finite_flag = 1;
+    V4<double> fh;
+    V4<float> fe;
+    bool ovf = false;
+    V4<float> b;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      fh.x[e] = xadd(v64.x[e], p.g.x[e]);
+      fe.x[e] = xadd(v32.x[e], p.g32.x[e]);
+      double r = p.s.x[e];
+      if (hh) r = xadd(r, xmul(ch, fh.x[e]));
+      if (he) r = xadd(r, xmul(ce, (double)fe.x[e]));
+      if (hg) r = xadd(r, xmul(cg, p.g.x[e]));
+      ovf |= f32_overflows(r);
+      b.x[e] = __double2float_rn(r);
+    }
+    if (fhi) st4(fhi + i, fh);
+    st4(bout + i, b);
+    st4(xout + i, b);
+    if (ovf) *ovf_flag = 1;
+    for (int a = 0; a < nacc; ++a) {
+      V4<double> s = ld4(ain[a] + i);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (hah[a]) s.x[e] = xadd(s.x[e], xmul(ah[a], fh.x[e]));
+        if (hae[a]) s.x[e] = xadd(s.x[e], xmul(ae[a], (double)fe.x[e]));
+      }
+      st4(aout[a] + i, s);
+    }
+  }
+  // (the generic paths never run this epilogue: feval_combine requires the TMA kernel)
+  __device__ __forceinline__ void v4p(State&, long, const V4<double>&, const V4<double>&, const Pre&) const {}
+  __device__ __forceinline__ void v4(State&, long, const V4<double>&, const V4<double>&) const {}
+  __device__ __forceinline__ void s1(State&, long, double, double) const {}
+  __device__ void finish(State&) const {}
+};
+
 // Planes a CTA marches over.  kb < ke: chunks of `chunk` planes of [kb, ke)
 // by blockIdx.z.  kb < 0: the two boundary planes of a split slab (z = 0 ->
 // plane 0, z = 1 -> plane nz - 1), the part that waits for the ghosts.
@@ -439,6 +515,11 @@ __global__ void __launch_bounds__(VX* VY)
 }
 
 
+template <class E, class = void>
+struct is_dual : std::false_type {};
+template <class E>
+struct is_dual<E, std::enable_if_t<E::kDual>> : std::true_type {};
+
 // ---- plane-pipelined TMA kernel (Dirichlet, real T, n % 128 == 0) --------------------
 // A CTA owns a 128 (i) x 8 (j) column of the grid over TKC planes.  Each
 // plane tile arrives once by a TMA tensor copy — (8 + 2) rows x (128 + 8)
@@ -558,7 +639,28 @@ __global__ void __launch_bounds__(TTHREADS)
         const T xr = e == 3 ? right : c.x[e + 1];
         v.x[e] = point<T>(0, s, g, T(0), c.x[e], xl, xr, ym.x[e], yp.x[e], zm.x[e], zp.x[e]);
       }
-      epi.v4p(st, gidx(r, k), v, c, pre[rr]);
+      if constexpr (is_dual<Epi>::value) {
+        // the same neighbourhood in binary32 arithmetic (apply_f's F32 policy)
+        const float4 c32 = *reinterpret_cast<const float4*>(pc + o);
+        const float4 ym32 = *reinterpret_cast<const float4*>(pc + o - TW), yp32 = *reinterpret_cast<const float4*>(pc + o + TW);
+        const float4 zm32 = *reinterpret_cast<const float4*>(pm + o), zp32 = *reinterpret_cast<const float4*>(pp + o);
+        const float cc[4] = {c32.x, c32.y, c32.z, c32.w};
+        const float ymv[4] = {ym32.x, ym32.y, ym32.z, ym32.w}, ypv[4] = {yp32.x, yp32.y, yp32.z, yp32.w};
+        const float zmv[4] = {zm32.x, zm32.y, zm32.z, zm32.w}, zpv[4] = {zp32.x, zp32.y, zp32.z, zp32.w};
+        float l32 = shfl_up1(cc[3]), r32 = shfl_down1(cc[0]);
+        if (lane == 0) l32 = pc[o - 1];
+        if (lane == 31) r32 = pc[o + 4];
+        V4<float> v32;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float xl = e == 0 ? l32 : cc[e - 1];
+          const float xr = e == 3 ? r32 : cc[e + 1];
+          v32.x[e] = point<float>(0, epi.s32, epi.g32k, 0.0f, cc[e], xl, xr, ymv[e], ypv[e], zmv[e], zpv[e]);
+        }
+        epi.v4dual(st, gidx(r, k), v, v32, c, pre[rr]);
+      } else {
+        epi.v4p(st, gidx(r, k), v, c, pre[rr]);
+      }
     }
 #pragma unroll
     for (int rr = 0; rr < TROWS; ++rr) pre[rr] = nxt[rr];
@@ -750,6 +852,38 @@ void apply_f32(const StencilSpec& k, const double* y, const float* y32, const fl
     launch(k, LdPlain<float>{y32}, EpiF32Forcing{g32, out32, finite_flag}, st, "apply_f32");
   else
     launch(k, LdD2F{y, flag}, EpiF32Forcing{g32, out32, finite_flag}, st, "apply_f32");
+}
+
+bool feval_combine_supported(const StencilSpec& k) {
+  return k.stencil == 0 && k.n % TI == 0 && tma_stencil_enabled();
+}
+
+void feval_combine(const StencilSpec& k, const float* y32, const FevalCombine& f, cudaStream_t st) {
+  if (!feval_combine_supported(k)) MPRKB_THROW(10, "feval_combine: needs the TMA stencil (Dirichlet, n % 128 == 0)");
+  if (f.nacc > kMaxAcc) MPRKB_THROW(10, "feval_combine: too many later stages");
+  EpiFevalCombine e;
+  e.s32 = (float)k.sigma;
+  e.g32k = (float)k.gamma;
+  e.g = f.g;
+  e.g32 = f.g32;
+  e.fhi = f.fhi;
+  e.finite_flag = f.finite_flag;
+  e.sin = f.sin;
+  e.ch = f.ch; e.ce = f.ce; e.cg = f.cg;
+  e.hh = f.hh; e.he = f.he; e.hg = f.hg;
+  e.bout = f.bout;
+  e.xout = f.xout;
+  e.ovf_flag = f.ovf_flag;
+  e.nacc = f.nacc;
+  for (int a = 0; a < f.nacc; ++a) {
+    e.ain[a] = f.ain[a];
+    e.aout[a] = f.aout[a];
+    e.ah[a] = f.ah[a];
+    e.ae[a] = f.ae[a];
+    e.hah[a] = f.hah[a];
+    e.hae[a] = f.hae[a];
+  }
+  launch(k, LdF2D{y32}, e, st, "feval_combine");
 }
 
 #define INST_STENCIL(T)                                                                          \

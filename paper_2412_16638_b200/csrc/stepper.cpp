@@ -1,6 +1,7 @@
 #include "stepper.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cmath>
 
@@ -105,6 +106,20 @@ Stepper::Stepper(const StepperConfig& cfg)
   }
   y_.alloc(m * sizeof(double));
   gate_dev_.alloc(sizeof(int) * 256);
+  {
+    // fused stage pipeline: fp32 heat stages, every stage implicit, forcing
+    // present, the TMA stencil path (MPRKB_FUSED_STAGES=0 disables it)
+    const char* env = std::getenv("MPRKB_FUSED_STAGES");
+    bool ok = !(env && env[0] == '0') && cfg_.eq == Equation::Heat && cfg_.f32 &&
+              q >= 2 && q - 2 <= 6 && !prob_.forcing.empty() && feval_combine_supported(kspec_);
+    for (int i = 0; i < q; ++i) ok = ok && t.ae(i, i) != 0.0 && t.ah(i, i) == 0.0;
+    fused_ = ok;
+    if (fused_) {
+      acc_.resize(q);
+      for (int k = 2; k < q; ++k) acc_[k].alloc(m * sizeof(double));
+      xsol2_.alloc(m * sizeof(float));
+    }
+  }
   if (!solvers_.empty()) {
     const size_t s = dtype_size(solve_dtype_);
     bsol_.alloc(m * s);
@@ -129,6 +144,10 @@ Stepper::~Stepper() {
 // raises a device flag in its own slot; the flags are inspected in program
 // order before u is touched, so the first failing check is the one thrown.
 void Stepper::step(double* u, StepTrace& trace) {
+  if (fused_) {
+    step_fused(u, trace);
+    return;
+  }
   trace = StepTrace{};
   flags_.clear();
   struct Check {
@@ -271,6 +290,121 @@ void Stepper::step(double* u, StepTrace& trace) {
     if (!slab_.split() && stage_checks > 0) {
       // stream-ordered copy of the (host-mapped) check flags to device memory:
       // the update's CTAs read it from L2, not across PCIe
+      CUDA_CHECK(cudaMemcpyAsync(gate_dev_.get(), flags_.dev(1), sizeof(int) * stage_checks, cudaMemcpyHostToDevice,
+                                 st_));
+      gate = gate_dev_.as<int>();
+    }
+    final_update(m, u, fin, fin_flag, st_, gate, stage_checks);
+  }
+  raise_flags();
+  if (timer_.enabled()) timer_.resolve();
+}
+
+// Stepper::step with stage i's f evaluations fused into stage i+1's
+// right-hand side.  Same kernels' arithmetic, same term order, same checks in
+// the same order as step() — bitwise the same results — with f_eps never
+// stored and each stage vector read once.  Stage solution buffers alternate
+// (the fused kernel reads y_i while writing x0 of stage i+1).
+void Stepper::step_fused(double* u, StepTrace& trace) {
+  trace = StepTrace{};
+  flags_.clear();
+  struct Check {
+    int slot, code;
+    const char* msg;
+  };
+  std::vector<Check> checks;
+  int next = 1;
+  auto check_slot = [&](int code, const char* msg) {
+    if (next >= 255) MPRKB_THROW(1, "stepper: too many checks");
+    checks.push_back({next, code, msg});
+    return flags_.dev(next++);
+  };
+  auto raise_flags = [&]() {
+    stream_sync(st_);
+    std::vector<double> v(checks.size());
+    for (size_t i = 0; i < checks.size(); ++i) v[i] = flags_.value(checks[i].slot) ? 1.0 : 0.0;
+    if (slab_.split() && !v.empty()) slab_.comm->allreduce_max(v.data(), (int)v.size());
+    for (size_t i = 0; i < checks.size(); ++i)
+      if (v[i] != 0.0) MPRKB_THROW(checks[i].code, checks[i].msg);
+  };
+  const Tableau& t = cfg_.tab;
+  const int q = t.q;
+  const double tau = cfg_.tau;
+  const size_t m = m_;
+  const Crit crit{cfg_.tol, cfg_.max_iter};
+  const char* kOverflow = "downcast: value exceeds the binary32 range";
+  const char* kStage = "stage vector picked up a NaN or infinity";
+  float* xs[2] = {xsol_.as<float>(), xsol2_.as<float>()};
+  float* b32 = bsol_.as<float>();
+  EventTimer* tm = timer_.enabled() ? &timer_ : nullptr;
+  auto solve = [&](int i) {
+    StageSolver& S = solvers_[solver_of_stage_[i]];
+    SolveReport rep;
+    cg_solve<float>(*S.op, S.pre.get(), b32, xs[i & 1], crit, cfg_.num, *w32_, rep, st_, tm);
+    if (!rep.converged) trace.solver_failure = true;
+    trace.solves.push_back(std::move(rep));
+  };
+
+  // stage 0: rhs = u + tau a_00 g (stepper.cpp:157-172), x0 = rhs
+  {
+    CombineTerms terms;
+    add_term(terms, tau * t.ae(0, 0), g64_.get(), 0);
+    Bracket br(timer_, "axpy", st_);
+    combine(m, u, terms, 1, b32, check_slot(6, kOverflow), st_, xs[0]);
+  }
+  solve(0);
+  for (int i = 0; i + 1 < q; ++i) {
+    const int nx = i + 1;
+    FevalCombine f;
+    f.g = g64_.as<double>();
+    f.g32 = g32_.as<float>();
+    f.fhi = t.b[i] != 0.0 ? f_hi_[i].as<double>() : nullptr;
+    f.finite_flag = check_slot(9, kStage);
+    f.sin = i == 0 ? u : acc_[nx].as<double>();
+    f.hh = t.ah(nx, i) != 0.0;
+    f.ch = tau * t.ah(nx, i);
+    f.he = t.ae(nx, i) != 0.0;
+    f.ce = tau * t.ae(nx, i);
+    f.hg = 1;
+    f.cg = tau * t.ae(nx, nx);
+    f.bout = b32;
+    f.xout = xs[nx & 1];
+    f.ovf_flag = check_slot(6, kOverflow);
+    for (int k = nx + 1; k < q; ++k) {
+      const int a = f.nacc++;
+      f.ain[a] = i == 0 ? u : acc_[k].as<double>();
+      f.aout[a] = acc_[k].as<double>();
+      f.hah[a] = t.ah(k, i) != 0.0;
+      f.ah[a] = tau * t.ah(k, i);
+      f.hae[a] = t.ae(k, i) != 0.0;
+      f.ae[a] = tau * t.ae(k, i);
+    }
+    {
+      Bracket br(timer_, "stencil", st_);
+      feval_combine(kspec_, xs[i & 1], f, st_);
+    }
+    solve(nx);
+  }
+  // last stage: its f_hi feeds only the final update
+  {
+    const int i = q - 1;
+    if (t.b[i] != 0.0) {
+      Bracket br(timer_, "stencil", st_);
+      apply_f64(kspec_, nullptr, xs[i & 1], g64_.as<double>(), f_hi_[i].as<double>(), check_slot(9, kStage), st_);
+    } else {
+      extract_stage(m, 0, xs[i & 1], y_.as<double>(), check_slot(9, kStage), st_);
+    }
+  }
+  const int stage_checks = next - 1;
+  if (slab_.split()) raise_flags();
+  CombineTerms fin;
+  for (int i = 0; i < q; ++i)
+    if (t.b[i] != 0.0) add_term(fin, tau * t.b[i], f_hi_[i].get(), 0);
+  {
+    Bracket br(timer_, "axpy", st_);
+    int* fin_flag = check_slot(9, "updated state picked up a NaN or infinity");
+    const int* gate = nullptr;
+    if (!slab_.split() && stage_checks > 0) {
       CUDA_CHECK(cudaMemcpyAsync(gate_dev_.get(), flags_.dev(1), sizeof(int) * stage_checks, cudaMemcpyHostToDevice,
                                  st_));
       gate = gate_dev_.as<int>();

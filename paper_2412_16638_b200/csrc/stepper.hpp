@@ -55,6 +55,13 @@ class Stepper {
     std::unique_ptr<Op> op;
     std::unique_ptr<Op> pre;
   };
+  // fp32-stage heat on the TMA stencil path: each stage's f evaluations are
+  // fused with the next stage's right-hand side (EpiFevalCombine); later
+  // stages' couplings accumulate in acc_ (see step_fused)
+  void step_fused(double* u, StepTrace& trace);
+  bool fused_ = false;
+  std::vector<DevBuf> acc_;
+  DevBuf xsol2_;
   StepperConfig cfg_;
   Slab slab_;
   std::unique_ptr<Halo> halo_;  // split grid only

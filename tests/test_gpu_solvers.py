@@ -292,3 +292,34 @@ def test_cpp_dropin_matches_reference(gpu, mp, ref, dropin_exe):
     want = ref.integrate(0, 16, tabd(mp.builtin("4s3pB")), 1.0 / 40.0, 0.1, 1e-4, "f32")
     assert (mean_it, emax, el2) == (want["mean_iterations"], want["error_max"], want["error_l2"])
     assert "solves 4" in out.stdout
+
+
+@pytest.mark.parametrize("name", ["4s3pB", "4s3pC"])
+def test_fused_stage_pipeline_bitwise(gpu, mp, ref, name):
+    """fp32 heat stages on the TMA stencil path run the fused pipeline (stage
+    i's f evaluations + stage i+1's right-hand side in one kernel, later
+    stages' couplings accumulated in place): bitwise the reference in PARITY
+    numerics, and bitwise the unfused kernels in FAST numerics."""
+    import os
+
+    t = mp.builtin(name)
+    n, tau = 128, 0.01
+    want = np.zeros(n ** 3)
+    cs = ref.stepper(0, n, tabd(t), tau, 1e-5, "f32")
+    wt = [cs.step(want)["iterations"] for _ in range(2)]
+    st = mp.Stepper("heat", n, t, tau, 1e-5, "f32", numerics="parity")
+    got = np.zeros(n ** 3)
+    gt = [st.step(got)["iterations"] for _ in range(2)]
+    assert gt == wt
+    assert same_bits(got, want)
+    fused = mp.Stepper("heat", 256, t, tau, 1e-3, "f32")
+    os.environ["MPRKB_FUSED_STAGES"] = "0"
+    try:
+        plain = mp.Stepper("heat", 256, t, tau, 1e-3, "f32")
+    finally:
+        del os.environ["MPRKB_FUSED_STAGES"]
+    a, b = np.zeros(256 ** 3), np.zeros(256 ** 3)
+    for _ in range(2):
+        fused.step(a)
+        plain.step(b)
+    assert same_bits(a, b)
