@@ -102,6 +102,15 @@ void pack_tf32_fold(int n, const float* q, float* qpack);
 // Host: split Q (n x n row-major) into tf32 hi/lo and pack as
 // [k-block of 16][row-group of 8][k-chunk of 4][8 rows][4].
 void pack_tf32_split(int n, const float* q, float* hi_packed, float* lo_packed);
+// Contraction with a periodic (DFT) factor Q[a][q] = n^-1/2 e^{sign 2 pi i aq/n}
+// as a batched Stockham FFT along the side's axis (fft.cu); complex T, FAST
+// numerics.  twiddles: n/2 values e^{-2 pi i k/n}.  pd: fused diagonal of the
+// output (nullable).  cols as for tensor_apply.
+bool fft_supported(int n, long cols);
+template <class T>
+void fft_lines(int side, int n, int sign, const T* x, T* out, const T* pd, const T* twiddles, cudaStream_t st,
+               long cols = 0);
+
 // pd_inv[i+jn+kn^2] = 1/(la_i + lb_j + lc_k) in T (precond.hpp:139-150); real
 // types only (IEEE division is correctly rounded on both sides).  *zero_flag
 // (initialised to INT_MAX by the caller) receives the smallest linear index

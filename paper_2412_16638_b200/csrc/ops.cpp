@@ -125,6 +125,44 @@ FastDiagOp<T>::FastDiagOp(int n, const T* qa, const T* qa_inv, const T* qb, cons
         fold_[f] = scale > 0.0 && worst <= 1e-6 * scale;
       }
   }
+  if constexpr (is_cplx<T>) {
+    // FAST numerics: a factor that is the scaled DFT n^-1/2 e^{+-2 pi i aq/n}
+    // (spectral_periodic, spectral.cpp:31-51) is applied as an FFT (fft.cu)
+    const char* env = std::getenv("MPRKB_FFT");
+    if (num == Numerics::Fast && !(env && env[0] == '0') && fft_supported(n, (long)n * n)) {
+      using H = typename HostOf<T>::type;
+      const double norm = 1.0 / std::sqrt((double)n), twopi = 2.0 * 3.14159265358979323846;
+      const double tol = std::is_same_v<T, c32> ? 1e-6 : 1e-13;
+      bool all = true;
+      for (int fct = 0; fct < 6 && all; ++fct) {
+        const H* Q = reinterpret_cast<const H*>(src[fct]);
+        int sign = 0;
+        for (int sg : {1, -1}) {
+          double worst = 0.0;
+          for (int a = 0; a < n && worst <= tol; ++a)
+            for (int qq = 0; qq < n; ++qq) {
+              const double ang = twopi * (double)(((long long)a * qq) % n) / n;
+              const std::complex<double> want = std::polar(norm, sg * ang);
+              const H v = Q[(size_t)a * n + qq];
+              worst = std::max(worst, std::abs(std::complex<double>((double)v.real(), (double)v.imag()) - want));
+            }
+          if (worst <= tol) sign = sg;
+        }
+        dft_[fct] = sign;
+        all = sign != 0;
+      }
+      if (!all)
+        for (int fct = 0; fct < 6; ++fct) dft_[fct] = 0;
+      if (all) {
+        std::vector<H> tw(n / 2);
+        for (int k = 0; k < n / 2; ++k) {
+          const std::complex<double> w = std::polar(1.0, -twopi * k / n);
+          tw[k] = H((typename H::value_type)w.real(), (typename H::value_type)w.imag());
+        }
+        upload(twid_, tw.data(), tw.size() * sizeof(T));
+      }
+    }
+  }
   if constexpr (std::is_same_v<T, float>) {
     // fp32 FAST numerics run on the tensor cores (3xTF32, tensor_tc.cu)
     // unless MPRKB_TENSOR_CORES=0 selects the CUDA-core kernels
@@ -213,6 +251,12 @@ FastDiagOp<T>::FastDiagOp(int n, const T* qa, const T* qa_inv, const T* qb, cons
 // diagonal scale fused into the L pass, then R, M, L with the forward factors.
 template <class T>
 void FastDiagOp<T>::contract(int side, int f, const T* in, T* o, const T* pd, long cols, cudaStream_t st) {
+  if constexpr (is_cplx<T>) {
+    if (dft_[f] != 0 && fft_supported(n_, cols > 0 ? cols : (long)n_ * n_)) {
+      fft_lines<T>(side, n_, dft_[f], in, o, pd, twid_.template as<T>(), st, cols);
+      return;
+    }
+  }
   if constexpr (std::is_same_v<T, float>) {
     if (tc_split_) {
       if (tcf_[f])
@@ -297,12 +341,13 @@ void FastDiagOp<T>::apply(const void* xv, void* outv, cudaStream_t st) {
       return;
     }
   }
-  tensor_apply<T>(2, n_, q_[1].as<T>(), x, t1, nullptr, num_, st, fold_[1]);
-  tensor_apply<T>(1, n_, q_[3].as<T>(), t1, t2, nullptr, num_, st, fold_[3]);
-  tensor_apply<T>(0, n_, q_[5].as<T>(), t2, t1, pd_.as<T>(), num_, st, fold_[5]);
-  tensor_apply<T>(2, n_, q_[0].as<T>(), t1, t2, nullptr, num_, st, fold_[0]);
-  tensor_apply<T>(1, n_, q_[2].as<T>(), t2, t1, nullptr, num_, st, fold_[2]);
-  tensor_apply<T>(0, n_, q_[4].as<T>(), t1, out, nullptr, num_, st, fold_[4]);
+  const long nn = (long)n_ * n_;
+  contract(2, 1, x, t1, nullptr, nn, st);
+  contract(1, 3, t1, t2, nullptr, nn, st);
+  contract(0, 5, t2, t1, pd_.as<T>(), nn, st);
+  contract(2, 0, t1, t2, nullptr, nn, st);
+  contract(1, 2, t2, t1, nullptr, nn, st);
+  contract(0, 4, t1, out, nullptr, nn, st);
 }
 
 template class FastDiagOp<float>;

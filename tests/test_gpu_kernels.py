@@ -239,3 +239,27 @@ def test_dot_conjugated(gpu, mp):
     assert got == acc
     fast = mp.dot(to_dev(torch, a), to_dev(torch, b), conjugate=True, numerics="fast")
     assert abs(fast - np.vdot(a, b)) < 1e-10
+
+
+@pytest.mark.parametrize("kind", [2, 3])
+@pytest.mark.parametrize("n", [64, 256])
+def test_fastdiag_fft_matches_dense(gpu, mp, kind, n):
+    """Periodic (DFT) FastDiag factors run as batched Stockham FFTs in FAST
+    numerics: the result matches the dense contraction path (MPRKB_FFT=0)
+    to the working precision."""
+    import os
+
+    import torch
+
+    rng = np.random.default_rng(600 + n + kind)
+    x = rnd(rng, kind, n ** 3)
+    xd = to_dev(torch, x)
+    fft = mp.Operator.fastdiag_stage(kind, "advection", n, 1.0 / 640.0, 0.5, "fast").apply(xd).cpu().numpy()
+    os.environ["MPRKB_FFT"] = "0"
+    try:
+        dense = mp.Operator.fastdiag_stage(kind, "advection", n, 1.0 / 640.0, 0.5, "fast").apply(xd).cpu().numpy()
+    finally:
+        del os.environ["MPRKB_FFT"]
+    scale = np.abs(dense).max()
+    tol = 2e-5 if kind == 2 else 1e-12
+    assert np.abs(fft - dense).max() <= tol * scale, np.abs(fft - dense).max() / scale
