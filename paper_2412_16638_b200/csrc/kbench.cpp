@@ -4,6 +4,7 @@
 // (SURVEY.md §8d).  Inputs are well above L2 (n = 256: one fp32 vector is
 // 64 MB, every kernel touches >= 128 MB), so back-to-back launches stream
 // from HBM.
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -145,6 +146,17 @@ void kernel_bench(const std::string& which, int n, int reps, double* ms, double*
         tensor_apply_tc_fold(side, n, qa.as<float>(), f32(0), f32(1), pd, st);
       else
         tensor_apply_tc(side, n, qa.as<float>(), qb.as<float>(), f32(0), f32(1), pd, st);
+    });
+  } else if (which.rfind("fft_", 0) == 0) {
+    // periodic FastDiag contraction as an FFT pass: fft_{R,M,L}, complex fp32
+    const char sd = which.back();
+    const int side = sd == 'R' ? 2 : sd == 'M' ? 1 : 0;
+    std::vector<c32> tw(n);
+    for (int k = 0; k < n; ++k) tw[k] = c32{(float)std::cos(-2.0 * M_PI * k / n), (float)std::sin(-2.0 * M_PI * k / n)};
+    DevBuf dt(tw.size() * sizeof(c32));
+    CUDA_CHECK(cudaMemcpy(dt.get(), tw.data(), tw.size() * sizeof(c32), cudaMemcpyHostToDevice));
+    t = time_it(st, reps, 16 * D, [&] {
+      fft_lines<c32>(side, n, -1, v[0].as<c32>(), v[1].as<c32>(), nullptr, dt.as<c32>(), st);
     });
   } else {
     MPRKB_THROW(10, "kernel_bench: unknown kernel '" + which + "'");

@@ -104,7 +104,7 @@ void pack_tf32_fold(int n, const float* q, float* qpack);
 void pack_tf32_split(int n, const float* q, float* hi_packed, float* lo_packed);
 // Contraction with a periodic (DFT) factor Q[a][q] = n^-1/2 e^{sign 2 pi i aq/n}
 // as a batched Stockham FFT along the side's axis (fft.cu); complex T, FAST
-// numerics.  twiddles: n/2 values e^{-2 pi i k/n}.  pd: fused diagonal of the
+// numerics.  twiddles: n values e^{-2 pi i k/n}.  pd: fused diagonal of the
 // output (nullable).  cols as for tensor_apply.
 bool fft_supported(int n, long cols);
 template <class T>

@@ -154,8 +154,8 @@ FastDiagOp<T>::FastDiagOp(int n, const T* qa, const T* qa_inv, const T* qb, cons
       if (!all)
         for (int fct = 0; fct < 6; ++fct) dft_[fct] = 0;
       if (all) {
-        std::vector<H> tw(n / 2);
-        for (int k = 0; k < n / 2; ++k) {
+        std::vector<H> tw(n);
+        for (int k = 0; k < n; ++k) {
           const std::complex<double> w = std::polar(1.0, -twopi * k / n);
           tw[k] = H((typename H::value_type)w.real(), (typename H::value_type)w.imag());
         }

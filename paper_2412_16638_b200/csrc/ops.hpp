@@ -79,7 +79,7 @@ class FastDiagOp final : public Op {
   DevBuf qhp_[6], qlp_[6];  // tf32 hi/lo split, UMMA-packed (tc_ only; folded: qhp_ holds all four blocks)
   bool tcf_[6] = {false, false, false, false, false, false};  // folded tcgen05 contraction per factor
   int dft_[6] = {0, 0, 0, 0, 0, 0};  // complex FAST: factor is the scaled DFT with this sign (FFT path)
-  DevBuf twid_;                      // e^{-2 pi i k/n}, k < n/2 (FFT path)
+  DevBuf twid_;                      // e^{-2 pi i k/n}, k < n (FFT path)
   DevBuf pd_, t1_, t2_, t3_;  // t3_: split grid only
 };
 
