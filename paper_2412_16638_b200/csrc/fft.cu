@@ -251,6 +251,13 @@ __global__ void __launch_bounds__(256) k_fft256(long cols, int side, int sign, c
     if (sign > 0) w.im = -w.im;
     sm[l * RS + k1 * 16 + (t ^ k1)] = k1 ? cmul(v[k1], w) : v[k1];  // (XOR swizzle: step 2 reads a column)
   }
+  // the diagonal of the outputs this thread writes, loaded while the
+  // transpose and the second DFT run
+  T d[DIAG ? 16 : 1];
+  if (DIAG) {
+#pragma unroll
+    for (int k2 = 0; k2 < 16; ++k2) d[k2] = ldg(pd + gaddr(t + 16 * k2));
+  }
   __syncthreads();
   // step 2: thread t owns k1 = t, values q2 = 0..15
 #pragma unroll
@@ -259,12 +266,11 @@ __global__ void __launch_bounds__(256) k_fft256(long cols, int side, int sign, c
   // v[k2] = X[t + 16 k2]
 #pragma unroll
   for (int k2 = 0; k2 < 16; ++k2) {
-    const long g = gaddr(t + 16 * k2);
     T r = v[k2];
     r.re *= scale;
     r.im *= scale;
-    if (DIAG) r = cmul(r, ldg(pd + g));
-    out[g] = r;
+    if constexpr (DIAG) r = cmul(r, d[k2]);
+    out[gaddr(t + 16 * k2)] = r;
   }
 }
 

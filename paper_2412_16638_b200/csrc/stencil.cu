@@ -104,6 +104,14 @@ template <class T>
 __device__ __forceinline__ T shfl_down1(T v) {
   return __shfl_down_sync(0xffffffffu, v, 1);
 }
+template <class R>
+__device__ __forceinline__ cplx<R> shfl_up1(cplx<R> v) {
+  return {__shfl_up_sync(0xffffffffu, v.re, 1), __shfl_up_sync(0xffffffffu, v.im, 1)};
+}
+template <class R>
+__device__ __forceinline__ cplx<R> shfl_down1(cplx<R> v) {
+  return {__shfl_down_sync(0xffffffffu, v.re, 1), __shfl_down_sync(0xffffffffu, v.im, 1)};
+}
 
 // The reference's arithmetic for one point (operators.hpp:133-140, 149-158);
 // xl/xr/ym/yp/zm/zp are the i-1, i+1, j-1, j+1, k-1, k+1 neighbours.
@@ -429,8 +437,8 @@ constexpr int VX = 32, VY = 4, VKC = 16;
 
 template <class Src, class Epi>
 __global__ void __launch_bounds__(VX* VY)
-    k_stencil4(int n, int nz, int kb, int ke, int stencil, typename Src::type s, typename Src::type g,
-               typename Src::type g2, Src src, Epi epi) {
+    k_stencil4(int n, int nz, int kb, int ke, int stencil, real_t<typename Src::type> s,
+               real_t<typename Src::type> g, real_t<typename Src::type> g2, Src src, Epi epi) {
   using T = typename Src::type;
   const int lane = threadIdx.x;
   const int i0 = (blockIdx.x * VX + lane) * 4;
@@ -754,7 +762,7 @@ void launch(const StencilSpec& sp, Src src, Epi epi, cudaStream_t st, const char
   using R = real_t<T>;
   const int n = sp.n;
   const int nz = sp.nz > 0 ? sp.nz : n;
-  const bool vec = !is_cplx<T> && n % 4 == 0;
+  const bool vec = n % 4 == 0;  // (complex too: 4 points per lane, shuffles per component)
   // the TMA plane pipeline covers the bench path: Dirichlet heat, real T, n % 128 == 0
   const bool tma = !is_cplx<T> && sp.stencil == 0 && n % TI == 0 && tma_stencil_enabled();
   const dim3 block = vec ? dim3(VX, VY) : dim3(SBX, SBY);
@@ -773,12 +781,12 @@ void launch(const StencilSpec& sp, Src src, Epi epi, cudaStream_t st, const char
         launch_tma(sp, src, e, kb, ke, chunk, gz, st, name);
         return;
       }
-      if (vec) {
-        k_stencil4<Src, Epi><<<dim3(gx, gy, gz), block, 0, st>>>(n, nz, kb, ke, sp.stencil, (R)sp.sigma,
-                                                                (R)sp.gamma, (R)sp.gamma2, src, e);
-        LAUNCHED(name);
-        return;
-      }
+    }
+    if (vec) {
+      k_stencil4<Src, Epi><<<dim3(gx, gy, gz), block, 0, st>>>(n, nz, kb, ke, sp.stencil, (R)sp.sigma,
+                                                              (R)sp.gamma, (R)sp.gamma2, src, e);
+      LAUNCHED(name);
+      return;
     }
     k_stencil<Src, Epi><<<dim3(gx, gy, gz), block, 0, st>>>(n, nz, kb, ke, sp.stencil, (R)sp.sigma, (R)sp.gamma,
                                                              (R)sp.gamma2, src, e);
