@@ -227,7 +227,7 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
   // reference would have skipped only touches scratch vectors (never x).
   const bool batch = fast && S != nullptr;
   const bool spec_true = batch && P != nullptr && P->exact_inverse();
-  const RedSlot s1 = w.red.slot(1), s2 = w.red.slot(2), s3 = w.red.slot(3);
+  const RedSlot s2 = w.red.slot(2), s3 = w.red.slot(3);
   double r0;
   R rz{}, pq_first{};
   bool have_pq = false;
@@ -237,15 +237,18 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
       stencil_residual<T>(*S, x, b, r, &s0, st);
     }
     pre(r, z);
-    dot_real<T>(m, r, z, s1, num, st);
     {
       Bracket br(timer, "stencil", st);
-      stencil_apply_dot<T>(*S, z, q, s2, st);
+      stencil_apply_dot2<T>(*S, z, q, r, s2, st);  // q = A z, (z.q, r.z)
     }
-    const auto v = finish_slots<T, 3>(w, {0, 1, 2}, st);
+    stream_sync(st);
+    double v[3];
+    w.red.result(0, 1, &v[0]);
+    w.red.result(2, 2, &v[1]);
+    if (w.comm && w.comm->size() > 1) w.comm->allreduce_sum(v, 3);
     r0 = (double)std::sqrt((R)v[0]);
-    rz = (R)v[1];
-    pq_first = (R)v[2];
+    rz = (R)v[2];
+    pq_first = (R)v[1];
     have_pq = true;
   } else {
     r0 = (double)std::sqrt(residual(r));

@@ -229,6 +229,39 @@ struct EpiStoreDot {
   __device__ void finish(State& s) const { grid_reduce<1>(s.v, red); }
 };
 
+// q = A p with (p.q, r.p) in one pass: the first CG iteration's two scalars
+// (krylov.hpp:126-137 with p = z) without a separate dot kernel re-reading p.
+template <class T>
+struct EpiStoreDot2 {
+  T* out;
+  const T* r;
+  RedSlot red;
+  struct State {
+    double v[2];
+  };
+  using Pre = V4<T>;
+  __device__ void init(State& s) const { s.v[0] = s.v[1] = 0.0; }
+  __device__ __forceinline__ Pre pre4(long i) const { return ld4rw(r + i); }
+  __device__ __forceinline__ static double (&one(double& d))[1] { return *reinterpret_cast<double(*)[1]>(&d); }
+  __device__ __forceinline__ void v4p(State& s, long i, const V4<T>& v, const V4<T>& xc, const Pre& rv) const {
+    st4(out + i, v);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      dot_acc(one(s.v[0]), xc.x[e], v.x[e]);
+      dot_acc(one(s.v[1]), rv.x[e], xc.x[e]);
+    }
+  }
+  __device__ __forceinline__ void v4(State& s, long i, const V4<T>& v, const V4<T>& xc) const {
+    v4p(s, i, v, xc, pre4(i));
+  }
+  __device__ __forceinline__ void s1(State& s, long i, T v, T xc) const {
+    out[i] = v;
+    dot_acc(one(s.v[0]), xc, v);
+    dot_acc(one(s.v[1]), r[i], xc);
+  }
+  __device__ void finish(State& s) const { grid_reduce<2>(s.v, red); }
+};
+
 // apply_f F64: out = K y + g   (operators.cpp:83-86)
 struct EpiF64Forcing {
   const double* g;
@@ -846,6 +879,11 @@ void stencil_apply_dot(const StencilSpec& s, const T* p, T* q, const RedSlot& re
   launch(s, LdPlain<T>{p}, EpiStoreDot<T>{q, red}, st, "stencil_dot");
 }
 
+template <class T>
+void stencil_apply_dot2(const StencilSpec& s, const T* p, T* q, const T* r, const RedSlot& red, cudaStream_t st) {
+  launch(s, LdPlain<T>{p}, EpiStoreDot2<T>{q, r, red}, st, "stencil_dot2");
+}
+
 void apply_f64(const StencilSpec& k, const double* y, const float* y32, const double* g, double* out,
                int* finite_flag, cudaStream_t st) {
   if (y32)
@@ -898,7 +936,8 @@ void feval_combine(const StencilSpec& k, const float* y32, const FevalCombine& f
   template void stencil_apply<T>(const StencilSpec&, const T*, T*, cudaStream_t);               \
   template void stencil_residual<T>(const StencilSpec&, const T*, const T*, T*, const RedSlot*, \
                                     cudaStream_t);                                              \
-  template void stencil_apply_dot<T>(const StencilSpec&, const T*, T*, const RedSlot&, cudaStream_t);
+  template void stencil_apply_dot<T>(const StencilSpec&, const T*, T*, const RedSlot&, cudaStream_t);           \
+  template void stencil_apply_dot2<T>(const StencilSpec&, const T*, T*, const T*, const RedSlot&, cudaStream_t);
 
 INST_STENCIL(float)
 INST_STENCIL(double)
