@@ -7,6 +7,7 @@
 // so results are bitwise the reference's except where a FAST reduction is
 // folded in (fp64-accumulated, deterministic, see reduce.cuh).
 #include "launch.hpp"
+#include "pdl.cuh"
 #include "reduce.cuh"
 #include "vec.cuh"
 
@@ -40,6 +41,8 @@ __device__ __forceinline__ void for_each4(size_t m, F4&& f4, F1&& f1) {
 // ============================================================================
 template <class T>
 __global__ void __launch_bounds__(kBlock) k_dot_fast(size_t m, const T* a, const T* b, RedSlot red) {
+  pdl_wait();
+  pdl_trigger();
   double v[1] = {0.0};
   for_each4(
       m,
@@ -54,6 +57,8 @@ __global__ void __launch_bounds__(kBlock) k_dot_fast(size_t m, const T* a, const
 
 template <class T>
 __global__ void __launch_bounds__(kBlock) k_cdot_fast(size_t m, const T* a, const T* b, RedSlot red) {
+  pdl_wait();
+  pdl_trigger();
   double v[2] = {0.0, 0.0};
   for_each4(
       m,
@@ -130,7 +135,7 @@ void dot_real(size_t m, const T* a, const T* b, const RedSlot& red, Numerics num
   if (num == Numerics::Parity)
     k_dot_seq<T><<<1, 256, 0, st>>>(m, a, b, init ? init[0] : 0.0, red.out);
   else
-    k_dot_fast<T><<<wave(m), kBlock, 0, st>>>(m, a, b, red);
+    launch_pdl(k_dot_fast<T>, dim3(wave(m)), dim3(kBlock), 0, st, m, a, b, red);
   note_partials(red, num == Numerics::Parity ? 0 : wave(m));
   LAUNCHED("dot");
 }
@@ -142,7 +147,7 @@ void dot_conj(size_t m, const T* a, const T* b, const RedSlot& red, Numerics num
     if (num == Numerics::Parity)
       k_cdot_seq<real_t<T>><<<1, 256, 0, st>>>(m, a, b, init ? init[0] : 0.0, init ? init[1] : 0.0, red.out);
     else
-      k_cdot_fast<T><<<wave(m), kBlock, 0, st>>>(m, a, b, red);
+      launch_pdl(k_cdot_fast<T>, dim3(wave(m)), dim3(kBlock), 0, st, m, a, b, red);
     note_partials(red, num == Numerics::Parity ? 0 : wave(m));
     LAUNCHED("dot");
   } else {
@@ -156,6 +161,8 @@ void dot_conj(size_t m, const T* a, const T* b, const RedSlot& red, Numerics num
 // r = b - q   (krylov.hpp:111, 141, 165, 193, 285, 308)
 template <class T, bool RED>
 __global__ void __launch_bounds__(kBlock) k_vsub(size_t m, const T* b, const T* q, T* r, RedSlot red) {
+  pdl_wait();
+  pdl_trigger();
   double v[1] = {0.0};
   for_each4(
       m,
@@ -180,10 +187,10 @@ __global__ void __launch_bounds__(kBlock) k_vsub(size_t m, const T* b, const T* 
 template <class T>
 void vsub(size_t m, const T* b, const T* q, T* r, const RedSlot* red, cudaStream_t st) {
   if (red) {
-    k_vsub<T, true><<<wave(m), kBlock, 0, st>>>(m, b, q, r, *red);
+    launch_pdl(k_vsub<T, true>, dim3(wave(m)), dim3(kBlock), 0, st, m, b, q, r, *red);
     note_partials(*red, wave(m));
   } else
-    k_vsub<T, false><<<wave(m), kBlock, 0, st>>>(m, b, q, r, RedSlot{});
+    launch_pdl(k_vsub<T, false>, dim3(wave(m)), dim3(kBlock), 0, st, m, b, q, r, RedSlot{});
   LAUNCHED("vsub");
 }
 
@@ -191,6 +198,8 @@ void vsub(size_t m, const T* b, const T* q, T* r, const RedSlot* red, cudaStream
 template <class T, bool RED>
 __global__ void __launch_bounds__(kBlock) k_cg_update(size_t m, real_t<T> alpha, T* x, const T* p, T* r,
                                                       const T* q, RedSlot red) {
+  pdl_wait();
+  pdl_trigger();
   double v[1] = {0.0};
   for_each4(
       m,
@@ -219,16 +228,18 @@ template <class T>
 void cg_update(size_t m, real_t<T> alpha, T* x, const T* p, T* r, const T* q, const RedSlot* red,
                cudaStream_t st) {
   if (red) {
-    k_cg_update<T, true><<<wave(m), kBlock, 0, st>>>(m, alpha, x, p, r, q, *red);
+    launch_pdl(k_cg_update<T, true>, dim3(wave(m)), dim3(kBlock), 0, st, m, alpha, x, p, r, q, *red);
     note_partials(*red, wave(m));
   } else
-    k_cg_update<T, false><<<wave(m), kBlock, 0, st>>>(m, alpha, x, p, r, q, RedSlot{});
+    launch_pdl(k_cg_update<T, false>, dim3(wave(m)), dim3(kBlock), 0, st, m, alpha, x, p, r, q, RedSlot{});
   LAUNCHED("cg_update");
 }
 
 // p = z + beta p   (krylov.hpp:158)
 template <class T>
 __global__ void __launch_bounds__(kBlock) k_xpby(size_t m, const T* z, real_t<T> beta, T* p) {
+  pdl_wait();
+  pdl_trigger();
   for_each4(
       m,
       [&](size_t i) {
@@ -243,7 +254,7 @@ __global__ void __launch_bounds__(kBlock) k_xpby(size_t m, const T* z, real_t<T>
 
 template <class T>
 void xpby(size_t m, const T* z, real_t<T> beta, T* p, cudaStream_t st) {
-  k_xpby<T><<<wave(m), kBlock, 0, st>>>(m, z, beta, p);
+  launch_pdl(k_xpby<T>, dim3(wave(m)), dim3(kBlock), 0, st, m, z, beta, p);
   LAUNCHED("xpby");
 }
 
@@ -350,6 +361,8 @@ __device__ __forceinline__ double term1(const CombineTerms& t, int c, size_t i) 
 template <int KIND>
 __global__ void __launch_bounds__(kBlock) k_combine(size_t m, const double* u, CombineTerms t, void* out,
                                                     void* out2, int* flag) {
+  pdl_wait();
+  pdl_trigger();
   bool bad = false;
   auto emit = [&](size_t i, double r) {
     if (KIND == 0) {
@@ -408,10 +421,10 @@ __global__ void __launch_bounds__(kBlock) k_combine(size_t m, const double* u, C
 void combine(size_t m, const double* u, const CombineTerms& t, int out_kind, void* out, int* flag,
              cudaStream_t st, void* out2) {
   switch (out_kind) {
-    case 0: k_combine<0><<<wave(m), kBlock, 0, st>>>(m, u, t, out, out2, flag); break;
-    case 1: k_combine<1><<<wave(m), kBlock, 0, st>>>(m, u, t, out, out2, flag); break;
-    case 2: k_combine<2><<<wave(m), kBlock, 0, st>>>(m, u, t, out, out2, flag); break;
-    default: k_combine<3><<<wave(m), kBlock, 0, st>>>(m, u, t, out, out2, flag); break;
+    case 0: launch_pdl(k_combine<0>, dim3(wave(m)), dim3(kBlock), 0, st, m, u, t, out, out2, flag); break;
+    case 1: launch_pdl(k_combine<1>, dim3(wave(m)), dim3(kBlock), 0, st, m, u, t, out, out2, flag); break;
+    case 2: launch_pdl(k_combine<2>, dim3(wave(m)), dim3(kBlock), 0, st, m, u, t, out, out2, flag); break;
+    default: launch_pdl(k_combine<3>, dim3(wave(m)), dim3(kBlock), 0, st, m, u, t, out, out2, flag); break;
   }
   LAUNCHED("combine");
 }
@@ -469,6 +482,8 @@ void extract_stage(size_t m, int src_kind, const void* x, double* y, int* flag, 
 // the update.
 __global__ void __launch_bounds__(kBlock) k_final(size_t m, double* u, CombineTerms t, int* flag, const int* gate,
                                                   int gate_count) {
+  pdl_wait();
+  pdl_trigger();
   if (gate_count) {  // one thread per CTA reads the flags (device memory)
     __shared__ int skip;
     if (threadIdx.x == 0) {
@@ -504,7 +519,7 @@ __global__ void __launch_bounds__(kBlock) k_final(size_t m, double* u, CombineTe
 
 void final_update(size_t m, double* u, const CombineTerms& t, int* flag, cudaStream_t st, const int* gate,
                   int gate_count) {
-  k_final<<<wave(m), kBlock, 0, st>>>(m, u, t, flag, gate, gate ? gate_count : 0);
+  launch_pdl(k_final, dim3(wave(m)), dim3(kBlock), 0, st, m, u, t, flag, gate, gate ? gate_count : 0);
   LAUNCHED("final_update");
 }
 

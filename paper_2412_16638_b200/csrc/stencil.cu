@@ -19,6 +19,7 @@
 
 #include "comm.hpp"
 #include "launch.hpp"
+#include "pdl.cuh"
 #include "reduce.cuh"
 #include "tma.cuh"
 #include "vec.cuh"
@@ -592,6 +593,8 @@ __global__ void __launch_bounds__(TTHREADS)
     k_stencil_tma(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap lomap,
                   const __grid_constant__ CUtensorMap himap, int has_lo, int has_hi, int n, int nz, int kb, int ke,
                   int kc, typename Src::type s, typename Src::type g, Src src, Epi epi) {
+  pdl_wait();
+  pdl_trigger();
   using T = typename Src::type;
   using Raw = typename Src::raw;
   constexpr int PLANE = tma_slot_elems<Raw>();
@@ -766,8 +769,8 @@ void launch_tma(const StencilSpec& sp, const Src& src, const Epi& epi, int kb, i
   const CUtensorMap lomap = src.glo ? make_map(dt, src.glo, 2, dims2, str2, box2) : xmap;
   const CUtensorMap himap = src.ghi ? make_map(dt, src.ghi, 2, dims2, str2, box2) : xmap;
   const dim3 grid((unsigned)(n / TI), (unsigned)(n / TJ), gz);
-  k_stencil_tma<Src, Epi><<<grid, TTHREADS, smem, st>>>(xmap, lomap, himap, src.glo ? 1 : 0, src.ghi ? 1 : 0, n, nz, kb,
-                                                        ke, kc, (T)sp.sigma, (T)sp.gamma, src, epi);
+  launch_pdl(k_stencil_tma<Src, Epi>, grid, dim3(TTHREADS), smem, st, xmap, lomap, himap, src.glo ? 1 : 0,
+             src.ghi ? 1 : 0, n, nz, kb, ke, kc, (T)sp.sigma, (T)sp.gamma, src, epi);
   LAUNCHED(name);
 }
 

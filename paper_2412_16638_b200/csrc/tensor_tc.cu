@@ -30,6 +30,7 @@
 #include <cstdlib>
 
 #include "launch.hpp"
+#include "pdl.cuh"
 #include "tma.cuh"
 #include "vec.cuh"
 
@@ -517,6 +518,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  pdl_wait();  // everything below reads the previous kernel's output
+  pdl_trigger();
   const uint32_t tmem = S.tmem_base;
 
   if (warp == TC_PROD_WARP) {
@@ -819,8 +822,8 @@ void launch_tcf(int n, long cols, const float* x, float* out, const float* pd, c
   }
   const int num_tiles = (n / 2 / TF_BM) * col_tiles * planes;
   const int grid = num_tiles < sm_count() ? num_tiles : sm_count();
-  k_tensor_tcf<SIDE, PDIN><<<grid, TC_THREADS, smem, st>>>(map, pmap, omap, out, qpack, n, col_tiles, num_tiles,
-                                                           cols, dbg);
+  launch_pdl(k_tensor_tcf<SIDE, PDIN>, dim3(grid), dim3(TC_THREADS), smem, st, map, pmap, omap, out, qpack, n,
+             col_tiles, num_tiles, cols, dbg);
   LAUNCHED("tensor_tc_fold");
 }
 
