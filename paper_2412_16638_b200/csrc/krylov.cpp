@@ -3,6 +3,7 @@
 #include <array>
 #include <cmath>
 #include <complex>
+#include <cstdlib>
 #include <cstring>
 
 namespace mprkb {
@@ -181,7 +182,7 @@ T* KrylovWork<T>::basis(int j) {
 // ---------------------------------------------------------------------------
 template <class T>
 void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, KrylovWork<T>& w,
-              SolveReport& rep, cudaStream_t st, EventTimer* timer) {
+              SolveReport& rep, cudaStream_t st, EventTimer* timer, T* x_alt, T** result) {
   using R = real_t<T>;
   const size_t m = w.size();
   if (A.size() != m || (P && P->size() != m)) MPRKB_THROW(2, "cg: operator size != vector length");
@@ -227,6 +228,13 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
   // reference would have skipped only touches scratch vectors (never x).
   const bool batch = fast && S != nullptr;
   const bool spec_true = batch && P != nullptr && P->exact_inverse();
+  // ... and (fp32, undivided grid, a second solution buffer) the first
+  // update, ||r1|| and the true residual in one pass that leaves q unwritten
+  bool fuse_first = false;
+  if constexpr (std::is_same_v<T, float>) {
+    const char* env = std::getenv("MPRKB_CG_FUSED");  // (=0: the unfused kernels, for A/B tests)
+    fuse_first = spec_true && x_alt != nullptr && cg_fused_supported(*S) && !(env && env[0] == '0');
+  }
   const RedSlot s2 = w.red.slot(2), s3 = w.red.slot(3);
   double r0;
   R rz{}, pq_first{};
@@ -239,7 +247,7 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
     pre(r, z);
     {
       Bracket br(timer, "stencil", st);
-      stencil_apply_dot2<T>(*S, z, q, r, s2, st);  // q = A z, (z.q, r.z)
+      stencil_apply_dot2<T>(*S, z, fuse_first ? nullptr : q, r, s2, st);  // q = A z, (z.q, r.z)
     }
     stream_sync(st);
     double v[3];
@@ -289,11 +297,41 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
         break;
       }
       const R alpha = rz / pq;
-      cg_update<T>(m, alpha, x, p, r, q, fast ? &s0 : nullptr, st);
+      bool fused = false;
+      if constexpr (std::is_same_v<T, float>) {
+        if (fuse_first && k == 0) {
+          {
+            Bracket br(timer, "stencil", st);
+            cg_fused_update(*S, alpha, x, p, b, r, x_alt, s0, st);
+          }
+          std::swap(x, x_alt);
+          fused = true;
+        }
+      }
+      if (!fused) cg_update<T>(m, alpha, x, p, r, q, fast ? &s0 : nullptr, st);
       x_clean = false;
       ++rep.iterations;
       double rt_spec = -1.0;
-      if (spec_true) {
+      if (fused) {
+        double v[2];
+        stream_sync(st);
+        w.red.result(0, 2, v);
+        if (w.comm && w.comm->size() > 1) w.comm->allreduce_sum(v, 2);
+        rnorm = (double)std::sqrt((R)v[0]);
+        rt_spec = (double)std::sqrt((R)v[1]);
+        // the pass stored neither r1 nor the true residual: materialise the
+        // one the reference continues from
+        if (crit.satisfied(rnorm, r0)) {
+          if (!crit.satisfied(rt_spec, r0)) {
+            Bracket br(timer, "stencil", st);
+            stencil_residual<T>(*S, x, b, q, nullptr, st);
+          }
+        } else {
+          Bracket br(timer, "stencil", st);
+          stencil_apply<T>(*S, p, q, st);
+          cg_update<T>(m, alpha, z, p, r, q, nullptr, st);  // r -= alpha q (z is scratch here)
+        }
+      } else if (spec_true) {
         {
           Bracket br(timer, "stencil", st);
           stencil_residual<T>(*S, x, b, q, &s3, st);  // q is free after the update
@@ -331,6 +369,7 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
   // exit true residual (krylov.hpp:164-166): recomputing it for an unchanged
   // x would reproduce the same value, so reuse it.
   rep.true_residual = x_clean ? clean_true : (double)std::sqrt(residual(q));
+  if (result) *result = x;
 }
 
 // ---------------------------------------------------------------------------
@@ -530,9 +569,9 @@ template class KrylovWork<c32>;
 template class KrylovWork<c64>;
 
 template void cg_solve<float>(Op&, Op*, const float*, float*, const Crit&, Numerics, KrylovWork<float>&,
-                              SolveReport&, cudaStream_t, EventTimer*);
+                              SolveReport&, cudaStream_t, EventTimer*, float*, float**);
 template void cg_solve<double>(Op&, Op*, const double*, double*, const Crit&, Numerics, KrylovWork<double>&,
-                               SolveReport&, cudaStream_t, EventTimer*);
+                               SolveReport&, cudaStream_t, EventTimer*, double*, double**);
 #define INST_GMRES(T)                                                                                      \
   template void gmres_solve<T>(Op&, Op*, const T*, T*, const Crit&, Numerics, KrylovWork<T>&, SolveReport&, \
                                cudaStream_t, EventTimer*, int);

@@ -80,9 +80,14 @@ class KrylovWork {
   std::vector<DevBuf> basis_, basis16_;
 };
 
+// x_alt (optional): a second solution buffer.  With it the first iteration
+// may run the fused update + true-residual pass (stencil.cu k_cg_fused),
+// which writes x1 there; *result (optional) receives the buffer holding the
+// solution on return — x or x_alt.
 template <class T>
 void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, KrylovWork<T>& w,
-              SolveReport& rep, cudaStream_t st, EventTimer* timer = nullptr);
+              SolveReport& rep, cudaStream_t st, EventTimer* timer = nullptr, T* x_alt = nullptr,
+              T** result = nullptr);
 
 // basis_storage: -1 = the working precision T (the reference), 4 = fp16
 // Krylov basis (accessor-style storage, fp64-accumulated dots; extension).

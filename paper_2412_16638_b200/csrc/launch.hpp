@@ -36,9 +36,14 @@ void stencil_residual(const StencilSpec& s, const T* x, const T* b, T* r, const 
 // q = A p with fused p.q (dot_real) into red
 template <class T>
 void stencil_apply_dot(const StencilSpec& s, const T* p, T* q, const RedSlot& red, cudaStream_t st);
-// q = A p; red gets (p.q, r.p) — dot_real order of terms per point
+// q = A p (q may be null: dots only); red gets (p.q, r.p) — dot_real order of terms per point
 template <class T>
 void stencil_apply_dot2(const StencilSpec& s, const T* p, T* q, const T* r, const RedSlot& red, cudaStream_t st);
+// x1 = x + alpha p with (||r - alpha A p||^2, ||b - A x1||^2) in red; fp32,
+// Dirichlet, undivided grid (stencil.cu k_cg_fused)
+bool cg_fused_supported(const StencilSpec& s);
+void cg_fused_update(const StencilSpec& s, float alpha, const float* x, const float* p, const float* b, const float* r,
+                     float* x1, const RedSlot& red, cudaStream_t st);
 
 // apply_f (operators.cpp:81-96), F64 policy: out = K y + g, y read as double
 // or widened from float (`y32`, the fp32 stage solution, exact), g may be

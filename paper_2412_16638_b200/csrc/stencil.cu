@@ -245,7 +245,7 @@ struct EpiStoreDot2 {
   __device__ __forceinline__ Pre pre4(long i) const { return ld4rw(r + i); }
   __device__ __forceinline__ static double (&one(double& d))[1] { return *reinterpret_cast<double(*)[1]>(&d); }
   __device__ __forceinline__ void v4p(State& s, long i, const V4<T>& v, const V4<T>& xc, const Pre& rv) const {
-    st4(out + i, v);
+    if (out) st4(out + i, v);
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       dot_acc(one(s.v[0]), xc.x[e], v.x[e]);
@@ -256,7 +256,7 @@ struct EpiStoreDot2 {
     v4p(s, i, v, xc, pre4(i));
   }
   __device__ __forceinline__ void s1(State& s, long i, T v, T xc) const {
-    out[i] = v;
+    if (out) out[i] = v;
     dot_acc(one(s.v[0]), xc, v);
     dot_acc(one(s.v[1]), r[i], xc);
   }
@@ -933,6 +933,183 @@ void feval_combine(const StencilSpec& k, const float* y32, const FevalCombine& f
     e.hae[a] = f.hae[a];
   }
   launch(k, LdF2D{y32}, e, st, "feval_combine");
+}
+
+// ---- CG update fused with the true-residual check (fp32, TMA pipeline) -----------
+// One CG iteration ends (krylov.hpp:134-153) with x1 = x + a p, r1 = r - a A p,
+// ||r1|| and — for an exact-inverse preconditioner, where ||r1|| normally
+// triggers — the confirming true residual ||b - A x1||.  Unfused that is
+// q = A p (written), the update (x, p, r, q in; x, r out) and a residual
+// stencil over x1 (x1, b in; the residual out).  Here one pass streams the x
+// and p planes through the TMA ring, forms x1 at every loaded point (the same
+// rounding as the update kernel), evaluates A p and A x1 from the resident
+// neighbourhoods and writes only x1 — to a second buffer, since neighbouring
+// CTAs still read x.  r1 and the true residual are not stored: the caller
+// recomputes whichever it needs on the rare path that continues.
+constexpr int CG_SLOT = tma_slot_elems<float>();
+constexpr size_t cg_fused_smem() { return (size_t)TST * 2 * CG_SLOT * sizeof(float) + TST * sizeof(uint64_t) + 128; }
+
+__global__ void __launch_bounds__(TTHREADS)
+    k_cg_fused(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap pmap, int n, int nz,
+               int kc, float s, float g, float alpha, const float* __restrict__ b, const float* __restrict__ r,
+               float* __restrict__ x1, RedSlot red) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ unsigned char smem_raw[];
+  float* buf = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(buf + TST * 2 * CG_SLOT);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int i0 = blockIdx.x * TI, j0 = blockIdx.y * TJ;
+  int k0, k1;
+  plane_range(nz, 0, nz, kc, k0, k1);
+  const int planes = k1 - k0 + 2;
+  constexpr uint32_t bytes = (TJ + 2) * TW * sizeof(float);
+  if (tid == 0) {
+    for (int q = 0; q < TST; ++q) mbar_init(&full[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const CUtensorMap* xm = &xmap;
+  const CUtensorMap* pm = &pmap;
+  auto issue = [&](int q) {
+    const int k = k0 - 1 + q, sl = q % TST;
+    float* dst = buf + sl * 2 * CG_SLOT;
+    mbar_expect_tx(&full[sl], 2 * bytes);
+    tma_3d(dst, xm, i0 - 4, j0 - 1, k, &full[sl]);
+    tma_3d(dst + CG_SLOT, pm, i0 - 4, j0 - 1, k, &full[sl]);
+  };
+  if (tid == 0)
+    for (int q = 0; q < TST && q < planes; ++q) issue(q);
+  auto wait = [&](int q) { mbar_wait(&full[q % TST], (uint32_t)(q / TST) & 1u); };
+  auto ld = [](const float* p) {
+    const float4 f = *reinterpret_cast<const float4*>(p);
+    V4<float> v;
+    v.x[0] = f.x; v.x[1] = f.y; v.x[2] = f.z; v.x[3] = f.w;
+    return v;
+  };
+  auto upd = [&](float xv, float pv) { return xadd(xv, xscale(alpha, pv)); };  // k_cg_update's x
+  auto upd4 = [&](const V4<float>& xv, const V4<float>& pv) {
+    V4<float> o;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o.x[e] = upd(xv.x[e], pv.x[e]);
+    return o;
+  };
+  double acc[2] = {0.0, 0.0};  // ||r1||^2, ||b - A x1||^2
+  const long nn = n, n2 = nn * nn;
+  const int col = 4 + 4 * lane;
+  auto gidx = [&](int row, int k) { return (i0 + 4 * lane) + (long)(j0 + row) * nn + (long)k * n2; };
+  V4<float> pb[TROWS], pr[TROWS];
+#pragma unroll
+  for (int rr = 0; rr < TROWS; ++rr) {
+    pb[rr] = ld4rw(b + gidx(warp * TROWS + rr, k0));
+    pr[rr] = ld4rw(r + gidx(warp * TROWS + rr, k0));
+  }
+  for (int k = k0; k < k1; ++k) {
+    const int q = k - k0 + 1;
+    if (k == k0) {
+      wait(0);
+      wait(1);
+    }
+    wait(q + 1);
+    const float* xmn = buf + ((q - 1) % TST) * 2 * CG_SLOT;
+    const float* xc = buf + (q % TST) * 2 * CG_SLOT;
+    const float* xpl = buf + ((q + 1) % TST) * 2 * CG_SLOT;
+    V4<float> nb[TROWS], nr[TROWS];
+#pragma unroll
+    for (int rr = 0; rr < TROWS; ++rr)
+      if (k + 1 < k1) {
+        nb[rr] = ld4rw(b + gidx(warp * TROWS + rr, k + 1));
+        nr[rr] = ld4rw(r + gidx(warp * TROWS + rr, k + 1));
+      }
+#pragma unroll
+    for (int rr = 0; rr < TROWS; ++rr) {
+      const int row = warp * TROWS + rr;
+      const int o = (row + 1) * TW + col;
+      // p neighbourhood -> q = A p
+      const V4<float> pc = ld(xc + CG_SLOT + o);
+      const V4<float> pym = ld(xc + CG_SLOT + o - TW), pyp = ld(xc + CG_SLOT + o + TW);
+      const V4<float> pzm = ld(xmn + CG_SLOT + o), pzp = ld(xpl + CG_SLOT + o);
+      float pl = shfl_up1(pc.x[3]), pr_ = shfl_down1(pc.x[0]);
+      if (lane == 0) pl = xc[CG_SLOT + o - 1];
+      if (lane == 31) pr_ = xc[CG_SLOT + o + 4];
+      // x1 neighbourhood -> A x1
+      const V4<float> c = upd4(ld(xc + o), pc);
+      const V4<float> ym = upd4(ld(xc + o - TW), pym), yp = upd4(ld(xc + o + TW), pyp);
+      const V4<float> zm = upd4(ld(xmn + o), pzm), zp = upd4(ld(xpl + o), pzp);
+      float xl = shfl_up1(c.x[3]), xr = shfl_down1(c.x[0]);
+      if (lane == 0) xl = upd(xc[o - 1], pl);
+      if (lane == 31) xr = upd(xc[o + 4], pr_);
+      const long gi = gidx(row, k);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float ql = e == 0 ? pl : pc.x[e - 1], qr = e == 3 ? pr_ : pc.x[e + 1];
+        const float qv = point<float>(0, s, g, 0.0f, pc.x[e], ql, qr, pym.x[e], pyp.x[e], pzm.x[e], pzp.x[e]);
+        const float r1 = xsub(pr[rr].x[e], xscale(alpha, qv));  // k_cg_update's r
+        dot_acc(*reinterpret_cast<double(*)[1]>(&acc[0]), r1, r1);
+        const float al = e == 0 ? xl : c.x[e - 1], ar = e == 3 ? xr : c.x[e + 1];
+        const float av = point<float>(0, s, g, 0.0f, c.x[e], al, ar, ym.x[e], yp.x[e], zm.x[e], zp.x[e]);
+        const float t = xsub(pb[rr].x[e], av);  // EpiResidual's b - A x
+        dot_acc(*reinterpret_cast<double(*)[1]>(&acc[1]), t, t);
+      }
+      st4(x1 + gi, c);
+    }
+#pragma unroll
+    for (int rr = 0; rr < TROWS; ++rr) {
+      pb[rr] = nb[rr];
+      pr[rr] = nr[rr];
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0 && q - 1 + TST < planes) issue(q - 1 + TST);
+  }
+  grid_reduce<2>(acc, red);
+}
+
+bool cg_fused_supported(const StencilSpec& k) {
+  return k.stencil == 0 && k.n % TI == 0 && k.halo == nullptr && tma_stencil_enabled();
+}
+
+void cg_fused_update(const StencilSpec& sp, float alpha, const float* x, const float* p, const float* b,
+                     const float* r, float* x1, const RedSlot& red, cudaStream_t st) {
+  if (!cg_fused_supported(sp)) MPRKB_THROW(10, "cg_fused_update: needs the TMA stencil on an undivided grid");
+  const int n = sp.n, nz = sp.nz > 0 ? sp.nz : n;
+  constexpr size_t smem = cg_fused_smem();
+  static int chunk = 0;
+  static long chunk_cols = -1;
+  static int resident = 0;
+  if (!resident) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_cg_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_fused, TTHREADS, smem));
+    resident = std::max(1, per_sm) * sm_count();
+  }
+  const long cols = (long)(n / TI) * (n / TJ);
+  if (cols != chunk_cols) {  // wave-sized k-chunks (as tma_chunk)
+    long best_cost = -1;
+    for (int kc = 4; kc <= 64; kc *= 2) {
+      const long units = cols * ((nz + kc - 1) / kc);
+      const long cost = ((units + resident - 1) / resident) * (std::min(kc, nz) + 2);
+      if (best_cost < 0 || cost < best_cost) {
+        chunk = kc;
+        best_cost = cost;
+      }
+    }
+    chunk_cols = cols;
+  }
+  const cuuint64_t nn = (cuuint64_t)n;
+  const cuuint64_t dims3[3] = {nn, nn, (cuuint64_t)nz}, str3[2] = {nn * 4, nn * nn * 4};
+  const cuuint32_t box3[3] = {(cuuint32_t)TW, (cuuint32_t)(TJ + 2), 1};
+  const CUtensorMap xmap = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, x, 3, dims3, str3, box3);
+  const CUtensorMap pmap = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, p, 3, dims3, str3, box3);
+  const unsigned gz = (unsigned)((nz + chunk - 1) / chunk);
+  const dim3 grid((unsigned)(n / TI), (unsigned)(n / TJ), gz);
+  RedSlot rs = red;
+  rs.base = 0;
+  rs.total = 0;
+  launch_pdl(k_cg_fused, grid, dim3(TTHREADS), smem, st, xmap, pmap, n, nz, chunk, (float)sp.sigma, (float)sp.gamma,
+             alpha, b, r, x1, rs);
+  note_partials(rs, grid.x * grid.y * grid.z);
+  LAUNCHED("cg_fused_update");
 }
 
 #define INST_STENCIL(T)                                                                          \

@@ -117,8 +117,9 @@ Stepper::Stepper(const StepperConfig& cfg)
     if (fused_) {
       acc_.resize(q);
       for (int k = 2; k < q; ++k) acc_[k].alloc(m * sizeof(double));
-      xsol2_.alloc(m * sizeof(float));
     }
+    // second fp32 solution buffer: the fused first CG update writes beside x
+    if (cfg_.eq == Equation::Heat && cfg_.f32 && !slab_.split()) xsol2_.alloc(m * sizeof(float));
   }
   if (!solvers_.empty()) {
     const size_t s = dtype_size(solve_dtype_);
@@ -205,9 +206,11 @@ void Stepper::step(double* u, StepTrace& trace) {
       }
       SolveReport rep;
       EventTimer* tm = timer_.enabled() ? &timer_ : nullptr;
+      float* sol32 = xsol_.as<float>();
       switch (solve_dtype_) {
         case 0:
-          cg_solve<float>(*S.op, S.pre.get(), bsol_.as<float>(), xsol_.as<float>(), crit, cfg_.num, *w32_, rep, st_, tm);
+          cg_solve<float>(*S.op, S.pre.get(), bsol_.as<float>(), xsol_.as<float>(), crit, cfg_.num, *w32_, rep, st_, tm,
+                          xsol2_.get() ? xsol2_.as<float>() : nullptr, &sol32);
           break;
         case 1:
           cg_solve<double>(*S.op, S.pre.get(), bsol_.as<double>(), xsol_.as<double>(), crit, cfg_.num, *w64_, rep, st_, tm);
@@ -224,7 +227,7 @@ void Stepper::step(double* u, StepTrace& trace) {
       // which also carry check_finite); complex (advection) stages take the
       // real part first.
       if (solve_dtype_ == 0) {
-        ys32 = xsol_.as<float>();
+        ys32 = sol32;
       } else if (solve_dtype_ == 1) {
         ys = xsol_.as<double>();
       } else {
@@ -337,12 +340,18 @@ void Stepper::step_fused(double* u, StepTrace& trace) {
   float* xs[2] = {xsol_.as<float>(), xsol2_.as<float>()};
   float* b32 = bsol_.as<float>();
   EventTimer* tm = timer_.enabled() ? &timer_ : nullptr;
-  auto solve = [&](int i) {
+  // The stage solve starts from x0 in one buffer and may finish in the other
+  // (the fused first CG update writes x1 beside x); the f-evaluation pass
+  // reads the solution and writes the next stage's x0 into the free one.
+  auto solve = [&](int i, float* x0) -> float* {
     StageSolver& S = solvers_[solver_of_stage_[i]];
     SolveReport rep;
-    cg_solve<float>(*S.op, S.pre.get(), b32, xs[i & 1], crit, cfg_.num, *w32_, rep, st_, tm);
+    float* other = x0 == xs[0] ? xs[1] : xs[0];
+    float* sol = x0;
+    cg_solve<float>(*S.op, S.pre.get(), b32, x0, crit, cfg_.num, *w32_, rep, st_, tm, other, &sol);
     if (!rep.converged) trace.solver_failure = true;
     trace.solves.push_back(std::move(rep));
+    return sol;
   };
 
   // stage 0: rhs = u + tau a_00 g (stepper.cpp:157-172), x0 = rhs
@@ -352,7 +361,7 @@ void Stepper::step_fused(double* u, StepTrace& trace) {
     Bracket br(timer_, "axpy", st_);
     combine(m, u, terms, 1, b32, check_slot(6, kOverflow), st_, xs[0]);
   }
-  solve(0);
+  float* cur = solve(0, xs[0]);  // stage i's solution
   for (int i = 0; i + 1 < q; ++i) {
     const int nx = i + 1;
     FevalCombine f;
@@ -368,7 +377,8 @@ void Stepper::step_fused(double* u, StepTrace& trace) {
     f.hg = 1;
     f.cg = tau * t.ae(nx, nx);
     f.bout = b32;
-    f.xout = xs[nx & 1];
+    float* next_x0 = cur == xs[0] ? xs[1] : xs[0];
+    f.xout = next_x0;
     f.ovf_flag = check_slot(6, kOverflow);
     for (int k = nx + 1; k < q; ++k) {
       const int a = f.nacc++;
@@ -381,18 +391,18 @@ void Stepper::step_fused(double* u, StepTrace& trace) {
     }
     {
       Bracket br(timer_, "stencil", st_);
-      feval_combine(kspec_, xs[i & 1], f, st_);
+      feval_combine(kspec_, cur, f, st_);
     }
-    solve(nx);
+    cur = solve(nx, next_x0);
   }
   // last stage: its f_hi feeds only the final update
   {
     const int i = q - 1;
     if (t.b[i] != 0.0) {
       Bracket br(timer_, "stencil", st_);
-      apply_f64(kspec_, nullptr, xs[i & 1], g64_.as<double>(), f_hi_[i].as<double>(), check_slot(9, kStage), st_);
+      apply_f64(kspec_, nullptr, cur, g64_.as<double>(), f_hi_[i].as<double>(), check_slot(9, kStage), st_);
     } else {
-      extract_stage(m, 0, xs[i & 1], y_.as<double>(), check_slot(9, kStage), st_);
+      extract_stage(m, 0, cur, y_.as<double>(), check_slot(9, kStage), st_);
     }
   }
   const int stage_checks = next - 1;

@@ -323,3 +323,36 @@ def test_fused_stage_pipeline_bitwise(gpu, mp, ref, name):
         fused.step(a)
         plain.step(b)
     assert same_bits(a, b)
+
+
+@pytest.mark.parametrize("tol", [1e-3, 1e-7])
+def test_cg_fused_first_update(gpu, mp, tol):
+    """The first CG iteration with an exact-inverse preconditioner runs the
+    update, ||r1|| and the confirming true residual in one pass (stencil.cu
+    k_cg_fused) that writes x1 beside x: the stepped state is bitwise the
+    unfused kernels' (same update and stencil arithmetic), the iteration
+    counts agree, and the residual histories differ only by the reduction
+    order of the fp64 norms.  tol 1e-7 is below fp32 reach, so every solve
+    continues past the first iteration through the r1-recompute path."""
+    import os
+
+    t = mp.builtin("4s3pB")
+    n = 256 if tol > 1e-5 else 128
+    fused = mp.Stepper("heat", n, t, 0.01, tol, "f32", 12)
+    os.environ["MPRKB_CG_FUSED"] = "0"
+    try:
+        plain = mp.Stepper("heat", n, t, 0.01, tol, "f32", 12)
+        a, b = np.zeros(n ** 3), np.zeros(n ** 3)
+        for _ in range(2):
+            del os.environ["MPRKB_CG_FUSED"]
+            ta = fused.step(a)
+            os.environ["MPRKB_CG_FUSED"] = "0"
+            tb = plain.step(b)
+            assert ta["iterations"] == tb["iterations"]
+            for s in range(len(ta["iterations"])):
+                ha, hb = fused.history(s), plain.history(s)
+                assert len(ha) == len(hb)
+                np.testing.assert_allclose(ha, hb, rtol=1e-9)
+    finally:
+        os.environ.pop("MPRKB_CG_FUSED", None)
+    assert same_bits(a, b)
