@@ -344,6 +344,11 @@ __device__ __forceinline__ bool f32_overflows(double x) {
 }
 
 __device__ __forceinline__ V4<double> term4(const CombineTerms& t, int c, size_t i) {
+  if (t.is_f32[c] == 2) {
+    V4<double> v;
+    forcing4(t.gen, (long)i, v.x);
+    return v;
+  }
   if (t.is_f32[c]) {
     const V4<float> f = ld4(static_cast<const float*>(t.ptr[c]) + i);
     return {{(double)f.x[0], (double)f.x[1], (double)f.x[2], (double)f.x[3]}};
@@ -351,6 +356,7 @@ __device__ __forceinline__ V4<double> term4(const CombineTerms& t, int c, size_t
   return ld4(static_cast<const double*>(t.ptr[c]) + i);
 }
 __device__ __forceinline__ double term1(const CombineTerms& t, int c, size_t i) {
+  if (t.is_f32[c] == 2) return forcing1(t.gen, (long)i);
   return t.is_f32[c] ? (double)ldg(static_cast<const float*>(t.ptr[c]) + i) : ldg(static_cast<const double*>(t.ptr[c]) + i);
 }
 

@@ -92,4 +92,35 @@ template <class T> __host__ __device__ __forceinline__ T zero_v() { return T{}; 
 __host__ __device__ __forceinline__ double to_d(float v) { return (double)v; }
 __host__ __device__ __forceinline__ double to_d(double v) { return v; }
 
+// ---- regenerated forcing (types.hpp ForcingGen) ----------------------------------
+__device__ __forceinline__ void forcing_ijk(const ForcingGen& f, long idx, int& i, int& j, int& k) {
+  if (f.lg >= 0) {
+    i = (int)(idx & (f.n - 1));
+    j = (int)((idx >> f.lg) & (f.n - 1));
+    k = (int)(idx >> (2 * f.lg)) + f.k0;
+  } else {
+    const long nn = f.n;
+    i = (int)(idx % nn);
+    j = (int)((idx / nn) % nn);
+    k = (int)(idx / (nn * nn)) + f.k0;
+  }
+}
+__device__ __forceinline__ double forcing1(const ForcingGen& f, long idx) {
+  int i, j, k;
+  forcing_ijk(f, idx, i, j, k);
+  return __dmul_rn(__dmul_rn(__ldg(f.s + i), __ldg(f.s + j)), __ldg(f.s + k));
+}
+// idx % 4 == 0 and n % 4 == 0: the four points share j and k
+__device__ __forceinline__ void forcing4(const ForcingGen& f, long idx, double (&g)[4]) {
+  int i, j, k;
+  forcing_ijk(f, idx, i, j, k);
+  const double sjk_j = __ldg(f.s + j), sk = __ldg(f.s + k);
+  const double2 a = __ldg(reinterpret_cast<const double2*>(f.s + i));
+  const double2 b = __ldg(reinterpret_cast<const double2*>(f.s + i) + 1);
+  g[0] = __dmul_rn(__dmul_rn(a.x, sjk_j), sk);
+  g[1] = __dmul_rn(__dmul_rn(a.y, sjk_j), sk);
+  g[2] = __dmul_rn(__dmul_rn(b.x, sjk_j), sk);
+  g[3] = __dmul_rn(__dmul_rn(b.y, sjk_j), sk);
+}
+
 }  // namespace mprkb

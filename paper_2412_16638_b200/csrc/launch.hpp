@@ -23,6 +23,7 @@ struct StencilSpec {
   double gamma2 = 0.0;  // second (diffusion) scale for stencil 2
   int nz = 0;           // local k-planes (0: the whole grid, n)
   const Halo* halo = nullptr;  // split grid: exchange ghost planes before every apply
+  ForcingGen forcing;          // apply_f / feval_combine: regenerate g instead of reading it
   size_t size() const { return (size_t)n * n * (nz > 0 ? nz : n); }
 };
 
@@ -192,7 +193,8 @@ struct CombineTerms {
   int count = 0;
   double coef[kMaxTerms];
   const void* ptr[kMaxTerms];
-  int is_f32[kMaxTerms];
+  int is_f32[kMaxTerms];  // 0 double, 1 float, 2 the regenerated forcing (gen; ptr unused)
+  ForcingGen gen;
 };
 // rhs = u + sum_t coef_t * v_t (one axpy per term, in order), written as:
 // out_kind 0: double (+ finite flag), 1: float (downcast, overflow flag),

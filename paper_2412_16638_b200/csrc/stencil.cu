@@ -268,10 +268,18 @@ struct EpiF64Forcing {
   const double* g;
   double* out;
   int* finite_flag;  // check_finite(y) on the centre values (nullable)
+  ForcingGen gen;    // g regenerated (types.hpp) when gen.s is set
   struct State {};
   using Pre = V4<double>;
   __device__ void init(State&) const {}
-  __device__ __forceinline__ Pre pre4(long i) const { return g ? ld4(g + i) : zero4<double>(); }
+  __device__ __forceinline__ Pre pre4(long i) const {
+    if (g && gen.s) {
+      V4<double> v;
+      forcing4(gen, i, v.x);
+      return v;
+    }
+    return g ? ld4(g + i) : zero4<double>();
+  }
   __device__ __forceinline__ void v4p(State&, long i, const V4<double>& v, const V4<double>& xc,
                                       const Pre& gv) const {
     if (finite_flag && !(isfinite(xc.x[0]) && isfinite(xc.x[1]) && isfinite(xc.x[2]) && isfinite(xc.x[3])))
@@ -290,7 +298,7 @@ struct EpiF64Forcing {
   }
   __device__ __forceinline__ void s1(State&, long i, double v, double xc) const {
     if (finite_flag && !isfinite(xc)) *finite_flag = 1;
-    out[i] = g ? xadd(v, ldg(g + i)) : v;
+    out[i] = g ? xadd(v, gen.s ? forcing1(gen, i) : ldg(g + i)) : v;
   }
   __device__ void finish(State&) const {}
 };
@@ -300,10 +308,21 @@ struct EpiF32Forcing {
   const float* g32;
   float* out;
   int* finite_flag;  // check_finite(y) on the centre values (nullable)
+  ForcingGen gen;    // g32 = narrow(g) regenerated when gen.s is set
   struct State {};
   using Pre = V4<float>;
   __device__ void init(State&) const {}
-  __device__ __forceinline__ Pre pre4(long i) const { return g32 ? ld4(g32 + i) : zero4<float>(); }
+  __device__ __forceinline__ Pre pre4(long i) const {
+    if (g32 && gen.s) {
+      double d[4];
+      forcing4(gen, i, d);
+      V4<float> v;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v.x[e] = __double2float_rn(d[e]);
+      return v;
+    }
+    return g32 ? ld4(g32 + i) : zero4<float>();
+  }
   __device__ __forceinline__ void v4p(State&, long i, const V4<float>& v, const V4<float>& xc,
                                       const Pre& gv) const {
     if (finite_flag && !(isfinite(xc.x[0]) && isfinite(xc.x[1]) && isfinite(xc.x[2]) && isfinite(xc.x[3])))
@@ -322,7 +341,7 @@ struct EpiF32Forcing {
   }
   __device__ __forceinline__ void s1(State&, long i, float v, float xc) const {
     if (finite_flag && !isfinite(xc)) *finite_flag = 1;
-    out[i] = g32 ? xadd(v, ldg(g32 + i)) : v;
+    out[i] = g32 ? xadd(v, gen.s ? __double2float_rn(forcing1(gen, i)) : ldg(g32 + i)) : v;
   }
   __device__ void finish(State&) const {}
 };
@@ -343,6 +362,7 @@ struct EpiFevalCombine {
   float s32 = 0.f, g32k = 0.f;    // the binary32 stencil's sigma / gamma
   const double* g = nullptr;      // forcing
   const float* g32 = nullptr;     // narrowed forcing
+  ForcingGen gen;                 // both regenerated when gen.s is set
   double* fhi = nullptr;          // f_hi output (nullable)
   int* finite_flag = nullptr;     // check_finite(y) (nullable)
   const double* sin = nullptr;    // S_{i+1} (u on the first stage)
@@ -362,7 +382,17 @@ struct EpiFevalCombine {
     V4<float> g32;
   };
   __device__ void init(State&) const {}
-  __device__ __forceinline__ Pre pre4(long i) const { return Pre{ld4(g + i), ld4(sin + i), ld4(g32 + i)}; }
+  __device__ __forceinline__ Pre pre4(long i) const {
+    if (gen.s) {
+      Pre p;
+      forcing4(gen, i, p.g.x);
+      p.s = ld4(sin + i);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) p.g32.x[e] = __double2float_rn(p.g.x[e]);
+      return p;
+    }
+    return Pre{ld4(g + i), ld4(sin + i), ld4(g32 + i)};
+  }
   __device__ __forceinline__ void v4dual(State&, long i, const V4<double>& v64, const V4<float>& v32,
                                          const V4<double>& xc, const Pre& p) const {
     if (finite_flag && !(isfinite(xc.x[0]) && isfinite(xc.x[1]) && isfinite(xc.x[2]) && isfinite(xc.x[3])))
@@ -890,17 +920,17 @@ void stencil_apply_dot2(const StencilSpec& s, const T* p, T* q, const T* r, cons
 void apply_f64(const StencilSpec& k, const double* y, const float* y32, const double* g, double* out,
                int* finite_flag, cudaStream_t st) {
   if (y32)
-    launch(k, LdF2D{y32}, EpiF64Forcing{g, out, finite_flag}, st, "apply_f64");
+    launch(k, LdF2D{y32}, EpiF64Forcing{g, out, finite_flag, k.forcing}, st, "apply_f64");
   else
-    launch(k, LdPlain<double>{y}, EpiF64Forcing{g, out, finite_flag}, st, "apply_f64");
+    launch(k, LdPlain<double>{y}, EpiF64Forcing{g, out, finite_flag, k.forcing}, st, "apply_f64");
 }
 
 void apply_f32(const StencilSpec& k, const double* y, const float* y32, const float* g32, float* out32, int* flag,
                int* finite_flag, cudaStream_t st) {
   if (y32)
-    launch(k, LdPlain<float>{y32}, EpiF32Forcing{g32, out32, finite_flag}, st, "apply_f32");
+    launch(k, LdPlain<float>{y32}, EpiF32Forcing{g32, out32, finite_flag, k.forcing}, st, "apply_f32");
   else
-    launch(k, LdD2F{y, flag}, EpiF32Forcing{g32, out32, finite_flag}, st, "apply_f32");
+    launch(k, LdD2F{y, flag}, EpiF32Forcing{g32, out32, finite_flag, k.forcing}, st, "apply_f32");
 }
 
 bool feval_combine_supported(const StencilSpec& k) {
@@ -915,6 +945,7 @@ void feval_combine(const StencilSpec& k, const float* y32, const FevalCombine& f
   e.g32k = (float)k.gamma;
   e.g = f.g;
   e.g32 = f.g32;
+  e.gen = k.forcing;
   e.fhi = f.fhi;
   e.finite_flag = f.finite_flag;
   e.sin = f.sin;

@@ -59,9 +59,12 @@ class Stepper {
   // fused with the next stage's right-hand side (EpiFevalCombine); later
   // stages' couplings accumulate in acc_ (see step_fused)
   void step_fused(double* u, StepTrace& trace);
+  void add_forcing(CombineTerms& t, double coef) const;  // + coef g (regenerated or read)
   bool fused_ = false;
   std::vector<DevBuf> acc_;
   DevBuf xsol2_;
+  DevBuf gtab_;     // sin table of the regenerated heat forcing
+  ForcingGen gen_;  // (types.hpp) s == nullptr: g is read from g64_ / g32_
   StepperConfig cfg_;
   Slab slab_;
   std::unique_ptr<Halo> halo_;  // split grid only

@@ -100,4 +100,16 @@ inline void note_partials(const RedSlot& r, unsigned tuples) {
 }
 constexpr int kMaxPartials = 1 << 16;
 
+// The heat forcing g[i + j n + k n^2] = (s_i s_j) s_k, s_t = sin(pi t h)
+// (problem.cpp, the reference's make_problem), regenerated in the kernels from
+// the n-entry table instead of streamed from HBM (12 bytes per point per f
+// evaluation): the same two roundings, so bitwise the stored vector — the
+// stepper verifies that on the host before enabling it.  s == nullptr: off.
+struct ForcingGen {
+  const double* s = nullptr;  // device table, global t = 0 .. n-1
+  int n = 0;
+  int lg = -1;  // log2 n when n is a power of two
+  int k0 = 0;   // first global plane of this slab
+};
+
 }  // namespace mprkb

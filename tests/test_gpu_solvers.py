@@ -356,3 +356,35 @@ def test_cg_fused_first_update(gpu, mp, tol):
     finally:
         os.environ.pop("MPRKB_CG_FUSED", None)
     assert same_bits(a, b)
+
+
+@pytest.mark.parametrize("name,prec,fused", [("4s3pB", "f32", True), ("4s3pA", "f32", False), ("4s3pB", "f64", False)])
+def test_regenerated_forcing_bitwise(gpu, mp, name, prec, fused):
+    """Heat steppers regenerate the forcing g = (s_i s_j) s_k from its sine
+    table inside the f-evaluation / combination kernels instead of streaming
+    the stored vector: the stepped states are bitwise those of the stored-g
+    kernels (MPRKB_FORCING_GEN=0), through the fused stage pipeline, the
+    unfused fp32 path and the fp64 path."""
+    import os
+
+    t = mp.builtin(name)
+    n = 128
+    gen = mp.Stepper("heat", n, t, 0.01, 1e-4 if prec == "f32" else 1e-8, prec, 40)
+    os.environ["MPRKB_FORCING_GEN"] = "0"
+    if not fused:
+        os.environ["MPRKB_FUSED_STAGES"] = "0"
+    try:
+        plain = mp.Stepper("heat", n, t, 0.01, 1e-4 if prec == "f32" else 1e-8, prec, 40)
+    finally:
+        os.environ.pop("MPRKB_FORCING_GEN", None)
+        os.environ.pop("MPRKB_FUSED_STAGES", None)
+    if not fused:
+        os.environ["MPRKB_FUSED_STAGES"] = "0"
+        try:
+            gen = mp.Stepper("heat", n, t, 0.01, 1e-4 if prec == "f32" else 1e-8, prec, 40)
+        finally:
+            os.environ.pop("MPRKB_FUSED_STAGES", None)
+    a, b = np.zeros(n ** 3), np.zeros(n ** 3)
+    for _ in range(3):
+        assert gen.step(a)["iterations"] == plain.step(b)["iterations"]
+    assert same_bits(a, b)
