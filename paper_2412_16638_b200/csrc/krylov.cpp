@@ -235,6 +235,16 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
     const char* env = std::getenv("MPRKB_CG_FUSED");  // (=0: the unfused kernels, for A/B tests)
     fuse_first = spec_true && x_alt != nullptr && cg_fused_supported(*S) && !(env && env[0] == '0');
   }
+  // x may alias b (x0 = rhs without a copy) only with a second buffer: the
+  // fused first update writes beside it; otherwise x0 is copied there first
+  if (x == b) {
+    if (!x_alt) MPRKB_THROW(2, "cg: x aliases b without a second solution buffer");
+    if (!fuse_first) {
+      CUDA_CHECK(cudaMemcpyAsync(x_alt, b, m * sizeof(T), cudaMemcpyDeviceToDevice, st));
+      x = x_alt;
+      x_alt = nullptr;
+    }
+  }
   const RedSlot s2 = w.red.slot(2), s3 = w.red.slot(3);
   double r0;
   R rz{}, pq_first{};
@@ -369,6 +379,10 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
   // exit true residual (krylov.hpp:164-166): recomputing it for an unchanged
   // x would reproduce the same value, so reuse it.
   rep.true_residual = x_clean ? clean_true : (double)std::sqrt(residual(q));
+  if (x == b) {  // converged at x0 = b: the solution leaves the rhs buffer
+    CUDA_CHECK(cudaMemcpyAsync(x_alt, b, m * sizeof(T), cudaMemcpyDeviceToDevice, st));
+    x = x_alt;
+  }
   if (result) *result = x;
 }
 

@@ -83,7 +83,8 @@ class KrylovWork {
 // x_alt (optional): a second solution buffer.  With it the first iteration
 // may run the fused update + true-residual pass (stencil.cu k_cg_fused),
 // which writes x1 there; *result (optional) receives the buffer holding the
-// solution on return — x or x_alt.
+// solution on return — x or x_alt.  x == b is allowed with x_alt (the
+// initial guess is the right-hand side; b is never written).
 template <class T>
 void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, KrylovWork<T>& w,
               SolveReport& rep, cudaStream_t st, EventTimer* timer = nullptr, T* x_alt = nullptr,

@@ -414,7 +414,7 @@ struct EpiFevalCombine {
     }
     if (fhi) st4(fhi + i, fh);
     st4(bout + i, b);
-    st4(xout + i, b);
+    if (xout) st4(xout + i, b);
     if (ovf) *ovf_flag = 1;
     for (int a = 0; a < nacc; ++a) {
       V4<double> s = ld4(ain[a] + i);

@@ -161,9 +161,6 @@ Stepper::Stepper(const StepperConfig& cfg)
       acc_.resize(q);
       for (int k = 2; k < q; ++k) acc_[k].alloc(m * sizeof(double));
     }
-    // second fp32 solution buffer: the fused first CG update writes beside x
-    // (and the fused pipeline's ping-pong partner)
-    if (fused_ || (cfg_.eq == Equation::Heat && cfg_.f32 && !slab_.split())) xsol2_.alloc(m * sizeof(float));
   }
   if (!solvers_.empty()) {
     const size_t s = dtype_size(solve_dtype_);
@@ -246,15 +243,16 @@ void Stepper::step(double* u, StepTrace& trace) {
       {
         // x0 = narrowed rhs (stepper.cpp:111, 120, 135, 146), written by the same pass
         Bracket br(timer_, "axpy", st_);
-        combine(m, u, terms, out_kind, bsol_.get(), flag, st_, xsol_.get());
+        combine(m, u, terms, out_kind, bsol_.get(), flag, st_, solve_dtype_ == 0 ? nullptr : xsol_.get());
       }
       SolveReport rep;
       EventTimer* tm = timer_.enabled() ? &timer_ : nullptr;
       float* sol32 = xsol_.as<float>();
       switch (solve_dtype_) {
         case 0:
-          cg_solve<float>(*S.op, S.pre.get(), bsol_.as<float>(), xsol_.as<float>(), crit, cfg_.num, *w32_, rep, st_, tm,
-                          xsol2_.get() ? xsol2_.as<float>() : nullptr, &sol32);
+          // x0 = rhs in place (b is never written); the solution lands in xsol_
+          cg_solve<float>(*S.op, S.pre.get(), bsol_.as<float>(), bsol_.as<float>(), crit, cfg_.num, *w32_, rep, st_,
+                          tm, xsol_.as<float>(), &sol32);
           break;
         case 1:
           cg_solve<double>(*S.op, S.pre.get(), bsol_.as<double>(), xsol_.as<double>(), crit, cfg_.num, *w64_, rep, st_, tm);
@@ -381,18 +379,20 @@ void Stepper::step_fused(double* u, StepTrace& trace) {
   const Crit crit{cfg_.tol, cfg_.max_iter};
   const char* kOverflow = "downcast: value exceeds the binary32 range";
   const char* kStage = "stage vector picked up a NaN or infinity";
-  float* xs[2] = {xsol_.as<float>(), xsol2_.as<float>()};
+  float* xs[1] = {xsol_.as<float>()};
   float* b32 = bsol_.as<float>();
   EventTimer* tm = timer_.enabled() ? &timer_ : nullptr;
   // The stage solve starts from x0 in one buffer and may finish in the other
   // (the fused first CG update writes x1 beside x); the f-evaluation pass
   // reads the solution and writes the next stage's x0 into the free one.
-  auto solve = [&](int i, float* x0) -> float* {
+  // x0 = rhs is the rhs buffer itself (the solver never writes b); the
+  // solution lands in xs[0], free again once the previous stage's f
+  // evaluations have read it.
+  auto solve = [&](int i) -> float* {
     StageSolver& S = solvers_[solver_of_stage_[i]];
     SolveReport rep;
-    float* other = x0 == xs[0] ? xs[1] : xs[0];
-    float* sol = x0;
-    cg_solve<float>(*S.op, S.pre.get(), b32, x0, crit, cfg_.num, *w32_, rep, st_, tm, other, &sol);
+    float* sol = nullptr;
+    cg_solve<float>(*S.op, S.pre.get(), b32, b32, crit, cfg_.num, *w32_, rep, st_, tm, xs[0], &sol);
     if (!rep.converged) trace.solver_failure = true;
     trace.solves.push_back(std::move(rep));
     return sol;
@@ -403,9 +403,9 @@ void Stepper::step_fused(double* u, StepTrace& trace) {
     CombineTerms terms;
     add_forcing(terms, tau * t.ae(0, 0));
     Bracket br(timer_, "axpy", st_);
-    combine(m, u, terms, 1, b32, check_slot(6, kOverflow), st_, xs[0]);
+    combine(m, u, terms, 1, b32, check_slot(6, kOverflow), st_);
   }
-  float* cur = solve(0, xs[0]);  // stage i's solution
+  float* cur = solve(0);  // stage i's solution
   for (int i = 0; i + 1 < q; ++i) {
     const int nx = i + 1;
     FevalCombine f;
@@ -421,8 +421,7 @@ void Stepper::step_fused(double* u, StepTrace& trace) {
     f.hg = 1;
     f.cg = tau * t.ae(nx, nx);
     f.bout = b32;
-    float* next_x0 = cur == xs[0] ? xs[1] : xs[0];
-    f.xout = next_x0;
+    f.xout = nullptr;  // x0 = rhs: the solver starts from b itself
     f.ovf_flag = check_slot(6, kOverflow);
     for (int k = nx + 1; k < q; ++k) {
       const int a = f.nacc++;
@@ -437,7 +436,7 @@ void Stepper::step_fused(double* u, StepTrace& trace) {
       Bracket br(timer_, "stencil", st_);
       feval_combine(kspec_, cur, f, st_);
     }
-    cur = solve(nx, next_x0);
+    cur = solve(nx);
   }
   // last stage: its f_hi feeds only the final update
   {

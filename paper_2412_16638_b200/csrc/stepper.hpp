@@ -62,7 +62,6 @@ class Stepper {
   void add_forcing(CombineTerms& t, double coef) const;  // + coef g (regenerated or read)
   bool fused_ = false;
   std::vector<DevBuf> acc_;
-  DevBuf xsol2_;
   DevBuf gtab_;     // sin table of the regenerated heat forcing
   ForcingGen gen_;  // (types.hpp) s == nullptr: g is read from g64_ / g32_
   StepperConfig cfg_;
