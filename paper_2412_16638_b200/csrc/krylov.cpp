@@ -245,10 +245,11 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
       x_alt = nullptr;
     }
   }
-  const RedSlot s2 = w.red.slot(2), s3 = w.red.slot(3);
+  const RedSlot s2 = fuse_first ? w.red.slot_dev(2) : w.red.slot(2), s3 = w.red.slot(3);
   double r0;
   R rz{}, pq_first{};
   bool have_pq = false;
+  double fused_v[2] = {0.0, 0.0};  // (||r1||^2, ||b - A x1||^2) of the fused first update
   if (batch) {
     {
       Bracket br(timer, "stencil", st);
@@ -259,10 +260,20 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
       Bracket br(timer, "stencil", st);
       stencil_apply_dot2<T>(*S, z, fuse_first ? nullptr : q, r, s2, st);  // q = A z, (z.q, r.z)
     }
+    if constexpr (std::is_same_v<T, float>) {
+      if (fuse_first) {
+        // the first update speculatively, alpha formed on the device from the
+        // tuples above: it only writes x_alt, so whatever the host decides
+        // below (r0 already small, breakdown) x is untouched
+        Bracket br(timer, "stencil", st);
+        cg_fused_update(*S, 0.0f, &s2, x, z, b, r, x_alt, s3, st);
+      }
+    }
     stream_sync(st);
     double v[3];
     w.red.result(0, 1, &v[0]);
     w.red.result(2, 2, &v[1]);
+    if (fuse_first) w.red.result(3, 2, fused_v);
     if (w.comm && w.comm->size() > 1) w.comm->allreduce_sum(v, 3);
     r0 = (double)std::sqrt((R)v[0]);
     rz = (R)v[2];
@@ -309,11 +320,7 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
       const R alpha = rz / pq;
       bool fused = false;
       if constexpr (std::is_same_v<T, float>) {
-        if (fuse_first && k == 0) {
-          {
-            Bracket br(timer, "stencil", st);
-            cg_fused_update(*S, alpha, x, p, b, r, x_alt, s0, st);
-          }
+        if (fuse_first && k == 0) {  // already ran (above), with this alpha
           std::swap(x, x_alt);
           fused = true;
         }
@@ -323,12 +330,8 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
       ++rep.iterations;
       double rt_spec = -1.0;
       if (fused) {
-        double v[2];
-        stream_sync(st);
-        w.red.result(0, 2, v);
-        if (w.comm && w.comm->size() > 1) w.comm->allreduce_sum(v, 2);
-        rnorm = (double)std::sqrt((R)v[0]);
-        rt_spec = (double)std::sqrt((R)v[1]);
+        rnorm = (double)std::sqrt((R)fused_v[0]);
+        rt_spec = (double)std::sqrt((R)fused_v[1]);
         // the pass stored neither r1 nor the true residual: materialise the
         // one the reference continues from
         if (crit.satisfied(rnorm, r0)) {

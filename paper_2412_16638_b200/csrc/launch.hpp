@@ -43,8 +43,10 @@ void stencil_apply_dot2(const StencilSpec& s, const T* p, T* q, const T* r, cons
 // x1 = x + alpha p with (||r - alpha A p||^2, ||b - A x1||^2) in red; fp32,
 // Dirichlet, undivided grid (stencil.cu k_cg_fused)
 bool cg_fused_supported(const StencilSpec& s);
-void cg_fused_update(const StencilSpec& s, float alpha, const float* x, const float* p, const float* b, const float* r,
-                     float* x1, const RedSlot& red, cudaStream_t st);
+// alpha_src (nullable): take alpha = (float)rz / (float)pq from that slot's
+// device tuples (components pq, rz — stencil_apply_dot2 into a slot_dev slot)
+void cg_fused_update(const StencilSpec& s, float alpha, const RedSlot* alpha_src, const float* x, const float* p,
+                     const float* b, const float* r, float* x1, const RedSlot& red, cudaStream_t st);
 
 // apply_f (operators.cpp:81-96), F64 policy: out = K y + g, y read as double
 // or widened from float (`y32`, the fp32 stage solution, exact), g may be

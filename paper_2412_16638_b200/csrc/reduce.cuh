@@ -57,7 +57,28 @@ __device__ __forceinline__ void grid_reduce(double (&v)[NV], const RedSlot& s) {
   block_sum<NV>(v);
   if (tid == 0)
 #pragma unroll
-    for (int c = 0; c < NV; ++c) s.partial[(size_t)bid * 2 + c] = v[c];
+    for (int c = 0; c < NV; ++c) {
+      s.partial[(size_t)bid * 2 + c] = v[c];
+      if (s.dpart) s.dpart[(size_t)bid * 2 + c] = v[c];
+    }
+}
+
+// Component c of a reduction's n device tuples in the host's order (types.hpp
+// kRedLanes); called by all threads of a kRedLanes-thread block, result in
+// every thread.
+__device__ __forceinline__ double sum_partials(const double* dp, int n, int c) {
+  __shared__ double lanes[kRedLanes];
+  const int t = threadIdx.x;
+  __syncthreads();
+  if (t < kRedLanes) {
+    double s = 0.0;
+    for (int b = t; b < n; b += kRedLanes) s += __ldcg(dp + 2 * (size_t)b + c);
+    lanes[t] = s;
+  }
+  __syncthreads();
+  double tot = 0.0;
+  for (int l = 0; l < kRedLanes; ++l) tot += lanes[l];
+  return tot;
 }
 
 // ---- per-element dot contributions in fp64 --------------------------------------

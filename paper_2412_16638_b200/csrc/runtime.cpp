@@ -71,6 +71,7 @@ Reducer::Reducer(int slots) : slots_(slots) {
   CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&partial_), sizeof(double) * 2 * kMaxPartials * slots,
                            cudaHostAllocMapped));
   CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&host_), sizeof(double) * 2 * slots, cudaHostAllocMapped));
+  CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(&dpart_), sizeof(double) * 2 * kMaxPartials * slots));
   std::memset(host_, 0, sizeof(double) * 2 * slots);
   count_ = new int[slots]();
 }
@@ -78,6 +79,7 @@ Reducer::Reducer(int slots) : slots_(slots) {
 Reducer::~Reducer() {
   if (partial_) cudaFreeHost(partial_);
   if (host_) cudaFreeHost(host_);
+  if (dpart_) cudaFree(dpart_);
   delete[] count_;
 }
 
@@ -92,6 +94,12 @@ RedSlot Reducer::slot(int i) const {
   return s;
 }
 
+RedSlot Reducer::slot_dev(int i) const {
+  RedSlot s = slot(i);
+  s.dpart = dpart_ + (size_t)2 * kMaxPartials * i;
+  return s;
+}
+
 void Reducer::result(int i, int nv, double* v) const {
   const int n = count_[i];
   if (n <= 0) {
@@ -100,9 +108,15 @@ void Reducer::result(int i, int nv, double* v) const {
   }
   const volatile double* p = partial_ + (size_t)2 * kMaxPartials * i;
   for (int c = 0; c < nv; ++c) {
-    double s = 0.0;
-    for (int b = 0; b < n; ++b) s += p[(size_t)2 * b + c];
-    v[c] = s;
+    double lanes[kRedLanes];
+    for (int t = 0; t < kRedLanes; ++t) {
+      double s = 0.0;
+      for (int b = t; b < n; b += kRedLanes) s += p[(size_t)2 * b + c];
+      lanes[t] = s;
+    }
+    double tot = 0.0;
+    for (int t = 0; t < kRedLanes; ++t) tot += lanes[t];
+    v[c] = tot;
   }
 }
 

@@ -50,6 +50,7 @@ class Reducer {
   Reducer(const Reducer&) = delete;
   Reducer& operator=(const Reducer&) = delete;
   RedSlot slot(int i) const;
+  RedSlot slot_dev(int i) const;  // + a device copy of the tuples (RedSlot::dpart)
   // after a stream synchronize: the reduction's nv value(s), partial tuples
   // added in CTA order
   void result(int i, int nv, double* v) const;
@@ -59,6 +60,7 @@ class Reducer {
   double* partial_ = nullptr;  // host pointer (mapped)
   double* host_ = nullptr;     // result pairs (mapped)
   int* count_ = nullptr;       // host only
+  double* dpart_ = nullptr;    // device tuple copies (slot_dev)
 };
 
 // Device error flags (non-finite / overflow) with host-mapped mirror.

@@ -982,10 +982,17 @@ constexpr size_t cg_fused_smem() { return (size_t)TST * 2 * CG_SLOT * sizeof(flo
 
 __global__ void __launch_bounds__(TTHREADS)
     k_cg_fused(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap pmap, int n, int nz,
-               int kc, float s, float g, float alpha, const float* __restrict__ b, const float* __restrict__ r,
-               float* __restrict__ x1, RedSlot red) {
+               int kc, float s, float g, float alpha, const double* apart, int an, const float* __restrict__ b,
+               const float* __restrict__ r, float* __restrict__ x1, RedSlot red) {
   pdl_wait();
   pdl_trigger();
+  if (apart) {
+    // alpha = r.z / p.Ap from the previous pass's tuples, summed and rounded
+    // as the host does (krylov.cpp: (R)rz / (R)pq), so no host round trip
+    // sits between the two kernels
+    const double pq = sum_partials(apart, an, 0), rz = sum_partials(apart, an, 1);
+    alpha = __fdiv_rn(__double2float_rn(rz), __double2float_rn(pq));
+  }
   extern __shared__ unsigned char smem_raw[];
   float* buf = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
   uint64_t* full = reinterpret_cast<uint64_t*>(buf + TST * 2 * CG_SLOT);
@@ -1100,8 +1107,8 @@ bool cg_fused_supported(const StencilSpec& k) {
   return k.stencil == 0 && k.n % TI == 0 && k.halo == nullptr && tma_stencil_enabled();
 }
 
-void cg_fused_update(const StencilSpec& sp, float alpha, const float* x, const float* p, const float* b,
-                     const float* r, float* x1, const RedSlot& red, cudaStream_t st) {
+void cg_fused_update(const StencilSpec& sp, float alpha, const RedSlot* alpha_src, const float* x, const float* p,
+                     const float* b, const float* r, float* x1, const RedSlot& red, cudaStream_t st) {
   if (!cg_fused_supported(sp)) MPRKB_THROW(10, "cg_fused_update: needs the TMA stencil on an undivided grid");
   const int n = sp.n, nz = sp.nz > 0 ? sp.nz : n;
   constexpr size_t smem = cg_fused_smem();
@@ -1137,8 +1144,11 @@ void cg_fused_update(const StencilSpec& sp, float alpha, const float* x, const f
   RedSlot rs = red;
   rs.base = 0;
   rs.total = 0;
+  const double* apart = alpha_src ? alpha_src->dpart : nullptr;
+  const int an = alpha_src ? *alpha_src->count : 0;
+  if (alpha_src && (!apart || an <= 0)) MPRKB_THROW(10, "cg_fused_update: alpha source has no device tuples");
   launch_pdl(k_cg_fused, grid, dim3(TTHREADS), smem, st, xmap, pmap, n, nz, chunk, (float)sp.sigma, (float)sp.gamma,
-             alpha, b, r, x1, rs);
+             alpha, apart, an, b, r, x1, rs);
   note_partials(rs, grid.x * grid.y * grid.z);
   LAUNCHED("cg_fused_update");
 }

@@ -94,7 +94,13 @@ struct RedSlot {
   // one reduction spread over several launches (interior + boundary planes of
   // a split-grid stencil): this launch's CTAs are tuples [base, base + gridDim)
   unsigned base = 0, total = 0;
+  double* dpart = nullptr;     // optional device copy of the tuples (a kernel downstream sums them)
 };
+// Partial tuples are summed in one fixed order on host and device alike:
+// kRedLanes interleaved running sums (lane t adds tuples t, t + kRedLanes, ...
+// in turn), then the lanes in order (runtime.cpp Reducer::result,
+// reduce.cuh sum_partials).
+constexpr int kRedLanes = 128;
 inline void note_partials(const RedSlot& r, unsigned tuples) {
   if (r.count) *r.count = (int)tuples;
 }
