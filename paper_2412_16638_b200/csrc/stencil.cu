@@ -760,7 +760,7 @@ int tma_chunk(long cols, int planes) {
   }
   int best = 8;
   long best_cost = -1;
-  for (int kc = 4; kc <= 64; kc *= 2) {
+  for (int kc = 4; kc <= 64; ++kc) {
     const long units = cols * ((planes + kc - 1) / kc);
     const long cost = ((units + resident - 1) / resident) * (std::min(kc, planes) + 2);
     if (best_cost < 0 || cost < best_cost) {
@@ -977,8 +977,8 @@ void feval_combine(const StencilSpec& k, const float* y32, const FevalCombine& f
 // neighbourhoods and writes only x1 — to a second buffer, since neighbouring
 // CTAs still read x.  r1 and the true residual are not stored: the caller
 // recomputes whichever it needs on the rare path that continues.
-constexpr int CG_SLOT = tma_slot_elems<float>();
-constexpr size_t cg_fused_smem() { return (size_t)TST * 2 * CG_SLOT * sizeof(float) + TST * sizeof(uint64_t) + 128; }
+constexpr int CG_SLOT = tma_slot_elems<float>(), CG_TST = 4;  // 3 planes in use + 1 in flight: 44 KB, 5 CTAs/SM
+constexpr size_t cg_fused_smem() { return (size_t)CG_TST * 2 * CG_SLOT * sizeof(float) + CG_TST * sizeof(uint64_t) + 128; }
 
 __global__ void __launch_bounds__(TTHREADS)
     k_cg_fused(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap pmap, int n, int nz,
@@ -995,7 +995,7 @@ __global__ void __launch_bounds__(TTHREADS)
   }
   extern __shared__ unsigned char smem_raw[];
   float* buf = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-  uint64_t* full = reinterpret_cast<uint64_t*>(buf + TST * 2 * CG_SLOT);
+  uint64_t* full = reinterpret_cast<uint64_t*>(buf + CG_TST * 2 * CG_SLOT);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int i0 = blockIdx.x * TI, j0 = blockIdx.y * TJ;
   int k0, k1;
@@ -1003,22 +1003,22 @@ __global__ void __launch_bounds__(TTHREADS)
   const int planes = k1 - k0 + 2;
   constexpr uint32_t bytes = (TJ + 2) * TW * sizeof(float);
   if (tid == 0) {
-    for (int q = 0; q < TST; ++q) mbar_init(&full[q], 1);
+    for (int q = 0; q < CG_TST; ++q) mbar_init(&full[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   const CUtensorMap* xm = &xmap;
   const CUtensorMap* pm = &pmap;
   auto issue = [&](int q) {
-    const int k = k0 - 1 + q, sl = q % TST;
+    const int k = k0 - 1 + q, sl = q % CG_TST;
     float* dst = buf + sl * 2 * CG_SLOT;
     mbar_expect_tx(&full[sl], 2 * bytes);
     tma_3d(dst, xm, i0 - 4, j0 - 1, k, &full[sl]);
     tma_3d(dst + CG_SLOT, pm, i0 - 4, j0 - 1, k, &full[sl]);
   };
   if (tid == 0)
-    for (int q = 0; q < TST && q < planes; ++q) issue(q);
-  auto wait = [&](int q) { mbar_wait(&full[q % TST], (uint32_t)(q / TST) & 1u); };
+    for (int q = 0; q < CG_TST && q < planes; ++q) issue(q);
+  auto wait = [&](int q) { mbar_wait(&full[q % CG_TST], (uint32_t)(q / CG_TST) & 1u); };
   auto ld = [](const float* p) {
     const float4 f = *reinterpret_cast<const float4*>(p);
     V4<float> v;
@@ -1049,9 +1049,9 @@ __global__ void __launch_bounds__(TTHREADS)
       wait(1);
     }
     wait(q + 1);
-    const float* xmn = buf + ((q - 1) % TST) * 2 * CG_SLOT;
-    const float* xc = buf + (q % TST) * 2 * CG_SLOT;
-    const float* xpl = buf + ((q + 1) % TST) * 2 * CG_SLOT;
+    const float* xmn = buf + ((q - 1) % CG_TST) * 2 * CG_SLOT;
+    const float* xc = buf + (q % CG_TST) * 2 * CG_SLOT;
+    const float* xpl = buf + ((q + 1) % CG_TST) * 2 * CG_SLOT;
     V4<float> nb[TROWS], nr[TROWS];
 #pragma unroll
     for (int rr = 0; rr < TROWS; ++rr)
@@ -1098,7 +1098,7 @@ __global__ void __launch_bounds__(TTHREADS)
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    if (tid == 0 && q - 1 + TST < planes) issue(q - 1 + TST);
+    if (tid == 0 && q - 1 + CG_TST < planes) issue(q - 1 + CG_TST);
   }
   grid_reduce<2>(acc, red);
 }
@@ -1124,7 +1124,7 @@ void cg_fused_update(const StencilSpec& sp, float alpha, const RedSlot* alpha_sr
   const long cols = (long)(n / TI) * (n / TJ);
   if (cols != chunk_cols) {  // wave-sized k-chunks (as tma_chunk)
     long best_cost = -1;
-    for (int kc = 4; kc <= 64; kc *= 2) {
+    for (int kc = 4; kc <= 64; ++kc) {  // (any chunk: fill the resident slots)
       const long units = cols * ((nz + kc - 1) / kc);
       const long cost = ((units + resident - 1) / resident) * (std::min(kc, nz) + 2);
       if (best_cost < 0 || cost < best_cost) {

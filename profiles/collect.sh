@@ -2,7 +2,7 @@
 # Evidence capture for profiles/<round>/ (run on the GPU box via gpurun):
 #   bench line (default N=1 run, CPU baseline included), the reference arm,
 #   an ncu launch list of 2 bench steps, and ncu --set full captures of the
-#   dominant kernels (folded tcgen05 contraction; TMA stencil).
+#   dominant kernels (folded tcgen05 contraction; TMA stencil; fused CG update).
 set -u
 OUT=${1:-gpurun_out}
 mkdir -p "$OUT"
@@ -14,4 +14,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_te
   -o "$OUT/tcf_full" python bench.py --steps 1 --warmup 1 --no-cpu-baseline > "$OUT/ncu_tcf.log" 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_stencil_tma -s 10 -c 3 \
   -o "$OUT/stencil_full" python bench.py --steps 1 --warmup 1 --no-cpu-baseline > "$OUT/ncu_stencil.log" 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_cg_fused -s 2 -c 1 \
+  -o "$OUT/cgfused_full" python bench.py --steps 1 --warmup 1 --no-cpu-baseline > "$OUT/ncu_cgfused.log" 2>&1
 ls -la "$OUT"
