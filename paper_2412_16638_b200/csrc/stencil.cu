@@ -377,38 +377,44 @@ struct EpiFevalCombine {
   double ah[kMaxAcc] = {}, ae[kMaxAcc] = {};
   int hah[kMaxAcc] = {}, hae[kMaxAcc] = {};
   struct State {};
+  // prefetched a plane ahead: S_{i+1} and the first later-stage accumulator
+  // (the forcing is regenerated at use — or read there when stored)
   struct Pre {
-    V4<double> g, s;
-    V4<float> g32;
+    V4<double> s, a0;
   };
   __device__ void init(State&) const {}
   __device__ __forceinline__ Pre pre4(long i) const {
-    if (gen.s) {
-      Pre p;
-      forcing4(gen, i, p.g.x);
-      p.s = ld4(sin + i);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) p.g32.x[e] = __double2float_rn(p.g.x[e]);
-      return p;
-    }
-    return Pre{ld4(g + i), ld4(sin + i), ld4(g32 + i)};
+    Pre p;
+    p.s = ld4(sin + i);
+    p.a0 = nacc > 0 ? ld4(ain[0] + i) : zero4<double>();
+    return p;
   }
   __device__ __forceinline__ void v4dual(State&, long i, const V4<double>& v64, const V4<float>& v32,
                                          const V4<double>& xc, const Pre& p) const {
     if (finite_flag && !(isfinite(xc.x[0]) && isfinite(xc.x[1]) && isfinite(xc.x[2]) && isfinite(xc.x[3])))
       *finite_flag = 1;
+    V4<double> gv;
+    V4<float> g32v;
+    if (gen.s) {
+      forcing4(gen, i, gv.x);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) g32v.x[e] = __double2float_rn(gv.x[e]);
+    } else {
+      gv = ld4(g + i);
+      g32v = ld4(g32 + i);
+    }
     V4<double> fh;
     V4<float> fe;
     bool ovf = false;
     V4<float> b;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      fh.x[e] = xadd(v64.x[e], p.g.x[e]);
-      fe.x[e] = xadd(v32.x[e], p.g32.x[e]);
+      fh.x[e] = xadd(v64.x[e], gv.x[e]);
+      fe.x[e] = xadd(v32.x[e], g32v.x[e]);
       double r = p.s.x[e];
       if (hh) r = xadd(r, xmul(ch, fh.x[e]));
       if (he) r = xadd(r, xmul(ce, (double)fe.x[e]));
-      if (hg) r = xadd(r, xmul(cg, p.g.x[e]));
+      if (hg) r = xadd(r, xmul(cg, gv.x[e]));
       ovf |= f32_overflows(r);
       b.x[e] = __double2float_rn(r);
     }
@@ -417,7 +423,7 @@ struct EpiFevalCombine {
     if (xout) st4(xout + i, b);
     if (ovf) *ovf_flag = 1;
     for (int a = 0; a < nacc; ++a) {
-      V4<double> s = ld4(ain[a] + i);
+      V4<double> s = a == 0 ? p.a0 : ld4(ain[a] + i);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         if (hah[a]) s.x[e] = xadd(s.x[e], xmul(ah[a], fh.x[e]));
@@ -618,8 +624,13 @@ constexpr size_t tma_stencil_smem() {
   return (size_t)TST * tma_slot_elems<Raw>() * sizeof(Raw) + TST * sizeof(uint64_t) + 128;
 }
 
+// resident CTAs per SM the register allocation must allow (the fused
+// f-evaluation epilogue otherwise takes 156 registers: 3 CTAs, latency-bound)
+template <class Epi>
+constexpr int tma_min_blocks() { return is_dual<Epi>::value ? 4 : 1; }
+
 template <class Src, class Epi>
-__global__ void __launch_bounds__(TTHREADS)
+__global__ void __launch_bounds__(TTHREADS, tma_min_blocks<Epi>())
     k_stencil_tma(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap lomap,
                   const __grid_constant__ CUtensorMap himap, int has_lo, int has_hi, int n, int nz, int kb, int ke,
                   int kc, typename Src::type s, typename Src::type g, Src src, Epi epi) {
