@@ -252,6 +252,43 @@ __global__ void __launch_bounds__(kBlock) k_xpby(size_t m, const T* z, real_t<T>
       [&](size_t i) { p[i] = xadd(ldg(z + i), xscale(beta, p[i])); });
 }
 
+// p = z + beta p with beta = (R)(r.z) / rz_old formed on the device from the
+// dot's tuples in the host's summation order (reduce.cuh sum_partials), so the
+// pipelined CG launches it before reading r.z back — same value as the host's.
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+template <class T>
+__global__ void __launch_bounds__(kBlock) k_xpby_dev(size_t m, const T* z, const double* tup, int nt,
+                                                     real_t<T> rz_old, T* p) {
+  pdl_wait();
+  pdl_trigger();
+  using R = real_t<T>;
+  const double s = sum_partials(tup, nt, 0);
+  R rz;
+  if constexpr (sizeof(R) == 4) rz = __double2float_rn(s); else rz = s;
+  const R beta = div_rn(rz, rz_old);
+  for_each4(
+      m,
+      [&](size_t i) {
+        const V4<T> zv = ld4(z + i);
+        V4<T> pv = ld4rw(p + i);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) pv.x[e] = xadd(zv.x[e], xscale(beta, pv.x[e]));
+        st4(p + i, pv);
+      },
+      [&](size_t i) { p[i] = xadd(ldg(z + i), xscale(beta, p[i])); });
+}
+
+template <class T>
+void xpby_dev(size_t m, const T* z, const RedSlot& rz_new, real_t<T> rz_old, T* p, cudaStream_t st) {
+  if (!rz_new.dpart || !rz_new.count || *rz_new.count <= 0) MPRKB_THROW(10, "xpby_dev: slot has no device tuples");
+  launch_pdl(k_xpby_dev<T>, dim3(wave(m)), dim3(kBlock), 0, st, m, z, (const double*)rz_new.dpart, *rz_new.count,
+             rz_old, p);
+  LAUNCHED("xpby");
+}
+template void xpby_dev<float>(size_t, const float*, const RedSlot&, float, float*, cudaStream_t);
+template void xpby_dev<double>(size_t, const double*, const RedSlot&, double, double*, cudaStream_t);
+
 template <class T>
 void xpby(size_t m, const T* z, real_t<T> beta, T* p, cudaStream_t st) {
   launch_pdl(k_xpby<T>, dim3(wave(m)), dim3(kBlock), 0, st, m, z, beta, p);

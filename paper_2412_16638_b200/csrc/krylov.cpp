@@ -250,6 +250,17 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
   R rz{}, pq_first{};
   bool have_pq = false;
   double fused_v[2] = {0.0, 0.0};  // (||r1||^2, ||b - A x1||^2) of the fused first update
+  // Pipelined iterations (FAST, fused stencil, a general preconditioner, one
+  // rank): right after the update the next iteration's z = P r, r.z,
+  // p = z + beta p (beta formed on the device, xpby_dev) and q = A p, p.q are
+  // launched speculatively, and ONE round trip returns ||r||, r.z and p.q —
+  // instead of one per scalar.  Decisions stay the reference's, in its
+  // order; if it stops (converged, breakdown, veto) only p, q, z — scratch
+  // from then on — were touched.
+  const char* pipe_env = std::getenv("MPRKB_CG_PIPE");  // (=0: one round trip per scalar, for A/B tests)
+  const bool pipe = batch && !spec_true && (!w.comm || w.comm->size() == 1) && !(pipe_env && pipe_env[0] == '0');
+  R spec_rz{}, spec_pq{};
+  bool have_spec = false;
   if (batch) {
     {
       Bracket br(timer, "stencil", st);
@@ -344,6 +355,24 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
           stencil_apply<T>(*S, p, q, st);
           cg_update<T>(m, alpha, z, p, r, q, nullptr, st);  // r -= alpha q (z is scratch here)
         }
+      } else if (pipe) {
+        const RedSlot s1d = w.red.slot_dev(1);
+        pre(r, z);
+        dot_real<T>(m, r, z, s1d, num, st);
+        xpby_dev<T>(m, z, s1d, rz, p, st);
+        {
+          Bracket br(timer, "stencil", st);
+          stencil_apply_dot<T>(*S, p, q, s2, st);
+        }
+        stream_sync(st);
+        double v[3];
+        w.red.result(0, 1, &v[0]);
+        w.red.result(1, 1, &v[1]);
+        w.red.result(2, 1, &v[2]);
+        rnorm = (double)std::sqrt((R)v[0]);
+        spec_rz = (R)v[1];
+        spec_pq = (R)v[2];
+        have_spec = true;
       } else if (spec_true) {
         {
           Bracket br(timer, "stencil", st);
@@ -369,6 +398,14 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
         pre(r, z);
         std::swap(p, z);
         rz = rdot(r, p);
+        have_spec = false;
+        continue;
+      }
+      if (have_spec) {  // z, r.z, p and q = A p are already formed
+        have_spec = false;
+        rz = spec_rz;
+        pq_first = spec_pq;
+        have_pq = true;
         continue;
       }
       pre(r, z);

@@ -180,6 +180,9 @@ void cg_update(size_t m, real_t<T> alpha, T* x, const T* p, T* r, const T* q, co
                cudaStream_t st);  // x += a p; r -= a q
 template <class T>
 void xpby(size_t m, const T* z, real_t<T> beta, T* p, cudaStream_t st);  // p = z + beta p
+// p = z + beta p, beta = (R)(sum of rz_new's device tuples) / rz_old (the host's rounding)
+template <class T>
+void xpby_dev(size_t m, const T* z, const RedSlot& rz_new, real_t<T> rz_old, T* p, cudaStream_t st);
 template <class T>
 void vscale(size_t m, const T* w, T s, T* v, cudaStream_t st);  // v = w * s
 template <class T>
