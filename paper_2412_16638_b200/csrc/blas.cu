@@ -258,12 +258,12 @@ __global__ void __launch_bounds__(kBlock) k_xpby(size_t m, const T* z, real_t<T>
 __device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
 __device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
 template <class T>
-__global__ void __launch_bounds__(kBlock) k_xpby_dev(size_t m, const T* z, const double* tup, int nt,
+__global__ void __launch_bounds__(kBlock) k_xpby_dev(size_t m, const T* z, const double* tup, int nt, int comp,
                                                      real_t<T> rz_old, T* p) {
   pdl_wait();
   pdl_trigger();
   using R = real_t<T>;
-  const double s = sum_partials(tup, nt, 0);
+  const double s = sum_partials(tup, nt, comp);
   R rz;
   if constexpr (sizeof(R) == 4) rz = __double2float_rn(s); else rz = s;
   const R beta = div_rn(rz, rz_old);
@@ -280,14 +280,14 @@ __global__ void __launch_bounds__(kBlock) k_xpby_dev(size_t m, const T* z, const
 }
 
 template <class T>
-void xpby_dev(size_t m, const T* z, const RedSlot& rz_new, real_t<T> rz_old, T* p, cudaStream_t st) {
+void xpby_dev(size_t m, const T* z, const RedSlot& rz_new, int comp, real_t<T> rz_old, T* p, cudaStream_t st) {
   if (!rz_new.dpart || !rz_new.count || *rz_new.count <= 0) MPRKB_THROW(10, "xpby_dev: slot has no device tuples");
   launch_pdl(k_xpby_dev<T>, dim3(wave(m)), dim3(kBlock), 0, st, m, z, (const double*)rz_new.dpart, *rz_new.count,
-             rz_old, p);
+             comp, rz_old, p);
   LAUNCHED("xpby");
 }
-template void xpby_dev<float>(size_t, const float*, const RedSlot&, float, float*, cudaStream_t);
-template void xpby_dev<double>(size_t, const double*, const RedSlot&, double, double*, cudaStream_t);
+template void xpby_dev<float>(size_t, const float*, const RedSlot&, int, float, float*, cudaStream_t);
+template void xpby_dev<double>(size_t, const double*, const RedSlot&, int, double, double*, cudaStream_t);
 
 template <class T>
 void xpby(size_t m, const T* z, real_t<T> beta, T* p, cudaStream_t st) {

@@ -7,6 +7,7 @@
 // All HBM-bound.  Algorithmic bytes per DOF: block-Jacobi (2 s + b s_b),
 // CSR (2 s + nnz_row (s_v + 4) + 4), basis ops 2-3 vector streams.
 #include "launch.hpp"
+#include "pdl.cuh"
 #include "reduce.cuh"
 #include "vec.cuh"
 
@@ -172,6 +173,112 @@ bool bj_row(int n, long lines, int b, const S* inv, const T* r, T* z, cudaStream
     }
   }
 }
+
+// CG update fused with the block-Jacobi apply (krylov.hpp:134-137 + the
+// next iteration's z = P r, r.z): one thread per x-line block of B points
+// loads x, p, r, q once, writes x, r and z = D_blk r, and reduces
+// (||r||^2, r.z).  Unfused: update (x, p, r, q in; x, r out), apply (r in,
+// z out), dot (r, z in) — 12 bytes per point per scalar more.  Each value
+// rounds as in the separate kernels.
+template <class T, class S, int B>
+__global__ void __launch_bounds__(128) k_cg_update_bj(long blocks, real_t<T> alpha, T* __restrict__ x,
+                                                      const T* __restrict__ p, T* __restrict__ r,
+                                                      const T* __restrict__ q, const S* __restrict__ inv,
+                                                      T* __restrict__ z, RedSlot red) {
+  pdl_wait();
+  pdl_trigger();
+  using R = real_t<T>;
+  double acc2[2] = {0.0, 0.0};
+  for (long blk = blockIdx.x * (long)blockDim.x + threadIdx.x; blk < blocks; blk += (long)gridDim.x * blockDim.x) {
+    const long o = blk * B;
+    R rv[B];
+#pragma unroll
+    for (int c = 0; c < B / 4; ++c) {
+      V4<T> xv = ld4rw(x + o + 4 * c), rw = ld4rw(r + o + 4 * c);
+      const V4<T> pv = ld4(p + o + 4 * c), qv = ld4(q + o + 4 * c);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        xv.x[u] = xadd(xv.x[u], xscale(alpha, pv.x[u]));
+        rw.x[u] = xsub(rw.x[u], xscale(alpha, qv.x[u]));
+        dot_acc(*reinterpret_cast<double(*)[1]>(&acc2[0]), rw.x[u], rw.x[u]);
+        rv[4 * c + u] = rw.x[u];
+      }
+      st4(x + o + 4 * c, xv);
+      st4(r + o + 4 * c, rw);
+    }
+    const S* D = inv + blk * (long)B * B;
+    R acc[B];
+#pragma unroll
+    for (int ii = 0; ii < B; ++ii) acc[ii] = R(0);
+#pragma unroll
+    for (int jj = 0; jj < B; ++jj) {
+      if constexpr (std::is_same_v<S, double>) {
+#pragma unroll
+        for (int c = 0; c < B / 2; ++c) {
+          const double2 w = __ldg(reinterpret_cast<const double2*>(D + jj * B) + c);
+          acc[2 * c] = xadd(acc[2 * c], rmul((R)w.x, rv[jj]));
+          acc[2 * c + 1] = xadd(acc[2 * c + 1], rmul((R)w.y, rv[jj]));
+        }
+      } else {
+        float col[B];
+        ld_col<S, B>(D + jj * B, col);
+#pragma unroll
+        for (int ii = 0; ii < B; ++ii) acc[ii] = xadd(acc[ii], rmul((R)col[ii], rv[jj]));
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < B / 4; ++c) {
+      V4<T> w;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        w.x[u] = acc[4 * c + u];
+        dot_acc(*reinterpret_cast<double(*)[1]>(&acc2[1]), rv[4 * c + u], w.x[u]);
+      }
+      st4(z + o + 4 * c, w);
+    }
+  }
+  grid_reduce<2>(acc2, red);
+}
+
+template <class T, class S>
+bool cg_bj(int n, long lines, int b, real_t<T> alpha, T* x, const T* p, T* r, const T* q, const S* inv, T* z,
+           const RedSlot& red, cudaStream_t st) {
+  if constexpr (is_cplx<T>) {
+    return false;
+  } else {
+    if (n % b) return false;
+    const long blocks = lines * (n / b);
+    const unsigned g = grid_for((size_t)blocks, 128, 16);
+    switch (b) {
+      case 4: launch_pdl(k_cg_update_bj<T, S, 4>, dim3(g), dim3(128), 0, st, blocks, alpha, x, p, r, q, inv, z, red); break;
+      case 8: launch_pdl(k_cg_update_bj<T, S, 8>, dim3(g), dim3(128), 0, st, blocks, alpha, x, p, r, q, inv, z, red); break;
+      case 16:
+        launch_pdl(k_cg_update_bj<T, S, 16>, dim3(g), dim3(128), 0, st, blocks, alpha, x, p, r, q, inv, z, red);
+        break;
+      default: return false;
+    }
+    note_partials(red, g);
+    return true;
+  }
+}
+
+template <class T>
+bool cg_update_block_jacobi(int n, int b, int storage, const void* inv, real_t<T> alpha, T* x, const T* p, T* r,
+                            const T* q, T* z, const RedSlot& red, cudaStream_t st, long lines) {
+  if (lines <= 0) lines = (long)n * n;
+  bool done = false;
+  switch (storage) {
+    case 4: done = cg_bj<T, __half>(n, lines, b, alpha, x, p, r, q, (const __half*)inv, z, red, st); break;
+    case 0: done = cg_bj<T, float>(n, lines, b, alpha, x, p, r, q, (const float*)inv, z, red, st); break;
+    default: done = cg_bj<T, double>(n, lines, b, alpha, x, p, r, q, (const double*)inv, z, red, st); break;
+  }
+  if (done) LAUNCHED("cg_update_bj");
+  return done;
+}
+template bool cg_update_block_jacobi<float>(int, int, int, const void*, float, float*, const float*, float*,
+                                            const float*, float*, const RedSlot&, cudaStream_t, long);
+template bool cg_update_block_jacobi<double>(int, int, int, const void*, double, double*, const double*, double*,
+                                             const double*, double*, const RedSlot&, cudaStream_t, long);
 
 template <class S>
 __global__ void k_bj_fill(long nblocks_per_line, long lines, int n, int b, const double* __restrict__ full,

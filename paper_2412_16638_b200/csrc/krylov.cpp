@@ -336,7 +336,14 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
           fused = true;
         }
       }
-      if (!fused) cg_update<T>(m, alpha, x, p, r, q, fast ? &s0 : nullptr, st);
+      // (pipelined: a preconditioner that folds into the update also forms
+      // the next z = P r and r.z in the same pass)
+      bool pre_fused = false;
+      if (!fused && pipe && P) {
+        Bracket br(timer, "precond", st);
+        pre_fused = P->cg_update_apply((double)alpha, x, p, r, q, z, w.red.slot_dev(1), st);
+      }
+      if (!fused && !pre_fused) cg_update<T>(m, alpha, x, p, r, q, fast ? &s0 : nullptr, st);
       x_clean = false;
       ++rep.iterations;
       double rt_spec = -1.0;
@@ -357,17 +364,23 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
         }
       } else if (pipe) {
         const RedSlot s1d = w.red.slot_dev(1);
-        pre(r, z);
-        dot_real<T>(m, r, z, s1d, num, st);
-        xpby_dev<T>(m, z, s1d, rz, p, st);
+        if (!pre_fused) {
+          pre(r, z);
+          dot_real<T>(m, r, z, s1d, num, st);
+        }
+        xpby_dev<T>(m, z, s1d, pre_fused ? 1 : 0, rz, p, st);
         {
           Bracket br(timer, "stencil", st);
           stencil_apply_dot<T>(*S, p, q, s2, st);
         }
         stream_sync(st);
         double v[3];
-        w.red.result(0, 1, &v[0]);
-        w.red.result(1, 1, &v[1]);
+        if (pre_fused) {
+          w.red.result(1, 2, &v[0]);  // (||r||^2, r.z) of the fused update
+        } else {
+          w.red.result(0, 1, &v[0]);
+          w.red.result(1, 1, &v[1]);
+        }
         w.red.result(2, 1, &v[2]);
         rnorm = (double)std::sqrt((R)v[0]);
         spec_rz = (R)v[1];

@@ -142,6 +142,11 @@ void slab_transpose_rows(int n, int nz, int ny, int P, size_t elem, const void* 
 template <class T>
 void block_jacobi_apply(int n, int b, int storage, const void* inv, const T* r, T* z, cudaStream_t st,
                         long lines = 0);
+// x += alpha p; r -= alpha q; z = blockdiag(inv) r; red <- (||r||^2, r.z) (FAST,
+// real T, n % b == 0, b in {4, 8, 16}); false when not covered
+template <class T>
+bool cg_update_block_jacobi(int n, int b, int storage, const void* inv, real_t<T> alpha, T* x, const T* p, T* r,
+                            const T* q, T* z, const RedSlot& red, cudaStream_t st, long lines = 0);
 // per-block inverse storage from the two distinct fp64 block inverses
 // (column-major b x b full blocks, n % b tail blocks)
 void block_jacobi_fill(int n, int b, int storage, const double* full_dev, const double* tail_dev, void* inv,
@@ -182,7 +187,7 @@ template <class T>
 void xpby(size_t m, const T* z, real_t<T> beta, T* p, cudaStream_t st);  // p = z + beta p
 // p = z + beta p, beta = (R)(sum of rz_new's device tuples) / rz_old (the host's rounding)
 template <class T>
-void xpby_dev(size_t m, const T* z, const RedSlot& rz_new, real_t<T> rz_old, T* p, cudaStream_t st);
+void xpby_dev(size_t m, const T* z, const RedSlot& rz_new, int comp, real_t<T> rz_old, T* p, cudaStream_t st);
 template <class T>
 void vscale(size_t m, const T* w, T s, T* v, cudaStream_t st);  // v = w * s
 template <class T>

@@ -26,6 +26,13 @@ class Op {
   // exact arithmetic (FastDiag): CG then normally converges after one update,
   // which the FAST solver exploits to batch its scalar round trips.
   virtual bool exact_inverse() const { return false; }
+  // A preconditioner that can fold itself into the CG update: x += a p,
+  // r -= a q, z = P r in one pass, reducing (||r||^2, r.z) into red.
+  // false: not available (the solver runs the separate kernels).
+  virtual bool cg_update_apply(double /*alpha*/, void* /*x*/, const void* /*p*/, void* /*r*/, const void* /*q*/,
+                               void* /*z*/, const RedSlot& /*red*/, cudaStream_t /*st*/) {
+    return false;
+  }
 
  private:
   int dtype_;

@@ -114,6 +114,15 @@ class BlockJacobiOp final : public Op {
   void apply(const void* x, void* out, cudaStream_t st) override {
     block_jacobi_apply<T>(n_, b_, storage_, inv_.get(), static_cast<const T*>(x), static_cast<T*>(out), st, lines_);
   }
+  bool cg_update_apply(double alpha, void* x, const void* p, void* r, const void* q, void* z, const RedSlot& red,
+                       cudaStream_t st) override {
+    if constexpr (std::is_same_v<T, float> || std::is_same_v<T, double>) {
+      return cg_update_block_jacobi<T>(n_, b_, storage_, inv_.get(), (T)alpha, static_cast<T*>(x),
+                                       static_cast<const T*>(p), static_cast<T*>(r), static_cast<const T*>(q),
+                                       static_cast<T*>(z), red, st, lines_);
+    }
+    return false;
+  }
 
  private:
   int n_;
