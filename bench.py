@@ -390,6 +390,8 @@ def run_cuda_arm(args):
             "kernels_note": (f"each kernel alone on {N_GRID}^3 vectors, CUDA events, algorithmic bytes "
                              "(SURVEY.md §8d) / time vs MEASURED_PEAKS hbm_gbs"),
         }
+        if world == 1 and not split and not args.no_variants:
+            line["config1_variants"] = config1_variants(mp, torch)
         if not args.no_cpu_baseline and world == 1 and not split:
             budget = float(os.environ.get("MPRKB_CPU_BASELINE_S", "30"))
             threads = os.cpu_count() or 1
@@ -405,6 +407,42 @@ def run_cuda_arm(args):
     if line is not None:
         print(json.dumps(line))
     return 0
+
+
+def config1_variants(mp, torch, steps=3):
+    """configs[1] reads "fp32-stored CG + block-Jacobi on 1 x B200 vs fp64
+    baseline stepper".  The headline runs the reference's own preconditioner
+    (FastDiag, the only one its CPU arm has); beside it, the same 256^3 4s3pB
+    step with the block-Jacobi extension (b = 8, fp16 block storage, fp32 CG)
+    and with the fp64 policy (the "baseline stepper"), device-resident,
+    CUDA events on the stepper's stream after one warm-up step."""
+    out = {}
+    tab = mp.builtin(METHOD)
+    for key, kw, note in (
+            ("cg_block_jacobi_b8_f16", dict(prec="f32", tol=TOL, max_iter=400, preconditioner="block-jacobi",
+                                            block_size=8, block_storage="f16"),
+             "fp32 stages, CG + block-Jacobi (x-line blocks of 8, fp16 storage), pipelined FAST CG"),
+            ("fp64_baseline_stepper", dict(prec="f64", tol=1e-5, max_iter=MAX_ITER),
+             "fp64 stages, CG + FastDiag on CUDA cores (the fp64 policy)")):
+        prec, tol, mi = kw.pop("prec"), kw.pop("tol"), kw.pop("max_iter")
+        st = mp.Stepper("heat", N_GRID, tab, TAU, tol, prec, mi, **kw)
+        s = torch.cuda.ExternalStream(st.stream)
+        u = torch.from_numpy(st.initial_state()).cuda()
+        st.step_device(u)
+        torch.cuda.synchronize()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        its = []
+        a.record(s)
+        for _ in range(steps):
+            its.append(st.step_device(u)["iterations"])
+        b.record(s)
+        b.synchronize()
+        ms = a.elapsed_time(b) / steps
+        out[key] = {"ms_per_step": ms, "value": N_GRID ** 3 / (ms * 1e-3), "unit": "DOF-updates/s",
+                    "iterations_per_solve": its, "tol": tol, "steps": steps, "note": note}
+        del st
+    return out
 
 
 KERNELS = ["copy_f32", "stencil_f64", "stencil_f32", "residual_f32", "apply_dot_f32", "dots2_f32", "cg_fused_f32",
@@ -474,6 +512,7 @@ def main():
     ap.add_argument("--steps", type=int, default=60)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--no-variants", action="store_true", help="skip the configs[1] companion steppers")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--split", action="store_true",
                     help="configs[2] path (512^3 through the NCCL split stepper) even on one GPU")
