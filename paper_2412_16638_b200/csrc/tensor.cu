@@ -332,6 +332,8 @@ void launch_fast(int side, int n, long cols, const T* q, const T* x, T* out, con
     launch_fast_cfg<T, 128, 64, 16, 8, 4, DIAG, FOLD>(side, n, cols, q, x, out, pd, st);
   else if constexpr (sizeof(T) == 4)
     launch_fast_cfg<T, 128, 128, 8, 8, 8, DIAG, FOLD>(side, n, cols, q, x, out, pd, st);
+  else if constexpr (FOLD)  // fp64, two accumulator sets: 8 x 4 thread tile (2.7 FMA per smem load)
+    launch_fast_cfg<T, 64, 64, 16, 8, 4, DIAG, FOLD>(side, n, cols, q, x, out, pd, st);
   else
     launch_fast_cfg<T, 64, 64, 16, 4, 4, DIAG, FOLD>(side, n, cols, q, x, out, pd, st);
 }
