@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(256) k_block_jacobi(int n, long lines, int b, 
   }
 }
 
-// One thread per block (n % B == 0, real T): the block's inverse (B columns
+// One thread per block (n % B == 0): the block's inverse (B columns
 // of B contiguous entries) and its r segment are read with 16-byte vector
 // loads, outputs accumulate over jj in the same ascending order as the
 // per-element kernel (bitwise identical), B outputs stored contiguously.
@@ -115,16 +115,16 @@ __global__ void __launch_bounds__(128) k_block_jacobi_row(long blocks, const S* 
   for (long blk = blockIdx.x * (long)blockDim.x + threadIdx.x; blk < blocks; blk += (long)gridDim.x * blockDim.x) {
     const S* D = inv + blk * (long)B * B;
     const T* rb = r + blk * B;
-    R rv[B];
+    T rv[B];
 #pragma unroll
     for (int c = 0; c < B / 4; ++c) {
       const V4<T> w = ld4(rb + 4 * c);
 #pragma unroll
       for (int u = 0; u < 4; ++u) rv[4 * c + u] = w.x[u];
     }
-    R acc[B];
+    T acc[B];
 #pragma unroll
-    for (int ii = 0; ii < B; ++ii) acc[ii] = R(0);
+    for (int ii = 0; ii < B; ++ii) acc[ii] = zero_v<T>();
 #pragma unroll
     for (int jj = 0; jj < B; ++jj) {
       if constexpr (std::is_same_v<S, double>) {
@@ -153,9 +153,7 @@ __global__ void __launch_bounds__(128) k_block_jacobi_row(long blocks, const S* 
 
 template <class T, class S>
 bool bj_row(int n, long lines, int b, const S* inv, const T* r, T* z, cudaStream_t st) {
-  if constexpr (is_cplx<T>) {
-    return false;
-  } else {
+  {  // (complex T: real blocks times complex segments, per component)
     if (n % b) return false;
     const long blocks = lines * (n / b);
     const unsigned g = grid_for((size_t)blocks, 128, 16);
@@ -399,59 +397,278 @@ struct Store16<c64> {
   }
 };
 
+// 4 consecutive fp16-stored elements: one 16-byte (complex) / 8-byte (real) access
+template <class T>
+__device__ __forceinline__ void ld16x4(const typename Store16<T>::type* v, T (&o)[4]) {
+  using S = typename Store16<T>::type;
+  if constexpr (sizeof(S) == 4) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(v));
+    const unsigned w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o[e] = Store16<T>::get(*reinterpret_cast<const S*>(&w[e]));
+  } else {
+    const uint2 u = __ldg(reinterpret_cast<const uint2*>(v));
+    const __half2 a = *reinterpret_cast<const __half2*>(&u.x), b = *reinterpret_cast<const __half2*>(&u.y);
+    o[0] = Store16<T>::get(__low2half(a));
+    o[1] = Store16<T>::get(__high2half(a));
+    o[2] = Store16<T>::get(__low2half(b));
+    o[3] = Store16<T>::get(__high2half(b));
+  }
+}
+template <class T>
+__device__ __forceinline__ void st16x4(typename Store16<T>::type* v, const T (&x)[4]) {
+  using S = typename Store16<T>::type;
+  if constexpr (sizeof(S) == 4) {
+    unsigned w[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const S h = Store16<T>::put(x[e]);
+      w[e] = *reinterpret_cast<const unsigned*>(&h);
+    }
+    *reinterpret_cast<uint4*>(v) = make_uint4(w[0], w[1], w[2], w[3]);
+  } else {
+    const __half2 a = __halves2half2(Store16<T>::put(x[0]), Store16<T>::put(x[1]));
+    const __half2 b = __halves2half2(Store16<T>::put(x[2]), Store16<T>::put(x[3]));
+    uint2 u;
+    u.x = *reinterpret_cast<const unsigned*>(&a);
+    u.y = *reinterpret_cast<const unsigned*>(&b);
+    *reinterpret_cast<uint2*>(v) = u;
+  }
+}
+template <class T>
+__device__ __forceinline__ void ldT4(const T* p, T (&o)[4]) {
+  const V4<T> v = ld4(p);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) o[e] = v.x[e];
+}
+template <class T>
+__device__ __forceinline__ void ldT4rw(const T* p, T (&o)[4]) {
+  const V4<T> v = ld4rw(p);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) o[e] = v.x[e];
+}
+template <class T>
+__device__ __forceinline__ void stT4(T* p, const T (&x)[4]) {
+  V4<T> v;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) v.x[e] = x[e];
+  st4(p, v);
+}
+// grid-stride over groups of 4 (f4) plus the scalar tail (f1)
+template <class F4, class F1>
+__device__ __forceinline__ void each4(size_t m, F4&& f4, F1&& f1) {
+  const size_t nv = m / 4, tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x, stride = (size_t)gridDim.x * blockDim.x;
+  for (size_t v = tid; v < nv; v += stride) f4(4 * v);
+  for (size_t i = 4 * nv + tid; i < m; i += stride) f1(i);
+}
+
 // v16 = w * s  (basis normalisation, krylov.hpp:229-231, 298-300)
 template <class T>
 __global__ void __launch_bounds__(256) k_vscale16(size_t m, const T* w, T s, typename Store16<T>::type* v) {
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < m; i += (size_t)gridDim.x * blockDim.x)
-    v[i] = Store16<T>::put(xmul(ldg(w + i), s));
+  pdl_wait();
+  pdl_trigger();
+  each4(
+      m,
+      [&](size_t i) {
+        T x[4];
+        ldT4(w + i, x);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) x[e] = xmul(x[e], s);
+        st16x4<T>(v + i, x);
+      },
+      [&](size_t i) { v[i] = Store16<T>::put(xmul(ldg(w + i), s)); });
 }
 // conj(v16) . w  in fp64
 template <class T>
-__global__ void __launch_bounds__(256) k_dot16(size_t m, const typename Store16<T>::type* v, const T* w, RedSlot red) {
-  double acc[2] = {0.0, 0.0};
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < m; i += (size_t)gridDim.x * blockDim.x) {
-    const T a = Store16<T>::get(v[i]);
-    const T b = ldg(w + i);
-    if constexpr (is_cplx<T>) {
-      cdot_acc(acc, a, b);
-    } else {
-      acc[0] = __fma_rn((double)a, (double)b, acc[0]);
-    }
+__device__ __forceinline__ void dot16_acc(double (&acc)[2], T a, T b) {
+  if constexpr (is_cplx<T>) {
+    cdot_acc(acc, a, b);
+  } else {
+    acc[0] = __fma_rn((double)a, (double)b, acc[0]);
   }
+}
+template <class T>
+__global__ void __launch_bounds__(256) k_dot16(size_t m, const typename Store16<T>::type* v, const T* w, RedSlot red) {
+  pdl_wait();
+  pdl_trigger();
+  double acc[2] = {0.0, 0.0};
+  each4(
+      m,
+      [&](size_t i) {
+        T a[4], b[4];
+        ld16x4<T>(v + i, a);
+        ldT4(w + i, b);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) dot16_acc(acc, a[e], b[e]);
+      },
+      [&](size_t i) { dot16_acc(acc, Store16<T>::get(v[i]), ldg(w + i)); });
   grid_reduce<2>(acc, red);
 }
 // w -= h * v16
 template <class T>
+__device__ __forceinline__ void vaxmy16_body(size_t m, T h, const typename Store16<T>::type* v, T* w) {
+  each4(
+      m,
+      [&](size_t i) {
+        T a[4], x[4];
+        ld16x4<T>(v + i, a);
+        ldT4rw(w + i, x);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) x[e] = xsub(x[e], xmul(h, a[e]));
+        stT4(w + i, x);
+      },
+      [&](size_t i) { w[i] = xsub(w[i], xmul(h, Store16<T>::get(v[i]))); });
+}
+template <class T>
 __global__ void __launch_bounds__(256) k_vaxmy16(size_t m, T h, const typename Store16<T>::type* v, T* w) {
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < m; i += (size_t)gridDim.x * blockDim.x)
-    w[i] = xsub(w[i], xmul(h, Store16<T>::get(v[i])));
+  pdl_wait();
+  pdl_trigger();
+  vaxmy16_body(m, h, v, w);
+}
+// the same with h = conj(v16).w formed on the device from the dot's tuples in
+// the host's order and rounding (krylov.cpp: H((R)re, (R)im)); block 0 also
+// reports the fp64 sums to hout (host-mapped) for the host's Givens update.
+template <class T>
+__global__ void __launch_bounds__(256) k_vaxmy16_dev(size_t m, const double* tup, int nt,
+                                                     const typename Store16<T>::type* v, T* w, double* hout) {
+  pdl_wait();
+  pdl_trigger();
+  using R = real_t<T>;
+  const double re = sum_partials(tup, nt, 0);
+  const double im = is_cplx<T> ? sum_partials(tup, nt, 1) : 0.0;
+  T h;
+  if constexpr (is_cplx<T>)
+    h = T{(R)re, (R)im};
+  else
+    h = (R)re;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    hout[0] = re;
+    hout[1] = im;
+  }
+  vaxmy16_body(m, h, v, w);
+}
+// w = widen(v16) (exact)
+template <class T>
+__global__ void __launch_bounds__(256) k_widen16(size_t m, const typename Store16<T>::type* v, T* w) {
+  pdl_wait();
+  pdl_trigger();
+  each4(
+      m,
+      [&](size_t i) {
+        T a[4];
+        ld16x4<T>(v + i, a);
+        stT4(w + i, a);
+      },
+      [&](size_t i) { w[i] = Store16<T>::get(v[i]); });
 }
 // xc += y_j * v16_j (one basis vector per launch)
 template <class T>
 __global__ void __launch_bounds__(256) k_axpy16(size_t m, T y, const typename Store16<T>::type* v, T* xc) {
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < m; i += (size_t)gridDim.x * blockDim.x)
-    xc[i] = xadd(xc[i], xmul(y, Store16<T>::get(v[i])));
+  pdl_wait();
+  pdl_trigger();
+  each4(
+      m,
+      [&](size_t i) {
+        T a[4], x[4];
+        ld16x4<T>(v + i, a);
+        ldT4rw(xc + i, x);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) x[e] = xadd(x[e], xmul(y, a[e]));
+        stT4(xc + i, x);
+      },
+      [&](size_t i) { xc[i] = xadd(xc[i], xmul(y, Store16<T>::get(v[i]))); });
 }
 
 template <class T>
 void basis16_scale(size_t m, const T* w, T s, void* v, cudaStream_t st) {
-  k_vscale16<T><<<grid_for(m, 256, 8), 256, 0, st>>>(m, w, s, (typename Store16<T>::type*)v);
+  launch_pdl(k_vscale16<T>, dim3(grid_for(m / 4 + 1, 256, 8)), dim3(256), 0, st, m, w, s,
+             (typename Store16<T>::type*)v);
   LAUNCHED("basis16_scale");
 }
 template <class T>
 void basis16_dot(size_t m, const void* v, const T* w, const RedSlot& red, cudaStream_t st) {
-  k_dot16<T><<<grid_for(m, 256, 4), 256, 0, st>>>(m, (const typename Store16<T>::type*)v, w, red);
-  note_partials(red, grid_for(m, 256, 4));
+  const unsigned g = grid_for(m / 4 + 1, 256, 4);  // (fewer tuples for the consumer's sum)
+  launch_pdl(k_dot16<T>, dim3(g), dim3(256), 0, st, m, (const typename Store16<T>::type*)v, w, red);
+  note_partials(red, g);
   LAUNCHED("basis16_dot");
 }
 template <class T>
 void basis16_axmy(size_t m, T h, const void* v, T* w, cudaStream_t st) {
-  k_vaxmy16<T><<<grid_for(m, 256, 8), 256, 0, st>>>(m, h, (const typename Store16<T>::type*)v, w);
+  launch_pdl(k_vaxmy16<T>, dim3(grid_for(m / 4 + 1, 256, 8)), dim3(256), 0, st, m, h,
+             (const typename Store16<T>::type*)v, w);
   LAUNCHED("basis16_axmy");
 }
 template <class T>
+void basis16_axmy_dev(size_t m, const RedSlot& h_tuples, const void* v, T* w, double* hout, cudaStream_t st) {
+  if (!h_tuples.dpart || *h_tuples.count <= 0) MPRKB_THROW(10, "basis16_axmy_dev: slot has no device tuples");
+  launch_pdl(k_vaxmy16_dev<T>, dim3(grid_for(m / 4 + 1, 256, 8)), dim3(256), 0, st, m, (const double*)h_tuples.dpart,
+             *h_tuples.count, (const typename Store16<T>::type*)v, w, hout);
+  LAUNCHED("basis16_axmy");
+}
+// xc = x; xc += y_j v16_j for j in order (krylov.hpp:223-226): every basis
+// vector read once, the same per-element rounding sequence as j axpys
+constexpr int kMaxBasis16 = 128;
+template <class T>
+struct Basis16Args {
+  const void* v[kMaxBasis16];
+  T y[kMaxBasis16];
+};
+template <class T>
+__global__ void __launch_bounds__(256) k_candidate16(size_t m, const T* x, int cols, const Basis16Args<T>* args, T* xc) {
+  pdl_wait();
+  pdl_trigger();
+  using S = typename Store16<T>::type;
+  each4(
+      m,
+      [&](size_t i) {
+        T acc[4];
+        ldT4(x + i, acc);
+        for (int j = 0; j < cols; ++j) {
+          T a[4];
+          ld16x4<T>(static_cast<const S*>(args->v[j]) + i, a);
+          const T y = args->y[j];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[e] = xadd(acc[e], xmul(y, a[e]));
+        }
+        stT4(xc + i, acc);
+      },
+      [&](size_t i) {
+        T acc = ldg(x + i);
+        for (int j = 0; j < cols; ++j)
+          acc = xadd(acc, xmul(args->y[j], Store16<T>::get(static_cast<const S*>(args->v[j])[i])));
+        xc[i] = acc;
+      });
+}
+template <class T>
+void basis16_candidate(size_t m, const T* x, void* const* basis, const T* y, int cols, T* xc, cudaStream_t st) {
+  static thread_local Basis16Args<T>* d_args = nullptr;
+  static thread_local Basis16Args<T>* h_args = nullptr;
+  if (cols > kMaxBasis16) MPRKB_THROW(1, "gmres: basis larger than 128 vectors is not supported");
+  if (!d_args) {
+    CUDA_CHECK(cudaMalloc(&d_args, sizeof(Basis16Args<T>)));
+    CUDA_CHECK(cudaMallocHost(&h_args, sizeof(Basis16Args<T>)));
+  }
+  CUDA_CHECK(cudaStreamSynchronize(st));  // the previous use of the staging block has finished
+  for (int j = 0; j < cols; ++j) {
+    h_args->v[j] = basis[j];
+    h_args->y[j] = y[j];
+  }
+  CUDA_CHECK(cudaMemcpyAsync(d_args, h_args, sizeof(Basis16Args<T>), cudaMemcpyHostToDevice, st));
+  launch_pdl(k_candidate16<T>, dim3(grid_for(m / 4 + 1, 256, 8)), dim3(256), 0, st, m, x, cols,
+             (const Basis16Args<T>*)d_args, xc);
+  LAUNCHED("basis16_candidate");
+}
+
+template <class T>
+void basis16_widen(size_t m, const void* v, T* w, cudaStream_t st) {
+  launch_pdl(k_widen16<T>, dim3(grid_for(m / 4 + 1, 256, 8)), dim3(256), 0, st, m,
+             (const typename Store16<T>::type*)v, w);
+  LAUNCHED("basis16_widen");
+}
+template <class T>
 void basis16_axpy(size_t m, T y, const void* v, T* xc, cudaStream_t st) {
-  k_axpy16<T><<<grid_for(m, 256, 8), 256, 0, st>>>(m, y, (const typename Store16<T>::type*)v, xc);
+  launch_pdl(k_axpy16<T>, dim3(grid_for(m / 4 + 1, 256, 8)), dim3(256), 0, st, m, y,
+             (const typename Store16<T>::type*)v, xc);
   LAUNCHED("basis16_axpy");
 }
 
@@ -481,7 +698,10 @@ void cast_f64_to_storage(size_t m, const double* src, int storage, void* dst, cu
   template void basis16_scale<T>(size_t, const T*, T, void*, cudaStream_t);                              \
   template void basis16_dot<T>(size_t, const void*, const T*, const RedSlot&, cudaStream_t);             \
   template void basis16_axmy<T>(size_t, T, const void*, T*, cudaStream_t);                               \
-  template void basis16_axpy<T>(size_t, T, const void*, T*, cudaStream_t);
+  template void basis16_axmy_dev<T>(size_t, const RedSlot&, const void*, T*, double*, cudaStream_t);      \
+  template void basis16_axpy<T>(size_t, T, const void*, T*, cudaStream_t);                               \
+  template void basis16_widen<T>(size_t, const void*, T*, cudaStream_t);                                 \
+  template void basis16_candidate<T>(size_t, const T*, void* const*, const T*, int, T*, cudaStream_t);
 
 INST_EXT(float)
 INST_EXT(double)

@@ -163,6 +163,13 @@ std::array<double, 2> global_dot(KrylovWork<T>& w, bool conj, const T* a, const 
 template <class T>
 KrylovWork<T>::KrylovWork(size_t m) : red(4), m_(m) {
   for (auto& v : vecs_) v.alloc(m * sizeof(T));
+  CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&h_host), sizeof(double) * 2 * kMaxH, cudaHostAllocMapped));
+  CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h_dev), h_host, 0));
+}
+
+template <class T>
+KrylovWork<T>::~KrylovWork() {
+  if (h_host) cudaFreeHost(h_host);
 }
 
 template <class T>
@@ -527,8 +534,7 @@ void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num,
       std::vector<T> yd(cols);
       for (int j = 0; j < cols; ++j) yd[j] = to_dev<T>(y[j]);
       if (b16) {
-        CUDA_CHECK(cudaMemcpyAsync(dst, x, m * sizeof(T), cudaMemcpyDeviceToDevice, st));
-        for (int j = 0; j < cols; ++j) basis16_axpy<T>(m, yd[j], basis16[j], dst, st);
+        basis16_candidate<T>(m, x, basis16.data(), yd.data(), cols, dst, st);
       } else {
         candidate<T>(m, x, basis.data(), yd.data(), cols, dst, st);
       }
@@ -540,8 +546,7 @@ void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num,
     for (; k < kmax;) {
       const T* vk;
       if (b16) {  // the operator reads the basis vector widened to T (exact)
-        CUDA_CHECK(cudaMemsetAsync(wt, 0, m * sizeof(T), st));
-        basis16_axpy<T>(m, to_dev<T>(scast<H>(1.0)), basis16[k], wt, st);
+        basis16_widen<T>(m, basis16[k], wt, st);
         vk = wt;
       } else {
         vk = basis[k];
@@ -549,7 +554,19 @@ void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num,
       op(vk, t);
       pre(t, wv);
       std::vector<H> h(k + 2, H{});
-      for (int j = 0; j <= k; ++j) {  // modified Gram-Schmidt
+      // fp16 basis, one rank: each h_j is formed on the device from its dot's
+      // tuples (the host's sum order and rounding) and consumed there, so the
+      // whole sweep runs without a round trip; the host reads the h_j after
+      // the norm's synchronize.
+      const bool dev_h = b16 && (!w.comm || w.comm->size() == 1) && k + 1 <= KrylovWork<T>::kMaxH;
+      if (dev_h) {
+        const RedSlot sd = w.red.slot_dev(0);
+        for (int j = 0; j <= k; ++j) {
+          basis16_dot<T>(m, basis16[j], wv, sd, st);
+          basis16_axmy_dev<T>(m, sd, basis16[j], wv, w.h_dev + 2 * j, st);
+        }
+      }
+      for (int j = 0; j <= k && !dev_h; ++j) {  // modified Gram-Schmidt
         H hj;
         if (b16) {
           basis16_dot<T>(m, basis16[j], wv, s0, st);
@@ -567,6 +584,14 @@ void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num,
         }
       }
       const R wnorm = norm2(wv);
+      if (dev_h)
+        for (int j = 0; j <= k; ++j) {
+          const volatile double* hv = w.h_host + 2 * j;
+          if constexpr (is_cplx<T>)
+            h[j] = H((R)hv[0], (R)hv[1]);
+          else
+            h[j] = (R)hv[0];
+        }
       h[k + 1] = scast<H>(static_cast<double>(wnorm));
       const bool happy = !(static_cast<double>(wnorm) > 0.0);
 

@@ -65,7 +65,15 @@ template <class T>
 class KrylovWork {
  public:
   explicit KrylovWork(size_t m);
+  ~KrylovWork();
+  KrylovWork(const KrylovWork&) = delete;
+  KrylovWork& operator=(const KrylovWork&) = delete;
   T* v(int i) { return vecs_[i].template as<T>(); }
+  // Gram-Schmidt coefficients reported by the device (host-mapped, 2 doubles
+  // per basis vector): host view / device alias
+  double* h_host = nullptr;
+  double* h_dev = nullptr;
+  static constexpr int kMaxH = 128;
   T* basis(int j);
   void* basis16(int j);  // fp16 storage (2 x fp16 for complex)
   size_t size() const { return m_; }

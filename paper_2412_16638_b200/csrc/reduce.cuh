@@ -71,8 +71,19 @@ __device__ __forceinline__ double sum_partials(const double* dp, int n, int c) {
   const int t = threadIdx.x;
   __syncthreads();
   if (t < kRedLanes) {
+    // (loads issued four at a time, added in the same sequential order)
     double s = 0.0;
-    for (int b = t; b < n; b += kRedLanes) s += __ldcg(dp + 2 * (size_t)b + c);
+    int b = t;
+    for (; b + 3 * kRedLanes < n; b += 4 * kRedLanes) {
+      const double v0 = __ldcg(dp + 2 * (size_t)b + c), v1 = __ldcg(dp + 2 * (size_t)(b + kRedLanes) + c);
+      const double v2 = __ldcg(dp + 2 * (size_t)(b + 2 * kRedLanes) + c);
+      const double v3 = __ldcg(dp + 2 * (size_t)(b + 3 * kRedLanes) + c);
+      s += v0;
+      s += v1;
+      s += v2;
+      s += v3;
+    }
+    for (; b < n; b += kRedLanes) s += __ldcg(dp + 2 * (size_t)b + c);
     lanes[t] = s;
   }
   __syncthreads();
