@@ -336,6 +336,54 @@ void vaxmy(size_t m, T h, const T* v, T* w, cudaStream_t st) {
   LAUNCHED("vaxmy");
 }
 
+// h = (conj) dot from its device tuples, summed and rounded as the host does
+// (krylov.cpp dotc: H((R)re, (R)im)), stored for the next kernel and reported
+// to the host (hout, host-mapped): one 128-thread CTA
+template <class T>
+__global__ void __launch_bounds__(128) k_finish_h(const double* tup, int nt, T* h, double* hout) {
+  pdl_wait();
+  pdl_trigger();
+  using R = real_t<T>;
+  const double re = sum_partials(tup, nt, 0);
+  const double im = is_cplx<T> ? sum_partials(tup, nt, 1) : 0.0;
+  if (threadIdx.x == 0) {
+    if constexpr (is_cplx<T>)
+      *h = T{(R)re, (R)im};
+    else
+      *h = (R)re;
+    hout[0] = re;
+    hout[1] = im;
+  }
+}
+template <class T>
+void finish_h(const RedSlot& h_tuples, T* h, double* hout, cudaStream_t st) {
+  if (!h_tuples.dpart || *h_tuples.count <= 0) MPRKB_THROW(10, "finish_h: slot has no device tuples");
+  launch_pdl(k_finish_h<T>, dim3(1), dim3(128), 0, st, (const double*)h_tuples.dpart, *h_tuples.count, h, hout);
+  LAUNCHED("finish_h");
+}
+// w -= (*h) v  (h on the device: finish_h)
+template <class T>
+__global__ void __launch_bounds__(kBlock) k_vaxmy_hp(size_t m, const T* hp, const T* v, T* w) {
+  pdl_wait();
+  pdl_trigger();
+  const T h = *hp;
+  for_each4(
+      m,
+      [&](size_t i) {
+        V4<T> a = ld4rw(w + i);
+        const V4<T> b = ld4(v + i);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) a.x[e] = xsub(a.x[e], xmul(h, b.x[e]));
+        st4(w + i, a);
+      },
+      [&](size_t i) { w[i] = xsub(w[i], xmul(h, ldg(v + i))); });
+}
+template <class T>
+void vaxmy_hp(size_t m, const T* h, const T* v, T* w, cudaStream_t st) {
+  launch_pdl(k_vaxmy_hp<T>, dim3(wave(m)), dim3(kBlock), 0, st, m, h, v, w);
+  LAUNCHED("vaxmy");
+}
+
 constexpr int kMaxBasis = 128;
 template <class T>
 struct BasisArgs {
@@ -664,6 +712,8 @@ void slab_transpose_rows(int n, int nz, int ny, int P, size_t elem, const void* 
   template void vsub<T>(size_t, const T*, const T*, T*, const RedSlot*, cudaStream_t);               \
   template void vscale<T>(size_t, const T*, T, T*, cudaStream_t);                                    \
   template void vaxmy<T>(size_t, T, const T*, T*, cudaStream_t);                                     \
+  template void finish_h<T>(const RedSlot&, T*, double*, cudaStream_t);                              \
+  template void vaxmy_hp<T>(size_t, const T*, const T*, T*, cudaStream_t);                           \
   template void candidate<T>(size_t, const T*, const T* const*, const T*, int, T*, cudaStream_t);
 
 INST_BLAS(float)

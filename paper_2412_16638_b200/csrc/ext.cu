@@ -525,27 +525,12 @@ __global__ void __launch_bounds__(256) k_vaxmy16(size_t m, T h, const typename S
   pdl_trigger();
   vaxmy16_body(m, h, v, w);
 }
-// the same with h = conj(v16).w formed on the device from the dot's tuples in
-// the host's order and rounding (krylov.cpp: H((R)re, (R)im)); block 0 also
-// reports the fp64 sums to hout (host-mapped) for the host's Givens update.
+// the same with h on the device (finish_h)
 template <class T>
-__global__ void __launch_bounds__(256) k_vaxmy16_dev(size_t m, const double* tup, int nt,
-                                                     const typename Store16<T>::type* v, T* w, double* hout) {
+__global__ void __launch_bounds__(256) k_vaxmy16_hp(size_t m, const T* hp, const typename Store16<T>::type* v, T* w) {
   pdl_wait();
   pdl_trigger();
-  using R = real_t<T>;
-  const double re = sum_partials(tup, nt, 0);
-  const double im = is_cplx<T> ? sum_partials(tup, nt, 1) : 0.0;
-  T h;
-  if constexpr (is_cplx<T>)
-    h = T{(R)re, (R)im};
-  else
-    h = (R)re;
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    hout[0] = re;
-    hout[1] = im;
-  }
-  vaxmy16_body(m, h, v, w);
+  vaxmy16_body(m, *hp, v, w);
 }
 // w = widen(v16) (exact)
 template <class T>
@@ -599,10 +584,9 @@ void basis16_axmy(size_t m, T h, const void* v, T* w, cudaStream_t st) {
   LAUNCHED("basis16_axmy");
 }
 template <class T>
-void basis16_axmy_dev(size_t m, const RedSlot& h_tuples, const void* v, T* w, double* hout, cudaStream_t st) {
-  if (!h_tuples.dpart || *h_tuples.count <= 0) MPRKB_THROW(10, "basis16_axmy_dev: slot has no device tuples");
-  launch_pdl(k_vaxmy16_dev<T>, dim3(grid_for(m / 4 + 1, 256, 8)), dim3(256), 0, st, m, (const double*)h_tuples.dpart,
-             *h_tuples.count, (const typename Store16<T>::type*)v, w, hout);
+void basis16_axmy_hp(size_t m, const T* h, const void* v, T* w, cudaStream_t st) {
+  launch_pdl(k_vaxmy16_hp<T>, dim3(grid_for(m / 4 + 1, 256, 8)), dim3(256), 0, st, m, h,
+             (const typename Store16<T>::type*)v, w);
   LAUNCHED("basis16_axmy");
 }
 // xc = x; xc += y_j v16_j for j in order (krylov.hpp:223-226): every basis
@@ -698,7 +682,7 @@ void cast_f64_to_storage(size_t m, const double* src, int storage, void* dst, cu
   template void basis16_scale<T>(size_t, const T*, T, void*, cudaStream_t);                              \
   template void basis16_dot<T>(size_t, const void*, const T*, const RedSlot&, cudaStream_t);             \
   template void basis16_axmy<T>(size_t, T, const void*, T*, cudaStream_t);                               \
-  template void basis16_axmy_dev<T>(size_t, const RedSlot&, const void*, T*, double*, cudaStream_t);      \
+  template void basis16_axmy_hp<T>(size_t, const T*, const void*, T*, cudaStream_t);                    \
   template void basis16_axpy<T>(size_t, T, const void*, T*, cudaStream_t);                               \
   template void basis16_widen<T>(size_t, const void*, T*, cudaStream_t);                                 \
   template void basis16_candidate<T>(size_t, const T*, void* const*, const T*, int, T*, cudaStream_t);

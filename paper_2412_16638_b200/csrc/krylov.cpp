@@ -558,12 +558,24 @@ void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num,
       // tuples (the host's sum order and rounding) and consumed there, so the
       // whole sweep runs without a round trip; the host reads the h_j after
       // the norm's synchronize.
-      const bool dev_h = b16 && (!w.comm || w.comm->size() == 1) && k + 1 <= KrylovWork<T>::kMaxH;
+      // (working-precision basis: the same in FAST numerics)
+      const char* dh_env = std::getenv("MPRKB_GMRES_DEV_H");  // 0: never, 2: also the working-precision basis
+      const int dh = dh_env ? dh_env[0] - '0' : 1;
+      const bool dev_h = (dh == 2 ? (b16 || num == Numerics::Fast) : (dh == 1 && b16)) &&
+                         (!w.comm || w.comm->size() == 1) && k + 1 <= KrylovWork<T>::kMaxH;
       if (dev_h) {
         const RedSlot sd = w.red.slot_dev(0);
         for (int j = 0; j <= k; ++j) {
-          basis16_dot<T>(m, basis16[j], wv, sd, st);
-          basis16_axmy_dev<T>(m, sd, basis16[j], wv, w.h_dev + 2 * j, st);
+          T* hd = w.h_val() + j;
+          if (b16) {
+            basis16_dot<T>(m, basis16[j], wv, sd, st);
+            finish_h<T>(sd, hd, w.h_dev + 2 * j, st);
+            basis16_axmy_hp<T>(m, hd, basis16[j], wv, st);
+          } else {
+            dot_conj<T>(m, basis[j], wv, sd, num, st, nullptr);
+            finish_h<T>(sd, hd, w.h_dev + 2 * j, st);
+            vaxmy_hp<T>(m, hd, basis[j], wv, st);
+          }
         }
       }
       for (int j = 0; j <= k && !dev_h; ++j) {  // modified Gram-Schmidt

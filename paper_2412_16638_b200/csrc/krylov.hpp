@@ -74,6 +74,10 @@ class KrylovWork {
   double* h_host = nullptr;
   double* h_dev = nullptr;
   static constexpr int kMaxH = 128;
+  T* h_val() {  // device copies of the coefficients (finish_h)
+    if (!hval_.get()) hval_.alloc(sizeof(T) * kMaxH);
+    return hval_.template as<T>();
+  }
   T* basis(int j);
   void* basis16(int j);  // fp16 storage (2 x fp16 for complex)
   size_t size() const { return m_; }
@@ -86,6 +90,7 @@ class KrylovWork {
   size_t m_;
   DevBuf vecs_[4];
   std::vector<DevBuf> basis_, basis16_;
+  DevBuf hval_;
 };
 
 // x_alt (optional): a second solution buffer.  With it the first iteration

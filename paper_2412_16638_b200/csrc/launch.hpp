@@ -161,15 +161,19 @@ template <class T>
 void basis16_dot(size_t m, const void* v, const T* w, const RedSlot& red, cudaStream_t st);
 template <class T>
 void basis16_axmy(size_t m, T h, const void* v, T* w, cudaStream_t st);
-// w -= h v16 with h = the dot's device tuples summed and rounded as the host
-// does (no round trip inside modified Gram-Schmidt); hout[0..1] <- the sums
+// *h = a (conj) dot from its device tuples, in the host's sum order and
+// rounding (hout[0..1] <- the fp64 sums, host-mapped); w -= (*h) v / v16
+template <class T>
+void finish_h(const RedSlot& h_tuples, T* h, double* hout, cudaStream_t st);
+template <class T>
+void vaxmy_hp(size_t m, const T* h, const T* v, T* w, cudaStream_t st);
+template <class T>
+void basis16_axmy_hp(size_t m, const T* h, const void* v, T* w, cudaStream_t st);
 template <class T>
 void basis16_widen(size_t m, const void* v, T* w, cudaStream_t st);  // w = widen(v16), exact
 // xc = x + sum_j y_j v16_j (j ascending, one pass)
 template <class T>
 void basis16_candidate(size_t m, const T* x, void* const* basis, const T* y, int cols, T* xc, cudaStream_t st);
-template <class T>
-void basis16_axmy_dev(size_t m, const RedSlot& h_tuples, const void* v, T* w, double* hout, cudaStream_t st);
 template <class T>
 void basis16_axpy(size_t m, T y, const void* v, T* xc, cudaStream_t st);
 void cast_f64_to_storage(size_t m, const double* src, int storage, void* dst, cudaStream_t st);

@@ -88,7 +88,13 @@ __device__ __forceinline__ double sum_partials(const double* dp, int n, int c) {
   }
   __syncthreads();
   double tot = 0.0;
-  for (int l = 0; l < kRedLanes; ++l) tot += lanes[l];
+  for (int l = 0; l < kRedLanes; l += 16) {  // (smem reads batched, adds in order)
+    double x[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) x[u] = lanes[l + u];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) tot += x[u];
+  }
   return tot;
 }
 
