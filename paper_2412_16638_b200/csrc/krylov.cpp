@@ -375,8 +375,20 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
           pre(r, z);
           dot_real<T>(m, r, z, s1d, num, st);
         }
-        xpby_dev<T>(m, z, s1d, pre_fused ? 1 : 0, rz, p, st);
-        {
+        bool pq_done = false;
+        if constexpr (std::is_same_v<T, float>) {
+          if (cg_fused_supported(*S)) {  // p update + A p + p.q in one pass, p ping-ponged
+            Bracket br(timer, "stencil", st);
+            T* pn = nullptr;  // the work vector that is none of r, z, p, q
+            for (T* c : {w.v(0), w.v(1), w.v(2), w.v(3), w.spare()})
+              if (c != r && c != z && c != p && c != q) pn = c;
+            pq_fused(*S, z, p, s1d, pre_fused ? 1 : 0, rz, pn, q, s2, st);
+            p = pn;
+            pq_done = true;
+          }
+        }
+        if (!pq_done) {
+          xpby_dev<T>(m, z, s1d, pre_fused ? 1 : 0, rz, p, st);
           Bracket br(timer, "stencil", st);
           stencil_apply_dot<T>(*S, p, q, s2, st);
         }

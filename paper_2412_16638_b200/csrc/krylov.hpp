@@ -74,6 +74,10 @@ class KrylovWork {
   double* h_host = nullptr;
   double* h_dev = nullptr;
   static constexpr int kMaxH = 128;
+  T* spare() {  // a fifth work vector (the pipelined CG's ping-pong direction)
+    if (!spare_.get()) spare_.alloc(m_ * sizeof(T));
+    return spare_.template as<T>();
+  }
   T* h_val() {  // device copies of the coefficients (finish_h)
     if (!hval_.get()) hval_.alloc(sizeof(T) * kMaxH);
     return hval_.template as<T>();
@@ -90,7 +94,7 @@ class KrylovWork {
   size_t m_;
   DevBuf vecs_[4];
   std::vector<DevBuf> basis_, basis16_;
-  DevBuf hval_;
+  DevBuf hval_, spare_;
 };
 
 // x_alt (optional): a second solution buffer.  With it the first iteration

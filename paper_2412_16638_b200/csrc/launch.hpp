@@ -43,6 +43,11 @@ void stencil_apply_dot2(const StencilSpec& s, const T* p, T* q, const T* r, cons
 // x1 = x + alpha p with (||r - alpha A p||^2, ||b - A x1||^2) in red; fp32,
 // Dirichlet, undivided grid (stencil.cu k_cg_fused)
 bool cg_fused_supported(const StencilSpec& s);
+// pipelined CG: pnew = z + beta p (beta = (R)(component beta_comp of
+// beta_src's device tuples) / rz_old), q = A pnew, red <- pnew.q (fp32, same
+// support as cg_fused_update)
+void pq_fused(const StencilSpec& s, const float* z, const float* p, const RedSlot& beta_src, int beta_comp,
+              float rz_old, float* pnew, float* q, const RedSlot& red, cudaStream_t st);
 // alpha_src (nullable): take alpha = (float)rz / (float)pq from that slot's
 // device tuples (components pq, rz — stencil_apply_dot2 into a slot_dev slot)
 void cg_fused_update(const StencilSpec& s, float alpha, const RedSlot* alpha_src, const float* x, const float* p,

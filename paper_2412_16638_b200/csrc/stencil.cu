@@ -1164,6 +1164,145 @@ void cg_fused_update(const StencilSpec& sp, float alpha, const RedSlot* alpha_sr
   LAUNCHED("cg_fused_update");
 }
 
+// ---- p = z + beta p fused with q = A p, p.q (fp32, pipelined CG) -----------------
+// The pipelined CG's direction update and the next A.p pass in one: the z and
+// p planes stream through a TMA ring, p_new = z + beta p (k_xpby's rounding)
+// is formed at every loaded point, and the pass writes p_new — to a second
+// buffer, since neighbouring CTAs still read p — q = A p_new and p_new.q.
+// beta = (R)(r.z) / rz_old from the update pass's device tuples.
+__global__ void __launch_bounds__(TTHREADS)
+    k_pq_fused(const __grid_constant__ CUtensorMap zmap, const __grid_constant__ CUtensorMap pmap, int n, int nz,
+               int kc, float s, float g, const double* btup, int bn, int bcomp, float rz_old,
+               float* __restrict__ pnew, float* __restrict__ q, RedSlot red) {
+  pdl_wait();
+  pdl_trigger();
+  const float beta = __fdiv_rn(__double2float_rn(sum_partials(btup, bn, bcomp)), rz_old);
+  extern __shared__ unsigned char smem_raw[];
+  float* buf = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(buf + CG_TST * 2 * CG_SLOT);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int i0 = blockIdx.x * TI, j0 = blockIdx.y * TJ;
+  int k0, k1;
+  plane_range(nz, 0, nz, kc, k0, k1);
+  const int planes = k1 - k0 + 2;
+  constexpr uint32_t bytes = (TJ + 2) * TW * sizeof(float);
+  if (tid == 0) {
+    for (int b = 0; b < CG_TST; ++b) mbar_init(&full[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const CUtensorMap* zm = &zmap;
+  const CUtensorMap* pm = &pmap;
+  auto issue = [&](int qq) {
+    const int k = k0 - 1 + qq, sl = qq % CG_TST;
+    float* dst = buf + sl * 2 * CG_SLOT;
+    mbar_expect_tx(&full[sl], 2 * bytes);
+    tma_3d(dst, zm, i0 - 4, j0 - 1, k, &full[sl]);
+    tma_3d(dst + CG_SLOT, pm, i0 - 4, j0 - 1, k, &full[sl]);
+  };
+  if (tid == 0)
+    for (int qq = 0; qq < CG_TST && qq < planes; ++qq) issue(qq);
+  auto wait = [&](int qq) { mbar_wait(&full[qq % CG_TST], (uint32_t)(qq / CG_TST) & 1u); };
+  auto ld = [](const float* ptr) {
+    const float4 f = *reinterpret_cast<const float4*>(ptr);
+    V4<float> v;
+    v.x[0] = f.x; v.x[1] = f.y; v.x[2] = f.z; v.x[3] = f.w;
+    return v;
+  };
+  auto upd = [&](float zv, float pv) { return xadd(zv, xscale(beta, pv)); };  // k_xpby's p
+  auto upd4 = [&](const V4<float>& zv, const V4<float>& pv) {
+    V4<float> o;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o.x[e] = upd(zv.x[e], pv.x[e]);
+    return o;
+  };
+  double acc[1] = {0.0};
+  const long nn = n, n2 = nn * nn;
+  const int col = 4 + 4 * lane;
+  for (int k = k0; k < k1; ++k) {
+    const int qq = k - k0 + 1;
+    if (k == k0) {
+      wait(0);
+      wait(1);
+    }
+    wait(qq + 1);
+    const float* bm = buf + ((qq - 1) % CG_TST) * 2 * CG_SLOT;
+    const float* bc = buf + (qq % CG_TST) * 2 * CG_SLOT;
+    const float* bp = buf + ((qq + 1) % CG_TST) * 2 * CG_SLOT;
+#pragma unroll
+    for (int rr = 0; rr < TROWS; ++rr) {
+      const int row = warp * TROWS + rr;
+      const int o = (row + 1) * TW + col;
+      const V4<float> c = upd4(ld(bc + o), ld(bc + CG_SLOT + o));
+      const V4<float> ym = upd4(ld(bc + o - TW), ld(bc + CG_SLOT + o - TW));
+      const V4<float> yp = upd4(ld(bc + o + TW), ld(bc + CG_SLOT + o + TW));
+      const V4<float> zmv = upd4(ld(bm + o), ld(bm + CG_SLOT + o));
+      const V4<float> zpv = upd4(ld(bp + o), ld(bp + CG_SLOT + o));
+      float xl = shfl_up1(c.x[3]), xr = shfl_down1(c.x[0]);
+      if (lane == 0) xl = upd(bc[o - 1], bc[CG_SLOT + o - 1]);
+      if (lane == 31) xr = upd(bc[o + 4], bc[CG_SLOT + o + 4]);
+      V4<float> v;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float al = e == 0 ? xl : c.x[e - 1], ar = e == 3 ? xr : c.x[e + 1];
+        v.x[e] = point<float>(0, s, g, 0.0f, c.x[e], al, ar, ym.x[e], yp.x[e], zmv.x[e], zpv.x[e]);
+        dot_acc(acc, c.x[e], v.x[e]);  // EpiStoreDot's p.q
+      }
+      const long gi = (i0 + 4 * lane) + (long)(j0 + row) * nn + (long)k * n2;
+      st4(pnew + gi, c);
+      st4(q + gi, v);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0 && qq - 1 + CG_TST < planes) issue(qq - 1 + CG_TST);
+  }
+  grid_reduce<1>(acc, red);
+}
+
+void pq_fused(const StencilSpec& sp, const float* z, const float* p, const RedSlot& beta_src, int beta_comp,
+              float rz_old, float* pnew, float* q, const RedSlot& red, cudaStream_t st) {
+  if (!cg_fused_supported(sp)) MPRKB_THROW(10, "pq_fused: needs the TMA stencil on an undivided grid");
+  if (!beta_src.dpart || *beta_src.count <= 0) MPRKB_THROW(10, "pq_fused: beta source has no device tuples");
+  const int n = sp.n, nz = sp.nz > 0 ? sp.nz : n;
+  constexpr size_t smem = cg_fused_smem();
+  static int chunk = 0;
+  static long chunk_cols = -1;
+  static int resident = 0;
+  if (!resident) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_pq_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pq_fused, TTHREADS, smem));
+    resident = std::max(1, per_sm) * sm_count();
+  }
+  const long cols = (long)(n / TI) * (n / TJ);
+  if (cols != chunk_cols) {
+    long best_cost = -1;
+    for (int kc = 4; kc <= 64; ++kc) {
+      const long units = cols * ((nz + kc - 1) / kc);
+      const long cost = ((units + resident - 1) / resident) * (std::min(kc, nz) + 2);
+      if (best_cost < 0 || cost < best_cost) {
+        chunk = kc;
+        best_cost = cost;
+      }
+    }
+    chunk_cols = cols;
+  }
+  const cuuint64_t nn = (cuuint64_t)n;
+  const cuuint64_t dims3[3] = {nn, nn, (cuuint64_t)nz}, str3[2] = {nn * 4, nn * nn * 4};
+  const cuuint32_t box3[3] = {(cuuint32_t)TW, (cuuint32_t)(TJ + 2), 1};
+  const CUtensorMap zmap = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, z, 3, dims3, str3, box3);
+  const CUtensorMap pmap = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, p, 3, dims3, str3, box3);
+  const unsigned gz = (unsigned)((nz + chunk - 1) / chunk);
+  const dim3 grid((unsigned)(n / TI), (unsigned)(n / TJ), gz);
+  RedSlot rs = red;
+  rs.base = 0;
+  rs.total = 0;
+  launch_pdl(k_pq_fused, grid, dim3(TTHREADS), smem, st, zmap, pmap, n, nz, chunk, (float)sp.sigma, (float)sp.gamma,
+             (const double*)beta_src.dpart, *beta_src.count, beta_comp, rz_old, pnew, q, rs);
+  note_partials(rs, grid.x * grid.y * grid.z);
+  LAUNCHED("pq_fused");
+}
+
 #define INST_STENCIL(T)                                                                          \
   template void stencil_apply<T>(const StencilSpec&, const T*, T*, cudaStream_t);               \
   template void stencil_residual<T>(const StencilSpec&, const T*, const T*, T*, const RedSlot*, \
