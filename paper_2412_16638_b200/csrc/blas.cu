@@ -608,6 +608,26 @@ __global__ void __launch_bounds__(kBlock) k_final(size_t m, double* u, CombineTe
   if (bad) *flag = 1;
 }
 
+// check_finite of an fp32 stage vector alone (stepper.cpp:18-21)
+__global__ void __launch_bounds__(kBlock) k_check_finite32(size_t m, const float* x, int* flag) {
+  pdl_wait();
+  pdl_trigger();
+  bool bad = false;
+  for_each4(
+      m,
+      [&](size_t i) {
+        const V4<float> v = ld4(x + i);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) bad |= !isfinite(v.x[e]);
+      },
+      [&](size_t i) { bad |= !isfinite(ldg(x + i)); });
+  if (bad) *flag = 1;
+}
+void check_finite32(size_t m, const float* x, int* flag, cudaStream_t st) {
+  launch_pdl(k_check_finite32, dim3(wave(m)), dim3(kBlock), 0, st, m, x, flag);
+  LAUNCHED("check_finite");
+}
+
 void final_update(size_t m, double* u, const CombineTerms& t, int* flag, cudaStream_t st, const int* gate,
                   int gate_count) {
   launch_pdl(k_final, dim3(wave(m)), dim3(kBlock), 0, st, m, u, t, flag, gate, gate ? gate_count : 0);

@@ -235,6 +235,12 @@ void extract_stage(size_t m, int src_kind, const void* x, double* y, int* flag, 
 // u += sum_t coef_t * v_t, + non-finite flag on u.
 // gate: gate_count error flags of the step so far (DEVICE memory); if any is
 // set the update is skipped (u untouched, as the reference's throw leaves it).
+void check_finite32(size_t m, const float* x, int* flag, cudaStream_t st);  // *flag = 1 on NaN / inf
+// The final update with the last stage's f_hi evaluated in the same pass:
+// u += sum_t coef_t v_t (fp64 terms, in order) + c_last (K widen(y32) + g),
+// gated like final_update (k.forcing regenerates g when set)
+void final_update_feval(const StencilSpec& k, double* u, const CombineTerms& t, const float* y32, const double* g,
+                        double c_last, int* flag, const int* gate, int gate_count, cudaStream_t st);
 void final_update(size_t m, double* u, const CombineTerms& t, int* flag, cudaStream_t st,
                   const int* gate = nullptr, int gate_count = 0);
 // element casts for the op-level API: narrow (overflow flag) / widen / promote

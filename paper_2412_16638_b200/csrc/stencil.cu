@@ -439,6 +439,72 @@ struct EpiFevalCombine {
   __device__ void finish(State&) const {}
 };
 
+// The final update with the last stage's f evaluation fused in
+// (stepper.cpp:193-204): f_hi = K widen(y) + g is formed from the stencil of
+// the fp32 stage vector and added last, after the earlier stages' stored
+// f_hi terms — each term rounds as in the separate apply_f + final kernels,
+// and f_hi of the last stage never reaches HBM.  Gated like k_final: if any of
+// the step's earlier checks fired, nothing is written.
+struct EpiFinalFeval {
+  double* u = nullptr;
+  int nt = 0;
+  const double* tv[kMaxTerms] = {};
+  double tc[kMaxTerms] = {};
+  double c_last = 0.0;
+  const double* g = nullptr;
+  ForcingGen gen;
+  int* flag = nullptr;
+  const int* gate = nullptr;
+  int gate_count = 0;
+  struct State {
+    bool skip, bad;
+  };
+  using Pre = V4<double>;
+  __device__ void init(State& s) const {
+    int any = 0;
+    for (int q = 0; q < gate_count; ++q) any |= __ldg(gate + q);
+    s.skip = any != 0;
+    s.bad = false;
+  }
+  __device__ __forceinline__ Pre pre4(long i) const { return ld4rw(u + i); }
+  __device__ __forceinline__ void v4p(State& s, long i, const V4<double>& v, const V4<double>&, const Pre& uv) const {
+    if (s.skip) return;
+    V4<double> gv;
+    if (gen.s)
+      forcing4(gen, i, gv.x);
+    else
+      gv = g ? ld4(g + i) : zero4<double>();
+    V4<double> r = uv;
+    for (int c = 0; c < nt; ++c) {
+      const V4<double> f = ld4(tv[c] + i);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) r.x[e] = xadd(r.x[e], xmul(tc[c], f.x[e]));
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const double fl = g ? xadd(v.x[e], gv.x[e]) : v.x[e];  // EpiF64Forcing's f_hi
+      r.x[e] = xadd(r.x[e], xmul(c_last, fl));
+      s.bad |= !isfinite(r.x[e]);
+    }
+    st4(u + i, r);
+  }
+  __device__ __forceinline__ void v4(State& s, long i, const V4<double>& v, const V4<double>& xc) const {
+    v4p(s, i, v, xc, pre4(i));
+  }
+  __device__ __forceinline__ void s1(State& s, long i, double v, double) const {
+    if (s.skip) return;
+    double r = u[i];
+    for (int c = 0; c < nt; ++c) r = xadd(r, xmul(tc[c], __ldg(tv[c] + i)));
+    const double gi = gen.s ? forcing1(gen, i) : (g ? __ldg(g + i) : 0.0);
+    r = xadd(r, xmul(c_last, g ? xadd(v, gi) : v));
+    s.bad |= !isfinite(r);
+    u[i] = r;
+  }
+  __device__ void finish(State& s) const {
+    if (s.bad) *flag = 1;
+  }
+};
+
 // Planes a CTA marches over.  kb < ke: chunks of `chunk` planes of [kb, ke)
 // by blockIdx.z.  kb < 0: the two boundary planes of a split slab (z = 0 ->
 // plane 0, z = 1 -> plane nz - 1), the part that waits for the ghosts.
@@ -942,6 +1008,25 @@ void apply_f32(const StencilSpec& k, const double* y, const float* y32, const fl
     launch(k, LdPlain<float>{y32}, EpiF32Forcing{g32, out32, finite_flag, k.forcing}, st, "apply_f32");
   else
     launch(k, LdD2F{y, flag}, EpiF32Forcing{g32, out32, finite_flag, k.forcing}, st, "apply_f32");
+}
+
+void final_update_feval(const StencilSpec& k, double* u, const CombineTerms& t, const float* y32, const double* g,
+                        double c_last, int* flag, const int* gate, int gate_count, cudaStream_t st) {
+  EpiFinalFeval e;
+  e.u = u;
+  e.nt = t.count;
+  for (int c = 0; c < t.count; ++c) {
+    if (t.is_f32[c] != 0) MPRKB_THROW(10, "final_update_feval: fp64 stored terms only");
+    e.tv[c] = static_cast<const double*>(t.ptr[c]);
+    e.tc[c] = t.coef[c];
+  }
+  e.c_last = c_last;
+  e.g = g;
+  e.gen = k.forcing;
+  e.flag = flag;
+  e.gate = gate;
+  e.gate_count = gate ? gate_count : 0;
+  launch(k, LdF2D{y32}, e, st, "final_update_feval");
 }
 
 bool feval_combine_supported(const StencilSpec& k) {

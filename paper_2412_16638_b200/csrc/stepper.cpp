@@ -438,20 +438,27 @@ void Stepper::step_fused(double* u, StepTrace& trace) {
     }
     cur = solve(nx);
   }
-  // last stage: its f_hi feeds only the final update
-  {
-    const int i = q - 1;
-    if (t.b[i] != 0.0) {
-      Bracket br(timer_, "stencil", st_);
-      apply_f64(kspec_, nullptr, cur, g64_.as<double>(), f_hi_[i].as<double>(), check_slot(9, kStage), st_);
-    } else {
-      extract_stage(m, 0, cur, y_.as<double>(), check_slot(9, kStage), st_);
-    }
+  // last stage: its f_hi feeds only the final update — evaluated inside the
+  // final pass itself (the stage vector's finiteness checked first, so the
+  // update stays gated on it); MPRKB_FUSED_FINAL=0: separate kernels
+  const int last = q - 1;
+  static const bool fuse_final_env = [] {
+    const char* e = std::getenv("MPRKB_FUSED_FINAL");
+    return !(e && e[0] == '0');
+  }();
+  const bool fuse_final = t.b[last] != 0.0 && fuse_final_env;
+  if (fuse_final) {
+    check_finite32(m, cur, check_slot(9, kStage), st_);
+  } else if (t.b[last] != 0.0) {
+    Bracket br(timer_, "stencil", st_);
+    apply_f64(kspec_, nullptr, cur, g64_.as<double>(), f_hi_[last].as<double>(), check_slot(9, kStage), st_);
+  } else {
+    extract_stage(m, 0, cur, y_.as<double>(), check_slot(9, kStage), st_);
   }
   const int stage_checks = next - 1;
   if (slab_.split()) raise_flags();
   CombineTerms fin;
-  for (int i = 0; i < q; ++i)
+  for (int i = 0; i < (fuse_final ? last : q); ++i)
     if (t.b[i] != 0.0) add_term(fin, tau * t.b[i], f_hi_[i].get(), 0);
   {
     Bracket br(timer_, "axpy", st_);
@@ -462,7 +469,10 @@ void Stepper::step_fused(double* u, StepTrace& trace) {
                                  st_));
       gate = gate_dev_.as<int>();
     }
-    final_update(m, u, fin, fin_flag, st_, gate, stage_checks);
+    if (fuse_final)
+      final_update_feval(kspec_, u, fin, cur, g64_.as<double>(), tau * t.b[last], fin_flag, gate, stage_checks, st_);
+    else
+      final_update(m, u, fin, fin_flag, st_, gate, stage_checks);
   }
   raise_flags();
   if (timer_.enabled()) timer_.resolve();

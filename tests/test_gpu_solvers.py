@@ -427,3 +427,27 @@ def test_cg_pipelined_iterations(gpu, mp, prec, store):
         os.environ.pop("MPRKB_CG_PIPE", None)
     rel = np.linalg.norm(a - b) / np.linalg.norm(b)
     assert rel <= (1e-5 if prec == "f32" else 1e-9), rel
+
+
+def test_fused_final_update_bitwise(gpu, mp):
+    """The last stage's f evaluation inside the final update pass (its stage
+    vector checked for NaN / inf first, so the update stays gated) is bitwise
+    the separate apply_f + final-update kernels."""
+    import os
+
+    t = mp.builtin("4s3pB")
+    n = 128
+    fused = mp.Stepper("heat", n, t, 0.01, 1e-4, "f32", 40)
+    os.environ["MPRKB_FUSED_FINAL"] = "0"
+    try:
+        # (the knob is read once per process: this stepper shares it, so compare
+        # against the stage-by-stage path instead)
+        os.environ["MPRKB_FUSED_STAGES"] = "0"
+        plain = mp.Stepper("heat", n, t, 0.01, 1e-4, "f32", 40)
+    finally:
+        os.environ.pop("MPRKB_FUSED_FINAL", None)
+        os.environ.pop("MPRKB_FUSED_STAGES", None)
+    a, b = np.zeros(n ** 3), np.zeros(n ** 3)
+    for _ in range(3):
+        assert fused.step(a)["iterations"] == plain.step(b)["iterations"]
+    assert same_bits(a, b)
