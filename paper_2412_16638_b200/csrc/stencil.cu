@@ -182,7 +182,7 @@ struct EpiResidual {
   };
   using Pre = V4<T>;
   __device__ void init(State& s) const { s.v[0] = 0.0; }
-  __device__ __forceinline__ Pre pre4(long i) const { return ld4rw(b + i); }
+  __device__ __forceinline__ Pre pre4(long i) const { return ld4(b + i); }
   __device__ __forceinline__ void v4p(State& s, long i, const V4<T>& v, const V4<T>&, const Pre& bv) const {
     V4<T> o;
 #pragma unroll
@@ -242,7 +242,7 @@ struct EpiStoreDot2 {
   };
   using Pre = V4<T>;
   __device__ void init(State& s) const { s.v[0] = s.v[1] = 0.0; }
-  __device__ __forceinline__ Pre pre4(long i) const { return ld4rw(r + i); }
+  __device__ __forceinline__ Pre pre4(long i) const { return ld4(r + i); }
   __device__ __forceinline__ static double (&one(double& d))[1] { return *reinterpret_cast<double(*)[1]>(&d); }
   __device__ __forceinline__ void v4p(State& s, long i, const V4<T>& v, const V4<T>& xc, const Pre& rv) const {
     if (out) st4(out + i, v);
@@ -1135,8 +1135,8 @@ __global__ void __launch_bounds__(TTHREADS)
   V4<float> pb[TROWS], pr[TROWS];
 #pragma unroll
   for (int rr = 0; rr < TROWS; ++rr) {
-    pb[rr] = ld4rw(b + gidx(warp * TROWS + rr, k0));
-    pr[rr] = ld4rw(r + gidx(warp * TROWS + rr, k0));
+    pb[rr] = ld4(b + gidx(warp * TROWS + rr, k0));
+    pr[rr] = ld4(r + gidx(warp * TROWS + rr, k0));
   }
   for (int k = k0; k < k1; ++k) {
     const int q = k - k0 + 1;
@@ -1152,8 +1152,8 @@ __global__ void __launch_bounds__(TTHREADS)
 #pragma unroll
     for (int rr = 0; rr < TROWS; ++rr)
       if (k + 1 < k1) {
-        nb[rr] = ld4rw(b + gidx(warp * TROWS + rr, k + 1));
-        nr[rr] = ld4rw(r + gidx(warp * TROWS + rr, k + 1));
+        nb[rr] = ld4(b + gidx(warp * TROWS + rr, k + 1));
+        nr[rr] = ld4(r + gidx(warp * TROWS + rr, k + 1));
       }
 #pragma unroll
     for (int rr = 0; rr < TROWS; ++rr) {
