@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(SBX* SBY)
 }
 
 // ---- vectorised kernel (real T, n % 4 == 0) -----------------------------------------
-constexpr int VX = 32, VY = 4, VKC = 16;
+constexpr int VX = 32, VY = 8, VKC = 16;
 
 template <class Src, class Epi>
 __global__ void __launch_bounds__(VX* VY)
