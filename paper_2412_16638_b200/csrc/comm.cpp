@@ -42,10 +42,11 @@ Halo::~Halo() {
   if (arrived) cudaEventDestroy(arrived);
 }
 
-void halo_exchange(const Halo& h, const void* x, size_t elem, bool periodic, cudaStream_t st, const void* g[2]) {
+void halo_exchange(const Halo& h, const void* x, size_t elem, bool periodic, cudaStream_t st, const void* g[2],
+                   size_t offset) {
   const Slab& s = h.slab;
   const size_t plane = (size_t)s.n * s.n * elem;
-  char* lo = h.ghost.as<char>();
+  char* lo = h.ghost.as<char>() + offset;
   char* hi = lo + plane;
   const char* xs = static_cast<const char*>(x);
   s.comm->halo(xs, xs + (size_t)(s.nz - 1) * plane, lo, hi, plane, periodic, st);

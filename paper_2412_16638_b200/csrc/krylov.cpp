@@ -252,7 +252,10 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
       x_alt = nullptr;
     }
   }
-  const RedSlot s2 = fuse_first ? w.red.slot_dev(2) : w.red.slot(2), s3 = w.red.slot(3);
+  // (split grid: the tuples are this rank's — alpha needs the global sums,
+  // so the fused update waits for the host's allreduced scalars)
+  const bool dev_alpha = fuse_first && !(w.comm && w.comm->size() > 1);
+  const RedSlot s2 = dev_alpha ? w.red.slot_dev(2) : w.red.slot(2), s3 = w.red.slot(3);
   double r0;
   R rz{}, pq_first{};
   bool have_pq = false;
@@ -279,7 +282,7 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
       stencil_apply_dot2<T>(*S, z, fuse_first ? nullptr : q, r, s2, st);  // q = A z, (z.q, r.z)
     }
     if constexpr (std::is_same_v<T, float>) {
-      if (fuse_first) {
+      if (dev_alpha) {
         // the first update speculatively, alpha formed on the device from the
         // tuples above: it only writes x_alt, so whatever the host decides
         // below (r0 already small, breakdown) x is untouched
@@ -291,8 +294,20 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
     double v[3];
     w.red.result(0, 1, &v[0]);
     w.red.result(2, 2, &v[1]);
-    if (fuse_first) w.red.result(3, 2, fused_v);
+    if (dev_alpha) w.red.result(3, 2, fused_v);
     if (w.comm && w.comm->size() > 1) w.comm->allreduce_sum(v, 3);
+    if constexpr (std::is_same_v<T, float>) {
+      if (fuse_first && !dev_alpha) {  // split grid: the same pass with the global alpha
+        const R a = (R)v[2] / (R)v[1];
+        {
+          Bracket br(timer, "stencil", st);
+          cg_fused_update(*S, a, nullptr, x, z, b, r, x_alt, s3, st);
+        }
+        stream_sync(st);
+        w.red.result(3, 2, fused_v);
+        w.comm->allreduce_sum(fused_v, 2);
+      }
+    }
     r0 = (double)std::sqrt((R)v[0]);
     rz = (R)v[2];
     pq_first = (R)v[1];
@@ -377,7 +392,7 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
         }
         bool pq_done = false;
         if constexpr (std::is_same_v<T, float>) {
-          if (cg_fused_supported(*S)) {  // p update + A p + p.q in one pass, p ping-ponged
+          if (pq_fused_ok(*S)) {  // p update + A p + p.q in one pass, p ping-ponged
             Bracket br(timer, "stencil", st);
             T* pn = nullptr;  // the work vector that is none of r, z, p, q
             for (T* c : {w.v(0), w.v(1), w.v(2), w.v(3), w.spare()})

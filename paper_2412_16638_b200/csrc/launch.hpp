@@ -13,7 +13,9 @@ struct Halo;  // comm.hpp: slab + ghost-plane scratch of a split grid
 // Exchange the boundary planes of the local slab `x` (elements of `elem`
 // bytes) with the k-neighbours; g[0]/g[1] receive the lo/hi ghost planes
 // (null where the domain ends: Dirichlet zero).  Stream-ordered on st.
-void halo_exchange(const Halo& h, const void* x, size_t elem, bool periodic, cudaStream_t st, const void* g[2]);
+// offset: bytes into the ghost buffer (two exchanges in flight side by side)
+void halo_exchange(const Halo& h, const void* x, size_t elem, bool periodic, cudaStream_t st, const void* g[2],
+                   size_t offset = 0);
 
 struct StencilSpec {
   int n = 0;
@@ -43,6 +45,7 @@ void stencil_apply_dot2(const StencilSpec& s, const T* p, T* q, const T* r, cons
 // x1 = x + alpha p with (||r - alpha A p||^2, ||b - A x1||^2) in red; fp32,
 // Dirichlet, undivided grid (stencil.cu k_cg_fused)
 bool cg_fused_supported(const StencilSpec& s);
+bool pq_fused_ok(const StencilSpec& s);  // pq_fused: additionally an undivided grid
 // pipelined CG: pnew = z + beta p (beta = (R)(component beta_comp of
 // beta_src's device tuples) / rz_old), q = A pnew, red <- pnew.q (fp32, same
 // support as cg_fused_update)

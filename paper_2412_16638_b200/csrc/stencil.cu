@@ -1077,9 +1077,11 @@ constexpr int CG_SLOT = tma_slot_elems<float>(), CG_TST = 4;  // 3 planes in use
 constexpr size_t cg_fused_smem() { return (size_t)CG_TST * 2 * CG_SLOT * sizeof(float) + CG_TST * sizeof(uint64_t) + 128; }
 
 __global__ void __launch_bounds__(TTHREADS)
-    k_cg_fused(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap pmap, int n, int nz,
-               int kc, float s, float g, float alpha, const double* apart, int an, const float* __restrict__ b,
-               const float* __restrict__ r, float* __restrict__ x1, RedSlot red) {
+    k_cg_fused(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap pmap,
+               const __grid_constant__ CUtensorMap xlo, const __grid_constant__ CUtensorMap xhi,
+               const __grid_constant__ CUtensorMap plo, const __grid_constant__ CUtensorMap phi, int has_lo,
+               int has_hi, int n, int nz, int kc, float s, float g, float alpha, const double* apart, int an,
+               const float* __restrict__ b, const float* __restrict__ r, float* __restrict__ x1, RedSlot red) {
   pdl_wait();
   pdl_trigger();
   if (apart) {
@@ -1105,12 +1107,24 @@ __global__ void __launch_bounds__(TTHREADS)
   __syncthreads();
   const CUtensorMap* xm = &xmap;
   const CUtensorMap* pm = &pmap;
-  auto issue = [&](int q) {
+  const CUtensorMap* xl = &xlo;
+  const CUtensorMap* xh = &xhi;
+  const CUtensorMap* pl = &plo;
+  const CUtensorMap* ph = &phi;
+  auto issue = [&](int q) {  // (split grid: planes -1 / nz from the ghost planes)
     const int k = k0 - 1 + q, sl = q % CG_TST;
     float* dst = buf + sl * 2 * CG_SLOT;
     mbar_expect_tx(&full[sl], 2 * bytes);
-    tma_3d(dst, xm, i0 - 4, j0 - 1, k, &full[sl]);
-    tma_3d(dst + CG_SLOT, pm, i0 - 4, j0 - 1, k, &full[sl]);
+    if (k < 0 && has_lo) {
+      tma_2d(dst, xl, i0 - 4, j0 - 1, &full[sl]);
+      tma_2d(dst + CG_SLOT, pl, i0 - 4, j0 - 1, &full[sl]);
+    } else if (k >= nz && has_hi) {
+      tma_2d(dst, xh, i0 - 4, j0 - 1, &full[sl]);
+      tma_2d(dst + CG_SLOT, ph, i0 - 4, j0 - 1, &full[sl]);
+    } else {
+      tma_3d(dst, xm, i0 - 4, j0 - 1, k, &full[sl]);
+      tma_3d(dst + CG_SLOT, pm, i0 - 4, j0 - 1, k, &full[sl]);
+    }
   };
   if (tid == 0)
     for (int q = 0; q < CG_TST && q < planes; ++q) issue(q);
@@ -1199,13 +1213,15 @@ __global__ void __launch_bounds__(TTHREADS)
   grid_reduce<2>(acc, red);
 }
 
-bool cg_fused_supported(const StencilSpec& k) {
-  return k.stencil == 0 && k.n % TI == 0 && k.halo == nullptr && tma_stencil_enabled();
+bool cg_fused_supported(const StencilSpec& k) {  // (k_cg_fused: ghost planes on a split grid)
+  return k.stencil == 0 && k.n % TI == 0 && tma_stencil_enabled();
 }
+static bool pq_fused_supported(const StencilSpec& k) { return cg_fused_supported(k) && k.halo == nullptr; }
+bool pq_fused_ok(const StencilSpec& k) { return pq_fused_supported(k); }
 
 void cg_fused_update(const StencilSpec& sp, float alpha, const RedSlot* alpha_src, const float* x, const float* p,
                      const float* b, const float* r, float* x1, const RedSlot& red, cudaStream_t st) {
-  if (!cg_fused_supported(sp)) MPRKB_THROW(10, "cg_fused_update: needs the TMA stencil on an undivided grid");
+  if (!cg_fused_supported(sp)) MPRKB_THROW(10, "cg_fused_update: needs the TMA stencil (Dirichlet, n % 128 == 0)");
   const int n = sp.n, nz = sp.nz > 0 ? sp.nz : n;
   constexpr size_t smem = cg_fused_smem();
   static int chunk = 0;
@@ -1235,6 +1251,35 @@ void cg_fused_update(const StencilSpec& sp, float alpha, const RedSlot* alpha_sr
   const cuuint32_t box3[3] = {(cuuint32_t)TW, (cuuint32_t)(TJ + 2), 1};
   const CUtensorMap xmap = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, x, 3, dims3, str3, box3);
   const CUtensorMap pmap = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, p, 3, dims3, str3, box3);
+  // split grid: both operands' boundary planes from the k-neighbours (x and p
+  // ghosts side by side in the halo buffer), before the pass
+  CUtensorMap gm[4] = {xmap, xmap, xmap, xmap};  // x lo, x hi, p lo, p hi
+  int has_lo = 0, has_hi = 0;
+  if (sp.halo) {
+    const Halo& h = *sp.halo;
+    const size_t plane = (size_t)n * n * sizeof(float);
+    if (h.ghost.bytes() < 4 * plane) MPRKB_THROW(10, "cg_fused_update: ghost buffer too small");
+    CUDA_CHECK(cudaEventRecord(h.ready, st));
+    CUDA_CHECK(cudaStreamWaitEvent(h.cs, h.ready, 0));
+    const void* gx[2];
+    const void* gp[2];
+    halo_exchange(h, x, sizeof(float), false, h.cs, gx, 0);
+    halo_exchange(h, p, sizeof(float), false, h.cs, gp, 2 * plane);
+    CUDA_CHECK(cudaEventRecord(h.arrived, h.cs));
+    CUDA_CHECK(cudaStreamWaitEvent(st, h.arrived, 0));
+    const cuuint64_t dims2[2] = {nn, nn}, str2[1] = {nn * 4};
+    const cuuint32_t box2[2] = {(cuuint32_t)TW, (cuuint32_t)(TJ + 2)};
+    has_lo = gx[0] != nullptr;
+    has_hi = gx[1] != nullptr;
+    if (has_lo) {
+      gm[0] = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, gx[0], 2, dims2, str2, box2);
+      gm[2] = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, gp[0], 2, dims2, str2, box2);
+    }
+    if (has_hi) {
+      gm[1] = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, gx[1], 2, dims2, str2, box2);
+      gm[3] = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, gp[1], 2, dims2, str2, box2);
+    }
+  }
   const unsigned gz = (unsigned)((nz + chunk - 1) / chunk);
   const dim3 grid((unsigned)(n / TI), (unsigned)(n / TJ), gz);
   RedSlot rs = red;
@@ -1243,8 +1288,8 @@ void cg_fused_update(const StencilSpec& sp, float alpha, const RedSlot* alpha_sr
   const double* apart = alpha_src ? alpha_src->dpart : nullptr;
   const int an = alpha_src ? *alpha_src->count : 0;
   if (alpha_src && (!apart || an <= 0)) MPRKB_THROW(10, "cg_fused_update: alpha source has no device tuples");
-  launch_pdl(k_cg_fused, grid, dim3(TTHREADS), smem, st, xmap, pmap, n, nz, chunk, (float)sp.sigma, (float)sp.gamma,
-             alpha, apart, an, b, r, x1, rs);
+  launch_pdl(k_cg_fused, grid, dim3(TTHREADS), smem, st, xmap, pmap, gm[0], gm[1], gm[2], gm[3], has_lo, has_hi, n,
+             nz, chunk, (float)sp.sigma, (float)sp.gamma, alpha, apart, an, b, r, x1, rs);
   note_partials(rs, grid.x * grid.y * grid.z);
   LAUNCHED("cg_fused_update");
 }
@@ -1346,7 +1391,7 @@ __global__ void __launch_bounds__(TTHREADS)
 
 void pq_fused(const StencilSpec& sp, const float* z, const float* p, const RedSlot& beta_src, int beta_comp,
               float rz_old, float* pnew, float* q, const RedSlot& red, cudaStream_t st) {
-  if (!cg_fused_supported(sp)) MPRKB_THROW(10, "pq_fused: needs the TMA stencil on an undivided grid");
+  if (!pq_fused_supported(sp)) MPRKB_THROW(10, "pq_fused: needs the TMA stencil on an undivided grid");
   if (!beta_src.dpart || *beta_src.count <= 0) MPRKB_THROW(10, "pq_fused: beta source has no device tuples");
   const int n = sp.n, nz = sp.nz > 0 ? sp.nz : n;
   constexpr size_t smem = cg_fused_smem();
