@@ -315,7 +315,7 @@ template <class T>
 void FastDiagOp<T>::apply(const void* xv, void* outv, cudaStream_t st) {
   const T* x = static_cast<const T*>(xv);
   T* out = static_cast<T*>(outv);
-  if (halo_) {
+  if (halo_ && P_ > 1) {  // (one rank: the slab is the whole grid, no transposes)
     apply_split(x, out, st);
     return;
   }
