@@ -115,8 +115,10 @@ bool tensor_tc_supported_cols(int n, long cols);
 // pd_in (nullable) scales the INPUT: out = contract(pd_in * x) — the FastDiag
 // diagonal of the previous contraction, applied where its load can be
 // pipelined (the product rounds exactly like an output scaling would).
+// in_bny / out_bny (side 1 only): X read from / C written to the split
+// grid's peer-blocked layout [s][plane][jl][i], j = s ny + jl (0: plain)
 void tensor_apply_tc_fold(int side, int n, const float* qpack, const float* x, float* out, const float* pd_in,
-                          cudaStream_t st, long cols = 0);
+                          cudaStream_t st, long cols = 0, int in_bny = 0, int out_bny = 0);
 void pack_tf32_fold(int n, const float* q, float* qpack);
 // Host: split Q (n x n row-major) into tf32 hi/lo and pack as
 // [k-block of 16][row-group of 8][k-chunk of 4][8 rows][4].

@@ -289,9 +289,23 @@ void FastDiagOp<T>::apply_split(const T* x, T* out, cudaStream_t st) {
     comm->alltoall(src, scratch, blk, st);
     slab_transpose_rows(n, nz_, ny_, P_, sizeof(T), scratch, dst, false, st);
   };
+  // FAST with folded tensor-core M factors: the M contractions write / read
+  // the all-to-all's peer-blocked layout directly (4D tensor maps), so the
+  // slab transposes cost no pass of their own
+  static const bool blocked_env = [] {
+    const char* e = std::getenv("MPRKB_SPLIT_BLOCKED");
+    return !(e && e[0] == '0');
+  }();
+  const bool blocked = num_ == Numerics::Fast && tc_split_ && tcf_[3] && tcf_[2] && ny_ % 32 == 0 && blocked_env;
   contract(2, 1, x, t1, nullptr, ck, st);   // R: Qa^-1
-  contract(1, 3, t1, t2, nullptr, ck, st);  // M: Qb^-1
-  to_j(t2, t1, t3);
+  if (blocked) {
+    tensor_apply_tc_fold(1, n, qhp_[3].template as<float>(), reinterpret_cast<const float*>(t1),
+                         reinterpret_cast<float*>(t2), nullptr, st, ck, 0, ny_);  // M: Qb^-1 -> blocked
+    comm->alltoall(t2, t3, blk, st);
+  } else {
+    contract(1, 3, t1, t2, nullptr, ck, st);  // M: Qb^-1
+    to_j(t2, t1, t3);
+  }
   // (folded tensor-core kernels take the diagonal on the next contraction's
   // input instead: FAST only, where L follows directly)
   const bool pd_next = tc_split_ && tcf_[0] && num_ == Numerics::Fast;
@@ -305,9 +319,16 @@ void FastDiagOp<T>::apply_split(const T* x, T* out, cudaStream_t st) {
     to_k(t1, t2, out);
   } else {
     contract(0, 4, t1, t2, pd_next ? pd : nullptr, cj, st);  // L: Qc (the factors commute exactly)
-    to_k(t2, t1, t3);
-    contract(1, 2, t3, t1, nullptr, ck, st);  // M: Qb
-    contract(2, 0, t1, out, nullptr, ck, st); // R: Qa
+    if (blocked) {
+      comm->alltoall(t2, t1, blk, st);  // lands peer-blocked
+      tensor_apply_tc_fold(1, n, qhp_[2].template as<float>(), reinterpret_cast<const float*>(t1),
+                           reinterpret_cast<float*>(t3), nullptr, st, ck, ny_, 0);  // M: Qb <- blocked
+      contract(2, 0, t3, out, nullptr, ck, st);  // R: Qa
+    } else {
+      to_k(t2, t1, t3);
+      contract(1, 2, t3, t1, nullptr, ck, st);  // M: Qb
+      contract(2, 0, t1, out, nullptr, ck, st); // R: Qa
+    }
   }
 }
 

@@ -458,7 +458,10 @@ template <int SIDE, bool PDIN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_tensor_tcf(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap pmap,
                  const __grid_constant__ CUtensorMap omap, float* __restrict__ C, const float* __restrict__ qpack,
-                 int n, int col_tiles, int num_tiles, long ldc, int dbg) {
+                 int n, int col_tiles, int num_tiles, long ldc, int dbg, int in_bny, int out_bny) {
+  // in_bny / out_bny (M side, split grid): X is read from / C written to the
+  // all-to-all's peer-blocked layout [s][plane][jl][i] (j = s ny + jl) through
+  // 4D tensor maps, so the k <-> j slab transposes need no pass of their own
   using Cfg = TfCfg<PDIN>;
   constexpr int RS = Cfg::RS, QS = Cfg::QS, CS = Cfg::CS;
   extern __shared__ unsigned char smem_raw[];
@@ -542,7 +545,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             tma_2d(RAW(s), xm, kb * TF_BK, (int)T.col0, &S.rawfull[s]);
             if (PDIN) tma_2d(PDR(s), pm, kb * TF_BK, (int)T.col0, &S.rawfull[s]);
           } else if (SIDE == 1) {
-            tma_3d(RAW(s), xm, (int)T.col0, kb * TF_BK, T.plane, &S.rawfull[s]);
+            if (in_bny)
+              tma_4d(RAW(s), xm, (int)T.col0, (kb * TF_BK) % in_bny, T.plane, (kb * TF_BK) / in_bny, &S.rawfull[s]);
+            else
+              tma_3d(RAW(s), xm, (int)T.col0, kb * TF_BK, T.plane, &S.rawfull[s]);
             if (PDIN) tma_3d(PDR(s), pm, (int)T.col0, kb * TF_BK, T.plane, &S.rawfull[s]);
           } else {
             tma_2d(RAW(s), xm, (int)T.col0, kb * TF_BK, &S.rawfull[s]);
@@ -743,6 +749,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(om),
                            "r"(r0), "r"((int)(T.col0 + cc)), "r"(sb)
                            : "memory");
+            else if (SIDE == 1 && out_bny)
+              asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(om),
+                           "r"((int)(T.col0 + cc)), "r"(r0 % out_bny), "r"(T.plane), "r"(r0 / out_bny), "r"(sb)
+                           : "memory");
             else if (SIDE == 1)
               asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(om),
                            "r"((int)(T.col0 + cc)), "r"(r0), "r"(T.plane), "r"(sb)
@@ -766,7 +776,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 }
 
 template <int SIDE, bool PDIN>
-void launch_tcf(int n, long cols, const float* x, float* out, const float* pd, const float* qpack, cudaStream_t st) {
+void launch_tcf(int n, long cols, const float* x, float* out, const float* pd, const float* qpack, cudaStream_t st,
+                int in_bny = 0, int out_bny = 0) {
+  if ((in_bny || out_bny) && (SIDE != 1 || PDIN)) MPRKB_THROW(10, "tensor_apply_tc_fold: blocked layouts are M-side only");
+  if ((in_bny && (in_bny % 32 || n % in_bny)) || (out_bny && (out_bny % 32 || n % out_bny)))
+    MPRKB_THROW(10, "tensor_apply_tc_fold: blocked row count must be a multiple of 32 dividing n");
   const size_t smem = sizeof(TfSmem<PDIN>) + 1024;
   static bool configured = false;
   if (!configured) {
@@ -793,7 +807,14 @@ void launch_tcf(int n, long cols, const float* x, float* out, const float* pd, c
   } else if (SIDE == 1) {
     const cuuint64_t dims[3] = {nn, nn, cc / nn}, strides[2] = {nn * 4, n2 * 4};
     const cuuint32_t box[3] = {(cuuint32_t)TF_BN, (cuuint32_t)TF_BK, 1};
-    map = mk(x, 3, dims, strides, box);
+    if (in_bny) {  // [s][plane][jl][i]
+      const cuuint64_t nb = (cuuint64_t)in_bny, pl = cc / nn;
+      const cuuint64_t d4[4] = {nn, nb, pl, nn / nb}, s4[3] = {nn * 4, nn * nb * 4, nn * nb * pl * 4};
+      const cuuint32_t b4[4] = {(cuuint32_t)TF_BN, (cuuint32_t)TF_BK, 1, 1};
+      map = mk(x, 4, d4, s4, b4);
+    } else {
+      map = mk(x, 3, dims, strides, box);
+    }
     pmap = PDIN ? mk(pd, 3, dims, strides, box) : map;
     col_tiles = (int)(nn / TF_BN);
     planes = (int)(cc / nn);
@@ -812,6 +833,11 @@ void launch_tcf(int n, long cols, const float* x, float* out, const float* pd, c
     if (SIDE == 2) {  // C[fibre][a]
       const cuuint64_t dims[2] = {nn, cc}, strides[1] = {nn * 4};
       omap = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, out, 2, dims, strides, ob2, CU_TENSOR_MAP_SWIZZLE_128B);
+    } else if (SIDE == 1 && out_bny) {  // C[s][plane][al][i], a = s ny + al
+      const cuuint64_t nb = (cuuint64_t)out_bny, pl = cc / nn;
+      const cuuint64_t d4[4] = {nn, nb, pl, nn / nb}, s4[3] = {nn * 4, nn * nb * 4, nn * nb * pl * 4};
+      const cuuint32_t ob4[4] = {32, 32, 1, 1};
+      omap = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, out, 4, d4, s4, ob4, CU_TENSOR_MAP_SWIZZLE_128B);
     } else if (SIDE == 1) {  // C[plane][a][i]
       const cuuint64_t dims[3] = {nn, nn, cc / nn}, strides[2] = {nn * 4, n2 * 4};
       omap = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, out, 3, dims, strides, ob3, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -823,14 +849,14 @@ void launch_tcf(int n, long cols, const float* x, float* out, const float* pd, c
   const int num_tiles = (n / 2 / TF_BM) * col_tiles * planes;
   const int grid = num_tiles < sm_count() ? num_tiles : sm_count();
   launch_pdl(k_tensor_tcf<SIDE, PDIN>, dim3(grid), dim3(TC_THREADS), smem, st, map, pmap, omap, out, qpack, n,
-             col_tiles, num_tiles, cols, dbg);
+             col_tiles, num_tiles, cols, dbg, in_bny, out_bny);
   LAUNCHED("tensor_tc_fold");
 }
 
 }  // namespace
 
 void tensor_apply_tc_fold(int side, int n, const float* qpack, const float* x, float* out, const float* pd_in,
-                          cudaStream_t st, long cols) {
+                          cudaStream_t st, long cols, int in_bny, int out_bny) {
   const float* pd = pd_in;
   if (cols <= 0) cols = (long)n * n;
   switch (side) {
@@ -838,7 +864,8 @@ void tensor_apply_tc_fold(int side, int n, const float* qpack, const float* x, f
       pd ? launch_tcf<2, true>(n, cols, x, out, pd, qpack, st) : launch_tcf<2, false>(n, cols, x, out, pd, qpack, st);
       break;
     case 1:
-      pd ? launch_tcf<1, true>(n, cols, x, out, pd, qpack, st) : launch_tcf<1, false>(n, cols, x, out, pd, qpack, st);
+      pd ? launch_tcf<1, true>(n, cols, x, out, pd, qpack, st, in_bny, out_bny)
+         : launch_tcf<1, false>(n, cols, x, out, pd, qpack, st, in_bny, out_bny);
       break;
     default:
       pd ? launch_tcf<0, true>(n, cols, x, out, pd, qpack, st) : launch_tcf<0, false>(n, cols, x, out, pd, qpack, st);

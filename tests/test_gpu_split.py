@@ -114,7 +114,8 @@ def test_split_fast_matches_undivided(gpu, mp, eq, n, method, prec, tol, P, rtol
     assert rel <= rtol, rel
 
 
-def test_split_fast_tensor_cores_256(gpu, mp):
+@pytest.mark.parametrize("ranks", [2, 4])
+def test_split_fast_tensor_cores_256(gpu, mp, ranks):
     """The bench path on a split grid: fp32 FastDiag on tcgen05 in both slab
     layouts (k-slab R/M, j-slab L), 256^3 on 2 ranks.  Bar (SURVEY.md §8c,
     as test_step_fast_256_within_reference_noise): one step within 2x the
@@ -123,7 +124,7 @@ def test_split_fast_tensor_cores_256(gpu, mp):
     make = maker(mp, "heat", 256, "4s3pB", "f32", "fast", 1e-3)
     want, wtr, _ = run_whole(mp, 1, make)
     exact, _, _ = run_whole(mp, 1, maker(mp, "heat", 256, "4s3pB", "f64", "fast", 1e-5))
-    got, gtr, _ = run_split(mp, 2, 1, make)
+    got, gtr, _ = run_split(mp, ranks, 1, make)  # (M contractions on the peer-blocked layout: ny = 128 / 64)
     assert [t["iterations"] for t in gtr] == [t["iterations"] for t in wtr]
     own = np.linalg.norm(want - exact)
     assert np.linalg.norm(got - want) <= 2 * own, (np.linalg.norm(got - want), own)
