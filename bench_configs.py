@@ -111,6 +111,12 @@ def config4(mp, torch):
 def config5(mp, torch, limit):
     n, tau = 384, 0.01
     tab = mp.builtin("4s3pB")
+    # (module loading / first-launch setup outside the timed single steps)
+    for store in ("f16", "f32", "f64"):
+        w = mp.Stepper("heat", 128, tab, tau, 1e-4, "f32", 300, preconditioner="block-jacobi", block_size=4,
+                       block_storage=store)
+        time_steps(mp, torch, w, 1, 1)
+        del w
     runs = list(itertools.product((1e-4, 1e-6, 1e-8, 1e-10), (4, 8, 16, 32), ("f16", "f32", "f64")))
     for tol, b, store in runs[:limit]:
         st = mp.Stepper("heat", n, tab, tau, tol, "f32", 300, preconditioner="block-jacobi", block_size=b,
