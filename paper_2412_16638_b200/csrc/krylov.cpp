@@ -523,6 +523,7 @@ void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num,
     vsub<T>(m, b, dst, dst, nullptr, st);
   };
 
+  double exit_true = -1.0;  // ||b - A x|| at exit when already formed (FAST)
   residual_of(x, t);
   pre(t, wv);  // w = P(b - A x0)
   const double beta = (double)norm2(wv);
@@ -549,6 +550,7 @@ void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num,
     };
     s[0] = scast<H>(beta);
     bool x_built = false;
+    double cand_true = -1.0;
 
     // xc = x + sum_j y_j v_j with y from the rotated triangular system
     auto candidate_into = [&](int cols, T* dst) {
@@ -671,10 +673,26 @@ void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num,
         candidate_into(k, xc);
         residual_of(xc, t);
         pre(t, wt);
-        const double rt = static_cast<double>(norm2(wt));
+        double rt;
+        if (fast) {
+          // FAST: ||P t|| and — should the candidate be accepted — the exit
+          // true residual ||t|| of the same x in one round trip
+          dot_real<T>(m, wt, wt, s0, num, st);
+          dot_real<T>(m, t, t, w.red.slot(1), num, st);
+          stream_sync(st);
+          double v[2];
+          w.red.result(0, 1, &v[0]);
+          w.red.result(1, 1, &v[1]);
+          if (w.comm && w.comm->size() > 1) w.comm->allreduce_sum(v, 2);
+          rt = (double)std::sqrt((R)v[0]);
+          cand_true = (double)std::sqrt((R)v[1]);
+        } else {
+          rt = static_cast<double>(norm2(wt));
+        }
         if (crit.satisfied(rt, beta)) {
           CUDA_CHECK(cudaMemcpyAsync(x, xc, m * sizeof(T), cudaMemcpyDeviceToDevice, st));
           x_built = true;
+          exit_true = cand_true;  // x is the candidate: its true residual is known
           rep.converged = true;
           break;
         }
@@ -690,8 +708,12 @@ void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num,
     }
   }
 
-  residual_of(x, t);
-  rep.true_residual = static_cast<double>(norm2(t));
+  if (exit_true >= 0.0) {
+    rep.true_residual = exit_true;
+  } else {
+    residual_of(x, t);
+    rep.true_residual = static_cast<double>(norm2(t));
+  }
 }
 
 template class KrylovWork<float>;
