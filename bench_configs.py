@@ -100,7 +100,7 @@ def config4(mp, torch):
     for pre, basis in (("fastdiag", "f16"), ("block-jacobi", "f16"), ("block-jacobi", None)):
         kw = dict(preconditioner=pre, block_size=8, block_storage="f16") if pre != "fastdiag" else {}
         st = mp.Stepper("advection-diffusion", n, tab, tau, 1e-3, "f32", 40, nu=nu, basis_storage=basis, **kw)
-        ms, its = time_steps(mp, torch, st, 3, 1)
+        ms, its = time_steps(mp, torch, st, 3, 2)  # (2 warm-up steps: the Krylov basis is allocated on first use)
         line(config=4, workload=(f"advection-diffusion {n}^3 nu={nu} 4s3pC, GMRES (complex fp32) + {pre}, "
                                  f"Krylov basis {basis or 'fp32 (working precision)'}, tau=1/640, tol=1e-3"),
              metric="DOF-updates/s", value=n ** 3 / (ms * 1e-3), ms_per_step=ms,
