@@ -393,8 +393,9 @@ struct BasisArgs {
 
 // xc = x; xc += y_j v_j for j in order   (krylov.hpp:223-226)
 template <class T>
-__global__ void __launch_bounds__(kBlock) k_candidate(size_t m, const T* x, int cols, const BasisArgs<T>* args,
-                                                      T* xc) {
+__global__ void __launch_bounds__(kBlock) k_candidate(size_t m, const T* x, int cols,
+                                                      const __grid_constant__ BasisArgs<T> a, T* xc) {
+  const BasisArgs<T>* args = &a;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < m; i += (size_t)gridDim.x * blockDim.x) {
     T acc = ldg(x + i);
     for (int j = 0; j < cols; ++j) acc = xadd(acc, xmul(args->y[j], ldg(args->v[j] + i)));
@@ -404,20 +405,13 @@ __global__ void __launch_bounds__(kBlock) k_candidate(size_t m, const T* x, int 
 
 template <class T>
 void candidate(size_t m, const T* x, const T* const* basis, const T* y, int cols, T* xc, cudaStream_t st) {
-  static thread_local BasisArgs<T>* d_args = nullptr;
-  static thread_local BasisArgs<T>* h_args = nullptr;
   if (cols > kMaxBasis) MPRKB_THROW(1, "gmres: basis larger than 128 vectors is not supported");
-  if (!d_args) {
-    CUDA_CHECK(cudaMalloc(&d_args, sizeof(BasisArgs<T>)));
-    CUDA_CHECK(cudaMallocHost(&h_args, sizeof(BasisArgs<T>)));
-  }
-  CUDA_CHECK(cudaStreamSynchronize(st));  // the previous use of the staging block has finished
+  BasisArgs<T> args{};  // by value (kernel parameter): no staging copy, no synchronize
   for (int j = 0; j < cols; ++j) {
-    h_args->v[j] = basis[j];
-    h_args->y[j] = y[j];
+    args.v[j] = basis[j];
+    args.y[j] = y[j];
   }
-  CUDA_CHECK(cudaMemcpyAsync(d_args, h_args, sizeof(BasisArgs<T>), cudaMemcpyHostToDevice, st));
-  k_candidate<T><<<grid_for(m, kBlock, 8), kBlock, 0, st>>>(m, x, cols, d_args, xc);
+  k_candidate<T><<<grid_for(m, kBlock, 8), kBlock, 0, st>>>(m, x, cols, args, xc);
   LAUNCHED("candidate");
 }
 

@@ -598,7 +598,9 @@ struct Basis16Args {
   T y[kMaxBasis16];
 };
 template <class T>
-__global__ void __launch_bounds__(256) k_candidate16(size_t m, const T* x, int cols, const Basis16Args<T>* args, T* xc) {
+__global__ void __launch_bounds__(256) k_candidate16(size_t m, const T* x, int cols, const __grid_constant__ Basis16Args<T> a,
+                                                     T* xc) {
+  const Basis16Args<T>* args = &a;
   pdl_wait();
   pdl_trigger();
   using S = typename Store16<T>::type;
@@ -625,21 +627,13 @@ __global__ void __launch_bounds__(256) k_candidate16(size_t m, const T* x, int c
 }
 template <class T>
 void basis16_candidate(size_t m, const T* x, void* const* basis, const T* y, int cols, T* xc, cudaStream_t st) {
-  static thread_local Basis16Args<T>* d_args = nullptr;
-  static thread_local Basis16Args<T>* h_args = nullptr;
   if (cols > kMaxBasis16) MPRKB_THROW(1, "gmres: basis larger than 128 vectors is not supported");
-  if (!d_args) {
-    CUDA_CHECK(cudaMalloc(&d_args, sizeof(Basis16Args<T>)));
-    CUDA_CHECK(cudaMallocHost(&h_args, sizeof(Basis16Args<T>)));
-  }
-  CUDA_CHECK(cudaStreamSynchronize(st));  // the previous use of the staging block has finished
+  Basis16Args<T> args{};  // by value (kernel parameter): no staging copy, no synchronize
   for (int j = 0; j < cols; ++j) {
-    h_args->v[j] = basis[j];
-    h_args->y[j] = y[j];
+    args.v[j] = basis[j];
+    args.y[j] = y[j];
   }
-  CUDA_CHECK(cudaMemcpyAsync(d_args, h_args, sizeof(Basis16Args<T>), cudaMemcpyHostToDevice, st));
-  launch_pdl(k_candidate16<T>, dim3(grid_for(m / 4 + 1, 256, 8)), dim3(256), 0, st, m, x, cols,
-             (const Basis16Args<T>*)d_args, xc);
+  launch_pdl(k_candidate16<T>, dim3(grid_for(m / 4 + 1, 256, 8)), dim3(256), 0, st, m, x, cols, args, xc);
   LAUNCHED("basis16_candidate");
 }
 
