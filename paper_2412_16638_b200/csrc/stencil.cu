@@ -989,8 +989,17 @@ void stencil_apply_dot(const StencilSpec& s, const T* p, T* q, const RedSlot& re
   launch(s, LdPlain<T>{p}, EpiStoreDot<T>{q, red}, st, "stencil_dot");
 }
 
+bool dots2_tma(const StencilSpec& sp, const float* z, const float* r, const RedSlot& red, cudaStream_t st);
+
 template <class T>
 void stencil_apply_dot2(const StencilSpec& s, const T* p, T* q, const T* r, const RedSlot& red, cudaStream_t st) {
+  if constexpr (std::is_same_v<T, float>) {
+    static const bool on = [] {
+      const char* e = std::getenv("MPRKB_DOTS2_TMA");
+      return !(e && e[0] == '0');
+    }();
+    if (!q && on && dots2_tma(s, p, r, red, st)) return;
+  }
   launch(s, LdPlain<T>{p}, EpiStoreDot2<T>{q, r, red}, st, "stencil_dot2");
 }
 
@@ -1431,6 +1440,130 @@ void pq_fused(const StencilSpec& sp, const float* z, const float* p, const RedSl
              (const double*)beta_src.dpart, *beta_src.count, beta_comp, rz_old, pnew, q, rs);
   note_partials(rs, grid.x * grid.y * grid.z);
   LAUNCHED("pq_fused");
+}
+
+// ---- the first CG iteration's two scalars with both operands by TMA (fp32) ---------
+// (z.Az, r.z) without storing Az: z (with its halo) and r stream through one
+// TMA ring instead of r by per-thread loads, whose short prefetch left the
+// read-only pass latency-bound.
+__global__ void __launch_bounds__(TTHREADS)
+    k_dots2_tma(const __grid_constant__ CUtensorMap zmap, const __grid_constant__ CUtensorMap rmap, int n, int nz,
+                int kc, float s, float g, RedSlot red) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ unsigned char smem_raw[];
+  float* buf = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(buf + CG_TST * 2 * CG_SLOT);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int i0 = blockIdx.x * TI, j0 = blockIdx.y * TJ;
+  int k0, k1;
+  plane_range(nz, 0, nz, kc, k0, k1);
+  const int planes = k1 - k0 + 2;
+  constexpr uint32_t zbytes = (TJ + 2) * TW * sizeof(float), rbytes = TJ * TI * sizeof(float);
+  if (tid == 0) {
+    for (int b = 0; b < CG_TST; ++b) mbar_init(&full[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const CUtensorMap* zm = &zmap;
+  const CUtensorMap* rm = &rmap;
+  auto issue = [&](int qq) {  // z plane k0 - 1 + qq (+ r's plane when it is computed)
+    const int k = k0 - 1 + qq, sl = qq % CG_TST;
+    float* dst = buf + sl * 2 * CG_SLOT;
+    const bool with_r = k >= k0 && k < k1;
+    mbar_expect_tx(&full[sl], zbytes + (with_r ? rbytes : 0));
+    tma_3d(dst, zm, i0 - 4, j0 - 1, k, &full[sl]);
+    if (with_r) tma_3d(dst + CG_SLOT, rm, i0, j0, k, &full[sl]);
+  };
+  if (tid == 0)
+    for (int qq = 0; qq < CG_TST && qq < planes; ++qq) issue(qq);
+  auto wait = [&](int qq) { mbar_wait(&full[qq % CG_TST], (uint32_t)(qq / CG_TST) & 1u); };
+  auto ld = [](const float* ptr) {
+    const float4 f = *reinterpret_cast<const float4*>(ptr);
+    V4<float> v;
+    v.x[0] = f.x; v.x[1] = f.y; v.x[2] = f.z; v.x[3] = f.w;
+    return v;
+  };
+  double acc[2] = {0.0, 0.0};
+  const int col = 4 + 4 * lane;
+  for (int k = k0; k < k1; ++k) {
+    const int qq = k - k0 + 1;
+    if (k == k0) {
+      wait(0);
+      wait(1);
+    }
+    wait(qq + 1);
+    const float* bm = buf + ((qq - 1) % CG_TST) * 2 * CG_SLOT;
+    const float* bc = buf + (qq % CG_TST) * 2 * CG_SLOT;
+    const float* bp = buf + ((qq + 1) % CG_TST) * 2 * CG_SLOT;
+#pragma unroll
+    for (int rr = 0; rr < TROWS; ++rr) {
+      const int row = warp * TROWS + rr;
+      const int o = (row + 1) * TW + col;
+      const V4<float> c = ld(bc + o);
+      const V4<float> ym = ld(bc + o - TW), yp = ld(bc + o + TW);
+      const V4<float> zmv = ld(bm + o), zpv = ld(bp + o);
+      const V4<float> rv = ld(bc + CG_SLOT + row * TI + 4 * lane);
+      float xl = shfl_up1(c.x[3]), xr = shfl_down1(c.x[0]);
+      if (lane == 0) xl = bc[o - 1];
+      if (lane == 31) xr = bc[o + 4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float al = e == 0 ? xl : c.x[e - 1], ar = e == 3 ? xr : c.x[e + 1];
+        const float v = point<float>(0, s, g, 0.0f, c.x[e], al, ar, ym.x[e], yp.x[e], zmv.x[e], zpv.x[e]);
+        dot_acc(*reinterpret_cast<double(*)[1]>(&acc[0]), c.x[e], v);      // EpiStoreDot2's p.q
+        dot_acc(*reinterpret_cast<double(*)[1]>(&acc[1]), rv.x[e], c.x[e]);  // and r.p
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0 && qq - 1 + CG_TST < planes) issue(qq - 1 + CG_TST);
+  }
+  grid_reduce<2>(acc, red);
+}
+
+bool dots2_tma(const StencilSpec& sp, const float* z, const float* r, const RedSlot& red, cudaStream_t st) {
+  if (!pq_fused_supported(sp)) return false;
+  const int n = sp.n, nz = sp.nz > 0 ? sp.nz : n;
+  constexpr size_t smem = cg_fused_smem();
+  static int chunk = 0;
+  static long chunk_cols = -1;
+  static int resident = 0;
+  if (!resident) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_dots2_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dots2_tma, TTHREADS, smem));
+    resident = std::max(1, per_sm) * sm_count();
+  }
+  const long cols = (long)(n / TI) * (n / TJ);
+  if (cols != chunk_cols) {
+    long best_cost = -1;
+    for (int kc = 4; kc <= 64; ++kc) {
+      const long units = cols * ((nz + kc - 1) / kc);
+      const long cost = ((units + resident - 1) / resident) * (std::min(kc, nz) + 2);
+      if (best_cost < 0 || cost < best_cost) {
+        chunk = kc;
+        best_cost = cost;
+      }
+    }
+    chunk_cols = cols;
+  }
+  const cuuint64_t nn = (cuuint64_t)n;
+  const cuuint64_t dims3[3] = {nn, nn, (cuuint64_t)nz}, str3[2] = {nn * 4, nn * nn * 4};
+  const cuuint32_t zbox[3] = {(cuuint32_t)TW, (cuuint32_t)(TJ + 2), 1};
+  const cuuint32_t rbox[3] = {(cuuint32_t)TI, (cuuint32_t)TJ, 1};
+  const CUtensorMap zmap = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, z, 3, dims3, str3, zbox);
+  const CUtensorMap rmap = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, r, 3, dims3, str3, rbox);
+  const unsigned gz = (unsigned)((nz + chunk - 1) / chunk);
+  const dim3 grid((unsigned)(n / TI), (unsigned)(n / TJ), gz);
+  RedSlot rs = red;
+  rs.base = 0;
+  rs.total = 0;
+  launch_pdl(k_dots2_tma, grid, dim3(TTHREADS), smem, st, zmap, rmap, n, nz, chunk, (float)sp.sigma, (float)sp.gamma,
+             rs);
+  note_partials(rs, grid.x * grid.y * grid.z);
+  LAUNCHED("dots2_tma");
+  return true;
 }
 
 #define INST_STENCIL(T)                                                                          \
