@@ -114,7 +114,7 @@ def test_split_fast_matches_undivided(gpu, mp, eq, n, method, prec, tol, P, rtol
     assert rel <= rtol, rel
 
 
-@pytest.mark.parametrize("ranks", [2, 4])
+@pytest.mark.parametrize("ranks", [2, 4, 8])
 def test_split_fast_tensor_cores_256(gpu, mp, ranks):
     """The bench path on a split grid: fp32 FastDiag on tcgen05 in both slab
     layouts (k-slab R/M, j-slab L), 256^3 on 2 ranks.  Bar (SURVEY.md §8c,
