@@ -205,6 +205,39 @@ struct EpiResidual {
   }
 };
 
+// r = x - A x: the residual of x0 = b (the CG's initial guess IS the rhs
+// buffer), b's values being the stencil's own centre values — no second
+// stream of b (stepper.cpp:111 x0 = rhs; krylov.hpp:110)
+template <class T>
+struct EpiResidualSelf {
+  T* r;
+  RedSlot red;
+  struct State {
+    double v[1];
+  };
+  using Pre = NoPre;
+  __device__ void init(State& s) const { s.v[0] = 0.0; }
+  __device__ __forceinline__ Pre pre4(long) const { return {}; }
+  __device__ __forceinline__ void v4p(State& s, long i, const V4<T>& v, const V4<T>& xc, const Pre&) const {
+    V4<T> o;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      o.x[e] = xsub(xc.x[e], v.x[e]);
+      dot_acc(s.v, o.x[e], o.x[e]);
+    }
+    st4(r + i, o);
+  }
+  __device__ __forceinline__ void v4(State& s, long i, const V4<T>& v, const V4<T>& xc) const {
+    v4p(s, i, v, xc, pre4(i));
+  }
+  __device__ __forceinline__ void s1(State& s, long i, T v, T xc) const {
+    const T o = xsub(xc, v);
+    r[i] = o;
+    dot_acc(s.v, o, o);
+  }
+  __device__ void finish(State& s) const { grid_reduce<1>(s.v, red); }
+};
+
 template <class T>
 struct EpiStoreDot {
   T* out;
@@ -978,6 +1011,10 @@ void stencil_apply(const StencilSpec& s, const T* x, T* out, cudaStream_t st) {
 
 template <class T>
 void stencil_residual(const StencilSpec& s, const T* x, const T* b, T* r, const RedSlot* red, cudaStream_t st) {
+  if (x == b && red) {  // x0 = b: b is the stencil's own centre
+    launch(s, LdPlain<T>{x}, EpiResidualSelf<T>{r, *red}, st, "stencil_residual");
+    return;
+  }
   if (red)
     launch(s, LdPlain<T>{x}, EpiResidual<T, true>{b, r, *red}, st, "stencil_residual");
   else
