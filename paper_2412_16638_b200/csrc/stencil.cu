@@ -861,7 +861,7 @@ __global__ void __launch_bounds__(TTHREADS, tma_min_blocks<Epi>())
 // (waves x planes per CTA incl. the 2-plane halo) for the resident capacity
 template <class Src, class Epi>
 int tma_chunk(long cols, int planes) {
-  static int resident = 0;
+  static thread_local int resident = 0;
   if (!resident) {
     int per_sm = 0;
     CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stencil_tma<Src, Epi>, TTHREADS,
@@ -883,7 +883,7 @@ int tma_chunk(long cols, int planes) {
 
 template <class Src, class Epi>
 void tma_configure() {
-  static bool configured = false;
+  static thread_local bool configured = false;
   if (!configured) {
     CUDA_CHECK(cudaFuncSetAttribute(k_stencil_tma<Src, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)tma_stencil_smem<typename Src::raw>()));
@@ -1270,9 +1270,9 @@ void cg_fused_update(const StencilSpec& sp, float alpha, const RedSlot* alpha_sr
   if (!cg_fused_supported(sp)) MPRKB_THROW(10, "cg_fused_update: needs the TMA stencil (Dirichlet, n % 128 == 0)");
   const int n = sp.n, nz = sp.nz > 0 ? sp.nz : n;
   constexpr size_t smem = cg_fused_smem();
-  static int chunk = 0;
-  static long chunk_cols = -1;
-  static int resident = 0;
+  static thread_local int chunk = 0;  // (per host thread: in-process ranks launch concurrently)
+  static thread_local long chunk_cols = -1;
+  static thread_local int resident = 0;
   if (!resident) {
     CUDA_CHECK(cudaFuncSetAttribute(k_cg_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
@@ -1441,9 +1441,9 @@ void pq_fused(const StencilSpec& sp, const float* z, const float* p, const RedSl
   if (!beta_src.dpart || *beta_src.count <= 0) MPRKB_THROW(10, "pq_fused: beta source has no device tuples");
   const int n = sp.n, nz = sp.nz > 0 ? sp.nz : n;
   constexpr size_t smem = cg_fused_smem();
-  static int chunk = 0;
-  static long chunk_cols = -1;
-  static int resident = 0;
+  static thread_local int chunk = 0;  // (per host thread: in-process ranks launch concurrently)
+  static thread_local long chunk_cols = -1;
+  static thread_local int resident = 0;
   if (!resident) {
     CUDA_CHECK(cudaFuncSetAttribute(k_pq_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
@@ -1563,9 +1563,9 @@ bool dots2_tma(const StencilSpec& sp, const float* z, const float* r, const RedS
   if (!pq_fused_supported(sp)) return false;
   const int n = sp.n, nz = sp.nz > 0 ? sp.nz : n;
   constexpr size_t smem = cg_fused_smem();
-  static int chunk = 0;
-  static long chunk_cols = -1;
-  static int resident = 0;
+  static thread_local int chunk = 0;  // (per host thread: in-process ranks launch concurrently)
+  static thread_local long chunk_cols = -1;
+  static thread_local int resident = 0;
   if (!resident) {
     CUDA_CHECK(cudaFuncSetAttribute(k_dots2_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;

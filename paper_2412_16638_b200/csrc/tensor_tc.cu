@@ -316,7 +316,7 @@ template <int SIDE, bool DIAG>
 void launch_tc(int n, long cols, const float* x, float* out, const float* pd, const float* qh, const float* ql,
                cudaStream_t st) {
   const size_t smem = sizeof(TcSmem) + 1024;
-  static bool configured = false;
+  static thread_local bool configured = false;
   if (!configured) {
     CUDA_CHECK(cudaFuncSetAttribute(k_tensor_tc<SIDE, DIAG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
@@ -782,7 +782,7 @@ void launch_tcf(int n, long cols, const float* x, float* out, const float* pd, c
   if ((in_bny && (in_bny % 32 || n % in_bny)) || (out_bny && (out_bny % 32 || n % out_bny)))
     MPRKB_THROW(10, "tensor_apply_tc_fold: blocked row count must be a multiple of 32 dividing n");
   const size_t smem = sizeof(TfSmem<PDIN>) + 1024;
-  static bool configured = false;
+  static thread_local bool configured = false;
   if (!configured) {
     CUDA_CHECK(cudaFuncSetAttribute(k_tensor_tcf<SIDE, PDIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
