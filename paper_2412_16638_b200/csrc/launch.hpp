@@ -244,8 +244,10 @@ void check_finite32(size_t m, const float* x, int* flag, cudaStream_t st);  // *
 // The final update with the last stage's f_hi evaluated in the same pass:
 // u += sum_t coef_t v_t (fp64 terms, in order) + c_last (K widen(y32) + g),
 // gated like final_update (k.forcing regenerates g when set)
-void final_update_feval(const StencilSpec& k, double* u, const CombineTerms& t, const float* y32, const double* g,
-                        double c_last, int* flag, const int* gate, int gate_count, cudaStream_t st);
+// uin: the running sum the pass starts from (u itself, or an accumulator of
+// u and the earlier stages' terms); the result is written to u
+void final_update_feval(const StencilSpec& k, double* u, const double* uin, const CombineTerms& t, const float* y32,
+                        const double* g, double c_last, int* flag, const int* gate, int gate_count, cudaStream_t st);
 void final_update(size_t m, double* u, const CombineTerms& t, int* flag, cudaStream_t st,
                   const int* gate = nullptr, int gate_count = 0);
 // element casts for the op-level API: narrow (overflow flag) / widen / promote

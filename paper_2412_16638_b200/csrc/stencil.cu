@@ -480,6 +480,7 @@ struct EpiFevalCombine {
 // the step's earlier checks fired, nothing is written.
 struct EpiFinalFeval {
   double* u = nullptr;
+  const double* uin = nullptr;  // the running sum read (u, or an accumulator)
   int nt = 0;
   const double* tv[kMaxTerms] = {};
   double tc[kMaxTerms] = {};
@@ -499,7 +500,7 @@ struct EpiFinalFeval {
     s.skip = any != 0;
     s.bad = false;
   }
-  __device__ __forceinline__ Pre pre4(long i) const { return ld4rw(u + i); }
+  __device__ __forceinline__ Pre pre4(long i) const { return ld4rw(uin + i); }
   __device__ __forceinline__ void v4p(State& s, long i, const V4<double>& v, const V4<double>&, const Pre& uv) const {
     if (s.skip) return;
     V4<double> gv;
@@ -526,7 +527,7 @@ struct EpiFinalFeval {
   }
   __device__ __forceinline__ void s1(State& s, long i, double v, double) const {
     if (s.skip) return;
-    double r = u[i];
+    double r = uin[i];
     for (int c = 0; c < nt; ++c) r = xadd(r, xmul(tc[c], __ldg(tv[c] + i)));
     const double gi = gen.s ? forcing1(gen, i) : (g ? __ldg(g + i) : 0.0);
     r = xadd(r, xmul(c_last, g ? xadd(v, gi) : v));
@@ -1056,10 +1057,11 @@ void apply_f32(const StencilSpec& k, const double* y, const float* y32, const fl
     launch(k, LdD2F{y, flag}, EpiF32Forcing{g32, out32, finite_flag, k.forcing}, st, "apply_f32");
 }
 
-void final_update_feval(const StencilSpec& k, double* u, const CombineTerms& t, const float* y32, const double* g,
-                        double c_last, int* flag, const int* gate, int gate_count, cudaStream_t st) {
+void final_update_feval(const StencilSpec& k, double* u, const double* uin, const CombineTerms& t, const float* y32,
+                        const double* g, double c_last, int* flag, const int* gate, int gate_count, cudaStream_t st) {
   EpiFinalFeval e;
   e.u = u;
+  e.uin = uin ? uin : u;
   e.nt = t.count;
   for (int c = 0; c < t.count; ++c) {
     if (t.is_f32[c] != 0) MPRKB_THROW(10, "final_update_feval: fp64 stored terms only");

@@ -158,8 +158,9 @@ Stepper::Stepper(const StepperConfig& cfg)
     for (int i = 0; i < q; ++i) ok = ok && t.ae(i, i) != 0.0 && t.ah(i, i) == 0.0;
     fused_ = ok;
     if (fused_) {
-      acc_.resize(q);
+      acc_.resize(q + 1);
       for (int k = 2; k < q; ++k) acc_[k].alloc(m * sizeof(double));
+      acc_[q].alloc(m * sizeof(double));  // the final update's running sum (u + tau sum b_i f_hi_i)
     }
   }
   if (!solvers_.empty()) {
@@ -405,13 +406,24 @@ void Stepper::step_fused(double* u, StepTrace& trace) {
     Bracket br(timer_, "axpy", st_);
     combine(m, u, terms, 1, b32, check_slot(6, kOverflow), st_);
   }
+  // The final update u + tau sum_i b_i f_hi_i accumulates stage by stage in
+  // acc_[q], in the reference's term order (u, then i ascending), while each
+  // f_hi is in registers — so no f_hi is stored; the last stage's term is
+  // added by the final pass (MPRKB_FUSED_FINAL=0: stored f_hi + final_update)
+  static const bool fuse_final_env = [] {
+    const char* e = std::getenv("MPRKB_FUSED_FINAL");
+    return !(e && e[0] == '0');
+  }();
+  const int last = q - 1;
+  const bool fuse_final = t.b[last] != 0.0 && fuse_final_env;
+  bool fin_started = false;  // acc_[q] holds u + earlier terms
   float* cur = solve(0);  // stage i's solution
   for (int i = 0; i + 1 < q; ++i) {
     const int nx = i + 1;
     FevalCombine f;
     f.g = g64_.as<double>();
     f.g32 = g32_.as<float>();
-    f.fhi = t.b[i] != 0.0 ? f_hi_[i].as<double>() : nullptr;
+    f.fhi = (t.b[i] != 0.0 && !fuse_final) ? f_hi_[i].as<double>() : nullptr;
     f.finite_flag = check_slot(9, kStage);
     f.sin = i == 0 ? u : acc_[nx].as<double>();
     f.hh = t.ah(nx, i) != 0.0;
@@ -432,21 +444,24 @@ void Stepper::step_fused(double* u, StepTrace& trace) {
       f.hae[a] = t.ae(k, i) != 0.0;
       f.ae[a] = tau * t.ae(k, i);
     }
+    if (fuse_final && t.b[i] != 0.0) {
+      const int a = f.nacc++;
+      f.ain[a] = fin_started ? acc_[q].as<double>() : u;
+      f.aout[a] = acc_[q].as<double>();
+      f.hah[a] = 1;
+      f.ah[a] = tau * t.b[i];
+      f.hae[a] = 0;
+      f.ae[a] = 0.0;
+      fin_started = true;
+    }
     {
       Bracket br(timer_, "stencil", st_);
       feval_combine(kspec_, cur, f, st_);
     }
     cur = solve(nx);
   }
-  // last stage: its f_hi feeds only the final update — evaluated inside the
-  // final pass itself (the stage vector's finiteness checked first, so the
-  // update stays gated on it); MPRKB_FUSED_FINAL=0: separate kernels
-  const int last = q - 1;
-  static const bool fuse_final_env = [] {
-    const char* e = std::getenv("MPRKB_FUSED_FINAL");
-    return !(e && e[0] == '0');
-  }();
-  const bool fuse_final = t.b[last] != 0.0 && fuse_final_env;
+  // last stage: its f_hi is evaluated inside the final pass itself (the stage
+  // vector's finiteness checked first, so the update stays gated on it)
   if (fuse_final) {
     check_finite32(m, cur, check_slot(9, kStage), st_);
   } else if (t.b[last] != 0.0) {
@@ -458,8 +473,9 @@ void Stepper::step_fused(double* u, StepTrace& trace) {
   const int stage_checks = next - 1;
   if (slab_.split()) raise_flags();
   CombineTerms fin;
-  for (int i = 0; i < (fuse_final ? last : q); ++i)
-    if (t.b[i] != 0.0) add_term(fin, tau * t.b[i], f_hi_[i].get(), 0);
+  if (!fuse_final)
+    for (int i = 0; i < q; ++i)
+      if (t.b[i] != 0.0) add_term(fin, tau * t.b[i], f_hi_[i].get(), 0);
   {
     Bracket br(timer_, "axpy", st_);
     int* fin_flag = check_slot(9, "updated state picked up a NaN or infinity");
@@ -470,7 +486,8 @@ void Stepper::step_fused(double* u, StepTrace& trace) {
       gate = gate_dev_.as<int>();
     }
     if (fuse_final)
-      final_update_feval(kspec_, u, fin, cur, g64_.as<double>(), tau * t.b[last], fin_flag, gate, stage_checks, st_);
+      final_update_feval(kspec_, u, fin_started ? acc_[q].as<double>() : u, fin, cur, g64_.as<double>(),
+                         tau * t.b[last], fin_flag, gate, stage_checks, st_);
     else
       final_update(m, u, fin, fin_flag, st_, gate, stage_checks);
   }
