@@ -135,11 +135,21 @@ int mprkb_op_fastdiag(int dtype, int n, const void* qa, const void* qa_inv, cons
  * for make_problem(equation, n) and stage coefficient (tau, a). */
 int mprkb_op_fastdiag_stage(int dtype, int equation, int n, double tau, double a, int numerics,
                             mprkb_op** out);
+/* The same for make_problem(equation, n, nu): nu is the diffusion
+ * coefficient of MPRKB_ADVECTION_DIFFUSION (ignored otherwise). */
+int mprkb_op_fastdiag_stage_nu(int dtype, int equation, int n, double nu, double tau, double a,
+                               int numerics, mprkb_op** out);
+/* stage_operator(problem, tau, a) = I - tau a K (operators.cpp:77-79) as a
+ * device stencil operator, for make_problem(equation, n, nu). */
+int mprkb_op_stage_operator(int dtype, int equation, int n, double nu, double tau, double a,
+                            mprkb_op** out);
 /* Block-Jacobi stage preconditioner (north_star extension; no reference
  * counterpart): exact inverses of the x-line blocks of length `block` of
  * (I - tau a K), stored in `storage` precision (F16/F32/F64), applied in dtype. */
 int mprkb_op_block_jacobi(int dtype, int equation, int n, double tau, double a, int block,
                           int storage, mprkb_op** out);
+int mprkb_op_block_jacobi_nu(int dtype, int equation, int n, double nu, double tau, double a,
+                             int block, int storage, mprkb_op** out);
 /* CSR operator y = A x (north_star extension): host CSR arrays (int32 row_ptr
  * (rows+1), int32 cols, values in `storage` precision F16/F32/F64), applied in dtype. */
 int mprkb_op_csr(int dtype, int rows, const int* row_ptr, const int* cols, const void* values,
@@ -222,8 +232,14 @@ int mprkb_stepper_create(const mprkb_config* cfg, mprkb_stepper** out);
 /* Stepper::step(u, trace) (stepper.cpp:149-206) on a HOST vector of n^3
  * doubles, updated in place (copied in and out every call). */
 int mprkb_stepper_step(mprkb_stepper* s, double* u_host, mprkb_step_trace* trace);
-/* The same step on a DEVICE vector (state stays resident in HBM). */
+/* The same step on a DEVICE vector (state stays resident in HBM).  The step
+ * is ordered after all work already queued on the legacy default stream
+ * (e.g. the kernels that produced u_dev) and has finished on the device when
+ * the call returns. */
 int mprkb_stepper_step_device(mprkb_stepper* s, double* u_dev, mprkb_step_trace* trace);
+/* Same, ordered after the work queued on `stream` (a cudaStream_t; null =
+ * the legacy default stream) instead. */
+int mprkb_stepper_step_device_on(mprkb_stepper* s, double* u_dev, mprkb_step_trace* trace, void* stream);
 /* problem().initial_state (host). */
 int mprkb_stepper_initial_state(mprkb_stepper* s, double* u_host);
 /* Residual history of solve `idx` of the last step. */

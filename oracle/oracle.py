@@ -153,6 +153,32 @@ class Reference:
         return x, dict(iterations=it.value, converged=bool(cv.value), failure=fl.value,
                        true_residual=tr.value, history=hist[: hl.value].copy())
 
+    def krylov_cb(self, kind, solver, op, precond, b, x0, tol, max_iter):
+        """The reference's own cg (solver 0) / gmres (1) on a caller-defined
+        system: op(x) and precond(x) (None: identity) are numpy callables
+        (the ApplyFn slot, krylov.hpp:38-39)."""
+        b = np.ascontiguousarray(b, dtype=DT[kind]); x0 = np.ascontiguousarray(x0, dtype=DT[kind])
+        m = b.size
+        x = np.empty_like(b)
+
+        def wrap(fn):
+            def tramp(ctx, xp, outp):
+                xin = np.ctypeslib.as_array(C.cast(xp, C.POINTER(C.c_byte)), shape=(m * b.itemsize,)).view(b.dtype)
+                out = np.ctypeslib.as_array(C.cast(outp, C.POINTER(C.c_byte)), shape=(m * b.itemsize,)).view(b.dtype)
+                out[:] = fn(xin.copy())
+            return self.CB(tramp)
+
+        cbo = wrap(op)
+        cbp = wrap(precond) if precond is not None else self.CB()
+        it = C.c_int(); cv = C.c_int(); fl = C.c_int(); tr = C.c_double(); hl = C.c_int()
+        hist = np.zeros(max_iter + 8)
+        self.lib.ref_krylov_cb.restype = C.c_int
+        self._chk(self.lib.ref_krylov_cb(kind, solver, C.c_longlong(m), cbo, None, cbp, None, _p(b), _p(x0),
+                                         C.c_double(tol), max_iter, _p(x), C.byref(it), C.byref(cv), C.byref(fl),
+                                         C.byref(tr), _p(hist), len(hist), C.byref(hl)))
+        return x, dict(iterations=it.value, converged=bool(cv.value), failure=fl.value,
+                       true_residual=tr.value, history=hist[: hl.value].copy())
+
     def stepper(self, eq, n, tab, tau, tol, precision, max_iter=40, t_end=0.1):
         return RefStepper(self, eq, n, tab, tau, tol, precision, max_iter, t_end)
 

@@ -370,6 +370,45 @@ int ref_stage_solve_cb(int dtype, int solver, int n, double tau, double a, ref_a
   });
 }
 
+// Krylov solve of a caller-defined system: operator AND preconditioner are
+// callbacks on host vectors of m scalars of the dtype (the ApplyFn slot,
+// krylov.hpp:38-39), consumed by the reference's own cg / gmres
+// (krylov.hpp:100-168, 181-311).  The route for operators the reference does
+// not have (advection-diffusion).
+int ref_krylov_cb(int dtype, int solver, long long m, ref_apply_cb opf, void* op_ctx, ref_apply_cb pre,
+                  void* pre_ctx, const void* b, const void* x0, double tol, int max_iter, void* x_out, int* iters,
+                  int* converged, int* failure, double* true_res, double* hist, int hist_cap, int* hist_len) {
+  return guarded([&] {
+    const StoppingCriterion crit{tol, max_iter};
+    SolveReport rep;
+    auto solve = [&](auto tag) {
+      using T = decltype(tag);
+      ApplyFn<T> A = [&](const std::vector<T>& v, std::vector<T>& o) {
+        o.resize(v.size());
+        opf(op_ctx, v.data(), o.data());
+      };
+      ApplyFn<T> P = [&](const std::vector<T>& v, std::vector<T>& o) {
+        o.resize(v.size());
+        if (pre)
+          pre(pre_ctx, v.data(), o.data());
+        else
+          o = v;
+      };
+      const std::size_t mm = static_cast<std::size_t>(m);
+      std::vector<T> x = solver == 0 ? cg<T>(A, P, vec<T>(b, mm), vec<T>(x0, mm), crit, rep)
+                                     : gmres<T>(A, P, vec<T>(b, mm), vec<T>(x0, mm), crit, rep);
+      put(x, x_out);
+    };
+    switch (dtype) {
+      case 0: solve(float{}); break;
+      case 1: solve(double{}); break;
+      case 2: solve(cf{}); break;
+      default: solve(cd{}); break;
+    }
+    fill_report(rep, iters, converged, failure, true_res, hist, hist_cap, hist_len);
+  });
+}
+
 // --- Stepper / integrate ------------------------------------------------------
 
 struct RefStepper {

@@ -281,7 +281,11 @@ class Stepper:
         """One step on a CUDA float64 tensor (no host copies)."""
         if u.dtype.is_complex or u.element_size() != 8 or u.numel() != self.size or not u.is_contiguous():
             raise LengthMismatch("step_device: u must be a contiguous CUDA float64 tensor of length n^3")
-        check(_c.lib.mprkb_stepper_step_device(self._h, C.c_void_p(u.data_ptr()), C.byref(self._trace)))
+        # ordered after torch's current stream (whatever produced u)
+        import torch
+        cs = torch.cuda.current_stream(u.device).cuda_stream
+        check(_c.lib.mprkb_stepper_step_device_on(self._h, C.c_void_p(u.data_ptr()), C.byref(self._trace),
+                                                  C.c_void_p(cs)))
         return self._trace_dict()
 
     def history(self, idx: int) -> np.ndarray:
@@ -552,11 +556,19 @@ class Operator:
         return Operator(h, dtype, n ** 3)
 
     @staticmethod
+    def stage_operator(dtype: int, equation: str, n: int, tau: float, a: float, nu: float = 0.0) -> "Operator":
+        """stage_operator(make_problem(equation, n), tau, a) = I - tau a K (operators.cpp:77-79);
+        nu: diffusion coefficient of the advection-diffusion extension."""
+        h = C.c_void_p()
+        check(_c.lib.mprkb_op_stage_operator(dtype, _EQ[equation], n, nu, tau, a, C.byref(h)))
+        return Operator(h, dtype, n ** 3)
+
+    @staticmethod
     def fastdiag_stage(dtype: int, equation: str, n: int, tau: float, a: float,
-                       numerics: str = "fast") -> "Operator":
+                       numerics: str = "fast", nu: float = 0.0) -> "Operator":
         """build_heat_precond(_f32) / build_advection_precond(_f32) (precond.cpp:14-42)."""
         h = C.c_void_p()
-        check(_c.lib.mprkb_op_fastdiag_stage(dtype, _EQ[equation], n, tau, a, _NUM[numerics], C.byref(h)))
+        check(_c.lib.mprkb_op_fastdiag_stage_nu(dtype, _EQ[equation], n, nu, tau, a, _NUM[numerics], C.byref(h)))
         return Operator(h, dtype, n ** 3)
 
     @staticmethod
@@ -571,9 +583,10 @@ class Operator:
 
     @staticmethod
     def block_jacobi(dtype: int, equation: str, n: int, tau: float, a: float, block: int,
-                     storage: str = "f32") -> "Operator":
+                     storage: str = "f32", nu: float = 0.0) -> "Operator":
         h = C.c_void_p()
-        check(_c.lib.mprkb_op_block_jacobi(dtype, _EQ[equation], n, tau, a, block, _STORE[storage], C.byref(h)))
+        check(_c.lib.mprkb_op_block_jacobi_nu(dtype, _EQ[equation], n, nu, tau, a, block, _STORE[storage],
+                                              C.byref(h)))
         return Operator(h, dtype, n ** 3)
 
     @staticmethod

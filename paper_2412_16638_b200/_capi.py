@@ -149,6 +149,9 @@ SIGNATURES = {
     "mprkb_op_fastdiag": (i32, [i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, i32, C.POINTER(vp)]),
     "mprkb_op_fastdiag_stage": (i32, [i32, i32, i32, f64, f64, i32, C.POINTER(vp)]),
     "mprkb_op_block_jacobi": (i32, [i32, i32, i32, f64, f64, i32, i32, C.POINTER(vp)]),
+    "mprkb_op_block_jacobi_nu": (i32, [i32, i32, i32, f64, f64, f64, i32, i32, C.POINTER(vp)]),
+    "mprkb_op_fastdiag_stage_nu": (i32, [i32, i32, i32, f64, f64, f64, i32, C.POINTER(vp)]),
+    "mprkb_op_stage_operator": (i32, [i32, i32, i32, f64, f64, f64, C.POINTER(vp)]),
     "mprkb_op_csr": (i32, [i32, i32, vp, vp, vp, i32, C.POINTER(vp)]),
     "mprkb_op_csr_stencil": (i32, [i32, i32, i32, f64, f64, i32, C.POINTER(vp)]),
     "mprkb_op_callback": (i32, [i32, sz, APPLY_FN, vp, C.POINTER(vp)]),
@@ -161,6 +164,7 @@ SIGNATURES = {
     "mprkb_stepper_create": (i32, [C.POINTER(Config), C.POINTER(vp)]),
     "mprkb_stepper_step": (i32, [vp, vp, C.POINTER(StepTrace)]),
     "mprkb_stepper_step_device": (i32, [vp, vp, C.POINTER(StepTrace)]),
+    "mprkb_stepper_step_device_on": (i32, [vp, vp, C.POINTER(StepTrace), vp]),
     "mprkb_stepper_initial_state": (i32, [vp, vp]),
     "mprkb_stepper_history": (i32, [vp, i32, dptr, i32, ip]),
     "mprkb_stepper_stream": (vp, [vp]),

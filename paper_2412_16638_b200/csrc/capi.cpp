@@ -123,8 +123,10 @@ struct mprkb_stepper {
   StepTrace last;
   DevBuf u;  // staging for the host-buffer entry point
   double* pinned = nullptr;
+  cudaEvent_t produced = nullptr;  // orders the step after the caller's stream
   ~mprkb_stepper() {
     if (pinned) cudaFreeHost(pinned);
+    if (produced) cudaEventDestroy(produced);
   }
 };
 
@@ -319,6 +321,35 @@ int mprkb_op_fastdiag_stage(int dtype, int equation, int n, double tau, double a
     check_dtype(dtype);
     const Problem p = make_problem(eq_of(equation), n);
     *out = new mprkb_op{make_stage_fastdiag(dtype, p, tau, a, num_of(numerics))};
+  });
+}
+
+int mprkb_op_stage_operator(int dtype, int equation, int n, double nu, double tau, double a, mprkb_op** out) {
+  return guarded([&] {
+    check_dtype(dtype);
+    const Problem p = make_problem(eq_of(equation), n, nu);
+    *out = new mprkb_op{std::make_unique<StencilOp>(dtype, stage_spec(p, tau, a))};
+  });
+}
+
+int mprkb_op_fastdiag_stage_nu(int dtype, int equation, int n, double nu, double tau, double a, int numerics,
+                               mprkb_op** out) {
+  return guarded([&] {
+    require_device();
+    check_dtype(dtype);
+    const Problem p = make_problem(eq_of(equation), n, nu);
+    *out = new mprkb_op{make_stage_fastdiag(dtype, p, tau, a, num_of(numerics))};
+  });
+}
+
+int mprkb_op_block_jacobi_nu(int dtype, int equation, int n, double nu, double tau, double a, int block,
+                             int storage, mprkb_op** out) {
+  return guarded([&] {
+    require_device();
+    check_dtype(dtype);
+    check_dtype(storage, true);
+    const Problem p = make_problem(eq_of(equation), n, nu);
+    *out = new mprkb_op{make_block_jacobi(dtype, p, tau, a, block, storage)};
   });
 }
 
@@ -580,11 +611,23 @@ int mprkb_stepper_step(mprkb_stepper* s, double* u_host, mprkb_step_trace* trace
   });
 }
 
-int mprkb_stepper_step_device(mprkb_stepper* s, double* u_dev, mprkb_step_trace* trace) {
+int mprkb_stepper_step_device_on(mprkb_stepper* s, double* u_dev, mprkb_step_trace* trace, void* stream) {
   return guarded([&] {
+    // the step runs on the stepper's own (non-blocking) stream: make it wait
+    // for whatever the caller's stream still has pending on u (the step
+    // itself returns only after its last kernel, so no ordering is needed on
+    // the way out)
+    if (!s->produced) CUDA_CHECK(cudaEventCreateWithFlags(&s->produced, cudaEventDisableTiming));
+    cudaStream_t cs = stream ? (cudaStream_t)stream : cudaStreamLegacy;
+    CUDA_CHECK(cudaEventRecord(s->produced, cs));
+    CUDA_CHECK(cudaStreamWaitEvent(s->s->stream(), s->produced, 0));
     s->s->step(u_dev, s->last);
     fill_trace(s->last, trace);
   });
+}
+
+int mprkb_stepper_step_device(mprkb_stepper* s, double* u_dev, mprkb_step_trace* trace) {
+  return mprkb_stepper_step_device_on(s, u_dev, trace, nullptr);
 }
 
 int mprkb_stepper_initial_state(mprkb_stepper* s, double* u_host) {

@@ -72,6 +72,7 @@ void apply_f32(const StencilSpec& k, const double* y, const float* y32, const fl
 // fp32 stage vector y32, Dirichlet stencil on the TMA path): see
 // EpiFevalCombine in stencil.cu.  All pointers are device vectors of the local
 // grid; `sin` / `ain[a]` may alias `aout[a]` (read-modify-write in place).
+constexpr int kFevalMaxAcc = 6;  // accumulators one fused pass carries (stencil.cu kMaxAcc)
 struct FevalCombine {
   const double* g = nullptr;
   const float* g32 = nullptr;
@@ -84,10 +85,10 @@ struct FevalCombine {
   float* xout = nullptr;
   int* ovf_flag = nullptr;
   int nacc = 0;
-  const double* ain[6] = {};
-  double* aout[6] = {};
-  double ah[6] = {}, ae[6] = {};
-  int hah[6] = {}, hae[6] = {};
+  const double* ain[kFevalMaxAcc] = {};
+  double* aout[kFevalMaxAcc] = {};
+  double ah[kFevalMaxAcc] = {}, ae[kFevalMaxAcc] = {};
+  int hah[kFevalMaxAcc] = {}, hae[kFevalMaxAcc] = {};
 };
 bool feval_combine_supported(const StencilSpec& k);
 void feval_combine(const StencilSpec& k, const float* y32, const FevalCombine& f, cudaStream_t st);

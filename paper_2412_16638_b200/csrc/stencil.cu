@@ -389,7 +389,7 @@ struct EpiF32Forcing {
 // reference's term order (j ascending, the fp64 term before the eps term, the
 // forcing last), so every value is rounded exactly as the per-stage
 // combination would round it; f_eps never touches HBM.
-constexpr int kMaxAcc = 6;
+constexpr int kMaxAcc = kFevalMaxAcc;
 struct EpiFevalCombine {
   static constexpr bool kDual = true;
   float s32 = 0.f, g32k = 0.f;    // the binary32 stencil's sigma / gamma
@@ -419,7 +419,8 @@ struct EpiFevalCombine {
   __device__ __forceinline__ Pre pre4(long i) const {
     Pre p;
     p.s = ld4(sin + i);
-    p.a0 = nacc > 0 ? ld4(ain[0] + i) : zero4<double>();
+    // accumulators are updated in place (ain[a] == aout[a] after stage 0): coherent loads
+    p.a0 = nacc > 0 ? ld4rw(ain[0] + i) : zero4<double>();
     return p;
   }
   __device__ __forceinline__ void v4dual(State&, long i, const V4<double>& v64, const V4<float>& v32,
@@ -456,7 +457,7 @@ struct EpiFevalCombine {
     if (xout) st4(xout + i, b);
     if (ovf) *ovf_flag = 1;
     for (int a = 0; a < nacc; ++a) {
-      V4<double> s = a == 0 ? p.a0 : ld4(ain[a] + i);
+      V4<double> s = a == 0 ? p.a0 : ld4rw(ain[a] + i);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         if (hah[a]) s.x[e] = xadd(s.x[e], xmul(ah[a], fh.x[e]));

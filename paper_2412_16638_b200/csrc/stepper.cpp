@@ -141,28 +141,39 @@ Stepper::Stepper(const StepperConfig& cfg)
       }
     }
   }
-  f_hi_.resize(q);
-  f_eps_.resize(q);
-  for (int i = 0; i < q; ++i) {
-    if (need_f64_[i]) f_hi_[i].alloc(m * sizeof(double));
-    if (need_feps_[i] && (cfg_.f32 || !need_f64_[i])) f_eps_[i].alloc(m * (cfg_.f32 ? sizeof(float) : sizeof(double)));
-  }
-  y_.alloc(m * sizeof(double));
-  gate_dev_.alloc(sizeof(int) * 256);
   {
     // fused stage pipeline: fp32 heat stages, every stage implicit, forcing
-    // present, the TMA stencil path (MPRKB_FUSED_STAGES=0 disables it)
+    // present, the TMA stencil path (MPRKB_FUSED_STAGES=0 disables it).
+    // Stage 0's pass carries q-2 later-stage accumulators, plus the final
+    // update's running sum when that is fused too (MPRKB_FUSED_FINAL=0 keeps
+    // stored f_hi vectors and a separate final update) — at most
+    // kFevalMaxAcc in one pass.
     const char* env = std::getenv("MPRKB_FUSED_STAGES");
     bool ok = !(env && env[0] == '0') && cfg_.eq == Equation::Heat && cfg_.f32 &&
-              q >= 2 && q - 2 <= 6 && !prob_.forcing.empty() && feval_combine_supported(kspec_);
+              q >= 2 && q - 2 <= kFevalMaxAcc && !prob_.forcing.empty() && feval_combine_supported(kspec_);
     for (int i = 0; i < q; ++i) ok = ok && t.ae(i, i) != 0.0 && t.ah(i, i) == 0.0;
     fused_ = ok;
+    const char* fe = std::getenv("MPRKB_FUSED_FINAL");
+    fuse_final_ = fused_ && !(fe && fe[0] == '0') && t.b[q - 1] != 0.0 && q - 1 <= kFevalMaxAcc;
     if (fused_) {
       acc_.resize(q + 1);
       for (int k = 2; k < q; ++k) acc_[k].alloc(m * sizeof(double));
-      acc_[q].alloc(m * sizeof(double));  // the final update's running sum (u + tau sum b_i f_hi_i)
+      if (fuse_final_) acc_[q].alloc(m * sizeof(double));  // the final update's running sum (u + tau sum b_i f_hi_i)
     }
   }
+  f_hi_.resize(q);
+  f_eps_.resize(q);
+  for (int i = 0; i < q; ++i) {
+    // the fused pipeline keeps f_eps in registers, and f_hi too when the
+    // final update is fused; it stores f_hi only for b_i != 0 otherwise
+    const bool hi = fused_ ? (!fuse_final_ && t.b[i] != 0.0) : need_f64_[i] != 0;
+    const bool eps = !fused_ && need_feps_[i] && (cfg_.f32 || !need_f64_[i]);
+    if (hi) f_hi_[i].alloc(m * sizeof(double));
+    if (eps) f_eps_[i].alloc(m * (cfg_.f32 ? sizeof(float) : sizeof(double)));
+  }
+  if (!fused_) y_.alloc(m * sizeof(double));
+  else if (!fuse_final_ && t.b[q - 1] == 0.0) y_.alloc(m * sizeof(double));
+  gate_dev_.alloc(sizeof(int) * 256);
   if (!solvers_.empty()) {
     const size_t s = dtype_size(solve_dtype_);
     bsol_.alloc(m * s);
@@ -410,12 +421,8 @@ void Stepper::step_fused(double* u, StepTrace& trace) {
   // acc_[q], in the reference's term order (u, then i ascending), while each
   // f_hi is in registers — so no f_hi is stored; the last stage's term is
   // added by the final pass (MPRKB_FUSED_FINAL=0: stored f_hi + final_update)
-  static const bool fuse_final_env = [] {
-    const char* e = std::getenv("MPRKB_FUSED_FINAL");
-    return !(e && e[0] == '0');
-  }();
   const int last = q - 1;
-  const bool fuse_final = t.b[last] != 0.0 && fuse_final_env;
+  const bool fuse_final = fuse_final_;
   bool fin_started = false;  // acc_[q] holds u + earlier terms
   float* cur = solve(0);  // stage i's solution
   for (int i = 0; i + 1 < q; ++i) {
@@ -445,6 +452,7 @@ void Stepper::step_fused(double* u, StepTrace& trace) {
       f.ae[a] = tau * t.ae(k, i);
     }
     if (fuse_final && t.b[i] != 0.0) {
+      if (f.nacc >= kFevalMaxAcc) MPRKB_THROW(10, "feval_combine: too many accumulators");
       const int a = f.nacc++;
       f.ain[a] = fin_started ? acc_[q].as<double>() : u;
       f.aout[a] = acc_[q].as<double>();

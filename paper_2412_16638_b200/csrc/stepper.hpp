@@ -61,6 +61,7 @@ class Stepper {
   void step_fused(double* u, StepTrace& trace);
   void add_forcing(CombineTerms& t, double coef) const;  // + coef g (regenerated or read)
   bool fused_ = false;
+  bool fuse_final_ = false;  // fused pipeline also accumulates the final update (decided at construction)
   std::vector<DevBuf> acc_;
   DevBuf gtab_;     // sin table of the regenerated heat forcing
   ForcingGen gen_;  // (types.hpp) s == nullptr: g is read from g64_ / g32_

@@ -1,0 +1,218 @@
+"""BASELINE.json configs pinned against the reference at their stated sizes.
+
+* configs[1] — heat 256^3, 4s3pB, tau 0.01, 10 steps (t_end 0.1), fp32 stage
+  solves at tol 1e-3 (the bench path: FAST numerics, tcgen05 FastDiag, fused
+  stage pipeline) and the fp64 "baseline stepper" at tol 1e-5, against the
+  UNMODIFIED reference's ``integrate`` (stepper.cpp:218-269) recorded in
+  tests/golden/configs.npz by tests/golden/make_golden_configs.py.  Bars
+  (north_star): iteration counts +-1 per solve; final-time
+  error_max / error_l2 within 1% of the reference's; the state within 2x the
+  reference's own fp32-vs-fp64 distance (fp32) or 1e-11 relative (fp64, 10
+  steps of the 1e-12-per-step bar).
+* configs[1] midpoint1, one step at 256^3: FAST within 2x the reference's own
+  fp32 noise; PARITY bitwise (subsampled state and full-grid moments).
+* configs[3] — advection-diffusion stage solves with complex-fp32 GMRES: the
+  GPU solver vs the reference's OWN gmres<complex<float>> with a numpy
+  operator and preconditioner plugged into its ApplyFn slot
+  (oracle/ref_shim.cpp ref_krylov_cb), at n = 32 and 64, with the
+  combined-eigenvalue FastDiag (FFT) and with block-Jacobi; the fp16 Krylov
+  basis against oracle/krylov_np.gmres_basis16 (krylov.hpp:181-311 restated
+  with the basis stored in binary16).
+* configs[4] — block-Jacobi CG at 64^3, b in {4, 32} x storage {f16, f32, f64}
+  x tol {1e-4, 1e-6}: iteration counts +-1 against the reference's own
+  cg<float> with the numpy block-Jacobi ApplyFn.
+"""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+GOLD = os.path.join(HERE, "golden", "configs.npz")
+
+
+@pytest.fixture(scope="module")
+def gold():
+    if not os.path.exists(GOLD):
+        pytest.fail("tests/golden/configs.npz missing (run tests/golden/make_golden_configs.py)")
+    return dict(np.load(GOLD))
+
+
+def _sub(state, n=256, s=8):
+    return state.reshape(n, n, n)[::s, ::s, ::s]
+
+
+def _moments(s):
+    return np.array([s.sum(), np.dot(s, s), np.abs(s).max()])
+
+
+# ---- configs[1]: 256^3 4s3pB, 10 steps ---------------------------------------------------
+def test_config2_4s3pB_256_fp32_ten_steps(gpu, mp, gold):
+    r = mp.integrate(mp.builtin("4s3pB"), "heat", 256, 0.01, 0.1, 1e-3, "f32", 40)
+    want_it = gold["c2_f32_iters"]
+    got_it = np.array(r["solve_iterations"])
+    assert got_it.shape == want_it.shape
+    assert np.abs(got_it - want_it).max() <= 1, (got_it, want_it)
+    em, el = gold["c2_f32_err"][:2]
+    assert abs(r["error_max"] - em) <= 0.01 * em, (r["error_max"], em)
+    assert abs(r["error_l2"] - el) <= 0.01 * el, (r["error_l2"], el)
+    # state: within 2x the reference's own fp32-vs-fp64 distance
+    g, r32, r64 = _sub(r["state"]), gold["c2_f32_sub"], gold["c2_f64_sub"]
+    noise = np.linalg.norm(r32 - r64)
+    assert np.linalg.norm(g - r32) <= 2 * noise, (np.linalg.norm(g - r32), noise)
+    assert not r["solver_failure"]
+
+
+def test_config2_4s3pB_256_fp64_baseline_stepper(gpu, mp, gold):
+    r = mp.integrate(mp.builtin("4s3pB"), "heat", 256, 0.01, 0.1, 1e-5, "f64", 40)
+    assert np.array_equal(np.array(r["solve_iterations"]), gold["c2_f64_iters"])
+    g, w = _sub(r["state"]), gold["c2_f64_sub"]
+    assert np.linalg.norm(g - w) <= 1e-11 * np.linalg.norm(w)
+    m, wm = _moments(r["state"]), gold["c2_f64_moments"]
+    assert np.all(np.abs(m - wm) <= 1e-11 * np.abs(wm))
+    em, el = gold["c2_f64_err"][:2]
+    assert abs(r["error_max"] - em) <= 1e-6 * em and abs(r["error_l2"] - el) <= 1e-6 * el
+
+
+# ---- configs[1]: midpoint1 one step at 256^3 ---------------------------------------------
+def test_midpoint1_256_one_step_fast_within_reference_noise(gpu, mp, gold):
+    r = mp.integrate(mp.midpoint_corrected(1), "heat", 256, 0.01, 0.01, 1e-3, "f32", 40)
+    assert r["solve_iterations"] == gold["m1_f32_iters"].tolist()
+    g, r32, r64 = _sub(r["state"]), gold["m1_f32_sub"], gold["m1_f64_sub"]
+    noise = np.linalg.norm(r32 - r64)
+    assert np.linalg.norm(g - r32) <= 2 * noise, (np.linalg.norm(g - r32), noise)
+    # error against heat_exact: the reference's fp32 value is rounding
+    # dominated (1.31e-2 vs 1.01e-4 in fp64, SURVEY §0 finding 3)
+    em32, em64 = gold["m1_f32_err"][0], gold["m1_f64_err"][0]
+    assert abs(r["error_max"] - em32) <= 2 * abs(em32 - em64)
+    r64g = mp.integrate(mp.midpoint_corrected(1), "heat", 256, 0.01, 0.01, 1e-5, "f64", 40)
+    assert np.linalg.norm(_sub(r64g["state"]) - r64) <= 1e-12 * np.linalg.norm(r64)
+    assert abs(r64g["error_max"] - em64) <= 1e-9 * em64
+
+
+def test_midpoint1_256_one_step_parity_bitwise(gpu, mp, gold):
+    for prec, tol in (("f32", 1e-3), ("f64", 1e-5)):
+        r = mp.integrate(mp.midpoint_corrected(1), "heat", 256, 0.01, 0.01, tol, prec, 40, numerics="parity")
+        key = "m1_" + prec
+        assert np.array_equal(_sub(r["state"]), gold[key + "_sub"]), prec
+        assert np.array_equal(_moments(r["state"]), gold[key + "_moments"]), prec
+        assert r["error_max"] == gold[key + "_err"][0] and r["error_l2"] == gold[key + "_err"][1]
+
+
+# ---- configs[3]: advection-diffusion GMRES -----------------------------------------------
+NU, TAU_AD, A_AD = 0.01, 1.0 / 640.0, 0.5
+
+
+def _adv_rhs(n):
+    from oracle.krylov_np import AdvDiff  # noqa: F401
+
+    h = 1.0 / n
+    x = np.arange(n) * h - 0.5
+    X, Y, Z = np.meshgrid(x, x, x, indexing="ij")
+    u0 = np.exp(-100.0 * (X ** 2 + Y ** 2 + Z ** 2)).transpose(2, 1, 0).ravel()  # [k][j][i]
+    rng = np.random.default_rng(n)
+    return (u0 + 1e-3 * rng.uniform(-1, 1, n ** 3)).astype(np.complex64)
+
+
+@pytest.mark.parametrize("n", [32, 64])
+def test_config4_gmres_fastdiag_vs_reference_gmres(gpu, mp, ref, n):
+    import torch
+    from oracle.krylov_np import AdvDiff
+
+    s, g, g2 = AdvDiff.stage(n, TAU_AD, A_AD, NU)
+    ad = AdvDiff(n, s, g, g2)
+    b = _adv_rhs(n)
+    tol = 1e-3
+    xw, rw = ref.krylov_cb(2, 1, ad.apply, ad.solve, b, b, tol, 40)
+    A = mp.Operator.stage_operator(2, "advection-diffusion", n, TAU_AD, A_AD, nu=NU)
+    P = mp.Operator.fastdiag_stage(2, "advection-diffusion", n, TAU_AD, A_AD, nu=NU)
+    bd = torch.from_numpy(b).cuda()
+    # the device operators are the oracle's operators
+    assert np.abs(A.apply(bd).cpu().numpy() - ad.apply(b)).max() <= 1e-5 * np.abs(b).max() * abs(g) * 8
+    z = P.apply(bd).cpu().numpy()
+    assert np.linalg.norm(z - ad.solve(b)) <= 2e-5 * np.linalg.norm(z)
+    xg, rg = mp.gmres(A, P, bd, bd.clone(), tol, 40)
+    assert rw["converged"] and rg["converged"]
+    assert abs(rg["iterations"] - rw["iterations"]) <= 1, (rg, rw)
+    assert np.linalg.norm(xg.cpu().numpy() - xw) <= 1e-5 * np.linalg.norm(xw)
+    assert abs(rg["true_residual"] - rw["true_residual"]) <= 0.5 * rw["true_residual"] + 1e-6
+
+
+@pytest.mark.parametrize("n", [32, 64])
+@pytest.mark.parametrize("storage", ["f16", "f32"])
+def test_config4_gmres_block_jacobi_vs_reference_gmres(gpu, mp, ref, n, storage):
+    import torch
+    from oracle.krylov_np import AdvDiff, BlockJacobi
+
+    s, g, g2 = AdvDiff.stage(n, TAU_AD, A_AD, NU)
+    ad = AdvDiff(n, s, g, g2)
+    bj = BlockJacobi(n, 8, s, g, storage, np.complex64, gamma2=g2)
+    b = _adv_rhs(n)
+    tol = 1e-4
+    xw, rw = ref.krylov_cb(2, 1, ad.apply, bj, b, np.zeros_like(b), tol, 80)
+    A = mp.Operator.stage_operator(2, "advection-diffusion", n, TAU_AD, A_AD, nu=NU)
+    P = mp.Operator.block_jacobi(2, "advection-diffusion", n, TAU_AD, A_AD, 8, storage, nu=NU)
+    bd = torch.from_numpy(b).cuda()
+    xg, rg = mp.gmres(A, P, bd, torch.zeros_like(bd), tol, 80)
+    assert rw["converged"] and rg["converged"] and rw["iterations"] > 2
+    assert abs(rg["iterations"] - rw["iterations"]) <= 1, (rg["iterations"], rw["iterations"])
+    assert np.linalg.norm(xg.cpu().numpy() - xw) <= 10 * tol * np.linalg.norm(xw)
+
+
+@pytest.mark.parametrize("n", [32, 64])
+def test_config4_gmres_fp16_basis_vs_restatement(gpu, mp, ref, n):
+    """fp16 Krylov basis, fp64-accumulated Gram-Schmidt: the GPU solver vs the
+    reference's GMRES restated with the basis stored in binary16
+    (oracle/krylov_np.gmres_basis16); and the restatement itself lands where
+    the reference's working-precision GMRES does."""
+    import torch
+    from oracle.krylov_np import AdvDiff, BlockJacobi, gmres_basis16
+
+    s, g, g2 = AdvDiff.stage(n, TAU_AD, A_AD, NU)
+    ad = AdvDiff(n, s, g, g2)
+    bj = BlockJacobi(n, 8, s, g, "f32", np.complex64, gamma2=g2)
+    b = _adv_rhs(n)
+    tol = 1e-3
+    xo, ro = gmres_basis16(ad.apply, bj, b, np.zeros_like(b), tol, 80)
+    xw, rw = ref.krylov_cb(2, 1, ad.apply, bj, b, np.zeros_like(b), tol, 80)
+    A = mp.Operator.stage_operator(2, "advection-diffusion", n, TAU_AD, A_AD, nu=NU)
+    P = mp.Operator.block_jacobi(2, "advection-diffusion", n, TAU_AD, A_AD, 8, "f32", nu=NU)
+    bd = torch.from_numpy(b).cuda()
+    xg, rg = mp.gmres(A, P, bd, torch.zeros_like(bd), tol, 80, basis_storage="f16")
+    assert ro["converged"] and rg["converged"] and ro["iterations"] > 2
+    assert abs(rg["iterations"] - ro["iterations"]) <= 1, (rg["iterations"], ro["iterations"])
+    h = min(len(rg["history"]), len(ro["history"])) - 1
+    np.testing.assert_allclose(rg["history"][:h], ro["history"][:h], rtol=2e-2, atol=1e-3 * ro["history"][0])
+    assert np.linalg.norm(xg.cpu().numpy() - xo) <= 10 * tol * np.linalg.norm(xo)
+    assert abs(ro["iterations"] - rw["iterations"]) <= 2
+    assert np.linalg.norm(xo - xw) <= 10 * tol * np.linalg.norm(xw)
+
+
+# ---- configs[4]: block-Jacobi CG sweep at 64^3 -------------------------------------------
+@pytest.mark.parametrize("tol", [1e-4, 1e-6])
+@pytest.mark.parametrize("storage", ["f16", "f32", "f64"])
+@pytest.mark.parametrize("b", [4, 32])
+def test_config5_block_jacobi_cg_iterations_64(gpu, mp, ref, b, storage, tol):
+    import torch
+    from oracle.krylov_np import BlockJacobi
+
+    n, tau, a = 64, 0.01, 0.5  # a_ii of 4s3pB's stages is 1/2 (tableau.cpp)
+    h = 1.0 / (n - 1)
+    sigma, gamma = 1.0, -tau * a * (-1.0 / h ** 2)
+    u0, gvec, _, _ = ref.make_problem(0, n)
+    rhs = (ref.heat_exact(n, 0.05) + tau * a * gvec).astype(np.float32)
+    pre = BlockJacobi(n, b, sigma, gamma, storage, np.float32)
+    cap = 400
+    xw, rw = ref.stage_solve_cb(0, 0, n, tau, a, pre, rhs, rhs, tol, cap)
+    A = mp.Operator.stencil(0, n, 0, sigma, gamma)
+    P = mp.Operator.block_jacobi(0, "heat", n, tau, a, b, storage)
+    bd = torch.from_numpy(rhs).cuda()
+    for numerics in ("fast", "parity"):
+        xg, rg = mp.cg(A, P, bd, bd.clone(), tol, cap, numerics)
+        assert rg["converged"] == rw["converged"], (numerics, rg["iterations"], rw["iterations"])
+        assert abs(rg["iterations"] - rw["iterations"]) <= 1, (numerics, rg["iterations"], rw["iterations"])
+        if rw["converged"]:
+            err = np.linalg.norm(xg.cpu().numpy() - xw) / np.linalg.norm(xw)
+            assert err <= 10 * tol
