@@ -451,3 +451,50 @@ def test_fused_final_update_bitwise(gpu, mp):
     for _ in range(3):
         assert fused.step(a)["iterations"] == plain.step(b)["iterations"]
     assert same_bits(a, b)
+
+
+def test_fused_final_switch_per_stepper_bitwise(gpu, mp):
+    """MPRKB_FUSED_FINAL is read per Stepper at construction: the fused
+    pipeline with the final update accumulated stage by stage is bitwise the
+    same pipeline with stored f_hi vectors and a separate final update."""
+    import os
+
+    t = mp.builtin("4s3pB")
+    n = 128
+    fused = mp.Stepper("heat", n, t, 0.01, 1e-4, "f32", 40)
+    os.environ["MPRKB_FUSED_FINAL"] = "0"
+    try:
+        stored = mp.Stepper("heat", n, t, 0.01, 1e-4, "f32", 40)
+    finally:
+        os.environ.pop("MPRKB_FUSED_FINAL", None)
+    a, b = np.zeros(n ** 3), np.zeros(n ** 3)
+    for _ in range(3):
+        assert fused.step(a)["iterations"] == stored.step(b)["iterations"]
+    assert same_bits(a, b)
+
+
+@pytest.mark.parametrize("q", [7, 8])
+def test_fused_pipeline_many_stages(gpu, mp, q):
+    """An all-implicit q-stage tableau with every b_i != 0: stage 0's fused
+    pass carries q-2 later-stage accumulators plus the final update's running
+    sum (q = 7 fills all six slots; q = 8 does not fit, so the final update
+    falls back to stored f_hi) — bitwise the stage-by-stage kernels."""
+    import os
+
+    rng = np.random.default_rng(q)
+    ah = np.tril(rng.uniform(0.0, 0.2, (q, q)), -1)
+    ae = np.tril(rng.uniform(0.0, 0.05, (q, q)), -1) + np.diag(np.full(q, 0.5))
+    b = np.full(q, 1.0 / q)
+    t = mp.Tableau("custom", q, None, ah.tolist(), ae.tolist(), b.tolist())
+    n = 128
+    fused = mp.Stepper("heat", n, t, 0.01, 1e-4, "f32", 40)
+    os.environ["MPRKB_FUSED_STAGES"] = "0"
+    try:
+        plain = mp.Stepper("heat", n, t, 0.01, 1e-4, "f32", 40)
+    finally:
+        os.environ.pop("MPRKB_FUSED_STAGES", None)
+    u0 = mp.heat_exact(n, 0.05)
+    a, c = u0.copy(), u0.copy()
+    for _ in range(2):
+        assert fused.step(a)["iterations"] == plain.step(c)["iterations"]
+    assert same_bits(a, c)
