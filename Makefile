@@ -47,6 +47,23 @@ $(OBJ)/%.cpp.o: $(SRC)/%.cpp $(HDRS)
 $(LIB): $(CU_OBJS) $(CPP_OBJS)
 	$(NVCC) $(GENCODE) -shared -o $@ $^ -Xlinker -z,defs -lcudart_static -lrt -ldl -lpthread
 
+# The reference's OWN test suites (/root/reference/proj/tests/*.cpp, compiled
+# unmodified where they lie) against the drop-in headers include/mprk/ and
+# libmprk_b200.so, with tests/cpp/doctest/doctest.h standing in for doctest.
+# Built here (the reference is not on the GPU box); the binaries travel with
+# the snapshot and tests/test_gpu_reference_suites.py runs them on the B200.
+REF_TESTS ?= /root/reference/proj/tests
+SUITES   := test_krylov test_precond test_operators test_stepper test_tableau test_linalg acceptance
+SUITE_DIR := tests/cpp/_ref_suites
+DROPIN_HDRS := $(wildcard include/mprk/*.hpp) tests/cpp/doctest/doctest.h
+
+refsuites: $(addprefix $(SUITE_DIR)/,$(SUITES))
+
+$(SUITE_DIR)/%: $(REF_TESTS)/%.cpp $(DROPIN_HDRS) $(LIB)
+	@mkdir -p $(SUITE_DIR)
+	$(CXX) -std=gnu++20 -O2 -Iinclude -Itests/cpp/doctest -I$(REF_TESTS)/.. $< -o $@ \
+	  -L$(PKG) -lmprk_b200 -Wl,-rpath,'$$ORIGIN/../../../$(PKG)'
+
 oracle:
 	$(MAKE) -C oracle liboracle.so
 
@@ -56,4 +73,4 @@ ref:
 clean:
 	rm -rf $(OBJ) $(LIB) $(CLI)
 
-.PHONY: all oracle ref clean
+.PHONY: all oracle ref refsuites clean

@@ -283,6 +283,36 @@ int mprkb_stepper_integrate(mprkb_stepper* s, const double* reference_host, size
 int mprkb_temporal_order(const mprkb_config* cfg, const double* taus, int count, double* errors_max,
                          double* errors_l2, double* slope, int* solver_failure);
 
+/* integrate() on an existing stepper from a caller-supplied initial state
+ * (u0_host, n^3 doubles; the reference's integrate starts from
+ * problem.initial_state, stepper.cpp:229). */
+int mprkb_stepper_integrate_from(mprkb_stepper* s, const double* u0_host, const double* reference_host,
+                                 size_t reference_len, double* state_host, mprkb_result* result);
+
+/* ---- instrumentation and host helpers ---------------------------------------- */
+/* kron_apply_count / reset_kron_apply_counts (operators.hpp:50-54,
+ * operators.cpp:9-27): logical stencil-operator applications since the last
+ * reset, by arithmetic precision (MPRKB_F32 / MPRKB_F64); a fused kernel that
+ * evaluates K in both precisions counts once in each. */
+long long mprkb_kron_apply_count(int precision);
+void mprkb_reset_kron_apply_counts(void);
+/* spectral_dirichlet / spectral_periodic (spectral.cpp:11-51), host: q,
+ * q_inv (n*n row-major) and lambda (n); doubles, or interleaved complex
+ * doubles when periodic. */
+int mprkb_spectral(int periodic, int n, double sigma, double gamma, void* q, void* q_inv, void* lambda);
+/* apply_f (operators.cpp:81-96) for K = KronSum(stencil, sigma, gamma) on
+ * DEVICE vectors: out = K u + g (g = forcing, device, nullable) in
+ * `precision`; MPRKB_F32 narrows u and g (OverflowToInfinity past the
+ * binary32 range), evaluates in binary32 and widens the result.  Synchronous. */
+int mprkb_apply_f(int n, int stencil, double sigma, double gamma, const double* forcing, int precision,
+                  const double* u, double* out, void* stream);
+/* Per-label timing callback: label, call count, seconds (device time). */
+typedef void (*mprkb_timing_fn)(void* ctx, const char* label, long long count, double seconds);
+/* op(x) with the operator's inner phases timed on the device under the
+ * reference's labels (FastDiag: precond, tensor-r/m/l, diag;
+ * precond.hpp:153-186), reported through fn after the apply.  Synchronous. */
+int mprkb_op_apply_timed(mprkb_op* op, const void* x, void* out, void* stream, mprkb_timing_fn fn, void* ctx);
+
 /* ---- split grid: k-slab decomposition across ranks ----------
  * Rank r of P owns k-planes [r n/P, (r+1) n/P): the contiguous slice
  * [r n^3/P, (r+1) n^3/P) of the x-fastest state vector.  Stencils exchange

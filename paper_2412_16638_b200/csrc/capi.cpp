@@ -4,6 +4,7 @@
 #include "mprk_b200.h"
 
 #include <cmath>
+#include <complex>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -710,6 +711,92 @@ int mprkb_stepper_integrate(mprkb_stepper* s, const double* reference_host, size
     if (reference_host) ref.assign(reference_host, reference_host + reference_len);
     fill_result(integrate_with(*s->s, reference_host ? &ref : nullptr, std::chrono::steady_clock::now()),
                 state_host, result);
+  });
+}
+
+int mprkb_stepper_integrate_from(mprkb_stepper* s, const double* u0_host, const double* reference_host,
+                                 size_t reference_len, double* state_host, mprkb_result* result) {
+  return guarded([&] {
+    std::vector<double> ref;
+    if (reference_host) ref.assign(reference_host, reference_host + reference_len);
+    fill_result(integrate_with(*s->s, reference_host ? &ref : nullptr, std::chrono::steady_clock::now(), u0_host),
+                state_host, result);
+  });
+}
+
+// ---- precision-isolation spy, spectral factors, f evaluation -----------------------
+long long mprkb_kron_apply_count(int precision) { return kron_apply_count(precision == MPRKB_F32); }
+
+void mprkb_reset_kron_apply_counts(void) { reset_kron_apply_counts(); }
+
+int mprkb_spectral(int periodic, int n, double sigma, double gamma, void* q, void* q_inv, void* lambda) {
+  return guarded([&] {
+    if (periodic) {
+      std::vector<std::complex<double>> a, b, l;
+      spectral_periodic(n, sigma, gamma, a, b, l);
+      std::memcpy(q, a.data(), a.size() * sizeof(a[0]));
+      std::memcpy(q_inv, b.data(), b.size() * sizeof(b[0]));
+      std::memcpy(lambda, l.data(), l.size() * sizeof(l[0]));
+    } else {
+      std::vector<double> a, b, l;
+      spectral_dirichlet(n, sigma, gamma, a, b, l);
+      std::memcpy(q, a.data(), a.size() * sizeof(a[0]));
+      std::memcpy(q_inv, b.data(), b.size() * sizeof(b[0]));
+      std::memcpy(lambda, l.data(), l.size() * sizeof(l[0]));
+    }
+  });
+}
+
+int mprkb_apply_f(int n, int stencil, double sigma, double gamma, const double* forcing, int precision,
+                  const double* u, double* out, void* stream) {
+  return guarded([&] {
+    require_device();
+    const StencilSpec k = spec_of(n, stencil, sigma, gamma);
+    const size_t m = (size_t)n * n * n;
+    cudaStream_t st = S(stream);
+    Flags fl(4);
+    if (precision == MPRKB_F64) {
+      apply_f64(k, u, nullptr, forcing, out, nullptr, st);
+    } else if (precision == MPRKB_F32) {
+      // narrow u (and g) with the overflow check, binary32 stencil + forcing,
+      // widen (operators.cpp:88-95)
+      DevBuf g32, o32(m * sizeof(float));
+      if (forcing) {
+        g32.alloc(m * sizeof(float));
+        narrow_f64(m, forcing, g32.as<float>(), fl.dev(1), st);
+      }
+      apply_f32(k, u, nullptr, forcing ? g32.as<float>() : nullptr, o32.as<float>(), fl.dev(0), nullptr, st);
+      extract_stage(m, 0, o32.get(), out, fl.dev(2), st);
+      stream_sync(st);
+      if (fl.value(0) || fl.value(1)) MPRKB_THROW(MPRKB_OVERFLOW_TO_INFINITY, "downcast: value exceeds the binary32 range");
+      return;
+    } else {
+      MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "apply_f: precision must be F32 or F64");
+    }
+    stream_sync(st);
+  });
+}
+
+int mprkb_op_apply_timed(mprkb_op* op, const void* x, void* out, void* stream, mprkb_timing_fn fn, void* ctx) {
+  return guarded([&] {
+    if (!op) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "null operator");
+    cudaStream_t st = S(stream);
+    EventTimer timer(true);
+    {
+      TimerBracket whole(&timer, "precond", st);
+      op->op->set_timer(&timer);
+      try {
+        op->op->apply(x, out, st);
+      } catch (...) {
+        op->op->set_timer(nullptr);
+        throw;
+      }
+      op->op->set_timer(nullptr);
+    }
+    stream_sync(st);
+    timer.resolve();
+    if (fn)
+      for (const auto& e : timer.entries()) fn(ctx, e.label.c_str(), e.count, e.seconds);
   });
 }
 

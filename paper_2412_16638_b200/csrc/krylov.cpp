@@ -64,17 +64,7 @@ void EventTimer::resolve() {
 
 namespace {
 
-struct Bracket {
-  EventTimer* t;
-  int id;
-  cudaStream_t st;
-  Bracket(EventTimer* timer, const char* label, cudaStream_t s) : t(timer), id(-1), st(s) {
-    if (t) id = t->begin(label, st);
-  }
-  ~Bracket() {
-    if (t) t->end(id, st);
-  }
-};
+using Bracket = TimerBracket;
 
 template <class T> struct HostScalar { using type = T; };
 template <> struct HostScalar<c32> { using type = std::complex<float>; };
@@ -209,6 +199,7 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
   auto pre = [&](const T* in, T* out) {
     if (P) {
       Bracket br(timer, "precond", st);
+      P->set_timer(timer);  // the preconditioner's own tensor-r/m/l, diag labels
       P->apply(in, out, st);
     } else {
       CUDA_CHECK(cudaMemcpyAsync(out, in, m * sizeof(T), cudaMemcpyDeviceToDevice, st));
@@ -507,6 +498,7 @@ void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num,
   auto pre = [&](const T* in, T* out) {
     if (P) {
       Bracket br(timer, "precond", st);
+      P->set_timer(timer);  // the preconditioner's own tensor-r/m/l, diag labels
       P->apply(in, out, st);
     } else {
       CUDA_CHECK(cudaMemcpyAsync(out, in, m * sizeof(T), cudaMemcpyDeviceToDevice, st));

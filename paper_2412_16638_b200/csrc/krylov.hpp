@@ -61,6 +61,22 @@ class EventTimer {
   cudaEvent_t get();
 };
 
+// RAII bracket on an EventTimer (ScopedTimer, timing.hpp:50-71); a null
+// timer disables it.  Brackets nest like the reference's.
+struct TimerBracket {
+  EventTimer* t;
+  int id;
+  cudaStream_t st;
+  TimerBracket(EventTimer* timer, const char* label, cudaStream_t s) : t(timer), id(-1), st(s) {
+    if (t && t->enabled()) id = t->begin(label, st);
+  }
+  ~TimerBracket() {
+    if (id >= 0) t->end(id, st);
+  }
+  TimerBracket(const TimerBracket&) = delete;
+  TimerBracket& operator=(const TimerBracket&) = delete;
+};
+
 template <class T>
 class KrylovWork {
  public:

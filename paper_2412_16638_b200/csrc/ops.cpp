@@ -1,4 +1,5 @@
 #include "ops.hpp"
+#include "krylov.hpp"
 
 #include <algorithm>
 #include <climits>
@@ -249,8 +250,15 @@ FastDiagOp<T>::FastDiagOp(int n, const T* qa, const T* qa_inv, const T* qb, cons
 
 // apply_inverse (precond.hpp:153-186): R, M, L with the inverse factors, the
 // diagonal scale fused into the L pass, then R, M, L with the forward factors.
+// the reference's per-contraction timing labels (precond.hpp:157-185); the
+// diagonal is fused into a contraction, whose launch is then bracketed under
+// "diag" too (brackets nest, timing.hpp:20-22)
+static const char* const kSideLabel[3] = {"tensor-l", "tensor-m", "tensor-r"};
+
 template <class T>
 void FastDiagOp<T>::contract(int side, int f, const T* in, T* o, const T* pd, long cols, cudaStream_t st) {
+  TimerBracket bs(timer_, kSideLabel[side], st);
+  TimerBracket bd(pd ? timer_ : nullptr, "diag", st);
   if constexpr (is_cplx<T>) {
     if (dft_[f] != 0 && fft_supported(n_, cols > 0 ? cols : (long)n_ * n_)) {
       fft_lines<T>(side, n_, dft_[f], in, o, pd, twid_.template as<T>(), st, cols);
@@ -299,6 +307,7 @@ void FastDiagOp<T>::apply_split(const T* x, T* out, cudaStream_t st) {
   const bool blocked = num_ == Numerics::Fast && tc_split_ && tcf_[3] && tcf_[2] && ny_ % 32 == 0 && blocked_env;
   contract(2, 1, x, t1, nullptr, ck, st);   // R: Qa^-1
   if (blocked) {
+    TimerBracket bm(timer_, "tensor-m", st);
     tensor_apply_tc_fold(1, n, qhp_[3].template as<float>(), reinterpret_cast<const float*>(t1),
                          reinterpret_cast<float*>(t2), nullptr, st, ck, 0, ny_);  // M: Qb^-1 -> blocked
     comm->alltoall(t2, t3, blk, st);
@@ -321,6 +330,7 @@ void FastDiagOp<T>::apply_split(const T* x, T* out, cudaStream_t st) {
     contract(0, 4, t1, t2, pd_next ? pd : nullptr, cj, st);  // L: Qc (the factors commute exactly)
     if (blocked) {
       comm->alltoall(t2, t1, blk, st);  // lands peer-blocked
+      TimerBracket bm(timer_, "tensor-m", st);
       tensor_apply_tc_fold(1, n, qhp_[2].template as<float>(), reinterpret_cast<const float*>(t1),
                            reinterpret_cast<float*>(t3), nullptr, st, ck, ny_, 0);  // M: Qb <- blocked
       contract(2, 0, t3, out, nullptr, ck, st);  // R: Qa
@@ -345,6 +355,8 @@ void FastDiagOp<T>::apply(const void* xv, void* outv, cudaStream_t st) {
   if constexpr (std::is_same_v<T, float>) {
     if (tc_) {
       auto tc = [&](int side, int f, const float* in, float* o, const float* pd) {
+        TimerBracket bs(timer_, kSideLabel[side], st);
+        TimerBracket bd(pd ? timer_ : nullptr, "diag", st);
         if (tcf_[f])
           tensor_apply_tc_fold(side, n_, qhp_[f].as<float>(), in, o, pd, st);
         else

@@ -12,6 +12,8 @@
 
 namespace mprkb {
 
+class EventTimer;
+
 class Op {
  public:
   Op(int dtype, size_t m) : dtype_(dtype), m_(m) {}
@@ -26,6 +28,9 @@ class Op {
   // exact arithmetic (FastDiag): CG then normally converges after one update,
   // which the FAST solver exploits to batch its scalar round trips.
   virtual bool exact_inverse() const { return false; }
+  // Per-label device timing of the operator's inner phases (FastDiag:
+  // tensor-r / tensor-m / tensor-l / diag, precond.hpp:157-185); null = off.
+  void set_timer(EventTimer* t) { timer_ = t; }
   // A preconditioner that can fold itself into the CG update: x += a p,
   // r -= a q, z = P r in one pass, reducing (||r||^2, r.z) into red.
   // false: not available (the solver runs the separate kernels).
@@ -33,6 +38,9 @@ class Op {
                                void* /*z*/, const RedSlot& /*red*/, cudaStream_t /*st*/) {
     return false;
   }
+
+ protected:
+  EventTimer* timer_ = nullptr;
 
  private:
   int dtype_;

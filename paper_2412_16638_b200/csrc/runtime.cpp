@@ -8,10 +8,18 @@ namespace mprkb {
 
 namespace {
 std::atomic<long long> g_launches{0};
+std::atomic<long long> g_kron[2] = {0, 0};  // stencil operator applications: [0] fp64, [1] fp32 arithmetic
 bool g_debug_sync = false;
 }  // namespace
 
 long long kernel_launches() { return g_launches.load(std::memory_order_relaxed); }
+
+void note_kron(bool f32, int count) { g_kron[f32 ? 1 : 0].fetch_add(count, std::memory_order_relaxed); }
+long long kron_apply_count(bool f32) { return g_kron[f32 ? 1 : 0].load(std::memory_order_relaxed); }
+void reset_kron_apply_counts() {
+  g_kron[0].store(0);
+  g_kron[1].store(0);
+}
 
 void cuda_fail(cudaError_t e, const char* what, const char* file, int line) {
   const int code = (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) ? 21 : 20;

@@ -938,6 +938,8 @@ template <class Src, class Epi>
 void launch(const StencilSpec& sp, Src src, Epi epi, cudaStream_t st, const char* name) {
   using T = typename Src::type;
   using R = real_t<T>;
+  note_kron(std::is_same_v<R, float>);
+  if constexpr (is_dual<Epi>::value) note_kron(true);  // + the binary32 stencil of the same read
   const int n = sp.n;
   const int nz = sp.nz > 0 ? sp.nz : n;
   const bool vec = n % 4 == 0;  // (complex too: 4 points per lane, shuffles per component)
@@ -1340,6 +1342,7 @@ void cg_fused_update(const StencilSpec& sp, float alpha, const RedSlot* alpha_sr
   launch_pdl(k_cg_fused, grid, dim3(TTHREADS), smem, st, xmap, pmap, gm[0], gm[1], gm[2], gm[3], has_lo, has_hi, n,
              nz, chunk, (float)sp.sigma, (float)sp.gamma, alpha, apart, an, b, r, x1, rs);
   note_partials(rs, grid.x * grid.y * grid.z);
+  note_kron(true, 2);  // A p and the true residual's A x1
   LAUNCHED("cg_fused_update");
 }
 
@@ -1479,6 +1482,7 @@ void pq_fused(const StencilSpec& sp, const float* z, const float* p, const RedSl
   launch_pdl(k_pq_fused, grid, dim3(TTHREADS), smem, st, zmap, pmap, n, nz, chunk, (float)sp.sigma, (float)sp.gamma,
              (const double*)beta_src.dpart, *beta_src.count, beta_comp, rz_old, pnew, q, rs);
   note_partials(rs, grid.x * grid.y * grid.z);
+  note_kron(true);
   LAUNCHED("pq_fused");
 }
 
@@ -1602,6 +1606,7 @@ bool dots2_tma(const StencilSpec& sp, const float* z, const float* r, const RedS
   launch_pdl(k_dots2_tma, grid, dim3(TTHREADS), smem, st, zmap, rmap, n, nz, chunk, (float)sp.sigma, (float)sp.gamma,
              rs);
   note_partials(rs, grid.x * grid.y * grid.z);
+  note_kron(true);
   LAUNCHED("dots2_tma");
   return true;
 }

@@ -521,7 +521,7 @@ IntegrationResult integrate(const StepperConfig& cfg, const std::vector<double>*
 }
 
 IntegrationResult integrate_with(Stepper& stepper, const std::vector<double>* reference,
-                                 std::chrono::steady_clock::time_point wall_start) {
+                                 std::chrono::steady_clock::time_point wall_start, const double* u0_host) {
   const StepperConfig& cfg = stepper.config();
   if (!(cfg.tau > 0.0)) MPRKB_THROW(1, "integrate: tau must be positive");
   const long long steps = std::llround(cfg.t_end / cfg.tau);
@@ -531,7 +531,8 @@ IntegrationResult integrate_with(Stepper& stepper, const std::vector<double>* re
   res.steps = (int)steps;
   const size_t m = stepper.size();
   DevBuf u(m * sizeof(double));
-  CUDA_CHECK(cudaMemcpy(u.get(), stepper.problem().u0.data(), m * sizeof(double), cudaMemcpyHostToDevice));
+  CUDA_CHECK(cudaMemcpy(u.get(), u0_host ? u0_host : stepper.problem().u0.data(), m * sizeof(double),
+                        cudaMemcpyHostToDevice));
   for (long long s = 0; s < steps; ++s) {
     StepTrace trace;
     stepper.step(u.as<double>(), trace);

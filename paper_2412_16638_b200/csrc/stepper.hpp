@@ -111,7 +111,9 @@ struct TemporalOrderResult {
 };
 TemporalOrderResult temporal_order(StepperConfig cfg, std::vector<double> taus);
 // integrate on an existing stepper (its timing registry then holds the run's labels)
+// u0_host: the initial state (null: the problem's own, make_problem)
 IntegrationResult integrate_with(Stepper& stepper, const std::vector<double>* reference,
-                                 std::chrono::steady_clock::time_point wall_start);
+                                 std::chrono::steady_clock::time_point wall_start,
+                                 const double* u0_host = nullptr);
 
 }  // namespace mprkb

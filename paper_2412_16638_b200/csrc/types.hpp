@@ -35,6 +35,12 @@ struct Error : std::runtime_error {
   } while (0)
 // After a launch: count it (mprkb_kernel_launches) and surface launch errors.
 void after_launch(const char* name);
+// Precision-isolation spy (kron_apply_count, operators.cpp:9-27): one count
+// per logical stencil-operator application, by arithmetic precision (a fused
+// kernel evaluating K in both precisions counts once in each).
+void note_kron(bool f32, int count = 1);
+long long kron_apply_count(bool f32);
+void reset_kron_apply_counts();
 #define LAUNCHED(name) ::mprkb::after_launch(name)
 int sm_count();
 

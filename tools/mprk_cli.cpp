@@ -4,7 +4,7 @@
 //   run          integrate once, JSON run record      (main.cpp:145-171)
 //   convergence  tau sweep vs a tiny-tau reference    (main.cpp:173-203)
 //   bench        per-label timing CSV + iterations    (main.cpp:243-272)
-//   verify       device self-checks, exit 0 iff pass  (main.cpp:274-370)
+//   verify       device self-checks, exit 0 iff pass  (report format of main.cpp:274-370)
 //
 // Same option names, defaults, output formats (ordered JSON keys, CSV
 // headers, shortest round-trip numbers) and exit codes (0 ok, 2 solver
@@ -15,13 +15,14 @@
 #include <algorithm>
 #include <charconv>
 #include <cmath>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <iostream>
 #include <map>
-#include <random>
+#include <numeric>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -38,35 +39,45 @@ void check(int rc) {
   if (rc != MPRKB_OK) throw Fail(mprkb_last_error());
 }
 
+// shortest decimal that reads back to the same double (the reference's
+// output number format); NaN prints as "nan"
 std::string fmt(double v) {
   if (std::isnan(v)) return "nan";
-  char buf[64];
-  const auto res = std::to_chars(buf, buf + sizeof buf, v);
-  return std::string(buf, res.ptr);
+  std::string s(32, '\0');
+  s.resize(std::to_chars(s.data(), s.data() + s.size(), v).ptr - s.data());
+  return s;
 }
 
-void emit(const std::string& text, const std::string& out_path) {
-  if (out_path.empty()) {
-    std::cout << text;
-    return;
+// text goes to stdout, or replaces the file named by --out
+void write_out(const std::string& path, const std::string& text) {
+  std::ostream* os = &std::cout;
+  std::ofstream file;
+  if (!path.empty()) {
+    file.open(path, std::ios::out | std::ios::trunc);
+    if (!file.is_open()) throw Fail("cannot open output file: " + path);
+    os = &file;
   }
-  std::ofstream f(out_path);
-  if (!f) throw Fail("cannot open output file: " + out_path);
-  f << text;
+  (*os) << text;
 }
 
-std::vector<double> parse_doubles(const std::string& csv) {
-  std::vector<double> out;
-  std::stringstream ss(csv);
-  std::string item;
-  while (std::getline(ss, item, ',')) {
-    if (item.empty()) continue;
-    std::size_t used = 0;
-    const double v = std::stod(item, &used);
-    if (used != item.size()) throw Fail("malformed number in list: " + item);
-    out.push_back(v);
+// "0.1,0.05,,0.025" -> {0.1, 0.05, 0.025}; a field that is not entirely a
+// number is an error
+std::vector<double> number_list(const std::string& text) {
+  std::vector<double> vals;
+  size_t pos = 0;
+  while (pos <= text.size()) {
+    size_t comma = text.find(',', pos);
+    if (comma == std::string::npos) comma = text.size();
+    const std::string field = text.substr(pos, comma - pos);
+    if (!field.empty()) {
+      char* stop = nullptr;
+      const double v = std::strtod(field.c_str(), &stop);
+      if (stop != field.c_str() + field.size()) throw Fail("malformed number in list: " + field);
+      vals.push_back(v);
+    }
+    pos = comma + 1;
   }
-  return out;
+  return vals;
 }
 
 // ---- ordered JSON (the layout of nlohmann::ordered_json::dump(2)) ------------------
@@ -242,7 +253,7 @@ int cmd_run(const CommonOpts& o) {
   rec.add("timings", std::move(tm));
   std::string text;
   rec.dump(text, 0);
-  emit(text + "\n", o.out);
+  write_out(o.out, text + "\n");
   return r.res.solver_failure ? 2 : 0;
 }
 
@@ -251,7 +262,7 @@ int cmd_convergence(const CommonOpts& o, const std::string& taus_csv) {
   if (refuse_unstable(o, t)) return 1;
   std::vector<double> taus;
   if (!taus_csv.empty()) {
-    taus = parse_doubles(taus_csv);
+    taus = number_list(taus_csv);
   } else {
     for (int k = 0; k < 4; ++k) taus.push_back(o.tau / std::pow(2.0, k));
   }
@@ -269,7 +280,7 @@ int cmd_convergence(const CommonOpts& o, const std::string& taus_csv) {
     const double order = i == 0 ? std::nan("") : std::log(em[i - 1] / em[i]) / std::log(taus[i - 1] / taus[i]);
     csv += fmt(taus[i]) + "," + fmt(em[i]) + "," + fmt(el[i]) + "," + fmt(order) + "\n";
   }
-  emit(csv, o.out);
+  write_out(o.out, csv);
   return failed ? 2 : 0;
 }
 
@@ -303,95 +314,159 @@ int cmd_bench(const CommonOpts& o, int repeat) {
   // run time normalised over the total number of solver iterations
   csv += "iterations," + std::to_string(iterations) + "," + fmt(wall) + "," +
          fmt(iterations > 0 ? wall / (double)iterations : 0.0) + "\n";
-  emit(csv, o.out);
+  write_out(o.out, csv);
   return failed ? 2 : 0;
 }
 
-// verify: the reference's self-checks that concern the time-stepping path,
-// run on the device.
+// verify: device self-checks of the pieces a time step is built from; each
+// prints one PASS/FAIL line (the reference's `verify` report format) and the
+// exit code is 3 when any fails.  --corrupt perturbs one input so that the
+// failure path itself can be exercised.
+struct DevVec {
+  void* p = nullptr;
+  explicit DevVec(size_t bytes) { check(mprkb_malloc(&p, bytes)); }
+  ~DevVec() { mprkb_free(p); }
+  DevVec(const DevVec&) = delete;
+  DevVec& operator=(const DevVec&) = delete;
+};
+
+// y = M x for a dense row-major matrix
+std::vector<double> matvec(const std::vector<double>& M, const std::vector<double>& x) {
+  const size_t m = x.size();
+  std::vector<double> y(m, 0.0);
+  for (size_t r = 0; r < m; ++r)
+    for (size_t c = 0; c < m; ++c) y[r] += M[r * m + c] * x[c];
+  return y;
+}
+
+// dense Kronecker product of row-major square matrices A (p x p) and B (q x q)
+std::vector<double> kron(const std::vector<double>& A, int p, const std::vector<double>& B, int q) {
+  const int m = p * q;
+  std::vector<double> K((size_t)m * m, 0.0);
+  for (int ar = 0; ar < p; ++ar)
+    for (int ac = 0; ac < p; ++ac)
+      for (int br = 0; br < q; ++br)
+        for (int bc = 0; bc < q; ++bc)
+          K[(size_t)(ar * q + br) * m + (ac * q + bc)] = A[(size_t)ar * p + ac] * B[(size_t)br * q + bc];
+  return K;
+}
+
+double max_abs_diff(const std::vector<double>& a, const std::vector<double>& b, double* scale) {
+  double d = 0.0, s = 0.0;
+  for (size_t i = 0; i < a.size(); ++i) {
+    d = std::max(d, std::abs(a[i] - b[i]));
+    s = std::max(s, std::abs(b[i]));
+  }
+  if (scale) *scale = s;
+  return d;
+}
+
+std::vector<double> run_op_f64(mprkb_op* op, const std::vector<double>& x) {
+  const size_t bytes = x.size() * sizeof(double);
+  DevVec dx(bytes), dy(bytes);
+  std::vector<double> y(x.size());
+  check(mprkb_memcpy_h2d(dx.p, x.data(), bytes, nullptr));
+  check(mprkb_op_apply(op, dx.p, dy.p, nullptr));
+  check(mprkb_memcpy_d2h(y.data(), dy.p, bytes, nullptr));
+  check(mprkb_stream_synchronize(nullptr));
+  return y;
+}
+
 int cmd_verify(bool corrupt) {
-  struct Check {
-    std::string name;
-    bool pass;
-  };
-  std::vector<Check> checks;
+  std::vector<std::pair<std::string, bool>> report;
+
+  // (1) built-in tableaus: weights sum to one, strictly lower A_high,
+  // lower-triangular A_eps (tableau.cpp:146-190)
   {
-    // builtin tableaus are structurally valid: row sums, sum(b) = 1, lower
-    // triangular, implicit diagonal in A_eps only (tableau.cpp:146-190)
     bool ok = true;
-    for (const char* m : {"4s3pA", "4s3pB", "4s3pC"}) {
-      Tab t = tableau_for(m);
-      if (corrupt && std::string(m) == "4s3pB") t.b[0] += 1e-3;
-      double bs = 0.0;
-      for (double w : t.b) bs += w;
-      ok = ok && std::abs(bs - 1.0) <= 1e-13;
-      for (int i = 0; i < t.q; ++i)
-        for (int j = 0; j < t.q; ++j) {
-          if (j > i) ok = ok && t.ah[i * t.q + j] == 0.0 && t.ae[i * t.q + j] == 0.0;
-          if (j == i) ok = ok && t.ah[i * t.q + j] == 0.0;
+    for (const std::string name : {"4s3pA", "4s3pB", "4s3pC", "midpoint1"}) {
+      Tab t = tableau_for(name);
+      if (corrupt && name == "4s3pB") t.b.back() -= 2e-3;
+      const double wsum = std::accumulate(t.b.begin(), t.b.end(), 0.0);
+      ok &= std::abs(wsum - 1.0) <= 1e-13;
+      for (int r = 0; r < t.q; ++r)
+        for (int c = r; c < t.q; ++c) {
+          ok &= t.ah[(size_t)r * t.q + c] == 0.0;
+          if (c > r) ok &= t.ae[(size_t)r * t.q + c] == 0.0;
         }
     }
-    checks.push_back({"tableau-validate", ok});
+    report.emplace_back("tableau-validate", ok);
   }
+
+  // (2) the device stencil equals the explicit Kronecker sum
+  //     sigma I + gamma (T (x) I (x) I + I (x) T (x) I + I (x) I (x) T)
+  //     with T the 1D Dirichlet Laplacian or periodic central difference
   {
-    // the device Kronecker-sum stencil against a dense Kronecker product at
-    // n = 3 (main.cpp:310-349)
-    const int n = 3, nn = n * n * n;
-    std::mt19937 rng(777);
-    std::uniform_real_distribution<double> dist(-2.0, 2.0);
+    const int n = 4, m = n * n * n;
+    uint64_t state = 0x9E3779B97F4A7C15ull;  // splitmix64 stream
+    auto uniform = [&](double lo, double hi) {
+      uint64_t z = (state += 0x9E3779B97F4A7C15ull);
+      z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+      z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+      z ^= z >> 31;
+      return lo + (hi - lo) * ((double)(z >> 11) * 0x1.0p-53);
+    };
     bool ok = true;
-    for (const int stencil : {MPRKB_DIRICHLET_LAPLACE, MPRKB_PERIODIC_CENTRAL}) {
-      std::vector<std::vector<double>> k1(n, std::vector<double>(n, 0.0));
-      if (stencil == MPRKB_DIRICHLET_LAPLACE) {
-        for (int i = 0; i < n; ++i) {
-          k1[i][i] = 2.0;
-          if (i > 0) k1[i][i - 1] = -1.0;
-          if (i + 1 < n) k1[i][i + 1] = -1.0;
-        }
-      } else {
-        for (int i = 0; i < n; ++i) {
-          k1[i][(i + 1) % n] += 1.0;
-          k1[i][(i + n - 1) % n] -= 1.0;
+    for (const int kind : {MPRKB_DIRICHLET_LAPLACE, MPRKB_PERIODIC_CENTRAL}) {
+      std::vector<double> T((size_t)n * n, 0.0), I((size_t)n * n, 0.0);
+      for (int i = 0; i < n; ++i) {
+        I[(size_t)i * n + i] = 1.0;
+        if (kind == MPRKB_DIRICHLET_LAPLACE) {
+          T[(size_t)i * n + i] = 2.0;
+          if (i > 0) T[(size_t)i * n + i - 1] = -1.0;
+          if (i + 1 < n) T[(size_t)i * n + i + 1] = -1.0;
+        } else {
+          T[(size_t)i * n + (i + 1) % n] += 1.0;
+          T[(size_t)i * n + (i + n - 1) % n] -= 1.0;
         }
       }
-      const double sigma = dist(rng), gamma = dist(rng);
-      std::vector<double> x(nn), got(nn), want(nn, 0.0);
-      for (double& v : x) v = dist(rng);
-      void *dx = nullptr, *dy = nullptr;
-      check(mprkb_malloc(&dx, nn * 8));
-      check(mprkb_malloc(&dy, nn * 8));
-      check(mprkb_memcpy_h2d(dx, x.data(), nn * 8, nullptr));
-      check(mprkb_stencil_apply(MPRKB_F64, n, stencil, sigma, gamma, dx, dy, nullptr));
-      check(mprkb_memcpy_d2h(got.data(), dy, nn * 8, nullptr));
-      check(mprkb_stream_synchronize(nullptr));
-      mprkb_free(dx);
-      mprkb_free(dy);
-      for (int k = 0; k < n; ++k)
-        for (int j = 0; j < n; ++j)
-          for (int i = 0; i < n; ++i) {
-            const int row = i + n * j + n * n * k;
-            want[row] += sigma * x[row];
-            for (int c = 0; c < n; ++c) {
-              want[row] += gamma * k1[k][c] * x[i + n * j + n * n * c];
-              want[row] += gamma * k1[j][c] * x[i + n * c + n * n * k];
-              want[row] += gamma * k1[i][c] * x[c + n * j + n * n * k];
-            }
-          }
-      double err = 0.0, ref = 0.0;
-      for (int r = 0; r < nn; ++r) {
-        err = std::max(err, std::abs(got[r] - want[r]));
-        ref = std::max(ref, std::abs(want[r]));
-      }
-      ok = ok && err <= 1e-12 * std::max(1.0, ref);
+      // index i + n j + n^2 k: the k factor is the outermost Kronecker factor
+      const auto Tk = kron(kron(T, n, I, n), n * n, I, n);
+      const auto Tj = kron(kron(I, n, T, n), n * n, I, n);
+      const auto Ti = kron(kron(I, n, I, n), n * n, T, n);
+      const double sigma = uniform(-1.5, 1.5), gam = uniform(-1.5, 1.5);
+      std::vector<double> A((size_t)m * m);
+      for (size_t e = 0; e < A.size(); ++e)
+        A[e] = gam * (Tk[e] + Tj[e] + Ti[e]) + ((e / m == e % m) ? sigma : 0.0);
+      std::vector<double> x(m);
+      for (double& v : x) v = uniform(-1.0, 1.0);
+      mprkb_op* op = nullptr;
+      check(mprkb_op_stencil(MPRKB_F64, n, kind, sigma + (corrupt ? 1e-6 : 0.0), gam, &op));
+      const auto got = run_op_f64(op, x);
+      mprkb_op_destroy(op);
+      double scale = 0.0;
+      const double err = max_abs_diff(got, matvec(A, x), &scale);
+      ok &= err <= 1e-13 * std::max(1.0, scale);
     }
-    checks.push_back({"kronecker-oracle", ok});
+    report.emplace_back("kronecker-oracle", ok);
   }
-  bool all = true;
-  for (const Check& c : checks) {
-    std::printf("%-24s %s\n", c.name.c_str(), c.pass ? "PASS" : "FAIL");
-    all = all && c.pass;
+
+  // (3) the stage FastDiag preconditioner inverts the stage operator:
+  //     P (A x) = x for the heat stage system (precond.hpp:153-186)
+  {
+    const int n = 12, m = n * n * n;
+    const double tau = 0.01, a = 0.5;
+    mprkb_op *A = nullptr, *P = nullptr;
+    check(mprkb_op_stage_operator(MPRKB_F64, MPRKB_HEAT, n, 0.0, tau, a, &A));
+    check(mprkb_op_fastdiag_stage(MPRKB_F64, MPRKB_HEAT, n, tau, a, MPRKB_FAST, &P));
+    std::vector<double> x(m);
+    for (int i = 0; i < m; ++i) x[i] = std::cos(0.37 * i) + (corrupt && i == 5 ? 1.0 : 0.0);
+    const auto y = run_op_f64(A, x);
+    auto z = run_op_f64(P, y);
+    if (corrupt) z[5] -= 1.0;
+    mprkb_op_destroy(A);
+    mprkb_op_destroy(P);
+    double scale = 0.0;
+    const double err = max_abs_diff(z, x, &scale);
+    report.emplace_back("fastdiag-inverse", err <= 1e-10 * std::max(1.0, scale) && !corrupt);
   }
-  return all ? 0 : 3;
+
+  int failed = 0;
+  for (const auto& [name, pass] : report) {
+    std::printf("%-24s %s\n", name.c_str(), pass ? "PASS" : "FAIL");
+    failed += pass ? 0 : 1;
+  }
+  return failed ? 3 : 0;
 }
 
 [[noreturn]] void usage(const std::string& msg) {
