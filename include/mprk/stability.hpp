@@ -2,9 +2,7 @@
 // (/root/reference/proj/include/mprk/stability.hpp:10-41).  Off the B200 hot
 // path: provided host-only so that reference callers that also
 // use them (e.g. the reference's acceptance gate) still compile against the
-// drop-in.  R(z) = 1 + z b^T (I - zA)^{-1} e; A = A_high + A_eps is lower
-// triangular for every tableau validate() accepts, so (I - zA) y = e is a
-// forward substitution, carried out in extended precision.
+// drop-in.
 #pragma once
 
 #include <cmath>
@@ -21,26 +19,47 @@ namespace mprk {
 
 enum class FloatFormat { Binary16, Binary32 };
 
+// R(z) = 1 + z b^T w with (I - zA) w = e solved by Gaussian elimination with
+// partial pivoting in extended precision (the reference's dense solve, so the
+// |R| = 1 boundary falls on the same lattice cells).
 inline std::complex<double> stability_function(const ButcherTableau& t, std::complex<double> z) {
   using cl = std::complex<long double>;
   const int q = t.q;
   const cl zl(z.real(), z.imag());
-  long double scale = 1.0L;
-  for (int i = 0; i < q; ++i)
-    for (int j = 0; j < q; ++j) scale = std::max(scale, std::abs(zl * (long double)(t.a_high[i][j] + t.a_eps[i][j])));
-  std::vector<cl> y(q);
-  for (int i = 0; i < q; ++i) {
-    cl rhs(1.0L, 0.0L);
-    for (int j = 0; j < i; ++j) rhs += zl * (long double)(t.a_high[i][j] + t.a_eps[i][j]) * y[j];
-    const cl d = cl(1.0L, 0.0L) - zl * (long double)(t.a_high[i][i] + t.a_eps[i][i]);
-    if (std::abs(d) <= scale * q * std::numeric_limits<double>::epsilon())
-      throw SingularSystem("stability_function: I - zA is singular");
-    y[i] = rhs / d;
+  std::vector<cl> M((std::size_t)q * q), w(q, cl(1.0L));
+  for (int r = 0; r < q; ++r)
+    for (int c = 0; c < q; ++c)
+      M[(std::size_t)r * q + c] =
+          (r == c ? cl(1.0L) : cl()) - zl * ((long double)t.a_high[r][c] + (long double)t.a_eps[r][c]);
+  long double big = 0.0L;
+  for (const cl& v : M) big = std::max(big, std::abs(v));
+  const long double tiny = big * q * std::numeric_limits<double>::epsilon();
+  auto at = [&](int r, int c) -> cl& { return M[(std::size_t)r * q + c]; };
+  for (int k = 0; k < q; ++k) {
+    int p = k;
+    for (int r = k + 1; r < q; ++r)
+      if (std::abs(at(r, k)) > std::abs(at(p, k))) p = r;
+    if (std::abs(at(p, k)) <= tiny) throw SingularSystem("stability_function: I - zA is singular");
+    if (p != k) {
+      for (int c = 0; c < q; ++c) std::swap(at(k, c), at(p, c));
+      std::swap(w[k], w[p]);
+    }
+    for (int r = k + 1; r < q; ++r) {
+      const cl f = at(r, k) / at(k, k);
+      if (f == cl()) continue;
+      for (int c = k; c < q; ++c) at(r, c) -= f * at(k, c);
+      w[r] -= f * w[k];
+    }
   }
-  cl acc(0.0L, 0.0L);
-  for (int i = 0; i < q; ++i) acc += (long double)t.b[i] * y[i];
-  const cl r = cl(1.0L, 0.0L) + zl * acc;
-  return {(double)r.real(), (double)r.imag()};
+  for (int r = q - 1; r >= 0; --r) {
+    cl s = w[r];
+    for (int c = r + 1; c < q; ++c) s -= at(r, c) * w[c];
+    w[r] = s / at(r, r);
+  }
+  cl acc;
+  for (int i = 0; i < q; ++i) acc += (long double)t.b[i] * w[i];
+  const cl R = cl(1.0L) + zl * acc;
+  return {(double)R.real(), (double)R.imag()};
 }
 
 inline std::complex<double> corrected_midpoint_reference(std::complex<double> z) {
@@ -53,6 +72,7 @@ inline ButcherTableau truncate_eps(const ButcherTableau& t, FloatFormat fmt) {
   for (auto& row : o.a_eps)
     for (double& v : row) v = fmt == FloatFormat::Binary16 ? round_binary16(v) : round_binary32(v);
   o.c = b200::row_sums(o.a_high, o.a_eps);
+  o.name += fmt == FloatFormat::Binary16 ? "+b16" : "+b32";
   return o;
 }
 
@@ -81,6 +101,7 @@ inline StabilityGrid region_scan(const ButcherTableau& t, double re_min, double 
       double v;
       try {
         v = std::abs(stability_function(t, {g.re_at(ix), g.im_at(iy)}));
+        if (std::isnan(v)) v = std::numeric_limits<double>::infinity();
       } catch (const SingularSystem&) {
         v = std::numeric_limits<double>::infinity();
       }

@@ -415,15 +415,18 @@ __device__ __forceinline__ uint64_t kmajor_desc16(const void* p) {
   d |= (uint64_t)1 << 46;
   return d;
 }
+// instruction descriptors: M = 128, N = 128 (full tile) / N = 64 (half tile)
 constexpr uint32_t kIdescF = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TF_BN >> 3) << 17) |
                              ((uint32_t)(TF_BM >> 4) << 24);
+constexpr uint32_t kIdescF64 = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)((TF_BN / 2) >> 3) << 17) |
+                               ((uint32_t)(TF_BM >> 4) << 24);
 
-__device__ __forceinline__ void mma_tf32f(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc) {
+__device__ __forceinline__ void mma_tf32f(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t acc, uint32_t idesc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(kIdescF), "r"(acc), "r"(0u), "r"(0u), "r"(0u), "r"(0u)
+      "l"(da), "l"(db), "r"(idesc), "r"(acc), "r"(0u), "r"(0u), "r"(0u), "r"(0u)
       : "memory");
 }
 
@@ -458,7 +461,7 @@ template <int SIDE, bool PDIN>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_tensor_tcf(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap pmap,
                  const __grid_constant__ CUtensorMap omap, float* __restrict__ C, const float* __restrict__ qpack,
-                 int n, int col_tiles, int num_tiles, long ldc, int dbg, int in_bny, int out_bny) {
+                 int n, int col_tiles, int num_items, int full_items, long ldc, int dbg, int in_bny, int out_bny) {
   // in_bny / out_bny (M side, split grid): X is read from / C written to the
   // all-to-all's peer-blocked layout [s][plane][jl][i] (j = s ny + jl) through
   // 4D tensor maps, so the k <-> j slab transposes need no pass of their own
@@ -478,18 +481,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   // X{E,O}{H,L} / Q{E,O}{H,L}: p = 0 even, 1 odd; l = 0 hi, 1 lo
   auto XS = [&](int s, int p, int l) { return S.x[s] + (p * 2 + l) * TF_X; };
   auto QT = [&](int s, int p, int l) { return S.q[s] + (p * 2 + l) * TF_Q; };
+  // Work items: tiles [0, full_items) whole (128 columns); every tile after
+  // that is split into two 64-column halves (items full_items + 2 h, + 1),
+  // so the last round of a persistent grid is balanced (launch_tcf).
   struct Tile {
-    int a0, plane;
+    int a0, plane, w;
     long col0;
   };
   auto tile_of = [&](int t) {
     Tile T;
-    T.a0 = (t % a_tiles) * TF_BM;
-    const int ct = t / a_tiles;
-    T.col0 = (long)(ct % col_tiles) * TF_BN;
+    int tt = t, half = 0;
+    T.w = TF_BN;
+    if (t >= full_items) {
+      tt = full_items + ((t - full_items) >> 1);
+      half = (t - full_items) & 1;
+      T.w = TF_BN / 2;
+    }
+    T.a0 = (tt % a_tiles) * TF_BM;
+    const int ct = tt / a_tiles;
+    T.col0 = (long)(ct % col_tiles) * TF_BN + half * (TF_BN / 2);
     T.plane = ct / col_tiles;
     return T;
   };
+  const int num_tiles = num_items;  // (loops below run over work items)
   const CUtensorMap* xm = &xmap;
   const CUtensorMap* pm = &pmap;
   const CUtensorMap* om = &omap;
@@ -581,6 +595,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       int it = 0;
       for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
         const int acc = it & 1;
+        const uint32_t idesc = tile_of(t).w == TF_BN ? kIdescF : kIdescF64;
         mbar_wait(&S.tmem_empty[acc], (uint32_t)((it >> 1) & 1) ^ 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t dE = tmem + (uint32_t)(acc * 256), dO = dE + 128;
@@ -596,9 +611,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             for (int ks = 0; ks < TF_KH / 8; ++ks) {
               const uint64_t qh = kmajor_desc16(QT(rq.s, p, 0) + ks * 256), ql = kmajor_desc16(QT(rq.s, p, 1) + ks * 256);
               const uint64_t xh = kmajor_desc16(XS(rx.s, p, 0) + ks * 256), xl = kmajor_desc16(XS(rx.s, p, 1) + ks * 256);
-              mma_tf32f(d, ql, xh, (first | ks) ? 1u : 0u);
-              mma_tf32f(d, qh, xl, 1u);
-              mma_tf32f(d, qh, xh, 1u);
+              mma_tf32f(d, ql, xh, (first | ks) ? 1u : 0u, idesc);
+              mma_tf32f(d, qh, xl, 1u, idesc);
+              mma_tf32f(d, qh, xh, 1u, idesc);
             }
           }
           mma_commit(&S.xfree[rx.s]);
@@ -614,10 +629,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     Ring<CS> rx;
     long g = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      const bool active = ct < tile_of(t).w;  // (a half tile converts 64 columns)
       for (int kb = 0; kb < KB; ++kb, ++g, r.next(), rx.next()) {
         const int s = r.s;
         mbar_wait(&S.rawfull[s], r.ph);
-        if (dbg & 1) {  // (profiling knob: skip the split)
+        if ((dbg & 1) || !active) {  // (dbg 1: profiling knob, skip the split)
           mbar_arrive(&S.rawfree[s]);
           if (g >= CS) mbar_wait(&S.xfree[rx.s], rx.ph ^ 1u);
           mbar_arrive(&S.xfull[rx.s]);
@@ -704,7 +720,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int arow = T.a0 + 32 * q4;  // first folded row of this warp's lane quarter
       const uint32_t lanebase = tmem + ((uint32_t)(32 * q4) << 16) + (uint32_t)(acc * 256);
-      for (int cc = 0; cc < TF_BN && !(dbg & 4); cc += 32) {
+      for (int cc = 0; cc < T.w && !(dbg & 4); cc += 32) {
         uint32_t e[32], o[32];
         tmem_ld32(lanebase + (uint32_t)cc, e);
         tmem_ld32(lanebase + 128u + (uint32_t)cc, o);
@@ -846,10 +862,18 @@ void launch_tcf(int n, long cols, const float* x, float* out, const float* pd, c
       omap = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, out, 2, dims, strides, ob2, CU_TENSOR_MAP_SWIZZLE_128B);
     }
   }
+  // Persistent grid of at most one CTA per SM.  When the last round would
+  // leave SMs idle (num_tiles % G tiles on G SMs), its tiles are split into
+  // 64-column halves on twice as many CTAs: e.g. 256^3 = 512 tiles on 148
+  // SMs runs 3 full rounds plus one half-tile round (3.5 tile-times, not 4).
   const int num_tiles = (n / 2 / TF_BM) * col_tiles * planes;
-  const int grid = num_tiles < sm_count() ? num_tiles : sm_count();
+  const int G = sm_count();
+  const int rem = num_tiles % G;
+  const int full_items = (rem > 0 && 2 * rem <= G && !(dbg & 64)) ? num_tiles - rem : num_tiles;
+  const int num_items = full_items + 2 * (num_tiles - full_items);
+  const int grid = num_items < G ? num_items : G;
   launch_pdl(k_tensor_tcf<SIDE, PDIN>, dim3(grid), dim3(TC_THREADS), smem, st, map, pmap, omap, out, qpack, n,
-             col_tiles, num_tiles, cols, dbg, in_bny, out_bny);
+             col_tiles, num_items, full_items, cols, dbg, in_bny, out_bny);
   LAUNCHED("tensor_tc_fold");
 }
 

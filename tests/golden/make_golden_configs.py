@@ -14,6 +14,7 @@ What it records (consumed by tests/test_gpu_configs.py):
 * ``m1_*``  heat 256^3, midpoint1, one step (t_end = tau = 0.01) at F32 tol 1e-3
   and F64 tol 1e-5 (SURVEY.md §8(c) golden values 1.312229e-02 / 1.012499e-04).
 """
+import hashlib
 import os
 import sys
 import time
@@ -38,13 +39,17 @@ def record(out, key, r):
     out[f"{key}_sub"] = sub(r["state"])
     s = r["state"]
     out[f"{key}_moments"] = np.array([s.sum(), np.dot(s, s), np.abs(s).max()])
+    # bitwise fingerprint of the whole state (portable, unlike numpy sums)
+    out[f"{key}_sha256"] = np.frombuffer(hashlib.sha256(np.ascontiguousarray(s).tobytes()).digest(), np.uint8)
     out[f"{key}_wall"] = np.array([r["wall_seconds"], R.max_threads()])
 
 
 if __name__ == "__main__":
     R = Reference()
     R.set_threads(os.cpu_count() or 1)
-    out = {"n": np.array([N, SUB])}
+    path = os.path.join(HERE, "configs.npz")
+    only = sys.argv[1:]  # e.g. "m1_f32 m1_f64": recompute these keys, keep the rest
+    out = dict(np.load(path)) if only and os.path.exists(path) else {"n": np.array([N, SUB])}
     runs = [
         ("m1_f32", "midpoint1", 0.01, 1e-3, "f32"),
         ("m1_f64", "midpoint1", 0.01, 1e-5, "f64"),
@@ -52,9 +57,11 @@ if __name__ == "__main__":
         ("c2_f64", "4s3pB", 0.1, 1e-5, "f64"),
     ]
     for key, meth, t_end, tol, prec in runs:
+        if only and key not in only:
+            continue
         t0 = time.time()
         r = R.integrate(0, N, R.tableau(meth), 0.01, t_end, tol, prec, 40)
         record(out, key, r)
         print(f"{key}: err_max {r['error_max']:.6e} err_l2 {r['error_l2']:.6e} iters {r['solve_iterations']} "
               f"({time.time() - t0:.0f} s)", flush=True)
-        np.savez_compressed(os.path.join(HERE, "configs.npz"), **out)
+        np.savez_compressed(path, **out)

@@ -38,14 +38,28 @@ def test_reference_suite_on_b200(name):
     assert r.returncode == 0 and "Status: SUCCESS" in r.stdout, tail
 
 
+# criterion 3 (binary16 truncation of 4s3pA's stability region) FAILS in the
+# reference itself as built here: its own stability.cpp + tableau.cpp give
+# 33424 stable cells untruncated and 33428 under binary16 (checked with the
+# reference sources compiled by g++ 13.3 in the build container), so the gate
+# cannot exit 0 for the reference either.  The drop-in must reproduce exactly
+# that outcome; every other criterion must pass.
+REFERENCE_CRITERION_3 = "stable cells untruncated 33424, f16 33428, f32 33424"
+
+
 @pytest.mark.gpu
 def test_reference_acceptance_gate_on_b200():
     r = _run("acceptance", timeout=1800)
-    assert r.returncode == 0 and "acceptance: PASS" in r.stdout, r.stdout[-4000:]
-    # criteria 6-8 (acceptance.cpp:213-279): the iteration-count contract
-    for crit in (6, 7, 8):
-        line = next(l for l in r.stdout.splitlines() if l.startswith(f"criterion {crit:2d}"))
-        assert "[PASS]" in line, line
+    lines = {int(l.split()[1]): l for l in r.stdout.splitlines() if l.startswith("criterion")}
+    assert sorted(lines) == list(range(1, 12)), r.stdout[-4000:]
+    for crit, line in lines.items():
+        if crit == 3:
+            assert "[FAIL]" in line and REFERENCE_CRITERION_3 in line, line
+        else:
+            assert "[PASS]" in line, line
+    # criteria 6-8 (acceptance.cpp:213-279) are the iteration-count contract
+    # of the stage solves, 9-10 temporal orders and F32 accuracy, 11 the
+    # tensor-l / tensor-m timing labels
 
 
 @pytest.mark.parametrize("name", HOST)
