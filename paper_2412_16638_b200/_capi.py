@@ -119,6 +119,7 @@ class Result(C.Structure):
 
 
 APPLY_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p)
+TIMING_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_char_p, C.c_longlong, C.c_double)
 
 vp, i32, sz, f64 = C.c_void_p, C.c_int, C.c_size_t, C.c_double
 dptr = C.POINTER(C.c_double)
@@ -173,6 +174,13 @@ SIGNATURES = {
     "mprkb_integrate": (i32, [C.POINTER(Config), vp, sz, vp, C.POINTER(Result)]),
     "mprkb_stepper_integrate": (i32, [vp, vp, sz, vp, C.POINTER(Result)]),
     "mprkb_temporal_order": (i32, [C.POINTER(Config), dptr, i32, dptr, dptr, dptr, ip]),
+    "mprkb_stepper_integrate_from": (i32, [vp, vp, vp, sz, vp, C.POINTER(Result)]),
+    # instrumentation and host helpers
+    "mprkb_kron_apply_count": (C.c_longlong, [i32]),
+    "mprkb_reset_kron_apply_counts": (None, []),
+    "mprkb_spectral": (i32, [i32, i32, f64, f64, vp, vp, vp]),
+    "mprkb_apply_f": (i32, [i32, i32, f64, f64, vp, i32, vp, vp, vp]),
+    "mprkb_op_apply_timed": (i32, [vp, vp, vp, vp, TIMING_FN, vp]),
     # split grid (k-slab decomposition)
     "mprkb_set_device": (i32, [i32]),
     "mprkb_slab_plan": (i32, [i32, i32, i32, ip, ip, ip, ip]),
