@@ -93,6 +93,34 @@ struct FevalCombine {
 bool feval_combine_supported(const StencilSpec& k);
 void feval_combine(const StencilSpec& k, const float* y32, const FevalCombine& f, cudaStream_t st);
 
+// Pull form (stencil.cu k_stage_pull): one pass forms a stage's right-hand
+// side u + sum_j (ch_j f_hi(y_j) + ce_j f_eps(y_j)) + cg g — or, `final`,
+// u + sum_j ch_j f_hi(y_j) written to uout — re-evaluating both f's from the
+// fp32 stage vectors y_0..y_{nin-1} (F32 policy, Dirichlet heat on the TMA
+// path, undivided grid).  Terms in the reference's order, bitwise the stored-f
+// combination.  finite_flag checks y_{nin-1} (the newest stage vector).
+struct StagePull {
+  int nin = 0;
+  bool final = false;
+  const float* y[4] = {};
+  double ch[4] = {}, ce[4] = {};
+  int hh[4] = {}, he[4] = {};
+  double cg = 0.0;
+  int hg = 0;
+  const double* u = nullptr;
+  double* uout = nullptr;
+  float* bout = nullptr;
+  int* ovf_flag = nullptr;
+  int* finite_flag = nullptr;
+  int* bad_flag = nullptr;
+  const int* gate = nullptr;
+  int gate_count = 0;
+  const double* g = nullptr;
+  const float* g32 = nullptr;
+};
+bool stage_pull_supported(const StencilSpec& k);
+void stage_pull(const StencilSpec& k, const StagePull& p, cudaStream_t st);
+
 // ---- tensor contractions (precond.hpp:69-122) --------------------------------------
 // side 0 L (stride n^2), 1 M (stride n), 2 R (stride 1).  pd: fused diag scale
 // of the output (precond.hpp:172) or null.  fold: Q has the Dirichlet sine

@@ -1611,6 +1611,282 @@ bool dots2_tma(const StencilSpec& sp, const float* z, const float* r, const RedS
   return true;
 }
 
+// ---- stage right-hand sides and the final update in pull form ----------------------
+// (stepper.cpp:157-172, 200-204)  The reference forms
+//     rhs_i = u + sum_{j<i} (tau a^h_ij f_hi_j + tau a^e_ij f_eps_j) + tau a^e_ii g
+//     u    <- u + sum_i tau b_i f_hi_i
+// from stored f vectors.  With fp32 stage solutions y_j both f's are pure
+// functions of y_j — f_hi_j = K widen(y_j) + g, f_eps_j = K32 y_j + g32 — so
+// one pass per right-hand side re-evaluates them from the stage vectors
+// themselves: 4 bytes per point per term instead of an fp64 f (or an fp64
+// accumulator read and written per later stage).  Every term is added to u in
+// the reference's order (j ascending, the fp64 term before the eps term, the
+// forcing last) and each f value is computed by the same arithmetic as the
+// stored one, so the sums round exactly as the reference's axpy chains do:
+// bitwise the push-form pipeline (EpiFevalCombine) and the unfused kernels.
+// The M stage vectors stream through one TMA plane ring (M tiles per slot,
+// one mbarrier), neighbours from smem and shuffles as in k_stencil_tma; u is
+// prefetched a plane ahead.  FINAL: u is written in place (gated on the
+// step's earlier checks; the non-finite flag covers the updated state).
+namespace {
+
+constexpr int kPullMax = 4;
+struct PullMaps {
+  CUtensorMap m[kPullMax];
+};
+struct PullArgs {
+  double ch[kPullMax] = {}, ce[kPullMax] = {};  // tau a^h_ij, tau a^e_ij  (FINAL: tau b_j in ch)
+  int hh[kPullMax] = {}, he[kPullMax] = {};     // present (nonzero in the tableau)
+  double cg = 0.0;                              // tau a^e_ii (forcing), when hg
+  int hg = 0;
+  float s32 = 0.f, g32k = 0.f;  // the binary32 stencil's sigma / gamma
+  const double* u = nullptr;
+  double* uout = nullptr;     // FINAL
+  float* bout = nullptr;      // rhs: narrowed right-hand side (the solve's b and x0)
+  int* ovf_flag = nullptr;    // rhs: downcast overflow
+  int* finite_flag = nullptr; // rhs: check_finite of the newest stage vector y_{M-1} (nullable)
+  int* bad_flag = nullptr;    // FINAL: updated state not finite
+  const int* gate = nullptr;  // FINAL: the step's earlier checks (device); any set -> no write
+  int gate_count = 0;
+  ForcingGen gen;             // forcing regenerated when gen.s is set, else read from g / g32
+  const double* g = nullptr;
+  const float* g32 = nullptr;
+};
+template <int M>
+constexpr int pull_stages() { return M == 1 ? 5 : 4; }  // ring depth: planes k-1..k+1 + 1-2 in flight
+template <int M>
+constexpr size_t pull_smem() {
+  return (size_t)pull_stages<M>() * M * tma_slot_elems<float>() * sizeof(float) + pull_stages<M>() * sizeof(uint64_t) +
+         128;
+}
+
+template <int M, bool FINAL>
+__global__ void __launch_bounds__(TTHREADS)
+    k_stage_pull(const __grid_constant__ PullMaps maps, int n, int kc, double s, double g, const PullArgs a) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int TSTM = pull_stages<M>();
+  constexpr int PLANE = tma_slot_elems<float>();
+  extern __shared__ unsigned char smem_raw[];
+  float* buf = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  uint64_t* full = reinterpret_cast<uint64_t*>(buf + TSTM * M * PLANE);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int i0 = blockIdx.x * TI, j0 = blockIdx.y * TJ;
+  int k0, k1;
+  plane_range(n, 0, n, kc, k0, k1);
+  const int planes = k1 - k0 + 2;
+  constexpr uint32_t bytes = (TJ + 2) * TW * sizeof(float);
+  if (tid == 0) {
+    for (int b = 0; b < TSTM; ++b) mbar_init(&full[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  bool skip = false;
+  if constexpr (FINAL) {
+    int any = 0;
+    for (int c = 0; c < a.gate_count; ++c) any |= __ldg(a.gate + c);
+    skip = any != 0;
+  }
+  auto issue = [&](int q) {  // plane k0 - 1 + q of every input into slot q % TSTM
+    const int k = k0 - 1 + q, b = q % TSTM;
+    mbar_expect_tx(&full[b], M * bytes);
+#pragma unroll
+    for (int j = 0; j < M; ++j) tma_3d(buf + (b * M + j) * PLANE, &maps.m[j], i0 - 4, j0 - 1, k, &full[b]);
+  };
+  if (tid == 0)
+    for (int q = 0; q < TSTM && q < planes; ++q) issue(q);
+  auto wait = [&](int q) { mbar_wait(&full[q % TSTM], (uint32_t)(q / TSTM) & 1u); };
+  const long nn = n, n2 = nn * nn;
+  const int col = 4 + 4 * lane;
+  auto gidx = [&](int r, int k) { return (i0 + 4 * lane) + (long)(j0 + r) * nn + (long)k * n2; };
+  // u is read coherently: the final pass writes it in place
+  auto ldu = [&](long i) { return FINAL ? ld4rw(a.u + i) : ld4(a.u + i); };
+  V4<double> pre[TROWS];
+#pragma unroll
+  for (int rr = 0; rr < TROWS; ++rr) pre[rr] = ldu(gidx(warp * TROWS + rr, k0));
+  bool bad = false, ovf = false, nonfinite = false;
+  for (int k = k0; k < k1; ++k) {
+    const int q = k - k0 + 1;
+    if (k == k0) {
+      wait(0);
+      wait(1);
+    }
+    wait(q + 1);
+    V4<double> nxt[TROWS];
+#pragma unroll
+    for (int rr = 0; rr < TROWS; ++rr)
+      if (k + 1 < k1) nxt[rr] = ldu(gidx(warp * TROWS + rr, k + 1));
+#pragma unroll
+    for (int rr = 0; rr < TROWS; ++rr) {
+      const int r = warp * TROWS + rr;
+      const int o = (r + 1) * TW + col;
+      const long gi = gidx(r, k);
+      V4<double> gv;
+      V4<float> g32v;
+      if (a.gen.s) {
+        forcing4(a.gen, gi, gv.x);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) g32v.x[e] = __double2float_rn(gv.x[e]);
+      } else {
+        gv = ld4(a.g + gi);
+        if (!FINAL) g32v = ld4(a.g32 + gi);
+      }
+      V4<double> acc = pre[rr];
+#pragma unroll
+      for (int j = 0; j < M; ++j) {
+        const float* pm = buf + (((q - 1) % TSTM) * M + j) * PLANE;
+        const float* pc = buf + ((q % TSTM) * M + j) * PLANE;
+        const float* pp = buf + (((q + 1) % TSTM) * M + j) * PLANE;
+        const float4 c4 = *reinterpret_cast<const float4*>(pc + o);
+        const float4 ym4 = *reinterpret_cast<const float4*>(pc + o - TW);
+        const float4 yp4 = *reinterpret_cast<const float4*>(pc + o + TW);
+        const float4 zm4 = *reinterpret_cast<const float4*>(pm + o);
+        const float4 zp4 = *reinterpret_cast<const float4*>(pp + o);
+        const float cc[4] = {c4.x, c4.y, c4.z, c4.w};
+        const float ymv[4] = {ym4.x, ym4.y, ym4.z, ym4.w}, ypv[4] = {yp4.x, yp4.y, yp4.z, yp4.w};
+        const float zmv[4] = {zm4.x, zm4.y, zm4.z, zm4.w}, zpv[4] = {zp4.x, zp4.y, zp4.z, zp4.w};
+        float l32 = shfl_up1(cc[3]), r32 = shfl_down1(cc[0]);
+        if (lane == 0) l32 = pc[o - 1];
+        if (lane == 31) r32 = pc[o + 4];
+        if (!FINAL && j == M - 1 && a.finite_flag)
+          nonfinite |= !(isfinite(cc[0]) && isfinite(cc[1]) && isfinite(cc[2]) && isfinite(cc[3]));
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float xl = e == 0 ? l32 : cc[e - 1];
+          const float xr = e == 3 ? r32 : cc[e + 1];
+          // f_hi: the fp64 stencil of the widened values (EpiFevalCombine / EpiF64Forcing)
+          const double v64 = point<double>(0, s, g, 0.0, (double)cc[e], (double)xl, (double)xr, (double)ymv[e],
+                                           (double)ypv[e], (double)zmv[e], (double)zpv[e]);
+          const double fh = xadd(v64, gv.x[e]);
+          if constexpr (FINAL) {
+            acc.x[e] = xadd(acc.x[e], xmul(a.ch[j], fh));
+          } else {
+            if (a.hh[j]) acc.x[e] = xadd(acc.x[e], xmul(a.ch[j], fh));
+            if (a.he[j]) {
+              const float v32 = point<float>(0, a.s32, a.g32k, 0.0f, cc[e], xl, xr, ymv[e], ypv[e], zmv[e], zpv[e]);
+              const float fe = xadd(v32, g32v.x[e]);
+              acc.x[e] = xadd(acc.x[e], xmul(a.ce[j], (double)fe));
+            }
+          }
+        }
+      }
+      if constexpr (FINAL) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) bad |= !isfinite(acc.x[e]);
+        if (!skip) st4(a.uout + gi, acc);
+      } else {
+        V4<float> b;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          double rv = acc.x[e];
+          if (a.hg) rv = xadd(rv, xmul(a.cg, gv.x[e]));
+          ovf |= f32_overflows(rv);
+          b.x[e] = __double2float_rn(rv);
+        }
+        st4(a.bout + gi, b);
+      }
+    }
+#pragma unroll
+    for (int rr = 0; rr < TROWS; ++rr) pre[rr] = nxt[rr];
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0 && q - 1 + TSTM < planes) issue(q - 1 + TSTM);
+  }
+  if (FINAL && bad && !skip) *a.bad_flag = 1;
+  if (!FINAL && ovf) *a.ovf_flag = 1;
+  if (!FINAL && nonfinite) *a.finite_flag = 1;
+}
+
+template <int M, bool FINAL>
+void launch_pull(const StencilSpec& sp, const float* const* y, const PullArgs& a, cudaStream_t st) {
+  constexpr size_t smem = pull_smem<M>();
+  const int n = sp.n;
+  static thread_local int resident = 0;
+  static thread_local int chunk = 0, chunk_n = -1;
+  if (!resident) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_stage_pull<M, FINAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stage_pull<M, FINAL>, TTHREADS, smem));
+    resident = std::max(1, per_sm) * sm_count();
+  }
+  const long cols = (long)(n / TI) * (n / TJ);
+  if (chunk_n != n) {  // the smallest (waves x planes per CTA incl. the 2-plane halo)
+    long best_cost = -1;
+    for (int kc = 4; kc <= 64; ++kc) {
+      const long units = cols * ((n + kc - 1) / kc);
+      const long cost = ((units + resident - 1) / resident) * (std::min(kc, n) + 2);
+      if (best_cost < 0 || cost < best_cost) {
+        chunk = kc;
+        best_cost = cost;
+      }
+    }
+    chunk_n = n;
+  }
+  PullMaps maps;
+  const cuuint64_t nn = (cuuint64_t)n;
+  const cuuint64_t dims3[3] = {nn, nn, nn}, str3[2] = {nn * 4, nn * nn * 4};
+  const cuuint32_t box3[3] = {(cuuint32_t)TW, (cuuint32_t)(TJ + 2), 1};
+  for (int j = 0; j < kPullMax; ++j)
+    maps.m[j] = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, y[j < M ? j : 0], 3, dims3, str3, box3);
+  const dim3 grid((unsigned)(n / TI), (unsigned)(n / TJ), (unsigned)((n + chunk - 1) / chunk));
+  launch_pdl(k_stage_pull<M, FINAL>, grid, dim3(TTHREADS), smem, st, maps, n, chunk, sp.sigma, sp.gamma, a);
+  LAUNCHED(FINAL ? "final_pull" : "rhs_pull");
+}
+
+}  // namespace
+
+bool stage_pull_supported(const StencilSpec& k) {
+  return k.stencil == 0 && k.n % TI == 0 && !k.halo && (k.nz == 0 || k.nz == k.n) && tma_stencil_enabled();
+}
+
+void stage_pull(const StencilSpec& k, const StagePull& p, cudaStream_t st) {
+  if (!stage_pull_supported(k)) MPRKB_THROW(10, "stage_pull: needs the undivided TMA stencil (Dirichlet, n % 128 == 0)");
+  if (p.nin < 1 || p.nin > kPullMax) MPRKB_THROW(10, "stage_pull: 1 to 4 stage vectors per pass");
+  PullArgs a;
+  for (int j = 0; j < p.nin; ++j) {
+    a.ch[j] = p.ch[j];
+    a.ce[j] = p.ce[j];
+    a.hh[j] = p.hh[j];
+    a.he[j] = p.he[j];
+  }
+  a.cg = p.cg;
+  a.hg = p.hg;
+  a.s32 = (float)k.sigma;
+  a.g32k = (float)k.gamma;
+  a.u = p.u;
+  a.uout = p.uout;
+  a.bout = p.bout;
+  a.ovf_flag = p.ovf_flag;
+  a.finite_flag = p.finite_flag;
+  a.bad_flag = p.bad_flag;
+  a.gate = p.gate;
+  a.gate_count = p.gate ? p.gate_count : 0;
+  a.gen = k.forcing;
+  a.g = p.g;
+  a.g32 = p.g32;
+  if (!a.gen.s && (!a.g || (!p.final && !a.g32))) MPRKB_THROW(10, "stage_pull: forcing required");
+  // logical stencil applications (kron_apply_count): the newest stage vector's
+  // f_hi (+ f_eps) — re-evaluations of earlier stages' f are not new applications
+  note_kron(false);
+  if (!p.final && p.he[p.nin - 1]) note_kron(true);
+  const float* const* y = p.y;
+  if (p.final) {
+    switch (p.nin) {
+      case 1: launch_pull<1, true>(k, y, a, st); break;
+      case 2: launch_pull<2, true>(k, y, a, st); break;
+      case 3: launch_pull<3, true>(k, y, a, st); break;
+      default: launch_pull<4, true>(k, y, a, st); break;
+    }
+  } else {
+    switch (p.nin) {
+      case 1: launch_pull<1, false>(k, y, a, st); break;
+      case 2: launch_pull<2, false>(k, y, a, st); break;
+      case 3: launch_pull<3, false>(k, y, a, st); break;
+      default: launch_pull<4, false>(k, y, a, st); break;
+    }
+  }
+}
+
 #define INST_STENCIL(T)                                                                          \
   template void stencil_apply<T>(const StencilSpec&, const T*, T*, cudaStream_t);               \
   template void stencil_residual<T>(const StencilSpec&, const T*, const T*, T*, const RedSlot*, \

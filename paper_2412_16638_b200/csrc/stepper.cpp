@@ -155,7 +155,32 @@ Stepper::Stepper(const StepperConfig& cfg)
     fused_ = ok;
     const char* fe = std::getenv("MPRKB_FUSED_FINAL");
     fuse_final_ = fused_ && !(fe && fe[0] == '0') && t.b[q - 1] != 0.0 && q - 1 <= kFevalMaxAcc;
-    if (fused_) {
+    // pull form (MPRKB_PULL=1, undivided grid): each right-hand side pass
+    // reads the earlier stage vectors it couples to (the newest always, for
+    // its finiteness check), the final pass those with b_i != 0 — at most 4
+    // per pass.  Off by default: it moves 52 N fewer bytes per 4s3pB step but
+    // re-evaluates 10 f pairs instead of 4, and the fp32 -> fp64 widening of
+    // every stencil operand runs on the quarter-rate XU pipe (ncu: XU 50 %
+    // busy), so the passes are conversion-bound (566 vs 505 us per step,
+    // profiles/r02/pull_vs_push.txt)
+    const char* pe = std::getenv("MPRKB_PULL");
+    bool pull = fused_ && fuse_final_ && (pe && pe[0] == '1') && stage_pull_supported(kspec_);
+    for (int i = 1; i < q && pull; ++i) {
+      int nin = 0;
+      for (int j = 0; j < i; ++j) nin += (j == i - 1 || t.ah(i, j) != 0.0 || t.ae(i, j) != 0.0) ? 1 : 0;
+      pull = nin <= 4;
+    }
+    if (pull) {
+      int nfin = 0;
+      for (int i = 0; i < q; ++i) nfin += t.b[i] != 0.0 ? 1 : 0;
+      pull = nfin <= 4;
+    }
+    pull_ = pull;
+    if (pull_) {
+      ys_.resize(q);
+      for (int i = 0; i < q; ++i) ys_[i].alloc(m * sizeof(float));
+    }
+    if (fused_ && !pull_) {
       acc_.resize(q + 1);
       for (int k = 2; k < q; ++k) acc_[k].alloc(m * sizeof(double));
       if (fuse_final_) acc_[q].alloc(m * sizeof(double));  // the final update's running sum (u + tau sum b_i f_hi_i)
@@ -166,7 +191,7 @@ Stepper::Stepper(const StepperConfig& cfg)
   for (int i = 0; i < q; ++i) {
     // the fused pipeline keeps f_eps in registers, and f_hi too when the
     // final update is fused; it stores f_hi only for b_i != 0 otherwise
-    const bool hi = fused_ ? (!fuse_final_ && t.b[i] != 0.0) : need_f64_[i] != 0;
+    const bool hi = pull_ ? false : fused_ ? (!fuse_final_ && t.b[i] != 0.0) : need_f64_[i] != 0;
     const bool eps = !fused_ && need_feps_[i] && (cfg_.f32 || !need_f64_[i]);
     if (hi) f_hi_[i].alloc(m * sizeof(double));
     if (eps) f_eps_[i].alloc(m * (cfg_.f32 ? sizeof(float) : sizeof(double)));
@@ -177,7 +202,7 @@ Stepper::Stepper(const StepperConfig& cfg)
   if (!solvers_.empty()) {
     const size_t s = dtype_size(solve_dtype_);
     bsol_.alloc(m * s);
-    xsol_.alloc(m * s);
+    if (!pull_) xsol_.alloc(m * s);
     Comm* comm = slab_.split() ? slab_.comm : nullptr;
     switch (solve_dtype_) {
       case 0: w32_ = std::make_unique<KrylovWork<float>>(m); w32_->comm = comm; break;
@@ -198,6 +223,10 @@ Stepper::~Stepper() {
 // raises a device flag in its own slot; the flags are inspected in program
 // order before u is touched, so the first failing check is the one thrown.
 void Stepper::step(double* u, StepTrace& trace) {
+  if (pull_) {
+    step_pull(u, trace);
+    return;
+  }
   if (fused_) {
     step_fused(u, trace);
     return;
@@ -500,6 +529,113 @@ void Stepper::step_fused(double* u, StepTrace& trace) {
       final_update(m, u, fin, fin_flag, st_, gate, stage_checks);
   }
   raise_flags();
+  if (timer_.enabled()) timer_.resolve();
+}
+
+// Stepper::step in pull form (undivided grid; see step_pull in stepper.hpp).
+// Stage i's right-hand side is ONE pass over u and the stage vectors it
+// couples to — f_hi and f_eps re-evaluated from the fp32 y_j, every term added
+// in the reference's order — so each value rounds exactly as in step() and
+// step_fused(); the same checks are raised in the same order: y_{i-1}'s
+// finiteness, then rhs_i's binary32 overflow, then the next solve.
+void Stepper::step_pull(double* u, StepTrace& trace) {
+  trace = StepTrace{};
+  flags_.clear();
+  struct Check {
+    int slot, code;
+    const char* msg;
+  };
+  std::vector<Check> checks;
+  int next = 1;
+  auto check_slot = [&](int code, const char* msg) {
+    if (next >= 255) MPRKB_THROW(1, "stepper: too many checks");
+    checks.push_back({next, code, msg});
+    return flags_.dev(next++);
+  };
+  const Tableau& t = cfg_.tab;
+  const int q = t.q;
+  const double tau = cfg_.tau;
+  const size_t m = m_;
+  const Crit crit{cfg_.tol, cfg_.max_iter};
+  const char* kOverflow = "downcast: value exceeds the binary32 range";
+  const char* kStage = "stage vector picked up a NaN or infinity";
+  float* b32 = bsol_.as<float>();
+  EventTimer* tm = timer_.enabled() ? &timer_ : nullptr;
+  // x0 = rhs is the rhs buffer itself; the solution always lands in ys_[i]
+  // (the fused first update writes x1 there, or x0 is copied there first)
+  auto solve = [&](int i) {
+    StageSolver& S = solvers_[solver_of_stage_[i]];
+    SolveReport rep;
+    float* sol = nullptr;
+    float* y = ys_[i].as<float>();
+    cg_solve<float>(*S.op, S.pre.get(), b32, b32, crit, cfg_.num, *w32_, rep, st_, tm, y, &sol);
+    if (sol != y) CUDA_CHECK(cudaMemcpyAsync(y, sol, m * sizeof(float), cudaMemcpyDeviceToDevice, st_));
+    if (!rep.converged) trace.solver_failure = true;
+    trace.solves.push_back(std::move(rep));
+  };
+  const double* g = g64_.as<double>();
+  const float* g32 = g32_.as<float>();
+  // stage 0: rhs = u + tau a_00 g (stepper.cpp:157-172), x0 = rhs
+  {
+    CombineTerms terms;
+    add_forcing(terms, tau * t.ae(0, 0));
+    Bracket br(timer_, "axpy", st_);
+    combine(m, u, terms, 1, b32, check_slot(6, kOverflow), st_);
+  }
+  solve(0);
+  for (int i = 1; i < q; ++i) {
+    StagePull p;
+    for (int j = 0; j < i; ++j) {
+      if (!(j == i - 1 || t.ah(i, j) != 0.0 || t.ae(i, j) != 0.0)) continue;
+      const int c = p.nin++;
+      p.y[c] = ys_[j].as<float>();
+      p.hh[c] = t.ah(i, j) != 0.0;
+      p.ch[c] = tau * t.ah(i, j);
+      p.he[c] = t.ae(i, j) != 0.0;
+      p.ce[c] = tau * t.ae(i, j);
+    }
+    p.finite_flag = check_slot(9, kStage);  // y_{i-1} (the last input)
+    p.hg = 1;
+    p.cg = tau * t.ae(i, i);
+    p.u = u;
+    p.bout = b32;
+    p.ovf_flag = check_slot(6, kOverflow);
+    p.g = g;
+    p.g32 = g32;
+    {
+      Bracket br(timer_, "stencil", st_);
+      stage_pull(kspec_, p, st_);
+    }
+    solve(i);
+  }
+  check_finite32(m, ys_[q - 1].as<float>(), check_slot(9, kStage), st_);
+  const int stage_checks = next - 1;
+  {
+    Bracket br(timer_, "axpy", st_);
+    StagePull p;
+    p.final = true;
+    for (int i = 0; i < q; ++i) {
+      if (t.b[i] == 0.0) continue;
+      const int c = p.nin++;
+      p.y[c] = ys_[i].as<float>();
+      p.hh[c] = 1;
+      p.ch[c] = tau * t.b[i];
+    }
+    p.u = u;
+    p.uout = u;
+    p.g = g;
+    p.bad_flag = check_slot(9, "updated state picked up a NaN or infinity");
+    if (stage_checks > 0) {
+      CUDA_CHECK(cudaMemcpyAsync(gate_dev_.get(), flags_.dev(1), sizeof(int) * stage_checks, cudaMemcpyHostToDevice,
+                                 st_));
+      p.gate = gate_dev_.as<int>();
+      p.gate_count = stage_checks;
+    }
+    stage_pull(kspec_, p, st_);
+  }
+  stream_sync(st_);
+  for (const Check& c : checks)
+    if (flags_.value(c.slot)) MPRKB_THROW(c.code, c.msg);
   if (timer_.enabled()) timer_.resolve();
 }
 

@@ -59,6 +59,12 @@ class Stepper {
   // fused with the next stage's right-hand side (EpiFevalCombine); later
   // stages' couplings accumulate in acc_ (see step_fused)
   void step_fused(double* u, StepTrace& trace);
+  // the same pipeline in pull form (undivided grid): every right-hand side
+  // and the final update re-evaluate f_hi / f_eps from the stored fp32 stage
+  // vectors ys_ (stencil.cu k_stage_pull) — no fp64 accumulators
+  void step_pull(double* u, StepTrace& trace);
+  bool pull_ = false;
+  std::vector<DevBuf> ys_;  // pull form: stage i's solution (fp32)
   void add_forcing(CombineTerms& t, double coef) const;  // + coef g (regenerated or read)
   bool fused_ = false;
   bool fuse_final_ = false;  // fused pipeline also accumulates the final update (decided at construction)

@@ -498,3 +498,58 @@ def test_fused_pipeline_many_stages(gpu, mp, q):
     for _ in range(2):
         assert fused.step(a)["iterations"] == plain.step(c)["iterations"]
     assert same_bits(a, c)
+
+
+@pytest.mark.parametrize("name", ["4s3pB", "4s3pC"])
+def test_pull_form_bitwise_push_form(gpu, mp, name):
+    """MPRKB_PULL=1: the fp32 heat pipeline on an undivided grid forms every
+    stage right-hand side and the final update in pull form (stencil.cu
+    k_stage_pull: f_hi / f_eps re-evaluated from the stored fp32 stage
+    vectors, no fp64 accumulators): bitwise the default push-form pipeline
+    (accumulators) and hence the stage-by-stage kernels."""
+    import os
+
+    t = mp.builtin(name)
+    n = 256
+    push = mp.Stepper("heat", n, t, 0.01, 1e-3, "f32")
+    os.environ["MPRKB_PULL"] = "1"
+    try:
+        pull = mp.Stepper("heat", n, t, 0.01, 1e-3, "f32")
+    finally:
+        os.environ.pop("MPRKB_PULL", None)
+    u0 = mp.heat_exact(n, 0.05)
+    a, b = u0.copy(), u0.copy()
+    for _ in range(2):
+        assert pull.step(a)["iterations"] == push.step(b)["iterations"]
+    assert same_bits(a, b)
+
+
+@pytest.mark.parametrize("value", [1e39, 3e38])
+def test_pull_form_errors_match_reference(gpu, mp, ref, value):
+    """Errors raised inside the push- and pull-form pipelines are the reference's, in
+    its order, and leave the state untouched: 1e39 overflows stage 0's
+    binary32 narrowing (OverflowToInfinity); 3e38 fits binary32 but the fp32
+    solve blows up, so a later check fires (the reference's own code)."""
+    from oracle.oracle import OracleError
+
+    t = mp.builtin("4s3pB")
+    n = 128
+    u = np.zeros(n ** 3)
+    u[(n // 2) * (n * n + n + 1)] = value
+    import os
+
+    rs = ref.stepper(0, n, tabd(t), 0.01, 1e-3, "f32")
+    with pytest.raises(OracleError) as e:
+        rs.step(u.copy())
+    for pull in ("0", "1"):
+        os.environ["MPRKB_PULL"] = pull
+        try:
+            st = mp.Stepper("heat", n, t, 0.01, 1e-3, "f32")
+        finally:
+            os.environ.pop("MPRKB_PULL", None)
+        v = u.copy()
+        with pytest.raises(mp.MprkError) as g:
+            st.step(v)
+        code = next(c for c, cls in mp._c._EXC.items() if type(g.value) is cls)
+        assert code == e.value.code, (pull, g.value, e.value.code)
+        assert np.array_equal(v, u)
