@@ -188,6 +188,13 @@ int mprkb_gmres(int dtype, size_t m, mprkb_op* op, mprkb_op* precond, const void
 int mprkb_gmres_ex(int dtype, size_t m, mprkb_op* op, mprkb_op* precond, const void* b, void* x,
                    double tol, int max_iter, int numerics, int basis_storage,
                    mprkb_solve_report* report, void* stream);
+/* cg with its work vectors r, z, p, q stored in `vec_storage` (-1 = dtype, as
+ * the reference; MPRKB_F16 under F32/F64, MPRKB_F32 under F64): every kernel
+ * reads the storage precision and computes in dtype (accessor-style
+ * extension; accessor.cu).  op: a heat stencil operator (undivided, n % 4 ==
+ * 0); precond: NULL or block-Jacobi; FAST numerics. */
+int mprkb_cg_ex(int dtype, size_t m, mprkb_op* op, mprkb_op* precond, const void* b, void* x, double tol,
+                int max_iter, int numerics, int vec_storage, mprkb_solve_report* report, void* stream);
 
 /* ---- coarse boundary: Stepper / integrate (stepper.hpp:20-99) --------------- */
 #define MPRKB_MAX_STAGES 16
@@ -211,6 +218,9 @@ typedef struct {
   int record_timings;      /* 1: CUDA-event brackets under the reference's labels       */
   int basis_storage;       /* GMRES Krylov-basis storage: -1 = working precision        */
                            /* (reference), MPRKB_F16 = fp16 basis, fp64 dots (extension) */
+  int krylov_storage;      /* CG vector storage (r, z, p, q): -1 = working precision    */
+                           /* (reference), MPRKB_F16, or MPRKB_F32 under F64 stages;     */
+                           /* heat + block-Jacobi / no preconditioner (extension)        */
 } mprkb_config;
 
 void mprkb_config_init(mprkb_config* cfg);

@@ -22,6 +22,14 @@ that have no reference counterpart; only tests/ import this.
   2 - 2cos(2 pi k / n)).
 * ``block_jacobi`` — x-line block-Jacobi with the inverse blocks rounded to
   the storage precision (the library's extension).
+* ``cg_storage`` — the reference's cg<T> (krylov.hpp:100-168, line by line)
+  with ONE change, the accessor-style extension under test: its work vectors
+  r, z, p, q are STORED through ``store`` (binary16 / binary32, RNE) and
+  widened exactly when read; x and b stay in T, vector arithmetic runs in T,
+  dots are fp64 sums of the stored values.  ``heat_apply`` is the reference's
+  Dirichlet KronSumOperator point arithmetic (operators.hpp:133-140) in T, and
+  ``BlockJacobiSeq`` the block apply with the GPU kernel's sequential sum
+  order (ext.cu / accessor.cu).
 """
 from __future__ import annotations
 
@@ -234,3 +242,113 @@ class BlockJacobi:
             Dinv = self.inv[bs].astype(self.R)
             Z[:, i0:i0 + bs] = (X[:, i0:i0 + bs] @ Dinv.T.astype(self.dtype)).astype(self.dtype)
         return Z.ravel()
+
+
+def heat_apply(x, n, sigma, gamma):
+    """sigma x + gamma (6 x - six Dirichlet neighbours) in x's dtype, the
+    reference's order of roundings (operators.hpp:133-140; numpy never fuses)."""
+    T = x.dtype.type
+    X = x.reshape(n, n, n)  # [k][j][i]
+    P = np.zeros((n + 2, n + 2, n + 2), dtype=x.dtype)
+    P[1:-1, 1:-1, 1:-1] = X
+    c = P[1:-1, 1:-1, 1:-1]
+    acc = T(6.0) * c
+    acc = acc - P[1:-1, 1:-1, :-2]
+    acc = acc - P[1:-1, 1:-1, 2:]
+    acc = acc - P[1:-1, :-2, 1:-1]
+    acc = acc - P[1:-1, 2:, 1:-1]
+    acc = acc - P[:-2, 1:-1, 1:-1]
+    acc = acc - P[2:, 1:-1, 1:-1]
+    return (T(sigma) * c + T(gamma) * acc).ravel()
+
+
+class BlockJacobiSeq(BlockJacobi):
+    """BlockJacobi with each output summed over the block's inputs in
+    ascending order in the compute precision (the kernels' order)."""
+
+    def __call__(self, r):
+        n, b = self.n, self.b
+        T = self.dtype.type
+        X = r.reshape(-1, n)
+        Z = np.zeros_like(X)
+        for i0 in range(0, n, b):
+            bs = min(b, n - i0)
+            D = self.inv[bs].astype(self.R)  # D[ii][jj] = inverse (row ii, column jj)
+            for ii in range(bs):
+                acc = np.zeros(X.shape[0], dtype=self.dtype)
+                for jj in range(bs):
+                    acc = acc + T(D[ii, jj]) * X[:, i0 + jj]
+                Z[:, i0 + ii] = acc
+        return Z.ravel()
+
+
+def cg_storage(op, precond, b, x0, tol, max_iter, store):
+    """krylov.hpp:100-168 with r, z, p, q stored through ``store`` (a function
+    rounding a T vector to the storage precision and widening it back);
+    precond None = identity.  Returns (x, report dict)."""
+    T = b.dtype.type
+    x = np.array(x0, dtype=b.dtype, copy=True)
+    hist = []
+
+    def dot(a, c):
+        return float(np.dot(a.astype(np.float64), c.astype(np.float64)))
+
+    def norm(sq):
+        return float(T(np.sqrt(T(sq))))
+
+    def satisfied(res, ref):  # StoppingCriterion::satisfied (krylov.hpp:21-23)
+        return res <= tol or (ref > 0 and res / ref <= tol)
+
+    def pre(r):
+        return r if precond is None else store(precond(r))
+
+    rep = dict(iterations=0, converged=False, failure=0)
+    r = store(b - op(x))
+    r_sq = dot(r, r)
+    r0 = norm(r_sq)
+    hist.append(r0)
+    rnorm = r0
+    if satisfied(rnorm, r0):
+        rep["converged"] = True
+    else:
+        z = pre(r)
+        p = z.copy()
+        rz = T(dot(r, z))
+        for _ in range(max_iter):
+            if not rz > 0:
+                rep["failure"] = 2
+                break
+            q = store(op(p))
+            pq = T(dot(p, q))
+            if not pq > 0:
+                rep["failure"] = 2
+                break
+            alpha = T(rz / pq)
+            x = x + alpha * p
+            r = store(r - alpha * q)
+            rep["iterations"] += 1
+            rnorm = norm(dot(r, r))
+            hist.append(rnorm)
+            if satisfied(rnorm, r0):
+                q = store(b - op(x))
+                rtnorm = norm(dot(q, q))
+                if satisfied(rtnorm, r0):
+                    rep["converged"] = True
+                    break
+                r = q
+                hist[-1] = rtnorm
+                z = pre(r)
+                p = z.copy()
+                rz = T(dot(r, z))
+                continue
+            z = pre(r)
+            rz_next = T(dot(r, z))
+            beta = T(rz_next / rz)
+            rz = rz_next
+            p = store(z + beta * p)
+        if not rep["converged"] and rep["failure"] == 0:
+            rep["failure"] = 1
+    q = b - op(x)
+    rep["true_residual"] = norm(dot(store(q), store(q)))
+    rep["history"] = np.array(hist)
+    return x, rep

@@ -191,7 +191,7 @@ def heat_exact(n: int, t: float) -> np.ndarray:
 
 
 def _config(tableau: Tableau, equation, n, tau, t_end, tol, precision, max_iter, numerics, preconditioner,
-            block_size, block_storage, nu, timings, basis_storage=None):
+            block_size, block_storage, nu, timings, basis_storage=None, krylov_storage=None):
     cfg = _c.Config()
     _c.lib.mprkb_config_init(C.byref(cfg))
     cfg.equation = _parse(_EQ, equation, "equation", "heat or advection")
@@ -214,6 +214,8 @@ def _config(tableau: Tableau, equation, n, tau, t_end, tol, precision, max_iter,
     cfg.nu = float(nu)
     cfg.record_timings = 1 if timings else 0
     cfg.basis_storage = _parse({None: -1, "f16": _c.F16}, basis_storage, "basis storage", "None or f16")
+    cfg.krylov_storage = _parse({None: -1, "f16": _c.F16, "f32": _c.F32}, krylov_storage, "krylov storage",
+                                "None, f16 or f32")
     return cfg, keep
 
 
@@ -234,9 +236,10 @@ class Stepper:
                  precision: str = "f64", max_iter: int = 40, *, t_end: float = 0.1, numerics: str = "fast",
                  preconditioner: str = "fastdiag", block_size: int = 8, block_storage: Optional[str] = None,
                  nu: float = 0.0, timings: bool = False, basis_storage: Optional[str] = None,
-                 comm: Optional["Comm"] = None):
+                 krylov_storage: Optional[str] = None, comm: Optional["Comm"] = None):
         cfg, keep = _config(tableau, equation, n, tau, t_end, tol, precision, max_iter, numerics,
-                            preconditioner, block_size, block_storage, nu, timings, basis_storage)
+                            preconditioner, block_size, block_storage, nu, timings, basis_storage,
+                            krylov_storage)
         self._h = C.c_void_p()
         self._comm = comm  # keeps the communicator alive as long as the stepper
         if comm is None:
@@ -635,9 +638,15 @@ def _krylov(fn, op: Operator, precond: Optional[Operator], b, x0, tol, max_iter,
 
 
 def cg(op: Operator, precond: Optional[Operator], b, x0, tol: float = 1e-6, max_iter: int = 40,
-       numerics: str = "fast"):
-    """cg<T>(op, precond, b, x0, crit, report) (krylov.hpp:100-168) -> (x, report)."""
-    return _krylov(_c.lib.mprkb_cg, op, precond, b, x0, tol, max_iter, numerics)
+       numerics: str = "fast", storage: Optional[str] = None):
+    """cg<T>(op, precond, b, x0, crit, report) (krylov.hpp:100-168) -> (x, report).
+    storage="f16" (or "f32" for float64 systems) keeps r, z, p, q in that
+    precision and computes in the system's (accessor-style extension:
+    heat stencil operator, block-Jacobi or no preconditioner)."""
+    if storage is None:
+        return _krylov(_c.lib.mprkb_cg, op, precond, b, x0, tol, max_iter, numerics)
+    code = _parse({"f16": _c.F16, "f32": _c.F32}, storage, "vector storage", "None, f16 or f32")
+    return _krylov(_c.lib.mprkb_cg_ex, op, precond, b, x0, tol, max_iter, numerics, extra=(code,))
 
 
 def gmres(op: Operator, precond: Optional[Operator], b, x0, tol: float = 1e-6, max_iter: int = 40,

@@ -102,7 +102,7 @@ class Config(C.Structure):
                 ("tol", C.c_double), ("implicit_precision", C.c_int), ("max_iter", C.c_int),
                 ("numerics", C.c_int), ("preconditioner", C.c_int), ("block_size", C.c_int),
                 ("block_storage", C.c_int), ("nu", C.c_double), ("record_timings", C.c_int),
-                ("basis_storage", C.c_int)]
+                ("basis_storage", C.c_int), ("krylov_storage", C.c_int)]
 
 
 class StepTrace(C.Structure):
@@ -161,6 +161,7 @@ SIGNATURES = {
     "mprkb_cg": (i32, [i32, sz, vp, vp, vp, vp, f64, i32, i32, C.POINTER(SolveReport), vp]),
     "mprkb_gmres": (i32, [i32, sz, vp, vp, vp, vp, f64, i32, i32, C.POINTER(SolveReport), vp]),
     "mprkb_gmres_ex": (i32, [i32, sz, vp, vp, vp, vp, f64, i32, i32, i32, C.POINTER(SolveReport), vp]),
+    "mprkb_cg_ex": (i32, [i32, sz, vp, vp, vp, vp, f64, i32, i32, i32, C.POINTER(SolveReport), vp]),
     "mprkb_config_init": (None, [C.POINTER(Config)]),
     "mprkb_stepper_create": (i32, [C.POINTER(Config), C.POINTER(vp)]),
     "mprkb_stepper_step": (i32, [vp, vp, C.POINTER(StepTrace)]),

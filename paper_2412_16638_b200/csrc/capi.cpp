@@ -10,6 +10,7 @@
 #include <string>
 
 #include "comm.hpp"
+#include "accessor.hpp"
 #include "krylov.hpp"
 #include "stepper.hpp"
 
@@ -97,6 +98,9 @@ StepperConfig config_of(const mprkb_config* c) {
   s.nu = c->nu;
   s.timings = c->record_timings != 0;
   s.basis_storage = c->basis_storage;
+  s.krylov_storage = c->krylov_storage;
+  if (s.krylov_storage != -1 && s.krylov_storage != MPRKB_F16 && s.krylov_storage != MPRKB_F32)
+    MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "krylov_storage must be -1, F16 or F32");
   if (s.basis_storage != -1 && s.basis_storage != MPRKB_F16)
     MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "basis storage must be -1 (working precision) or F16");
   return s;
@@ -452,6 +456,37 @@ int mprkb_gmres(int dtype, size_t m, mprkb_op* op, mprkb_op* precond, const void
   return krylov(false, dtype, m, op, precond, b, x, tol, max_iter, numerics, report, stream);
 }
 
+int mprkb_cg_ex(int dtype, size_t m, mprkb_op* op, mprkb_op* precond, const void* b, void* x, double tol,
+                int max_iter, int numerics, int vec_storage, mprkb_solve_report* report, void* stream) {
+  if (vec_storage == -1) return krylov(true, dtype, m, op, precond, b, x, tol, max_iter, numerics, report, stream);
+  return guarded([&] {
+    require_device();
+    if (dtype != MPRKB_F32 && dtype != MPRKB_F64) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "cg (vector storage): real F32 / F64 only");
+    if (!op) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "null operator");
+    if (op->op->size() != m || (precond && precond->op->size() != m))
+      MPRKB_THROW(MPRKB_LENGTH_MISMATCH, "cg: x0 length != b length");
+    if (op->op->dtype() != dtype || (precond && precond->op->dtype() != dtype))
+      MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "operator dtype != solve dtype");
+    const StencilSpec* A = op->op->stencil();
+    if (!A) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "cg (vector storage): the operator must be a stencil");
+    if (num_of(numerics) != Numerics::Fast) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "cg (vector storage): FAST numerics only");
+    const int sto = vec_storage == MPRKB_F16 ? 4 : vec_storage == MPRKB_F32 ? 0 : -2;
+    if (sto == -2 || (sto == 0 && dtype != MPRKB_F64))
+      MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "cg (vector storage): F16, or F32 under F64");
+    const Crit crit{tol, max_iter};
+    Op* P = precond ? precond->op.get() : nullptr;
+    SolveReport rep;
+    cudaStream_t st = S(stream);
+    AccWork w(m, sto);
+    if (dtype == MPRKB_F32)
+      cg_solve_acc<float>(*A, P, (const float*)b, (float*)x, crit, w, rep, st);
+    else
+      cg_solve_acc<double>(*A, P, (const double*)b, (double*)x, crit, w, rep, st);
+    stream_sync(st);
+    fill_report(rep, report);
+  });
+}
+
 int mprkb_gmres_ex(int dtype, size_t m, mprkb_op* op, mprkb_op* precond, const void* b, void* x, double tol,
                    int max_iter, int numerics, int basis_storage, mprkb_solve_report* report, void* stream) {
   return krylov(false, dtype, m, op, precond, b, x, tol, max_iter, numerics, report, stream, basis_storage);
@@ -469,6 +504,7 @@ void mprkb_config_init(mprkb_config* c) {
   c->preconditioner = MPRKB_PRECOND_FASTDIAG;
   c->block_size = 8;
   c->block_storage = -1;
+  c->krylov_storage = -1;
   c->nu = 0.0;
   c->basis_storage = -1;
 }

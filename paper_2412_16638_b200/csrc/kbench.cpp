@@ -136,9 +136,9 @@ void kernel_bench(const std::string& which, int n, int reps, double* ms, double*
     // x in + out (+ pd: the folded kernel scales its input, the unfolded its
     // output), flops reported by the caller as 2 n^4
     const bool fold = which.find("fold") != std::string::npos;
-    const char sd = which.back() == 'd' ? 'D' : which.back();
+    const bool diag = which.size() > 2 && which.compare(which.size() - 2, 2, "pd") == 0;
+    const char sd = which[which.size() - (diag ? 3 : 1)];
     const int side = sd == 'R' ? 2 : sd == 'M' ? 1 : 0;
-    const bool diag = sd == 'D';
     std::vector<double> q64, qi, lam;
     spectral_dirichlet(n, 1.0, 0.3, q64, qi, lam);
     std::vector<float> q(q64.begin(), q64.end());

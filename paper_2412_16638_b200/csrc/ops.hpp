@@ -38,6 +38,13 @@ class Op {
                                void* /*z*/, const RedSlot& /*red*/, cudaStream_t /*st*/) {
     return false;
   }
+  // Accessor-style apply (accessor.cu): z = P r with r and z stored in
+  // `storage` (4 fp16, 0 fp32, 1 fp64), arithmetic in the operator's dtype,
+  // red <- r.z of the stored values.  false: not available.
+  virtual bool apply_storage(const void* /*r*/, int /*storage*/, void* /*z*/, const RedSlot& /*red*/,
+                             cudaStream_t /*st*/) {
+    return false;
+  }
 
  protected:
   EventTimer* timer_ = nullptr;

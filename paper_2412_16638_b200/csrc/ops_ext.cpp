@@ -8,6 +8,7 @@
 #include <cstring>
 #include <vector>
 
+#include "accessor.hpp"
 #include "ops.hpp"
 
 namespace mprkb {
@@ -120,6 +121,13 @@ class BlockJacobiOp final : public Op {
       return cg_update_block_jacobi<T>(n_, b_, storage_, inv_.get(), (T)alpha, static_cast<T*>(x),
                                        static_cast<const T*>(p), static_cast<T*>(r), static_cast<const T*>(q),
                                        static_cast<T*>(z), red, st, lines_);
+    }
+    return false;
+  }
+  bool apply_storage(const void* r, int storage, void* z, const RedSlot& red, cudaStream_t st) override {
+    if constexpr (std::is_same_v<T, float> || std::is_same_v<T, double>) {
+      block_jacobi_acc<T>(n_, b_, storage_, inv_.get(), storage, r, z, red, st, lines_);
+      return true;
     }
     return false;
   }

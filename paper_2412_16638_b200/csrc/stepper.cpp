@@ -149,7 +149,7 @@ Stepper::Stepper(const StepperConfig& cfg)
     // stored f_hi vectors and a separate final update) — at most
     // kFevalMaxAcc in one pass.
     const char* env = std::getenv("MPRKB_FUSED_STAGES");
-    bool ok = !(env && env[0] == '0') && cfg_.eq == Equation::Heat && cfg_.f32 &&
+    bool ok = !(env && env[0] == '0') && cfg_.eq == Equation::Heat && cfg_.f32 && cfg_.krylov_storage < 0 &&
               q >= 2 && q - 2 <= kFevalMaxAcc && !prob_.forcing.empty() && feval_combine_supported(kspec_);
     for (int i = 0; i < q; ++i) ok = ok && t.ae(i, i) != 0.0 && t.ah(i, i) == 0.0;
     fused_ = ok;
@@ -199,6 +199,16 @@ Stepper::Stepper(const StepperConfig& cfg)
   if (!fused_) y_.alloc(m * sizeof(double));
   else if (!fuse_final_ && t.b[q - 1] == 0.0) y_.alloc(m * sizeof(double));
   gate_dev_.alloc(sizeof(int) * 256);
+  if (cfg_.krylov_storage >= 0) {
+    // accessor-style CG vectors (accessor.cu): heat, CG, FAST numerics, the
+    // undivided grid, identity or block-Jacobi preconditioner
+    if (cfg_.eq != Equation::Heat || cfg_.num != Numerics::Fast || cfg_.precond == 0 || !accessor_supported(kspec_))
+      MPRKB_THROW(10, "krylov_storage: needs heat, FAST numerics, block-Jacobi or no preconditioner, and the "
+                      "undivided grid with n % 4 == 0");
+    if (!(cfg_.krylov_storage == 4 || (cfg_.krylov_storage == 0 && !cfg_.f32)))
+      MPRKB_THROW(10, "krylov_storage: fp16, or fp32 under fp64 stages");
+    acc_work_ = std::make_unique<AccWork>(m, cfg_.krylov_storage);
+  }
   if (!solvers_.empty()) {
     const size_t s = dtype_size(solve_dtype_);
     bsol_.alloc(m * s);
@@ -291,12 +301,23 @@ void Stepper::step(double* u, StepTrace& trace) {
       float* sol32 = xsol_.as<float>();
       switch (solve_dtype_) {
         case 0:
+          if (acc_work_) {  // accessor-style CG vectors: x0 = rhs copied into the solution buffer
+            CUDA_CHECK(cudaMemcpyAsync(xsol_.get(), bsol_.get(), m * sizeof(float), cudaMemcpyDeviceToDevice, st_));
+            cg_solve_acc<float>(*S.op->stencil(), S.pre.get(), bsol_.as<float>(), xsol_.as<float>(), crit,
+                                *acc_work_, rep, st_, tm);
+            break;
+          }
           // x0 = rhs in place (b is never written); the solution lands in xsol_
           cg_solve<float>(*S.op, S.pre.get(), bsol_.as<float>(), bsol_.as<float>(), crit, cfg_.num, *w32_, rep, st_,
                           tm, xsol_.as<float>(), &sol32);
           break;
         case 1:
-          cg_solve<double>(*S.op, S.pre.get(), bsol_.as<double>(), xsol_.as<double>(), crit, cfg_.num, *w64_, rep, st_, tm);
+          if (acc_work_)
+            cg_solve_acc<double>(*S.op->stencil(), S.pre.get(), bsol_.as<double>(), xsol_.as<double>(), crit,
+                                 *acc_work_, rep, st_, tm);
+          else
+            cg_solve<double>(*S.op, S.pre.get(), bsol_.as<double>(), xsol_.as<double>(), crit, cfg_.num, *w64_, rep,
+                             st_, tm);
           break;
         case 2:
           gmres_solve<c32>(*S.op, S.pre.get(), bsol_.as<c32>(), xsol_.as<c32>(), crit, cfg_.num, *wc32_, rep, st_, tm, cfg_.basis_storage);

@@ -7,6 +7,7 @@
 #include <optional>
 #include <vector>
 
+#include "accessor.hpp"
 #include "krylov.hpp"
 #include "problem.hpp"
 
@@ -26,6 +27,7 @@ struct StepperConfig {
   double nu = 0.0;
   bool timings = false;
   int basis_storage = -1;  // GMRES basis storage (-1: working precision; 4: fp16)
+  int krylov_storage = -1;  // CG vector storage (-1: working precision; 4: fp16; 0: fp32 under fp64) — accessor.cu
   // Split grid: this rank steps k-planes [rank n/P, (rank+1) n/P)
   // and exchanges halos / transposes / scalars through comm (null: undivided).
   Comm* comm = nullptr;
@@ -65,6 +67,7 @@ class Stepper {
   void step_pull(double* u, StepTrace& trace);
   bool pull_ = false;
   std::vector<DevBuf> ys_;  // pull form: stage i's solution (fp32)
+  std::unique_ptr<AccWork> acc_work_;  // CG vectors in krylov_storage (accessor.cu)
   void add_forcing(CombineTerms& t, double coef) const;  // + coef g (regenerated or read)
   bool fused_ = false;
   bool fuse_final_ = false;  // fused pipeline also accumulates the final update (decided at construction)

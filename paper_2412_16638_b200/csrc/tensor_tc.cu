@@ -376,12 +376,30 @@ constexpr int TF_Q = TF_BM * TF_KH * 4;             // 8 KB per {even, odd} x {h
 // Three decoupled rings: raw X (+ pd) tiles, released by the converters as
 // soon as they are read, so the TMA runs up to RS k-blocks ahead; the packed
 // Q tiles (L2-resident), released by the MMA; the split X hi/lo operands.
+#ifndef TF_RS_N
+#define TF_RS_N 5  // raw ring depth (X only)
+#endif
+#ifndef TF_RS_P
+#define TF_RS_P 2  // raw ring depth (X + pd)
+#endif
+#ifndef TF_QS
+#define TF_QS 2
+#endif
+#ifndef TF_CS
+#define TF_CS 2
+#endif
+#ifndef TF_CS_P
+#define TF_CS_P TF_CS
+#endif
+#ifndef TF_EB
+#define TF_EB 1  // epilogue staging blocks per warp
+#endif
 template <bool PDIN>
 struct TfCfg {
   static constexpr int RAWB = TF_RAW * (PDIN ? 2 : 1);
-  static constexpr int RS = PDIN ? 2 : 5;  // raw ring
-  static constexpr int QS = 2;             // Q ring
-  static constexpr int CS = 2;             // converted ring
+  static constexpr int RS = PDIN ? TF_RS_P : TF_RS_N;  // raw ring
+  static constexpr int QS = TF_QS;                     // Q ring
+  static constexpr int CS = PDIN ? TF_CS_P : TF_CS;    // converted ring
 };
 
 template <bool PDIN>
@@ -392,7 +410,7 @@ struct TfSmem {
   alignas(1024) unsigned char x[Cfg::CS][4 * TF_X];
   // epilogue: per epilogue warp one 32x32 fp32 staging block (128B-swizzled
   // rows), drained by a TMA tensor store
-  alignas(1024) float stagec[4][1][32 * 32];
+  alignas(1024) float stagec[4][TF_EB][32 * 32];
   alignas(8) uint64_t rawfull[Cfg::RS];
   alignas(8) uint64_t rawfree[Cfg::RS];
   alignas(8) uint64_t qfull[Cfg::QS];
@@ -726,9 +744,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tmem_ld32(lanebase + 128u + (uint32_t)cc, o);
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
-          const uint32_t sb = smem_u32(S.stagec[q4][0]);
-          // the previous block's store must have read the staging buffer
-          if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          const uint32_t sb = smem_u32(S.stagec[q4][TF_EB > 1 ? half : 0]);
+          // the store that last used this staging buffer must have read it
+          if (lane == 0) {
+            if (TF_EB > 1)
+              asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            else
+              asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          }
           __syncwarp();
           if (SIDE == 2) {
             // block [32 fibres][32 a]: row j = fibre, column = a (lane; reversed for n-1-a)

@@ -91,3 +91,40 @@ def test_block_jacobi_np_matches_reference_cg(ref):
     b = np.random.default_rng(1).uniform(-1, 1, n ** 3)
     x, r = ref.stage_solve_cb(1, 0, n, tau, a, bj, b, b, 1e-8, 200)
     assert r["converged"] and r["iterations"] > 1
+
+
+def test_cg_storage_restatement_matches_reference_cg(ref):
+    """oracle/krylov_np.cg_storage without storage rounding IS the reference's
+    cg<double> (krylov.hpp:100-168): same iterations and iterate, with the
+    numpy heat stencil and the sequential block-Jacobi in the ApplyFn slots."""
+    from oracle.krylov_np import BlockJacobiSeq, cg_storage, heat_apply
+
+    n, tau, a = 16, 0.01, 0.5
+    h = 1.0 / (n - 1)
+    s, g = 1.0, -tau * a * (-1.0 / h ** 2)
+    op = lambda v: heat_apply(v, n, s, g)  # noqa: E731
+    bj = BlockJacobiSeq(n, 4, s, g, "f32", np.float64)
+    b = np.random.default_rng(3).uniform(-1, 1, n ** 3)
+    for pre in (bj, None):
+        xw, rw = ref.krylov_cb(1, 0, op, pre, b, np.zeros_like(b), 1e-9, 300)
+        xo, ro = cg_storage(op, pre, b, np.zeros_like(b), 1e-9, 300, store=lambda v: v)
+        assert rw["converged"] and ro["converged"]
+        assert abs(ro["iterations"] - rw["iterations"]) <= 1, (ro["iterations"], rw["iterations"])
+        assert np.linalg.norm(xo - xw) <= 1e-8 * np.linalg.norm(xw)
+        assert abs(ro["true_residual"] - rw["true_residual"]) <= 1e-6 * np.linalg.norm(b)
+
+
+def test_cg_storage_fp16_converges_to_its_floor():
+    """fp16 vector storage under fp32 compute: CG still reaches tol 1e-3 at
+    n = 16 (the fp16 rounding floor of the recurrence is ~1e-3 relative)."""
+    from oracle.krylov_np import BlockJacobiSeq, cg_storage, heat_apply, round16
+
+    n, tau, a = 16, 0.01, 0.5
+    h = 1.0 / (n - 1)
+    s, g = np.float32(1.0), np.float32(-tau * a * (-1.0 / h ** 2))
+    op = lambda v: heat_apply(v, n, s, g)  # noqa: E731
+    bj = BlockJacobiSeq(n, 8, s, g, "f16", np.float32)
+    b = np.random.default_rng(4).uniform(-1, 1, n ** 3).astype(np.float32)
+    x, r = cg_storage(op, bj, b, np.zeros_like(b), 1e-3, 200, store=round16)
+    assert r["converged"] and r["iterations"] > 3
+    assert r["true_residual"] <= 2e-3 * np.linalg.norm(b)
