@@ -442,7 +442,33 @@ def config1_variants(mp, torch, steps=3):
         out[key] = {"ms_per_step": ms, "value": N_GRID ** 3 / (ms * 1e-3), "unit": "DOF-updates/s",
                     "iterations_per_solve": its, "tol": tol, "steps": steps, "note": note}
         del st
+    out["fp64_baseline_stepper"]["contraction"] = fp64_contraction_roofline(mp)
     return out
+
+
+def fp64_contraction_roofline(mp, reps=10):
+    """The fp64 stepper's dominant kernel, the sine-folded FastDiag
+    contraction on the FP64 tensor cores (k_tensor_dmma, mma.sync m16n8k8
+    .f64), timed alone per side at 256^3 against the measured DMMA peak
+    (csrc/peak.cu): n N / 2 executed FMAs = n N flop per launch (the fold
+    halves the 2 n N algorithmic flop).  The CUDA-core DFMA peak is
+    reported beside it (the DFMA kernel it replaced: profiles/r02)."""
+    import ctypes as C
+
+    peak = mp_fma_peak(mp, 2)
+    dfma_peak = mp_fma_peak(mp, 1)
+    n = N_GRID
+    flop = float(n) * n ** 3  # folded: n/2 rows x n q per output pair = n N / 2 FMAs = n N flop
+    sides = {}
+    for sd in "RML":
+        ms, by = C.c_double(), C.c_double()
+        mp.check(mp._c.lib.mprkb_kernel_bench(f"tensor_f64_{sd}".encode(), n, reps, C.byref(ms), C.byref(by)))
+        tf = flop / (ms.value * 1e-3) / 1e12
+        sides[sd] = {"us": round(ms.value * 1e3, 2), "executed_tflops": round(tf, 2), "frac": round(tf / peak, 3)}
+    return {"kernel": "k_tensor_dmma (sine-folded fp64 GEMM on the FP64 tensor cores, mma.sync m16n8k8)",
+            "bound": "fp64 tensor (DMMA)", "peak_tflops": round(peak, 2),
+            "peak_source": "csrc/peak.cu independent DMMA chains, one wave, measured here",
+            "dfma_peak_tflops": round(dfma_peak, 2), "executed_flop_per_launch": flop, "sides": sides}
 
 
 KERNELS = ["copy_f32", "stencil_f64", "stencil_f32", "residual_f32", "apply_dot_f32", "dots2_f32", "cg_fused_f32",

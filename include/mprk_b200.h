@@ -73,8 +73,10 @@ int mprkb_stream_synchronize(void* stream);
 int mprkb_device_synchronize(void);
 /* Number of kernels this library has launched since load (instrumentation). */
 long long mprkb_kernel_launches(void);
-/* Measured CUDA-core FMA throughput (TFLOP/s) for F32 or F64: the roofline
- * denominator of the FastDiag contractions (instrumentation). */
+/* Measured FMA throughput (TFLOP/s): CUDA-core F32 or F64, or
+ * MPRKB_PEAK_DMMA = the FP64 tensor cores (mma.sync m16n8k8 .f64) — the
+ * roofline denominators of the FastDiag contractions (instrumentation). */
+#define MPRKB_PEAK_DMMA 2
 int mprkb_measure_fma_peak(int dtype, double* tflops);
 /* Roofline helper: time one HBM-bound kernel of the step alone on n^3
  * vectors (CUDA events, `reps` back-to-back launches after warm-up) and

@@ -851,7 +851,8 @@ extern "C" int mprkb_kernel_bench(const char* which, int n, int reps, double* ms
 extern "C" int mprkb_measure_fma_peak(int dtype, double* tflops) {
   return guarded([&] {
     require_device();
-    if (dtype != MPRKB_F32 && dtype != MPRKB_F64) MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "dtype must be F32 or F64");
+    if (dtype != MPRKB_F32 && dtype != MPRKB_F64 && dtype != MPRKB_PEAK_DMMA)
+      MPRKB_THROW(MPRKB_INVALID_ARGUMENT, "dtype must be F32, F64 or MPRKB_PEAK_DMMA");
     *tflops = mprkb::fma_peak_tflops(dtype);
   });
 }

@@ -131,6 +131,18 @@ void kernel_bench(const std::string& which, int n, int reps, double* ms, double*
   } else if (which == "csr_f16") {
     auto op = make_csr_stencil(0, sp, 4);
     t = time_it(st, reps, (8 + 7 * (2 + 4) + 4) * D, [&] { op->apply(f32(0), f32(1), st); });
+  } else if (which.rfind("tensor_f64_", 0) == 0) {
+    // fp64 FastDiag contraction on CUDA cores (sine-folded DFMA GEMM, FAST):
+    // tensor_f64_{R,M,L}; bytes = x in + out; the caller derives flops (n^4 folded FMAs)
+    const char sd = which.back();
+    const int side = sd == 'R' ? 2 : sd == 'M' ? 1 : 0;
+    std::vector<double> q64, qi, lam;
+    spectral_dirichlet(n, 1.0, 0.3, q64, qi, lam);
+    DevBuf qd(q64.size() * 8);
+    CUDA_CHECK(cudaMemcpy(qd.get(), q64.data(), q64.size() * 8, cudaMemcpyHostToDevice));
+    t = time_it(st, reps, 16 * D, [&] {
+      tensor_apply<double>(side, n, qd.as<double>(), f64(0), f64(1), nullptr, Numerics::Fast, st, 2);
+    });
   } else if (which.rfind("tc_", 0) == 0) {
     // FastDiag contractions on tcgen05: tc_{fold,split}_{R,M,L,Lpd}; bytes =
     // x in + out (+ pd: the folded kernel scales its input, the unfolded its

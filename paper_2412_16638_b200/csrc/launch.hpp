@@ -130,7 +130,7 @@ void stage_pull(const StencilSpec& k, const StagePull& p, cudaStream_t st);
 // column stride n * ny).
 template <class T>
 void tensor_apply(int side, int n, const T* q, const T* x, T* out, const T* pd, Numerics num,
-                  cudaStream_t st, bool fold = false, long cols = 0);
+                  cudaStream_t st, int fold = 0, long cols = 0);
 // Tensor-core (tcgen05, 3xTF32) contraction for fp32, FAST numerics
 // (tensor_tc.cu).  q_{hi,lo}_packed: Q split into tf32 hi/lo parts and packed
 // by pack_tf32_split() into the canonical UMMA K-major layout.

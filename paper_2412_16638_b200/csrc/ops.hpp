@@ -95,7 +95,7 @@ class FastDiagOp final : public Op {
   const Halo* halo_ = nullptr;
   int P_ = 1, nz_ = 0, ny_ = 0;
   bool tc_split_ = false;  // tensor cores usable on both slab layouts
-  bool fold_[6] = {false, false, false, false, false, false};  // sine symmetry per factor
+  int fold_[6] = {0, 0, 0, 0, 0, 0};  // sine symmetry per factor (1: Q[n-1-a][q] = (-1)^q Q[a][q])
   bool tc_ = false;  // fp32 FAST: tensor-core (3xTF32) contractions
   DevBuf q_[6];  // qa, qa_inv, qb, qb_inv, qc, qc_inv
   DevBuf qhp_[6], qlp_[6];  // tf32 hi/lo split, UMMA-packed (tc_ only; folded: qhp_ holds all four blocks)

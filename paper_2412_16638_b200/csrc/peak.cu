@@ -20,6 +20,34 @@ __global__ void __launch_bounds__(256) k_fma_peak(T* out, int iters, T a, T b) {
   if (s == (T)123.456) out[0] = s;  // keep the chains alive
 }
 
+// FP64 tensor cores: independent m16n8k8 DMMA chains (the fp64 FastDiag
+// contraction's roofline, tensor.cu k_tensor_dmma); 1024 FMAs per instruction
+__global__ void __launch_bounds__(256) k_dmma_peak(double* out, int iters) {
+  double a[4], b[2], c[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) a[i] = threadIdx.x * 1e-3 + i;
+  b[0] = 1.0;
+  b[1] = 1.0001;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) c[i][j] = i + j;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      asm volatile(
+          "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+          : "+d"(c[i][0]), "+d"(c[i][1]), "+d"(c[i][2]), "+d"(c[i][3])
+          : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) s += c[i][j];
+  if (s == 123.456) out[0] = s;
+}
+
 double fma_peak_tflops(int dtype) {
   const int blocks = sm_count() * 4, threads = 256, iters = dtype == 0 ? 1 << 16 : 1 << 14;
   void* out = nullptr;
@@ -32,8 +60,10 @@ double fma_peak_tflops(int dtype) {
     CUDA_CHECK(cudaEventRecord(a));
     if (dtype == 0)
       k_fma_peak<float><<<blocks, threads>>>((float*)out, iters, 0.9999f, 1e-7f);
-    else
+    else if (dtype == 1)
       k_fma_peak<double><<<blocks, threads>>>((double*)out, iters, 0.9999, 1e-7);
+    else
+      k_dmma_peak<<<blocks, threads>>>((double*)out, iters / 4);
     LAUNCHED("fma_peak");
     CUDA_CHECK(cudaEventRecord(b));
     CUDA_CHECK(cudaEventSynchronize(b));
@@ -44,7 +74,8 @@ double fma_peak_tflops(int dtype) {
   cudaEventDestroy(a);
   cudaEventDestroy(b);
   cudaFree(out);
-  const double flops = 2.0 * 8.0 * (double)iters * blocks * threads;
+  const double flops = dtype == 2 ? 2.0 * 1024.0 * 4.0 * (double)(iters / 4) * blocks * (threads / 32)
+                                  : 2.0 * 8.0 * (double)iters * blocks * threads;
   return flops / (best * 1e-3) / 1e12;
 }
 

@@ -17,6 +17,8 @@
 //                  writes C[a] = E + O, C[n-1-a] = E - O — half the FLOPs.
 // Zero-filled K padding is harmless: an accumulator started at +0 never
 // becomes -0, so adding +-0 leaves it unchanged.
+#include <cstdlib>
+
 #include "launch.hpp"
 #include "vec.cuh"
 
@@ -338,11 +340,195 @@ void launch_fast(int side, int n, long cols, const T* q, const T* x, T* out, con
     launch_fast_cfg<T, 64, 64, 16, 4, 4, DIAG, FOLD>(side, n, cols, q, x, out, pd, st);
 }
 
+// ---------------------------------------------------------------------------
+// fp64 on the FP64 tensor cores (DMMA, mma.sync m16n8k8 .f64).  The CUDA-core
+// DFMA GEMM above tops out near half the DFMA peak (every FMA reads three
+// register operands: register-file bound, ncu fp64 pipe ~46 %); one DMMA
+// instruction performs 1024 FMAs from 6 fragment registers, and the measured
+// DMMA rate is 37 TFLOP/s (profiles/r02/dmma_peak.txt).  Same sine-folded
+// arithmetic as k_tensor_fast<double, FOLD>: E / O sums over even / odd q,
+// C[a] = E + O, C[n-1-a] = E - O; each BK = 16 block of K is stored
+// de-interleaved in shared memory (even q in k-slots 0-7, odd q in 8-15) so
+// E and O are one m16n8k8 step each.  CTA 64 x 64 (4 warps of 32 x 32: 2 x 4
+// m16n8 tiles, E and O accumulators = 64 fp64 per thread), register-prefetched
+// double-buffered tiles as in k_tensor_fast.
+// Fragments (PTX m16n8k8 .f64, g = lane / 4, t = lane % 4):
+//   A (16 x 8, row): a0 (g, t), a1 (g+8, t), a2 (g, t+4), a3 (g+8, t+4)
+//   B (8 x 8, col):  b0 (t, g), b1 (t+4, g)
+//   C (16 x 8):      c0 (g, 2t), c1 (g, 2t+1), c2 (g+8, 2t), c3 (g+8, 2t+1)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void dmma16808(double (&c)[4], const double (&a)[4], const double (&b)[2]) {
+  asm volatile("mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+               : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+               : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
+}
+
+template <bool RIGHT, bool DIAG>
+__global__ void __launch_bounds__(128, 2)
+    k_tensor_dmma(const double* __restrict__ Q, const double* __restrict__ X, double* __restrict__ C,
+                  const double* __restrict__ pd, int n, long Mdim, long Ndim, long ldx, long bstride) {
+  constexpr int BM = 64, BN = 64, BK = 16, NT = 128, PAD = 4;
+  constexpr int ACH = BM * BK / 4 / NT, BCH = BN * BK / 4 / NT;  // 2, 2
+  __shared__ __align__(16) double As[2][BK][BM + PAD];
+  __shared__ __align__(16) double Bs[2][BK][BN + PAD];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp >> 1) * 32, wn = (warp & 1) * 32;  // warp tile origin
+  const long m0 = (long)blockIdx.y * BM;
+  const long c0 = (long)blockIdx.x * BN;
+  const long boff = (long)blockIdx.z * bstride;
+  // de-interleaved k slot of element k (k0 even): even q -> 0..7, odd q -> 8..15
+  auto kslot = [](int kk) { return (kk & 1) * (BK / 2) + (kk >> 1); };
+
+  double acc[2][2][4][4];  // [E/O][mi][ni][c]
+#pragma unroll
+  for (int p = 0; p < 2; ++p)
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[p][i][j][e] = 0.0;
+
+  V4<double> ra[ACH], rb[BCH];
+  auto load_a = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < ACH; ++i) {
+      const int c = tid + i * NT;
+      const int row = c / (BK / 4), kq = (c % (BK / 4)) * 4;
+      const long m = m0 + row;
+      const int k = k0 + kq;
+      ra[i] = (m < Mdim && k < n) ? ld4(RIGHT ? X + boff + m * n + k : Q + m * n + k) : zero4<double>();
+    }
+  };
+  auto load_b = [&](int k0) {
+#pragma unroll
+    for (int i = 0; i < BCH; ++i) {
+      const int c = tid + i * NT;
+      if (RIGHT) {  // B[q][a] = Q[a][q]
+        const int col = c / (BK / 4), kq = (c % (BK / 4)) * 4;
+        const long a = c0 + col;
+        const int k = k0 + kq;
+        rb[i] = (a < Ndim && k < n) ? ld4(Q + a * n + k) : zero4<double>();
+      } else {  // B[q][c] = X[q][c]
+        const int row = c / (BN / 4), col = (c % (BN / 4)) * 4;
+        const int k = k0 + row;
+        const long cc = c0 + col;
+        rb[i] = (k < n && cc < Ndim) ? ld4(X + boff + (long)k * ldx + cc) : zero4<double>();
+      }
+    }
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int i = 0; i < ACH; ++i) {
+      const int c = tid + i * NT;
+      const int row = c / (BK / 4), kq = (c % (BK / 4)) * 4;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) As[buf][kslot(kq + e)][row] = ra[i].x[e];
+    }
+#pragma unroll
+    for (int i = 0; i < BCH; ++i) {
+      const int c = tid + i * NT;
+      if (RIGHT) {
+        const int col = c / (BK / 4), kq = (c % (BK / 4)) * 4;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) Bs[buf][kslot(kq + e)][col] = rb[i].x[e];
+      } else {
+        const int row = c / (BN / 4), col = (c % (BN / 4)) * 4;
+        st4(&Bs[buf][kslot(row)][col], rb[i]);
+      }
+    }
+  };
+
+  load_a(0);
+  load_b(0);
+  store(0);
+  __syncthreads();
+  int buf = 0;
+  for (int k0 = 0; k0 < n; k0 += BK) {
+    const bool more = k0 + BK < n;
+    if (more) {
+      load_a(k0 + BK);
+      load_b(k0 + BK);
+    }
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {  // E (even q) then O (odd q): k-slots 8p .. 8p+7
+      const int ks = p * (BK / 2);
+      double af[2][4], bf[4][2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int r = wm + i * 16 + g;
+        af[i][0] = As[buf][ks + t][r];
+        af[i][1] = As[buf][ks + t][r + 8];
+        af[i][2] = As[buf][ks + t + 4][r];
+        af[i][3] = As[buf][ks + t + 4][r + 8];
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int cn = wn + j * 8 + g;
+        bf[j][0] = Bs[buf][ks + t][cn];
+        bf[j][1] = Bs[buf][ks + t + 4][cn];
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma16808(acc[p][i][j], af[i], bf[j]);
+    }
+    if (more) {
+      store(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+  // epilogue: rows (LEFT) / columns (RIGHT) a and n-1-a from the parity sums
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const long m = m0 + wm + i * 16 + g + (e >> 1) * 8;
+        const long c = c0 + wn + j * 8 + 2 * t + (e & 1);
+        if (m >= Mdim || c >= Ndim) continue;
+        const double ev = acc[0][i][j][e], od = acc[1][i][j][e];
+        const long qa = RIGHT ? c : m, qb = n - 1 - qa;
+        const long o1 = RIGHT ? m * n + qa : boff + qa * ldx + c;
+        const long o2 = RIGHT ? m * n + qb : boff + qb * ldx + c;
+        double v1 = ev + od;
+        if (DIAG) v1 *= ldg(pd + o1);
+        C[o1] = v1;
+        if (qb != qa) {
+          double v2 = ev - od;
+          if (DIAG) v2 *= ldg(pd + o2);
+          C[o2] = v2;
+        }
+      }
+}
+
+template <bool DIAG>
+void launch_dmma(int side, int n, long cols, const double* q, const double* x, double* out, const double* pd,
+                 cudaStream_t st) {
+  constexpr int BM = 64, BN = 64;
+  const long nn = n, n2 = nn * nn;
+  const long nq = (nn + 1) / 2;  // folded rows of Q
+  if (side == 2) {
+    dim3 grid((unsigned)((nq + BN - 1) / BN), (unsigned)((cols + BM - 1) / BM), 1);
+    k_tensor_dmma<true, DIAG><<<grid, 128, 0, st>>>(q, x, out, pd, n, cols, nq, nn, 0);
+  } else if (side == 1) {
+    dim3 grid((unsigned)((nn + BN - 1) / BN), (unsigned)((nq + BM - 1) / BM), (unsigned)(cols / nn));
+    k_tensor_dmma<false, DIAG><<<grid, 128, 0, st>>>(q, x, out, pd, n, nq, nn, nn, n2);
+  } else {
+    dim3 grid((unsigned)((cols + BN - 1) / BN), (unsigned)((nq + BM - 1) / BM), 1);
+    k_tensor_dmma<false, DIAG><<<grid, 128, 0, st>>>(q, x, out, pd, n, nq, cols, cols, 0);
+  }
+  LAUNCHED("tensor_dmma");
+}
+
 }  // namespace
 
 template <class T>
 void tensor_apply(int side, int n, const T* q, const T* x, T* out, const T* pd, Numerics num, cudaStream_t st,
-                  bool fold, long cols) {
+                  int fold, long cols) {
   if (cols <= 0) cols = (long)n * n;
   if (num == Numerics::Parity) {
     if (pd)
@@ -350,6 +536,18 @@ void tensor_apply(int side, int n, const T* q, const T* x, T* out, const T* pd, 
     else
       launch_generic<T, true, false>(side, n, cols, q, x, out, pd, st);
     return;
+  }
+  if constexpr (std::is_same_v<T, double>) {
+    // fp64 sine-folded contractions on the FP64 tensor cores (MPRKB_DMMA=0:
+    // the CUDA-core DFMA kernel below)
+    static const bool dmma_on = [] {
+      const char* e = std::getenv("MPRKB_DMMA");
+      return !(e && e[0] == '0');
+    }();
+    if (fold && n % 16 == 0 && n >= 64 && dmma_on) {
+      if (pd) return launch_dmma<true>(side, n, cols, q, x, out, pd, st);
+      return launch_dmma<false>(side, n, cols, q, x, out, pd, st);
+    }
   }
   if constexpr (!is_cplx<T>) {
     if (n % 4 == 0 && n >= 64) {
@@ -367,9 +565,9 @@ void tensor_apply(int side, int n, const T* q, const T* x, T* out, const T* pd, 
     launch_generic<T, false, false>(side, n, cols, q, x, out, pd, st);
 }
 
-template void tensor_apply<float>(int, int, const float*, const float*, float*, const float*, Numerics, cudaStream_t, bool, long);
-template void tensor_apply<double>(int, int, const double*, const double*, double*, const double*, Numerics, cudaStream_t, bool, long);
-template void tensor_apply<c32>(int, int, const c32*, const c32*, c32*, const c32*, Numerics, cudaStream_t, bool, long);
-template void tensor_apply<c64>(int, int, const c64*, const c64*, c64*, const c64*, Numerics, cudaStream_t, bool, long);
+template void tensor_apply<float>(int, int, const float*, const float*, float*, const float*, Numerics, cudaStream_t, int, long);
+template void tensor_apply<double>(int, int, const double*, const double*, double*, const double*, Numerics, cudaStream_t, int, long);
+template void tensor_apply<c32>(int, int, const c32*, const c32*, c32*, const c32*, Numerics, cudaStream_t, int, long);
+template void tensor_apply<c64>(int, int, const c64*, const c64*, c64*, const c64*, Numerics, cudaStream_t, int, long);
 
 }  // namespace mprkb
