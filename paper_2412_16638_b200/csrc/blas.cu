@@ -235,6 +235,46 @@ void cg_update(size_t m, real_t<T> alpha, T* x, const T* p, T* r, const T* q, co
   LAUNCHED("cg_update");
 }
 
+// ---- CG device loop: the host's scalar steps on the device (krylov.cpp) -------------
+// One CTA of kRedLanes threads; every value is formed exactly as the host forms
+// it from the same tuples (Reducer::result's order, (float) casts, IEEE
+// division and square root), so the iterates equal the host-driven loop's.
+__global__ void __launch_bounds__(kRedLanes) k_cg_ctl(CgCtl* ctl, const double* utup, int un, int rcomp, int rzcomp,
+                                                    const double* ptup, int pn) {
+  pdl_wait();
+  pdl_trigger();
+  if (ctl->stop) return;
+  const double rsq = sum_partials(utup, un, rcomp);
+  const double rzs = sum_partials(utup, un, rzcomp);
+  const double pqs = sum_partials(ptup, pn, 0);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const double rnorm = (double)sqrtf(__double2float_rn(rsq));
+  const int it = ctl->iters;
+  if (it < CgCtl::kMaxBatch) ctl->hist[it] = rnorm;
+  ctl->iters = it + 1;
+  const float rz = __double2float_rn(rzs), pq = __double2float_rn(pqs);
+  ctl->rz = rz;
+  ctl->pq = pq;
+  const double tol = ctl->tol, r0 = ctl->r0;
+  if (rnorm <= tol || (r0 > 0 && rnorm / r0 <= tol)) {  // StoppingCriterion::satisfied
+    ctl->stop = 1;
+  } else if (!(rz > 0.0f)) {
+    ctl->stop = 2;
+  } else if (!(pq > 0.0f)) {
+    ctl->stop = 3;
+  } else {
+    ctl->alpha = __fdiv_rn(rz, pq);
+  }
+}
+
+void cg_ctl_step(CgCtl* ctl, const RedSlot& upd, int rcomp, int rzcomp, const RedSlot& pq, cudaStream_t st) {
+  if (!upd.dpart || !pq.dpart) MPRKB_THROW(10, "cg_ctl_step: the reductions need device tuples");
+  launch_pdl(k_cg_ctl, dim3(1), dim3(kRedLanes), 0, st, ctl, (const double*)upd.dpart, *upd.count, rcomp, rzcomp,
+             (const double*)pq.dpart, *pq.count);
+  LAUNCHED("cg_ctl");
+}
+
 // p = z + beta p   (krylov.hpp:158)
 template <class T>
 __global__ void __launch_bounds__(kBlock) k_xpby(size_t m, const T* z, real_t<T> beta, T* p) {

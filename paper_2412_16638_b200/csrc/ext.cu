@@ -182,10 +182,14 @@ template <class T, class S, int B>
 __global__ void __launch_bounds__(128) k_cg_update_bj(long blocks, real_t<T> alpha, T* __restrict__ x,
                                                       const T* __restrict__ p, T* __restrict__ r,
                                                       const T* __restrict__ q, const S* __restrict__ inv,
-                                                      T* __restrict__ z, RedSlot red) {
+                                                      T* __restrict__ z, RedSlot red, const CgCtl* ctl) {
   pdl_wait();
   pdl_trigger();
   using R = real_t<T>;
+  if (ctl) {  // device loop: alpha from the control block; no-op once stopped
+    if (ctl->stop) return;
+    alpha = (R)ctl->alpha;
+  }
   double acc2[2] = {0.0, 0.0};
   for (long blk = blockIdx.x * (long)blockDim.x + threadIdx.x; blk < blocks; blk += (long)gridDim.x * blockDim.x) {
     const long o = blk * B;
@@ -239,7 +243,7 @@ __global__ void __launch_bounds__(128) k_cg_update_bj(long blocks, real_t<T> alp
 }
 
 template <class T, class S>
-bool cg_bj(int n, long lines, int b, real_t<T> alpha, T* x, const T* p, T* r, const T* q, const S* inv, T* z,
+bool cg_bj(int n, long lines, int b, real_t<T> alpha, const CgCtl* ctl, T* x, const T* p, T* r, const T* q, const S* inv, T* z,
            const RedSlot& red, cudaStream_t st) {
   if constexpr (is_cplx<T>) {
     return false;
@@ -248,10 +252,10 @@ bool cg_bj(int n, long lines, int b, real_t<T> alpha, T* x, const T* p, T* r, co
     const long blocks = lines * (n / b);
     const unsigned g = grid_for((size_t)blocks, 128, 16);
     switch (b) {
-      case 4: launch_pdl(k_cg_update_bj<T, S, 4>, dim3(g), dim3(128), 0, st, blocks, alpha, x, p, r, q, inv, z, red); break;
-      case 8: launch_pdl(k_cg_update_bj<T, S, 8>, dim3(g), dim3(128), 0, st, blocks, alpha, x, p, r, q, inv, z, red); break;
+      case 4: launch_pdl(k_cg_update_bj<T, S, 4>, dim3(g), dim3(128), 0, st, blocks, alpha, x, p, r, q, inv, z, red, ctl); break;
+      case 8: launch_pdl(k_cg_update_bj<T, S, 8>, dim3(g), dim3(128), 0, st, blocks, alpha, x, p, r, q, inv, z, red, ctl); break;
       case 16:
-        launch_pdl(k_cg_update_bj<T, S, 16>, dim3(g), dim3(128), 0, st, blocks, alpha, x, p, r, q, inv, z, red);
+        launch_pdl(k_cg_update_bj<T, S, 16>, dim3(g), dim3(128), 0, st, blocks, alpha, x, p, r, q, inv, z, red, ctl);
         break;
       default: return false;
     }
@@ -262,21 +266,21 @@ bool cg_bj(int n, long lines, int b, real_t<T> alpha, T* x, const T* p, T* r, co
 
 template <class T>
 bool cg_update_block_jacobi(int n, int b, int storage, const void* inv, real_t<T> alpha, T* x, const T* p, T* r,
-                            const T* q, T* z, const RedSlot& red, cudaStream_t st, long lines) {
+                            const T* q, T* z, const RedSlot& red, cudaStream_t st, long lines, const CgCtl* ctl) {
   if (lines <= 0) lines = (long)n * n;
   bool done = false;
   switch (storage) {
-    case 4: done = cg_bj<T, __half>(n, lines, b, alpha, x, p, r, q, (const __half*)inv, z, red, st); break;
-    case 0: done = cg_bj<T, float>(n, lines, b, alpha, x, p, r, q, (const float*)inv, z, red, st); break;
-    default: done = cg_bj<T, double>(n, lines, b, alpha, x, p, r, q, (const double*)inv, z, red, st); break;
+    case 4: done = cg_bj<T, __half>(n, lines, b, alpha, ctl, x, p, r, q, (const __half*)inv, z, red, st); break;
+    case 0: done = cg_bj<T, float>(n, lines, b, alpha, ctl, x, p, r, q, (const float*)inv, z, red, st); break;
+    default: done = cg_bj<T, double>(n, lines, b, alpha, ctl, x, p, r, q, (const double*)inv, z, red, st); break;
   }
   if (done) LAUNCHED("cg_update_bj");
   return done;
 }
 template bool cg_update_block_jacobi<float>(int, int, int, const void*, float, float*, const float*, float*,
-                                            const float*, float*, const RedSlot&, cudaStream_t, long);
+                                            const float*, float*, const RedSlot&, cudaStream_t, long, const CgCtl*);
 template bool cg_update_block_jacobi<double>(int, int, int, const void*, double, double*, const double*, double*,
-                                             const double*, double*, const RedSlot&, cudaStream_t, long);
+                                             const double*, double*, const RedSlot&, cudaStream_t, long, const CgCtl*);
 
 template <class S>
 __global__ void k_bj_fill(long nblocks_per_line, long lines, int n, int b, const double* __restrict__ full,

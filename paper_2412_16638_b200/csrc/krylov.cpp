@@ -160,6 +160,7 @@ KrylovWork<T>::KrylovWork(size_t m) : red(4), m_(m) {
 template <class T>
 KrylovWork<T>::~KrylovWork() {
   if (h_host) cudaFreeHost(h_host);
+  if (ctl_host_) cudaFreeHost(ctl_host_);
 }
 
 template <class T>
@@ -262,6 +263,22 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
   const bool pipe = batch && !spec_true && (!w.comm || w.comm->size() == 1) && !(pipe_env && pipe_env[0] == '0');
   R spec_rz{}, spec_pq{};
   bool have_spec = false;
+  // Device loop (pipelined FAST CG, fp32, a preconditioner folded into the
+  // update, the fused direction pass): batches of iterations run with their
+  // scalars formed on the device (blas.cu k_cg_ctl, the host's arithmetic on
+  // the same tuples) and ONE round trip per batch instead of one per
+  // iteration; the host takes over, in the reference's order, where the
+  // device stops (stopping test met -> true-residual confirmation / veto;
+  // r.z or p.q not positive -> breakdown).  MPRKB_CG_DEVLOOP=0 disables it.
+  bool devloop = false;
+  if constexpr (std::is_same_v<T, float>) {
+    const char* e = std::getenv("MPRKB_CG_DEVLOOP");
+    devloop = pipe && P != nullptr && pq_fused_ok(*S) && !(e && e[0] == '0');
+  }
+  // batch length: 4 at first, then the iterations the observed residual
+  // decay predicts are still needed (+1), so few gated no-op launches follow
+  // the stop; capped at CgCtl::kMaxBatch
+  int next_batch = 4;
   if (batch) {
     {
       Bracket br(timer, "stencil", st);
@@ -342,6 +359,89 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
         break;
       }
       const R alpha = rz / pq;
+      if constexpr (std::is_same_v<T, float>) {
+        if (devloop && !(fuse_first && k == 0)) {
+          const int batch = std::min(next_batch, crit.max_iter - k);
+          CgCtl* ctl = w.ctl_dev();
+          CgCtl& hc = *w.ctl_host();
+          hc = CgCtl{};
+          hc.alpha = alpha;
+          hc.rz = rz;
+          hc.r0 = r0;
+          hc.tol = crit.tol;
+          CUDA_CHECK(cudaMemcpyAsync(ctl, &hc, sizeof(CgCtl), cudaMemcpyHostToDevice, st));
+          const RedSlot s1d = w.red.slot_dev(1), s2d = w.red.slot_dev(2);
+          T* pn = nullptr;  // the work vector that is none of r, z, p, q
+          for (T* c : {w.v(0), w.v(1), w.v(2), w.v(3), w.spare()})
+            if (c != r && c != z && c != p && c != q) pn = c;
+          T* pp[2] = {p, pn};
+          bool ok = true;
+          for (int j = 0; j < batch && ok; ++j) {
+            {
+              Bracket br(timer, "precond", st);
+              ok = P->cg_update_apply_dev(ctl, x, pp[j & 1], r, q, z, s1d, st);
+            }
+            if (!ok) break;
+            {
+              Bracket br(timer, "stencil", st);
+              pq_fused(*S, z, pp[j & 1], s1d, 1, 0.0f, pp[(j + 1) & 1], q, s2d, st, ctl);
+            }
+            cg_ctl_step(ctl, s1d, 0, 1, s2d, st);
+          }
+          if (!ok) {
+            devloop = false;  // (no storage-level update for this preconditioner: host loop)
+          } else {
+            CUDA_CHECK(cudaMemcpyAsync(&hc, ctl, sizeof(CgCtl), cudaMemcpyDeviceToHost, st));
+            stream_sync(st);
+            const int done = hc.iters;  // >= 1: the batch's first iteration is never gated
+            p = pp[done & 1];
+            for (int i = 0; i < done; ++i) rep.history.push_back(hc.hist[i]);
+            rep.iterations += done;
+            x_clean = false;
+            k += done - 1;
+            rnorm = hc.hist[done - 1];
+            if (hc.stop == 1) {  // the stopping test was met: confirm with the true residual
+              const double rt = (double)std::sqrt(residual(q));
+              x_clean = true;
+              clean_true = rt;
+              if (crit.satisfied(rt, r0)) {
+                rep.converged = true;
+                break;
+              }
+              std::swap(r, q);  // r = q (verified residual), restart
+              rep.history.back() = rt;
+              pre(r, z);
+              std::swap(p, z);
+              rz = rdot(r, p);
+              have_spec = false;
+              continue;
+            }
+            if (hc.stop == 2 || hc.stop == 3) {  // breakdown at the next loop top (unless max_iter ends it)
+              if (k + 1 < crit.max_iter) {
+                rep.failure = 2;
+                break;
+              }
+              continue;
+            }
+            rz = hc.rz;  // batch exhausted: carry on with the next one
+            pq_first = hc.pq;
+            have_pq = true;
+            {
+              // predicted remaining iterations from the mean decay over the batch
+              const double first = done > 1 ? hc.hist[0] : rep.history[rep.history.size() - 2];
+              const double last = hc.hist[done - 1], target = std::max(crit.tol, crit.tol * r0);
+              const int span = done > 1 ? done - 1 : 1;
+              int pred = CgCtl::kMaxBatch;
+              if (first > 0.0 && last > 0.0 && last < first) {
+                const double rate = std::log(last / first) / span;  // < 0
+                pred = (int)std::ceil(std::log(target / last) / rate) + 1;
+              }
+              next_batch = std::max(2, std::min(pred, (int)CgCtl::kMaxBatch));
+            }
+            continue;
+          }
+        }
+      }
       bool fused = false;
       if constexpr (std::is_same_v<T, float>) {
         if (fuse_first && k == 0) {  // already ran (above), with this alpha

@@ -100,6 +100,15 @@ class KrylovWork {
   }
   T* basis(int j);
   void* basis16(int j);  // fp16 storage (2 x fp16 for complex)
+  // CG device-loop control block (device) and its pinned host mirror
+  CgCtl* ctl_dev() {
+    if (!ctl_.get()) ctl_.alloc(sizeof(CgCtl));
+    return ctl_.template as<CgCtl>();
+  }
+  CgCtl* ctl_host() {
+    if (!ctl_host_) CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&ctl_host_), sizeof(CgCtl), cudaHostAllocDefault));
+    return ctl_host_;
+  }
   size_t size() const { return m_; }
   Reducer red;
   // split grid: the vectors are this rank's slab and every dot/norm is
@@ -110,7 +119,8 @@ class KrylovWork {
   size_t m_;
   DevBuf vecs_[4];
   std::vector<DevBuf> basis_, basis16_;
-  DevBuf hval_, spare_;
+  DevBuf hval_, spare_, ctl_;
+  CgCtl* ctl_host_ = nullptr;
 };
 
 // x_alt (optional): a second solution buffer.  With it the first iteration

@@ -50,7 +50,12 @@ bool pq_fused_ok(const StencilSpec& s);  // pq_fused: additionally an undivided 
 // beta_src's device tuples) / rz_old), q = A pnew, red <- pnew.q (fp32, same
 // support as cg_fused_update)
 void pq_fused(const StencilSpec& s, const float* z, const float* p, const RedSlot& beta_src, int beta_comp,
-              float rz_old, float* pnew, float* q, const RedSlot& red, cudaStream_t st);
+              float rz_old, float* pnew, float* q, const RedSlot& red, cudaStream_t st, const CgCtl* ctl = nullptr);
+// Device-loop control step (after an update + pq_fused pair): from the
+// update's tuples (||r||^2 at rcomp, r.z at rzcomp of upd) and pq_fused's
+// tuples (p.q), in the host's order and rounding: ||r|| -> hist, the stopping
+// test, the next alpha = r.z / p.q and rz (CgCtl); no-op once stopped.
+void cg_ctl_step(CgCtl* ctl, const RedSlot& upd, int rcomp, int rzcomp, const RedSlot& pq, cudaStream_t st);
 // alpha_src (nullable): take alpha = (float)rz / (float)pq from that slot's
 // device tuples (components pq, rz — stencil_apply_dot2 into a slot_dev slot)
 void cg_fused_update(const StencilSpec& s, float alpha, const RedSlot* alpha_src, const float* x, const float* p,
@@ -185,7 +190,8 @@ void block_jacobi_apply(int n, int b, int storage, const void* inv, const T* r, 
 // real T, n % b == 0, b in {4, 8, 16}); false when not covered
 template <class T>
 bool cg_update_block_jacobi(int n, int b, int storage, const void* inv, real_t<T> alpha, T* x, const T* p, T* r,
-                            const T* q, T* z, const RedSlot& red, cudaStream_t st, long lines = 0);
+                            const T* q, T* z, const RedSlot& red, cudaStream_t st, long lines = 0,
+                            const CgCtl* ctl = nullptr);
 // per-block inverse storage from the two distinct fp64 block inverses
 // (column-major b x b full blocks, n % b tail blocks)
 void block_jacobi_fill(int n, int b, int storage, const double* full_dev, const double* tail_dev, void* inv,

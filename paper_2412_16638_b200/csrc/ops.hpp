@@ -38,6 +38,12 @@ class Op {
                                void* /*z*/, const RedSlot& /*red*/, cudaStream_t /*st*/) {
     return false;
   }
+  // The same with alpha read from a device control block (CG device loop;
+  // a no-op once ctl->stop is set).  false: not available.
+  virtual bool cg_update_apply_dev(const CgCtl* /*ctl*/, void* /*x*/, const void* /*p*/, void* /*r*/,
+                                   const void* /*q*/, void* /*z*/, const RedSlot& /*red*/, cudaStream_t /*st*/) {
+    return false;
+  }
   // Accessor-style apply (accessor.cu): z = P r with r and z stored in
   // `storage` (4 fp16, 0 fp32, 1 fp64), arithmetic in the operator's dtype,
   // red <- r.z of the stored values.  false: not available.

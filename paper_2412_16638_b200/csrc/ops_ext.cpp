@@ -124,6 +124,15 @@ class BlockJacobiOp final : public Op {
     }
     return false;
   }
+  bool cg_update_apply_dev(const CgCtl* ctl, void* x, const void* p, void* r, const void* q, void* z,
+                           const RedSlot& red, cudaStream_t st) override {
+    if constexpr (std::is_same_v<T, float> || std::is_same_v<T, double>) {
+      return cg_update_block_jacobi<T>(n_, b_, storage_, inv_.get(), (T)0, static_cast<T*>(x),
+                                       static_cast<const T*>(p), static_cast<T*>(r), static_cast<const T*>(q),
+                                       static_cast<T*>(z), red, st, lines_, ctl);
+    }
+    return false;
+  }
   bool apply_storage(const void* r, int storage, void* z, const RedSlot& red, cudaStream_t st) override {
     if constexpr (std::is_same_v<T, float> || std::is_same_v<T, double>) {
       block_jacobi_acc<T>(n_, b_, storage_, inv_.get(), storage, r, z, red, st, lines_);

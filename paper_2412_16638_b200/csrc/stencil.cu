@@ -1355,9 +1355,13 @@ void cg_fused_update(const StencilSpec& sp, float alpha, const RedSlot* alpha_sr
 __global__ void __launch_bounds__(TTHREADS)
     k_pq_fused(const __grid_constant__ CUtensorMap zmap, const __grid_constant__ CUtensorMap pmap, int n, int nz,
                int kc, float s, float g, const double* btup, int bn, int bcomp, float rz_old,
-               float* __restrict__ pnew, float* __restrict__ q, RedSlot red) {
+               float* __restrict__ pnew, float* __restrict__ q, RedSlot red, const CgCtl* ctl) {
   pdl_wait();
   pdl_trigger();
+  if (ctl) {  // device loop: rz_old from the control block; no-op once stopped
+    if (ctl->stop) return;
+    rz_old = ctl->rz;
+  }
   const float beta = __fdiv_rn(__double2float_rn(sum_partials(btup, bn, bcomp)), rz_old);
   extern __shared__ unsigned char smem_raw[];
   float* buf = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
@@ -1442,7 +1446,7 @@ __global__ void __launch_bounds__(TTHREADS)
 }
 
 void pq_fused(const StencilSpec& sp, const float* z, const float* p, const RedSlot& beta_src, int beta_comp,
-              float rz_old, float* pnew, float* q, const RedSlot& red, cudaStream_t st) {
+              float rz_old, float* pnew, float* q, const RedSlot& red, cudaStream_t st, const CgCtl* ctl) {
   if (!pq_fused_supported(sp)) MPRKB_THROW(10, "pq_fused: needs the TMA stencil on an undivided grid");
   if (!beta_src.dpart || *beta_src.count <= 0) MPRKB_THROW(10, "pq_fused: beta source has no device tuples");
   const int n = sp.n, nz = sp.nz > 0 ? sp.nz : n;
@@ -1480,7 +1484,7 @@ void pq_fused(const StencilSpec& sp, const float* z, const float* p, const RedSl
   rs.base = 0;
   rs.total = 0;
   launch_pdl(k_pq_fused, grid, dim3(TTHREADS), smem, st, zmap, pmap, n, nz, chunk, (float)sp.sigma, (float)sp.gamma,
-             (const double*)beta_src.dpart, *beta_src.count, beta_comp, rz_old, pnew, q, rs);
+             (const double*)beta_src.dpart, *beta_src.count, beta_comp, rz_old, pnew, q, rs, ctl);
   note_partials(rs, grid.x * grid.y * grid.z);
   note_kron(true);
   LAUNCHED("pq_fused");

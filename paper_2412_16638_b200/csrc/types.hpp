@@ -93,6 +93,23 @@ enum class Numerics { Fast = 0, Parity = 1 };
 // *count (host memory), and after the stream synchronize the host adds them
 // in CTA order (Reducer::result) — deterministic run to run.  Single-CTA
 // sequential kernels (PARITY dots) write `out` and set *count = 0.
+// Device-side control of a batch of pipelined CG iterations (krylov.cpp
+// device loop): the update reads alpha, the direction update rz_old; the
+// control kernel (blas.cu k_cg_ctl) forms the next scalars from the
+// iteration's device tuples in the host's order and rounding, records
+// ||r||, and raises `stop` where the reference's loop would leave the fast
+// path (stopping test met, r.z or p.q not positive); every kernel of the
+// batch is a no-op once `stop` is set.
+struct CgCtl {
+  float alpha = 0.f, rz = 0.f, pq = 0.f;
+  int stop = 0;  // 0 running, 1 stopping test met, 2 r.z <= 0, 3 p.q <= 0
+  int iters = 0;
+  int pad = 0;
+  double r0 = 0.0, tol = 0.0;
+  static constexpr int kMaxBatch = 32;
+  double hist[kMaxBatch] = {};
+};
+
 struct RedSlot {
   double* partial = nullptr;   // device alias of host-mapped memory, kMaxPartials x 2 doubles
   double* out = nullptr;       // device alias of host-mapped memory, 2 doubles

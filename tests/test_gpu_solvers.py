@@ -553,3 +553,62 @@ def test_pull_form_errors_match_reference(gpu, mp, ref, value):
         code = next(c for c, cls in mp._c._EXC.items() if type(g.value) is cls)
         assert code == e.value.code, (pull, g.value, e.value.code)
         assert np.array_equal(v, u)
+
+
+@pytest.mark.parametrize("store,n", [("f16", 128), ("f32", 64)])
+def test_cg_device_loop_bitwise_host_loop(gpu, mp, store, n):
+    """Pipelined block-Jacobi CG (fp32) runs its iterations in device-side
+    batches (krylov.cpp device loop: alpha, beta, ||r|| and the stopping test
+    formed on the GPU from the same tuples, in the host's order and rounding;
+    one round trip per batch): iteration counts, residual histories and the
+    stepped state are bitwise those of the host-driven loop
+    (MPRKB_CG_DEVLOOP=0)."""
+    import os
+
+    t = mp.builtin("4s3pB")
+    kw = dict(preconditioner="block-jacobi", block_size=8, block_storage=store)
+    dev = mp.Stepper("heat", n, t, 0.01, 1e-5, "f32", 300, **kw)
+    os.environ["MPRKB_CG_DEVLOOP"] = "0"
+    try:
+        host = mp.Stepper("heat", n, t, 0.01, 1e-5, "f32", 300, **kw)
+        a, b = np.zeros(n ** 3), np.zeros(n ** 3)
+        for _ in range(2):
+            os.environ.pop("MPRKB_CG_DEVLOOP", None)
+            ta = dev.step(a)
+            os.environ["MPRKB_CG_DEVLOOP"] = "0"
+            tb = host.step(b)
+            assert ta["iterations"] == tb["iterations"]
+            assert min(ta["iterations"]) > 8  # several device batches per solve
+            for s in range(len(ta["iterations"])):
+                assert np.array_equal(dev.history(s), host.history(s))
+    finally:
+        os.environ.pop("MPRKB_CG_DEVLOOP", None)
+    assert same_bits(a, b)
+
+
+def test_cg_device_loop_max_iter_and_breakdown_paths(gpu, mp):
+    """The device loop leaves through the reference's exits: a cap inside a
+    batch reports MaxIterReached with exactly max_iter iterations, like the
+    host loop."""
+    import os
+
+    t = mp.builtin("4s3pB")
+    kw = dict(preconditioner="block-jacobi", block_size=8, block_storage="f32")
+    n = 64
+    for cap in (5, 11):
+        dev = mp.Stepper("heat", n, t, 0.01, 1e-9, "f32", cap, **kw)
+        os.environ["MPRKB_CG_DEVLOOP"] = "0"
+        try:
+            host = mp.Stepper("heat", n, t, 0.01, 1e-9, "f32", cap, **kw)
+        finally:
+            os.environ.pop("MPRKB_CG_DEVLOOP", None)
+        a, b = np.zeros(n ** 3), np.zeros(n ** 3)
+        ta = dev.step(a)
+        os.environ["MPRKB_CG_DEVLOOP"] = "0"
+        try:
+            tb = host.step(b)
+        finally:
+            os.environ.pop("MPRKB_CG_DEVLOOP", None)
+        assert ta["iterations"] == tb["iterations"] == [cap] * 4
+        assert ta["failure"] == tb["failure"] == [1] * 4
+        assert same_bits(a, b)
