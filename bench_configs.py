@@ -126,6 +126,17 @@ def config5(mp, torch, limit):
              metric="DOF-updates/s", value=n ** 3 / (ms * 1e-3), ms_per_step=ms,
              iterations=its[0], ms_per_cg_iteration=ms / max(1, sum(its[0])))
         del st
+    # accessor-style CG vectors (r, z, p, q in fp16; accessor.cu) beside the
+    # working-precision vectors, b = 8 fp16 blocks, tol 1e-4
+    for kst in (None, "f16"):
+        st = mp.Stepper("heat", n, tab, tau, 1e-4, "f32", 300, preconditioner="block-jacobi", block_size=8,
+                        block_storage="f16", krylov_storage=kst)
+        ms, its = time_steps(mp, torch, st, 1, 1)
+        line(config=5, workload=(f"heat {n}^3 4s3pB f32 stages, CG + block-Jacobi b=8 (f16), tol=1e-4, "
+                                 f"CG vectors {kst or 'fp32 (working precision)'}"),
+             metric="DOF-updates/s", value=n ** 3 / (ms * 1e-3), ms_per_step=ms, iterations=its[0],
+             ms_per_cg_iteration=ms / max(1, sum(its[0])))
+        del st
 
 
 def main():
