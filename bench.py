@@ -472,6 +472,7 @@ def fp64_contraction_roofline(mp, reps=10):
 
 
 KERNELS = ["copy_f32", "stencil_f64", "stencil_f32", "residual_f32", "apply_dot_f32", "dots2_f32", "cg_fused_f32",
+           "cg_fused_self_f32",
            "apply_f64", "apply_f32", "dot_f32", "cg_update_f32", "combine_7", "final_4", "block_jacobi_f16", "cg_bj_f16",
            "csr_f32", "csr_f16"]
 

@@ -84,6 +84,9 @@ void kernel_bench(const std::string& which, int n, int reps, double* ms, double*
   } else if (which == "cg_fused_f32") {  // x1 = x + a p, ||r - a A p||^2, ||b - A x1||^2: x, p, b, r in; x1 out
     const RedSlot s1 = red.slot(0);
     t = time_it(st, reps, 20 * D, [&] { cg_fused_update(sp, 0.5f, nullptr, f32(0), f32(1), f32(2), f32(3), f32(4), s1, st); });
+  } else if (which == "cg_fused_self_f32") {  // the same with x0 = b (the stepper's case): x, p in; x1 out
+    const RedSlot s1 = red.slot(0);
+    t = time_it(st, reps, 12 * D, [&] { cg_fused_update(sp, 0.5f, nullptr, f32(0), f32(1), f32(0), f32(3), f32(4), s1, st); });
   } else if (which == "apply_f64") {  // f_hi = K widen(y32) + g
     StencilSpec k = sp;
     k.sigma = 0.0;

@@ -1127,6 +1127,11 @@ void feval_combine(const StencilSpec& k, const float* y32, const FevalCombine& f
 constexpr int CG_SLOT = tma_slot_elems<float>(), CG_TST = 4;  // 3 planes in use + 1 in flight: 44 KB, 5 CTAs/SM
 constexpr size_t cg_fused_smem() { return (size_t)CG_TST * 2 * CG_SLOT * sizeof(float) + CG_TST * sizeof(uint64_t) + 128; }
 
+// SELF (x0 = b, the stepper's case): b is x's own tile centre and r = b - A b
+// is re-formed from the resident x neighbourhood with the residual kernel's
+// arithmetic (EpiResidualSelf) — bitwise the stored r — so only x, p (TMA)
+// and x1 cross HBM: 3 s N instead of 5 s N.
+template <bool SELF>
 __global__ void __launch_bounds__(TTHREADS)
     k_cg_fused(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap pmap,
                const __grid_constant__ CUtensorMap xlo, const __grid_constant__ CUtensorMap xhi,
@@ -1198,10 +1203,12 @@ __global__ void __launch_bounds__(TTHREADS)
   const int col = 4 + 4 * lane;
   auto gidx = [&](int row, int k) { return (i0 + 4 * lane) + (long)(j0 + row) * nn + (long)k * n2; };
   V4<float> pb[TROWS], pr[TROWS];
+  if (!SELF) {
 #pragma unroll
-  for (int rr = 0; rr < TROWS; ++rr) {
-    pb[rr] = ld4(b + gidx(warp * TROWS + rr, k0));
-    pr[rr] = ld4(r + gidx(warp * TROWS + rr, k0));
+    for (int rr = 0; rr < TROWS; ++rr) {
+      pb[rr] = ld4(b + gidx(warp * TROWS + rr, k0));
+      pr[rr] = ld4(r + gidx(warp * TROWS + rr, k0));
+    }
   }
   for (int k = k0; k < k1; ++k) {
     const int q = k - k0 + 1;
@@ -1214,12 +1221,14 @@ __global__ void __launch_bounds__(TTHREADS)
     const float* xc = buf + (q % CG_TST) * 2 * CG_SLOT;
     const float* xpl = buf + ((q + 1) % CG_TST) * 2 * CG_SLOT;
     V4<float> nb[TROWS], nr[TROWS];
+    if (!SELF) {
 #pragma unroll
-    for (int rr = 0; rr < TROWS; ++rr)
-      if (k + 1 < k1) {
-        nb[rr] = ld4(b + gidx(warp * TROWS + rr, k + 1));
-        nr[rr] = ld4(r + gidx(warp * TROWS + rr, k + 1));
-      }
+      for (int rr = 0; rr < TROWS; ++rr)
+        if (k + 1 < k1) {
+          nb[rr] = ld4(b + gidx(warp * TROWS + rr, k + 1));
+          nr[rr] = ld4(r + gidx(warp * TROWS + rr, k + 1));
+        }
+    }
 #pragma unroll
     for (int rr = 0; rr < TROWS; ++rr) {
       const int row = warp * TROWS + rr;
@@ -1231,10 +1240,24 @@ __global__ void __launch_bounds__(TTHREADS)
       float pl = shfl_up1(pc.x[3]), pr_ = shfl_down1(pc.x[0]);
       if (lane == 0) pl = xc[CG_SLOT + o - 1];
       if (lane == 31) pr_ = xc[CG_SLOT + o + 4];
-      // x1 neighbourhood -> A x1
-      const V4<float> c = upd4(ld(xc + o), pc);
-      const V4<float> ym = upd4(ld(xc + o - TW), pym), yp = upd4(ld(xc + o + TW), pyp);
-      const V4<float> zm = upd4(ld(xmn + o), pzm), zp = upd4(ld(xpl + o), pzp);
+      // x neighbourhood (SELF: b's, for r = b - A b) and x1's -> A x1
+      const V4<float> xcv = ld(xc + o), xym = ld(xc + o - TW), xyp = ld(xc + o + TW);
+      const V4<float> xzm = ld(xmn + o), xzp = ld(xpl + o);
+      if (SELF) {
+        float bl = shfl_up1(xcv.x[3]), br = shfl_down1(xcv.x[0]);
+        if (lane == 0) bl = xc[o - 1];
+        if (lane == 31) br = xc[o + 4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float l = e == 0 ? bl : xcv.x[e - 1], rgt = e == 3 ? br : xcv.x[e + 1];
+          const float v = point<float>(0, s, g, 0.0f, xcv.x[e], l, rgt, xym.x[e], xyp.x[e], xzm.x[e], xzp.x[e]);
+          pb[rr].x[e] = xcv.x[e];
+          pr[rr].x[e] = xsub(xcv.x[e], v);  // EpiResidualSelf's r
+        }
+      }
+      const V4<float> c = upd4(xcv, pc);
+      const V4<float> ym = upd4(xym, pym), yp = upd4(xyp, pyp);
+      const V4<float> zm = upd4(xzm, pzm), zp = upd4(xzp, pzp);
       float xl = shfl_up1(c.x[3]), xr = shfl_down1(c.x[0]);
       if (lane == 0) xl = upd(xc[o - 1], pl);
       if (lane == 31) xr = upd(xc[o + 4], pr_);
@@ -1252,10 +1275,12 @@ __global__ void __launch_bounds__(TTHREADS)
       }
       st4(x1 + gi, c);
     }
+    if (!SELF) {
 #pragma unroll
-    for (int rr = 0; rr < TROWS; ++rr) {
-      pb[rr] = nb[rr];
-      pr[rr] = nr[rr];
+      for (int rr = 0; rr < TROWS; ++rr) {
+        pb[rr] = nb[rr];
+        pr[rr] = nr[rr];
+      }
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
@@ -1279,9 +1304,10 @@ void cg_fused_update(const StencilSpec& sp, float alpha, const RedSlot* alpha_sr
   static thread_local long chunk_cols = -1;
   static thread_local int resident = 0;
   if (!resident) {
-    CUDA_CHECK(cudaFuncSetAttribute(k_cg_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_CHECK(cudaFuncSetAttribute(k_cg_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_CHECK(cudaFuncSetAttribute(k_cg_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_fused, TTHREADS, smem));
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_fused<false>, TTHREADS, smem));
     resident = std::max(1, per_sm) * sm_count();
   }
   const long cols = (long)(n / TI) * (n / TJ);
@@ -1339,7 +1365,8 @@ void cg_fused_update(const StencilSpec& sp, float alpha, const RedSlot* alpha_sr
   const double* apart = alpha_src ? alpha_src->dpart : nullptr;
   const int an = alpha_src ? *alpha_src->count : 0;
   if (alpha_src && (!apart || an <= 0)) MPRKB_THROW(10, "cg_fused_update: alpha source has no device tuples");
-  launch_pdl(k_cg_fused, grid, dim3(TTHREADS), smem, st, xmap, pmap, gm[0], gm[1], gm[2], gm[3], has_lo, has_hi, n,
+  // x0 = b (x aliases b): the SELF pass re-forms b and r from x's tile
+  launch_pdl(x == b ? k_cg_fused<true> : k_cg_fused<false>, grid, dim3(TTHREADS), smem, st, xmap, pmap, gm[0], gm[1], gm[2], gm[3], has_lo, has_hi, n,
              nz, chunk, (float)sp.sigma, (float)sp.gamma, alpha, apart, an, b, r, x1, rs);
   note_partials(rs, grid.x * grid.y * grid.z);
   note_kron(true, 2);  // A p and the true residual's A x1
