@@ -390,8 +390,18 @@ struct EpiF32Forcing {
 // forcing last), so every value is rounded exactly as the per-stage
 // combination would round it; f_eps never touches HBM.
 constexpr int kMaxAcc = kFevalMaxAcc;
-struct EpiFevalCombine {
+// NA = the number of accumulators this pass carries (a template so every
+// accumulator is prefetched a plane ahead into registers like S_{i+1}: the
+// in-loop loads of the later ones left their full HBM latency exposed —
+// ncu source samples on the dependent DADDs)
+template <int NA>
+struct EpiFevalCombineN {
   static constexpr bool kDual = true;
+  // accumulators prefetched a plane ahead: all of them up to two (register
+  // budget: 3 CTAs per SM for two), otherwise the first only (4 CTAs per SM;
+  // prefetching three spills and ran slower, profiles/r02)
+  static constexpr int PF = NA <= 2 ? NA : 1;
+  static constexpr int kMinBlocks = PF >= 2 ? 3 : 4;
   float s32 = 0.f, g32k = 0.f;    // the binary32 stencil's sigma / gamma
   const double* g = nullptr;      // forcing
   const float* g32 = nullptr;     // narrowed forcing
@@ -410,17 +420,19 @@ struct EpiFevalCombine {
   double ah[kMaxAcc] = {}, ae[kMaxAcc] = {};
   int hah[kMaxAcc] = {}, hae[kMaxAcc] = {};
   struct State {};
-  // prefetched a plane ahead: S_{i+1} and the first later-stage accumulator
+  // prefetched a plane ahead: S_{i+1} and every later-stage accumulator
   // (the forcing is regenerated at use — or read there when stored)
   struct Pre {
-    V4<double> s, a0;
+    V4<double> s;
+    V4<double> a[PF > 0 ? PF : 1];
   };
   __device__ void init(State&) const {}
   __device__ __forceinline__ Pre pre4(long i) const {
     Pre p;
     p.s = ld4(sin + i);
     // accumulators are updated in place (ain[a] == aout[a] after stage 0): coherent loads
-    p.a0 = nacc > 0 ? ld4rw(ain[0] + i) : zero4<double>();
+#pragma unroll
+    for (int a = 0; a < PF; ++a) p.a[a] = ld4rw(ain[a] + i);
     return p;
   }
   __device__ __forceinline__ void v4dual(State&, long i, const V4<double>& v64, const V4<float>& v32,
@@ -456,8 +468,9 @@ struct EpiFevalCombine {
     st4(bout + i, b);
     if (xout) st4(xout + i, b);
     if (ovf) *ovf_flag = 1;
-    for (int a = 0; a < nacc; ++a) {
-      V4<double> s = a == 0 ? p.a0 : ld4rw(ain[a] + i);
+#pragma unroll
+    for (int a = 0; a < NA; ++a) {
+      V4<double> s = a < PF ? p.a[a < PF ? a : 0] : ld4rw(ain[a] + i);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         if (hah[a]) s.x[e] = xadd(s.x[e], xmul(ah[a], fh.x[e]));
@@ -728,7 +741,10 @@ constexpr size_t tma_stencil_smem() {
 // resident CTAs per SM the register allocation must allow (the fused
 // f-evaluation epilogue otherwise takes 156 registers: 3 CTAs, latency-bound)
 template <class Epi>
-constexpr int tma_min_blocks() { return is_dual<Epi>::value ? 4 : 1; }
+constexpr int tma_min_blocks() {
+  if constexpr (is_dual<Epi>::value) return Epi::kMinBlocks;
+  return 1;
+}
 
 template <class Src, class Epi>
 __global__ void __launch_bounds__(TTHREADS, tma_min_blocks<Epi>())
@@ -1084,10 +1100,9 @@ bool feval_combine_supported(const StencilSpec& k) {
   return k.stencil == 0 && k.n % TI == 0 && tma_stencil_enabled();
 }
 
-void feval_combine(const StencilSpec& k, const float* y32, const FevalCombine& f, cudaStream_t st) {
-  if (!feval_combine_supported(k)) MPRKB_THROW(10, "feval_combine: needs the TMA stencil (Dirichlet, n % 128 == 0)");
-  if (f.nacc > kMaxAcc) MPRKB_THROW(10, "feval_combine: too many later stages");
-  EpiFevalCombine e;
+template <int NA>
+void feval_combine_n(const StencilSpec& k, const float* y32, const FevalCombine& f, cudaStream_t st) {
+  EpiFevalCombineN<NA> e;
   e.s32 = (float)k.sigma;
   e.g32k = (float)k.gamma;
   e.g = f.g;
@@ -1111,6 +1126,20 @@ void feval_combine(const StencilSpec& k, const float* y32, const FevalCombine& f
     e.hae[a] = f.hae[a];
   }
   launch(k, LdF2D{y32}, e, st, "feval_combine");
+}
+
+void feval_combine(const StencilSpec& k, const float* y32, const FevalCombine& f, cudaStream_t st) {
+  if (!feval_combine_supported(k)) MPRKB_THROW(10, "feval_combine: needs the TMA stencil (Dirichlet, n % 128 == 0)");
+  if (f.nacc > kMaxAcc) MPRKB_THROW(10, "feval_combine: too many later stages");
+  switch (f.nacc) {
+    case 0: return feval_combine_n<0>(k, y32, f, st);
+    case 1: return feval_combine_n<1>(k, y32, f, st);
+    case 2: return feval_combine_n<2>(k, y32, f, st);
+    case 3: return feval_combine_n<3>(k, y32, f, st);
+    case 4: return feval_combine_n<4>(k, y32, f, st);
+    case 5: return feval_combine_n<5>(k, y32, f, st);
+    default: return feval_combine_n<6>(k, y32, f, st);
+  }
 }
 
 // ---- CG update fused with the true-residual check (fp32, TMA pipeline) -----------
