@@ -28,6 +28,15 @@ namespace mprkb {
 
 namespace {
 
+// The 128-byte aligned start of the dynamic shared memory window, formed by
+// pointer arithmetic on the __shared__ array itself (an integer round-trip
+// would lose the address space and turn every tile read into a generic
+// LD.E instead of LDS).
+__device__ __forceinline__ unsigned char* smem_align128(unsigned char* base) {
+  const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(base));
+  return base + ((128u - (a & 127u)) & 127u);
+}
+
 // MPRKB_STENCIL_TMA=0 selects the register-marching kernel everywhere (A/B runs)
 bool tma_stencil_enabled() {
   static const bool on = [] {
@@ -757,7 +766,7 @@ __global__ void __launch_bounds__(TTHREADS, tma_min_blocks<Epi>())
   using Raw = typename Src::raw;
   constexpr int PLANE = tma_slot_elems<Raw>();
   extern __shared__ unsigned char smem_raw[];
-  Raw* buf = reinterpret_cast<Raw*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  Raw* buf = reinterpret_cast<Raw*>(smem_align128(smem_raw));
   uint64_t* full = reinterpret_cast<uint64_t*>(buf + TST * PLANE);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int i0 = blockIdx.x * TI, j0 = blockIdx.y * TJ;
@@ -1177,7 +1186,7 @@ __global__ void __launch_bounds__(TTHREADS)
     alpha = __fdiv_rn(__double2float_rn(rz), __double2float_rn(pq));
   }
   extern __shared__ unsigned char smem_raw[];
-  float* buf = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  float* buf = reinterpret_cast<float*>(smem_align128(smem_raw));
   uint64_t* full = reinterpret_cast<uint64_t*>(buf + CG_TST * 2 * CG_SLOT);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int i0 = blockIdx.x * TI, j0 = blockIdx.y * TJ;
@@ -1420,7 +1429,7 @@ __global__ void __launch_bounds__(TTHREADS)
   }
   const float beta = __fdiv_rn(__double2float_rn(sum_partials(btup, bn, bcomp)), rz_old);
   extern __shared__ unsigned char smem_raw[];
-  float* buf = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  float* buf = reinterpret_cast<float*>(smem_align128(smem_raw));
   uint64_t* full = reinterpret_cast<uint64_t*>(buf + CG_TST * 2 * CG_SLOT);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int i0 = blockIdx.x * TI, j0 = blockIdx.y * TJ;
@@ -1556,7 +1565,7 @@ __global__ void __launch_bounds__(TTHREADS)
   pdl_wait();
   pdl_trigger();
   extern __shared__ unsigned char smem_raw[];
-  float* buf = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  float* buf = reinterpret_cast<float*>(smem_align128(smem_raw));
   uint64_t* full = reinterpret_cast<uint64_t*>(buf + CG_TST * 2 * CG_SLOT);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int i0 = blockIdx.x * TI, j0 = blockIdx.y * TJ;
@@ -1728,7 +1737,7 @@ __global__ void __launch_bounds__(TTHREADS)
   constexpr int TSTM = pull_stages<M>();
   constexpr int PLANE = tma_slot_elems<float>();
   extern __shared__ unsigned char smem_raw[];
-  float* buf = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+  float* buf = reinterpret_cast<float*>(smem_align128(smem_raw));
   uint64_t* full = reinterpret_cast<uint64_t*>(buf + TSTM * M * PLANE);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int i0 = blockIdx.x * TI, j0 = blockIdx.y * TJ;
