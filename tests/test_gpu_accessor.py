@@ -102,13 +102,14 @@ def test_cg_vector_storage_errors(gpu, mp):
 def test_stepper_vector_storage(gpu, mp, prec, storage):
     """Stepper(..., preconditioner="block-jacobi", krylov_storage=...): the
     stage solves keep r, z, p, q in the storage precision; the stepped state
-    agrees with the working-precision stepper to the stage tolerance.  With
-    fp16 vectors the stage tolerance 1e-3 sits at the storage's rounding
-    floor, so the recurrence needs more iterations (measured 51-75 vs 39-42);
-    bounded at twice the working-precision count."""
+    agrees with the working-precision stepper to the stage tolerance.  fp16
+    vectors put a floor near 2.6e-3 of ||r0|| under the recurrence (measured:
+    the second step's solves stall at 2.4e-3 / 0.91 with tol 1e-3), so the
+    fp16 case runs at tol 1e-2, above it; iteration counts within twice the
+    working-precision count."""
     n = 64
     t = mp.builtin("4s3pB")
-    tol = 1e-3 if storage == "f16" else 1e-6
+    tol = 1e-2 if storage == "f16" else 1e-6
     kw = dict(preconditioner="block-jacobi", block_size=8, block_storage="f32")
     acc = mp.Stepper("heat", n, t, 0.01, tol, prec, 400, krylov_storage=storage, **kw)
     ref = mp.Stepper("heat", n, t, 0.01, tol, prec, 400, **kw)
