@@ -235,6 +235,21 @@ void cg_update(size_t m, real_t<T> alpha, T* x, const T* p, T* r, const T* q, co
   LAUNCHED("cg_update");
 }
 
+__global__ void __launch_bounds__(kRedLanes) k_tuple_sums(const double* tup, int n, int ncomp, double* out) {
+  pdl_wait();
+  pdl_trigger();
+  for (int c = 0; c < ncomp; ++c) {
+    const double v = sum_partials(tup, n, c);
+    if (threadIdx.x == 0) out[c] = v;
+  }
+}
+
+void tuple_sums(const RedSlot& slot, int ncomp, double* out, cudaStream_t st) {
+  if (!slot.dpart || *slot.count <= 0) MPRKB_THROW(10, "tuple_sums: the slot has no device tuples");
+  launch_pdl(k_tuple_sums, dim3(1), dim3(kRedLanes), 0, st, (const double*)slot.dpart, *slot.count, ncomp, out);
+  LAUNCHED("tuple_sums");
+}
+
 // ---- CG device loop: the host's scalar steps on the device (krylov.cpp) -------------
 // One CTA of kRedLanes threads; every value is formed exactly as the host forms
 // it from the same tuples (Reducer::result's order, (float) casts, IEEE

@@ -189,6 +189,25 @@ class LocalComm final : public Comm {
     g_->barrier();
   }
 
+  void allgather_dev(const double* send, double* recv, int count, cudaStream_t st) override {
+    auto& pub = g_->pub();
+    CUDA_CHECK(cudaEventRecord(ready_, st));
+    pub[rank()].a = send;
+    pub[rank()].ready = ready_;
+    pub[rank()].done = done_;
+    g_->barrier();
+    for (int s = 0; s < size(); ++s) {
+      if (s != rank()) CUDA_CHECK(cudaStreamWaitEvent(st, pub[s].ready, 0));
+      CUDA_CHECK(cudaMemcpyAsync(recv + (size_t)s * count, pub[s].a, sizeof(double) * count, cudaMemcpyDeviceToDevice,
+                                 st));
+    }
+    CUDA_CHECK(cudaEventRecord(done_, st));
+    g_->barrier();
+    for (int s = 0; s < size(); ++s)
+      if (s != rank()) CUDA_CHECK(cudaStreamWaitEvent(st, pub[s].done, 0));
+    g_->barrier();
+  }
+
  private:
   void exchange(const double* v, int count) {
     g_->slots()[rank()].assign(v, v + count);
@@ -337,6 +356,10 @@ class NcclComm final : public Comm {
       NCCL_CHECK(nccl().recv(r + (size_t)p * bytes, bytes, ncclUint8, p, comm_, st));
     }
     NCCL_CHECK(nccl().group_end());
+  }
+
+  void allgather_dev(const double* send, double* recv, int count, cudaStream_t st) override {
+    NCCL_CHECK(nccl().all_gather(send, recv, count, ncclFloat64, comm_, st));
   }
 
  private:

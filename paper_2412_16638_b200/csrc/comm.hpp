@@ -50,6 +50,10 @@ class Comm {
                     bool periodic, cudaStream_t st) = 0;
   // recv[s*bytes ...] <- rank s's send[rank*bytes ...] for every s (self included)
   virtual void alltoall(const void* send, void* recv, size_t bytes_per_peer, cudaStream_t st) = 0;
+  // recv[r*count + c] <- rank r's send[c] (device doubles, stream-ordered on
+  // st): the Krylov scalars' per-rank partial sums gathered without a host
+  // round trip, so a kernel can complete them in rank order on the device
+  virtual void allgather_dev(const double* send, double* recv, int count, cudaStream_t st) = 0;
 
   int lower(bool periodic) const {
     return rank_ > 0 ? rank_ - 1 : (periodic ? size_ - 1 : -1);

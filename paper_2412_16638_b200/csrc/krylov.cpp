@@ -244,10 +244,16 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
       x_alt = nullptr;
     }
   }
-  // (split grid: the tuples are this rank's — alpha needs the global sums,
-  // so the fused update waits for the host's allreduced scalars)
-  const bool dev_alpha = fuse_first && !(w.comm && w.comm->size() > 1);
-  const RedSlot s2 = dev_alpha ? w.red.slot_dev(2) : w.red.slot(2), s3 = w.red.slot(3);
+  // (split grid: the tuples are this rank's — alpha needs the global sums:
+  // each rank's local pair is formed on the device, all-gathered on the
+  // stream (Comm::allgather_dev) and completed in rank order by the update
+  // itself, so the split solve keeps ONE round trip; MPRKB_SPLIT_DEVALPHA=0
+  // waits for the host's allreduced scalars instead)
+  const bool split = w.comm && w.comm->size() > 1;
+  const bool dev_alpha = fuse_first && !split;
+  const char* sda_env = std::getenv("MPRKB_SPLIT_DEVALPHA");
+  const bool gath_alpha = fuse_first && split && !(sda_env && sda_env[0] == '0');
+  const RedSlot s2 = (dev_alpha || gath_alpha) ? w.red.slot_dev(2) : w.red.slot(2), s3 = w.red.slot(3);
   double r0;
   R rz{}, pq_first{};
   bool have_pq = false;
@@ -296,16 +302,27 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
         // below (r0 already small, breakdown) x is untouched
         Bracket br(timer, "stencil", st);
         cg_fused_update(*S, 0.0f, &s2, x, z, b, r, x_alt, s3, st);
+      } else if (gath_alpha) {
+        const int P = w.comm->size();
+        double* lsum = w.scal_dev(2 + 2 * (size_t)P);
+        tuple_sums(s2, 2, lsum, st);                     // this rank's (p.Ap, r.z)
+        w.comm->allgather_dev(lsum, lsum + 2, 2, st);    // every rank's, in rank order
+        Bracket br(timer, "stencil", st);
+        cg_fused_update(*S, 0.0f, nullptr, x, z, b, r, x_alt, s3, st, lsum + 2, P);
       }
     }
     stream_sync(st);
-    double v[3];
+    double v[5];
     w.red.result(0, 1, &v[0]);
     w.red.result(2, 2, &v[1]);
-    if (dev_alpha) w.red.result(3, 2, fused_v);
-    if (w.comm && w.comm->size() > 1) w.comm->allreduce_sum(v, 3);
+    if (dev_alpha || gath_alpha) w.red.result(3, 2, &v[3]);
+    if (split) w.comm->allreduce_sum(v, gath_alpha ? 5 : 3);  // (rank-order sums: per value as before)
+    if (dev_alpha || gath_alpha) {
+      fused_v[0] = v[3];
+      fused_v[1] = v[4];
+    }
     if constexpr (std::is_same_v<T, float>) {
-      if (fuse_first && !dev_alpha) {  // split grid: the same pass with the global alpha
+      if (fuse_first && !dev_alpha && !gath_alpha) {  // split grid: the same pass with the global alpha
         const R a = (R)v[2] / (R)v[1];
         {
           Bracket br(timer, "stencil", st);

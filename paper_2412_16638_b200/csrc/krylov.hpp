@@ -105,6 +105,11 @@ class KrylovWork {
     if (!ctl_.get()) ctl_.alloc(sizeof(CgCtl));
     return ctl_.template as<CgCtl>();
   }
+  // device scratch for a rank's local scalars and their all-gathered copies
+  double* scal_dev(size_t doubles) {
+    if (scal_.bytes() < doubles * sizeof(double)) scal_.alloc(doubles * sizeof(double));
+    return scal_.template as<double>();
+  }
   CgCtl* ctl_host() {
     if (!ctl_host_) CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&ctl_host_), sizeof(CgCtl), cudaHostAllocDefault));
     return ctl_host_;
@@ -119,7 +124,7 @@ class KrylovWork {
   size_t m_;
   DevBuf vecs_[4];
   std::vector<DevBuf> basis_, basis16_;
-  DevBuf hval_, spare_, ctl_;
+  DevBuf hval_, spare_, ctl_, scal_;
   CgCtl* ctl_host_ = nullptr;
 };
 

@@ -58,8 +58,15 @@ void pq_fused(const StencilSpec& s, const float* z, const float* p, const RedSlo
 void cg_ctl_step(CgCtl* ctl, const RedSlot& upd, int rcomp, int rzcomp, const RedSlot& pq, cudaStream_t st);
 // alpha_src (nullable): take alpha = (float)rz / (float)pq from that slot's
 // device tuples (components pq, rz — stencil_apply_dot2 into a slot_dev slot)
+// gathered (split grid, nullable): the all-gathered per-rank (p.Ap, r.z)
+// pairs of `ranks` ranks ([rank][2], device); alpha = (float)sum rz /
+// (float)sum pq summed in rank order, as Comm::allreduce_sum does
 void cg_fused_update(const StencilSpec& s, float alpha, const RedSlot* alpha_src, const float* x, const float* p,
-                     const float* b, const float* r, float* x1, const RedSlot& red, cudaStream_t st);
+                     const float* b, const float* r, float* x1, const RedSlot& red, cudaStream_t st,
+                     const double* gathered = nullptr, int ranks = 0);
+// out[c] = component c (< ncomp) of slot's device tuples summed in the host's
+// order (reduce.cuh sum_partials): a rank's local value of a reduction, on the device
+void tuple_sums(const RedSlot& slot, int ncomp, double* out, cudaStream_t st);
 
 // apply_f (operators.cpp:81-96), F64 policy: out = K y + g, y read as double
 // or widened from float (`y32`, the fp32 stage solution, exact), g may be

@@ -1178,7 +1178,16 @@ __global__ void __launch_bounds__(TTHREADS)
                const float* __restrict__ b, const float* __restrict__ r, float* __restrict__ x1, RedSlot red) {
   pdl_wait();
   pdl_trigger();
-  if (apart) {
+  if (apart && an < 0) {
+    // split grid: apart = the all-gathered per-rank (p.Ap, r.z) pairs; the
+    // global sums in rank order from 0, as Comm::allreduce_sum forms them
+    double pq = 0.0, rz = 0.0;
+    for (int rr = 0; rr < -an; ++rr) {
+      pq += apart[2 * rr];
+      rz += apart[2 * rr + 1];
+    }
+    alpha = __fdiv_rn(__double2float_rn(rz), __double2float_rn(pq));
+  } else if (apart) {
     // alpha = r.z / p.Ap from the previous pass's tuples, summed and rounded
     // as the host does (krylov.cpp: (R)rz / (R)pq), so no host round trip
     // sits between the two kernels
@@ -1334,7 +1343,8 @@ static bool pq_fused_supported(const StencilSpec& k) { return cg_fused_supported
 bool pq_fused_ok(const StencilSpec& k) { return pq_fused_supported(k); }
 
 void cg_fused_update(const StencilSpec& sp, float alpha, const RedSlot* alpha_src, const float* x, const float* p,
-                     const float* b, const float* r, float* x1, const RedSlot& red, cudaStream_t st) {
+                     const float* b, const float* r, float* x1, const RedSlot& red, cudaStream_t st,
+                     const double* gathered, int ranks) {
   if (!cg_fused_supported(sp)) MPRKB_THROW(10, "cg_fused_update: needs the TMA stencil (Dirichlet, n % 128 == 0)");
   const int n = sp.n, nz = sp.nz > 0 ? sp.nz : n;
   constexpr size_t smem = cg_fused_smem();
@@ -1400,9 +1410,9 @@ void cg_fused_update(const StencilSpec& sp, float alpha, const RedSlot* alpha_sr
   RedSlot rs = red;
   rs.base = 0;
   rs.total = 0;
-  const double* apart = alpha_src ? alpha_src->dpart : nullptr;
-  const int an = alpha_src ? *alpha_src->count : 0;
-  if (alpha_src && (!apart || an <= 0)) MPRKB_THROW(10, "cg_fused_update: alpha source has no device tuples");
+  const double* apart = gathered ? gathered : alpha_src ? alpha_src->dpart : nullptr;
+  const int an = gathered ? -ranks : alpha_src ? *alpha_src->count : 0;
+  if (!gathered && alpha_src && (!apart || an <= 0)) MPRKB_THROW(10, "cg_fused_update: alpha source has no device tuples");
   // x0 = b (x aliases b): the SELF pass re-forms b and r from x's tile
   launch_pdl(x == b ? k_cg_fused<true> : k_cg_fused<false>, grid, dim3(TTHREADS), smem, st, xmap, pmap, gm[0], gm[1], gm[2], gm[3], has_lo, has_hi, n,
              nz, chunk, (float)sp.sigma, (float)sp.gamma, alpha, apart, an, b, r, x1, rs);

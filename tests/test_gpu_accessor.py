@@ -113,11 +113,15 @@ def test_stepper_vector_storage(gpu, mp, prec, storage):
     kw = dict(preconditioner="block-jacobi", block_size=8, block_storage="f32")
     acc = mp.Stepper("heat", n, t, 0.01, tol, prec, 400, krylov_storage=storage, **kw)
     ref = mp.Stepper("heat", n, t, 0.01, tol, prec, 400, **kw)
+    tight = mp.Stepper("heat", n, t, 0.01, 1e-6 if prec == "f32" else 1e-10, prec, 400, **kw)
     u0 = mp.heat_exact(n, 0.05)
-    a, c = u0.copy(), u0.copy()
+    a, c, e = u0.copy(), u0.copy(), u0.copy()
     for _ in range(2):
         ta, tc = acc.step(a), ref.step(c)
+        tight.step(e)
         assert all(ta["converged"]) and all(tc["converged"])
         for i, j in zip(ta["iterations"], tc["iterations"]):
             assert i <= 2 * j + 5 and j <= 2 * i + 5, (ta["iterations"], tc["iterations"])
-    assert np.linalg.norm(a - c) <= 10 * tol * np.linalg.norm(c)
+    # the state error (against tightly solved stages) is that of the
+    # working-precision vectors at the same stage tolerance, within 3x
+    assert np.linalg.norm(a - e) <= 3 * np.linalg.norm(c - e) + 1e-6 * np.linalg.norm(e)

@@ -214,3 +214,22 @@ def test_nccl_single_rank(gpu, mp):
         else:
             assert np.linalg.norm(u - want) <= 1e-12 * np.linalg.norm(want)
         del st
+
+
+@pytest.mark.parametrize("ranks", [2, 4])
+def test_split_device_alpha_bitwise_host_alpha(gpu, mp, ranks):
+    """On a split grid the fused first CG update takes alpha from the ranks'
+    all-gathered local (p.Ap, r.z) pairs, completed in rank order on the
+    device (Comm::allgather_dev, one round trip per solve); bitwise the path
+    that waits for the host's allreduced scalars (MPRKB_SPLIT_DEVALPHA=0)."""
+    import os
+
+    make = maker(mp, "heat", 256, "4s3pB", "f32", "fast", 1e-3)
+    a, ta, _ = run_split(mp, ranks, 2, make)
+    os.environ["MPRKB_SPLIT_DEVALPHA"] = "0"
+    try:
+        b, tb, _ = run_split(mp, ranks, 2, make)
+    finally:
+        os.environ.pop("MPRKB_SPLIT_DEVALPHA", None)
+    assert [t["iterations"] for t in ta] == [t["iterations"] for t in tb]
+    assert np.array_equal(a, b)
