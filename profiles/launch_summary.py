@@ -8,8 +8,9 @@ rows = list(csv.reader(open(sys.argv[1])))
 hdr_i = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
 hdr = rows[hdr_i]
 ki, vi, ii = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("ID")
+mi = hdr.index("Metric Name") if "Metric Name" in hdr else None  # (lists with several metrics per launch)
 ks = [(int(r[ii]), r[ki].split("(")[0].replace("void ", "").replace("mprkb::", "")[:70], float(r[vi].replace(",", "")))
-      for r in rows[hdr_i + 1:] if len(r) > vi]
+      for r in rows[hdr_i + 1:] if len(r) > vi and (mi is None or r[mi] == "gpu__time_duration.sum")]
 if len(sys.argv) > 3:
     lo, hi = int(sys.argv[2]), int(sys.argv[3])
     ks = [k for k in ks if lo <= k[0] <= hi]
