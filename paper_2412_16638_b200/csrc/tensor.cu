@@ -505,21 +505,199 @@ __global__ void __launch_bounds__(128, 2)
       }
 }
 
+// Multistage variant: the tiles arrive by cp.async (16-byte, zero-filled
+// outside the operands) into a 4-deep shared-memory ring, so no prefetch
+// registers are held and three k-blocks are in flight behind the DMMAs; the
+// tiles keep global order (A [row][k], B [k][n] or, for R, [n][k]) and the
+// even / odd q of a block are picked by the fragment indexing (k = 2 k' + p).
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+constexpr int DM_BM = 64, DM_BN = 64, DM_BK = 16, DM_ST = 4, DM_PA = DM_BK + 4, DM_PB = DM_BN + 4;
+constexpr size_t dmma_ms_smem() {
+  return sizeof(double) * DM_ST * ((size_t)DM_BM * DM_PA + (size_t)DM_BK * DM_PB > (size_t)DM_BM * DM_PA + (size_t)DM_BN * DM_PA
+                                        ? (size_t)DM_BM * DM_PA + (size_t)DM_BK * DM_PB
+                                        : (size_t)DM_BM * DM_PA + (size_t)DM_BN * DM_PA);
+}
+
+// NJ: n8 tiles per warp (4: 32 x 32 warp tiles, 4 warps; 2: 32 x 16, 8 warps —
+// half the accumulators per thread, twice the warps per SM)
+template <bool RIGHT, bool DIAG, int NJ>
+__global__ void __launch_bounds__(NJ == 4 ? 128 : 256, 2)
+    k_tensor_dmma_ms(const double* __restrict__ Q, const double* __restrict__ X, double* __restrict__ C,
+                     const double* __restrict__ pd, int n, long Mdim, long Ndim, long ldx, long bstride) {
+  constexpr int BM = DM_BM, BN = DM_BN, BK = DM_BK, ST = DM_ST, PA = DM_PA, PB = DM_PB, NT = NJ == 4 ? 128 : 256;
+  constexpr int WARPS_N = BN / (8 * NJ);
+  // A [ST][BM][PA]; B [ST][BK][PB] (L / M: rows q) or [ST][BN][PA] (R: rows a)
+  constexpr int A_STAGE = BM * PA, B_STAGE = RIGHT ? BN * PA : BK * PB;
+  extern __shared__ __align__(16) unsigned char dsm[];
+  double* As = reinterpret_cast<double*>(dsm);
+  double* Bs = As + ST * A_STAGE;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp / WARPS_N) * 32, wn = (warp % WARPS_N) * (8 * NJ);
+  const long m0 = (long)blockIdx.y * BM;
+  const long c0 = (long)blockIdx.x * BN;
+  const long boff = (long)blockIdx.z * bstride;
+  const int KB = n / BK;
+
+  auto load = [&](int kb, int stage) {
+    const int k0 = kb * BK;
+    double* a = As + stage * A_STAGE;
+    double* b = Bs + stage * B_STAGE;
+#pragma unroll
+    for (int i = 0; i < BM * BK / 2 / NT; ++i) {  // A: BM rows x BK/2 chunks of 2 doubles
+      const int c = tid + i * NT, row = c / (BK / 2), kc = (c % (BK / 2)) * 2;
+      const long m = m0 + row;
+      const bool ok = m < Mdim;
+      const double* src = RIGHT ? X + boff + (ok ? m : 0) * n + k0 + kc : Q + (ok ? m : 0) * n + k0 + kc;
+      cp_async16(a + row * PA + kc, src, ok);
+    }
+    if (RIGHT) {  // B[q][a] = Q[a][q]: BN rows a x BK/2 chunks
+#pragma unroll
+      for (int i = 0; i < BN * BK / 2 / NT; ++i) {
+        const int c = tid + i * NT, col = c / (BK / 2), kc = (c % (BK / 2)) * 2;
+        const long aa = c0 + col;
+        const bool ok = aa < Ndim;
+        cp_async16(b + col * PA + kc, Q + (ok ? aa : 0) * n + k0 + kc, ok);
+      }
+    } else {  // B[q][c] = X[q][c]: BK rows q x BN/2 chunks
+#pragma unroll
+      for (int i = 0; i < BK * BN / 2 / NT; ++i) {
+        const int c = tid + i * NT, row = c / (BN / 2), cc = (c % (BN / 2)) * 2;
+        const long col = c0 + cc;
+        const bool ok = col < Ndim;
+        cp_async16(b + row * PB + cc, X + boff + (long)(k0 + row) * ldx + (ok ? col : 0), ok);
+      }
+    }
+  };
+
+  double acc[2][2][NJ][4];
+#pragma unroll
+  for (int p = 0; p < 2; ++p)
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < NJ; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[p][i][j][e] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < ST - 1; ++s) {
+    if (s < KB) load(s, s);
+    cp_async_commit();
+  }
+  for (int kb = 0; kb < KB; ++kb) {
+    cp_async_wait<ST - 2>();
+    __syncthreads();  // stage kb landed for every thread; stage kb-1 fully consumed
+    if (kb + ST - 1 < KB) load(kb + ST - 1, (kb + ST - 1) % ST);
+    cp_async_commit();
+    const double* a = As + (kb % ST) * A_STAGE;
+    const double* b = Bs + (kb % ST) * B_STAGE;
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {  // E (even q) then O (odd q): k = 2 k' + p
+      const int k_lo = 2 * t + p, k_hi = 2 * (t + 4) + p;
+      double af[2][4], bf[NJ][2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int r = wm + i * 16 + g;
+        af[i][0] = a[r * PA + k_lo];
+        af[i][1] = a[(r + 8) * PA + k_lo];
+        af[i][2] = a[r * PA + k_hi];
+        af[i][3] = a[(r + 8) * PA + k_hi];
+      }
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) {
+        const int cn = wn + j * 8 + g;
+        if (RIGHT) {
+          bf[j][0] = b[cn * PA + k_lo];
+          bf[j][1] = b[cn * PA + k_hi];
+        } else {
+          bf[j][0] = b[k_lo * PB + cn];
+          bf[j][1] = b[k_hi * PB + cn];
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) dmma16808(acc[p][i][j], af[i], bf[j]);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const long m = m0 + wm + i * 16 + g + (e >> 1) * 8;
+        const long c = c0 + wn + j * 8 + 2 * t + (e & 1);
+        if (m >= Mdim || c >= Ndim) continue;
+        const double ev = acc[0][i][j][e], od = acc[1][i][j][e];
+        const long qa = RIGHT ? c : m, qb = n - 1 - qa;
+        const long o1 = RIGHT ? m * n + qa : boff + qa * ldx + c;
+        const long o2 = RIGHT ? m * n + qb : boff + qb * ldx + c;
+        double v1 = ev + od;
+        if (DIAG) v1 *= ldg(pd + o1);
+        C[o1] = v1;
+        if (qb != qa) {
+          double v2 = ev - od;
+          if (DIAG) v2 *= ldg(pd + o2);
+          C[o2] = v2;
+        }
+      }
+}
+
 template <bool DIAG>
 void launch_dmma(int side, int n, long cols, const double* q, const double* x, double* out, const double* pd,
                  cudaStream_t st) {
   constexpr int BM = 64, BN = 64;
   const long nn = n, n2 = nn * nn;
   const long nq = (nn + 1) / 2;  // folded rows of Q
+  static const int ms = [] {
+    const char* e = std::getenv("MPRKB_DMMA_MS");  // =0: the register-prefetch kernel; 4 / 2: n8 tiles per warp
+    return e ? std::atoi(e) : 2;
+  }();
+  constexpr size_t smem = dmma_ms_smem();
+  static thread_local bool configured = false;
+  if (ms && !configured) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_tensor_dmma_ms<true, DIAG, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_CHECK(cudaFuncSetAttribute(k_tensor_dmma_ms<false, DIAG, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_CHECK(cudaFuncSetAttribute(k_tensor_dmma_ms<true, DIAG, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_CHECK(cudaFuncSetAttribute(k_tensor_dmma_ms<false, DIAG, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = true;
+  }
+  const unsigned nt = ms == 4 ? 128 : 256;
   if (side == 2) {
     dim3 grid((unsigned)((nq + BN - 1) / BN), (unsigned)((cols + BM - 1) / BM), 1);
-    k_tensor_dmma<true, DIAG><<<grid, 128, 0, st>>>(q, x, out, pd, n, cols, nq, nn, 0);
+    if (ms == 4)
+      k_tensor_dmma_ms<true, DIAG, 4><<<grid, nt, smem, st>>>(q, x, out, pd, n, cols, nq, nn, 0);
+    else if (ms)
+      k_tensor_dmma_ms<true, DIAG, 2><<<grid, nt, smem, st>>>(q, x, out, pd, n, cols, nq, nn, 0);
+    else
+      k_tensor_dmma<true, DIAG><<<grid, 128, 0, st>>>(q, x, out, pd, n, cols, nq, nn, 0);
   } else if (side == 1) {
     dim3 grid((unsigned)((nn + BN - 1) / BN), (unsigned)((nq + BM - 1) / BM), (unsigned)(cols / nn));
-    k_tensor_dmma<false, DIAG><<<grid, 128, 0, st>>>(q, x, out, pd, n, nq, nn, nn, n2);
+    if (ms == 4)
+      k_tensor_dmma_ms<false, DIAG, 4><<<grid, nt, smem, st>>>(q, x, out, pd, n, nq, nn, nn, n2);
+    else if (ms)
+      k_tensor_dmma_ms<false, DIAG, 2><<<grid, nt, smem, st>>>(q, x, out, pd, n, nq, nn, nn, n2);
+    else
+      k_tensor_dmma<false, DIAG><<<grid, 128, 0, st>>>(q, x, out, pd, n, nq, nn, nn, n2);
   } else {
     dim3 grid((unsigned)((cols + BN - 1) / BN), (unsigned)((nq + BM - 1) / BM), 1);
-    k_tensor_dmma<false, DIAG><<<grid, 128, 0, st>>>(q, x, out, pd, n, nq, cols, cols, 0);
+    if (ms == 4)
+      k_tensor_dmma_ms<false, DIAG, 4><<<grid, nt, smem, st>>>(q, x, out, pd, n, nq, cols, cols, 0);
+    else if (ms)
+      k_tensor_dmma_ms<false, DIAG, 2><<<grid, nt, smem, st>>>(q, x, out, pd, n, nq, cols, cols, 0);
+    else
+      k_tensor_dmma<false, DIAG><<<grid, 128, 0, st>>>(q, x, out, pd, n, nq, cols, cols, 0);
   }
   LAUNCHED("tensor_dmma");
 }
