@@ -179,7 +179,7 @@ def run_reference_arm(args):
     t0 = time.perf_counter()
     warm = reference_steps(N_GRID, min(args.warmup, 1), budget / 3, threads) if args.warmup else []
     if warm is None:
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libmprk_ref.so not built"}))
+        emit({"impl": "reference", "unavailable": "oracle/_ref/libmprk_ref.so not built"})
         return 0
     times = reference_steps(N_GRID, args.steps, budget, threads)
     per_step = sum(times) / len(times)
@@ -204,7 +204,7 @@ def run_reference_arm(args):
         "e2e": {"value": value, "unit": "DOF-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": time.perf_counter() - t0,
     }
-    print(json.dumps(line))
+    emit(line)
     return 0
 
 
@@ -405,7 +405,7 @@ def run_cuda_arm(args):
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
     if line is not None:
-        print(json.dumps(line))
+        emit(line)
     return 0
 
 
@@ -533,7 +533,32 @@ def load_peaks():
     return out
 
 
+# The driver parses ONE JSON line from stdout.  Libraries print to the C-level
+# stdout on their own (NCCL's "NCCL version ..." banner at communicator init,
+# whatever a dlopen'ed library printf's), so the process's fd 1 is pointed at
+# stderr for the whole run and only emit() writes to the original stdout.
+_STDOUT_FD = None
+
+
+def _isolate_stdout():
+    global _STDOUT_FD
+    if _STDOUT_FD is None:
+        sys.stdout.flush()
+        _STDOUT_FD = os.dup(1)
+        os.dup2(2, 1)
+
+
+def emit(obj):
+    data = (json.dumps(obj) + "\n").encode()
+    if _STDOUT_FD is None:
+        sys.stdout.write(data.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_STDOUT_FD, data)
+
+
 def main():
+    _isolate_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=60)
