@@ -515,6 +515,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       half = (t - full_items) & 1;
       T.w = TF_BN / 2;
     }
+    if (dbg & 128) tt = full_items + ((num_items - full_items) >> 1) - 1 - tt;  // reversed tile order
     T.a0 = (tt % a_tiles) * TF_BM;
     const int ct = tt / a_tiles;
     T.col0 = (long)(ct % col_tiles) * TF_BN + half * (TF_BN / 2);
@@ -826,10 +827,20 @@ void launch_tcf(int n, long cols, const float* x, float* out, const float* pd, c
     CUDA_CHECK(cudaFuncSetAttribute(k_tensor_tcf<SIDE, PDIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = true;
   }
-  static const int dbg = [] {
+  static const int dbg0 = [] {
     const char* e = std::getenv("MPRKB_TC_DBG");  // profiling knobs only (results are garbage when set)
     return e ? std::atoi(e) : 0;
   }();
+  // every other launch walks its tiles in reverse, so it starts with the
+  // tiles whose inputs the previous launch wrote last (L2-resident): -1 %
+  // per contraction in the step (MPRKB_TC_REV=0: always forward).  Each tile's
+  // arithmetic is unchanged, so results are identical either way.
+  static const bool rev_on = [] {
+    const char* e = std::getenv("MPRKB_TC_REV");
+    return !(e && e[0] == '0');
+  }();
+  static thread_local unsigned launches = 0;
+  const int dbg = dbg0 | ((rev_on && (launches++ & 1)) ? 128 : 0);
   const cuuint64_t nn = (cuuint64_t)n, n2 = nn * nn, cc = (cuuint64_t)cols;
   CUtensorMap map, pmap;
   int col_tiles, planes = 1;
