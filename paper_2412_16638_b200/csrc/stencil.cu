@@ -403,7 +403,8 @@ constexpr int kMaxAcc = kFevalMaxAcc;
 // accumulator is prefetched a plane ahead into registers like S_{i+1}: the
 // in-loop loads of the later ones left their full HBM latency exposed —
 // ncu source samples on the dependent DADDs)
-template <int NA>
+// FS (stage 0): every accumulator starts from S_{i+1} = u, one load serves all
+template <int NA, bool FS = false>
 struct EpiFevalCombineN {
   static constexpr bool kDual = true;
   // accumulators prefetched a plane ahead: all of them up to two (register
@@ -441,7 +442,7 @@ struct EpiFevalCombineN {
     p.s = ld4(sin + i);
     // accumulators are updated in place (ain[a] == aout[a] after stage 0): coherent loads
 #pragma unroll
-    for (int a = 0; a < PF; ++a) p.a[a] = ld4rw(ain[a] + i);
+    for (int a = 0; a < PF; ++a) p.a[a] = FS ? p.s : ld4rw(ain[a] + i);
     return p;
   }
   __device__ __forceinline__ void v4dual(State&, long i, const V4<double>& v64, const V4<float>& v32,
@@ -479,7 +480,7 @@ struct EpiFevalCombineN {
     if (ovf) *ovf_flag = 1;
 #pragma unroll
     for (int a = 0; a < NA; ++a) {
-      V4<double> s = a < PF ? p.a[a < PF ? a : 0] : ld4rw(ain[a] + i);
+      V4<double> s = FS ? p.s : a < PF ? p.a[a < PF ? a : 0] : ld4rw(ain[a] + i);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         if (hah[a]) s.x[e] = xadd(s.x[e], xmul(ah[a], fh.x[e]));
@@ -1109,9 +1110,9 @@ bool feval_combine_supported(const StencilSpec& k) {
   return k.stencil == 0 && k.n % TI == 0 && tma_stencil_enabled();
 }
 
-template <int NA>
+template <int NA, bool FS>
 void feval_combine_n(const StencilSpec& k, const float* y32, const FevalCombine& f, cudaStream_t st) {
-  EpiFevalCombineN<NA> e;
+  EpiFevalCombineN<NA, FS> e;
   e.s32 = (float)k.sigma;
   e.g32k = (float)k.gamma;
   e.g = f.g;
@@ -1140,14 +1141,24 @@ void feval_combine_n(const StencilSpec& k, const float* y32, const FevalCombine&
 void feval_combine(const StencilSpec& k, const float* y32, const FevalCombine& f, cudaStream_t st) {
   if (!feval_combine_supported(k)) MPRKB_THROW(10, "feval_combine: needs the TMA stencil (Dirichlet, n % 128 == 0)");
   if (f.nacc > kMaxAcc) MPRKB_THROW(10, "feval_combine: too many later stages");
+  bool fs = f.nacc >= 3;  // (stage 0 of a >= 4-stage tableau: all accumulators start from u)
+  for (int a = 0; a < f.nacc; ++a) fs = fs && f.ain[a] == f.sin;
+  if (fs) {
+    switch (f.nacc) {
+      case 3: return feval_combine_n<3, true>(k, y32, f, st);
+      case 4: return feval_combine_n<4, true>(k, y32, f, st);
+      case 5: return feval_combine_n<5, true>(k, y32, f, st);
+      default: return feval_combine_n<6, true>(k, y32, f, st);
+    }
+  }
   switch (f.nacc) {
-    case 0: return feval_combine_n<0>(k, y32, f, st);
-    case 1: return feval_combine_n<1>(k, y32, f, st);
-    case 2: return feval_combine_n<2>(k, y32, f, st);
-    case 3: return feval_combine_n<3>(k, y32, f, st);
-    case 4: return feval_combine_n<4>(k, y32, f, st);
-    case 5: return feval_combine_n<5>(k, y32, f, st);
-    default: return feval_combine_n<6>(k, y32, f, st);
+    case 0: return feval_combine_n<0, false>(k, y32, f, st);
+    case 1: return feval_combine_n<1, false>(k, y32, f, st);
+    case 2: return feval_combine_n<2, false>(k, y32, f, st);
+    case 3: return feval_combine_n<3, false>(k, y32, f, st);
+    case 4: return feval_combine_n<4, false>(k, y32, f, st);
+    case 5: return feval_combine_n<5, false>(k, y32, f, st);
+    default: return feval_combine_n<6, false>(k, y32, f, st);
   }
 }
 
