@@ -394,6 +394,10 @@ constexpr int TF_Q = TF_BM * TF_KH * 4;             // 8 KB per {even, odd} x {h
 #ifndef TF_EB
 #define TF_EB 1  // epilogue staging blocks per warp
 #endif
+#ifndef TF_EPIW
+#define TF_EPIW 4  // epilogue warps (4 or 8: two per TMEM lane quarter, each half the columns)
+#endif
+constexpr int TF_PROD_WARP = 4 + TF_EPIW, TF_MMA_WARP = 5 + TF_EPIW, TF_THREADS = (6 + TF_EPIW) * 32;
 template <bool PDIN>
 struct TfCfg {
   static constexpr int RAWB = TF_RAW * (PDIN ? 2 : 1);
@@ -410,7 +414,7 @@ struct TfSmem {
   alignas(1024) unsigned char x[Cfg::CS][4 * TF_X];
   // epilogue: per epilogue warp one 32x32 fp32 staging block (128B-swizzled
   // rows), drained by a TMA tensor store
-  alignas(1024) float stagec[4][TF_EB][32 * 32];
+  alignas(1024) float stagec[TF_EPIW][TF_EB][32 * 32];
   alignas(8) uint64_t rawfull[Cfg::RS];
   alignas(8) uint64_t rawfree[Cfg::RS];
   alignas(8) uint64_t qfull[Cfg::QS];
@@ -476,7 +480,7 @@ struct Ring {
 };
 
 template <int SIDE, bool PDIN>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(TF_THREADS, 1)
     k_tensor_tcf(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap pmap,
                  const __grid_constant__ CUtensorMap omap, float* __restrict__ C, const float* __restrict__ qpack,
                  int n, int col_tiles, int num_items, int full_items, long ldc, int dbg, int in_bny, int out_bny) {
@@ -532,7 +536,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                  "r"(512u));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
-  if (tid == 32 * TC_PROD_WARP) {
+  if (tid == 32 * TF_PROD_WARP) {
     for (int s = 0; s < RS; ++s) {
       mbar_init(&S.rawfull[s], 1);
       mbar_init(&S.rawfree[s], 32 * TC_CONV_WARPS);
@@ -547,7 +551,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&S.tmem_full[b], 1);
-      mbar_init(&S.tmem_empty[b], 128);
+      mbar_init(&S.tmem_empty[b], 32 * TF_EPIW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -558,7 +562,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   pdl_trigger();
   const uint32_t tmem = S.tmem_base;
 
-  if (warp == TC_PROD_WARP) {
+  if (warp == TF_PROD_WARP) {
     // lane 0: raw X (+ pd) tiles; lane 1: the packed Q tiles — two
     // independent producers so neither ring throttles the other
     if (lane == 0) {
@@ -607,7 +611,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
       }
     }
-  } else if (warp == TC_MMA_WARP) {
+  } else if (warp == TF_MMA_WARP) {
     if (lane == 0) {
       Ring<CS> rx;
       Ring<QS> rq;
@@ -725,12 +729,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         mbar_arrive(&S.xfull[rx.s]);
       }
     }
-  } else if (warp < TC_EPI_WARP0 + 4) {
+  } else if (warp < TC_EPI_WARP0 + TF_EPIW) {
     // TMEM -> E +- O -> swizzled smem block -> TMA tensor store.  Each 32x32
     // block of the output (rows a, and the mirrored rows n-1-a written with
     // the row order reversed so the block is ascending) goes out as one bulk
     // store, asynchronous to the warp.
-    const int q4 = warp - TC_EPI_WARP0;
+    const int ew = warp - TC_EPI_WARP0;
+    const int q4 = ew & 3;              // TMEM lane quarter
+    const int part = ew >> 2, parts = TF_EPIW / 4;  // column share of this warp
     int it = 0;
     for (int t = blockIdx.x; t < num_tiles; t += gridDim.x, ++it) {
       const Tile T = tile_of(t);
@@ -739,13 +745,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int arow = T.a0 + 32 * q4;  // first folded row of this warp's lane quarter
       const uint32_t lanebase = tmem + ((uint32_t)(32 * q4) << 16) + (uint32_t)(acc * 256);
-      for (int cc = 0; cc < T.w && !(dbg & 4); cc += 32) {
+      const int cw = T.w / parts, cbeg = part * cw;
+      for (int cc = cbeg; cc < cbeg + cw && !(dbg & 4); cc += 32) {
         uint32_t e[32], o[32];
         tmem_ld32(lanebase + (uint32_t)cc, e);
         tmem_ld32(lanebase + 128u + (uint32_t)cc, o);
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
-          const uint32_t sb = smem_u32(S.stagec[q4][TF_EB > 1 ? half : 0]);
+          const uint32_t sb = smem_u32(S.stagec[ew][TF_EB > 1 ? half : 0]);
           // the store that last used this staging buffer must have read it
           if (lane == 0) {
             if (TF_EB > 1)
@@ -906,7 +913,7 @@ void launch_tcf(int n, long cols, const float* x, float* out, const float* pd, c
   const int full_items = (rem > 0 && 2 * rem <= G && !(dbg & 64)) ? num_tiles - rem : num_tiles;
   const int num_items = full_items + 2 * (num_tiles - full_items);
   const int grid = num_items < G ? num_items : G;
-  launch_pdl(k_tensor_tcf<SIDE, PDIN>, dim3(grid), dim3(TC_THREADS), smem, st, map, pmap, omap, out, qpack, n,
+  launch_pdl(k_tensor_tcf<SIDE, PDIN>, dim3(grid), dim3(TF_THREADS), smem, st, map, pmap, omap, out, qpack, n,
              col_tiles, num_items, full_items, cols, dbg, in_bny, out_bny);
   LAUNCHED("tensor_tc_fold");
 }
