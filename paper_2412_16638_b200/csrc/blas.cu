@@ -250,6 +250,35 @@ void tuple_sums(const RedSlot& slot, int ncomp, double* out, cudaStream_t st) {
   LAUNCHED("tuple_sums");
 }
 
+__global__ void __launch_bounds__(kRedLanes) k_cg_spec(const double* t0, int n0, const double* t2, int n2,
+                                                     const double* t3, int n3, double tol, double* rec, int* fail) {
+  pdl_wait();
+  pdl_trigger();
+  const double r0s = sum_partials(t0, n0, 0);
+  const double pqs = sum_partials(t2, n2, 0), rzs = sum_partials(t2, n2, 1);
+  const double f0 = sum_partials(t3, n3, 0), f1 = sum_partials(t3, n3, 1);
+  if (threadIdx.x != 0) return;
+  // krylov.cpp: r0 = (double)sqrt((R)v0); rnorm / rt likewise; rz, pq = (R) sums
+  const double r0 = (double)sqrtf(__double2float_rn(r0s));
+  const double rn = (double)sqrtf(__double2float_rn(f0)), rt = (double)sqrtf(__double2float_rn(f1));
+  const float rz = __double2float_rn(rzs), pq = __double2float_rn(pqs);
+  auto sat = [&](double v) { return v <= tol || (r0 > 0 && v / r0 <= tol); };  // StoppingCriterion::satisfied
+  const bool ok = !sat(r0) && rz > 0.0f && pq > 0.0f && sat(rn) && sat(rt);
+  rec[0] = r0;
+  rec[1] = rn;
+  rec[2] = rt;
+  rec[3] = ok ? 1.0 : 0.0;
+  if (!ok) *fail = 1;
+}
+
+void cg_spec_judge(const RedSlot& s0, const RedSlot& s2, const RedSlot& s3, double tol, double* rec, int* fail,
+                   cudaStream_t st) {
+  if (!s0.dpart || !s2.dpart || !s3.dpart) MPRKB_THROW(10, "cg_spec_judge: the reductions need device tuples");
+  launch_pdl(k_cg_spec, dim3(1), dim3(kRedLanes), 0, st, (const double*)s0.dpart, *s0.count, (const double*)s2.dpart,
+             *s2.count, (const double*)s3.dpart, *s3.count, tol, rec, fail);
+  LAUNCHED("cg_spec");
+}
+
 // ---- CG device loop: the host's scalar steps on the device (krylov.cpp) -------------
 // One CTA of kRedLanes threads; every value is formed exactly as the host forms
 // it from the same tuples (Reducer::result's order, (float) casts, IEEE

@@ -180,7 +180,7 @@ T* KrylovWork<T>::basis(int j) {
 // ---------------------------------------------------------------------------
 template <class T>
 void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, KrylovWork<T>& w,
-              SolveReport& rep, cudaStream_t st, EventTimer* timer, T* x_alt, T** result) {
+              SolveReport& rep, cudaStream_t st, EventTimer* timer, T* x_alt, T** result, const CgSpec* spec) {
   using R = real_t<T>;
   const size_t m = w.size();
   if (A.size() != m || (P && P->size() != m)) MPRKB_THROW(2, "cg: operator size != vector length");
@@ -253,7 +253,9 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
   const bool dev_alpha = fuse_first && !split;
   const char* sda_env = std::getenv("MPRKB_SPLIT_DEVALPHA");
   const bool gath_alpha = fuse_first && split && !(sda_env && sda_env[0] == '0');
-  const RedSlot s2 = (dev_alpha || gath_alpha) ? w.red.slot_dev(2) : w.red.slot(2), s3 = w.red.slot(3);
+  const bool speculate = dev_alpha && spec != nullptr;
+  const RedSlot s2 = (dev_alpha || gath_alpha) ? w.red.slot_dev(2) : w.red.slot(2);
+  const RedSlot s3 = speculate ? w.red.slot_dev(3) : w.red.slot(3);
   double r0;
   R rz{}, pq_first{};
   bool have_pq = false;
@@ -288,7 +290,12 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
   if (batch) {
     {
       Bracket br(timer, "stencil", st);
-      stencil_residual<T>(*S, x, b, r, &s0, st);
+      if (speculate) {
+        const RedSlot s0d = w.red.slot_dev(0);
+        stencil_residual<T>(*S, x, b, r, &s0d, st);
+      } else {
+        stencil_residual<T>(*S, x, b, r, &s0, st);
+      }
     }
     pre(r, z);
     {
@@ -300,8 +307,20 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
         // the first update speculatively, alpha formed on the device from the
         // tuples above: it only writes x_alt, so whatever the host decides
         // below (r0 already small, breakdown) x is untouched
-        Bracket br(timer, "stencil", st);
-        cg_fused_update(*S, 0.0f, &s2, x, z, b, r, x_alt, s3, st);
+        {
+          Bracket br(timer, "stencil", st);
+          cg_fused_update(*S, 0.0f, &s2, x, z, b, r, x_alt, s3, st);
+        }
+        if (speculate) {
+          // no round trip: the device judges the one-iteration exit; the
+          // caller reads the record after its own synchronize
+          cg_spec_judge(w.red.slot_dev(0), s2, s3, crit.tol, spec->rec, spec->fail, st);
+          rep.iterations = 1;
+          rep.converged = true;
+          rep.speculative = true;
+          if (result) *result = x_alt;
+          return;
+        }
       } else if (gath_alpha) {
         const int P = w.comm->size();
         double* lsum = w.scal_dev(2 + 2 * (size_t)P);
@@ -831,9 +850,9 @@ template class KrylovWork<c32>;
 template class KrylovWork<c64>;
 
 template void cg_solve<float>(Op&, Op*, const float*, float*, const Crit&, Numerics, KrylovWork<float>&,
-                              SolveReport&, cudaStream_t, EventTimer*, float*, float**);
+                              SolveReport&, cudaStream_t, EventTimer*, float*, float**, const CgSpec*);
 template void cg_solve<double>(Op&, Op*, const double*, double*, const Crit&, Numerics, KrylovWork<double>&,
-                               SolveReport&, cudaStream_t, EventTimer*, double*, double**);
+                               SolveReport&, cudaStream_t, EventTimer*, double*, double**, const CgSpec*);
 #define INST_GMRES(T)                                                                                      \
   template void gmres_solve<T>(Op&, Op*, const T*, T*, const Crit&, Numerics, KrylovWork<T>&, SolveReport&, \
                                cudaStream_t, EventTimer*, int);

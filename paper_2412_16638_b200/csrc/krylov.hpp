@@ -30,6 +30,22 @@ struct SolveReport {
   int failure = 0;  // 0 none, 1 max-iter, 2 breakdown
   double true_residual = 0.0;
   std::vector<double> history;
+  // speculative (CgSpec): the device judged the one-iteration path; history
+  // and true_residual arrive in the CgSpec record after the caller's sync
+  bool speculative = false;
+};
+
+// Speculative one-iteration CG (FAST, an exact-inverse preconditioner, the
+// fused first update on an undivided grid): no host round trip — the device
+// forms r0, ||r1|| and ||b - A x1|| from the tuples exactly as the host would
+// and checks the reference's decisions for the one-iteration exit (r0 not
+// already small, r.z > 0, p.Ap > 0, the stopping test met and confirmed by
+// the true residual).  rec <- (r0, ||r1||, ||b - A x1||, ok); *fail is set
+// when the exit does not hold, and the caller must then redo the work
+// without speculation (its results are meaningless).
+struct CgSpec {
+  double* rec = nullptr;  // device, 4 doubles
+  int* fail = nullptr;    // device-writable flag (host-mapped)
 };
 
 // Per-label device-time accumulator (TimingRegistry, timing.hpp:23-47) fed by
@@ -136,7 +152,7 @@ class KrylovWork {
 template <class T>
 void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, KrylovWork<T>& w,
               SolveReport& rep, cudaStream_t st, EventTimer* timer = nullptr, T* x_alt = nullptr,
-              T** result = nullptr);
+              T** result = nullptr, const CgSpec* spec = nullptr);
 
 // basis_storage: -1 = the working precision T (the reference), 4 = fp16
 // Krylov basis (accessor-style storage, fp64-accumulated dots; extension).

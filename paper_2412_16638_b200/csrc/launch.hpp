@@ -67,6 +67,12 @@ void cg_fused_update(const StencilSpec& s, float alpha, const RedSlot* alpha_src
 // out[c] = component c (< ncomp) of slot's device tuples summed in the host's
 // order (reduce.cuh sum_partials): a rank's local value of a reduction, on the device
 void tuple_sums(const RedSlot& slot, int ncomp, double* out, cudaStream_t st);
+// Speculative one-iteration CG judge (krylov.hpp CgSpec): from the residual's
+// (||r0||^2), the first-iteration scalars' (p.Ap, r.z) and the fused update's
+// (||r1||^2, ||b - A x1||^2) device tuples, in the host's order and fp32
+// rounding: rec = (r0, ||r1||, ||b - A x1||, ok); *fail = 1 unless ok.
+void cg_spec_judge(const RedSlot& s0, const RedSlot& s2, const RedSlot& s3, double tol, double* rec, int* fail,
+                   cudaStream_t st);
 
 // apply_f (operators.cpp:81-96), F64 policy: out = K y + g, y read as double
 // or widened from float (`y32`, the fp32 stage solution, exact), g may be

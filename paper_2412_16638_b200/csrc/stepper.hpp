@@ -60,7 +60,13 @@ class Stepper {
   // fp32-stage heat on the TMA stencil path: each stage's f evaluations are
   // fused with the next stage's right-hand side (EpiFevalCombine); later
   // stages' couplings accumulate in acc_ (see step_fused)
-  void step_fused(double* u, StepTrace& trace);
+  void step_fused(double* u, StepTrace& trace, bool speculate);
+  // speculative stage solves (CgSpec, krylov.hpp): no host round trip per
+  // solve; the device judges each one-iteration exit, the final update is
+  // gated on the verdicts, and a failed speculation redoes the step without
+  // it (MPRKB_SPECULATE=0: never)
+  bool speculate_ = false;
+  DevBuf spec_rec_;
   // the same pipeline in pull form (undivided grid): every right-hand side
   // and the final update re-evaluate f_hi / f_eps from the stored fp32 stage
   // vectors ys_ (stencil.cu k_stage_pull) — no fp64 accumulators

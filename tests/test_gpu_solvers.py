@@ -612,3 +612,29 @@ def test_cg_device_loop_max_iter_and_breakdown_paths(gpu, mp):
         assert ta["iterations"] == tb["iterations"] == [cap] * 4
         assert ta["failure"] == tb["failure"] == [1] * 4
         assert same_bits(a, b)
+
+
+def test_speculative_stage_solves_bitwise(gpu, mp):
+    """The fused pipeline's stage solves run speculatively (CgSpec: no host
+    round trip per solve; the device judges each one-iteration exit and gates
+    the final update): the state, iteration counts and residual histories are
+    bitwise those of the round-trip path (MPRKB_SPECULATE=0); a forced miss
+    (tolerance below the one-iteration reach) redoes the step and still
+    matches."""
+    import os
+
+    t = mp.builtin("4s3pB")
+    for tol, n in ((1e-3, 256), (1e-7, 128)):
+        spec = mp.Stepper("heat", n, t, 0.01, tol, "f32", 12)
+        os.environ["MPRKB_SPECULATE"] = "0"
+        try:
+            plain = mp.Stepper("heat", n, t, 0.01, tol, "f32", 12)
+        finally:
+            os.environ.pop("MPRKB_SPECULATE", None)
+        a, b = np.zeros(n ** 3), np.zeros(n ** 3)
+        for _ in range(2):
+            ta, tb = spec.step(a), plain.step(b)
+            assert ta == tb
+            for s in range(len(ta["iterations"])):
+                assert np.array_equal(spec.history(s), plain.history(s))
+        assert same_bits(a, b)
