@@ -180,7 +180,7 @@ T* KrylovWork<T>::basis(int j) {
 // ---------------------------------------------------------------------------
 template <class T>
 void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, KrylovWork<T>& w,
-              SolveReport& rep, cudaStream_t st, EventTimer* timer, T* x_alt, T** result, const CgSpec* spec) {
+              SolveReport& rep, cudaStream_t st, EventTimer* timer, T* x_alt, T** result, CgSpec* spec) {
   using R = real_t<T>;
   const size_t m = w.size();
   if (A.size() != m || (P && P->size() != m)) MPRKB_THROW(2, "cg: operator size != vector length");
@@ -303,6 +303,15 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
       stencil_apply_dot2<T>(*S, z, fuse_first ? nullptr : q, r, s2, st);  // q = A z, (z.q, r.z)
     }
     if constexpr (std::is_same_v<T, float>) {
+      if (speculate && spec->defer) {
+        // the caller fuses the update into its next pass and judges it
+        spec->dir = z;
+        rep.iterations = 1;
+        rep.converged = true;
+        rep.speculative = true;
+        if (result) *result = nullptr;
+        return;
+      }
       if (dev_alpha) {
         // the first update speculatively, alpha formed on the device from the
         // tuples above: it only writes x_alt, so whatever the host decides
@@ -850,9 +859,9 @@ template class KrylovWork<c32>;
 template class KrylovWork<c64>;
 
 template void cg_solve<float>(Op&, Op*, const float*, float*, const Crit&, Numerics, KrylovWork<float>&,
-                              SolveReport&, cudaStream_t, EventTimer*, float*, float**, const CgSpec*);
+                              SolveReport&, cudaStream_t, EventTimer*, float*, float**, CgSpec*);
 template void cg_solve<double>(Op&, Op*, const double*, double*, const Crit&, Numerics, KrylovWork<double>&,
-                               SolveReport&, cudaStream_t, EventTimer*, double*, double**, const CgSpec*);
+                               SolveReport&, cudaStream_t, EventTimer*, double*, double**, CgSpec*);
 #define INST_GMRES(T)                                                                                      \
   template void gmres_solve<T>(Op&, Op*, const T*, T*, const Crit&, Numerics, KrylovWork<T>&, SolveReport&, \
                                cudaStream_t, EventTimer*, int);

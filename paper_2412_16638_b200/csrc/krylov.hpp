@@ -46,6 +46,11 @@ struct SolveReport {
 struct CgSpec {
   double* rec = nullptr;  // device, 4 doubles
   int* fail = nullptr;    // device-writable flag (host-mapped)
+  // defer: stop before the fused update — the caller forms x1 = b + alpha z
+  // itself (update_feval) and runs the judge; dir <- z (null if the solve did
+  // not take the speculative path)
+  bool defer = false;
+  const void* dir = nullptr;
 };
 
 // Per-label device-time accumulator (TimingRegistry, timing.hpp:23-47) fed by
@@ -152,7 +157,7 @@ class KrylovWork {
 template <class T>
 void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, KrylovWork<T>& w,
               SolveReport& rep, cudaStream_t st, EventTimer* timer = nullptr, T* x_alt = nullptr,
-              T** result = nullptr, const CgSpec* spec = nullptr);
+              T** result = nullptr, CgSpec* spec = nullptr);
 
 // basis_storage: -1 = the working precision T (the reference), 4 = fp16
 // Krylov basis (accessor-style storage, fp64-accumulated dots; extension).

@@ -110,6 +110,14 @@ struct FevalCombine {
 };
 bool feval_combine_supported(const StencilSpec& k);
 void feval_combine(const StencilSpec& k, const float* y32, const FevalCombine& f, cudaStream_t st);
+// A speculative one-iteration stage solve's update fused with that stage's
+// feval_combine (stencil.cu k_update_feval): x1 = b + alpha z (alpha from
+// alpha_src's device tuples, as cg_fused_update) is formed on the fly and never
+// stored; red <- (||r1||^2, ||b - A_s x1||^2) for cg_spec_judge; f consumes x1
+// as feval_combine consumes y32.  f.bout must not alias b.  Undivided grid.
+bool update_feval_supported(const StencilSpec& s, const StencilSpec& k);
+void update_feval(const StencilSpec& s, const StencilSpec& k, const RedSlot& alpha_src, const float* b,
+                  const float* z, const FevalCombine& f, const RedSlot& red, cudaStream_t st);
 
 // Pull form (stencil.cu k_stage_pull): one pass forms a stage's right-hand
 // side u + sum_j (ch_j f_hi(y_j) + ce_j f_eps(y_j)) + cg g — or, `final`,

@@ -1111,7 +1111,7 @@ bool feval_combine_supported(const StencilSpec& k) {
 }
 
 template <int NA, bool FS>
-void feval_combine_n(const StencilSpec& k, const float* y32, const FevalCombine& f, cudaStream_t st) {
+EpiFevalCombineN<NA, FS> feval_epi(const StencilSpec& k, const FevalCombine& f) {
   EpiFevalCombineN<NA, FS> e;
   e.s32 = (float)k.sigma;
   e.g32k = (float)k.gamma;
@@ -1135,31 +1135,43 @@ void feval_combine_n(const StencilSpec& k, const float* y32, const FevalCombine&
     e.hah[a] = f.hah[a];
     e.hae[a] = f.hae[a];
   }
-  launch(k, LdF2D{y32}, e, st, "feval_combine");
+  return e;
+}
+
+template <int NA, bool FS>
+void feval_combine_n(const StencilSpec& k, const float* y32, const FevalCombine& f, cudaStream_t st) {
+  launch(k, LdF2D{y32}, feval_epi<NA, FS>(k, f), st, "feval_combine");
+}
+
+// feval_combine's instantiation for f: Fn<NA, FS>() (NA = f.nacc; FS when the
+// accumulators of a >= 4-stage tableau's stage 0 all start from S_{i+1} = u)
+template <class Fn>
+void feval_dispatch(const FevalCombine& f, Fn&& fn) {
+  bool fs = f.nacc >= 3;
+  for (int a = 0; a < f.nacc; ++a) fs = fs && f.ain[a] == f.sin;
+  if (fs) {
+    switch (f.nacc) {
+      case 3: return fn(std::integral_constant<int, 3>{}, std::true_type{});
+      case 4: return fn(std::integral_constant<int, 4>{}, std::true_type{});
+      case 5: return fn(std::integral_constant<int, 5>{}, std::true_type{});
+      default: return fn(std::integral_constant<int, 6>{}, std::true_type{});
+    }
+  }
+  switch (f.nacc) {
+    case 0: return fn(std::integral_constant<int, 0>{}, std::false_type{});
+    case 1: return fn(std::integral_constant<int, 1>{}, std::false_type{});
+    case 2: return fn(std::integral_constant<int, 2>{}, std::false_type{});
+    case 3: return fn(std::integral_constant<int, 3>{}, std::false_type{});
+    case 4: return fn(std::integral_constant<int, 4>{}, std::false_type{});
+    case 5: return fn(std::integral_constant<int, 5>{}, std::false_type{});
+    default: return fn(std::integral_constant<int, 6>{}, std::false_type{});
+  }
 }
 
 void feval_combine(const StencilSpec& k, const float* y32, const FevalCombine& f, cudaStream_t st) {
   if (!feval_combine_supported(k)) MPRKB_THROW(10, "feval_combine: needs the TMA stencil (Dirichlet, n % 128 == 0)");
   if (f.nacc > kMaxAcc) MPRKB_THROW(10, "feval_combine: too many later stages");
-  bool fs = f.nacc >= 3;  // (stage 0 of a >= 4-stage tableau: all accumulators start from u)
-  for (int a = 0; a < f.nacc; ++a) fs = fs && f.ain[a] == f.sin;
-  if (fs) {
-    switch (f.nacc) {
-      case 3: return feval_combine_n<3, true>(k, y32, f, st);
-      case 4: return feval_combine_n<4, true>(k, y32, f, st);
-      case 5: return feval_combine_n<5, true>(k, y32, f, st);
-      default: return feval_combine_n<6, true>(k, y32, f, st);
-    }
-  }
-  switch (f.nacc) {
-    case 0: return feval_combine_n<0, false>(k, y32, f, st);
-    case 1: return feval_combine_n<1, false>(k, y32, f, st);
-    case 2: return feval_combine_n<2, false>(k, y32, f, st);
-    case 3: return feval_combine_n<3, false>(k, y32, f, st);
-    case 4: return feval_combine_n<4, false>(k, y32, f, st);
-    case 5: return feval_combine_n<5, false>(k, y32, f, st);
-    default: return feval_combine_n<6, false>(k, y32, f, st);
-  }
+  feval_dispatch(f, [&](auto na, auto fs) { feval_combine_n<decltype(na)::value, decltype(fs)::value>(k, y32, f, st); });
 }
 
 // ---- CG update fused with the true-residual check (fp32, TMA pipeline) -----------
@@ -1430,6 +1442,230 @@ void cg_fused_update(const StencilSpec& sp, float alpha, const RedSlot* alpha_sr
   note_partials(rs, grid.x * grid.y * grid.z);
   note_kron(true, 2);  // A p and the true residual's A x1
   LAUNCHED("cg_fused_update");
+}
+
+// ---- speculative stage solve's update fused with the stage's f evaluations -------
+// The stepper's speculative pipeline (stepper.cpp step_fused) ends stage i's
+// one-iteration solve with k_cg_fused<SELF> (x1 = b + alpha z written, the
+// judge's norms) and then reads x1 back in feval_combine.  Here the two are
+// ONE pass: b (= x0) and z stream through the cg_fused ring, x1 is formed at
+// every loaded point with k_cg_update's rounding, the judge's (||r1||^2,
+// ||b - A_s x1||^2) accumulate as in k_cg_fused, and from the same resident
+// x1 neighbourhood the f evaluations (K x1 in binary64 over the widened
+// values, and in binary32) feed EpiFevalCombineN unchanged — x1 never
+// reaches HBM: 2 s N read (b, z) instead of 3 s N + 1 s N written + s N read.
+// Every value rounds as in the two-kernel sequence.  The next stage's rhs is
+// written to a buffer other than b (neighbouring CTAs still read b).
+// ring depth UF_TST (MPRKB_UF_TST, default 4 = 3 planes in use + 1 in
+// flight): 5 / 6 slots cost a resident CTA per SM and measured slower
+template <int UF_TST>
+constexpr size_t uf_smem() { return (size_t)UF_TST * 2 * CG_SLOT * sizeof(float) + UF_TST * sizeof(uint64_t) + 128; }
+
+template <class Epi, int UF_TST>
+__global__ void __launch_bounds__(TTHREADS, Epi::kMinBlocks)
+    k_update_feval(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap pmap, int n, int kc,
+                   float s, float g, double sk, double gk, const double* apart, int an, RedSlot red, Epi epi) {
+  pdl_wait();
+  pdl_trigger();
+  float alpha;
+  {
+    const double pq = sum_partials(apart, an, 0), rz = sum_partials(apart, an, 1);
+    alpha = __fdiv_rn(__double2float_rn(rz), __double2float_rn(pq));
+  }
+  extern __shared__ unsigned char smem_raw[];
+  float* buf = reinterpret_cast<float*>(smem_align128(smem_raw));
+  uint64_t* full = reinterpret_cast<uint64_t*>(buf + UF_TST * 2 * CG_SLOT);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int i0 = blockIdx.x * TI, j0 = blockIdx.y * TJ;
+  const int nz = n;
+  int k0, k1;
+  plane_range(nz, 0, nz, kc, k0, k1);
+  const int planes = k1 - k0 + 2;
+  constexpr uint32_t bytes = (TJ + 2) * TW * sizeof(float);
+  if (tid == 0) {
+    for (int q = 0; q < UF_TST; ++q) mbar_init(&full[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const CUtensorMap* xm = &xmap;
+  const CUtensorMap* pm = &pmap;
+  auto issue = [&](int q) {  // planes -1 / nz: out of range -> zeros (Dirichlet)
+    const int k = k0 - 1 + q, sl = q % UF_TST;
+    float* dst = buf + sl * 2 * CG_SLOT;
+    mbar_expect_tx(&full[sl], 2 * bytes);
+    tma_3d(dst, xm, i0 - 4, j0 - 1, k, &full[sl]);
+    tma_3d(dst + CG_SLOT, pm, i0 - 4, j0 - 1, k, &full[sl]);
+  };
+  if (tid == 0)
+    for (int q = 0; q < UF_TST && q < planes; ++q) issue(q);
+  auto wait = [&](int q) { mbar_wait(&full[q % UF_TST], (uint32_t)(q / UF_TST) & 1u); };
+  auto ld = [](const float* p) {
+    const float4 f = *reinterpret_cast<const float4*>(p);
+    V4<float> v;
+    v.x[0] = f.x; v.x[1] = f.y; v.x[2] = f.z; v.x[3] = f.w;
+    return v;
+  };
+  auto upd = [&](float xv, float pv) { return xadd(xv, xscale(alpha, pv)); };  // k_cg_update's x
+  auto upd4 = [&](const V4<float>& xv, const V4<float>& pv) {
+    V4<float> o;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o.x[e] = upd(xv.x[e], pv.x[e]);
+    return o;
+  };
+  double acc[2] = {0.0, 0.0};  // ||r1||^2, ||b - A x1||^2
+  typename Epi::State est;
+  epi.init(est);
+  const long nn = n, n2 = nn * nn;
+  const int col = 4 + 4 * lane;
+  auto gidx = [&](int row, int k) { return (i0 + 4 * lane) + (long)(j0 + row) * nn + (long)k * n2; };
+  typename Epi::Pre pre[TROWS];
+#pragma unroll
+  for (int rr = 0; rr < TROWS; ++rr) pre[rr] = epi.pre4(gidx(warp * TROWS + rr, k0));
+  for (int k = k0; k < k1; ++k) {
+    const int q = k - k0 + 1;
+    if (k == k0) {
+      wait(0);
+      wait(1);
+    }
+    wait(q + 1);
+    const float* xmn = buf + ((q - 1) % UF_TST) * 2 * CG_SLOT;
+    const float* xc = buf + (q % UF_TST) * 2 * CG_SLOT;
+    const float* xpl = buf + ((q + 1) % UF_TST) * 2 * CG_SLOT;
+    typename Epi::Pre nxt[TROWS];
+#pragma unroll
+    for (int rr = 0; rr < TROWS; ++rr)
+      if (k + 1 < k1) nxt[rr] = epi.pre4(gidx(warp * TROWS + rr, k + 1));
+#pragma unroll
+    for (int rr = 0; rr < TROWS; ++rr) {
+      const int row = warp * TROWS + rr;
+      const int o = (row + 1) * TW + col;
+      const V4<float> pc = ld(xc + CG_SLOT + o);
+      const V4<float> pym = ld(xc + CG_SLOT + o - TW), pyp = ld(xc + CG_SLOT + o + TW);
+      const V4<float> pzm = ld(xmn + CG_SLOT + o), pzp = ld(xpl + CG_SLOT + o);
+      float pl = shfl_up1(pc.x[3]), pr_ = shfl_down1(pc.x[0]);
+      if (lane == 0) pl = xc[CG_SLOT + o - 1];
+      if (lane == 31) pr_ = xc[CG_SLOT + o + 4];
+      const V4<float> xcv = ld(xc + o), xym = ld(xc + o - TW), xyp = ld(xc + o + TW);
+      const V4<float> xzm = ld(xmn + o), xzp = ld(xpl + o);
+      float bl = shfl_up1(xcv.x[3]), br = shfl_down1(xcv.x[0]);
+      if (lane == 0) bl = xc[o - 1];
+      if (lane == 31) br = xc[o + 4];
+      const V4<float> c = upd4(xcv, pc);
+      const V4<float> ym = upd4(xym, pym), yp = upd4(xyp, pyp);
+      const V4<float> zm = upd4(xzm, pzm), zp = upd4(xzp, pzp);
+      float xl = shfl_up1(c.x[3]), xr = shfl_down1(c.x[0]);
+      if (lane == 0) xl = upd(xc[o - 1], pl);
+      if (lane == 31) xr = upd(xc[o + 4], pr_);
+      V4<double> v64, c64;
+      V4<float> v32;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float l = e == 0 ? bl : xcv.x[e - 1], rgt = e == 3 ? br : xcv.x[e + 1];
+        const float rv = xsub(xcv.x[e], point<float>(0, s, g, 0.0f, xcv.x[e], l, rgt, xym.x[e], xyp.x[e], xzm.x[e],
+                                                     xzp.x[e]));  // EpiResidualSelf's r
+        const float ql = e == 0 ? pl : pc.x[e - 1], qr = e == 3 ? pr_ : pc.x[e + 1];
+        const float qv = point<float>(0, s, g, 0.0f, pc.x[e], ql, qr, pym.x[e], pyp.x[e], pzm.x[e], pzp.x[e]);
+        const float r1 = xsub(rv, xscale(alpha, qv));  // k_cg_update's r
+        dot_acc(*reinterpret_cast<double(*)[1]>(&acc[0]), r1, r1);
+        const float al = e == 0 ? xl : c.x[e - 1], ar = e == 3 ? xr : c.x[e + 1];
+        const float av = point<float>(0, s, g, 0.0f, c.x[e], al, ar, ym.x[e], yp.x[e], zm.x[e], zp.x[e]);
+        const float t = xsub(xcv.x[e], av);  // EpiResidual's b - A x
+        dot_acc(*reinterpret_cast<double(*)[1]>(&acc[1]), t, t);
+        // stage i's f evaluations of x1 (k_stencil_tma's dual path over LdF2D)
+        c64.x[e] = (double)c.x[e];
+        v64.x[e] = point<double>(0, sk, gk, 0.0, c64.x[e], (double)al, (double)ar, (double)ym.x[e], (double)yp.x[e],
+                                 (double)zm.x[e], (double)zp.x[e]);
+        v32.x[e] = point<float>(0, epi.s32, epi.g32k, 0.0f, c.x[e], al, ar, ym.x[e], yp.x[e], zm.x[e], zp.x[e]);
+      }
+      epi.v4dual(est, gidx(row, k), v64, v32, c64, pre[rr]);
+    }
+#pragma unroll
+    for (int rr = 0; rr < TROWS; ++rr) pre[rr] = nxt[rr];
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0 && q - 1 + UF_TST < planes) issue(q - 1 + UF_TST);
+  }
+  epi.finish(est);
+  grid_reduce<2>(acc, red);
+}
+
+bool update_feval_supported(const StencilSpec& sp, const StencilSpec& k) {
+  return cg_fused_supported(sp) && feval_combine_supported(k) && !sp.halo && !k.halo && sp.n == k.n &&
+         (sp.nz <= 0 || sp.nz == sp.n) && (k.nz <= 0 || k.nz == k.n);
+}
+
+template <int NA, bool FS, int UF_TST>
+static void update_feval_d(const StencilSpec& sp, const StencilSpec& k, const RedSlot& alpha_src, const float* x,
+                           const float* p, const FevalCombine& f, const RedSlot& red, cudaStream_t st) {
+  using Epi = EpiFevalCombineN<NA, FS>;
+  const int n = sp.n;
+  constexpr size_t smem = uf_smem<UF_TST>();
+  static thread_local int resident = 0;
+  static thread_local int chunk = 0;
+  static thread_local int chunk_n = -1;
+  if (!resident) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_update_feval<Epi, UF_TST>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_update_feval<Epi, UF_TST>, TTHREADS, smem));
+    resident = std::max(1, per_sm) * sm_count();
+  }
+  const long cols = (long)(n / TI) * (n / TJ);
+  if (n != chunk_n) {  // wave-sized k-chunks (as tma_chunk)
+    long best_cost = -1;
+    for (int kc = 4; kc <= 64; ++kc) {
+      const long units = cols * ((n + kc - 1) / kc);
+      const long cost = ((units + resident - 1) / resident) * (std::min(kc, n) + 2);
+      if (best_cost < 0 || cost < best_cost) {
+        chunk = kc;
+        best_cost = cost;
+      }
+    }
+    chunk_n = n;
+  }
+  const cuuint64_t nn = (cuuint64_t)n;
+  const cuuint64_t dims3[3] = {nn, nn, nn}, str3[2] = {nn * 4, nn * nn * 4};
+  const cuuint32_t box3[3] = {(cuuint32_t)TW, (cuuint32_t)(TJ + 2), 1};
+  const CUtensorMap xmap = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, x, 3, dims3, str3, box3);
+  const CUtensorMap pmap = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, p, 3, dims3, str3, box3);
+  const unsigned gz = (unsigned)((n + chunk - 1) / chunk);
+  const dim3 grid((unsigned)(n / TI), (unsigned)(n / TJ), gz);
+  RedSlot rs = red;
+  rs.base = 0;
+  rs.total = 0;
+  launch_pdl(k_update_feval<Epi, UF_TST>, grid, dim3(TTHREADS), smem, st, xmap, pmap, n, chunk, (float)sp.sigma,
+             (float)sp.gamma, k.sigma, k.gamma, (const double*)alpha_src.dpart, *alpha_src.count, rs,
+             feval_epi<NA, FS>(k, f));
+  note_partials(rs, grid.x * grid.y * grid.z);
+  note_kron(true, 2);  // (k_cg_fused's A p and A x1)
+  note_kron(false);    // (the f evaluations: binary64 and binary32 stencils of x1)
+  note_kron(true);
+  LAUNCHED("update_feval");
+}
+
+template <int NA, bool FS>
+static void update_feval_n(const StencilSpec& sp, const StencilSpec& k, const RedSlot& alpha_src, const float* x,
+                           const float* p, const FevalCombine& f, const RedSlot& red, cudaStream_t st) {
+  static const int depth = [] {
+    const char* e = std::getenv("MPRKB_UF_TST");
+    return e ? std::atoi(e) : 4;
+  }();
+  if (depth <= 4) return update_feval_d<NA, FS, 4>(sp, k, alpha_src, x, p, f, red, st);
+  if (depth == 5) return update_feval_d<NA, FS, 5>(sp, k, alpha_src, x, p, f, red, st);
+  return update_feval_d<NA, FS, 6>(sp, k, alpha_src, x, p, f, red, st);
+}
+
+void update_feval(const StencilSpec& sp, const StencilSpec& k, const RedSlot& alpha_src, const float* x,
+                  const float* p, const FevalCombine& f, const RedSlot& red, cudaStream_t st) {
+  if (!update_feval_supported(sp, k))
+    MPRKB_THROW(10, "update_feval: needs the TMA stencils on an undivided grid (Dirichlet, n % 128 == 0)");
+  if (f.nacc > kMaxAcc) MPRKB_THROW(10, "update_feval: too many later stages");
+  if (!alpha_src.dpart || !alpha_src.count || *alpha_src.count <= 0)
+    MPRKB_THROW(10, "update_feval: alpha source has no device tuples");
+  if ((const void*)f.bout == (const void*)x || (const void*)f.xout == (const void*)x)
+    MPRKB_THROW(10, "update_feval: the next right-hand side must not overwrite b (neighbouring tiles read it)");
+  feval_dispatch(f, [&](auto na, auto fs) {
+    update_feval_n<decltype(na)::value, decltype(fs)::value>(sp, k, alpha_src, x, p, f, red, st);
+  });
 }
 
 // ---- p = z + beta p fused with q = A p, p.q (fp32, pipelined CG) -----------------

@@ -206,6 +206,10 @@ Stepper::Stepper(const StepperConfig& cfg)
     speculate_ = fused_ && !pull_ && !slab_.split() && cfg_.num == Numerics::Fast && cfg_.precond == 0 &&
                  !(e && e[0] == '0');
     if (speculate_) spec_rec_.alloc(sizeof(double) * 4 * (size_t)q);
+    const char* me = std::getenv("MPRKB_SPEC_MERGE");
+    spec_merge_ = speculate_ && me && me[0] == '1';  // (opt-in: measured no faster)
+    for (const StageSolver& S : solvers_)
+      spec_merge_ = spec_merge_ && S.op->stencil() && update_feval_supported(*S.op->stencil(), kspec_);
   }
   if (cfg_.krylov_storage >= 0) {
     // accessor-style CG vectors (accessor.cu): heat, CG, FAST numerics, the
@@ -462,7 +466,15 @@ void Stepper::step_fused(double* u, StepTrace& trace, bool speculate) {
   // x0 = rhs is the rhs buffer itself (the solver never writes b); the
   // solution lands in xs[0], free again once the previous stage's f
   // evaluations have read it.
-  auto solve = [&](int i) -> float* {
+  // Speculative merge (spec_merge_): stage i < q - 1 stops before its update
+  // (CgSpec::defer) and update_feval forms x1 = rhs + alpha z inside the f
+  // evaluation pass, writing the next rhs to the spare buffer — the two
+  // buffers then swap roles.
+  const bool merge = speculate && spec_merge_;
+  float* rhs = b32;
+  float* spare = xs[0];
+  const void* dir = nullptr;  // the deferred solve's direction z (null: x1 is in the returned buffer)
+  auto solve = [&](int i, bool defer) -> float* {
     StageSolver& S = solvers_[solver_of_stage_[i]];
     SolveReport rep;
     float* sol = nullptr;
@@ -470,9 +482,11 @@ void Stepper::step_fused(double* u, StepTrace& trace, bool speculate) {
     if (speculate) {
       spec.rec = spec_rec_.as<double>() + 4 * i;
       spec.fail = spec_fail;
+      spec.defer = defer;
     }
-    cg_solve<float>(*S.op, S.pre.get(), b32, b32, crit, cfg_.num, *w32_, rep, st_, tm, xs[0], &sol,
+    cg_solve<float>(*S.op, S.pre.get(), rhs, rhs, crit, cfg_.num, *w32_, rep, st_, tm, spare, &sol,
                     speculate ? &spec : nullptr);
+    dir = spec.dir;
     if (!rep.converged) trace.solver_failure = true;
     trace.solves.push_back(std::move(rep));
     return sol;
@@ -492,7 +506,7 @@ void Stepper::step_fused(double* u, StepTrace& trace, bool speculate) {
   const int last = q - 1;
   const bool fuse_final = fuse_final_;
   bool fin_started = false;  // acc_[q] holds u + earlier terms
-  float* cur = solve(0);  // stage i's solution
+  float* cur = solve(0, merge && q > 1);  // stage i's solution
   for (int i = 0; i + 1 < q; ++i) {
     const int nx = i + 1;
     FevalCombine f;
@@ -507,7 +521,7 @@ void Stepper::step_fused(double* u, StepTrace& trace, bool speculate) {
     f.ce = tau * t.ae(nx, i);
     f.hg = 1;
     f.cg = tau * t.ae(nx, nx);
-    f.bout = b32;
+    f.bout = rhs;
     f.xout = nullptr;  // x0 = rhs: the solver starts from b itself
     f.ovf_flag = check_slot(6, kOverflow);
     for (int k = nx + 1; k < q; ++k) {
@@ -530,11 +544,21 @@ void Stepper::step_fused(double* u, StepTrace& trace, bool speculate) {
       f.ae[a] = 0.0;
       fin_started = true;
     }
-    {
+    if (dir) {
+      f.bout = spare;
+      {
+        Bracket br(timer_, "stencil", st_);
+        update_feval(*solvers_[solver_of_stage_[i]].op->stencil(), kspec_, w32_->red.slot_dev(2), rhs,
+                     static_cast<const float*>(dir), f, w32_->red.slot_dev(3), st_);
+      }
+      cg_spec_judge(w32_->red.slot_dev(0), w32_->red.slot_dev(2), w32_->red.slot_dev(3), crit.tol,
+                    spec_rec_.as<double>() + 4 * i, spec_fail, st_);
+      std::swap(rhs, spare);
+    } else {
       Bracket br(timer_, "stencil", st_);
       feval_combine(kspec_, cur, f, st_);
     }
-    cur = solve(nx);
+    cur = solve(nx, merge && nx < last);
   }
   // last stage: its f_hi is evaluated inside the final pass itself (the stage
   // vector's finiteness checked first, so the update stays gated on it)

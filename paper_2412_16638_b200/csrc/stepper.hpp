@@ -66,6 +66,11 @@ class Stepper {
   // gated on the verdicts, and a failed speculation redoes the step without
   // it (MPRKB_SPECULATE=0: never)
   bool speculate_ = false;
+  // speculative stages 0..q-2 end in ONE pass: the solve's update fused with
+  // the stage's f evaluations (update_feval; opt-in, MPRKB_SPEC_MERGE=1: it
+  // cuts 52 -> 44 B/point but runs issue-bound at 4 CTAs/SM, and in a real
+  // step L2 already absorbs most of x1's round trip — no faster)
+  bool spec_merge_ = false;
   DevBuf spec_rec_;
   // the same pipeline in pull form (undivided grid): every right-hand side
   // and the final update re-evaluate f_hi / f_eps from the stored fp32 stage

@@ -614,27 +614,57 @@ def test_cg_device_loop_max_iter_and_breakdown_paths(gpu, mp):
         assert same_bits(a, b)
 
 
-def test_speculative_stage_solves_bitwise(gpu, mp):
-    """The fused pipeline's stage solves run speculatively (CgSpec: no host
-    round trip per solve; the device judges each one-iteration exit and gates
-    the final update): the state, iteration counts and residual histories are
-    bitwise those of the round-trip path (MPRKB_SPECULATE=0); a forced miss
-    (tolerance below the one-iteration reach) redoes the step and still
-    matches."""
+def _stepper_env(mp, env, *args, **kw):
     import os
 
-    t = mp.builtin("4s3pB")
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return mp.Stepper(*args, **kw)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+def _implicit_tableau(mp, q):  # all-implicit, every b_i != 0 (test_fused_pipeline_many_stages)
+    rng = np.random.default_rng(q)
+    ah = np.tril(rng.uniform(0.0, 0.2, (q, q)), -1)
+    ae = np.tril(rng.uniform(0.0, 0.05, (q, q)), -1) + np.diag(np.full(q, 0.5))
+    return mp.Tableau("custom", q, None, ah.tolist(), ae.tolist(), np.full(q, 1.0 / q).tolist())
+
+
+@pytest.mark.parametrize("name", ["4s3pB", "4s3pC", "custom7"])
+def test_speculative_stage_solves_bitwise(gpu, mp, name):
+    """The fused pipeline's stage solves run speculatively (CgSpec: no host
+    round trip per solve; the device judges each one-iteration exit and gates
+    the final update), stages 0..q-2 with the update merged into the f
+    evaluation pass (update_feval, opt-in MPRKB_SPEC_MERGE=1) or not: the
+    state, iteration counts and residual histories are bitwise those of the
+    round-trip path (MPRKB_SPECULATE=0); a
+    forced miss (tolerance below the one-iteration reach) redoes the step and
+    still matches.  custom7's stage 0 carries all six accumulators."""
+    t = _implicit_tableau(mp, 7) if name == "custom7" else mp.builtin(name)
     for tol, n in ((1e-3, 256), (1e-7, 128)):
-        spec = mp.Stepper("heat", n, t, 0.01, tol, "f32", 12)
-        os.environ["MPRKB_SPECULATE"] = "0"
-        try:
-            plain = mp.Stepper("heat", n, t, 0.01, tol, "f32", 12)
-        finally:
-            os.environ.pop("MPRKB_SPECULATE", None)
-        a, b = np.zeros(n ** 3), np.zeros(n ** 3)
+        args = ("heat", n, t, 0.01, tol, "f32", 12)
+        steppers = [_stepper_env(mp, {"MPRKB_SPEC_MERGE": "1"}, *args), mp.Stepper(*args),
+                    _stepper_env(mp, {"MPRKB_SPECULATE": "0"}, *args)]
+        u0 = np.asarray(mp.heat_exact(n, 0.05))
+        us = [u0.copy() for _ in steppers]
         for _ in range(2):
-            ta, tb = spec.step(a), plain.step(b)
-            assert ta == tb
-            for s in range(len(ta["iterations"])):
-                assert np.array_equal(spec.history(s), plain.history(s))
-        assert same_bits(a, b)
+            tr = [s.step(u) for s, u in zip(steppers, us)]
+            assert tr[0] == tr[1] == tr[2]
+            for s in range(len(tr[0]["iterations"])):
+                h = steppers[2].history(s)
+                assert np.array_equal(steppers[0].history(s), h)
+                assert np.array_equal(steppers[1].history(s), h)
+        assert same_bits(us[0], us[2]) and same_bits(us[1], us[2])
+        if tol == 1e-3:  # one-iteration solves: each merged stage drops the separate update pass
+            launched = []
+            for s, u in zip(steppers[:2], us[:2]):
+                l0 = mp.kernel_launches()
+                s.step(u)
+                launched.append(mp.kernel_launches() - l0)
+            assert launched[0] == launched[1] - (t.q - 1), launched
