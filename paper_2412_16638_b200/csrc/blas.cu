@@ -250,14 +250,34 @@ void tuple_sums(const RedSlot& slot, int ncomp, double* out, cudaStream_t st) {
   LAUNCHED("tuple_sums");
 }
 
-__global__ void __launch_bounds__(kRedLanes) k_cg_spec(const double* t0, int n0, const double* t2, int n2,
-                                                     const double* t3, int n3, double tol, double* rec, int* fail) {
+// Three warp groups sum the three slots' lane shares concurrently (one
+// 16-byte load per tuple for the pairs), then five threads add the 128 lanes
+// of one component each in lane order — every sum bitwise sum_partials'.
+__global__ void __launch_bounds__(3 * kRedLanes) k_cg_spec(const double* t0, int n0, const double* t2, int n2,
+                                                         const double* t3, int n3, double tol, double* rec, int* fail) {
   pdl_wait();
   pdl_trigger();
-  const double r0s = sum_partials(t0, n0, 0);
-  const double pqs = sum_partials(t2, n2, 0), rzs = sum_partials(t2, n2, 1);
-  const double f0 = sum_partials(t3, n3, 0), f1 = sum_partials(t3, n3, 1);
+  __shared__ double lanes[5][kRedLanes];
+  __shared__ double tot[5];
+  const int t = threadIdx.x % kRedLanes, grp = threadIdx.x / kRedLanes;
+  if (grp == 0) {
+    double s = 0.0;
+    for (int b = t; b < n0; b += kRedLanes) s += __ldcg(t0 + 2 * (size_t)b);
+    lanes[0][t] = s;
+  } else {
+    const double2 v = lane_partials2(grp == 1 ? t2 : t3, grp == 1 ? n2 : n3, t);
+    lanes[2 * grp - 1][t] = v.x;
+    lanes[2 * grp][t] = v.y;
+  }
+  __syncthreads();
+  if (threadIdx.x < 5) {
+    double s = 0.0;
+    for (int l = 0; l < kRedLanes; ++l) s += lanes[threadIdx.x][l];
+    tot[threadIdx.x] = s;
+  }
+  __syncthreads();
   if (threadIdx.x != 0) return;
+  const double r0s = tot[0], pqs = tot[1], rzs = tot[2], f0 = tot[3], f1 = tot[4];
   // krylov.cpp: r0 = (double)sqrt((R)v0); rnorm / rt likewise; rz, pq = (R) sums
   const double r0 = (double)sqrtf(__double2float_rn(r0s));
   const double rn = (double)sqrtf(__double2float_rn(f0)), rt = (double)sqrtf(__double2float_rn(f1));
@@ -274,7 +294,7 @@ __global__ void __launch_bounds__(kRedLanes) k_cg_spec(const double* t0, int n0,
 void cg_spec_judge(const RedSlot& s0, const RedSlot& s2, const RedSlot& s3, double tol, double* rec, int* fail,
                    cudaStream_t st) {
   if (!s0.dpart || !s2.dpart || !s3.dpart) MPRKB_THROW(10, "cg_spec_judge: the reductions need device tuples");
-  launch_pdl(k_cg_spec, dim3(1), dim3(kRedLanes), 0, st, (const double*)s0.dpart, *s0.count, (const double*)s2.dpart,
+  launch_pdl(k_cg_spec, dim3(1), dim3(3 * kRedLanes), 0, st, (const double*)s0.dpart, *s0.count, (const double*)s2.dpart,
              *s2.count, (const double*)s3.dpart, *s3.count, tol, rec, fail);
   LAUNCHED("cg_spec");
 }

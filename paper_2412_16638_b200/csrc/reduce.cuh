@@ -63,6 +63,30 @@ __device__ __forceinline__ void grid_reduce(double (&v)[NV], const RedSlot& s) {
     }
 }
 
+// Lane t's share of components 0 and 1 of a reduction's n device tuples
+// (tuples t, t + kRedLanes, ... added in that order, one 16-byte load per
+// tuple; dp 16-byte aligned, as Reducer::slot_dev's copies are): each
+// component equals sum_partials' lane sum bitwise.
+__device__ __forceinline__ double2 lane_partials2(const double* dp, int n, int t) {
+  const double2* d2 = reinterpret_cast<const double2*>(dp);
+  double s0 = 0.0, s1 = 0.0;
+  int b = t;
+  for (; b + 3 * kRedLanes < n; b += 4 * kRedLanes) {
+    const double2 v0 = __ldcg(d2 + b), v1 = __ldcg(d2 + b + kRedLanes);
+    const double2 v2 = __ldcg(d2 + b + 2 * kRedLanes), v3 = __ldcg(d2 + b + 3 * kRedLanes);
+    s0 += v0.x; s1 += v0.y;
+    s0 += v1.x; s1 += v1.y;
+    s0 += v2.x; s1 += v2.y;
+    s0 += v3.x; s1 += v3.y;
+  }
+  for (; b < n; b += kRedLanes) {
+    const double2 v = __ldcg(d2 + b);
+    s0 += v.x;
+    s1 += v.y;
+  }
+  return make_double2(s0, s1);
+}
+
 // Component c of a reduction's n device tuples in the host's order (types.hpp
 // kRedLanes); called by all threads of a kRedLanes-thread block, result in
 // every thread.
@@ -121,6 +145,28 @@ __device__ __forceinline__ void cdot_acc(double (&v)[2], cplx<R> a, cplx<R> b) {
   v[0] = __fma_rn((double)a.im, (double)b.im, v[0]);
   v[1] = __fma_rn((double)a.re, (double)b.im, v[1]);
   v[1] = __fma_rn(-(double)a.im, (double)b.re, v[1]);
+}
+
+// Components 0 and 1 together (lane_partials2): each equals
+// sum_partials(dp, n, c) bitwise, with one round of loads instead of two.
+__device__ __forceinline__ double2 sum_partials2(const double* dp, int n) {
+  __shared__ double2 lanes2[kRedLanes];
+  const int t = threadIdx.x;
+  __syncthreads();
+  if (t < kRedLanes) lanes2[t] = lane_partials2(dp, n, t);
+  __syncthreads();
+  double a = 0.0, b = 0.0;
+  for (int l = 0; l < kRedLanes; l += 16) {
+    double2 x[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) x[u] = lanes2[l + u];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      a += x[u].x;
+      b += x[u].y;
+    }
+  }
+  return make_double2(a, b);
 }
 
 }  // namespace mprkb

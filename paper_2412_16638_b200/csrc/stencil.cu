@@ -1214,7 +1214,8 @@ __global__ void __launch_bounds__(TTHREADS)
     // alpha = r.z / p.Ap from the previous pass's tuples, summed and rounded
     // as the host does (krylov.cpp: (R)rz / (R)pq), so no host round trip
     // sits between the two kernels
-    const double pq = sum_partials(apart, an, 0), rz = sum_partials(apart, an, 1);
+    const double2 tp = sum_partials2(apart, an);  // (p.Ap, r.z)
+    const double pq = tp.x, rz = tp.y;
     alpha = __fdiv_rn(__double2float_rn(rz), __double2float_rn(pq));
   }
   extern __shared__ unsigned char smem_raw[];
@@ -1469,7 +1470,8 @@ __global__ void __launch_bounds__(TTHREADS, Epi::kMinBlocks)
   pdl_trigger();
   float alpha;
   {
-    const double pq = sum_partials(apart, an, 0), rz = sum_partials(apart, an, 1);
+    const double2 tp = sum_partials2(apart, an);  // (p.Ap, r.z)
+    const double pq = tp.x, rz = tp.y;
     alpha = __fdiv_rn(__double2float_rn(rz), __double2float_rn(pq));
   }
   extern __shared__ unsigned char smem_raw[];
