@@ -318,7 +318,7 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
         // below (r0 already small, breakdown) x is untouched
         {
           Bracket br(timer, "stencil", st);
-          cg_fused_update(*S, 0.0f, &s2, x, z, b, r, x_alt, s3, st);
+          cg_fused_update(*S, 0.0f, &s2, x, z, b, r, x_alt, s3, st, nullptr, 0, speculate ? spec->x1_finite : nullptr);
         }
         if (speculate) {
           // no round trip: the device judges the one-iteration exit; the

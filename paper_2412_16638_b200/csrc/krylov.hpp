@@ -51,6 +51,9 @@ struct CgSpec {
   // not take the speculative path)
   bool defer = false;
   const void* dir = nullptr;
+  // x1_finite (nullable): set when x1 holds a NaN or infinity (the stage
+  // vector's check_finite folded into the fused update)
+  int* x1_finite = nullptr;
 };
 
 // Per-label device-time accumulator (TimingRegistry, timing.hpp:23-47) fed by

@@ -61,9 +61,11 @@ void cg_ctl_step(CgCtl* ctl, const RedSlot& upd, int rcomp, int rzcomp, const Re
 // gathered (split grid, nullable): the all-gathered per-rank (p.Ap, r.z)
 // pairs of `ranks` ranks ([rank][2], device); alpha = (float)sum rz /
 // (float)sum pq summed in rank order, as Comm::allreduce_sum does
+// finite_flag (nullable): set when x1 holds a NaN or infinity (check_finite of
+// the stage vector folded into the pass that writes it)
 void cg_fused_update(const StencilSpec& s, float alpha, const RedSlot* alpha_src, const float* x, const float* p,
                      const float* b, const float* r, float* x1, const RedSlot& red, cudaStream_t st,
-                     const double* gathered = nullptr, int ranks = 0);
+                     const double* gathered = nullptr, int ranks = 0, int* finite_flag = nullptr);
 // out[c] = component c (< ncomp) of slot's device tuples summed in the host's
 // order (reduce.cuh sum_partials): a rank's local value of a reduction, on the device
 void tuple_sums(const RedSlot& slot, int ncomp, double* out, cudaStream_t st);

@@ -1198,7 +1198,8 @@ __global__ void __launch_bounds__(TTHREADS)
                const __grid_constant__ CUtensorMap xlo, const __grid_constant__ CUtensorMap xhi,
                const __grid_constant__ CUtensorMap plo, const __grid_constant__ CUtensorMap phi, int has_lo,
                int has_hi, int n, int nz, int kc, float s, float g, float alpha, const double* apart, int an,
-               const float* __restrict__ b, const float* __restrict__ r, float* __restrict__ x1, RedSlot red) {
+               const float* __restrict__ b, const float* __restrict__ r, float* __restrict__ x1, RedSlot red,
+               int* finite_flag) {
   pdl_wait();
   pdl_trigger();
   if (apart && an < 0) {
@@ -1270,6 +1271,7 @@ __global__ void __launch_bounds__(TTHREADS)
     return o;
   };
   double acc[2] = {0.0, 0.0};  // ||r1||^2, ||b - A x1||^2
+  bool bad = false;             // x1 not finite
   const long nn = n, n2 = nn * nn;
   const int col = 4 + 4 * lane;
   auto gidx = [&](int row, int k) { return (i0 + 4 * lane) + (long)(j0 + row) * nn + (long)k * n2; };
@@ -1343,6 +1345,7 @@ __global__ void __launch_bounds__(TTHREADS)
         const float av = point<float>(0, s, g, 0.0f, c.x[e], al, ar, ym.x[e], yp.x[e], zm.x[e], zp.x[e]);
         const float t = xsub(pb[rr].x[e], av);  // EpiResidual's b - A x
         dot_acc(*reinterpret_cast<double(*)[1]>(&acc[1]), t, t);
+        bad |= !isfinite(c.x[e]);
       }
       st4(x1 + gi, c);
     }
@@ -1357,6 +1360,7 @@ __global__ void __launch_bounds__(TTHREADS)
     __syncthreads();
     if (tid == 0 && q - 1 + CG_TST < planes) issue(q - 1 + CG_TST);
   }
+  if (bad && finite_flag) *finite_flag = 1;
   grid_reduce<2>(acc, red);
 }
 
@@ -1368,7 +1372,7 @@ bool pq_fused_ok(const StencilSpec& k) { return pq_fused_supported(k); }
 
 void cg_fused_update(const StencilSpec& sp, float alpha, const RedSlot* alpha_src, const float* x, const float* p,
                      const float* b, const float* r, float* x1, const RedSlot& red, cudaStream_t st,
-                     const double* gathered, int ranks) {
+                     const double* gathered, int ranks, int* finite_flag) {
   if (!cg_fused_supported(sp)) MPRKB_THROW(10, "cg_fused_update: needs the TMA stencil (Dirichlet, n % 128 == 0)");
   const int n = sp.n, nz = sp.nz > 0 ? sp.nz : n;
   constexpr size_t smem = cg_fused_smem();
@@ -1439,7 +1443,7 @@ void cg_fused_update(const StencilSpec& sp, float alpha, const RedSlot* alpha_sr
   if (!gathered && alpha_src && (!apart || an <= 0)) MPRKB_THROW(10, "cg_fused_update: alpha source has no device tuples");
   // x0 = b (x aliases b): the SELF pass re-forms b and r from x's tile
   launch_pdl(x == b ? k_cg_fused<true> : k_cg_fused<false>, grid, dim3(TTHREADS), smem, st, xmap, pmap, gm[0], gm[1], gm[2], gm[3], has_lo, has_hi, n,
-             nz, chunk, (float)sp.sigma, (float)sp.gamma, alpha, apart, an, b, r, x1, rs);
+             nz, chunk, (float)sp.sigma, (float)sp.gamma, alpha, apart, an, b, r, x1, rs, finite_flag);
   note_partials(rs, grid.x * grid.y * grid.z);
   note_kron(true, 2);  // A p and the true residual's A x1
   LAUNCHED("cg_fused_update");
@@ -1818,6 +1822,12 @@ void pq_fused(const StencilSpec& sp, const float* z, const float* p, const RedSl
 // (z.Az, r.z) without storing Az: z (with its halo) and r stream through one
 // TMA ring instead of r by per-thread loads, whose short prefetch left the
 // read-only pass latency-bound.
+// D ring slots of one z plane (with halo) + r's tile (no halo)
+constexpr int D2_SLOT = CG_SLOT + TI * TJ;
+template <int D>
+constexpr size_t d2_smem() { return (size_t)D * D2_SLOT * sizeof(float) + D * sizeof(uint64_t) + 128; }
+
+template <int D>
 __global__ void __launch_bounds__(TTHREADS)
     k_dots2_tma(const __grid_constant__ CUtensorMap zmap, const __grid_constant__ CUtensorMap rmap, int n, int nz,
                 int kc, float s, float g, RedSlot red) {
@@ -1825,7 +1835,7 @@ __global__ void __launch_bounds__(TTHREADS)
   pdl_trigger();
   extern __shared__ unsigned char smem_raw[];
   float* buf = reinterpret_cast<float*>(smem_align128(smem_raw));
-  uint64_t* full = reinterpret_cast<uint64_t*>(buf + CG_TST * 2 * CG_SLOT);
+  uint64_t* full = reinterpret_cast<uint64_t*>(buf + D * D2_SLOT);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int i0 = blockIdx.x * TI, j0 = blockIdx.y * TJ;
   int k0, k1;
@@ -1833,23 +1843,23 @@ __global__ void __launch_bounds__(TTHREADS)
   const int planes = k1 - k0 + 2;
   constexpr uint32_t zbytes = (TJ + 2) * TW * sizeof(float), rbytes = TJ * TI * sizeof(float);
   if (tid == 0) {
-    for (int b = 0; b < CG_TST; ++b) mbar_init(&full[b], 1);
+    for (int b = 0; b < D; ++b) mbar_init(&full[b], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   const CUtensorMap* zm = &zmap;
   const CUtensorMap* rm = &rmap;
   auto issue = [&](int qq) {  // z plane k0 - 1 + qq (+ r's plane when it is computed)
-    const int k = k0 - 1 + qq, sl = qq % CG_TST;
-    float* dst = buf + sl * 2 * CG_SLOT;
+    const int k = k0 - 1 + qq, sl = qq % D;
+    float* dst = buf + sl * D2_SLOT;
     const bool with_r = k >= k0 && k < k1;
     mbar_expect_tx(&full[sl], zbytes + (with_r ? rbytes : 0));
     tma_3d(dst, zm, i0 - 4, j0 - 1, k, &full[sl]);
     if (with_r) tma_3d(dst + CG_SLOT, rm, i0, j0, k, &full[sl]);
   };
   if (tid == 0)
-    for (int qq = 0; qq < CG_TST && qq < planes; ++qq) issue(qq);
-  auto wait = [&](int qq) { mbar_wait(&full[qq % CG_TST], (uint32_t)(qq / CG_TST) & 1u); };
+    for (int qq = 0; qq < D && qq < planes; ++qq) issue(qq);
+  auto wait = [&](int qq) { mbar_wait(&full[qq % D], (uint32_t)(qq / D) & 1u); };
   auto ld = [](const float* ptr) {
     const float4 f = *reinterpret_cast<const float4*>(ptr);
     V4<float> v;
@@ -1865,9 +1875,9 @@ __global__ void __launch_bounds__(TTHREADS)
       wait(1);
     }
     wait(qq + 1);
-    const float* bm = buf + ((qq - 1) % CG_TST) * 2 * CG_SLOT;
-    const float* bc = buf + (qq % CG_TST) * 2 * CG_SLOT;
-    const float* bp = buf + ((qq + 1) % CG_TST) * 2 * CG_SLOT;
+    const float* bm = buf + ((qq - 1) % D) * D2_SLOT;
+    const float* bc = buf + (qq % D) * D2_SLOT;
+    const float* bp = buf + ((qq + 1) % D) * D2_SLOT;
 #pragma unroll
     for (int rr = 0; rr < TROWS; ++rr) {
       const int row = warp * TROWS + rr;
@@ -1889,22 +1899,22 @@ __global__ void __launch_bounds__(TTHREADS)
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
-    if (tid == 0 && qq - 1 + CG_TST < planes) issue(qq - 1 + CG_TST);
+    if (tid == 0 && qq - 1 + D < planes) issue(qq - 1 + D);
   }
   grid_reduce<2>(acc, red);
 }
 
-bool dots2_tma(const StencilSpec& sp, const float* z, const float* r, const RedSlot& red, cudaStream_t st) {
-  if (!pq_fused_supported(sp)) return false;
+template <int D>
+static void dots2_tma_d(const StencilSpec& sp, const float* z, const float* r, const RedSlot& red, cudaStream_t st) {
   const int n = sp.n, nz = sp.nz > 0 ? sp.nz : n;
-  constexpr size_t smem = cg_fused_smem();
+  constexpr size_t smem = d2_smem<D>();
   static thread_local int chunk = 0;  // (per host thread: in-process ranks launch concurrently)
   static thread_local long chunk_cols = -1;
   static thread_local int resident = 0;
   if (!resident) {
-    CUDA_CHECK(cudaFuncSetAttribute(k_dots2_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_CHECK(cudaFuncSetAttribute(k_dots2_tma<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dots2_tma, TTHREADS, smem));
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dots2_tma<D>, TTHREADS, smem));
     resident = std::max(1, per_sm) * sm_count();
   }
   const long cols = (long)(n / TI) * (n / TJ);
@@ -1931,11 +1941,23 @@ bool dots2_tma(const StencilSpec& sp, const float* z, const float* r, const RedS
   RedSlot rs = red;
   rs.base = 0;
   rs.total = 0;
-  launch_pdl(k_dots2_tma, grid, dim3(TTHREADS), smem, st, zmap, rmap, n, nz, chunk, (float)sp.sigma, (float)sp.gamma,
+  launch_pdl(k_dots2_tma<D>, grid, dim3(TTHREADS), smem, st, zmap, rmap, n, nz, chunk, (float)sp.sigma, (float)sp.gamma,
              rs);
   note_partials(rs, grid.x * grid.y * grid.z);
   note_kron(true);
   LAUNCHED("dots2_tma");
+}
+
+bool dots2_tma(const StencilSpec& sp, const float* z, const float* r, const RedSlot& red, cudaStream_t st) {
+  if (!pq_fused_supported(sp)) return false;
+  static const int depth = [] {
+    const char* e = std::getenv("MPRKB_D2_TST");  // (ring depth: 5 measured 29.2 -> 28.8 us at 256^3; 6+ lose a CTA/SM)
+    return e ? std::atoi(e) : 5;
+  }();
+  if (depth <= 4) dots2_tma_d<4>(sp, z, r, red, st);
+  else if (depth == 5) dots2_tma_d<5>(sp, z, r, red, st);
+  else if (depth == 6) dots2_tma_d<6>(sp, z, r, red, st);
+  else dots2_tma_d<8>(sp, z, r, red, st);
   return true;
 }
 

@@ -474,6 +474,11 @@ void Stepper::step_fused(double* u, StepTrace& trace, bool speculate) {
   float* rhs = b32;
   float* spare = xs[0];
   const void* dir = nullptr;  // the deferred solve's direction z (null: x1 is in the returned buffer)
+  const int last = q - 1;
+  const bool fuse_final = fuse_final_;
+  // the last stage vector's finiteness check: folded into a speculative
+  // solve's fused update (x1 is the stage vector), else check_finite32
+  int* last_finite = nullptr;
   auto solve = [&](int i, bool defer) -> float* {
     StageSolver& S = solvers_[solver_of_stage_[i]];
     SolveReport rep;
@@ -483,6 +488,7 @@ void Stepper::step_fused(double* u, StepTrace& trace, bool speculate) {
       spec.rec = spec_rec_.as<double>() + 4 * i;
       spec.fail = spec_fail;
       spec.defer = defer;
+      if (i == last && fuse_final) spec.x1_finite = last_finite = check_slot(9, kStage);
     }
     cg_solve<float>(*S.op, S.pre.get(), rhs, rhs, crit, cfg_.num, *w32_, rep, st_, tm, spare, &sol,
                     speculate ? &spec : nullptr);
@@ -503,8 +509,6 @@ void Stepper::step_fused(double* u, StepTrace& trace, bool speculate) {
   // acc_[q], in the reference's term order (u, then i ascending), while each
   // f_hi is in registers — so no f_hi is stored; the last stage's term is
   // added by the final pass (MPRKB_FUSED_FINAL=0: stored f_hi + final_update)
-  const int last = q - 1;
-  const bool fuse_final = fuse_final_;
   bool fin_started = false;  // acc_[q] holds u + earlier terms
   float* cur = solve(0, merge && q > 1);  // stage i's solution
   for (int i = 0; i + 1 < q; ++i) {
@@ -563,7 +567,8 @@ void Stepper::step_fused(double* u, StepTrace& trace, bool speculate) {
   // last stage: its f_hi is evaluated inside the final pass itself (the stage
   // vector's finiteness checked first, so the update stays gated on it)
   if (fuse_final) {
-    check_finite32(m, cur, check_slot(9, kStage), st_);
+    if (!last_finite || !trace.solves.back().speculative)
+      check_finite32(m, cur, last_finite ? last_finite : check_slot(9, kStage), st_);
   } else if (t.b[last] != 0.0) {
     Bracket br(timer_, "stencil", st_);
     apply_f64(kspec_, nullptr, cur, g64_.as<double>(), f_hi_[last].as<double>(), check_slot(9, kStage), st_);
