@@ -1283,16 +1283,32 @@ __global__ void __launch_bounds__(TTHREADS)
       pr[rr] = ld4(r + gidx(warp * TROWS + rr, k0));
     }
   }
+  // x1 at this warp's rows of planes k - 1 and k, carried across the march
+  // (each x1 value is formed once per plane — the same operation on the same
+  // operands as forming it per use, so bitwise unchanged)
+  V4<float> x1m[TROWS], x1c[TROWS];
   for (int k = k0; k < k1; ++k) {
     const int q = k - k0 + 1;
     if (k == k0) {
       wait(0);
       wait(1);
+#pragma unroll
+      for (int rr = 0; rr < TROWS; ++rr) {
+        const int o = (warp * TROWS + rr + 1) * TW + col;
+        x1m[rr] = upd4(ld(buf + o), ld(buf + CG_SLOT + o));
+        x1c[rr] = upd4(ld(buf + 2 * CG_SLOT + o), ld(buf + 3 * CG_SLOT + o));
+      }
     }
     wait(q + 1);
     const float* xmn = buf + ((q - 1) % CG_TST) * 2 * CG_SLOT;
     const float* xc = buf + (q % CG_TST) * 2 * CG_SLOT;
     const float* xpl = buf + ((q + 1) % CG_TST) * 2 * CG_SLOT;
+    V4<float> x1n[TROWS];
+#pragma unroll
+    for (int rr = 0; rr < TROWS; ++rr) {
+      const int o = (warp * TROWS + rr + 1) * TW + col;
+      x1n[rr] = upd4(ld(xpl + o), ld(xpl + CG_SLOT + o));
+    }
     V4<float> nb[TROWS], nr[TROWS];
     if (!SELF) {
 #pragma unroll
@@ -1328,9 +1344,10 @@ __global__ void __launch_bounds__(TTHREADS)
           pr[rr].x[e] = xsub(xcv.x[e], v);  // EpiResidualSelf's r
         }
       }
-      const V4<float> c = upd4(xcv, pc);
-      const V4<float> ym = upd4(xym, pym), yp = upd4(xyp, pyp);
-      const V4<float> zm = upd4(xzm, pzm), zp = upd4(xzp, pzp);
+      const V4<float> c = x1c[rr];
+      const V4<float> ym = rr > 0 ? x1c[rr > 0 ? rr - 1 : 0] : upd4(xym, pym);
+      const V4<float> yp = rr + 1 < TROWS ? x1c[rr + 1 < TROWS ? rr + 1 : 0] : upd4(xyp, pyp);
+      const V4<float> zm = x1m[rr], zp = x1n[rr];
       float xl = shfl_up1(c.x[3]), xr = shfl_down1(c.x[0]);
       if (lane == 0) xl = upd(xc[o - 1], pl);
       if (lane == 31) xr = upd(xc[o + 4], pr_);
@@ -1355,6 +1372,11 @@ __global__ void __launch_bounds__(TTHREADS)
         pb[rr] = nb[rr];
         pr[rr] = nr[rr];
       }
+    }
+#pragma unroll
+    for (int rr = 0; rr < TROWS; ++rr) {
+      x1m[rr] = x1c[rr];
+      x1c[rr] = x1n[rr];
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
