@@ -131,6 +131,25 @@ def test_split_fast_tensor_cores_256(gpu, mp, ranks):
     assert np.linalg.norm(got - exact) <= 2 * own
 
 
+@pytest.mark.parametrize("ranks", [2, 4])
+def test_split_config3_512(gpu, mp, ranks):
+    """Config 3's size (BASELINE.json configs[2]: heat 512^3, k-slabs): one
+    4s3pB fp32 FAST step on 2 / 4 in-process ranks against the undivided
+    512^3 step, with the 256^3 test's bar — within 2x the fp32 policy's own
+    distance from the fp64-policy step; iteration counts equal.  (The
+    reference needs ~18 min per 4s3pB step at 512^3 on 8 cores, SURVEY.md
+    §8d, so the size-independent split-vs-undivided property is the check.)"""
+    make = maker(mp, "heat", 512, "4s3pB", "f32", "fast", 1e-3)
+    want, wtr, _ = run_whole(mp, 1, make)
+    exact, _, _ = run_whole(mp, 1, maker(mp, "heat", 512, "4s3pB", "f64", "fast", 1e-5))
+    got, gtr, _ = run_split(mp, ranks, 1, make)
+    assert [t["iterations"] for t in gtr] == [t["iterations"] for t in wtr]
+    own = np.linalg.norm(want - exact)
+    assert own > 0
+    assert np.linalg.norm(got - want) <= 2 * own, (np.linalg.norm(got - want), own)
+    assert np.linalg.norm(got - exact) <= 2 * own
+
+
 def test_split_block_jacobi_fp16(gpu, mp):
     """Multi-iteration CG with the block-Jacobi extension (x-line blocks stay
     inside a slab) and fp16 block storage."""
