@@ -194,7 +194,8 @@ void vsub(size_t m, const T* b, const T* q, T* r, const RedSlot* red, cudaStream
   LAUNCHED("vsub");
 }
 
-// x += alpha p; r -= alpha q  (+ r.r)   (krylov.hpp:134-137)
+// x += alpha p; r -= alpha q  (+ r.r)   (krylov.hpp:134-137); x may be null
+// (r only: the fused first update's continuing path)
 template <class T, bool RED>
 __global__ void __launch_bounds__(kBlock) k_cg_update(size_t m, real_t<T> alpha, T* x, const T* p, T* r,
                                                       const T* q, RedSlot red) {
@@ -204,19 +205,24 @@ __global__ void __launch_bounds__(kBlock) k_cg_update(size_t m, real_t<T> alpha,
   for_each4(
       m,
       [&](size_t i) {
-        V4<T> xv = ld4rw(x + i), rv = ld4rw(r + i);
-        const V4<T> pv = ld4(p + i), qv = ld4(q + i);
+        V4<T> rv = ld4rw(r + i);
+        const V4<T> qv = ld4(q + i);
+        if (x) {
+          V4<T> xv = ld4rw(x + i);
+          const V4<T> pv = ld4(p + i);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) xv.x[e] = xadd(xv.x[e], xscale(alpha, pv.x[e]));
+          st4(x + i, xv);
+        }
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          xv.x[e] = xadd(xv.x[e], xscale(alpha, pv.x[e]));
           rv.x[e] = xsub(rv.x[e], xscale(alpha, qv.x[e]));
           if (RED) dot_acc(v, rv.x[e], rv.x[e]);
         }
-        st4(x + i, xv);
         st4(r + i, rv);
       },
       [&](size_t i) {
-        x[i] = xadd(x[i], xscale(alpha, ldg(p + i)));
+        if (x) x[i] = xadd(x[i], xscale(alpha, ldg(p + i)));
         const T rv = xsub(r[i], xscale(alpha, ldg(q + i)));
         r[i] = rv;
         if (RED) dot_acc(v, rv, rv);

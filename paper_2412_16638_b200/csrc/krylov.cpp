@@ -518,7 +518,7 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
         } else {
           Bracket br(timer, "stencil", st);
           stencil_apply<T>(*S, p, q, st);
-          cg_update<T>(m, alpha, z, p, r, q, nullptr, st);  // r -= alpha q (z is scratch here)
+          cg_update<T>(m, alpha, nullptr, p, r, q, nullptr, st);  // r -= alpha q only
         }
       } else if (pipe) {
         const RedSlot s1d = w.red.slot_dev(1);
