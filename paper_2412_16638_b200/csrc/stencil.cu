@@ -123,6 +123,17 @@ __device__ __forceinline__ cplx<R> shfl_down1(cplx<R> v) {
   return {__shfl_down_sync(0xffffffffu, v.re, 1), __shfl_down_sync(0xffffffffu, v.im, 1)};
 }
 
+// The warp-edge neighbour of a TMA tile row, branch-free: lane 0 reads
+// row[-1] (its left neighbour), lane 31 row[4] (its right one), every other
+// lane lane 0's address (a broadcast: no extra shared-memory wavefront); the
+// caller selects it with lane == 0 / lane == 31 over the shuffled values.
+// `row` = the lane's own 4 columns.  (Branches here cost ~8 issue slots per
+// row: BSSY / BRA / BSYNC around two scalar loads.)
+template <class Raw>
+__device__ __forceinline__ Raw edge_ld(const Raw* row, int lane) {
+  return row[lane == 31 ? 4 : -1 - 4 * lane];
+}
+
 // The reference's arithmetic for one point (operators.hpp:133-140, 149-158);
 // xl/xr/ym/yp/zm/zp are the i-1, i+1, j-1, j+1, k-1, k+1 neighbours.
 template <class T>
@@ -842,8 +853,15 @@ __global__ void __launch_bounds__(TTHREADS, tma_min_blocks<Epi>())
       const V4<T> zm = ld(pm + o), zp = ld(pp + o);
       T left = shfl_up1(c.x[3]);
       T right = shfl_down1(c.x[0]);
-      if (lane == 0) left = src.cv(pc[o - 1]);
-      if (lane == 31) right = src.cv(pc[o + 4]);
+      Raw ev{};
+      if constexpr (std::is_same_v<Raw, T>) {  // (no conversion: select, no branch)
+        ev = edge_ld(pc + o, lane);
+        left = lane == 0 ? ev : left;
+        right = lane == 31 ? ev : right;
+      } else {
+        if (lane == 0) left = src.cv(pc[o - 1]);
+        if (lane == 31) right = src.cv(pc[o + 4]);
+      }
       V4<T> v;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -860,8 +878,9 @@ __global__ void __launch_bounds__(TTHREADS, tma_min_blocks<Epi>())
         const float ymv[4] = {ym32.x, ym32.y, ym32.z, ym32.w}, ypv[4] = {yp32.x, yp32.y, yp32.z, yp32.w};
         const float zmv[4] = {zm32.x, zm32.y, zm32.z, zm32.w}, zpv[4] = {zp32.x, zp32.y, zp32.z, zp32.w};
         float l32 = shfl_up1(cc[3]), r32 = shfl_down1(cc[0]);
-        if (lane == 0) l32 = pc[o - 1];
-        if (lane == 31) r32 = pc[o + 4];
+        const float e32 = edge_ld(pc + o, lane);
+        l32 = lane == 0 ? e32 : l32;
+        r32 = lane == 31 ? e32 : r32;
         V4<float> v32;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
@@ -1327,15 +1346,16 @@ __global__ void __launch_bounds__(TTHREADS)
       const V4<float> pym = ld(xc + CG_SLOT + o - TW), pyp = ld(xc + CG_SLOT + o + TW);
       const V4<float> pzm = ld(xmn + CG_SLOT + o), pzp = ld(xpl + CG_SLOT + o);
       float pl = shfl_up1(pc.x[3]), pr_ = shfl_down1(pc.x[0]);
-      if (lane == 0) pl = xc[CG_SLOT + o - 1];
-      if (lane == 31) pr_ = xc[CG_SLOT + o + 4];
+      const float pe = edge_ld(xc + CG_SLOT + o, lane), xe = edge_ld(xc + o, lane);
+      pl = lane == 0 ? pe : pl;
+      pr_ = lane == 31 ? pe : pr_;
       // x neighbourhood (SELF: b's, for r = b - A b) and x1's -> A x1
       const V4<float> xcv = ld(xc + o), xym = ld(xc + o - TW), xyp = ld(xc + o + TW);
       const V4<float> xzm = ld(xmn + o), xzp = ld(xpl + o);
       if (SELF) {
         float bl = shfl_up1(xcv.x[3]), br = shfl_down1(xcv.x[0]);
-        if (lane == 0) bl = xc[o - 1];
-        if (lane == 31) br = xc[o + 4];
+        bl = lane == 0 ? xe : bl;
+        br = lane == 31 ? xe : br;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float l = e == 0 ? bl : xcv.x[e - 1], rgt = e == 3 ? br : xcv.x[e + 1];
@@ -1349,8 +1369,9 @@ __global__ void __launch_bounds__(TTHREADS)
       const V4<float> yp = rr + 1 < TROWS ? x1c[rr + 1 < TROWS ? rr + 1 : 0] : upd4(xyp, pyp);
       const V4<float> zm = x1m[rr], zp = x1n[rr];
       float xl = shfl_up1(c.x[3]), xr = shfl_down1(c.x[0]);
-      if (lane == 0) xl = upd(xc[o - 1], pl);
-      if (lane == 31) xr = upd(xc[o + 4], pr_);
+      const float x1e = upd(xe, pe);  // (lane 0: x1 left of the warp; lane 31: right)
+      xl = lane == 0 ? x1e : xl;
+      xr = lane == 31 ? x1e : xr;
       const long gi = gidx(row, k);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -1571,19 +1592,21 @@ __global__ void __launch_bounds__(TTHREADS, Epi::kMinBlocks)
       const V4<float> pym = ld(xc + CG_SLOT + o - TW), pyp = ld(xc + CG_SLOT + o + TW);
       const V4<float> pzm = ld(xmn + CG_SLOT + o), pzp = ld(xpl + CG_SLOT + o);
       float pl = shfl_up1(pc.x[3]), pr_ = shfl_down1(pc.x[0]);
-      if (lane == 0) pl = xc[CG_SLOT + o - 1];
-      if (lane == 31) pr_ = xc[CG_SLOT + o + 4];
+      const float pe = edge_ld(xc + CG_SLOT + o, lane), xe = edge_ld(xc + o, lane);
+      pl = lane == 0 ? pe : pl;
+      pr_ = lane == 31 ? pe : pr_;
       const V4<float> xcv = ld(xc + o), xym = ld(xc + o - TW), xyp = ld(xc + o + TW);
       const V4<float> xzm = ld(xmn + o), xzp = ld(xpl + o);
       float bl = shfl_up1(xcv.x[3]), br = shfl_down1(xcv.x[0]);
-      if (lane == 0) bl = xc[o - 1];
-      if (lane == 31) br = xc[o + 4];
+      bl = lane == 0 ? xe : bl;
+      br = lane == 31 ? xe : br;
       const V4<float> c = upd4(xcv, pc);
       const V4<float> ym = upd4(xym, pym), yp = upd4(xyp, pyp);
       const V4<float> zm = upd4(xzm, pzm), zp = upd4(xzp, pzp);
       float xl = shfl_up1(c.x[3]), xr = shfl_down1(c.x[0]);
-      if (lane == 0) xl = upd(xc[o - 1], pl);
-      if (lane == 31) xr = upd(xc[o + 4], pr_);
+      const float x1e = upd(xe, pe);  // (lane 0: x1 left of the warp; lane 31: right)
+      xl = lane == 0 ? x1e : xl;
+      xr = lane == 31 ? x1e : xr;
       V4<double> v64, c64;
       V4<float> v32;
 #pragma unroll
@@ -1775,8 +1798,9 @@ __global__ void __launch_bounds__(TTHREADS)
       const V4<float> zmv = upd4(ld(bm + o), ld(bm + CG_SLOT + o));
       const V4<float> zpv = upd4(ld(bp + o), ld(bp + CG_SLOT + o));
       float xl = shfl_up1(c.x[3]), xr = shfl_down1(c.x[0]);
-      if (lane == 0) xl = upd(bc[o - 1], bc[CG_SLOT + o - 1]);
-      if (lane == 31) xr = upd(bc[o + 4], bc[CG_SLOT + o + 4]);
+      const float pe = upd(edge_ld(bc + o, lane), edge_ld(bc + CG_SLOT + o, lane));
+      xl = lane == 0 ? pe : xl;
+      xr = lane == 31 ? pe : xr;
       V4<float> v;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -1909,8 +1933,9 @@ __global__ void __launch_bounds__(TTHREADS)
       const V4<float> zmv = ld(bm + o), zpv = ld(bp + o);
       const V4<float> rv = ld(bc + CG_SLOT + row * TI + 4 * lane);
       float xl = shfl_up1(c.x[3]), xr = shfl_down1(c.x[0]);
-      if (lane == 0) xl = bc[o - 1];
-      if (lane == 31) xr = bc[o + 4];
+      const float ze = edge_ld(bc + o, lane);
+      xl = lane == 0 ? ze : xl;
+      xr = lane == 31 ? ze : xr;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const float al = e == 0 ? xl : c.x[e - 1], ar = e == 3 ? xr : c.x[e + 1];
@@ -2118,8 +2143,9 @@ __global__ void __launch_bounds__(TTHREADS)
         const float ymv[4] = {ym4.x, ym4.y, ym4.z, ym4.w}, ypv[4] = {yp4.x, yp4.y, yp4.z, yp4.w};
         const float zmv[4] = {zm4.x, zm4.y, zm4.z, zm4.w}, zpv[4] = {zp4.x, zp4.y, zp4.z, zp4.w};
         float l32 = shfl_up1(cc[3]), r32 = shfl_down1(cc[0]);
-        if (lane == 0) l32 = pc[o - 1];
-        if (lane == 31) r32 = pc[o + 4];
+        const float e32 = edge_ld(pc + o, lane);
+        l32 = lane == 0 ? e32 : l32;
+        r32 = lane == 31 ? e32 : r32;
         if (!FINAL && j == M - 1 && a.finite_flag)
           nonfinite |= !(isfinite(cc[0]) && isfinite(cc[1]) && isfinite(cc[2]) && isfinite(cc[3]));
 #pragma unroll
