@@ -232,13 +232,12 @@ __global__ void __launch_bounds__(kAccBlock)
   pdl_wait();
   pdl_trigger();
   const long nn = n, m = nn * lines;
-  const int per_line = (n + b - 1) / b;
   double v[1] = {0.0};
   for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < m; idx += (long)gridDim.x * blockDim.x) {
     const int i = (int)(idx % nn);
     const long line = idx / nn;
     const int blk = i / b, i0 = blk * b, bs = min(b, n - i0), ii = i - i0;
-    const SB* D = inv + (line * per_line + blk) * (long)b * b;
+    const SB* D = inv + (bs < b ? (long)b * b : 0L);  // (ext.cu: one copy per distinct block)
     const S* rb = r + line * nn + i0;
     T acc = T(0);
     for (int jj = 0; jj < bs; ++jj) acc = xadd(acc, xmul(widen_s<T>(__ldg(D + (long)jj * bs + ii)), lds1<T>(rb + jj)));

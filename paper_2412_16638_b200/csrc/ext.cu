@@ -53,21 +53,23 @@ __device__ __forceinline__ cplx<R> rmul(R a, cplx<R> x) {
 // ---------------------------------------------------------------------------------
 // block-Jacobi
 //   blocks: x-line segments [i0, i0 + bs) of each (j, k) line, bs = min(b, n - i0)
-//   inv: per block, column-major bs x bs inverse in storage S (block B at
-//   offset B * b * b), so for fixed j the rows of a block read consecutive
-//   addresses (coalesced).
+//   inv: the column-major bs x bs inverses in storage S, ONE copy per distinct
+//   block: the stage operators have constant coefficients, so every full
+//   block of every line is the same matrix (slot 0) and so is every line's
+//   tail block when b does not divide n (slot 1, offset b * b).  A warp's
+//   loads of the block are broadcasts served from L1 — the block data no
+//   longer streams from HBM (b * sizeof(S) bytes per DOF per apply before).
 // ---------------------------------------------------------------------------------
 template <class T, class S>
 __global__ void __launch_bounds__(256) k_block_jacobi(int n, long lines, int b, const S* __restrict__ inv,
                                                       const T* __restrict__ r, T* __restrict__ z) {
   using R = real_t<T>;
   const long nn = n, m = nn * lines;
-  const int per_line = (n + b - 1) / b;
   for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < m; idx += (long)gridDim.x * blockDim.x) {
     const int i = (int)(idx % nn);
     const long line = idx / nn;
     const int blk = i / b, i0 = blk * b, bs = min(b, n - i0), ii = i - i0;
-    const S* D = inv + (line * per_line + blk) * (long)b * b;
+    const S* D = inv + (bs < b ? (long)b * b : 0L);  // (slot 1: the line's tail block)
     const T* rb = r + line * nn + i0;
     T acc = zero_v<T>();
     for (int jj = 0; jj < bs; ++jj) acc = xadd(acc, rmul(ld_store<R>(D + (long)jj * bs + ii), ldg(rb + jj)));
@@ -108,12 +110,71 @@ __device__ __forceinline__ void ld_col(const S* p, float (&o)[CNT]) {
   }
 }
 
+// The shared B x B block, converted once per CTA to the compute type R
+// (the same rounding as converting each loaded entry) and read back with
+// broadcast vector LDS: no per-entry conversion (quarter-rate F2F for fp64
+// storage under fp32 compute) and no per-thread global loads of the block.
+template <class R, class S, int B>
+__device__ __forceinline__ void bj_stage(const S* inv, R* sblk) {
+  for (int e = threadIdx.x; e < B * B; e += blockDim.x) sblk[e] = ld_store<R>(inv + e);
+  __syncthreads();
+}
+// acc[ii] += D[jj][ii] * rv[jj], jj ascending (column jj of the column-major
+// block), D read from global storage S (L1-resident broadcast loads, each
+// entry converted at use): faster than staging for B <= 8
+template <class R, class S, class V, int B>
+__device__ __forceinline__ void bj_mul_global(const S* D, const V (&rv)[B], V (&acc)[B]) {
+#pragma unroll
+  for (int jj = 0; jj < B; ++jj) {
+    if constexpr (std::is_same_v<S, double>) {
+#pragma unroll
+      for (int c = 0; c < B / 2; ++c) {
+        const double2 w = __ldg(reinterpret_cast<const double2*>(D + jj * B) + c);
+        acc[2 * c] = xadd(acc[2 * c], rmul((R)w.x, rv[jj]));
+        acc[2 * c + 1] = xadd(acc[2 * c + 1], rmul((R)w.y, rv[jj]));
+      }
+    } else {
+      float col[B];
+      ld_col<S, B>(D + jj * B, col);
+#pragma unroll
+      for (int ii = 0; ii < B; ++ii) acc[ii] = xadd(acc[ii], rmul((R)col[ii], rv[jj]));
+    }
+  }
+}
+// the same from the staged block (bj_stage)
+template <class R, class V, int B>
+__device__ __forceinline__ void bj_mul(const R* sblk, const V (&rv)[B], V (&acc)[B]) {
+#pragma unroll
+  for (int jj = 0; jj < B; ++jj) {
+    const R* col = sblk + jj * B;
+    if constexpr (std::is_same_v<R, double>) {
+#pragma unroll
+      for (int c = 0; c < B / 2; ++c) {
+        const double2 w = *reinterpret_cast<const double2*>(col + 2 * c);
+        acc[2 * c] = xadd(acc[2 * c], rmul(w.x, rv[jj]));
+        acc[2 * c + 1] = xadd(acc[2 * c + 1], rmul(w.y, rv[jj]));
+      }
+    } else {
+#pragma unroll
+      for (int c = 0; c < B / 4; ++c) {
+        const float4 w = *reinterpret_cast<const float4*>(col + 4 * c);
+        acc[4 * c] = xadd(acc[4 * c], rmul(w.x, rv[jj]));
+        acc[4 * c + 1] = xadd(acc[4 * c + 1], rmul(w.y, rv[jj]));
+        acc[4 * c + 2] = xadd(acc[4 * c + 2], rmul(w.z, rv[jj]));
+        acc[4 * c + 3] = xadd(acc[4 * c + 3], rmul(w.w, rv[jj]));
+      }
+    }
+  }
+}
+
 template <class T, class S, int B>
 __global__ void __launch_bounds__(128) k_block_jacobi_row(long blocks, const S* __restrict__ inv,
                                                           const T* __restrict__ r, T* __restrict__ z) {
   using R = real_t<T>;
+  constexpr bool kStage = B >= 16;  // (measured: staging pays from B = 16 on)
+  __shared__ __align__(16) R sblk[kStage ? B * B : 4];
+  if constexpr (kStage) bj_stage<R, S, B>(inv, sblk);  // (n % B == 0: every block is slot 0)
   for (long blk = blockIdx.x * (long)blockDim.x + threadIdx.x; blk < blocks; blk += (long)gridDim.x * blockDim.x) {
-    const S* D = inv + blk * (long)B * B;
     const T* rb = r + blk * B;
     T rv[B];
 #pragma unroll
@@ -125,22 +186,10 @@ __global__ void __launch_bounds__(128) k_block_jacobi_row(long blocks, const S* 
     T acc[B];
 #pragma unroll
     for (int ii = 0; ii < B; ++ii) acc[ii] = zero_v<T>();
-#pragma unroll
-    for (int jj = 0; jj < B; ++jj) {
-      if constexpr (std::is_same_v<S, double>) {
-#pragma unroll
-        for (int c = 0; c < B / 2; ++c) {
-          const double2 w = __ldg(reinterpret_cast<const double2*>(D + jj * B) + c);
-          acc[2 * c] = xadd(acc[2 * c], rmul((R)w.x, rv[jj]));
-          acc[2 * c + 1] = xadd(acc[2 * c + 1], rmul((R)w.y, rv[jj]));
-        }
-      } else {
-        float col[B];
-        ld_col<S, B>(D + jj * B, col);
-#pragma unroll
-        for (int ii = 0; ii < B; ++ii) acc[ii] = xadd(acc[ii], rmul((R)col[ii], rv[jj]));
-      }
-    }
+    if constexpr (kStage)
+      bj_mul<R, T, B>(sblk, rv, acc);
+    else
+      bj_mul_global<R, S, T, B>(inv, rv, acc);
 #pragma unroll
     for (int c = 0; c < B / 4; ++c) {
       V4<T> w;
@@ -183,9 +232,12 @@ __global__ void __launch_bounds__(128) k_cg_update_bj(long blocks, real_t<T> alp
                                                       const T* __restrict__ p, T* __restrict__ r,
                                                       const T* __restrict__ q, const S* __restrict__ inv,
                                                       T* __restrict__ z, RedSlot red, const CgCtl* ctl) {
+  using R = real_t<T>;
+  constexpr bool kStage = B >= 16;
+  __shared__ __align__(16) R sblk[kStage ? B * B : 4];
+  if constexpr (kStage) bj_stage<R, S, B>(inv, sblk);  // (constant since construction: before the dependency wait)
   pdl_wait();
   pdl_trigger();
-  using R = real_t<T>;
   if (ctl) {  // device loop: alpha from the control block; no-op once stopped
     if (ctl->stop) return;
     alpha = (R)ctl->alpha;
@@ -208,26 +260,13 @@ __global__ void __launch_bounds__(128) k_cg_update_bj(long blocks, real_t<T> alp
       st4(x + o + 4 * c, xv);
       st4(r + o + 4 * c, rw);
     }
-    const S* D = inv + blk * (long)B * B;
     R acc[B];
 #pragma unroll
     for (int ii = 0; ii < B; ++ii) acc[ii] = R(0);
-#pragma unroll
-    for (int jj = 0; jj < B; ++jj) {
-      if constexpr (std::is_same_v<S, double>) {
-#pragma unroll
-        for (int c = 0; c < B / 2; ++c) {
-          const double2 w = __ldg(reinterpret_cast<const double2*>(D + jj * B) + c);
-          acc[2 * c] = xadd(acc[2 * c], rmul((R)w.x, rv[jj]));
-          acc[2 * c + 1] = xadd(acc[2 * c + 1], rmul((R)w.y, rv[jj]));
-        }
-      } else {
-        float col[B];
-        ld_col<S, B>(D + jj * B, col);
-#pragma unroll
-        for (int ii = 0; ii < B; ++ii) acc[ii] = xadd(acc[ii], rmul((R)col[ii], rv[jj]));
-      }
-    }
+    if constexpr (kStage)  // (n % B == 0: every block is slot 0)
+      bj_mul<R, R, B>(sblk, rv, acc);
+    else
+      bj_mul_global<R, S, R, B>(inv, rv, acc);
 #pragma unroll
     for (int c = 0; c < B / 4; ++c) {
       V4<T> w;
@@ -257,6 +296,12 @@ bool cg_bj(int n, long lines, int b, real_t<T> alpha, const CgCtl* ctl, T* x, co
       case 16:
         launch_pdl(k_cg_update_bj<T, S, 16>, dim3(g), dim3(128), 0, st, blocks, alpha, x, p, r, q, inv, z, red, ctl);
         break;
+      case 32:
+        if constexpr (sizeof(T) == 4) {  // (fp32 compute: 2 x 32 accumulators fit the register budget)
+          launch_pdl(k_cg_update_bj<T, S, 32>, dim3(g), dim3(128), 0, st, blocks, alpha, x, p, r, q, inv, z, red, ctl);
+          break;
+        }
+        return false;
       default: return false;
     }
     note_partials(red, g);
@@ -282,15 +327,16 @@ template bool cg_update_block_jacobi<float>(int, int, int, const void*, float, f
 template bool cg_update_block_jacobi<double>(int, int, int, const void*, double, double*, const double*, double*,
                                              const double*, double*, const RedSlot&, cudaStream_t, long, const CgCtl*);
 
+// slot 0 <- the full block, slot 1 <- the tail block (bs = n % b) when present
 template <class S>
-__global__ void k_bj_fill(long nblocks_per_line, long lines, int n, int b, const double* __restrict__ full,
+__global__ void k_bj_fill(int slots, int b, int tail_bs, const double* __restrict__ full,
                           const double* __restrict__ tail, S* __restrict__ inv) {
-  const long total = nblocks_per_line * lines * (long)b * b;
+  const long total = (long)slots * b * b;
   for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
-    const long blk = (e / ((long)b * b)) % nblocks_per_line;
+    const int slot = (int)(e / ((long)b * b));
     const int off = (int)(e % ((long)b * b));
-    const int i0 = (int)blk * b, bs = min(b, n - i0);
-    const double* src = bs == b ? full : tail;
+    const int bs = slot == 0 ? b : tail_bs;
+    const double* src = slot == 0 ? full : tail;
     double v = off < bs * bs ? src[off] : 0.0;
     if constexpr (std::is_same_v<S, __half>)
       inv[e] = __double2half(v);
@@ -322,16 +368,16 @@ void block_jacobi_apply(int n, int b, int storage, const void* inv, const T* r, 
   LAUNCHED("block_jacobi");
 }
 
+size_t block_jacobi_slots(int n, int b) { return n % b ? 2 : 1; }
+
 void block_jacobi_fill(int n, int b, int storage, const double* full_dev, const double* tail_dev, void* inv,
-                       cudaStream_t st, long lines) {
-  if (lines <= 0) lines = (long)n * n;
-  const long per_line = (n + b - 1) / b;
-  const size_t total = (size_t)per_line * lines * b * b;
-  const unsigned g = grid_for(total, 256, 8);
+                       cudaStream_t st) {
+  const int slots = (int)block_jacobi_slots(n, b);
+  const unsigned g = grid_for((size_t)slots * b * b, 256, 8);
   switch (storage) {
-    case 4: k_bj_fill<__half><<<g, 256, 0, st>>>(per_line, lines, n, b, full_dev, tail_dev, (__half*)inv); break;
-    case 0: k_bj_fill<float><<<g, 256, 0, st>>>(per_line, lines, n, b, full_dev, tail_dev, (float*)inv); break;
-    default: k_bj_fill<double><<<g, 256, 0, st>>>(per_line, lines, n, b, full_dev, tail_dev, (double*)inv); break;
+    case 4: k_bj_fill<__half><<<g, 256, 0, st>>>(slots, b, n % b, full_dev, tail_dev, (__half*)inv); break;
+    case 0: k_bj_fill<float><<<g, 256, 0, st>>>(slots, b, n % b, full_dev, tail_dev, (float*)inv); break;
+    default: k_bj_fill<double><<<g, 256, 0, st>>>(slots, b, n % b, full_dev, tail_dev, (double*)inv); break;
   }
   LAUNCHED("block_jacobi_fill");
 }

@@ -215,10 +215,12 @@ template <class T>
 bool cg_update_block_jacobi(int n, int b, int storage, const void* inv, real_t<T> alpha, T* x, const T* p, T* r,
                             const T* q, T* z, const RedSlot& red, cudaStream_t st, long lines = 0,
                             const CgCtl* ctl = nullptr);
-// per-block inverse storage from the two distinct fp64 block inverses
-// (column-major b x b full blocks, n % b tail blocks)
+// block inverse storage (ext.cu): the two distinct fp64 block inverses
+// (column-major b x b full block, n % b tail block) rounded to the storage
+// precision, block_jacobi_slots(n, b) slots of b * b entries
+size_t block_jacobi_slots(int n, int b);
 void block_jacobi_fill(int n, int b, int storage, const double* full_dev, const double* tail_dev, void* inv,
-                       cudaStream_t st, long lines = 0);
+                       cudaStream_t st);
 template <class T>
 void csr_apply(int rows, const int* rp, const int* cols, const void* vals, int storage, const T* x, T* y,
                cudaStream_t st);

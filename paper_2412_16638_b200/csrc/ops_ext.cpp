@@ -107,9 +107,8 @@ class BlockJacobiOp final : public Op {
     DevBuf df(full.size() * 8), dt(tl.size() * 8);
     CUDA_CHECK(cudaMemcpy(df.get(), full.data(), full.size() * 8, cudaMemcpyHostToDevice));
     CUDA_CHECK(cudaMemcpy(dt.get(), tl.data(), tl.size() * 8, cudaMemcpyHostToDevice));
-    const size_t per_line = (n_ + b_ - 1) / b_;
-    inv_.alloc(per_line * (size_t)lines_ * b_ * b_ * storage_size(storage));
-    block_jacobi_fill(n_, b_, storage_, df.as<double>(), dt.as<double>(), inv_.get(), 0, lines_);
+    inv_.alloc(block_jacobi_slots(n_, b_) * b_ * b_ * storage_size(storage));
+    block_jacobi_fill(n_, b_, storage_, df.as<double>(), dt.as<double>(), inv_.get(), 0);
     CUDA_CHECK(cudaDeviceSynchronize());
   }
   void apply(const void* x, void* out, cudaStream_t st) override {
