@@ -14,6 +14,8 @@
 // 2.4x fewer at fp16 under fp32.  Control flow, stopping tests, the
 // true-residual veto and breakdown checks are the reference's, in its order.
 #include <cmath>
+#include <cstdlib>
+#include <utility>
 
 #include "accessor.hpp"
 #include "pdl.cuh"
@@ -248,6 +250,117 @@ __global__ void __launch_bounds__(kAccBlock)
   grid_reduce<1>(v, red);
 }
 
+// The CG update fused with the block-Jacobi apply (one thread per x-line
+// block of B points, n % B == 0): x += alpha p (T), r = S(r - alpha q),
+// z = S(blockdiag(inv) r) from the stored r, red <- (||r||^2, r.z) of the
+// stored values — each value rounds as in k_acc_update + k_acc_block_jacobi
+// (only the order of the fp64 partial sums differs).  The block (ext.cu:
+// one copy, n % B == 0 so slot 0) is read from L1 (B <= 8) or staged widened
+// in shared memory (B >= 16).
+template <class T, class S, class SB, int B>
+__global__ void __launch_bounds__(128)
+    k_acc_update_bj(long blocks, T alpha, T* __restrict__ x, const S* __restrict__ p, S* __restrict__ r,
+                    const S* __restrict__ q, const SB* __restrict__ inv, S* __restrict__ z, RedSlot red) {
+  constexpr bool kStage = B >= 16;
+  __shared__ __align__(16) T sblk[kStage ? B * B : 4];
+  if constexpr (kStage) {
+    for (int e = threadIdx.x; e < B * B; e += blockDim.x) sblk[e] = widen_s<T>(inv[e]);
+    __syncthreads();
+  }
+  pdl_wait();
+  pdl_trigger();
+  double v[2] = {0.0, 0.0};
+  for (long blk = blockIdx.x * (long)blockDim.x + threadIdx.x; blk < blocks; blk += (long)gridDim.x * blockDim.x) {
+    const long o = blk * B;
+    T rv[B];
+#pragma unroll
+    for (int c = 0; c < B / 4; ++c) {
+      V4<T> xv = ld4rw(x + o + 4 * c);
+      const V4<T> pv = lds4<T>(p + o + 4 * c), qv = lds4<T>(q + o + 4 * c);
+      V4<T> rw = lds4rw<T>(r + o + 4 * c);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        xv.x[e] = xadd(xv.x[e], xmul(alpha, pv.x[e]));
+        rw.x[e] = xsub(rw.x[e], xmul(alpha, qv.x[e]));
+      }
+      st4(x + o + 4 * c, xv);
+      const V4<T> rs = sts4<S>(r + o + 4 * c, rw);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        v[0] = __fma_rn((double)rs.x[e], (double)rs.x[e], v[0]);
+        rv[4 * c + e] = rs.x[e];
+      }
+    }
+    T acc[B];
+#pragma unroll
+    for (int ii = 0; ii < B; ++ii) acc[ii] = T(0);
+#pragma unroll
+    for (int jj = 0; jj < B; ++jj)
+#pragma unroll
+      for (int ii = 0; ii < B; ++ii) {
+        const T d = kStage ? sblk[kStage ? jj * B + ii : 0] : widen_s<T>(__ldg(inv + jj * B + ii));
+        acc[ii] = xadd(acc[ii], xmul(d, rv[jj]));
+      }
+#pragma unroll
+    for (int c = 0; c < B / 4; ++c) {
+      V4<T> w;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) w.x[e] = acc[4 * c + e];
+      const V4<T> zs = sts4<S>(z + o + 4 * c, w);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[1] = __fma_rn((double)zs.x[e], (double)rv[4 * c + e], v[1]);
+    }
+  }
+  grid_reduce<2>(v, red);
+}
+
+// p' = S(z + beta p) (k_acc_xpby's rounding) fused with q = S(A p') and p'.q
+// (k_acc_stencil's arithmetic and reduction, same grid: bitwise the two
+// kernels).  p' goes to a second buffer — neighbouring threads still read p —
+// and every neighbour's p' is re-formed from z and p.
+template <class T, class S>
+__global__ void __launch_bounds__(kAccBlock)
+    k_acc_pq(int n, T s, T g, const S* __restrict__ z, T beta, const S* __restrict__ p, S* __restrict__ pn,
+             S* __restrict__ q, RedSlot red) {
+  pdl_wait();
+  pdl_trigger();
+  const long nn = n, n2 = nn * nn, q4 = nn / 4, quads = q4 * n2;
+  auto rt = [](T v) { return widen_s<T>(round_s<S>(v)); };
+  auto pnew4 = [&](long off) {
+    const V4<T> zv = lds4<T>(z + off), pv = lds4<T>(p + off);
+    V4<T> o;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o.x[e] = rt(xadd(zv.x[e], xmul(beta, pv.x[e])));
+    return o;
+  };
+  auto pnew1 = [&](long off) { return rt(xadd(lds1<T>(z + off), xmul(beta, lds1<T>(p + off)))); };
+  double v[1] = {0.0};
+  for (long qd = blockIdx.x * (long)blockDim.x + threadIdx.x; qd < quads; qd += (long)gridDim.x * blockDim.x) {
+    const long i0 = (qd % q4) * 4, jk = qd / q4;
+    const int j = (int)(jk % nn), k = (int)(jk / nn);
+    const long idx = i0 + jk * nn;
+    const V4<T> c = pnew4(idx);
+    sts4<S>(pn + idx, c);  // (exact: c is already representable in S)
+    const V4<T> ym = j > 0 ? pnew4(idx - nn) : zero4<T>();
+    const V4<T> yp = j + 1 < n ? pnew4(idx + nn) : zero4<T>();
+    const V4<T> zm = k > 0 ? pnew4(idx - n2) : zero4<T>();
+    const V4<T> zp = k + 1 < n ? pnew4(idx + n2) : zero4<T>();
+    const T xl = i0 > 0 ? pnew1(idx - 1) : T(0);
+    const T xr = i0 + 4 < nn ? pnew1(idx + 4) : T(0);
+    V4<T> o;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const T l = e == 0 ? xl : c.x[e - 1];
+      const T r = e == 3 ? xr : c.x[e + 1];
+      o.x[e] = heat_point<T>(s, g, c.x[e], l, r, ym.x[e], yp.x[e], zm.x[e], zp.x[e]);
+    }
+    const V4<T> st = sts4<S>(q + idx, o);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) v[0] = __fma_rn((double)c.x[e], (double)st.x[e], v[0]);
+  }
+  grid_reduce<1>(v, red);
+}
+
 inline unsigned acc_grid(size_t work) { return grid_for(work, kAccBlock, 8); }
 
 template <class T, class S>
@@ -276,6 +389,16 @@ struct AccKernels {
     note_partials(red, g);
     LAUNCHED("acc_update");
   }
+  // pn = z + beta p, q = A pn, red <- pn.q (bitwise xpby + apply_dot)
+  static void pq(const StencilSpec& A, const S* z, T beta, const S* p, S* pn, S* q, const RedSlot& red,
+                 cudaStream_t st) {
+    const size_t quads = A.size() / 4;
+    const unsigned g = acc_grid(quads);
+    launch_pdl(k_acc_pq<T, S>, dim3(g), dim3(kAccBlock), 0, st, A.n, (T)A.sigma, (T)A.gamma, z, beta, p, pn, q, red);
+    note_partials(red, g);
+    note_kron(std::is_same_v<T, float>);
+    LAUNCHED("acc_pq");
+  }
   static void xpby(size_t m, const S* z, T beta, S* p, cudaStream_t st) {
     const unsigned g = acc_grid(m / 4);
     launch_pdl(k_acc_xpby<T, S>, dim3(g), dim3(kAccBlock), 0, st, m, z, beta, p);
@@ -290,6 +413,10 @@ double finish(AccWork& w, int slot, cudaStream_t st) {
   w.red.result(slot, 1, v);
   return v[0];
 }
+inline void finish2(AccWork& w, int slot, cudaStream_t st, double (&v)[2]) {
+  stream_sync(st);
+  w.red.result(slot, 2, v);
+}
 
 template <class T, class S>
 void run_cg(const StencilSpec& A, Op* P, const T* b, T* x, const Crit& crit, AccWork& w, SolveReport& rep,
@@ -301,6 +428,7 @@ void run_cg(const StencilSpec& A, Op* P, const T* b, T* x, const Crit& crit, Acc
   S* z = w.vecs[1].as<S>();
   S* p = w.vecs[2].as<S>();
   S* q = w.vecs[3].as<S>();
+  S* pn = w.vecs[4].as<S>();
   const RedSlot s0 = w.red.slot(0);
   const int sto = std::is_same_v<S, __half> ? 4 : std::is_same_v<S, float> ? 0 : 1;
   rep = SolveReport{};
@@ -330,13 +458,23 @@ void run_cg(const StencilSpec& A, Op* P, const T* b, T* x, const Crit& crit, Acc
     R rz = P ? precond(r) : (R)r_sq;
     if (P) zz = z;
     CUDA_CHECK(cudaMemcpyAsync(p, zz, m * sizeof(S), cudaMemcpyDeviceToDevice, st));
+    // (fused passes, MPRKB_ACC_FUSED=0 disables: the update with the
+    // block-Jacobi apply, and p = z + beta p with q = A p, p.q — the latter
+    // hands the next iteration its p.q, so 2 round trips per iteration, not 4)
+    const char* fe = std::getenv("MPRKB_ACC_FUSED");
+    const bool fused_on = !(fe && fe[0] == '0');
+    bool have_pq = false;
+    R pq_next{};
     for (int k = 0; k < crit.max_iter; ++k) {
       if (!(rz > R{})) {
         rep.failure = 2;
         break;
       }
       R pq;
-      {
+      if (have_pq) {
+        pq = pq_next;
+        have_pq = false;
+      } else {
         TimerBracket br(timer, "stencil", st);
         K::apply_dot(A, p, q, s0, st);
         pq = (R)finish<T, S>(w, 0, st);
@@ -347,7 +485,19 @@ void run_cg(const StencilSpec& A, Op* P, const T* b, T* x, const Crit& crit, Acc
       }
       const R alpha = rz / pq;
       double rsq;
-      {
+      bool pre_fused = false;
+      R rz_fused{};
+      if (P && fused_on) {
+        TimerBracket br(timer, "precond", st);
+        pre_fused = P->cg_update_apply_storage((double)alpha, x, p, r, q, z, sto, s0, st);
+        if (pre_fused) {
+          double v2[2];
+          finish2(w, 0, st, v2);
+          rsq = v2[0];
+          rz_fused = (R)v2[1];
+        }
+      }
+      if (!pre_fused) {
         TimerBracket br(timer, "axpy", st);
         K::update(m, alpha, x, p, r, q, s0, st);
         rsq = finish<T, S>(w, 0, st);
@@ -374,10 +524,16 @@ void run_cg(const StencilSpec& A, Op* P, const T* b, T* x, const Crit& crit, Acc
         CUDA_CHECK(cudaMemcpyAsync(p, P ? z : r, m * sizeof(S), cudaMemcpyDeviceToDevice, st));
         continue;
       }
-      const R rz_next = P ? precond(r) : (R)rsq;
+      const R rz_next = pre_fused ? rz_fused : P ? precond(r) : (R)rsq;
       const R beta = rz_next / rz;
       rz = rz_next;
-      {
+      if (fused_on) {
+        TimerBracket br(timer, "stencil", st);
+        K::pq(A, P ? z : r, beta, p, pn, q, s0, st);
+        pq_next = (R)finish<T, S>(w, 0, st);
+        have_pq = true;
+        std::swap(p, pn);
+      } else {
         TimerBracket br(timer, "axpy", st);
         K::xpby(m, P ? z : r, beta, p, st);
       }
@@ -446,6 +602,52 @@ void block_jacobi_acc(int n, int b, int block_storage, const void* inv, int vec_
   note_partials(red, g);
   LAUNCHED("acc_block_jacobi");
 }
+
+template <class T>
+bool cg_update_bj_acc(int n, int b, int block_storage, const void* inv, int vec_storage, T alpha, T* x,
+                      const void* p, void* r, const void* q, void* z, const RedSlot& red, cudaStream_t st,
+                      long lines) {
+  if (lines <= 0) lines = (long)n * n;
+  if (n % b || !(b == 4 || b == 8 || b == 16 || (b == 32 && sizeof(T) == 4))) return false;
+  if (!(vec_storage == 4 || (vec_storage == 0 && sizeof(T) == 8))) return false;
+  const long blocks = lines * (n / b);
+  const unsigned g = grid_for((size_t)blocks, 128, 16);
+  auto go = [&](auto s_tag, auto sb_tag) {
+    using S = decltype(s_tag);
+    using SB = decltype(sb_tag);
+    auto k = [&](auto kern) {
+      launch_pdl(kern, dim3(g), dim3(128), 0, st, blocks, alpha, x, (const S*)p, (S*)r, (const S*)q, (const SB*)inv,
+                 (S*)z, red);
+    };
+    switch (b) {
+      case 4: k(k_acc_update_bj<T, S, SB, 4>); break;
+      case 8: k(k_acc_update_bj<T, S, SB, 8>); break;
+      case 16: k(k_acc_update_bj<T, S, SB, 16>); break;
+      default:
+        if constexpr (sizeof(T) == 4) k(k_acc_update_bj<T, S, SB, 32>);
+        break;
+    }
+  };
+  auto by_block = [&](auto s_tag) {
+    switch (block_storage) {
+      case 4: go(s_tag, __half{}); break;
+      case 0: go(s_tag, float{}); break;
+      default: go(s_tag, double{}); break;
+    }
+  };
+  if (vec_storage == 4)
+    by_block(__half{});
+  else if constexpr (sizeof(T) == 8)
+    by_block(float{});
+  note_partials(red, g);
+  LAUNCHED("acc_update_bj");
+  return true;
+}
+
+template bool cg_update_bj_acc<float>(int, int, int, const void*, int, float, float*, const void*, void*,
+                                      const void*, void*, const RedSlot&, cudaStream_t, long);
+template bool cg_update_bj_acc<double>(int, int, int, const void*, int, double, double*, const void*, void*,
+                                       const void*, void*, const RedSlot&, cudaStream_t, long);
 
 template void cg_solve_acc<float>(const StencilSpec&, Op*, const float*, float*, const Crit&, AccWork&, SolveReport&,
                                   cudaStream_t, EventTimer*);

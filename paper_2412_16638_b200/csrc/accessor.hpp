@@ -16,7 +16,7 @@ class AccWork {
   AccWork(size_t m, int storage);
   size_t size() const { return m_; }
   int storage() const { return storage_; }
-  std::array<DevBuf, 4> vecs;
+  std::array<DevBuf, 5> vecs;  // r, z, p, q, and p's second buffer (the fused direction pass)
   Reducer red;
 
  private:
@@ -37,5 +37,13 @@ void cg_solve_acc(const StencilSpec& A, Op* P, const T* b, T* x, const Crit& cri
 template <class T>
 void block_jacobi_acc(int n, int b, int block_storage, const void* inv, int vec_storage, const void* r, void* z,
                       const RedSlot& red, cudaStream_t st, long lines = 0);
+// the CG update fused with that apply (one thread per x-line block, n % b == 0,
+// b in {4, 8, 16, 32}): x += alpha p (T), r -= alpha q and z = blockdiag(inv) r
+// stored in vec_storage, red <- (||r||^2, r.z) of the stored values; false
+// when the shape is not covered
+template <class T>
+bool cg_update_bj_acc(int n, int b, int block_storage, const void* inv, int vec_storage, T alpha, T* x,
+                      const void* p, void* r, const void* q, void* z, const RedSlot& red, cudaStream_t st,
+                      long lines = 0);
 
 }  // namespace mprkb

@@ -51,6 +51,14 @@ class Op {
                              cudaStream_t /*st*/) {
     return false;
   }
+  // Accessor-style CG update fused with the apply (accessor.cu
+  // k_acc_update_bj): x (dtype) += alpha p, r -= alpha q, z = P r with p, r,
+  // q, z in `storage`; red <- (||r||^2, r.z) of the stored values.
+  virtual bool cg_update_apply_storage(double /*alpha*/, void* /*x*/, const void* /*p*/, void* /*r*/,
+                                       const void* /*q*/, void* /*z*/, int /*storage*/, const RedSlot& /*red*/,
+                                       cudaStream_t /*st*/) {
+    return false;
+  }
 
  protected:
   EventTimer* timer_ = nullptr;

@@ -132,6 +132,14 @@ class BlockJacobiOp final : public Op {
     }
     return false;
   }
+  bool cg_update_apply_storage(double alpha, void* x, const void* p, void* r, const void* q, void* z, int storage,
+                               const RedSlot& red, cudaStream_t st) override {
+    if constexpr (std::is_same_v<T, float> || std::is_same_v<T, double>) {
+      return cg_update_bj_acc<T>(n_, b_, storage_, inv_.get(), storage, (T)alpha, static_cast<T*>(x), p, r, q, z,
+                                 red, st, lines_);
+    }
+    return false;
+  }
   bool apply_storage(const void* r, int storage, void* z, const RedSlot& red, cudaStream_t st) override {
     if constexpr (std::is_same_v<T, float> || std::is_same_v<T, double>) {
       block_jacobi_acc<T>(n_, b_, storage_, inv_.get(), storage, r, z, red, st, lines_);

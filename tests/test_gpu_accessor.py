@@ -63,8 +63,9 @@ def test_cg_vector_storage_matches_restatement(gpu, mp, dtype, storage, precond)
 def test_cg_vector_storage_launches_storage_kernels(gpu, mp):
     """The storage path runs its own kernels (no working-precision fallback)
     and reads 2-byte vectors: the identity-preconditioned fp16 solve performs
-    exactly one residual, one stencil + dot, one update (+ one p update) per
-    iteration plus the initial and exit residuals."""
+    one update and one fused direction + stencil + dot pass per iteration
+    (k_acc_pq) plus the initial residual, the first stencil, the exit
+    residual and the true-residual checks."""
     import torch
 
     n = 32
@@ -76,8 +77,8 @@ def test_cg_vector_storage_launches_storage_kernels(gpu, mp):
     launched = mp.kernel_launches() - l0
     it = r["iterations"]
     assert r["converged"] and it >= 3
-    # resid x2 (+1 true-residual check per convergence trigger), per iteration stencil + update + xpby
-    assert 3 * it - 1 + 2 <= launched <= 3 * it + 2 + 2 * it, (launched, it)
+    # resid x2 + first stencil (+1 true-residual check per convergence trigger), per iteration update + pq
+    assert 2 * it + 2 <= launched <= 3 * it + 3, (launched, it)
 
 
 def test_cg_vector_storage_errors(gpu, mp):
@@ -125,3 +126,33 @@ def test_stepper_vector_storage(gpu, mp, prec, storage):
     # the state error (against tightly solved stages) is that of the
     # working-precision vectors at the same stage tolerance, within 3x
     assert np.linalg.norm(a - e) <= 3 * np.linalg.norm(c - e) + 1e-6 * np.linalg.norm(e)
+
+
+@pytest.mark.parametrize("dtype,storage,b", [("f32", "f16", 8), ("f32", "f16", 32), ("f64", "f32", 16),
+                                             ("f64", "f16", 4)])
+def test_cg_vector_storage_fused_passes(gpu, mp, monkeypatch, dtype, storage, b):
+    """The fused accessor passes — the update with the block-Jacobi apply
+    (k_acc_update_bj) and p = z + beta p with q = A p, p.q (k_acc_pq) — agree
+    with the separate kernels (MPRKB_ACC_FUSED=0): the direction pass is
+    bitwise, the fused update only reorders the fp64 partial sums of
+    ||r||^2 and r.z (last-bit changes of the working-precision scalars), so
+    iterations agree within one and histories / solutions to 1e-5."""
+    import torch
+
+    n = 64
+    T = np.float32 if dtype == "f32" else np.float64
+    code = 0 if dtype == "f32" else 1
+    tau, a, sigma, gamma, bv = _system(n, T, seed=11)
+    A = mp.Operator.stencil(code, n, 0, sigma, gamma)
+    P = mp.Operator.block_jacobi(code, "heat", n, tau, a, b, "f16")
+    bd = torch.from_numpy(bv).cuda()
+    tol = 1e-3 if storage == "f16" else 1e-7
+    xf, rf = mp.cg(A, P, bd, torch.zeros_like(bd), tol, 300, storage=storage)
+    monkeypatch.setenv("MPRKB_ACC_FUSED", "0")
+    xs, rs = mp.cg(A, P, bd, torch.zeros_like(bd), tol, 300, storage=storage)
+    assert rf["converged"] and rs["converged"]
+    assert abs(rf["iterations"] - rs["iterations"]) <= 1 and rf["iterations"] >= 3
+    h = min(len(rf["history"]), len(rs["history"]))
+    np.testing.assert_allclose(rf["history"][:h], rs["history"][:h], rtol=1e-5)
+    xf, xs = xf.cpu().numpy(), xs.cpu().numpy()
+    assert np.linalg.norm(xf - xs) <= 1e-5 * np.linalg.norm(xs) + 2 * tol * np.linalg.norm(xs)
