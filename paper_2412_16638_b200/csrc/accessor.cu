@@ -14,6 +14,7 @@
 // 2.4x fewer at fp16 under fp32.  Control flow, stopping tests, the
 // true-residual veto and breakdown checks are the reference's, in its order.
 #include <cmath>
+#include <algorithm>
 #include <cstdlib>
 #include <utility>
 
@@ -315,16 +316,20 @@ __global__ void __launch_bounds__(128)
 }
 
 // p' = S(z + beta p) (k_acc_xpby's rounding) fused with q = S(A p') and p'.q
-// (k_acc_stencil's arithmetic and reduction, same grid: bitwise the two
-// kernels).  p' goes to a second buffer — neighbouring threads still read p —
-// and every neighbour's p' is re-formed from z and p.
+// (k_acc_stencil's arithmetic).  p' goes to a second buffer — neighbouring
+// threads still read p — and every neighbour's p' is re-formed from z and p.
+// A thread owns 4 points of one (j) row and marches a chunk of k-planes,
+// carrying p' of planes k - 1, k, k + 1 in registers (a CTA = 128 x 8
+// points, so the j neighbours come from L1): 3 quad loads per array and
+// point instead of 6.
+constexpr int kPqX = 32, kPqY = 8;
 template <class T, class S>
-__global__ void __launch_bounds__(kAccBlock)
-    k_acc_pq(int n, T s, T g, const S* __restrict__ z, T beta, const S* __restrict__ p, S* __restrict__ pn,
+__global__ void __launch_bounds__(kPqX* kPqY)
+    k_acc_pq(int n, int kc, T s, T g, const S* __restrict__ z, T beta, const S* __restrict__ p, S* __restrict__ pn,
              S* __restrict__ q, RedSlot red) {
   pdl_wait();
   pdl_trigger();
-  const long nn = n, n2 = nn * nn, q4 = nn / 4, quads = q4 * n2;
+  const long nn = n, n2 = nn * nn;
   auto rt = [](T v) { return widen_s<T>(round_s<S>(v)); };
   auto pnew4 = [&](long off) {
     const V4<T> zv = lds4<T>(z + off), pv = lds4<T>(p + off);
@@ -334,29 +339,39 @@ __global__ void __launch_bounds__(kAccBlock)
     return o;
   };
   auto pnew1 = [&](long off) { return rt(xadd(lds1<T>(z + off), xmul(beta, lds1<T>(p + off)))); };
+  const int iq = blockIdx.x * kPqX + threadIdx.x, j = blockIdx.y * kPqY + threadIdx.y;
+  const int k0 = blockIdx.z * kc, k1 = min(n, k0 + kc);
   double v[1] = {0.0};
-  for (long qd = blockIdx.x * (long)blockDim.x + threadIdx.x; qd < quads; qd += (long)gridDim.x * blockDim.x) {
-    const long i0 = (qd % q4) * 4, jk = qd / q4;
-    const int j = (int)(jk % nn), k = (int)(jk / nn);
-    const long idx = i0 + jk * nn;
-    const V4<T> c = pnew4(idx);
-    sts4<S>(pn + idx, c);  // (exact: c is already representable in S)
-    const V4<T> ym = j > 0 ? pnew4(idx - nn) : zero4<T>();
-    const V4<T> yp = j + 1 < n ? pnew4(idx + nn) : zero4<T>();
-    const V4<T> zm = k > 0 ? pnew4(idx - n2) : zero4<T>();
-    const V4<T> zp = k + 1 < n ? pnew4(idx + n2) : zero4<T>();
-    const T xl = i0 > 0 ? pnew1(idx - 1) : T(0);
-    const T xr = i0 + 4 < nn ? pnew1(idx + 4) : T(0);
-    V4<T> o;
+  const bool active = iq < n / 4 && j < n;
+  const unsigned mask = __ballot_sync(0xffffffffu, active);  // (the warp's active lanes are contiguous from 0)
+  const int lane = threadIdx.x;
+  if (active) {
+    const long i0 = 4L * iq, row = i0 + (long)j * nn;
+    V4<T> cm = k0 > 0 ? pnew4(row + (long)(k0 - 1) * n2) : zero4<T>();
+    V4<T> c = pnew4(row + (long)k0 * n2);
+    for (int k = k0; k < k1; ++k) {
+      const long idx = row + (long)k * n2;
+      const V4<T> cp = k + 1 < n ? pnew4(idx + n2) : zero4<T>();
+      sts4<S>(pn + idx, c);  // (exact: c is already representable in S)
+      const V4<T> ym = j > 0 ? pnew4(idx - nn) : zero4<T>();
+      const V4<T> yp = j + 1 < n ? pnew4(idx + nn) : zero4<T>();
+      // i neighbours: the adjacent lanes' quads by shuffle, loads at the warp's edges
+      const T up = __shfl_up_sync(mask, c.x[3], 1), dn = __shfl_down_sync(mask, c.x[0], 1);
+      const T xl = i0 == 0 ? T(0) : lane == 0 ? pnew1(idx - 1) : up;
+      const T xr = i0 + 4 >= nn ? T(0) : lane == kPqX - 1 ? pnew1(idx + 4) : dn;
+      V4<T> o;
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const T l = e == 0 ? xl : c.x[e - 1];
-      const T r = e == 3 ? xr : c.x[e + 1];
-      o.x[e] = heat_point<T>(s, g, c.x[e], l, r, ym.x[e], yp.x[e], zm.x[e], zp.x[e]);
+      for (int e = 0; e < 4; ++e) {
+        const T l = e == 0 ? xl : c.x[e - 1];
+        const T r = e == 3 ? xr : c.x[e + 1];
+        o.x[e] = heat_point<T>(s, g, c.x[e], l, r, ym.x[e], yp.x[e], cm.x[e], cp.x[e]);
+      }
+      const V4<T> st = sts4<S>(q + idx, o);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[0] = __fma_rn((double)c.x[e], (double)st.x[e], v[0]);
+      cm = c;
+      c = cp;
     }
-    const V4<T> st = sts4<S>(q + idx, o);
-#pragma unroll
-    for (int e = 0; e < 4; ++e) v[0] = __fma_rn((double)c.x[e], (double)st.x[e], v[0]);
   }
   grid_reduce<1>(v, red);
 }
@@ -389,13 +404,19 @@ struct AccKernels {
     note_partials(red, g);
     LAUNCHED("acc_update");
   }
-  // pn = z + beta p, q = A pn, red <- pn.q (bitwise xpby + apply_dot)
+  // pn = z + beta p, q = A pn, red <- pn.q (xpby + apply_dot's values; the
+  // dot's partial sums in another order)
   static void pq(const StencilSpec& A, const S* z, T beta, const S* p, S* pn, S* q, const RedSlot& red,
                  cudaStream_t st) {
-    const size_t quads = A.size() / 4;
-    const unsigned g = acc_grid(quads);
-    launch_pdl(k_acc_pq<T, S>, dim3(g), dim3(kAccBlock), 0, st, A.n, (T)A.sigma, (T)A.gamma, z, beta, p, pn, q, red);
-    note_partials(red, g);
+    const int n = A.n;
+    const unsigned gx = (unsigned)((n / 4 + kPqX - 1) / kPqX), gy = (unsigned)((n + kPqY - 1) / kPqY);
+    // k-chunks: about 8 resident CTAs of 256 threads per SM in one wave
+    const long cols = (long)gx * gy;
+    const int chunks = (int)std::max(1L, std::min((long)n, (long)sm_count() * 8 / std::max(1L, cols)));
+    const int kc = (n + chunks - 1) / chunks;
+    const dim3 grid(gx, gy, (unsigned)((n + kc - 1) / kc));
+    launch_pdl(k_acc_pq<T, S>, grid, dim3(kPqX, kPqY), 0, st, n, kc, (T)A.sigma, (T)A.gamma, z, beta, p, pn, q, red);
+    note_partials(red, grid.x * grid.y * grid.z);
     note_kron(std::is_same_v<T, float>);
     LAUNCHED("acc_pq");
   }
