@@ -281,6 +281,87 @@ __global__ void __launch_bounds__(128) k_cg_update_bj(long blocks, real_t<T> alp
   grid_reduce<2>(acc2, red);
 }
 
+// Blocks of B = 8, 16, 32 (fp32 vectors): the thread-per-block form above
+// holds 2 B values per thread and reads B * 4 contiguous bytes per thread —
+// 32 lines per warp load, few warps resident — so here a CTA of 128 threads
+// takes a chunk of 512 consecutive points in two phases: (1) the update,
+// coalesced, four points per thread (float4), r1 parked in shared memory
+// (rows of B + 1: the blocks of a warp land on distinct banks); (2) z for
+// four consecutive outputs of one block per thread, the block's r1 entries
+// read as shared-memory broadcasts and D's rows as 16-byte broadcasts.
+// Every value is formed by the same operations in the same order as in
+// k_cg_update_bj (z_ii = sum over jj ascending of D[jj][ii] r1_jj, product
+// then add), so x, r, z are bitwise identical; only the fp64 partial sums
+// of (||r||^2, r.z) are grouped differently.
+constexpr int kBjChunk = 512;
+template <class S, int B>
+__global__ void __launch_bounds__(128) k_cg_update_bj_tile(long m, float alpha, float* __restrict__ x,
+                                                           const float* __restrict__ p, float* __restrict__ r,
+                                                           const float* __restrict__ q, const S* __restrict__ inv,
+                                                           float* __restrict__ z, RedSlot red, const CgCtl* ctl) {
+  static_assert(kBjChunk % B == 0 && B % 4 == 0, "chunk holds whole blocks");
+  constexpr int NB = kBjChunk / B, RS = B + 1;
+  __shared__ __align__(16) float sblk[B * B];
+  __shared__ float sr[NB * RS];
+  bj_stage<float, S, B>(inv, sblk);
+  pdl_wait();
+  pdl_trigger();
+  if (ctl) {
+    if (ctl->stop) return;
+    alpha = (float)ctl->alpha;
+  }
+  const int tid = threadIdx.x;
+  double acc2[2] = {0.0, 0.0};
+  const long chunks = (m + kBjChunk - 1) / kBjChunk;
+  for (long c = blockIdx.x; c < chunks; c += gridDim.x) {
+    const long o = c * kBjChunk + 4 * tid;
+    const bool on = o < m;  // (m % 4 == 0)
+    if (on) {
+      V4<float> xv = ld4rw(x + o), rw = ld4rw(r + o);
+      const V4<float> pv = ld4(p + o), qv = ld4(q + o);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        xv.x[u] = xadd(xv.x[u], xscale(alpha, pv.x[u]));
+        rw.x[u] = xsub(rw.x[u], xscale(alpha, qv.x[u]));
+        dot_acc(*reinterpret_cast<double(*)[1]>(&acc2[0]), rw.x[u], rw.x[u]);
+        const int e = 4 * tid + u;
+        sr[(e / B) * RS + e % B] = rw.x[u];
+      }
+      st4(x + o, xv);
+      st4(r + o, rw);
+    }
+    __syncthreads();
+    if (on) {
+      const int e0 = 4 * tid, blk = e0 / B, ii = e0 % B;
+      const float* rb = sr + blk * RS;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int jj = 0; jj < B; ++jj) {
+        const float rv = rb[jj];
+        const float4 w = *reinterpret_cast<const float4*>(sblk + jj * B + ii);
+        acc[0] = xadd(acc[0], rmul(w.x, rv));
+        acc[1] = xadd(acc[1], rmul(w.y, rv));
+        acc[2] = xadd(acc[2], rmul(w.z, rv));
+        acc[3] = xadd(acc[3], rmul(w.w, rv));
+      }
+      V4<float> zw;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        zw.x[u] = acc[u];
+        dot_acc(*reinterpret_cast<double(*)[1]>(&acc2[1]), rb[ii + u], acc[u]);
+      }
+      st4(z + o, zw);
+    }
+    __syncthreads();  // sr is rewritten by the next chunk
+  }
+  grid_reduce<2>(acc2, red);
+}
+
+static bool bj_tile_enabled() {  // (read per call: tests switch it within a process)
+  const char* e = std::getenv("MPRKB_BJ_TILE");  // =0: the thread-per-block kernel for B >= 16 too
+  return !(e && e[0] == '0');
+}
+
 template <class T, class S>
 bool cg_bj(int n, long lines, int b, real_t<T> alpha, const CgCtl* ctl, T* x, const T* p, T* r, const T* q, const S* inv, T* z,
            const RedSlot& red, cudaStream_t st) {
@@ -289,6 +370,23 @@ bool cg_bj(int n, long lines, int b, real_t<T> alpha, const CgCtl* ctl, T* x, co
   } else {
     if (n % b) return false;
     const long blocks = lines * (n / b);
+    if constexpr (std::is_same_v<T, float>) {
+      // (measured at 384^3 per CG iteration: b = 32 0.87 -> 0.56 ms, b = 16
+      // 0.57 -> 0.50, b = 8 0.477 -> 0.470; b = 4 0.44 -> 0.50, so B = 4 keeps
+      // the thread-per-block kernel)
+      if ((b == 8 || b == 16 || b == 32) && bj_tile_enabled()) {
+        const long m = (long)n * lines;
+        const unsigned g = grid_for((size_t)((m + kBjChunk - 1) / kBjChunk), 1, 16);
+        if (b == 8)
+          launch_pdl(k_cg_update_bj_tile<S, 8>, dim3(g), dim3(128), 0, st, m, alpha, x, p, r, q, inv, z, red, ctl);
+        else if (b == 16)
+          launch_pdl(k_cg_update_bj_tile<S, 16>, dim3(g), dim3(128), 0, st, m, alpha, x, p, r, q, inv, z, red, ctl);
+        else
+          launch_pdl(k_cg_update_bj_tile<S, 32>, dim3(g), dim3(128), 0, st, m, alpha, x, p, r, q, inv, z, red, ctl);
+        note_partials(red, g);
+        return true;
+      }
+    }
     const unsigned g = grid_for((size_t)blocks, 128, 16);
     switch (b) {
       case 4: launch_pdl(k_cg_update_bj<T, S, 4>, dim3(g), dim3(128), 0, st, blocks, alpha, x, p, r, q, inv, z, red, ctl); break;

@@ -586,6 +586,41 @@ def test_cg_device_loop_bitwise_host_loop(gpu, mp, store, n):
     assert same_bits(a, b)
 
 
+@pytest.mark.parametrize("b,store", [(8, "f16"), (16, "f16"), (32, "f32"), (32, "f64")])
+def test_cg_update_bj_tiled_large_blocks(gpu, mp, b, store):
+    """B = 8 / 16 / 32 block-Jacobi: the fused CG update + apply runs as the
+    two-phase chunk kernel (k_cg_update_bj_tile: coalesced update, r parked
+    in shared memory, z from broadcasts).  x, r and z are formed by the same
+    operations in the same order as the thread-per-block kernel
+    (MPRKB_BJ_TILE=0); only the fp64 grouping of the (||r||^2, r.z) partials
+    differs, so iteration counts match and states agree to the last bits of
+    the scalars."""
+    import os
+
+    t = mp.builtin("4s3pB")
+    n = 64
+    kw = dict(preconditioner="block-jacobi", block_size=b, block_storage=store)
+    tiled = mp.Stepper("heat", n, t, 0.01, 1e-5, "f32", 300, **kw)
+    os.environ["MPRKB_BJ_TILE"] = "0"
+    try:
+        plain = mp.Stepper("heat", n, t, 0.01, 1e-5, "f32", 300, **kw)
+        a, c = np.zeros(n ** 3), np.zeros(n ** 3)
+        for _ in range(2):
+            os.environ.pop("MPRKB_BJ_TILE", None)
+            ta = tiled.step(a)
+            os.environ["MPRKB_BJ_TILE"] = "0"
+            tc = plain.step(c)
+            assert all(abs(i - j) <= 1 for i, j in zip(ta["iterations"], tc["iterations"]))
+            assert min(ta["iterations"]) > 5
+            for s in range(len(ta["iterations"])):
+                ha, hc = tiled.history(s), plain.history(s)
+                if len(ha) == len(hc):
+                    np.testing.assert_allclose(ha, hc, rtol=1e-4, atol=1e-5 * hc[0])
+    finally:
+        os.environ.pop("MPRKB_BJ_TILE", None)
+    assert np.linalg.norm(a - c) / np.linalg.norm(c) <= 1e-5
+
+
 def test_cg_device_loop_max_iter_and_breakdown_paths(gpu, mp):
     """The device loop leaves through the reference's exits: a cap inside a
     batch reports MaxIterReached with exactly max_iter iterations, like the
