@@ -200,8 +200,71 @@ __global__ void __launch_bounds__(128) k_block_jacobi_row(long blocks, const S* 
   }
 }
 
+// The apply alone (B = 8, 16, 32) in the chunked two-phase form of
+// k_cg_update_bj_tile (below; 256^3, b = 8 fp16 blocks: 30.8 -> 28.8 us): r arrives coalesced (float4 per thread) into shared memory rows of
+// B + 1, then each thread forms four consecutive outputs of one block from
+// broadcasts — the same operations in the same order as k_block_jacobi_row.
+constexpr int kBjApplyChunk = 512;
+template <class S, int B>
+__global__ void __launch_bounds__(128) k_block_jacobi_tile(long m, const S* __restrict__ inv,
+                                                           const float* __restrict__ r, float* __restrict__ z) {
+  constexpr int NB = kBjApplyChunk / B, RS = B + 1;
+  __shared__ __align__(16) float sblk[B * B];
+  __shared__ float sr[NB * RS];
+  bj_stage<float, S, B>(inv, sblk);
+  const int tid = threadIdx.x;
+  const long chunks = (m + kBjApplyChunk - 1) / kBjApplyChunk;
+  for (long c = blockIdx.x; c < chunks; c += gridDim.x) {
+    const long o = c * kBjApplyChunk + 4 * tid;
+    const bool on = o < m;
+    if (on) {
+      const V4<float> rw = ld4(r + o);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int e = 4 * tid + u;
+        sr[(e / B) * RS + e % B] = rw.x[u];
+      }
+    }
+    __syncthreads();
+    if (on) {
+      const int e0 = 4 * tid, ii = e0 % B;
+      const float* rb = sr + (e0 / B) * RS;
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int jj = 0; jj < B; ++jj) {
+        const float rv = rb[jj];
+        const float4 w = *reinterpret_cast<const float4*>(sblk + jj * B + ii);
+        acc[0] = xadd(acc[0], rmul(w.x, rv));
+        acc[1] = xadd(acc[1], rmul(w.y, rv));
+        acc[2] = xadd(acc[2], rmul(w.z, rv));
+        acc[3] = xadd(acc[3], rmul(w.w, rv));
+      }
+      V4<float> zw;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) zw.x[u] = acc[u];
+      st4(z + o, zw);
+    }
+    __syncthreads();
+  }
+}
+
+static bool bj_tile_enabled();
+
 template <class T, class S>
 bool bj_row(int n, long lines, int b, const S* inv, const T* r, T* z, cudaStream_t st) {
+  if constexpr (std::is_same_v<T, float>) {
+    if (n % b == 0 && (b == 8 || b == 16 || b == 32) && bj_tile_enabled()) {
+      const long m = (long)n * lines;
+      const unsigned g = grid_for((size_t)((m + kBjApplyChunk - 1) / kBjApplyChunk), 1, 16);
+      if (b == 8)
+        k_block_jacobi_tile<S, 8><<<g, 128, 0, st>>>(m, inv, r, z);
+      else if (b == 16)
+        k_block_jacobi_tile<S, 16><<<g, 128, 0, st>>>(m, inv, r, z);
+      else
+        k_block_jacobi_tile<S, 32><<<g, 128, 0, st>>>(m, inv, r, z);
+      return true;
+    }
+  }
   {  // (complex T: real blocks times complex segments, per component)
     if (n % b) return false;
     const long blocks = lines * (n / b);
@@ -281,7 +344,7 @@ __global__ void __launch_bounds__(128) k_cg_update_bj(long blocks, real_t<T> alp
   grid_reduce<2>(acc2, red);
 }
 
-// Blocks of B = 8, 16, 32 (fp32 vectors): the thread-per-block form above
+// Blocks of B = 16, 32 (fp32 vectors): the thread-per-block form above
 // holds 2 B values per thread and reads B * 4 contiguous bytes per thread —
 // 32 lines per warp load, few warps resident — so here a CTA of 128 threads
 // takes a chunk of 512 consecutive points in two phases: (1) the update,
@@ -372,14 +435,12 @@ bool cg_bj(int n, long lines, int b, real_t<T> alpha, const CgCtl* ctl, T* x, co
     const long blocks = lines * (n / b);
     if constexpr (std::is_same_v<T, float>) {
       // (measured at 384^3 per CG iteration: b = 32 0.87 -> 0.56 ms, b = 16
-      // 0.57 -> 0.50, b = 8 0.477 -> 0.470; b = 4 0.44 -> 0.50, so B = 4 keeps
-      // the thread-per-block kernel)
-      if ((b == 8 || b == 16 || b == 32) && bj_tile_enabled()) {
+      // 0.57 -> 0.50; b = 8 within +-2 % either way (384^3 / 256^3) and b = 4
+      // 0.44 -> 0.50, so B <= 8 keeps the thread-per-block kernel)
+      if ((b == 16 || b == 32) && bj_tile_enabled()) {
         const long m = (long)n * lines;
         const unsigned g = grid_for((size_t)((m + kBjChunk - 1) / kBjChunk), 1, 16);
-        if (b == 8)
-          launch_pdl(k_cg_update_bj_tile<S, 8>, dim3(g), dim3(128), 0, st, m, alpha, x, p, r, q, inv, z, red, ctl);
-        else if (b == 16)
+        if (b == 16)
           launch_pdl(k_cg_update_bj_tile<S, 16>, dim3(g), dim3(128), 0, st, m, alpha, x, p, r, q, inv, z, red, ctl);
         else
           launch_pdl(k_cg_update_bj_tile<S, 32>, dim3(g), dim3(128), 0, st, m, alpha, x, p, r, q, inv, z, red, ctl);

@@ -93,6 +93,35 @@ def test_block_jacobi_apply(gpu, mp, kind, storage, b):
     assert np.abs(back - r.reshape(-1, n)[:, :bs]).max() <= eps * max(1.0, np.abs(D).sum(1).max())
 
 
+@pytest.mark.parametrize("storage", ["f16", "f32", "f64"])
+@pytest.mark.parametrize("b", [8, 16, 32])
+def test_block_jacobi_apply_chunked_bitwise(gpu, mp, storage, b):
+    """fp32 block-Jacobi apply with n % b == 0 runs as the chunked two-phase
+    kernel (k_block_jacobi_tile); it forms every output with the same
+    operations in the same order as the thread-per-block kernel
+    (MPRKB_BJ_TILE=0), so the results are bitwise equal, and they match the
+    numpy emulation like the generic path."""
+    import os
+
+    import torch
+
+    n, tau, a = 64, 0.025, 0.5
+    sigma, gamma = stage_params(0, n, tau, a)
+    P = mp.Operator.block_jacobi(0, "heat", n, tau, a, b, storage)
+    r = np.random.default_rng(b).uniform(-1, 1, n ** 3).astype(np.float32)
+    rt = torch.from_numpy(r).cuda()
+    got = P.apply(rt).cpu().numpy()
+    os.environ["MPRKB_BJ_TILE"] = "0"
+    try:
+        ref_k = P.apply(rt).cpu().numpy()
+    finally:
+        os.environ.pop("MPRKB_BJ_TILE", None)
+    assert np.array_equal(got.view(np.uint32), ref_k.view(np.uint32))
+    want = NumpyBlockJacobi(n, b, sigma, gamma, storage, 0, 0)(r)
+    tol = 2e-3 if storage == "f16" else 2e-6
+    assert np.abs(got - want).max() <= tol * max(1.0, np.abs(want).max())
+
+
 @pytest.mark.parametrize("kind,storage", [(1, "f64"), (0, "f32"), (0, "f16")])
 def test_cg_block_jacobi_matches_reference_cg(gpu, mp, ref, kind, storage):
     """Block-Jacobi CG on the GPU vs the reference's own cg<T> with the numpy

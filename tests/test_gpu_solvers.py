@@ -586,9 +586,9 @@ def test_cg_device_loop_bitwise_host_loop(gpu, mp, store, n):
     assert same_bits(a, b)
 
 
-@pytest.mark.parametrize("b,store", [(8, "f16"), (16, "f16"), (32, "f32"), (32, "f64")])
+@pytest.mark.parametrize("b,store", [(16, "f16"), (32, "f32"), (32, "f64")])
 def test_cg_update_bj_tiled_large_blocks(gpu, mp, b, store):
-    """B = 8 / 16 / 32 block-Jacobi: the fused CG update + apply runs as the
+    """B = 16 / 32 block-Jacobi: the fused CG update + apply runs as the
     two-phase chunk kernel (k_cg_update_bj_tile: coalesced update, r parked
     in shared memory, z from broadcasts).  x, r and z are formed by the same
     operations in the same order as the thread-per-block kernel
