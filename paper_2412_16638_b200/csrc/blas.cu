@@ -259,8 +259,28 @@ void tuple_sums(const RedSlot& slot, int ncomp, double* out, cudaStream_t st) {
 // Three warp groups sum the three slots' lane shares concurrently (one
 // 16-byte load per tuple for the pairs), then five threads add the 128 lanes
 // of one component each in lane order — every sum bitwise sum_partials'.
+// The verdict from the five global sums (||r0||^2, p.Ap, r.z, ||r1||^2,
+// ||b - A x1||^2): krylov.cpp's casts and the reference's decisions.
+__device__ __forceinline__ void spec_verdict(double r0s, double pqs, double rzs, double f0, double f1, double tol,
+                                             double* rec, int* fail) {
+  // krylov.cpp: r0 = (double)sqrt((R)v0); rnorm / rt likewise; rz, pq = (R) sums
+  const double r0 = (double)sqrtf(__double2float_rn(r0s));
+  const double rn = (double)sqrtf(__double2float_rn(f0)), rt = (double)sqrtf(__double2float_rn(f1));
+  const float rz = __double2float_rn(rzs), pq = __double2float_rn(pqs);
+  auto sat = [&](double v) { return v <= tol || (r0 > 0 && v / r0 <= tol); };  // StoppingCriterion::satisfied
+  const bool ok = !sat(r0) && rz > 0.0f && pq > 0.0f && sat(rn) && sat(rt);
+  rec[0] = r0;
+  rec[1] = rn;
+  rec[2] = rt;
+  rec[3] = ok ? 1.0 : 0.0;
+  if (!ok) *fail = 1;
+}
+
+// loc (split grid, nullable): write this rank's five sums there instead of
+// judging (they are all-gathered and judged by k_cg_spec_ranks)
 __global__ void __launch_bounds__(3 * kRedLanes) k_cg_spec(const double* t0, int n0, const double* t2, int n2,
-                                                         const double* t3, int n3, double tol, double* rec, int* fail) {
+                                                         const double* t3, int n3, double tol, double* rec, int* fail,
+                                                         double* loc) {
   pdl_wait();
   pdl_trigger();
   __shared__ double lanes[5][kRedLanes];
@@ -283,25 +303,47 @@ __global__ void __launch_bounds__(3 * kRedLanes) k_cg_spec(const double* t0, int
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
-  const double r0s = tot[0], pqs = tot[1], rzs = tot[2], f0 = tot[3], f1 = tot[4];
-  // krylov.cpp: r0 = (double)sqrt((R)v0); rnorm / rt likewise; rz, pq = (R) sums
-  const double r0 = (double)sqrtf(__double2float_rn(r0s));
-  const double rn = (double)sqrtf(__double2float_rn(f0)), rt = (double)sqrtf(__double2float_rn(f1));
-  const float rz = __double2float_rn(rzs), pq = __double2float_rn(pqs);
-  auto sat = [&](double v) { return v <= tol || (r0 > 0 && v / r0 <= tol); };  // StoppingCriterion::satisfied
-  const bool ok = !sat(r0) && rz > 0.0f && pq > 0.0f && sat(rn) && sat(rt);
-  rec[0] = r0;
-  rec[1] = rn;
-  rec[2] = rt;
-  rec[3] = ok ? 1.0 : 0.0;
-  if (!ok) *fail = 1;
+  if (loc) {
+#pragma unroll
+    for (int c = 0; c < 5; ++c) loc[c] = tot[c];
+    return;
+  }
+  spec_verdict(tot[0], tot[1], tot[2], tot[3], tot[4], tol, rec, fail);
+}
+
+// g = the ranks' five local sums ([rank][5], all-gathered): each global sum
+// added in rank order from 0, as Comm::allreduce_sum forms it on the host
+__global__ void k_cg_spec_ranks(const double* g, int ranks, double tol, double* rec, int* fail) {
+  pdl_wait();
+  pdl_trigger();
+  if (threadIdx.x != 0) return;
+  double v[5];
+#pragma unroll
+  for (int c = 0; c < 5; ++c) {
+    double s = 0.0;
+    for (int r = 0; r < ranks; ++r) s += g[5 * r + c];
+    v[c] = s;
+  }
+  spec_verdict(v[0], v[1], v[2], v[3], v[4], tol, rec, fail);
 }
 
 void cg_spec_judge(const RedSlot& s0, const RedSlot& s2, const RedSlot& s3, double tol, double* rec, int* fail,
                    cudaStream_t st) {
   if (!s0.dpart || !s2.dpart || !s3.dpart) MPRKB_THROW(10, "cg_spec_judge: the reductions need device tuples");
   launch_pdl(k_cg_spec, dim3(1), dim3(3 * kRedLanes), 0, st, (const double*)s0.dpart, *s0.count, (const double*)s2.dpart,
-             *s2.count, (const double*)s3.dpart, *s3.count, tol, rec, fail);
+             *s2.count, (const double*)s3.dpart, *s3.count, tol, rec, fail, (double*)nullptr);
+  LAUNCHED("cg_spec");
+}
+
+void cg_spec_local(const RedSlot& s0, const RedSlot& s2, const RedSlot& s3, double* loc, cudaStream_t st) {
+  if (!s0.dpart || !s2.dpart || !s3.dpart) MPRKB_THROW(10, "cg_spec_local: the reductions need device tuples");
+  launch_pdl(k_cg_spec, dim3(1), dim3(3 * kRedLanes), 0, st, (const double*)s0.dpart, *s0.count, (const double*)s2.dpart,
+             *s2.count, (const double*)s3.dpart, *s3.count, 0.0, (double*)nullptr, (int*)nullptr, loc);
+  LAUNCHED("cg_spec");
+}
+
+void cg_spec_ranks(const double* gathered, int ranks, double tol, double* rec, int* fail, cudaStream_t st) {
+  launch_pdl(k_cg_spec_ranks, dim3(1), dim3(32), 0, st, gathered, ranks, tol, rec, fail);
   LAUNCHED("cg_spec");
 }
 

@@ -253,7 +253,9 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
   const bool dev_alpha = fuse_first && !split;
   const char* sda_env = std::getenv("MPRKB_SPLIT_DEVALPHA");
   const bool gath_alpha = fuse_first && split && !(sda_env && sda_env[0] == '0');
-  const bool speculate = dev_alpha && spec != nullptr;
+  // (split grid: the judge adds the ranks' all-gathered local sums on the
+  // device, so a split solve needs no round trip either)
+  const bool speculate = (dev_alpha || gath_alpha) && spec != nullptr && !(gath_alpha && spec->defer);
   const RedSlot s2 = (dev_alpha || gath_alpha) ? w.red.slot_dev(2) : w.red.slot(2);
   const RedSlot s3 = speculate ? w.red.slot_dev(3) : w.red.slot(3);
   double r0;
@@ -332,11 +334,25 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
         }
       } else if (gath_alpha) {
         const int P = w.comm->size();
-        double* lsum = w.scal_dev(2 + 2 * (size_t)P);
+        double* lsum = w.scal_dev(2 + 2 * (size_t)P + 5 + 5 * (size_t)P);
         tuple_sums(s2, 2, lsum, st);                     // this rank's (p.Ap, r.z)
         w.comm->allgather_dev(lsum, lsum + 2, 2, st);    // every rank's, in rank order
-        Bracket br(timer, "stencil", st);
-        cg_fused_update(*S, 0.0f, nullptr, x, z, b, r, x_alt, s3, st, lsum + 2, P);
+        {
+          Bracket br(timer, "stencil", st);
+          cg_fused_update(*S, 0.0f, nullptr, x, z, b, r, x_alt, s3, st, lsum + 2, P,
+                          speculate ? spec->x1_finite : nullptr);
+        }
+        if (speculate) {
+          double* l5 = lsum + 2 + 2 * (size_t)P;
+          cg_spec_local(w.red.slot_dev(0), s2, s3, l5, st);
+          w.comm->allgather_dev(l5, l5 + 5, 5, st);
+          cg_spec_ranks(l5 + 5, P, crit.tol, spec->rec, spec->fail, st);
+          rep.iterations = 1;
+          rep.converged = true;
+          rep.speculative = true;
+          if (result) *result = x_alt;
+          return;
+        }
       }
     }
     stream_sync(st);

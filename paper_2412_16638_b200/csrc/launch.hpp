@@ -75,6 +75,12 @@ void tuple_sums(const RedSlot& slot, int ncomp, double* out, cudaStream_t st);
 // rounding: rec = (r0, ||r1||, ||b - A x1||, ok); *fail = 1 unless ok.
 void cg_spec_judge(const RedSlot& s0, const RedSlot& s2, const RedSlot& s3, double tol, double* rec, int* fail,
                    cudaStream_t st);
+// The same on a split grid: cg_spec_local writes this rank's five sums
+// (||r0||^2, p.Ap, r.z, ||r1||^2, ||b - A x1||^2) to loc (device); after they
+// are all-gathered ([rank][5]), cg_spec_ranks adds each in rank order (as
+// Comm::allreduce_sum) and judges — the same verdict on every rank.
+void cg_spec_local(const RedSlot& s0, const RedSlot& s2, const RedSlot& s3, double* loc, cudaStream_t st);
+void cg_spec_ranks(const double* gathered, int ranks, double tol, double* rec, int* fail, cudaStream_t st);
 
 // apply_f (operators.cpp:81-96), F64 policy: out = K y + g, y read as double
 // or widened from float (`y32`, the fp32 stage solution, exact), g may be

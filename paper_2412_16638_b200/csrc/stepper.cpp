@@ -203,11 +203,14 @@ Stepper::Stepper(const StepperConfig& cfg)
     // speculative stage solves: the fused fp32 pipeline, undivided grid,
     // FAST numerics, the exact-inverse preconditioner (FastDiag)
     const char* e = std::getenv("MPRKB_SPECULATE");
-    speculate_ = fused_ && !pull_ && !slab_.split() && cfg_.num == Numerics::Fast && cfg_.precond == 0 &&
-                 !(e && e[0] == '0');
+    // (a split grid speculates too: its judge adds the ranks' all-gathered
+    // sums on the device; MPRKB_SPLIT_SPECULATE=0 keeps the round trips there)
+    const char* se = std::getenv("MPRKB_SPLIT_SPECULATE");
+    speculate_ = fused_ && !pull_ && (!slab_.split() || !(se && se[0] == '0')) && cfg_.num == Numerics::Fast &&
+                 cfg_.precond == 0 && !(e && e[0] == '0');
     if (speculate_) spec_rec_.alloc(sizeof(double) * 4 * (size_t)q);
     const char* me = std::getenv("MPRKB_SPEC_MERGE");
-    spec_merge_ = speculate_ && me && me[0] == '1';  // (opt-in: measured no faster)
+    spec_merge_ = speculate_ && !slab_.split() && me && me[0] == '1';  // (opt-in: measured no faster)
     for (const StageSolver& S : solvers_)
       spec_merge_ = spec_merge_ && S.op->stencil() && update_feval_supported(*S.op->stencil(), kspec_);
   }
@@ -438,13 +441,19 @@ void Stepper::step_fused(double* u, StepTrace& trace, bool speculate) {
     checks.push_back({next, code, msg});
     return flags_.dev(next++);
   };
+  // returns whether a code-0 check (the speculation verdict) is raised on
+  // any rank
   auto raise_flags = [&]() {
     stream_sync(st_);
     std::vector<double> v(checks.size());
     for (size_t i = 0; i < checks.size(); ++i) v[i] = flags_.value(checks[i].slot) ? 1.0 : 0.0;
     if (slab_.split() && !v.empty()) slab_.comm->allreduce_max(v.data(), (int)v.size());
-    for (size_t i = 0; i < checks.size(); ++i)
+    bool missed = false;
+    for (size_t i = 0; i < checks.size(); ++i) {
       if (v[i] != 0.0 && checks[i].code != 0) MPRKB_THROW(checks[i].code, checks[i].msg);
+      if (v[i] != 0.0 && checks[i].code == 0) missed = true;
+    }
+    return missed;
   };
   // (speculation: its verdict flag is the first slot, inside the range the
   // final update is gated on; code 0 = not an error)
@@ -576,7 +585,15 @@ void Stepper::step_fused(double* u, StepTrace& trace, bool speculate) {
     extract_stage(m, 0, cur, y_.as<double>(), check_slot(9, kStage), st_);
   }
   const int stage_checks = next - 1;
-  if (slab_.split()) raise_flags();
+  // (a split grid decides on the host before its final update — one round
+  // trip per step — instead of gating it on the device: a failed speculative
+  // solve (the verdict, the same on every rank) leaves u untouched and redoes
+  // the step with round trips, like the gated undivided path)
+  if (slab_.split() && raise_flags() && speculate) {
+    if (timer_.enabled()) timer_.resolve();
+    step_fused(u, trace, false);
+    return;
+  }
   CombineTerms fin;
   if (!fuse_final)
     for (int i = 0; i < q; ++i)

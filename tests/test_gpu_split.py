@@ -235,6 +235,35 @@ def test_nccl_single_rank(gpu, mp):
         del st
 
 
+
+@pytest.mark.parametrize("ranks,tol", [(2, 1e-3), (4, 1e-3), (2, 1e-7)])
+def test_split_speculative_stage_solves_bitwise(gpu, mp, ranks, tol):
+    """Split grids speculate like the undivided grid: each solve's judge adds
+    the ranks' all-gathered local sums (||r0||^2, p.Ap, r.z, ||r1||^2,
+    ||b - A x1||^2) in rank order on the device, so the step needs no round
+    trip per solve; states, iteration counts and residual histories are
+    bitwise the round-trip path (MPRKB_SPLIT_SPECULATE=0).  tol 1e-7 forces
+    misses (the one-iteration exit fails, the step is redone with round trips)."""
+    import os
+
+    make = maker(mp, "heat", 256, "4s3pB", "f32", "fast", tol)
+    a, ta, ha = run_split(mp, ranks, 2, make)
+    os.environ["MPRKB_SPLIT_SPECULATE"] = "0"
+    try:
+        b, tb, hb = run_split(mp, ranks, 2, make)
+    finally:
+        os.environ.pop("MPRKB_SPLIT_SPECULATE", None)
+    assert [t["iterations"] for t in ta] == [t["iterations"] for t in tb]
+    if tol > 1e-5:
+        assert all(i == 1 for t in ta for i in t["iterations"])
+    else:
+        assert max(i for t in ta for i in t["iterations"]) > 1
+    for x, y in zip(ha, hb):
+        for hx, hy in zip(x, y):
+            assert np.array_equal(np.asarray(hx), np.asarray(hy))
+    assert np.array_equal(a, b)
+
+
 @pytest.mark.parametrize("ranks", [2, 4])
 def test_split_device_alpha_bitwise_host_alpha(gpu, mp, ranks):
     """On a split grid the fused first CG update takes alpha from the ranks'
