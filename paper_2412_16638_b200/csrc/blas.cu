@@ -6,6 +6,7 @@
 // 148 x 8 CTAs; per-element arithmetic is the reference's (no contraction),
 // so results are bitwise the reference's except where a FAST reduction is
 // folded in (fp64-accumulated, deterministic, see reduce.cuh).
+#include "comm.hpp"
 #include "launch.hpp"
 #include "pdl.cuh"
 #include "reduce.cuh"
@@ -340,6 +341,28 @@ void cg_spec_local(const RedSlot& s0, const RedSlot& s2, const RedSlot& s3, doub
   launch_pdl(k_cg_spec, dim3(1), dim3(3 * kRedLanes), 0, st, (const double*)s0.dpart, *s0.count, (const double*)s2.dpart,
              *s2.count, (const double*)s3.dpart, *s3.count, 0.0, (double*)nullptr, (int*)nullptr, loc);
   LAUNCHED("cg_spec");
+}
+
+// Split-grid gate of the final update: every rank's stage-check flags
+// all-gathered on the stream ([rank][n] as doubles), OR-ed into `gate`, so a
+// check raised on any rank keeps every rank's u untouched without a host
+// round trip (the host raises the errors collectively after the step).
+__global__ void k_flags_f64(const int* flags, int n, double* out) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = flags[i] ? 1.0 : 0.0;
+}
+__global__ void k_gate_or(const double* g, int ranks, int n, int* gate) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    int v = 0;
+    for (int r = 0; r < ranks; ++r) v |= g[(size_t)r * n + i] != 0.0;
+    gate[i] = v;
+  }
+}
+void split_gate(const int* flags, int n, Comm& comm, double* scratch, int* gate, cudaStream_t st) {
+  k_flags_f64<<<1, 256, 0, st>>>(flags, n, scratch);
+  LAUNCHED("split_gate");
+  comm.allgather_dev(scratch, scratch + n, n, st);
+  k_gate_or<<<1, 256, 0, st>>>(scratch + n, comm.size(), n, gate);
+  LAUNCHED("split_gate");
 }
 
 void cg_spec_ranks(const double* gathered, int ranks, double tol, double* rec, int* fail, cudaStream_t st) {

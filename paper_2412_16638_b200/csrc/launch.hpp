@@ -81,6 +81,10 @@ void cg_spec_judge(const RedSlot& s0, const RedSlot& s2, const RedSlot& s3, doub
 // Comm::allreduce_sum) and judges — the same verdict on every rank.
 void cg_spec_local(const RedSlot& s0, const RedSlot& s2, const RedSlot& s3, double* loc, cudaStream_t st);
 void cg_spec_ranks(const double* gathered, int ranks, double tol, double* rec, int* fail, cudaStream_t st);
+// gate[i] <- OR over the ranks of flags[i] (i < n), stream-ordered through
+// comm.allgather_dev; scratch: (ranks + 1) n device doubles
+class Comm;
+void split_gate(const int* flags, int n, Comm& comm, double* scratch, int* gate, cudaStream_t st);
 
 // apply_f (operators.cpp:81-96), F64 policy: out = K y + g, y read as double
 // or widened from float (`y32`, the fp32 stage solution, exact), g may be

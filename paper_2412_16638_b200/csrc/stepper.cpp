@@ -585,11 +585,14 @@ void Stepper::step_fused(double* u, StepTrace& trace, bool speculate) {
     extract_stage(m, 0, cur, y_.as<double>(), check_slot(9, kStage), st_);
   }
   const int stage_checks = next - 1;
-  // (a split grid decides on the host before its final update — one round
-  // trip per step — instead of gating it on the device: a failed speculative
-  // solve (the verdict, the same on every rank) leaves u untouched and redoes
-  // the step with round trips, like the gated undivided path)
-  if (slab_.split() && raise_flags() && speculate) {
+  // (a split grid gates its final update on the device too: the ranks'
+  // stage-check flags are all-gathered on the stream and OR-ed, so a check —
+  // or a failed speculative solve — on any rank leaves every rank's u
+  // untouched; MPRKB_SPLIT_GATE=0 decides on the host before the update, one
+  // more round trip per step)
+  const char* sg = std::getenv("MPRKB_SPLIT_GATE");
+  const bool split_gate_dev = slab_.split() && !(sg && sg[0] == '0');
+  if (slab_.split() && !split_gate_dev && raise_flags() && speculate) {
     if (timer_.enabled()) timer_.resolve();
     step_fused(u, trace, false);
     return;
@@ -605,6 +608,11 @@ void Stepper::step_fused(double* u, StepTrace& trace, bool speculate) {
     if (!slab_.split() && stage_checks > 0) {
       CUDA_CHECK(cudaMemcpyAsync(gate_dev_.get(), flags_.dev(1), sizeof(int) * stage_checks, cudaMemcpyHostToDevice,
                                  st_));
+      gate = gate_dev_.as<int>();
+    } else if (split_gate_dev && stage_checks > 0) {
+      const size_t need = sizeof(double) * (size_t)(slab_.comm->size() + 1) * stage_checks;
+      if (gate_scratch_.bytes() < need) gate_scratch_.alloc(need);
+      split_gate(flags_.dev(1), stage_checks, *slab_.comm, gate_scratch_.as<double>(), gate_dev_.as<int>(), st_);
       gate = gate_dev_.as<int>();
     }
     if (fuse_final)

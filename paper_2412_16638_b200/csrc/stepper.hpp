@@ -100,6 +100,7 @@ class Stepper {
   std::vector<DevBuf> f_hi_, f_eps_;
   DevBuf y_, bsol_, xsol_;
   DevBuf gate_dev_;  // device copy of the stage checks gating the final update
+  DevBuf gate_scratch_;  // split grid: the ranks' all-gathered stage-check flags
   std::unique_ptr<KrylovWork<float>> w32_;
   std::unique_ptr<KrylovWork<double>> w64_;
   std::unique_ptr<KrylovWork<c32>> wc32_;

@@ -201,6 +201,37 @@ def test_split_errors_raised_on_every_rank(gpu, mp):
     assert mp.run_ranks(2, body) == ["raised", "raised"]
 
 
+@pytest.mark.parametrize("gate", ["device", "host"])
+def test_split_fused_step_error_leaves_every_slab_untouched(gpu, mp, gate):
+    """The fused fp32 split step gates its final update on the OR of every
+    rank's stage checks (all-gathered on the stream; MPRKB_SPLIT_GATE=0: the
+    host decides before the update): a NaN in one rank's slab raises
+    NonFiniteState on every rank and no rank's state is modified."""
+    import os
+
+    tab = mp.builtin("4s3pB")
+
+    def body(rank, comm):
+        st = mp.Stepper("heat", 256, tab, 0.01, 1e-3, "f32", 40, comm=comm)
+        u = st.initial_state() + 0.5
+        if rank == 1:
+            u[12345] = np.nan
+        u0 = u.copy()
+        try:
+            st.step(u)
+        except mp.NonFiniteState:
+            return "raised", np.array_equal(u, u0, equal_nan=True)
+        return "no error", False
+
+    if gate == "host":
+        os.environ["MPRKB_SPLIT_GATE"] = "0"
+    try:
+        res = mp.run_ranks(2, body)
+    finally:
+        os.environ.pop("MPRKB_SPLIT_GATE", None)
+    assert res == [("raised", True), ("raised", True)]
+
+
 def test_split_rejects_uneven_slabs(gpu, mp):
     tab = mp.builtin("4s3pB")
 
