@@ -227,10 +227,10 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
   // reference would have skipped only touches scratch vectors (never x).
   const bool batch = fast && S != nullptr;
   const bool spec_true = batch && P != nullptr && P->exact_inverse();
-  // ... and (fp32, undivided grid, a second solution buffer) the first
-  // update, ||r1|| and the true residual in one pass that leaves q unwritten
+  // ... and (fp32 / fp64 real, a second solution buffer) the first update,
+  // ||r1|| and the true residual in one pass that leaves q unwritten
   bool fuse_first = false;
-  if constexpr (std::is_same_v<T, float>) {
+  if constexpr (std::is_same_v<T, float> || std::is_same_v<T, double>) {
     const char* env = std::getenv("MPRKB_CG_FUSED");  // (=0: the unfused kernels, for A/B tests)
     fuse_first = spec_true && x_alt != nullptr && cg_fused_supported(*S) && !(env && env[0] == '0');
   }
@@ -304,7 +304,7 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
       Bracket br(timer, "stencil", st);
       stencil_apply_dot2<T>(*S, z, fuse_first ? nullptr : q, r, s2, st);  // q = A z, (z.q, r.z)
     }
-    if constexpr (std::is_same_v<T, float>) {
+    if constexpr (std::is_same_v<T, float> || std::is_same_v<T, double>) {
       if (speculate && spec->defer) {
         // the caller fuses the update into its next pass and judges it
         spec->dir = z;
@@ -365,7 +365,7 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
       fused_v[0] = v[3];
       fused_v[1] = v[4];
     }
-    if constexpr (std::is_same_v<T, float>) {
+    if constexpr (std::is_same_v<T, float> || std::is_same_v<T, double>) {
       if (fuse_first && !dev_alpha && !gath_alpha) {  // split grid: the same pass with the global alpha
         const R a = (R)v[2] / (R)v[1];
         {
@@ -504,7 +504,7 @@ void cg_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num, Kr
         }
       }
       bool fused = false;
-      if constexpr (std::is_same_v<T, float>) {
+      if constexpr (std::is_same_v<T, float> || std::is_same_v<T, double>) {
         if (fuse_first && k == 0) {  // already ran (above), with this alpha
           std::swap(x, x_alt);
           fused = true;

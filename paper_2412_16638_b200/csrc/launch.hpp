@@ -66,6 +66,10 @@ void cg_ctl_step(CgCtl* ctl, const RedSlot& upd, int rcomp, int rzcomp, const Re
 void cg_fused_update(const StencilSpec& s, float alpha, const RedSlot* alpha_src, const float* x, const float* p,
                      const float* b, const float* r, float* x1, const RedSlot& red, cudaStream_t st,
                      const double* gathered = nullptr, int ranks = 0, int* finite_flag = nullptr);
+// (fp64 stage solves: the same pass in double, the TMA ring at 2 CTAs / SM)
+void cg_fused_update(const StencilSpec& s, double alpha, const RedSlot* alpha_src, const double* x, const double* p,
+                     const double* b, const double* r, double* x1, const RedSlot& red, cudaStream_t st,
+                     const double* gathered = nullptr, int ranks = 0, int* finite_flag = nullptr);
 // out[c] = component c (< ncomp) of slot's device tuples summed in the host's
 // order (reduce.cuh sum_partials): a rank's local value of a reduction, on the device
 void tuple_sums(const RedSlot& slot, int ncomp, double* out, cudaStream_t st);

@@ -1206,18 +1206,33 @@ void feval_combine(const StencilSpec& k, const float* y32, const FevalCombine& f
 // recomputes whichever it needs on the rare path that continues.
 constexpr int CG_SLOT = tma_slot_elems<float>(), CG_TST = 4;  // 3 planes in use + 1 in flight: 44 KB, 5 CTAs/SM
 constexpr size_t cg_fused_smem() { return (size_t)CG_TST * 2 * CG_SLOT * sizeof(float) + CG_TST * sizeof(uint64_t) + 128; }
+template <class T>
+constexpr size_t cg_fused_smem_t() {
+  return (size_t)CG_TST * 2 * tma_slot_elems<T>() * sizeof(T) + CG_TST * sizeof(uint64_t) + 128;
+}
+// alpha = (R) r.z / (R) p.Ap from the fp64 sums, as the host forms it (krylov.cpp)
+template <class T>
+__device__ __forceinline__ T cg_alpha(double rz, double pq);
+template <>
+__device__ __forceinline__ float cg_alpha<float>(double rz, double pq) {
+  return __fdiv_rn(__double2float_rn(rz), __double2float_rn(pq));
+}
+template <>
+__device__ __forceinline__ double cg_alpha<double>(double rz, double pq) {
+  return __ddiv_rn(rz, pq);
+}
 
 // SELF (x0 = b, the stepper's case): b is x's own tile centre and r = b - A b
 // is re-formed from the resident x neighbourhood with the residual kernel's
 // arithmetic (EpiResidualSelf) — bitwise the stored r — so only x, p (TMA)
 // and x1 cross HBM: 3 s N instead of 5 s N.
-template <bool SELF>
+template <class T, bool SELF>
 __global__ void __launch_bounds__(TTHREADS)
     k_cg_fused(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap pmap,
                const __grid_constant__ CUtensorMap xlo, const __grid_constant__ CUtensorMap xhi,
                const __grid_constant__ CUtensorMap plo, const __grid_constant__ CUtensorMap phi, int has_lo,
-               int has_hi, int n, int nz, int kc, float s, float g, float alpha, const double* apart, int an,
-               const float* __restrict__ b, const float* __restrict__ r, float* __restrict__ x1, RedSlot red,
+               int has_hi, int n, int nz, int kc, T s, T g, T alpha, const double* apart, int an,
+               const T* __restrict__ b, const T* __restrict__ r, T* __restrict__ x1, RedSlot red,
                int* finite_flag) {
   pdl_wait();
   pdl_trigger();
@@ -1229,24 +1244,25 @@ __global__ void __launch_bounds__(TTHREADS)
       pq += apart[2 * rr];
       rz += apart[2 * rr + 1];
     }
-    alpha = __fdiv_rn(__double2float_rn(rz), __double2float_rn(pq));
+    alpha = cg_alpha<T>(rz, pq);
   } else if (apart) {
     // alpha = r.z / p.Ap from the previous pass's tuples, summed and rounded
     // as the host does (krylov.cpp: (R)rz / (R)pq), so no host round trip
     // sits between the two kernels
     const double2 tp = sum_partials2(apart, an);  // (p.Ap, r.z)
     const double pq = tp.x, rz = tp.y;
-    alpha = __fdiv_rn(__double2float_rn(rz), __double2float_rn(pq));
+    alpha = cg_alpha<T>(rz, pq);
   }
+  constexpr int SLOT = tma_slot_elems<T>();
   extern __shared__ unsigned char smem_raw[];
-  float* buf = reinterpret_cast<float*>(smem_align128(smem_raw));
-  uint64_t* full = reinterpret_cast<uint64_t*>(buf + CG_TST * 2 * CG_SLOT);
+  T* buf = reinterpret_cast<T*>(smem_align128(smem_raw));
+  uint64_t* full = reinterpret_cast<uint64_t*>(buf + CG_TST * 2 * SLOT);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int i0 = blockIdx.x * TI, j0 = blockIdx.y * TJ;
   int k0, k1;
   plane_range(nz, 0, nz, kc, k0, k1);
   const int planes = k1 - k0 + 2;
-  constexpr uint32_t bytes = (TJ + 2) * TW * sizeof(float);
+  constexpr uint32_t bytes = (TJ + 2) * TW * sizeof(T);
   if (tid == 0) {
     for (int q = 0; q < CG_TST; ++q) mbar_init(&full[q], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1260,31 +1276,36 @@ __global__ void __launch_bounds__(TTHREADS)
   const CUtensorMap* ph = &phi;
   auto issue = [&](int q) {  // (split grid: planes -1 / nz from the ghost planes)
     const int k = k0 - 1 + q, sl = q % CG_TST;
-    float* dst = buf + sl * 2 * CG_SLOT;
+    T* dst = buf + sl * 2 * SLOT;
     mbar_expect_tx(&full[sl], 2 * bytes);
     if (k < 0 && has_lo) {
       tma_2d(dst, xl, i0 - 4, j0 - 1, &full[sl]);
-      tma_2d(dst + CG_SLOT, pl, i0 - 4, j0 - 1, &full[sl]);
+      tma_2d(dst + SLOT, pl, i0 - 4, j0 - 1, &full[sl]);
     } else if (k >= nz && has_hi) {
       tma_2d(dst, xh, i0 - 4, j0 - 1, &full[sl]);
-      tma_2d(dst + CG_SLOT, ph, i0 - 4, j0 - 1, &full[sl]);
+      tma_2d(dst + SLOT, ph, i0 - 4, j0 - 1, &full[sl]);
     } else {
       tma_3d(dst, xm, i0 - 4, j0 - 1, k, &full[sl]);
-      tma_3d(dst + CG_SLOT, pm, i0 - 4, j0 - 1, k, &full[sl]);
+      tma_3d(dst + SLOT, pm, i0 - 4, j0 - 1, k, &full[sl]);
     }
   };
   if (tid == 0)
     for (int q = 0; q < CG_TST && q < planes; ++q) issue(q);
   auto wait = [&](int q) { mbar_wait(&full[q % CG_TST], (uint32_t)(q / CG_TST) & 1u); };
-  auto ld = [](const float* p) {
-    const float4 f = *reinterpret_cast<const float4*>(p);
-    V4<float> v;
-    v.x[0] = f.x; v.x[1] = f.y; v.x[2] = f.z; v.x[3] = f.w;
+  auto ld = [](const T* p) {
+    V4<T> v;
+    if constexpr (sizeof(T) == 4) {
+      const float4 f = *reinterpret_cast<const float4*>(p);
+      v.x[0] = f.x; v.x[1] = f.y; v.x[2] = f.z; v.x[3] = f.w;
+    } else {
+      const double2 a = reinterpret_cast<const double2*>(p)[0], c = reinterpret_cast<const double2*>(p)[1];
+      v.x[0] = a.x; v.x[1] = a.y; v.x[2] = c.x; v.x[3] = c.y;
+    }
     return v;
   };
-  auto upd = [&](float xv, float pv) { return xadd(xv, xscale(alpha, pv)); };  // k_cg_update's x
-  auto upd4 = [&](const V4<float>& xv, const V4<float>& pv) {
-    V4<float> o;
+  auto upd = [&](T xv, T pv) { return xadd(xv, xscale(alpha, pv)); };  // k_cg_update's x
+  auto upd4 = [&](const V4<T>& xv, const V4<T>& pv) {
+    V4<T> o;
 #pragma unroll
     for (int e = 0; e < 4; ++e) o.x[e] = upd(xv.x[e], pv.x[e]);
     return o;
@@ -1294,7 +1315,7 @@ __global__ void __launch_bounds__(TTHREADS)
   const long nn = n, n2 = nn * nn;
   const int col = 4 + 4 * lane;
   auto gidx = [&](int row, int k) { return (i0 + 4 * lane) + (long)(j0 + row) * nn + (long)k * n2; };
-  V4<float> pb[TROWS], pr[TROWS];
+  V4<T> pb[TROWS], pr[TROWS];
   if (!SELF) {
 #pragma unroll
     for (int rr = 0; rr < TROWS; ++rr) {
@@ -1305,7 +1326,7 @@ __global__ void __launch_bounds__(TTHREADS)
   // x1 at this warp's rows of planes k - 1 and k, carried across the march
   // (each x1 value is formed once per plane — the same operation on the same
   // operands as forming it per use, so bitwise unchanged)
-  V4<float> x1m[TROWS], x1c[TROWS];
+  V4<T> x1m[TROWS], x1c[TROWS];
   for (int k = k0; k < k1; ++k) {
     const int q = k - k0 + 1;
     if (k == k0) {
@@ -1314,21 +1335,21 @@ __global__ void __launch_bounds__(TTHREADS)
 #pragma unroll
       for (int rr = 0; rr < TROWS; ++rr) {
         const int o = (warp * TROWS + rr + 1) * TW + col;
-        x1m[rr] = upd4(ld(buf + o), ld(buf + CG_SLOT + o));
-        x1c[rr] = upd4(ld(buf + 2 * CG_SLOT + o), ld(buf + 3 * CG_SLOT + o));
+        x1m[rr] = upd4(ld(buf + o), ld(buf + SLOT + o));
+        x1c[rr] = upd4(ld(buf + 2 * SLOT + o), ld(buf + 3 * SLOT + o));
       }
     }
     wait(q + 1);
-    const float* xmn = buf + ((q - 1) % CG_TST) * 2 * CG_SLOT;
-    const float* xc = buf + (q % CG_TST) * 2 * CG_SLOT;
-    const float* xpl = buf + ((q + 1) % CG_TST) * 2 * CG_SLOT;
-    V4<float> x1n[TROWS];
+    const T* xmn = buf + ((q - 1) % CG_TST) * 2 * SLOT;
+    const T* xc = buf + (q % CG_TST) * 2 * SLOT;
+    const T* xpl = buf + ((q + 1) % CG_TST) * 2 * SLOT;
+    V4<T> x1n[TROWS];
 #pragma unroll
     for (int rr = 0; rr < TROWS; ++rr) {
       const int o = (warp * TROWS + rr + 1) * TW + col;
-      x1n[rr] = upd4(ld(xpl + o), ld(xpl + CG_SLOT + o));
+      x1n[rr] = upd4(ld(xpl + o), ld(xpl + SLOT + o));
     }
-    V4<float> nb[TROWS], nr[TROWS];
+    V4<T> nb[TROWS], nr[TROWS];
     if (!SELF) {
 #pragma unroll
       for (int rr = 0; rr < TROWS; ++rr)
@@ -1342,46 +1363,46 @@ __global__ void __launch_bounds__(TTHREADS)
       const int row = warp * TROWS + rr;
       const int o = (row + 1) * TW + col;
       // p neighbourhood -> q = A p
-      const V4<float> pc = ld(xc + CG_SLOT + o);
-      const V4<float> pym = ld(xc + CG_SLOT + o - TW), pyp = ld(xc + CG_SLOT + o + TW);
-      const V4<float> pzm = ld(xmn + CG_SLOT + o), pzp = ld(xpl + CG_SLOT + o);
-      float pl = shfl_up1(pc.x[3]), pr_ = shfl_down1(pc.x[0]);
-      const float pe = edge_ld(xc + CG_SLOT + o, lane), xe = edge_ld(xc + o, lane);
+      const V4<T> pc = ld(xc + SLOT + o);
+      const V4<T> pym = ld(xc + SLOT + o - TW), pyp = ld(xc + SLOT + o + TW);
+      const V4<T> pzm = ld(xmn + SLOT + o), pzp = ld(xpl + SLOT + o);
+      T pl = shfl_up1(pc.x[3]), pr_ = shfl_down1(pc.x[0]);
+      const T pe = edge_ld(xc + SLOT + o, lane), xe = edge_ld(xc + o, lane);
       pl = lane == 0 ? pe : pl;
       pr_ = lane == 31 ? pe : pr_;
       // x neighbourhood (SELF: b's, for r = b - A b) and x1's -> A x1
-      const V4<float> xcv = ld(xc + o), xym = ld(xc + o - TW), xyp = ld(xc + o + TW);
-      const V4<float> xzm = ld(xmn + o), xzp = ld(xpl + o);
+      const V4<T> xcv = ld(xc + o), xym = ld(xc + o - TW), xyp = ld(xc + o + TW);
+      const V4<T> xzm = ld(xmn + o), xzp = ld(xpl + o);
       if (SELF) {
-        float bl = shfl_up1(xcv.x[3]), br = shfl_down1(xcv.x[0]);
+        T bl = shfl_up1(xcv.x[3]), br = shfl_down1(xcv.x[0]);
         bl = lane == 0 ? xe : bl;
         br = lane == 31 ? xe : br;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float l = e == 0 ? bl : xcv.x[e - 1], rgt = e == 3 ? br : xcv.x[e + 1];
-          const float v = point<float>(0, s, g, 0.0f, xcv.x[e], l, rgt, xym.x[e], xyp.x[e], xzm.x[e], xzp.x[e]);
+          const T l = e == 0 ? bl : xcv.x[e - 1], rgt = e == 3 ? br : xcv.x[e + 1];
+          const T v = point<T>(0, s, g, T(0), xcv.x[e], l, rgt, xym.x[e], xyp.x[e], xzm.x[e], xzp.x[e]);
           pb[rr].x[e] = xcv.x[e];
           pr[rr].x[e] = xsub(xcv.x[e], v);  // EpiResidualSelf's r
         }
       }
-      const V4<float> c = x1c[rr];
-      const V4<float> ym = rr > 0 ? x1c[rr > 0 ? rr - 1 : 0] : upd4(xym, pym);
-      const V4<float> yp = rr + 1 < TROWS ? x1c[rr + 1 < TROWS ? rr + 1 : 0] : upd4(xyp, pyp);
-      const V4<float> zm = x1m[rr], zp = x1n[rr];
-      float xl = shfl_up1(c.x[3]), xr = shfl_down1(c.x[0]);
-      const float x1e = upd(xe, pe);  // (lane 0: x1 left of the warp; lane 31: right)
+      const V4<T> c = x1c[rr];
+      const V4<T> ym = rr > 0 ? x1c[rr > 0 ? rr - 1 : 0] : upd4(xym, pym);
+      const V4<T> yp = rr + 1 < TROWS ? x1c[rr + 1 < TROWS ? rr + 1 : 0] : upd4(xyp, pyp);
+      const V4<T> zm = x1m[rr], zp = x1n[rr];
+      T xl = shfl_up1(c.x[3]), xr = shfl_down1(c.x[0]);
+      const T x1e = upd(xe, pe);  // (lane 0: x1 left of the warp; lane 31: right)
       xl = lane == 0 ? x1e : xl;
       xr = lane == 31 ? x1e : xr;
       const long gi = gidx(row, k);
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const float ql = e == 0 ? pl : pc.x[e - 1], qr = e == 3 ? pr_ : pc.x[e + 1];
-        const float qv = point<float>(0, s, g, 0.0f, pc.x[e], ql, qr, pym.x[e], pyp.x[e], pzm.x[e], pzp.x[e]);
-        const float r1 = xsub(pr[rr].x[e], xscale(alpha, qv));  // k_cg_update's r
+        const T ql = e == 0 ? pl : pc.x[e - 1], qr = e == 3 ? pr_ : pc.x[e + 1];
+        const T qv = point<T>(0, s, g, T(0), pc.x[e], ql, qr, pym.x[e], pyp.x[e], pzm.x[e], pzp.x[e]);
+        const T r1 = xsub(pr[rr].x[e], xscale(alpha, qv));  // k_cg_update's r
         dot_acc(*reinterpret_cast<double(*)[1]>(&acc[0]), r1, r1);
-        const float al = e == 0 ? xl : c.x[e - 1], ar = e == 3 ? xr : c.x[e + 1];
-        const float av = point<float>(0, s, g, 0.0f, c.x[e], al, ar, ym.x[e], yp.x[e], zm.x[e], zp.x[e]);
-        const float t = xsub(pb[rr].x[e], av);  // EpiResidual's b - A x
+        const T al = e == 0 ? xl : c.x[e - 1], ar = e == 3 ? xr : c.x[e + 1];
+        const T av = point<T>(0, s, g, T(0), c.x[e], al, ar, ym.x[e], yp.x[e], zm.x[e], zp.x[e]);
+        const T t = xsub(pb[rr].x[e], av);  // EpiResidual's b - A x
         dot_acc(*reinterpret_cast<double(*)[1]>(&acc[1]), t, t);
         bad |= !isfinite(c.x[e]);
       }
@@ -1413,20 +1434,22 @@ bool cg_fused_supported(const StencilSpec& k) {  // (k_cg_fused: ghost planes on
 static bool pq_fused_supported(const StencilSpec& k) { return cg_fused_supported(k) && k.halo == nullptr; }
 bool pq_fused_ok(const StencilSpec& k) { return pq_fused_supported(k); }
 
-void cg_fused_update(const StencilSpec& sp, float alpha, const RedSlot* alpha_src, const float* x, const float* p,
-                     const float* b, const float* r, float* x1, const RedSlot& red, cudaStream_t st,
-                     const double* gathered, int ranks, int* finite_flag) {
+template <class T>
+static void cg_fused_update_t(const StencilSpec& sp, T alpha, const RedSlot* alpha_src, const T* x, const T* p,
+                              const T* b, const T* r, T* x1, const RedSlot& red, cudaStream_t st,
+                              const double* gathered, int ranks, int* finite_flag) {
   if (!cg_fused_supported(sp)) MPRKB_THROW(10, "cg_fused_update: needs the TMA stencil (Dirichlet, n % 128 == 0)");
   const int n = sp.n, nz = sp.nz > 0 ? sp.nz : n;
-  constexpr size_t smem = cg_fused_smem();
+  constexpr size_t smem = cg_fused_smem_t<T>();
+  const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
   static thread_local int chunk = 0;  // (per host thread: in-process ranks launch concurrently)
   static thread_local long chunk_cols = -1;
   static thread_local int resident = 0;
   if (!resident) {
-    CUDA_CHECK(cudaFuncSetAttribute(k_cg_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CUDA_CHECK(cudaFuncSetAttribute(k_cg_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_CHECK(cudaFuncSetAttribute(k_cg_fused<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CUDA_CHECK(cudaFuncSetAttribute(k_cg_fused<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_fused<false>, TTHREADS, smem));
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cg_fused<T, false>, TTHREADS, smem));
     resident = std::max(1, per_sm) * sm_count();
   }
   const long cols = (long)(n / TI) * (n / TJ);
@@ -1443,37 +1466,37 @@ void cg_fused_update(const StencilSpec& sp, float alpha, const RedSlot* alpha_sr
     chunk_cols = cols;
   }
   const cuuint64_t nn = (cuuint64_t)n;
-  const cuuint64_t dims3[3] = {nn, nn, (cuuint64_t)nz}, str3[2] = {nn * 4, nn * nn * 4};
+  const cuuint64_t dims3[3] = {nn, nn, (cuuint64_t)nz}, str3[2] = {nn * sizeof(T), nn * nn * sizeof(T)};
   const cuuint32_t box3[3] = {(cuuint32_t)TW, (cuuint32_t)(TJ + 2), 1};
-  const CUtensorMap xmap = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, x, 3, dims3, str3, box3);
-  const CUtensorMap pmap = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, p, 3, dims3, str3, box3);
+  const CUtensorMap xmap = make_map(dt, x, 3, dims3, str3, box3);
+  const CUtensorMap pmap = make_map(dt, p, 3, dims3, str3, box3);
   // split grid: both operands' boundary planes from the k-neighbours (x and p
   // ghosts side by side in the halo buffer), before the pass
   CUtensorMap gm[4] = {xmap, xmap, xmap, xmap};  // x lo, x hi, p lo, p hi
   int has_lo = 0, has_hi = 0;
   if (sp.halo) {
     const Halo& h = *sp.halo;
-    const size_t plane = (size_t)n * n * sizeof(float);
+    const size_t plane = (size_t)n * n * sizeof(T);
     if (h.ghost.bytes() < 4 * plane) MPRKB_THROW(10, "cg_fused_update: ghost buffer too small");
     CUDA_CHECK(cudaEventRecord(h.ready, st));
     CUDA_CHECK(cudaStreamWaitEvent(h.cs, h.ready, 0));
     const void* gx[2];
     const void* gp[2];
-    halo_exchange(h, x, sizeof(float), false, h.cs, gx, 0);
-    halo_exchange(h, p, sizeof(float), false, h.cs, gp, 2 * plane);
+    halo_exchange(h, x, sizeof(T), false, h.cs, gx, 0);
+    halo_exchange(h, p, sizeof(T), false, h.cs, gp, 2 * plane);
     CUDA_CHECK(cudaEventRecord(h.arrived, h.cs));
     CUDA_CHECK(cudaStreamWaitEvent(st, h.arrived, 0));
-    const cuuint64_t dims2[2] = {nn, nn}, str2[1] = {nn * 4};
+    const cuuint64_t dims2[2] = {nn, nn}, str2[1] = {nn * sizeof(T)};
     const cuuint32_t box2[2] = {(cuuint32_t)TW, (cuuint32_t)(TJ + 2)};
     has_lo = gx[0] != nullptr;
     has_hi = gx[1] != nullptr;
     if (has_lo) {
-      gm[0] = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, gx[0], 2, dims2, str2, box2);
-      gm[2] = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, gp[0], 2, dims2, str2, box2);
+      gm[0] = make_map(dt, gx[0], 2, dims2, str2, box2);
+      gm[2] = make_map(dt, gp[0], 2, dims2, str2, box2);
     }
     if (has_hi) {
-      gm[1] = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, gx[1], 2, dims2, str2, box2);
-      gm[3] = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT32, gp[1], 2, dims2, str2, box2);
+      gm[1] = make_map(dt, gx[1], 2, dims2, str2, box2);
+      gm[3] = make_map(dt, gp[1], 2, dims2, str2, box2);
     }
   }
   const unsigned gz = (unsigned)((nz + chunk - 1) / chunk);
@@ -1485,11 +1508,22 @@ void cg_fused_update(const StencilSpec& sp, float alpha, const RedSlot* alpha_sr
   const int an = gathered ? -ranks : alpha_src ? *alpha_src->count : 0;
   if (!gathered && alpha_src && (!apart || an <= 0)) MPRKB_THROW(10, "cg_fused_update: alpha source has no device tuples");
   // x0 = b (x aliases b): the SELF pass re-forms b and r from x's tile
-  launch_pdl(x == b ? k_cg_fused<true> : k_cg_fused<false>, grid, dim3(TTHREADS), smem, st, xmap, pmap, gm[0], gm[1], gm[2], gm[3], has_lo, has_hi, n,
-             nz, chunk, (float)sp.sigma, (float)sp.gamma, alpha, apart, an, b, r, x1, rs, finite_flag);
+  launch_pdl(x == b ? k_cg_fused<T, true> : k_cg_fused<T, false>, grid, dim3(TTHREADS), smem, st, xmap, pmap, gm[0], gm[1], gm[2], gm[3], has_lo, has_hi, n,
+             nz, chunk, (T)sp.sigma, (T)sp.gamma, alpha, apart, an, b, r, x1, rs, finite_flag);
   note_partials(rs, grid.x * grid.y * grid.z);
   note_kron(true, 2);  // A p and the true residual's A x1
   LAUNCHED("cg_fused_update");
+}
+
+void cg_fused_update(const StencilSpec& sp, float alpha, const RedSlot* alpha_src, const float* x, const float* p,
+                     const float* b, const float* r, float* x1, const RedSlot& red, cudaStream_t st,
+                     const double* gathered, int ranks, int* finite_flag) {
+  cg_fused_update_t<float>(sp, alpha, alpha_src, x, p, b, r, x1, red, st, gathered, ranks, finite_flag);
+}
+void cg_fused_update(const StencilSpec& sp, double alpha, const RedSlot* alpha_src, const double* x, const double* p,
+                     const double* b, const double* r, double* x1, const RedSlot& red, cudaStream_t st,
+                     const double* gathered, int ranks, int* finite_flag) {
+  cg_fused_update_t<double>(sp, alpha, alpha_src, x, p, b, r, x1, red, st, gathered, ranks, finite_flag);
 }
 
 // ---- speculative stage solve's update fused with the stage's f evaluations -------

@@ -309,11 +309,13 @@ void Stepper::step(double* u, StepTrace& trace) {
       {
         // x0 = narrowed rhs (stepper.cpp:111, 120, 135, 146), written by the same pass
         Bracket br(timer_, "axpy", st_);
-        combine(m, u, terms, out_kind, bsol_.get(), flag, st_, solve_dtype_ == 0 ? nullptr : xsol_.get());
+        // (heat stages solve from x0 = rhs in place: no second copy is written)
+        combine(m, u, terms, out_kind, bsol_.get(), flag, st_, solve_dtype_ <= 1 ? nullptr : xsol_.get());
       }
       SolveReport rep;
       EventTimer* tm = timer_.enabled() ? &timer_ : nullptr;
       float* sol32 = xsol_.as<float>();
+      double* sol64 = xsol_.as<double>();
       switch (solve_dtype_) {
         case 0:
           if (acc_work_) {  // accessor-style CG vectors: x0 = rhs copied into the solution buffer
@@ -327,12 +329,16 @@ void Stepper::step(double* u, StepTrace& trace) {
                           tm, xsol_.as<float>(), &sol32);
           break;
         case 1:
-          if (acc_work_)
+          if (acc_work_) {
+            CUDA_CHECK(cudaMemcpyAsync(xsol_.get(), bsol_.get(), m * sizeof(double), cudaMemcpyDeviceToDevice, st_));
             cg_solve_acc<double>(*S.op->stencil(), S.pre.get(), bsol_.as<double>(), xsol_.as<double>(), crit,
                                  *acc_work_, rep, st_, tm);
-          else
-            cg_solve<double>(*S.op, S.pre.get(), bsol_.as<double>(), xsol_.as<double>(), crit, cfg_.num, *w64_, rep,
-                             st_, tm);
+          } else {
+            // x0 = rhs in place, as the fp32 stages: the solution lands in xsol_
+            // (or stays in bsol_ when x0 already satisfies the criterion)
+            cg_solve<double>(*S.op, S.pre.get(), bsol_.as<double>(), bsol_.as<double>(), crit, cfg_.num, *w64_, rep,
+                             st_, tm, xsol_.as<double>(), &sol64);
+          }
           break;
         case 2:
           gmres_solve<c32>(*S.op, S.pre.get(), bsol_.as<c32>(), xsol_.as<c32>(), crit, cfg_.num, *wc32_, rep, st_, tm, cfg_.basis_storage);
@@ -348,7 +354,7 @@ void Stepper::step(double* u, StepTrace& trace) {
       if (solve_dtype_ == 0) {
         ys32 = sol32;
       } else if (solve_dtype_ == 1) {
-        ys = xsol_.as<double>();
+        ys = sol64;
       } else {
         extract_stage(m, solve_dtype_, xsol_.get(), y_.as<double>(), check_slot(9, kStage), st_);
         stage_checked = true;

@@ -358,6 +358,43 @@ def test_cg_fused_first_update(gpu, mp, tol):
     assert same_bits(a, b)
 
 
+@pytest.mark.parametrize("tol", [1e-5, 1e-15])
+def test_cg_fused_first_update_f64(gpu, mp, tol):
+    """fp64 stage solves run the same fused first update (k_cg_fused<double>:
+    x1 = b + alpha z, ||r1|| and the true residual in one TMA pass, alpha
+    formed on the device from the first-iteration tuples) from x0 = rhs in
+    place: stepped states bitwise the unfused kernels' (MPRKB_CG_FUSED=0),
+    iteration counts equal, histories equal up to the fp64 reduction order of
+    the fused norms.  tol 1e-15 is below fp64 reach: every solve continues
+    past the first iteration through the r1-recompute path."""
+    import os
+
+    t = mp.builtin("4s3pB")
+    n = 256 if tol > 1e-10 else 128
+    fused = mp.Stepper("heat", n, t, 0.01, tol, "f64", 12)
+    os.environ["MPRKB_CG_FUSED"] = "0"
+    try:
+        plain = mp.Stepper("heat", n, t, 0.01, tol, "f64", 12)
+        a, b = np.zeros(n ** 3), np.zeros(n ** 3)
+        for _ in range(2):
+            del os.environ["MPRKB_CG_FUSED"]
+            ta = fused.step(a)
+            os.environ["MPRKB_CG_FUSED"] = "0"
+            tb = plain.step(b)
+            assert ta["iterations"] == tb["iterations"]
+            if tol > 1e-10:
+                assert all(i == 1 for i in ta["iterations"])
+            else:
+                assert min(ta["iterations"]) > 1
+            for s in range(len(ta["iterations"])):
+                ha, hb = fused.history(s), plain.history(s)
+                assert len(ha) == len(hb)
+                np.testing.assert_allclose(ha, hb, rtol=1e-9)
+    finally:
+        os.environ.pop("MPRKB_CG_FUSED", None)
+    assert same_bits(a, b)
+
+
 @pytest.mark.parametrize("name,prec,fused", [("4s3pB", "f32", True), ("4s3pA", "f32", False), ("4s3pB", "f64", False)])
 def test_regenerated_forcing_bitwise(gpu, mp, name, prec, fused):
     """Heat steppers regenerate the forcing g = (s_i s_j) s_k from its sine
