@@ -45,6 +45,10 @@ bool tma_stencil_enabled() {
   }();
   return on;
 }
+static bool tma_periodic_enabled() {  // (read per call: tests compare both paths in one process)
+  const char* e = std::getenv("MPRKB_STENCIL_TMA_PERIODIC");
+  return !(e && e[0] == '0');
+}
 
 __device__ __forceinline__ bool f32_overflows(double x) {
   return !isnan(x) && fabs(x) >= 3.402823669209384634633746074317e+38;
@@ -771,7 +775,8 @@ template <class Src, class Epi>
 __global__ void __launch_bounds__(TTHREADS, tma_min_blocks<Epi>())
     k_stencil_tma(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap lomap,
                   const __grid_constant__ CUtensorMap himap, int has_lo, int has_hi, int n, int nz, int kb, int ke,
-                  int kc, typename Src::type s, typename Src::type g, Src src, Epi epi) {
+                  int kc, real_t<typename Src::type> s, real_t<typename Src::type> g, real_t<typename Src::type> g2,
+                  int stencil, Src src, Epi epi) {
   pdl_wait();
   pdl_trigger();
   using T = typename Src::type;
@@ -797,8 +802,15 @@ __global__ void __launch_bounds__(TTHREADS, tma_min_blocks<Epi>())
   const CUtensorMap* xm = &xmap;
   const CUtensorMap* lm = &lomap;
   const CUtensorMap* hm = &himap;
+  // periodic (stencil 1 / 2, undivided grid): planes -1 / nz wrap around;
+  // the wrapped j rows and i columns of the boundary tiles are read from
+  // global memory a plane ahead (the TMA box zero-fills them)
+  const bool periodic = stencil != 0;
   auto issue = [&](int q) {  // plane k0 - 1 + q into ring slot q % TST
-    const int k = k0 - 1 + q, b = q % TST;
+    int k = k0 - 1 + q;
+    const int b = q % TST;
+    if (periodic && !has_lo && k < 0) k += nz;
+    if (periodic && !has_hi && k >= nz) k -= nz;
     Raw* dst = buf + b * PLANE;
     mbar_expect_tx(&full[b], bytes);
     if (k < 0 && has_lo)
@@ -816,9 +828,18 @@ __global__ void __launch_bounds__(TTHREADS, tma_min_blocks<Epi>())
     if constexpr (sizeof(Raw) == 4) {
       const float4 f = *reinterpret_cast<const float4*>(p);
       v.x[0] = src.cv(f.x); v.x[1] = src.cv(f.y); v.x[2] = src.cv(f.z); v.x[3] = src.cv(f.w);
-    } else {
+    } else if constexpr (std::is_same_v<Raw, double>) {
       const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
       v.x[0] = src.cv(a.x); v.x[1] = src.cv(a.y); v.x[2] = src.cv(b.x); v.x[3] = src.cv(b.y);
+    } else {  // 8-byte complex: two 16-byte words
+      static_assert(sizeof(Raw) == 8, "TMA stencil rows hold 4- or 8-byte elements");
+      union {
+        uint4 w[2];
+        Raw e[4];
+      } u;
+      u.w[0] = reinterpret_cast<const uint4*>(p)[0];
+      u.w[1] = reinterpret_cast<const uint4*>(p)[1];
+      v.x[0] = src.cv(u.e[0]); v.x[1] = src.cv(u.e[1]); v.x[2] = src.cv(u.e[2]); v.x[3] = src.cv(u.e[3]);
     }
     return v;
   };
@@ -830,8 +851,37 @@ __global__ void __launch_bounds__(TTHREADS, tma_min_blocks<Epi>())
   typename Epi::Pre pre[TROWS];
 #pragma unroll
   for (int rr = 0; rr < TROWS; ++rr) pre[rr] = epi.pre4(gidx(warp * TROWS + rr, k0));
+  // periodic boundary tiles: the wrapped row below j0 (warp 0's first row),
+  // above j0 + TJ - 1 (the last warp's last row) and the wrapped column
+  // left of i0 (lane 0) / right of i0 + TI - 1 (lane 31), for plane k
+  const bool wrap_lo = periodic && j0 == 0 && warp == 0;
+  const bool wrap_hi = periodic && j0 + TJ == n && warp == TTHREADS / 32 - 1;
+  const bool wrap_l = periodic && i0 == 0 && lane == 0;
+  const bool wrap_r = periodic && i0 + TI == n && lane == 31;
+  auto wrow = [&](int jj, int k) { return src.ld4((i0 + 4 * lane) + (long)jj * nn + (long)k * n2); };
+  auto wcol = [&](int ii, int r, int k) { return src.ld1(ii + (long)(j0 + r) * nn + (long)k * n2); };
+  V4<T> wy{}, wyn{};
+  T we[TROWS], wen[TROWS];
+  if (wrap_lo) wy = wrow(n - 1, k0);
+  if (wrap_hi) wy = wrow(0, k0);
+#pragma unroll
+  for (int rr = 0; rr < TROWS; ++rr) {
+    we[rr] = T{};
+    wen[rr] = T{};
+    if (wrap_l) we[rr] = wcol(n - 1, warp * TROWS + rr, k0);
+    if (wrap_r) we[rr] = wcol(0, warp * TROWS + rr, k0);
+  }
   for (int k = k0; k < k1; ++k) {
     const int q = k - k0 + 1;
+    if (k + 1 < k1) {
+      if (wrap_lo) wyn = wrow(n - 1, k + 1);
+      if (wrap_hi) wyn = wrow(0, k + 1);
+#pragma unroll
+      for (int rr = 0; rr < TROWS; ++rr) {
+        if (wrap_l) wen[rr] = wcol(n - 1, warp * TROWS + rr, k + 1);
+        if (wrap_r) wen[rr] = wcol(0, warp * TROWS + rr, k + 1);
+      }
+    }
     if (k == k0) {
       wait(0);
       wait(1);
@@ -849,7 +899,7 @@ __global__ void __launch_bounds__(TTHREADS, tma_min_blocks<Epi>())
       const int r = warp * TROWS + rr;  // tile row
       const int o = (r + 1) * TW + col;
       const V4<T> c = ld(pc + o);
-      const V4<T> ym = ld(pc + o - TW), yp = ld(pc + o + TW);
+      V4<T> ym = ld(pc + o - TW), yp = ld(pc + o + TW);
       const V4<T> zm = ld(pm + o), zp = ld(pp + o);
       T left = shfl_up1(c.x[3]);
       T right = shfl_down1(c.x[0]);
@@ -862,12 +912,18 @@ __global__ void __launch_bounds__(TTHREADS, tma_min_blocks<Epi>())
         if (lane == 0) left = src.cv(pc[o - 1]);
         if (lane == 31) right = src.cv(pc[o + 4]);
       }
+      if (periodic) {
+        if (wrap_lo && rr == 0) ym = wy;
+        if (wrap_hi && rr == TROWS - 1) yp = wy;
+        if (wrap_l) left = we[rr];
+        if (wrap_r) right = we[rr];
+      }
       V4<T> v;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const T xl = e == 0 ? left : c.x[e - 1];
         const T xr = e == 3 ? right : c.x[e + 1];
-        v.x[e] = point<T>(0, s, g, T(0), c.x[e], xl, xr, ym.x[e], yp.x[e], zm.x[e], zp.x[e]);
+        v.x[e] = point<T>(stencil, s, g, g2, c.x[e], xl, xr, ym.x[e], yp.x[e], zm.x[e], zp.x[e]);
       }
       if constexpr (is_dual<Epi>::value) {
         // the same neighbourhood in binary32 arithmetic (apply_f's F32 policy)
@@ -895,6 +951,11 @@ __global__ void __launch_bounds__(TTHREADS, tma_min_blocks<Epi>())
     }
 #pragma unroll
     for (int rr = 0; rr < TROWS; ++rr) pre[rr] = nxt[rr];
+    if (periodic) {
+      wy = wyn;
+#pragma unroll
+      for (int rr = 0; rr < TROWS; ++rr) we[rr] = wen[rr];
+    }
     // ring slot of plane q - 1 is free: order this thread's generic reads of it
     // before the async-proxy (TMA) refill, then let thread 0 issue it
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -956,8 +1017,9 @@ void launch_tma(const StencilSpec& sp, const Src& src, const Epi& epi, int kb, i
   const CUtensorMap lomap = src.glo ? make_map(dt, src.glo, 2, dims2, str2, box2) : xmap;
   const CUtensorMap himap = src.ghi ? make_map(dt, src.ghi, 2, dims2, str2, box2) : xmap;
   const dim3 grid((unsigned)(n / TI), (unsigned)(n / TJ), gz);
+  using R = real_t<T>;
   launch_pdl(k_stencil_tma<Src, Epi>, grid, dim3(TTHREADS), smem, st, xmap, lomap, himap, src.glo ? 1 : 0,
-             src.ghi ? 1 : 0, n, nz, kb, ke, kc, (T)sp.sigma, (T)sp.gamma, src, epi);
+             src.ghi ? 1 : 0, n, nz, kb, ke, kc, (R)sp.sigma, (R)sp.gamma, (R)sp.gamma2, sp.stencil, src, epi);
   LAUNCHED(name);
 }
 
@@ -988,11 +1050,16 @@ void launch(const StencilSpec& sp, Src src, Epi epi, cudaStream_t st, const char
   const int n = sp.n;
   const int nz = sp.nz > 0 ? sp.nz : n;
   const bool vec = n % 4 == 0;  // (complex too: 4 points per lane, shuffles per component)
-  // the TMA plane pipeline covers the bench path: Dirichlet heat, real T, n % 128 == 0
-  const bool tma = !is_cplx<T> && sp.stencil == 0 && n % TI == 0 && tma_stencil_enabled();
+  // the TMA plane pipeline: n % 128 == 0, Dirichlet (real) or — on an
+  // undivided grid — periodic (real and complex<float>: config 4's
+  // advection-diffusion stages; MPRKB_STENCIL_TMA_PERIODIC=0 keeps those on
+  // the register-marching kernel)
+  const bool tma_periodic = sp.stencil != 0 && !sp.halo && sizeof(typename Src::raw) <= 8 && tma_periodic_enabled();
+  const bool tma = (is_cplx<T> ? tma_periodic : (sp.stencil == 0 || tma_periodic)) && n % TI == 0 &&
+                   tma_stencil_enabled();
   const dim3 block = vec ? dim3(VX, VY) : dim3(SBX, SBY);
   int chunk = vec ? VKC : SKC;
-  if constexpr (!is_cplx<T>) {
+  if constexpr (sizeof(typename Src::raw) <= 8) {
     if (tma) {
       tma_configure<Src, Epi>();
       chunk = tma_chunk<Src, Epi>((long)(n / TI) * (n / TJ), sp.halo && nz > 2 ? nz - 2 : nz);
@@ -1001,7 +1068,7 @@ void launch(const StencilSpec& sp, Src src, Epi epi, cudaStream_t st, const char
   const unsigned gx = tma ? n / TI : vec ? (n / 4 + VX - 1) / VX : (n + SBX - 1) / SBX;
   const unsigned gy = tma ? n / TJ : vec ? (n + VY - 1) / VY : (n + SBY - 1) / SBY;
   auto go = [&](int kb, int ke, unsigned gz, const Epi& e) {
-    if constexpr (!is_cplx<T>) {
+    if constexpr (sizeof(typename Src::raw) <= 8) {
       if (tma) {
         launch_tma(sp, src, e, kb, ke, chunk, gz, st, name);
         return;

@@ -55,6 +55,44 @@ def test_stencil_bitwise(gpu, mp, ref, kind, stencil, n):
 
 
 @pytest.mark.parametrize("kind", [0, 1, 2, 3])
+@pytest.mark.parametrize("stencil", [0, 1])
+def test_stencil_tma_sizes_bitwise(gpu, mp, ref, kind, stencil):
+    """n % 128 == 0: the TMA plane pipeline (Dirichlet, and — periodic —
+    with wrapped planes, rows and columns read a plane ahead; complex<float>
+    rows as 8-byte elements) is bitwise the reference's apply<T>."""
+    import torch
+
+    n = 128
+    rng = np.random.default_rng(77 + kind + 5 * stencil)
+    x = rnd(rng, kind, n ** 3)
+    for sigma, gamma in ((1.0, -0.37), (0.5, 12.5)):
+        want = ref.stencil(kind, n, stencil, sigma, gamma, x)
+        got = mp.stencil_apply(to_dev(torch, x), n, stencil, sigma, gamma).cpu().numpy()
+        assert same_bits(got, want), (kind, stencil, sigma, np.abs(got - want).max())
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2])
+def test_stencil_tma_periodic_matches_register_kernel(gpu, mp, kind):
+    """Periodic stencils (incl. the advection-diffusion kind 2, which has no
+    reference counterpart) on the TMA path equal the register-marching
+    kernel bit for bit (MPRKB_STENCIL_TMA_PERIODIC=0), at 256^3."""
+    import os
+
+    import torch
+
+    n = 256
+    A = mp.Operator.stage_operator(kind, "advection", n, 0.01, 0.5, 0.01)
+    x = to_dev(torch, rnd(np.random.default_rng(5 + kind), kind, n ** 3))
+    got = A.apply(x).cpu().numpy()
+    os.environ["MPRKB_STENCIL_TMA_PERIODIC"] = "0"
+    try:
+        want = A.apply(x).cpu().numpy()
+    finally:
+        os.environ.pop("MPRKB_STENCIL_TMA_PERIODIC", None)
+    assert same_bits(got, want)
+
+
+@pytest.mark.parametrize("kind", [0, 1, 2, 3])
 @pytest.mark.parametrize("side", [0, 1, 2])
 @pytest.mark.parametrize("n", [2, 3, 7, 33, 64, 130])
 def test_tensor_parity_and_fast(gpu, mp, ref, kind, side, n):
