@@ -771,7 +771,9 @@ constexpr int tma_min_blocks() {
   return 1;
 }
 
-template <class Src, class Epi>
+// PER: the periodic variant (a template parameter, so the Dirichlet
+// instantiations carry none of the wrap logic)
+template <class Src, class Epi, bool PER>
 __global__ void __launch_bounds__(TTHREADS, tma_min_blocks<Epi>())
     k_stencil_tma(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap lomap,
                   const __grid_constant__ CUtensorMap himap, int has_lo, int has_hi, int n, int nz, int kb, int ke,
@@ -805,7 +807,7 @@ __global__ void __launch_bounds__(TTHREADS, tma_min_blocks<Epi>())
   // periodic (stencil 1 / 2, undivided grid): planes -1 / nz wrap around;
   // the wrapped j rows and i columns of the boundary tiles are read from
   // global memory a plane ahead (the TMA box zero-fills them)
-  const bool periodic = stencil != 0;
+  constexpr bool periodic = PER;
   auto issue = [&](int q) {  // plane k0 - 1 + q into ring slot q % TST
     int k = k0 - 1 + q;
     const int b = q % TST;
@@ -873,7 +875,7 @@ __global__ void __launch_bounds__(TTHREADS, tma_min_blocks<Epi>())
   }
   for (int k = k0; k < k1; ++k) {
     const int q = k - k0 + 1;
-    if (k + 1 < k1) {
+    if (periodic && k + 1 < k1) {
       if (wrap_lo) wyn = wrow(n - 1, k + 1);
       if (wrap_hi) wyn = wrow(0, k + 1);
 #pragma unroll
@@ -912,7 +914,7 @@ __global__ void __launch_bounds__(TTHREADS, tma_min_blocks<Epi>())
         if (lane == 0) left = src.cv(pc[o - 1]);
         if (lane == 31) right = src.cv(pc[o + 4]);
       }
-      if (periodic) {
+      if constexpr (periodic) {
         if (wrap_lo && rr == 0) ym = wy;
         if (wrap_hi && rr == TROWS - 1) yp = wy;
         if (wrap_l) left = we[rr];
@@ -923,7 +925,8 @@ __global__ void __launch_bounds__(TTHREADS, tma_min_blocks<Epi>())
       for (int e = 0; e < 4; ++e) {
         const T xl = e == 0 ? left : c.x[e - 1];
         const T xr = e == 3 ? right : c.x[e + 1];
-        v.x[e] = point<T>(stencil, s, g, g2, c.x[e], xl, xr, ym.x[e], yp.x[e], zm.x[e], zp.x[e]);
+        v.x[e] = point<T>(PER ? stencil : 0, s, g, PER ? g2 : real_t<T>(0), c.x[e], xl, xr, ym.x[e], yp.x[e], zm.x[e],
+                          zp.x[e]);
       }
       if constexpr (is_dual<Epi>::value) {
         // the same neighbourhood in binary32 arithmetic (apply_f's F32 policy)
@@ -951,7 +954,7 @@ __global__ void __launch_bounds__(TTHREADS, tma_min_blocks<Epi>())
     }
 #pragma unroll
     for (int rr = 0; rr < TROWS; ++rr) pre[rr] = nxt[rr];
-    if (periodic) {
+    if constexpr (periodic) {
       wy = wyn;
 #pragma unroll
       for (int rr = 0; rr < TROWS; ++rr) we[rr] = wen[rr];
@@ -967,12 +970,12 @@ __global__ void __launch_bounds__(TTHREADS, tma_min_blocks<Epi>())
 
 // k-chunk for `planes` planes over `cols` tile columns: the smallest
 // (waves x planes per CTA incl. the 2-plane halo) for the resident capacity
-template <class Src, class Epi>
+template <class Src, class Epi, bool PER>
 int tma_chunk(long cols, int planes) {
   static thread_local int resident = 0;
   if (!resident) {
     int per_sm = 0;
-    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stencil_tma<Src, Epi>, TTHREADS,
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_stencil_tma<Src, Epi, PER>, TTHREADS,
                                                              tma_stencil_smem<typename Src::raw>()));
     resident = std::max(1, per_sm) * sm_count();
   }
@@ -989,24 +992,24 @@ int tma_chunk(long cols, int planes) {
   return best;
 }
 
-template <class Src, class Epi>
+template <class Src, class Epi, bool PER>
 void tma_configure() {
   static thread_local bool configured = false;
   if (!configured) {
-    CUDA_CHECK(cudaFuncSetAttribute(k_stencil_tma<Src, Epi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CUDA_CHECK(cudaFuncSetAttribute(k_stencil_tma<Src, Epi, PER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)tma_stencil_smem<typename Src::raw>()));
     configured = true;
   }
 }
 
-template <class Src, class Epi>
+template <class Src, class Epi, bool PER>
 void launch_tma(const StencilSpec& sp, const Src& src, const Epi& epi, int kb, int ke, int kc, unsigned gz,
                 cudaStream_t st, const char* name) {
   using T = typename Src::type;
   using Raw = typename Src::raw;
   const int n = sp.n, nz = sp.nz > 0 ? sp.nz : n;
   constexpr size_t smem = tma_stencil_smem<Raw>();
-  tma_configure<Src, Epi>();
+  tma_configure<Src, Epi, PER>();
   const CUtensorMapDataType dt = sizeof(Raw) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
   const cuuint64_t nn = (cuuint64_t)n;
   const cuuint64_t dims3[3] = {nn, nn, (cuuint64_t)nz}, str3[2] = {nn * sizeof(Raw), nn * nn * sizeof(Raw)};
@@ -1018,7 +1021,7 @@ void launch_tma(const StencilSpec& sp, const Src& src, const Epi& epi, int kb, i
   const CUtensorMap himap = src.ghi ? make_map(dt, src.ghi, 2, dims2, str2, box2) : xmap;
   const dim3 grid((unsigned)(n / TI), (unsigned)(n / TJ), gz);
   using R = real_t<T>;
-  launch_pdl(k_stencil_tma<Src, Epi>, grid, dim3(TTHREADS), smem, st, xmap, lomap, himap, src.glo ? 1 : 0,
+  launch_pdl(k_stencil_tma<Src, Epi, PER>, grid, dim3(TTHREADS), smem, st, xmap, lomap, himap, src.glo ? 1 : 0,
              src.ghi ? 1 : 0, n, nz, kb, ke, kc, (R)sp.sigma, (R)sp.gamma, (R)sp.gamma2, sp.stencil, src, epi);
   LAUNCHED(name);
 }
@@ -1061,8 +1064,15 @@ void launch(const StencilSpec& sp, Src src, Epi epi, cudaStream_t st, const char
   int chunk = vec ? VKC : SKC;
   if constexpr (sizeof(typename Src::raw) <= 8) {
     if (tma) {
-      tma_configure<Src, Epi>();
-      chunk = tma_chunk<Src, Epi>((long)(n / TI) * (n / TJ), sp.halo && nz > 2 ? nz - 2 : nz);
+      const long cols = (long)(n / TI) * (n / TJ);
+      const int planes = sp.halo && nz > 2 ? nz - 2 : nz;
+      if (sp.stencil != 0) {
+        tma_configure<Src, Epi, true>();
+        chunk = tma_chunk<Src, Epi, true>(cols, planes);
+      } else {
+        tma_configure<Src, Epi, false>();
+        chunk = tma_chunk<Src, Epi, false>(cols, planes);
+      }
     }
   }
   const unsigned gx = tma ? n / TI : vec ? (n / 4 + VX - 1) / VX : (n + SBX - 1) / SBX;
@@ -1070,7 +1080,10 @@ void launch(const StencilSpec& sp, Src src, Epi epi, cudaStream_t st, const char
   auto go = [&](int kb, int ke, unsigned gz, const Epi& e) {
     if constexpr (sizeof(typename Src::raw) <= 8) {
       if (tma) {
-        launch_tma(sp, src, e, kb, ke, chunk, gz, st, name);
+        if (sp.stencil != 0)
+          launch_tma<Src, Epi, true>(sp, src, e, kb, ke, chunk, gz, st, name);
+        else
+          launch_tma<Src, Epi, false>(sp, src, e, kb, ke, chunk, gz, st, name);
         return;
       }
     }
