@@ -741,6 +741,38 @@ __global__ void __launch_bounds__(256) k_vaxmy16_hp(size_t m, const T* hp, const
   pdl_trigger();
   vaxmy16_body(m, *hp, v, w);
 }
+// One modified Gram-Schmidt step fused with the next one's dot:
+// w -= (*hp) v16_j, then conj(v16_next) . w over the updated w — the same
+// element operations as k_vaxmy16_hp followed by k_dot16, and the dot on
+// k_dot16's grid and traversal, so the partials (and h_{j+1}) are bitwise
+// the two-kernel sweep's; one pass over w instead of two.
+template <class T>
+__global__ void __launch_bounds__(256) k_vaxmy_dot16(size_t m, const T* hp, const typename Store16<T>::type* v,
+                                                     const typename Store16<T>::type* vn, T* w, RedSlot red) {
+  pdl_wait();
+  pdl_trigger();
+  const T h = *hp;
+  double acc[2] = {0.0, 0.0};
+  each4(
+      m,
+      [&](size_t i) {
+        T a[4], x[4], b[4];
+        ld16x4<T>(v + i, a);
+        ld16x4<T>(vn + i, b);
+        ldT4rw(w + i, x);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) x[e] = xsub(x[e], xmul(h, a[e]));
+        stT4(w + i, x);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) dot16_acc(acc, b[e], x[e]);
+      },
+      [&](size_t i) {
+        const T x = xsub(w[i], xmul(h, Store16<T>::get(v[i])));
+        w[i] = x;
+        dot16_acc(acc, Store16<T>::get(vn[i]), x);
+      });
+  grid_reduce<2>(acc, red);
+}
 // w = widen(v16) (exact)
 template <class T>
 __global__ void __launch_bounds__(256) k_widen16(size_t m, const typename Store16<T>::type* v, T* w) {
@@ -791,6 +823,14 @@ void basis16_axmy(size_t m, T h, const void* v, T* w, cudaStream_t st) {
   launch_pdl(k_vaxmy16<T>, dim3(grid_for(m / 4 + 1, 256, 8)), dim3(256), 0, st, m, h,
              (const typename Store16<T>::type*)v, w);
   LAUNCHED("basis16_axmy");
+}
+template <class T>
+void basis16_axmy_dot(size_t m, const T* h, const void* v, const void* vn, T* w, const RedSlot& red, cudaStream_t st) {
+  const unsigned g = grid_for(m / 4 + 1, 256, 4);  // (basis16_dot's grid: the same partials)
+  using S = typename Store16<T>::type;
+  launch_pdl(k_vaxmy_dot16<T>, dim3(g), dim3(256), 0, st, m, h, (const S*)v, (const S*)vn, w, red);
+  note_partials(red, g);
+  LAUNCHED("basis16_axmy_dot");
 }
 template <class T>
 void basis16_axmy_hp(size_t m, const T* h, const void* v, T* w, cudaStream_t st) {
@@ -886,6 +926,7 @@ void cast_f64_to_storage(size_t m, const double* src, int storage, void* dst, cu
   template void basis16_dot<T>(size_t, const void*, const T*, const RedSlot&, cudaStream_t);             \
   template void basis16_axmy<T>(size_t, T, const void*, T*, cudaStream_t);                               \
   template void basis16_axmy_hp<T>(size_t, const T*, const void*, T*, cudaStream_t);                    \
+  template void basis16_axmy_dot<T>(size_t, const T*, const void*, const void*, T*, const RedSlot&, cudaStream_t); \
   template void basis16_axpy<T>(size_t, T, const void*, T*, cudaStream_t);                               \
   template void basis16_widen<T>(size_t, const void*, T*, cudaStream_t);                                 \
   template void basis16_candidate<T>(size_t, const T*, void* const*, const T*, int, T*, cudaStream_t);

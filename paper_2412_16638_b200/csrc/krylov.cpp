@@ -745,11 +745,26 @@ void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num,
       const int dh = dh_env ? dh_env[0] - '0' : 1;
       const bool dev_h = (dh == 2 ? (b16 || num == Numerics::Fast) : (dh == 1 && b16)) &&
                          (!w.comm || w.comm->size() == 1) && k + 1 <= KrylovWork<T>::kMaxH;
+      // (fp16 basis: step j's update and step j + 1's dot share one pass,
+      // bitwise the separate kernels; MPRKB_GMRES_FUSE_MGS=0 splits them)
+      const char* fm_env = std::getenv("MPRKB_GMRES_FUSE_MGS");
+      const bool fuse_mgs = !(fm_env && fm_env[0] == '0');
       if (dev_h) {
         const RedSlot sd = w.red.slot_dev(0);
         for (int j = 0; j <= k; ++j) {
           T* hd = w.h_val() + j;
-          if (b16) {
+          if (b16 && fuse_mgs) {
+            if (j == 0) {
+              basis16_dot<T>(m, basis16[0], wv, sd, st);
+              finish_h<T>(sd, hd, w.h_dev, st);
+            }
+            if (j < k) {
+              basis16_axmy_dot<T>(m, hd, basis16[j], basis16[j + 1], wv, sd, st);
+              finish_h<T>(sd, hd + 1, w.h_dev + 2 * (j + 1), st);
+            } else {
+              basis16_axmy_hp<T>(m, hd, basis16[j], wv, st);
+            }
+          } else if (b16) {
             basis16_dot<T>(m, basis16[j], wv, sd, st);
             finish_h<T>(sd, hd, w.h_dev + 2 * j, st);
             basis16_axmy_hp<T>(m, hd, basis16[j], wv, st);

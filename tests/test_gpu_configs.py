@@ -177,6 +177,35 @@ def test_config4_gmres_block_jacobi_vs_reference_gmres(gpu, mp, ref, n, storage)
     assert np.linalg.norm(xg.cpu().numpy() - xw) <= 10 * tol * np.linalg.norm(xw)
 
 
+
+def test_gmres_fp16_basis_fused_mgs_bitwise(gpu, mp):
+    """fp16-basis GMRES fuses each modified Gram-Schmidt update with the next
+    coefficient's dot (k_vaxmy_dot16: one pass over w instead of two, the dot
+    on k_dot16's grid): stepped states, iteration counts and residual
+    histories are bitwise the separate kernels' (MPRKB_GMRES_FUSE_MGS=0), on
+    multi-iteration block-Jacobi solves."""
+    import os
+
+    kw = dict(nu=1e-2, preconditioner="block-jacobi", block_size=8, basis_storage="f16")
+    t = mp.builtin("4s3pC")
+    runs = []
+    for env in (None, "0"):
+        if env:
+            os.environ["MPRKB_GMRES_FUSE_MGS"] = env
+        try:
+            st = mp.Stepper("advection-diffusion", 64, t, 1.0 / 160.0, 1e-4, "f32", 40, **kw)
+            u = st.initial_state()
+            trs = [st.step(u) for _ in range(2)]
+            runs.append((u, [tr["iterations"] for tr in trs], [st.history(i) for i in range(4)]))
+        finally:
+            os.environ.pop("MPRKB_GMRES_FUSE_MGS", None)
+    (ua, ia, ha), (ub, ib, hb) = runs
+    assert ia == ib and max(max(i) for i in ia) > 2
+    for x, y in zip(ha, hb):
+        assert np.array_equal(np.asarray(x), np.asarray(y))
+    assert np.array_equal(ua, ub)
+
+
 @pytest.mark.parametrize("n", [32, 64])
 def test_config4_gmres_fp16_basis_vs_restatement(gpu, mp, ref, n):
     """fp16 Krylov basis, fp64-accumulated Gram-Schmidt: the GPU solver vs the
