@@ -727,13 +727,26 @@ void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num,
     int k = 0;
     for (; k < kmax;) {
       const T* vk;
-      if (b16) {  // the operator reads the basis vector widened to T (exact)
-        basis16_widen<T>(m, basis16[k], wt, st);
-        vk = wt;
-      } else {
-        vk = basis[k];
+      bool applied = false;
+      if constexpr (std::is_same_v<T, c32>) {
+        // a stencil operator reads the fp16 basis vector itself (widened
+        // exactly on load: bitwise the widen + apply; MPRKB_GMRES_H16_OP=0)
+        const char* ho = std::getenv("MPRKB_GMRES_H16_OP");
+        if (b16 && A.stencil() && !A.stencil()->halo && !(ho && ho[0] == '0')) {
+          Bracket br(timer, "stencil", st);
+          stencil_apply_h16(*A.stencil(), basis16[k], t, st);
+          applied = true;
+        }
       }
-      op(vk, t);
+      if (!applied) {
+        if (b16) {  // the operator reads the basis vector widened to T (exact)
+          basis16_widen<T>(m, basis16[k], wt, st);
+          vk = wt;
+        } else {
+          vk = basis[k];
+        }
+        op(vk, t);
+      }
       pre(t, wv);
       std::vector<H> h(k + 2, H{});
       // fp16 basis, one rank: each h_j is formed on the device from its dot's

@@ -32,6 +32,9 @@ struct StencilSpec {
 // out = sigma x + gamma K3 x
 template <class T>
 void stencil_apply(const StencilSpec& s, const T* x, T* out, cudaStream_t st);
+// the stencil of an fp16-stored complex vector (__half2 per element, the GMRES
+// fp16 basis), widened exactly on load: bitwise stencil_apply of the widened vector
+void stencil_apply_h16(const StencilSpec& s, const void* x16, c32* out, cudaStream_t st);
 // r = b - (sigma x + gamma K3 x); optional fused fp64 sum of r.r into `red`
 template <class T>
 void stencil_residual(const StencilSpec& s, const T* x, const T* b, T* r, const RedSlot* red,

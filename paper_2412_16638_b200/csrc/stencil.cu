@@ -110,6 +110,29 @@ struct LdF2D {
   __device__ __forceinline__ double cv(float r) const { return (double)r; }
 };
 
+// fp16-stored complex vector (the GMRES fp16 Krylov basis, __half2 per
+// element) read in complex<float>: widening is exact, so the stencil of the
+// loaded values equals the stencil of the widened vector
+struct LdH2C {
+  using type = c32;
+  using raw = __half2;
+  const __half2* p;
+  const __half2* glo = nullptr;
+  const __half2* ghi = nullptr;
+  __device__ __forceinline__ c32 cv(__half2 r) const { return {__low2float(r), __high2float(r)}; }
+  __device__ __forceinline__ c32 ld1f(const __half2* b, long i) const { return cv(b[i]); }
+  __device__ __forceinline__ V4<c32> ld4f(const __half2* b, long i) const {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(b + i));
+    const unsigned w[4] = {u.x, u.y, u.z, u.w};
+    V4<c32> v;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) v.x[e] = cv(*reinterpret_cast<const __half2*>(&w[e]));
+    return v;
+  }
+  __device__ __forceinline__ c32 ld1(long i) const { return ld1f(p, i); }
+  __device__ __forceinline__ V4<c32> ld4(long i) const { return ld4f(p, i); }
+};
+
 template <class T>
 __device__ __forceinline__ T shfl_up1(T v) {
   return __shfl_up_sync(0xffffffffu, v, 1);
@@ -827,9 +850,16 @@ __global__ void __launch_bounds__(TTHREADS, tma_min_blocks<Epi>())
   auto wait = [&](int q) { mbar_wait(&full[q % TST], (uint32_t)(q / TST) & 1u); };
   auto ld = [&](const Raw* p) -> V4<T> {
     V4<T> v;
-    if constexpr (sizeof(Raw) == 4) {
+    if constexpr (std::is_same_v<Raw, float>) {
       const float4 f = *reinterpret_cast<const float4*>(p);
       v.x[0] = src.cv(f.x); v.x[1] = src.cv(f.y); v.x[2] = src.cv(f.z); v.x[3] = src.cv(f.w);
+    } else if constexpr (sizeof(Raw) == 4) {  // (fp16 complex: one 16-byte word)
+      union {
+        uint4 w;
+        Raw e[4];
+      } u;
+      u.w = *reinterpret_cast<const uint4*>(p);
+      v.x[0] = src.cv(u.e[0]); v.x[1] = src.cv(u.e[1]); v.x[2] = src.cv(u.e[2]); v.x[3] = src.cv(u.e[3]);
     } else if constexpr (std::is_same_v<Raw, double>) {
       const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
       v.x[0] = src.cv(a.x); v.x[1] = src.cv(a.y); v.x[2] = src.cv(b.x); v.x[3] = src.cv(b.y);
@@ -1148,6 +1178,10 @@ void stencil_residual(const StencilSpec& s, const T* x, const T* b, T* r, const 
     launch(s, LdPlain<T>{x}, EpiResidual<T, true>{b, r, *red}, st, "stencil_residual");
   else
     launch(s, LdPlain<T>{x}, EpiResidual<T, false>{b, r, RedSlot{}}, st, "stencil_residual");
+}
+
+void stencil_apply_h16(const StencilSpec& s, const void* x16, c32* out, cudaStream_t st) {
+  launch(s, LdH2C{static_cast<const __half2*>(x16)}, EpiStore<c32>{out}, st, "stencil");
 }
 
 template <class T>

@@ -178,12 +178,15 @@ def test_config4_gmres_block_jacobi_vs_reference_gmres(gpu, mp, ref, n, storage)
 
 
 
-def test_gmres_fp16_basis_fused_mgs_bitwise(gpu, mp):
+@pytest.mark.parametrize("switch,n", [("MPRKB_GMRES_FUSE_MGS", 64), ("MPRKB_GMRES_H16_OP", 128)])
+def test_gmres_fp16_basis_fused_mgs_bitwise(gpu, mp, switch, n):
     """fp16-basis GMRES fuses each modified Gram-Schmidt update with the next
     coefficient's dot (k_vaxmy_dot16: one pass over w instead of two, the dot
-    on k_dot16's grid): stepped states, iteration counts and residual
-    histories are bitwise the separate kernels' (MPRKB_GMRES_FUSE_MGS=0), on
-    multi-iteration block-Jacobi solves."""
+    on k_dot16's grid), and the stencil operator reads the fp16 basis vector
+    itself (widened exactly on load, no widened copy): stepped states,
+    iteration counts and residual histories are bitwise the separate kernels'
+    (MPRKB_GMRES_FUSE_MGS=0 / MPRKB_GMRES_H16_OP=0), on multi-iteration
+    block-Jacobi solves (n = 128: the periodic TMA stencil pipeline)."""
     import os
 
     kw = dict(nu=1e-2, preconditioner="block-jacobi", block_size=8, basis_storage="f16")
@@ -191,14 +194,14 @@ def test_gmres_fp16_basis_fused_mgs_bitwise(gpu, mp):
     runs = []
     for env in (None, "0"):
         if env:
-            os.environ["MPRKB_GMRES_FUSE_MGS"] = env
+            os.environ[switch] = env
         try:
-            st = mp.Stepper("advection-diffusion", 64, t, 1.0 / 160.0, 1e-4, "f32", 40, **kw)
+            st = mp.Stepper("advection-diffusion", n, t, 1.0 / 160.0, 1e-4, "f32", 40, **kw)
             u = st.initial_state()
             trs = [st.step(u) for _ in range(2)]
             runs.append((u, [tr["iterations"] for tr in trs], [st.history(i) for i in range(4)]))
         finally:
-            os.environ.pop("MPRKB_GMRES_FUSE_MGS", None)
+            os.environ.pop(switch, None)
     (ua, ia, ha), (ub, ib, hb) = runs
     assert ia == ib and max(max(i) for i in ia) > 2
     for x, y in zip(ha, hb):
