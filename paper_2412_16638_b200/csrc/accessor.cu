@@ -408,6 +408,9 @@ struct AccKernels {
   // dot's partial sums in another order)
   static void pq(const StencilSpec& A, const S* z, T beta, const S* p, S* pn, S* q, const RedSlot& red,
                  cudaStream_t st) {
+    if constexpr (std::is_same_v<T, float> && std::is_same_v<S, __half>) {
+      if (acc_pq_tma(A, z, beta, p, pn, q, red, st)) return;
+    }
     const int n = A.n;
     const unsigned gx = (unsigned)((n / 4 + kPqX - 1) / kPqX), gy = (unsigned)((n + kPqY - 1) / kPqY);
     // k-chunks: about 8 resident CTAs of 256 threads per SM in one wave

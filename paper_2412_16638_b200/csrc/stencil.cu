@@ -1967,6 +1967,165 @@ __global__ void __launch_bounds__(TTHREADS)
   grid_reduce<1>(acc, red);
 }
 
+// ---- the accessor-storage direction pass on the TMA plane pipeline -----------------
+// (accessor.cu k_acc_pq: p' = rt(z + beta p), q = rt(A p'), p'.q with z, p,
+// p', q stored in fp16 and every value computed in fp32, rt = round to fp16
+// and widen.)  z and p stream through one TMA ring of fp16 plane tiles (a
+// quarter of the fp32 ring's bytes); p' is formed at every loaded point, so
+// its j / k neighbours come from shared memory instead of three cached row
+// reads per point.  Same element operations as k_acc_pq; the p'.q partials
+// are grouped by this grid.
+// (fp16 rows carry an 8-element halo on each side, so every box starts on a
+// 16-byte boundary: i0 - 8 elements = i0 * 2 - 16 bytes)
+constexpr int AQ_W = TI + 16;
+constexpr int AQ_SLOT = (int)((((size_t)(TJ + 2) * AQ_W * 2 + 127) / 128) * 128 / 2);
+constexpr size_t aq_smem() { return (size_t)CG_TST * 2 * AQ_SLOT * sizeof(__half) + CG_TST * sizeof(uint64_t) + 128; }
+
+__global__ void __launch_bounds__(TTHREADS)
+    k_acc_pq_tma(const __grid_constant__ CUtensorMap zmap, const __grid_constant__ CUtensorMap pmap, int n, int nz,
+                 int kc, float s, float g, float beta, __half* __restrict__ pnew, __half* __restrict__ q, RedSlot red) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ unsigned char smem_raw[];
+  __half* buf = reinterpret_cast<__half*>(smem_align128(smem_raw));
+  uint64_t* full = reinterpret_cast<uint64_t*>(buf + CG_TST * 2 * AQ_SLOT);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int i0 = blockIdx.x * TI, j0 = blockIdx.y * TJ;
+  int k0, k1;
+  plane_range(nz, 0, nz, kc, k0, k1);
+  const int planes = k1 - k0 + 2;
+  constexpr uint32_t bytes = (TJ + 2) * AQ_W * sizeof(__half);
+  if (tid == 0) {
+    for (int b = 0; b < CG_TST; ++b) mbar_init(&full[b], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const CUtensorMap* zm = &zmap;
+  const CUtensorMap* pm = &pmap;
+  auto issue = [&](int qq) {
+    const int k = k0 - 1 + qq, sl = qq % CG_TST;
+    __half* dst = buf + sl * 2 * AQ_SLOT;
+    mbar_expect_tx(&full[sl], 2 * bytes);
+    tma_3d(dst, zm, i0 - 8, j0 - 1, k, &full[sl]);
+    tma_3d(dst + AQ_SLOT, pm, i0 - 8, j0 - 1, k, &full[sl]);
+  };
+  if (tid == 0)
+    for (int qq = 0; qq < CG_TST && qq < planes; ++qq) issue(qq);
+  auto wait = [&](int qq) { mbar_wait(&full[qq % CG_TST], (uint32_t)(qq / CG_TST) & 1u); };
+  auto ld = [](const __half* ptr) {  // 4 fp16 values (8 bytes), widened exactly
+    const uint2 u = *reinterpret_cast<const uint2*>(ptr);
+    const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+    const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+    V4<float> v;
+    v.x[0] = a.x; v.x[1] = a.y; v.x[2] = b.x; v.x[3] = b.y;
+    return v;
+  };
+  auto rt = [](float v) { return __half2float(__float2half_rn(v)); };
+  auto upd = [&](float zv, float pv) { return rt(xadd(zv, xmul(beta, pv))); };  // k_acc_pq's p'
+  auto upd4 = [&](const V4<float>& zv, const V4<float>& pv) {
+    V4<float> o;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o.x[e] = upd(zv.x[e], pv.x[e]);
+    return o;
+  };
+  auto st4h = [](__half* dst, const V4<float>& v) {  // round to fp16, store 8 bytes; returns nothing
+    const __half2 a = __floats2half2_rn(v.x[0], v.x[1]), b = __floats2half2_rn(v.x[2], v.x[3]);
+    uint2 u;
+    u.x = *reinterpret_cast<const unsigned*>(&a);
+    u.y = *reinterpret_cast<const unsigned*>(&b);
+    *reinterpret_cast<uint2*>(dst) = u;
+  };
+  double acc[1] = {0.0};
+  const long nn = n, n2 = nn * nn;
+  const int col = 8 + 4 * lane;
+  for (int k = k0; k < k1; ++k) {
+    const int qq = k - k0 + 1;
+    if (k == k0) {
+      wait(0);
+      wait(1);
+    }
+    wait(qq + 1);
+    const __half* bm = buf + ((qq - 1) % CG_TST) * 2 * AQ_SLOT;
+    const __half* bc = buf + (qq % CG_TST) * 2 * AQ_SLOT;
+    const __half* bp = buf + ((qq + 1) % CG_TST) * 2 * AQ_SLOT;
+#pragma unroll
+    for (int rr = 0; rr < TROWS; ++rr) {
+      const int row = warp * TROWS + rr;
+      const int o = (row + 1) * AQ_W + col;
+      const V4<float> c = upd4(ld(bc + o), ld(bc + AQ_SLOT + o));
+      const V4<float> ym = upd4(ld(bc + o - AQ_W), ld(bc + AQ_SLOT + o - AQ_W));
+      const V4<float> yp = upd4(ld(bc + o + AQ_W), ld(bc + AQ_SLOT + o + AQ_W));
+      const V4<float> zmv = upd4(ld(bm + o), ld(bm + AQ_SLOT + o));
+      const V4<float> zpv = upd4(ld(bp + o), ld(bp + AQ_SLOT + o));
+      float xl = shfl_up1(c.x[3]), xr = shfl_down1(c.x[0]);
+      const float pe = upd(__half2float(edge_ld(bc + o, lane)), __half2float(edge_ld(bc + AQ_SLOT + o, lane)));
+      xl = lane == 0 ? pe : xl;
+      xr = lane == 31 ? pe : xr;
+      V4<float> v, sq;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float al = e == 0 ? xl : c.x[e - 1], ar = e == 3 ? xr : c.x[e + 1];
+        v.x[e] = point<float>(0, s, g, 0.0f, c.x[e], al, ar, ym.x[e], yp.x[e], zmv.x[e], zpv.x[e]);
+        sq.x[e] = rt(v.x[e]);
+        acc[0] = __fma_rn((double)c.x[e], (double)sq.x[e], acc[0]);  // k_acc_pq's p'.q (stored q)
+      }
+      const long gi = (i0 + 4 * lane) + (long)(j0 + row) * nn + (long)k * n2;
+      st4h(pnew + gi, c);  // (exact: c is representable in fp16)
+      st4h(q + gi, v);
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (tid == 0 && qq - 1 + CG_TST < planes) issue(qq - 1 + CG_TST);
+  }
+  grid_reduce<1>(acc, red);
+}
+
+bool acc_pq_tma(const StencilSpec& sp, const void* z, float beta, const void* p, void* pnew, void* q,
+                const RedSlot& red, cudaStream_t st) {
+  const char* e = std::getenv("MPRKB_ACC_PQ_TMA");  // =0: the register-marching k_acc_pq
+  if ((e && e[0] == '0') || !pq_fused_supported(sp)) return false;
+  const int n = sp.n, nz = sp.nz > 0 ? sp.nz : n;
+  constexpr size_t smem = aq_smem();
+  static thread_local int chunk = 0;
+  static thread_local long chunk_cols = -1;
+  static thread_local int resident = 0;
+  if (!resident) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_acc_pq_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_acc_pq_tma, TTHREADS, smem));
+    resident = std::max(1, per_sm) * sm_count();
+  }
+  const long cols = (long)(n / TI) * (n / TJ);
+  if (cols != chunk_cols) {
+    long best_cost = -1;
+    for (int kc = 4; kc <= 64; ++kc) {
+      const long units = cols * ((nz + kc - 1) / kc);
+      const long cost = ((units + resident - 1) / resident) * (std::min(kc, nz) + 2);
+      if (best_cost < 0 || cost < best_cost) {
+        chunk = kc;
+        best_cost = cost;
+      }
+    }
+    chunk_cols = cols;
+  }
+  const cuuint64_t nn = (cuuint64_t)n;
+  const cuuint64_t dims3[3] = {nn, nn, (cuuint64_t)nz}, str3[2] = {nn * 2, nn * nn * 2};
+  const cuuint32_t box3[3] = {(cuuint32_t)AQ_W, (cuuint32_t)(TJ + 2), 1};
+  const CUtensorMap zmap = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, z, 3, dims3, str3, box3);
+  const CUtensorMap pmap = make_map(CU_TENSOR_MAP_DATA_TYPE_FLOAT16, p, 3, dims3, str3, box3);
+  const unsigned gz = (unsigned)((nz + chunk - 1) / chunk);
+  const dim3 grid((unsigned)(n / TI), (unsigned)(n / TJ), gz);
+  RedSlot rs = red;
+  rs.base = 0;
+  rs.total = 0;
+  launch_pdl(k_acc_pq_tma, grid, dim3(TTHREADS), smem, st, zmap, pmap, n, nz, chunk, (float)sp.sigma, (float)sp.gamma,
+             beta, static_cast<__half*>(pnew), static_cast<__half*>(q), rs);
+  note_partials(rs, grid.x * grid.y * grid.z);
+  note_kron(true);
+  LAUNCHED("acc_pq");
+  return true;
+}
+
 void pq_fused(const StencilSpec& sp, const float* z, const float* p, const RedSlot& beta_src, int beta_comp,
               float rz_old, float* pnew, float* q, const RedSlot& red, cudaStream_t st, const CgCtl* ctl) {
   if (!pq_fused_supported(sp)) MPRKB_THROW(10, "pq_fused: needs the TMA stencil on an undivided grid");

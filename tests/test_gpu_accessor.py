@@ -156,3 +156,27 @@ def test_cg_vector_storage_fused_passes(gpu, mp, monkeypatch, dtype, storage, b)
     np.testing.assert_allclose(rf["history"][:h], rs["history"][:h], rtol=1e-5)
     xf, xs = xf.cpu().numpy(), xs.cpu().numpy()
     assert np.linalg.norm(xf - xs) <= 1e-5 * np.linalg.norm(xs) + 2 * tol * np.linalg.norm(xs)
+
+
+def test_cg_vector_storage_tma_direction_pass(gpu, mp, monkeypatch):
+    """fp16 vectors on a TMA-sized grid (n % 128 == 0): the direction pass
+    p = z + beta p, q = A p, p.q runs on the TMA plane pipeline
+    (k_acc_pq_tma) with the same element operations as k_acc_pq
+    (MPRKB_ACC_PQ_TMA=0); only the fp64 grouping of p.q differs, so the
+    iterations agree within one and histories / solutions closely."""
+    import torch
+
+    n = 128
+    tau, a, sigma, gamma, bv = _system(n, np.float32, seed=5)
+    A = mp.Operator.stencil(0, n, 0, sigma, gamma)
+    P = mp.Operator.block_jacobi(0, "heat", n, tau, a, 8, "f16")
+    bd = torch.from_numpy(bv).cuda()
+    xf, rf = mp.cg(A, P, bd, torch.zeros_like(bd), 1e-3, 300, storage="f16")
+    monkeypatch.setenv("MPRKB_ACC_PQ_TMA", "0")
+    xs, rs = mp.cg(A, P, bd, torch.zeros_like(bd), 1e-3, 300, storage="f16")
+    assert rf["converged"] and rs["converged"]
+    assert abs(rf["iterations"] - rs["iterations"]) <= 1 and rf["iterations"] >= 3
+    h = min(len(rf["history"]), len(rs["history"]))
+    np.testing.assert_allclose(rf["history"][:h], rs["history"][:h], rtol=1e-5)
+    xf, xs = xf.cpu().numpy(), xs.cpu().numpy()
+    assert np.linalg.norm(xf - xs) <= 1e-5 * np.linalg.norm(xs) + 2e-3 * np.linalg.norm(xs)
