@@ -773,6 +773,36 @@ __global__ void __launch_bounds__(256) k_vaxmy_dot16(size_t m, const T* hp, cons
       });
   grid_reduce<2>(acc, red);
 }
+// The sweep's last update fused with the norm of its result: w -= (*hp) v16,
+// then w.w on the updated w — accumulated exactly as k_dot_fast(m, w, w)
+// (blas.cu: the same grid, block, traversal and per-element order), so the
+// partials are bitwise the separate norm's.
+template <class T>
+__global__ void __launch_bounds__(256) k_vaxmy16_norm(size_t m, const T* hp, const typename Store16<T>::type* v, T* w,
+                                                      RedSlot red) {
+  pdl_wait();
+  pdl_trigger();
+  const T h = *hp;
+  double acc[1] = {0.0};
+  each4(
+      m,
+      [&](size_t i) {
+        T a[4], x[4];
+        ld16x4<T>(v + i, a);
+        ldT4rw(w + i, x);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) x[e] = xsub(x[e], xmul(h, a[e]));
+        stT4(w + i, x);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) dot_acc(acc, x[e], x[e]);
+      },
+      [&](size_t i) {
+        const T x = xsub(w[i], xmul(h, Store16<T>::get(v[i])));
+        w[i] = x;
+        dot_acc(acc, x, x);
+      });
+  grid_reduce<1>(acc, red);
+}
 // w = widen(v16) (exact)
 template <class T>
 __global__ void __launch_bounds__(256) k_widen16(size_t m, const typename Store16<T>::type* v, T* w) {
@@ -831,6 +861,13 @@ void basis16_axmy_dot(size_t m, const T* h, const void* v, const void* vn, T* w,
   launch_pdl(k_vaxmy_dot16<T>, dim3(g), dim3(256), 0, st, m, h, (const S*)v, (const S*)vn, w, red);
   note_partials(red, g);
   LAUNCHED("basis16_axmy_dot");
+}
+template <class T>
+void basis16_axmy_norm(size_t m, const T* h, const void* v, T* w, const RedSlot& red, cudaStream_t st) {
+  const unsigned g = grid_for((m + 3) / 4, 256, 8);  // (blas.cu dot_real's grid: the same partials)
+  launch_pdl(k_vaxmy16_norm<T>, dim3(g), dim3(256), 0, st, m, h, (const typename Store16<T>::type*)v, w, red);
+  note_partials(red, g);
+  LAUNCHED("basis16_axmy_norm");
 }
 template <class T>
 void basis16_axmy_hp(size_t m, const T* h, const void* v, T* w, cudaStream_t st) {
@@ -927,6 +964,7 @@ void cast_f64_to_storage(size_t m, const double* src, int storage, void* dst, cu
   template void basis16_axmy<T>(size_t, T, const void*, T*, cudaStream_t);                               \
   template void basis16_axmy_hp<T>(size_t, const T*, const void*, T*, cudaStream_t);                    \
   template void basis16_axmy_dot<T>(size_t, const T*, const void*, const void*, T*, const RedSlot&, cudaStream_t); \
+  template void basis16_axmy_norm<T>(size_t, const T*, const void*, T*, const RedSlot&, cudaStream_t);        \
   template void basis16_axpy<T>(size_t, T, const void*, T*, cudaStream_t);                               \
   template void basis16_widen<T>(size_t, const void*, T*, cudaStream_t);                                 \
   template void basis16_candidate<T>(size_t, const T*, void* const*, const T*, int, T*, cudaStream_t);

@@ -762,6 +762,7 @@ void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num,
       // bitwise the separate kernels; MPRKB_GMRES_FUSE_MGS=0 splits them)
       const char* fm_env = std::getenv("MPRKB_GMRES_FUSE_MGS");
       const bool fuse_mgs = !(fm_env && fm_env[0] == '0');
+      bool norm_fused = false;
       if (dev_h) {
         const RedSlot sd = w.red.slot_dev(0);
         for (int j = 0; j <= k; ++j) {
@@ -774,6 +775,9 @@ void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num,
             if (j < k) {
               basis16_axmy_dot<T>(m, hd, basis16[j], basis16[j + 1], wv, sd, st);
               finish_h<T>(sd, hd + 1, w.h_dev + 2 * (j + 1), st);
+            } else if (fast) {  // (the last update carries ||w||^2: read below)
+              basis16_axmy_norm<T>(m, hd, basis16[j], wv, s0, st);
+              norm_fused = true;
             } else {
               basis16_axmy_hp<T>(m, hd, basis16[j], wv, st);
             }
@@ -805,7 +809,7 @@ void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num,
           vaxmy<T>(m, to_dev<T>(hj), basis[j], wv, st);
         }
       }
-      const R wnorm = norm2(wv);
+      const R wnorm = norm_fused ? std::sqrt((R)finish_red(w, 1, st)[0]) : norm2(wv);
       if (dev_h)
         for (int j = 0; j <= k; ++j) {
           const volatile double* hv = w.h_host + 2 * j;

@@ -264,6 +264,10 @@ void basis16_axmy_hp(size_t m, const T* h, const void* v, T* w, cudaStream_t st)
 // basis16_axmy_hp followed by basis16_dot)
 template <class T>
 void basis16_axmy_dot(size_t m, const T* h, const void* v, const void* vn, T* w, const RedSlot& red, cudaStream_t st);
+// w -= (*h) v16 and w.w in one pass (bitwise basis16_axmy_hp followed by the
+// FAST dot_real(w, w))
+template <class T>
+void basis16_axmy_norm(size_t m, const T* h, const void* v, T* w, const RedSlot& red, cudaStream_t st);
 template <class T>
 void basis16_widen(size_t m, const void* v, T* w, cudaStream_t st);  // w = widen(v16), exact
 // xc = x + sum_j y_j v16_j (j ascending, one pass)
