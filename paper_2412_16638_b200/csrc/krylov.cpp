@@ -727,15 +727,24 @@ void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num,
     int k = 0;
     for (; k < kmax;) {
       const T* vk;
-      bool applied = false;
+      bool applied = false, pre_applied = false;
       if constexpr (std::is_same_v<T, c32>) {
         // a stencil operator reads the fp16 basis vector itself (widened
-        // exactly on load: bitwise the widen + apply; MPRKB_GMRES_H16_OP=0)
+        // exactly on load: bitwise the widen + apply; MPRKB_GMRES_H16_OP=0),
+        // and a b = 8 block-Jacobi preconditioner folds into that pass
+        // (bitwise A then P; MPRKB_GMRES_BJ_FOLD=0)
         const char* ho = std::getenv("MPRKB_GMRES_H16_OP");
+        const char* bf = std::getenv("MPRKB_GMRES_BJ_FOLD");
         if (b16 && A.stencil() && !A.stencil()->halo && !(ho && ho[0] == '0')) {
-          Bracket br(timer, "stencil", st);
-          stencil_apply_h16(*A.stencil(), basis16[k], t, st);
-          applied = true;
+          if (P && !(bf && bf[0] == '0')) {
+            Bracket br(timer, "stencil", st);
+            pre_applied = applied = P->stencil_then_apply_h16(*A.stencil(), basis16[k], wv, st);
+          }
+          if (!applied) {
+            Bracket br(timer, "stencil", st);
+            stencil_apply_h16(*A.stencil(), basis16[k], t, st);
+            applied = true;
+          }
         }
       }
       if (!applied) {
@@ -747,7 +756,7 @@ void gmres_solve(Op& A, Op* P, const T* b, T* x, const Crit& crit, Numerics num,
         }
         op(vk, t);
       }
-      pre(t, wv);
+      if (!pre_applied) pre(t, wv);
       std::vector<H> h(k + 2, H{});
       // fp16 basis, one rank: each h_j is formed on the device from its dot's
       // tuples (the host's sum order and rounding) and consumed there, so the

@@ -35,6 +35,10 @@ void stencil_apply(const StencilSpec& s, const T* x, T* out, cudaStream_t st);
 // the stencil of an fp16-stored complex vector (__half2 per element, the GMRES
 // fp16 basis), widened exactly on load: bitwise stencil_apply of the widened vector
 void stencil_apply_h16(const StencilSpec& s, const void* x16, c32* out, cudaStream_t st);
+// out = P (A v) with P the b = 8 block-Jacobi inverse (one stored 8 x 8 block,
+// fp32 / fp16 storage) folded into the stencil pass of an fp16 complex basis
+// vector; false when the grid does not take the TMA path (caller falls back)
+bool stencil_bj8_h16(const StencilSpec& s, const void* x16, int storage, const void* inv, c32* out, cudaStream_t st);
 // accessor-storage CG direction pass (fp16 z, p, p', q; fp32 compute) on the
 // TMA plane pipeline; false when the grid does not take it (caller falls back)
 bool acc_pq_tma(const StencilSpec& sp, const void* z, float beta, const void* p, void* pnew, void* q,

@@ -44,6 +44,13 @@ class Op {
                                    const void* /*q*/, void* /*z*/, const RedSlot& /*red*/, cudaStream_t /*st*/) {
     return false;
   }
+  // out = P (A v16) with A a stencil and v16 an fp16 complex vector (GMRES's
+  // fp16 basis), the preconditioner folded into the stencil pass.  false:
+  // not available (the solver runs A then P).
+  virtual bool stencil_then_apply_h16(const StencilSpec& /*A*/, const void* /*v16*/, void* /*out*/,
+                                      cudaStream_t /*st*/) {
+    return false;
+  }
   // Accessor-style apply (accessor.cu): z = P r with r and z stored in
   // `storage` (4 fp16, 0 fp32, 1 fp64), arithmetic in the operator's dtype,
   // red <- r.z of the stored values.  false: not available.

@@ -140,6 +140,13 @@ class BlockJacobiOp final : public Op {
     }
     return false;
   }
+  bool stencil_then_apply_h16(const StencilSpec& A, const void* v16, void* out, cudaStream_t st) override {
+    if constexpr (std::is_same_v<T, c32>) {
+      if (b_ == 8 && n_ % 8 == 0 && lines_ == (long)n_ * n_)
+        return stencil_bj8_h16(A, v16, storage_, inv_.get(), static_cast<c32*>(out), st);
+    }
+    return false;
+  }
   bool apply_storage(const void* r, int storage, void* z, const RedSlot& red, cudaStream_t st) override {
     if constexpr (std::is_same_v<T, float> || std::is_same_v<T, double>) {
       block_jacobi_acc<T>(n_, b_, storage_, inv_.get(), storage, r, z, red, st, lines_);

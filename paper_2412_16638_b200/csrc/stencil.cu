@@ -219,6 +219,58 @@ struct EpiStore {
   __device__ void finish(State&) const {}
 };
 
+// z = D_blk (A v) for b = 8 x-line blocks (complex<float> GMRES with a
+// block-Jacobi preconditioner, left-preconditioned: w = P A v): a block is
+// the 4 + 4 outputs of a lane pair, exchanged by shuffles; every output
+// accumulates D[jj][ii] t_jj over jj ascending with the product then the sum,
+// exactly as k_block_jacobi_row<c32, S, 8>.  Needs every lane of the warp
+// active (the TMA path: n % 128 == 0).  D = the one stored 8 x 8 inverse
+// (column-major, storage S).
+template <class S>
+struct EpiBJ8 {
+  c32* out;
+  const S* inv;
+  struct State {};
+  using Pre = NoPre;
+  __device__ void init(State&) const {}
+  __device__ __forceinline__ Pre pre4(long) const { return {}; }
+  __device__ __forceinline__ static float dv(const S* p) {
+    if constexpr (std::is_same_v<S, __half>)
+      return __half2float(__ldg(p));
+    else
+      return __ldg(p);
+  }
+  __device__ __forceinline__ void v4p(State&, long i, const V4<c32>& v, const V4<c32>&, const Pre&) const {
+    const int lane = threadIdx.x & 31, hi = lane & 1;
+    c32 o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      o[e] = {__shfl_xor_sync(0xffffffffu, v.x[e].re, 1), __shfl_xor_sync(0xffffffffu, v.x[e].im, 1)};
+    c32 t[8];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      t[e] = hi ? o[e] : v.x[e];
+      t[4 + e] = hi ? v.x[e] : o[e];
+    }
+    V4<c32> acc;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc.x[e] = c32{0.f, 0.f};
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float d = dv(inv + jj * 8 + 4 * hi + e);
+        acc.x[e] = xadd(acc.x[e], c32{xmul(d, t[jj].re), xmul(d, t[jj].im)});
+      }
+    st4(out + i, acc);
+  }
+  __device__ __forceinline__ void v4(State& s, long i, const V4<c32>& v, const V4<c32>& xc) const {
+    v4p(s, i, v, xc, pre4(i));
+  }
+  __device__ __forceinline__ void s1(State&, long, c32, c32) const { __trap(); }  // (vector paths only)
+  __device__ void finish(State&) const {}
+};
+
 template <class T, bool RED>
 struct EpiResidual {
   const T* b;
@@ -1182,6 +1234,20 @@ void stencil_residual(const StencilSpec& s, const T* x, const T* b, T* r, const 
 
 void stencil_apply_h16(const StencilSpec& s, const void* x16, c32* out, cudaStream_t st) {
   launch(s, LdH2C{static_cast<const __half2*>(x16)}, EpiStore<c32>{out}, st, "stencil");
+}
+
+bool stencil_bj8_h16(const StencilSpec& s, const void* x16, int storage, const void* inv, c32* out, cudaStream_t st) {
+  // (the TMA path only: every lane active, so the block's lane pairs can shuffle)
+  if (s.n % TI || s.halo || s.stencil == 0 || !tma_stencil_enabled() || !tma_periodic_enabled()) return false;
+  if (storage == 0)
+    launch(s, LdH2C{static_cast<const __half2*>(x16)}, EpiBJ8<float>{out, static_cast<const float*>(inv)}, st,
+           "stencil_bj");
+  else if (storage == 4)
+    launch(s, LdH2C{static_cast<const __half2*>(x16)}, EpiBJ8<__half>{out, static_cast<const __half*>(inv)}, st,
+           "stencil_bj");
+  else
+    return false;
+  return true;
 }
 
 template <class T>

@@ -178,14 +178,16 @@ def test_config4_gmres_block_jacobi_vs_reference_gmres(gpu, mp, ref, n, storage)
 
 
 
-@pytest.mark.parametrize("switch,n", [("MPRKB_GMRES_FUSE_MGS", 64), ("MPRKB_GMRES_H16_OP", 128)])
+@pytest.mark.parametrize("switch,n", [("MPRKB_GMRES_FUSE_MGS", 64), ("MPRKB_GMRES_H16_OP", 128), ("MPRKB_GMRES_BJ_FOLD", 128)])
 def test_gmres_fp16_basis_fused_mgs_bitwise(gpu, mp, switch, n):
     """fp16-basis GMRES fuses each modified Gram-Schmidt update with the next
     coefficient's dot (k_vaxmy_dot16: one pass over w instead of two, the dot
-    on k_dot16's grid), and the stencil operator reads the fp16 basis vector
-    itself (widened exactly on load, no widened copy): stepped states,
-    iteration counts and residual histories are bitwise the separate kernels'
-    (MPRKB_GMRES_FUSE_MGS=0 / MPRKB_GMRES_H16_OP=0), on multi-iteration
+    on k_dot16's grid), the stencil operator reads the fp16 basis vector
+    itself (widened exactly on load, no widened copy) and the b = 8
+    block-Jacobi preconditioner folds into that stencil pass (lane-pair
+    shuffles): stepped states, iteration counts and residual histories are
+    bitwise the separate kernels' (MPRKB_GMRES_FUSE_MGS=0 /
+    MPRKB_GMRES_H16_OP=0 / MPRKB_GMRES_BJ_FOLD=0), on multi-iteration
     block-Jacobi solves (n = 128: the periodic TMA stencil pipeline)."""
     import os
 
