@@ -262,7 +262,9 @@ template <class T, class S, class SB, int B>
 __global__ void __launch_bounds__(128)
     k_acc_update_bj(long blocks, T alpha, T* __restrict__ x, const S* __restrict__ p, S* __restrict__ r,
                     const S* __restrict__ q, const SB* __restrict__ inv, S* __restrict__ z, RedSlot red) {
-  constexpr bool kStage = B >= 16;
+  // (a block stored in another precision than T is converted once into
+  // shared memory: per-entry loads + conversions cost more than the reads)
+  constexpr bool kStage = B >= 16 || !std::is_same_v<SB, T>;
   __shared__ __align__(16) T sblk[kStage ? B * B : 4];
   if constexpr (kStage) {
     for (int e = threadIdx.x; e < B * B; e += blockDim.x) sblk[e] = widen_s<T>(inv[e]);
