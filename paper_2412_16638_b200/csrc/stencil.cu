@@ -230,9 +230,19 @@ template <class S>
 struct EpiBJ8 {
   c32* out;
   const S* inv;
-  struct State {};
+  // this lane's 4 columns of the block (ii = 4 (lane & 1) + e), all 8 jj,
+  // loaded once per thread (the block is the same for every line)
+  struct State {
+    float d[8][4];
+  };
   using Pre = NoPre;
-  __device__ void init(State&) const {}
+  __device__ void init(State& st) const {
+    const int hi = threadIdx.x & 1;
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) st.d[jj][e] = dv(inv + jj * 8 + 4 * hi + e);
+  }
   __device__ __forceinline__ Pre pre4(long) const { return {}; }
   __device__ __forceinline__ static float dv(const S* p) {
     if constexpr (std::is_same_v<S, __half>)
@@ -240,7 +250,7 @@ struct EpiBJ8 {
     else
       return __ldg(p);
   }
-  __device__ __forceinline__ void v4p(State&, long i, const V4<c32>& v, const V4<c32>&, const Pre&) const {
+  __device__ __forceinline__ void v4p(State& st, long i, const V4<c32>& v, const V4<c32>&, const Pre&) const {
     const int lane = threadIdx.x & 31, hi = lane & 1;
     c32 o[4];
 #pragma unroll
@@ -259,7 +269,7 @@ struct EpiBJ8 {
     for (int jj = 0; jj < 8; ++jj)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        const float d = dv(inv + jj * 8 + 4 * hi + e);
+        const float d = st.d[jj][e];
         acc.x[e] = xadd(acc.x[e], c32{xmul(d, t[jj].re), xmul(d, t[jj].im)});
       }
     st4(out + i, acc);
@@ -2104,25 +2114,41 @@ __global__ void __launch_bounds__(TTHREADS)
   double acc[1] = {0.0};
   const long nn = n, n2 = nn * nn;
   const int col = 8 + 4 * lane;
+  // p' of this warp's rows of planes k - 1 and k, carried across the march
+  // (each formed once per plane; the same operation on the same operands as
+  // forming it per use, so bitwise unchanged)
+  V4<float> pm_[TROWS], pc_[TROWS];
   for (int k = k0; k < k1; ++k) {
     const int qq = k - k0 + 1;
     if (k == k0) {
       wait(0);
       wait(1);
+#pragma unroll
+      for (int rr = 0; rr < TROWS; ++rr) {
+        const int o = (warp * TROWS + rr + 1) * AQ_W + col;
+        pm_[rr] = upd4(ld(buf + o), ld(buf + AQ_SLOT + o));
+        pc_[rr] = upd4(ld(buf + 2 * AQ_SLOT + o), ld(buf + 3 * AQ_SLOT + o));
+      }
     }
     wait(qq + 1);
-    const __half* bm = buf + ((qq - 1) % CG_TST) * 2 * AQ_SLOT;
     const __half* bc = buf + (qq % CG_TST) * 2 * AQ_SLOT;
     const __half* bp = buf + ((qq + 1) % CG_TST) * 2 * AQ_SLOT;
+    V4<float> pn_[TROWS];
+#pragma unroll
+    for (int rr = 0; rr < TROWS; ++rr) {
+      const int o = (warp * TROWS + rr + 1) * AQ_W + col;
+      pn_[rr] = upd4(ld(bp + o), ld(bp + AQ_SLOT + o));
+    }
 #pragma unroll
     for (int rr = 0; rr < TROWS; ++rr) {
       const int row = warp * TROWS + rr;
       const int o = (row + 1) * AQ_W + col;
-      const V4<float> c = upd4(ld(bc + o), ld(bc + AQ_SLOT + o));
-      const V4<float> ym = upd4(ld(bc + o - AQ_W), ld(bc + AQ_SLOT + o - AQ_W));
-      const V4<float> yp = upd4(ld(bc + o + AQ_W), ld(bc + AQ_SLOT + o + AQ_W));
-      const V4<float> zmv = upd4(ld(bm + o), ld(bm + AQ_SLOT + o));
-      const V4<float> zpv = upd4(ld(bp + o), ld(bp + AQ_SLOT + o));
+      const V4<float> c = pc_[rr];
+      const V4<float> ym = rr > 0 ? pc_[rr > 0 ? rr - 1 : 0] : upd4(ld(bc + o - AQ_W), ld(bc + AQ_SLOT + o - AQ_W));
+      const V4<float> yp =
+          rr + 1 < TROWS ? pc_[rr + 1 < TROWS ? rr + 1 : 0] : upd4(ld(bc + o + AQ_W), ld(bc + AQ_SLOT + o + AQ_W));
+      const V4<float> zmv = pm_[rr];
+      const V4<float> zpv = pn_[rr];
       float xl = shfl_up1(c.x[3]), xr = shfl_down1(c.x[0]);
       const float pe = upd(__half2float(edge_ld(bc + o, lane)), __half2float(edge_ld(bc + AQ_SLOT + o, lane)));
       xl = lane == 0 ? pe : xl;
@@ -2138,6 +2164,11 @@ __global__ void __launch_bounds__(TTHREADS)
       const long gi = (i0 + 4 * lane) + (long)(j0 + row) * nn + (long)k * n2;
       st4h(pnew + gi, c);  // (exact: c is representable in fp16)
       st4h(q + gi, v);
+    }
+#pragma unroll
+    for (int rr = 0; rr < TROWS; ++rr) {
+      pm_[rr] = pc_[rr];
+      pc_[rr] = pn_[rr];
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
