@@ -228,6 +228,7 @@ struct EpiStore {
 // (column-major, storage S).
 template <class S>
 struct EpiBJ8 {
+  static constexpr int kTmaMinBlocks = 4;  // (register cap: 145 -> <= 128, 3 -> 4 CTAs per SM)
   c32* out;
   const S* inv;
   // this lane's 4 columns of the block (ii = 4 (lane & 1) + e), all 8 jj,
@@ -850,9 +851,14 @@ constexpr size_t tma_stencil_smem() {
 
 // resident CTAs per SM the register allocation must allow (the fused
 // f-evaluation epilogue otherwise takes 156 registers: 3 CTAs, latency-bound)
+template <class E, class = void>
+struct has_min_blocks : std::false_type {};
+template <class E>
+struct has_min_blocks<E, std::void_t<decltype(E::kTmaMinBlocks)>> : std::true_type {};
 template <class Epi>
 constexpr int tma_min_blocks() {
   if constexpr (is_dual<Epi>::value) return Epi::kMinBlocks;
+  if constexpr (has_min_blocks<Epi>::value) return Epi::kTmaMinBlocks;
   return 1;
 }
 
